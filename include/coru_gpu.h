@@ -1,0 +1,151 @@
+/*
+ * coru_gpu — C-ABI of the B200-native CoR-UTV hot path.
+ *
+ * Drop-in boundary for the reference's decomposition entry point and its sketch stage:
+ *
+ *   coru::corutv(const Matrix& a, size_t ell, int q, DVariant variant, RngSeed seed)
+ *       -> UtvApprox{u, t, v, ell, q, variant, seed, lower, conditioning_warning}
+ *       /root/reference/proj/include/coru/corutv.hpp:79-100 (UtvApprox :23-34)
+ *   coru::detail::sketch_bases(const Matrix& a, size_t ell, int q, RngSeed seed)
+ *       -> SketchBases{q1, q2, c1, c2_prev, conditioning_warning}
+ *       /root/reference/proj/include/coru/corutv.hpp:42-65
+ *   the projection D = (q1^T a) q2                      corutv.hpp:90
+ *   coru::gaussian(rows, cols, seed)                    rng.hpp:107-112
+ *
+ * The reference is a header-only C++ library with no FFI; a C++ caller uses the header-only
+ * wrapper include/coru_gpu.hpp (same names and types as the reference), other languages bind
+ * these symbols directly. Plain pointers and sizes only.
+ *
+ * Matrices are dense row-major (the layout of coru::Matrix, matrix.hpp:44-45) with an explicit
+ * leading dimension. "_dev" entry points take device pointers; the others take host pointers
+ * and copy in and out inside the call. There is no CPU fallback: without a usable sm_100 GPU
+ * every entry point fails with CORU_ECUDA.
+ *
+ * Errors mirror the reference: CORU_EINVAL is std::invalid_argument (corutv.hpp:68-70,81 — ell < 1,
+ * ell >= min(rows, cols), q < 0; matrix.hpp:29-31 — non-finite host input), everything else maps
+ * to std::runtime_error in the C++ wrapper. coru_last_error() returns the calling thread's message.
+ */
+#ifndef CORU_GPU_H
+#define CORU_GPU_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define CORU_GPU_ABI_VERSION 1
+
+enum coru_status {
+    CORU_OK = 0,
+    CORU_EINVAL = 1,  /* std::invalid_argument in the reference */
+    CORU_ECUDA = 2,   /* CUDA runtime / launch failure, or no sm_100 device */
+    CORU_ENCCL = 3,   /* NCCL failure (multi-GPU) */
+    CORU_ENOMEM = 4,  /* device or pinned-host allocation failed */
+    CORU_ENOTSUP = 5  /* valid in the reference, not provided by this build */
+};
+
+/* DVariant (corutv.hpp:17). Only CORU_D_EXACT is in the hot-path scope. */
+enum coru_variant { CORU_D_EXACT = 0, CORU_D_APPROX = 1 };
+
+/* Opaque per-device context: stream, workspace arena, pinned staging, optional communicator.
+ * Calls on one context are serialised by an internal mutex; use one context per host thread
+ * for concurrent decompositions (the reference is re-entrant; coru_cli.cpp:171). */
+typedef struct coru_ctx coru_ctx;
+
+int coru_abi_version(void);
+const char* coru_last_error(void);
+
+int coru_ctx_create(int device, coru_ctx** out);
+void coru_ctx_destroy(coru_ctx* ctx);
+/* Run on the caller's cudaStream_t (NULL restores the context-owned stream). */
+int coru_ctx_set_stream(coru_ctx* ctx, void* cuda_stream);
+/* Host threads used for the bit-exact Gaussian test matrix (default: hardware concurrency). */
+int coru_ctx_set_host_threads(coru_ctx* ctx, int threads);
+
+/* ---- multi-GPU: one process (and context) per GPU, A row-block sharded --------------------- */
+/* Rank 0 creates the id and distributes it (e.g. torch.distributed broadcast); every rank then
+ * calls coru_ctx_init_comm. NCCL is loaded at run time (libnccl.so.2). */
+int coru_comm_unique_id(unsigned char id[128]);
+int coru_ctx_init_comm(coru_ctx* ctx, int rank, int world, const unsigned char id[128]);
+/* Rows [*row0, *row0 + *rows) of an m-row matrix belong to `rank` of `world`. */
+void coru_shard_rows(int64_t m, int rank, int world, int64_t* row0, int64_t* rows);
+
+/* ---- the decomposition: corutv (corutv.hpp:79-100) ------------------------------------------ */
+/* Output record (UtvApprox, corutv.hpp:23-34). u: rows(A) x ell (this rank's rows when sharded),
+ * t: ell x ell (upper for URV, lower for ULV), v: cols(A) x ell. perm (optional, host) receives the
+ * QRCP pivots of the core (V(:,j) = Q2(:,perm[j]), corutv.hpp:95-97). */
+typedef struct {
+    void* u;
+    int64_t ldu;
+    void* t;
+    int64_t ldt;
+    void* v;
+    int64_t ldv;
+    int64_t* perm;            /* host, ell entries, may be NULL */
+    int lower;                /* out: 1 for the ULV orientation (rows(A) < cols(A)) */
+    int conditioning_warning; /* out: |R1(ell,ell)| <= 1e-14 |R1(1,1)| (corutv.hpp:61-64) */
+} coru_utv;
+
+/* A: device, row-major, lda >= n. With a communicator, A is this rank's m_local rows of the
+ * global m x n matrix (coru_shard_rows layout); without one, m_local == m. */
+int coru_corutv_f64_dev(coru_ctx* ctx, const double* A, int64_t m_local, int64_t m, int64_t n, int64_t lda,
+                        int64_t ell, int q, int variant, uint64_t seed, uint64_t stream, coru_utv* out);
+int coru_corutv_f32_dev(coru_ctx* ctx, const float* A, int64_t m_local, int64_t m, int64_t n, int64_t lda,
+                        int64_t ell, int q, int variant, uint64_t seed, uint64_t stream, coru_utv* out);
+
+/* Host-buffer drop-in for coru::corutv: A host row-major m x n (dense); U (m x ell), T (ell x ell),
+ * V (n x ell) host row-major dense; perm optional. Single GPU (the context's device). */
+int coru_corutv_f64(coru_ctx* ctx, const double* A, int64_t m, int64_t n, int64_t ell, int q, int variant,
+                    uint64_t seed, uint64_t stream, double* U, double* T, double* V, int64_t* perm, int* lower,
+                    int* conditioning_warning);
+int coru_corutv_f32(coru_ctx* ctx, const float* A, int64_t m, int64_t n, int64_t ell, int q, int variant,
+                    uint64_t seed, uint64_t stream, float* U, float* T, float* V, int64_t* perm, int* lower,
+                    int* conditioning_warning);
+
+/* ---- the sketch stage: detail::sketch_bases (corutv.hpp:42-65) ------------------------------- */
+/* Requires rows(A) >= cols(A) like the reference's callers (rpca.hpp:135, baselines.hpp:68).
+ * Q1/C1: m_local x ell, Q2/C2prev: n x ell (device, row-major). C1 and C2prev may be NULL. */
+int coru_sketch_bases_f64_dev(coru_ctx* ctx, const double* A, int64_t m_local, int64_t m, int64_t n, int64_t lda,
+                              int64_t ell, int q, uint64_t seed, uint64_t stream, double* Q1, int64_t ldq1,
+                              double* Q2, int64_t ldq2, double* C1, int64_t ldc1, double* C2prev, int64_t ldc2,
+                              int* conditioning_warning);
+int coru_sketch_bases_f64(coru_ctx* ctx, const double* A, int64_t m, int64_t n, int64_t ell, int q,
+                          uint64_t seed, uint64_t stream, double* Q1, double* Q2, double* C1, double* C2prev,
+                          int* conditioning_warning);
+
+/* ---- the projection D = (Q1^T A) Q2 (corutv.hpp:90), summed over ranks ----------------------- */
+int coru_project_f64_dev(coru_ctx* ctx, const double* A, int64_t m_local, int64_t n, int64_t lda, const double* Q1,
+                         int64_t ldq1, const double* Q2, int64_t ldq2, int64_t ell, double* D, int64_t ldd);
+
+/* ---- the test matrix Φ: gaussian(rows, cols, {seed, stream}) (rng.hpp:107-112), host --------- */
+int coru_gaussian(int64_t rows, int64_t cols, uint64_t seed, uint64_t stream, double* out, int threads);
+
+/* ---- kernel-level entry points (parity tests and benchmarks of the A-pass kernels) ----------- */
+/* C (rows x N) = op(A) · X, op 0: A (rows x K), op 1: A^T with A (K x rows); device row-major. */
+int coru_gemm_f64_dev(coru_ctx* ctx, int op, const double* A, int64_t lda, const double* X, int64_t ldx,
+                      double* C, int64_t ldc, int64_t rows, int64_t K, int64_t N);
+/* householder_qr (qr.hpp:85-99) via TSQR: B (m x n, m > n) -> Q (m x n), R (n x n). Device. */
+int coru_tsqr_f64_dev(coru_ctx* ctx, const double* B, int64_t ldb, int64_t m, int64_t n, double* Q, int64_t ldq,
+                      double* R, int64_t ldr);
+/* qrcp (qr.hpp:106-143) of a square n x n matrix: Q, R (n x n), perm (host, n). Device. */
+int coru_qrcp_f64_dev(coru_ctx* ctx, const double* M, int64_t ldm, int64_t n, double* Q, int64_t ldq, double* R,
+                      int64_t ldr, int64_t* perm);
+
+/* A-pass profiling: when enabled, CUDA events are recorded on the launching stream around every
+ * GEMM that streams the caller's A (the sketch, power and projection passes). The read call
+ * returns the summed device time, the number of A-passes, and their algorithmic flops
+ * (2·rows·cols·ell) and A bytes (rows·cols·sizeof(T)), then resets the counters. */
+int coru_ctx_set_profiling(coru_ctx* ctx, int enable);
+int coru_ctx_profile_apass(coru_ctx* ctx, double* total_ms, int64_t* launches, double* flops, double* bytes);
+
+/* Number of this library's kernels launched by the calling thread since the last reset
+ * (bench evidence: "gpu_launches"). */
+int64_t coru_launch_count(int reset);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* CORU_GPU_H */

@@ -1,0 +1,142 @@
+// coru_gpu.hpp — header-only C++ mirror of the reference's decomposition API over the C-ABI.
+//
+// A C++ caller of the reference switches by replacing
+//     #include "coru/corutv.hpp"      coru::corutv(a, ell, q, coru::DVariant::exact, {seed, stream})
+// with
+//     #include "coru_gpu.hpp"         coru_gpu::corutv(a, ell, q, coru_gpu::DVariant::exact, {seed, stream})
+// Same argument list and meaning, same output record (UtvApprox, corutv.hpp:23-34), same error
+// behaviour (std::invalid_argument for the reference's parameter errors, corutv.hpp:68-70,81 and
+// matrix.hpp:29-31); GPU failures throw std::runtime_error. Matrix is row-major fp64 like
+// coru::Matrix (matrix.hpp:17-110; construction validation is the reference's own).
+#pragma once
+
+#include <cmath>
+#include <cstdint>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "coru_gpu.h"
+
+namespace coru_gpu {
+
+struct RngSeed {  // rng.hpp:13-16
+    std::uint64_t seed = 0;
+    std::uint64_t stream = 0;
+};
+inline RngSeed substream(RngSeed s, std::uint64_t offset) { return {s.seed, s.stream + offset}; }  // rng.hpp:18
+
+enum class DVariant { exact, approx };  // corutv.hpp:17
+
+class Matrix {  // row-major fp64, matrix.hpp:17-110 (the subset the hot path's callers use)
+public:
+    Matrix(std::size_t rows, std::size_t cols) : rows_(rows), cols_(cols), data_(check(rows, cols), 0.0) {}
+    Matrix(std::size_t rows, std::size_t cols, std::vector<double> entries)
+        : rows_(rows), cols_(cols), data_(std::move(entries)) {
+        check(rows, cols);
+        if (data_.size() != rows * cols)
+            throw std::invalid_argument("Matrix: entries size " + std::to_string(data_.size()) + " does not match " +
+                                        std::to_string(rows) + "x" + std::to_string(cols));
+        for (double x : data_)
+            if (!std::isfinite(x)) throw std::invalid_argument("Matrix: non-finite entry");
+    }
+    std::size_t rows() const noexcept { return rows_; }
+    std::size_t cols() const noexcept { return cols_; }
+    std::size_t size() const noexcept { return data_.size(); }
+    double operator()(std::size_t i, std::size_t j) const noexcept { return data_[i * cols_ + j]; }
+    double& operator()(std::size_t i, std::size_t j) noexcept { return data_[i * cols_ + j]; }
+    const std::vector<double>& data() const noexcept { return data_; }
+    std::vector<double>& data() noexcept { return data_; }
+
+private:
+    static std::size_t check(std::size_t r, std::size_t c) {
+        if (r == 0 || c == 0) throw std::invalid_argument("Matrix: dimensions must be positive");
+        return r * c;
+    }
+    std::size_t rows_, cols_;
+    std::vector<double> data_;
+};
+
+struct UtvApprox {  // corutv.hpp:23-34
+    Matrix u, t, v;
+    std::size_t ell;
+    int q;
+    DVariant variant;
+    RngSeed seed;
+    bool lower = false;
+    bool conditioning_warning = false;
+    std::vector<std::int64_t> perm;  // QRCP pivots of the core (extra)
+};
+
+struct SketchBases {  // corutv.hpp:42-47
+    Matrix q1, q2, c1, c2_prev;
+    bool conditioning_warning = false;
+};
+
+namespace detail {
+inline void throw_status(int rc) {
+    if (rc == CORU_OK) return;
+    const std::string msg = coru_last_error();
+    if (rc == CORU_EINVAL) throw std::invalid_argument(msg);
+    throw std::runtime_error("coru_gpu: " + msg);
+}
+// One context per thread: the reference is re-entrant across threads (coru_cli.cpp:171-177).
+inline coru_ctx* thread_context() {
+    struct Holder {
+        coru_ctx* c = nullptr;
+        ~Holder() { coru_ctx_destroy(c); }
+    };
+    thread_local Holder h;
+    if (!h.c) throw_status(coru_ctx_create(0, &h.c));
+    return h.c;
+}
+}  // namespace detail
+
+// coru::corutv (corutv.hpp:79-100)
+inline UtvApprox corutv(const Matrix& a, std::size_t ell, int q, DVariant variant, RngSeed seed) {
+    const std::int64_t m = std::int64_t(a.rows()), n = std::int64_t(a.cols()), l = std::int64_t(ell);
+    if (ell < 1) throw std::invalid_argument("corutv: ell must be >= 1");
+    if (ell >= std::min(a.rows(), a.cols())) throw std::invalid_argument("corutv: ell must be < min(rows, cols)");
+    if (q < 0) throw std::invalid_argument("corutv: q must be >= 0");
+    UtvApprox f{Matrix(a.rows(), ell), Matrix(ell, ell), Matrix(a.cols(), ell), ell, q, variant, seed,
+                false, false, std::vector<std::int64_t>(ell)};
+    int lower = 0, warn = 0;
+    detail::throw_status(coru_corutv_f64(detail::thread_context(), a.data().data(), m, n, l, q,
+                                         variant == DVariant::exact ? CORU_D_EXACT : CORU_D_APPROX, seed.seed,
+                                         seed.stream, f.u.data().data(), f.t.data().data(), f.v.data().data(),
+                                         f.perm.data(), &lower, &warn));
+    f.lower = lower != 0;
+    f.conditioning_warning = warn != 0;
+    return f;
+}
+
+// detail::sketch_bases (corutv.hpp:49-65)
+inline SketchBases sketch_bases(const Matrix& a, std::size_t ell, int q, RngSeed seed) {
+    SketchBases s{Matrix(a.rows(), ell), Matrix(a.cols(), ell), Matrix(a.rows(), ell), Matrix(a.cols(), ell), false};
+    int warn = 0;
+    detail::throw_status(coru_sketch_bases_f64(detail::thread_context(), a.data().data(), std::int64_t(a.rows()),
+                                               std::int64_t(a.cols()), std::int64_t(ell), q, seed.seed, seed.stream,
+                                               s.q1.data().data(), s.q2.data().data(), s.c1.data().data(),
+                                               s.c2_prev.data().data(), &warn));
+    s.conditioning_warning = warn != 0;
+    return s;
+}
+
+// gaussian (rng.hpp:107-112): bit-exact host generator.
+inline Matrix gaussian(std::size_t rows, std::size_t cols, RngSeed seed) {
+    Matrix m(rows, cols);
+    detail::throw_status(coru_gaussian(std::int64_t(rows), std::int64_t(cols), seed.seed, seed.stream,
+                                       m.data().data(), 1));
+    return m;
+}
+
+// singular_estimates (corutv.hpp:113-117)
+inline std::vector<double> singular_estimates(const UtvApprox& f) {
+    std::vector<double> s(f.ell);
+    for (std::size_t j = 0; j < f.ell; ++j) s[j] = std::abs(f.t(j, j));
+    return s;
+}
+
+}  // namespace coru_gpu

@@ -1,0 +1,244 @@
+"""TEST INFRASTRUCTURE — NOT PRODUCT CODE.
+
+ctypes front-end for the two CPU checkers of the CoR-UTV hot path:
+
+* ``Oracle`` — ``liboracle.so``, the plain-C restatement in ``coru_oracle.c`` (fp64 and
+  fp32), each function citing the reference file:line it follows.
+* ``Reference`` — ``_ref/libcoru_ref.so``, the unmodified reference headers
+  (``/root/reference/proj/include/coru``) compiled by ``oracle/Makefile`` behind a C-ABI.
+
+Only ``tests/``, ``__graft_entry__.smoke()`` and ``bench.py`` (its ``cpu_baseline`` leg and
+``--impl reference``) may import this package, and only as the checker / CPU baseline.
+The product package ``paper_1810_07323_b200`` never imports it.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ORACLE_SO = os.path.join(HERE, "liboracle.so")
+REF_SO = os.path.join(HERE, "_ref", "libcoru_ref.so")
+
+_i64, _u64, _int, _dbl = C.c_int64, C.c_uint64, C.c_int, C.c_double
+_p = C.c_void_p
+
+
+def _ptr(a: np.ndarray | None):
+    return None if a is None else a.ctypes.data_as(_p)
+
+
+def build(quiet: bool = True) -> None:
+    """Compile the checkers (oracle/Makefile). The reference part only where /root/reference exists."""
+    import subprocess
+
+    subprocess.run(["make", "-C", HERE, "all"], check=True,
+                   stdout=subprocess.DEVNULL if quiet else None)
+
+
+@dataclass
+class Utv:
+    u: np.ndarray
+    t: np.ndarray
+    v: np.ndarray
+    lower: bool
+    conditioning_warning: bool
+    perm: np.ndarray | None = None
+
+
+class CoruError(ValueError):
+    """Mirrors the reference's std::invalid_argument."""
+
+
+class Oracle:
+    """The plain-C restatement (liboracle.so)."""
+
+    def __init__(self, path: str = ORACLE_SO):
+        if not os.path.exists(path):
+            build()
+        self.lib = L = C.CDLL(path)
+        L.oracle_gaussian.argtypes = [_i64, _i64, _u64, _u64, _p]
+        L.oracle_xoshiro_words.argtypes = [_u64, _u64, _i64, _p]
+        L.oracle_max_threads.restype = _int
+        for sfx in ("f64", "f32"):
+            getattr(L, f"oracle_matmul_{sfx}").argtypes = [_p, _i64, _i64, _p, _i64, _p, _int]
+            getattr(L, f"oracle_matmul_tn_{sfx}").argtypes = [_p, _i64, _i64, _p, _i64, _p, _int]
+            getattr(L, f"oracle_householder_qr_{sfx}").argtypes = [_p, _i64, _i64, _p, _p]
+            getattr(L, f"oracle_qrcp_{sfx}").argtypes = [_p, _i64, _i64, _p, _p, _p]
+            getattr(L, f"oracle_sketch_bases_{sfx}").argtypes = [
+                _p, _i64, _i64, _i64, _int, _u64, _u64, _int, _p, _p, _p, _p, _p]
+            getattr(L, f"oracle_corutv_{sfx}").argtypes = [
+                _p, _i64, _i64, _i64, _int, _int, _u64, _u64, _int, _p, _p, _p, _p, _p]
+
+    @staticmethod
+    def _sfx(dtype):
+        return "f64" if np.dtype(dtype) == np.float64 else "f32"
+
+    def max_threads(self) -> int:
+        return self.lib.oracle_max_threads()
+
+    def gaussian(self, rows: int, cols: int, seed: int, stream: int = 0) -> np.ndarray:
+        out = np.empty((rows, cols), np.float64)
+        self.lib.oracle_gaussian(rows, cols, seed, stream, _ptr(out))
+        return out
+
+    def xoshiro_words(self, seed: int, stream: int, count: int) -> np.ndarray:
+        out = np.empty(count, np.uint64)
+        self.lib.oracle_xoshiro_words(seed, stream, count, _ptr(out))
+        return out
+
+    def matmul(self, a, b, threads=1):
+        a = np.ascontiguousarray(a); b = np.ascontiguousarray(b, a.dtype)
+        c = np.empty((a.shape[0], b.shape[1]), a.dtype)
+        getattr(self.lib, f"oracle_matmul_{self._sfx(a.dtype)}")(
+            _ptr(a), a.shape[0], a.shape[1], _ptr(b), b.shape[1], _ptr(c), threads)
+        return c
+
+    def matmul_tn(self, a, y, threads=1):
+        """a^T · y in the order of matmul(a.transposed(), y)."""
+        a = np.ascontiguousarray(a); y = np.ascontiguousarray(y, a.dtype)
+        c = np.empty((a.shape[1], y.shape[1]), a.dtype)
+        getattr(self.lib, f"oracle_matmul_tn_{self._sfx(a.dtype)}")(
+            _ptr(a), a.shape[0], a.shape[1], _ptr(y), y.shape[1], _ptr(c), threads)
+        return c
+
+    def householder_qr(self, a):
+        a = np.ascontiguousarray(a); m, n = a.shape
+        q = np.empty((m, n), a.dtype); r = np.empty((n, n), a.dtype)
+        if getattr(self.lib, f"oracle_householder_qr_{self._sfx(a.dtype)}")(_ptr(a), m, n, _ptr(q), _ptr(r)):
+            raise CoruError("householder_qr: requires rows >= cols")
+        return q, r
+
+    def qrcp(self, a):
+        a = np.ascontiguousarray(a); m, n = a.shape
+        q = np.empty((m, n), a.dtype); r = np.empty((n, n), a.dtype); perm = np.empty(n, np.int64)
+        if getattr(self.lib, f"oracle_qrcp_{self._sfx(a.dtype)}")(_ptr(a), m, n, _ptr(q), _ptr(r), _ptr(perm)):
+            raise CoruError("qrcp: requires rows >= cols")
+        return q, r, perm
+
+    def sketch_bases(self, a, ell, q, seed, stream=0, threads=1):
+        a = np.ascontiguousarray(a); m, n = a.shape; dt = a.dtype
+        q1 = np.empty((m, ell), dt); q2 = np.empty((n, ell), dt)
+        c1 = np.empty((m, ell), dt); c2p = np.empty((n, ell), dt); w = np.zeros(1, np.int32)
+        rc = getattr(self.lib, f"oracle_sketch_bases_{self._sfx(dt)}")(
+            _ptr(a), m, n, ell, q, seed, stream, threads, _ptr(q1), _ptr(q2), _ptr(c1), _ptr(c2p), _ptr(w))
+        if rc:
+            raise CoruError("sketch_bases: bad parameters")
+        return q1, q2, c1, c2p, bool(w[0])
+
+    def corutv(self, a, ell, q, variant=0, seed=0, stream=0, threads=1) -> Utv:
+        a = np.ascontiguousarray(a); m, n = a.shape; dt = a.dtype
+        u = np.empty((m, ell), dt); t = np.empty((ell, ell), dt); v = np.empty((n, ell), dt)
+        flags = np.zeros(2, np.int32); perm = np.empty(ell, np.int64)
+        if ell < 1 or ell >= min(m, n) or q < 0:
+            raise CoruError("corutv: bad parameters")
+        rc = getattr(self.lib, f"oracle_corutv_{self._sfx(dt)}")(
+            _ptr(a), m, n, ell, q, variant, seed, stream, threads, _ptr(u), _ptr(t), _ptr(v), _ptr(flags), _ptr(perm))
+        if rc == 1:
+            raise CoruError("corutv: bad parameters")
+        if rc == 3:
+            raise NotImplementedError("DVariant::approx is outside the hot-path scope")
+        return Utv(u, t, v, bool(flags[0]), bool(flags[1]), perm)
+
+
+class Reference:
+    """The reference library itself, compiled from /root/reference headers (oracle/_ref)."""
+
+    def __init__(self, path: str = REF_SO):
+        if not os.path.exists(path):
+            raise FileNotFoundError(f"{path} missing: build it here with `make -C oracle ref`")
+        self.lib = L = C.CDLL(path)
+        L.ref_last_error.restype = C.c_char_p
+        L.ref_gaussian.argtypes = [_i64, _i64, _u64, _u64, _p]
+        L.ref_xoshiro_words.argtypes = [_u64, _u64, _i64, _p]
+        L.ref_matmul.argtypes = [_p, _i64, _i64, _p, _i64, _p]
+        L.ref_householder_qr.argtypes = [_p, _i64, _i64, _p, _p]
+        L.ref_qrcp.argtypes = [_p, _i64, _i64, _p, _p, _p]
+        L.ref_corutv.argtypes = [_p, _i64, _i64, _i64, _int, _int, _u64, _u64, _p, _p, _p, _p]
+        L.ref_corutv_mt.argtypes = [_p, _i64, _i64, _i64, _int, _u64, _u64, _int, _p, _p, _p, _p]
+        L.ref_sketch_bases.argtypes = [_p, _i64, _i64, _i64, _int, _u64, _u64, _p, _p, _p, _p, _p]
+        L.ref_gen_fast_decay.argtypes = [_i64, _i64, _u64, _u64, _p]
+        L.ref_gen_noisy_lowrank.argtypes = [_i64, _i64, _dbl, _u64, _u64, _p]
+        L.ref_corutv_batch.argtypes = [_p, _i64, _i64, _i64, _int, _u64, _u64, _int, _int]
+        L.ref_corutv_batch.restype = _dbl
+        L.ref_frobenius.argtypes = [_p, _i64, _i64]
+        L.ref_frobenius.restype = _dbl
+
+    def _check(self, rc):
+        if rc == 1:
+            raise CoruError(self.lib.ref_last_error().decode())
+        if rc:
+            raise RuntimeError(self.lib.ref_last_error().decode())
+
+    def gaussian(self, rows, cols, seed, stream=0):
+        out = np.empty((rows, cols), np.float64)
+        self._check(self.lib.ref_gaussian(rows, cols, seed, stream, _ptr(out)))
+        return out
+
+    def xoshiro_words(self, seed, stream, count):
+        out = np.empty(count, np.uint64)
+        self.lib.ref_xoshiro_words(seed, stream, count, _ptr(out))
+        return out
+
+    def matmul(self, a, b):
+        a = np.ascontiguousarray(a, np.float64); b = np.ascontiguousarray(b, np.float64)
+        c = np.empty((a.shape[0], b.shape[1]))
+        self._check(self.lib.ref_matmul(_ptr(a), a.shape[0], a.shape[1], _ptr(b), b.shape[1], _ptr(c)))
+        return c
+
+    def householder_qr(self, a):
+        a = np.ascontiguousarray(a, np.float64); m, n = a.shape
+        q = np.empty((m, n)); r = np.empty((n, n))
+        self._check(self.lib.ref_householder_qr(_ptr(a), m, n, _ptr(q), _ptr(r)))
+        return q, r
+
+    def qrcp(self, a):
+        a = np.ascontiguousarray(a, np.float64); m, n = a.shape
+        q = np.empty((m, n)); r = np.empty((n, n)); perm = np.empty(n, np.int64)
+        self._check(self.lib.ref_qrcp(_ptr(a), m, n, _ptr(q), _ptr(r), _ptr(perm)))
+        return q, r, perm
+
+    def corutv(self, a, ell, q, variant=0, seed=0, stream=0, threads=1) -> Utv:
+        a = np.ascontiguousarray(a, np.float64); m, n = a.shape
+        u = np.empty((m, ell)); t = np.empty((ell, ell)); v = np.empty((n, ell)); flags = np.zeros(2, np.int32)
+        if threads > 1 and m >= n and variant == 0:
+            self._check(self.lib.ref_corutv_mt(_ptr(a), m, n, ell, q, seed, stream, threads,
+                                               _ptr(u), _ptr(t), _ptr(v), _ptr(flags)))
+        else:
+            self._check(self.lib.ref_corutv(_ptr(a), m, n, ell, q, variant, seed, stream,
+                                            _ptr(u), _ptr(t), _ptr(v), _ptr(flags)))
+        return Utv(u, t, v, bool(flags[0]), bool(flags[1]))
+
+    def corutv_batch(self, a, ell, q, seed, stream0, count, threads):
+        """`count` unchanged corutv calls fanned out over `threads` threads; returns a checksum."""
+        a = np.ascontiguousarray(a, np.float64); m, n = a.shape
+        return self.lib.ref_corutv_batch(_ptr(a), m, n, ell, q, seed, stream0, count, threads)
+
+    def sketch_bases(self, a, ell, q, seed, stream=0):
+        a = np.ascontiguousarray(a, np.float64); m, n = a.shape
+        q1 = np.empty((m, ell)); q2 = np.empty((n, ell)); c1 = np.empty((m, ell)); c2p = np.empty((n, ell))
+        w = np.zeros(1, np.int32)
+        self._check(self.lib.ref_sketch_bases(_ptr(a), m, n, ell, q, seed, stream,
+                                              _ptr(q1), _ptr(q2), _ptr(c1), _ptr(c2p), _ptr(w)))
+        return q1, q2, c1, c2p, bool(w[0])
+
+    def gen_fast_decay(self, n, k, seed, stream=0):
+        out = np.empty((n, n))
+        self._check(self.lib.ref_gen_fast_decay(n, k, seed, stream, _ptr(out)))
+        return out
+
+    def gen_noisy_lowrank(self, n, k, gap, seed, stream=0):
+        out = np.empty((n, n))
+        self._check(self.lib.ref_gen_noisy_lowrank(n, k, gap, seed, stream, _ptr(out)))
+        return out
+
+    def frobenius(self, a):
+        a = np.ascontiguousarray(a, np.float64)
+        return self.lib.ref_frobenius(_ptr(a), a.shape[0], a.reshape(a.shape[0], -1).shape[1])
+
+
+def has_reference() -> bool:
+    return os.path.exists(REF_SO)

@@ -1,0 +1,234 @@
+// TEST INFRASTRUCTURE — NOT PRODUCT CODE.
+//
+// C-ABI driver around the *unmodified* reference implementation. It #includes the
+// reference headers in place (-I/root/reference/proj/include; nothing is copied into
+// this repo) and is built by oracle/Makefile into oracle/_ref/libcoru_ref.so, which is
+// git-ignored and travels to the GPU box prebuilt. Only tests/, __graft_entry__.smoke()
+// and bench.py (cpu_baseline leg and --impl reference) may load it.
+//
+// Every matrix crossing this boundary is dense row-major fp64, the layout of
+// coru::Matrix (proj/include/coru/matrix.hpp:44-45).
+#include <algorithm>
+#include <atomic>
+#include <cstdint>
+#include <cstring>
+#include <exception>
+#include <stdexcept>
+#include <thread>
+#include <vector>
+
+#include "coru/corutv.hpp"
+#include "coru/norms.hpp"
+#include "coru/testgen.hpp"
+
+using coru::Matrix;
+
+namespace {
+
+thread_local std::string g_err;
+
+Matrix wrap(const double* a, int64_t m, int64_t n) {
+    // The validating constructor (matrix.hpp:22-32): rejects non-finite entries like the reference.
+    return Matrix(size_t(m), size_t(n), std::vector<double>(a, a + m * n));
+}
+
+void put(const Matrix& x, double* out) {
+    if (out) std::memcpy(out, x.data().data(), x.size() * sizeof(double));
+}
+
+template <class F>
+int guarded(F&& f) {
+    try {
+        f();
+        return 0;
+    } catch (const std::invalid_argument& e) {
+        g_err = e.what();
+        return 1;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return 2;
+    }
+}
+
+// Row-parallel i-k-j product. matmul's i loop carries no dependency
+// (matrix.hpp:121-129), so splitting it over threads leaves every output bit unchanged.
+Matrix matmul_rows(const Matrix& a, const Matrix& b, int threads) {
+    if (threads <= 1) return coru::matmul(a, b);
+    Matrix c(a.rows(), b.cols());
+    const size_t n = b.cols(), kk = a.cols(), m = a.rows();
+    std::vector<std::thread> pool;
+    for (int t = 0; t < threads; ++t) {
+        pool.emplace_back([&, t] {
+            const size_t lo = m * t / threads, hi = m * (t + 1) / threads;
+            for (size_t i = lo; i < hi; ++i) {
+                double* ci = c.row(i);
+                const double* ai = a.row(i);
+                for (size_t k = 0; k < kk; ++k) {
+                    const double aik = ai[k];
+                    const double* bk = b.row(k);
+                    for (size_t j = 0; j < n; ++j) ci[j] += aik * bk[j];
+                }
+            }
+        });
+    }
+    for (auto& th : pool) th.join();
+    return c;
+}
+
+Matrix transposed_rows(const Matrix& a, int threads) {
+    if (threads <= 1) return a.transposed();
+    Matrix t(a.cols(), a.rows());
+    std::vector<std::thread> pool;
+    const size_t rows = a.cols();
+    for (int th = 0; th < threads; ++th)
+        pool.emplace_back([&, th] {
+            for (size_t j = rows * th / threads; j < rows * (th + 1) / threads; ++j)
+                for (size_t i = 0; i < a.rows(); ++i) t(j, i) = a(i, j);
+        });
+    for (auto& th : pool) th.join();
+    return t;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* ref_last_error() { return g_err.c_str(); }
+
+// coru::gaussian (rng.hpp:107-112)
+int ref_gaussian(int64_t rows, int64_t cols, uint64_t seed, uint64_t stream, double* out) {
+    return guarded([&] { put(coru::gaussian(size_t(rows), size_t(cols), {seed, stream}), out); });
+}
+
+// Raw xoshiro256++ words (rng.hpp:39-61), for pinning the host RNG restatement.
+int ref_xoshiro_words(uint64_t seed, uint64_t stream, int64_t count, uint64_t* out) {
+    coru::Xoshiro256pp r({seed, stream});
+    for (int64_t i = 0; i < count; ++i) out[i] = r.next();
+    return 0;
+}
+
+// coru::matmul (matrix.hpp:115-131)
+int ref_matmul(const double* a, int64_t m, int64_t k, const double* b, int64_t n, double* out) {
+    return guarded([&] { put(coru::matmul(wrap(a, m, k), wrap(b, k, n)), out); });
+}
+
+// coru::householder_qr (qr.hpp:85-99): q m×n, r n×n
+int ref_householder_qr(const double* a, int64_t m, int64_t n, double* q, double* r) {
+    return guarded([&] {
+        coru::QrFactors f = coru::householder_qr(wrap(a, m, n));
+        put(f.q, q);
+        put(f.r, r);
+    });
+}
+
+// coru::qrcp (qr.hpp:106-143): q m×n, r n×n, perm n
+int ref_qrcp(const double* a, int64_t m, int64_t n, double* q, double* r, int64_t* perm) {
+    return guarded([&] {
+        coru::QrcpFactors f = coru::qrcp(wrap(a, m, n));
+        put(f.q, q);
+        put(f.r, r);
+        for (int64_t j = 0; j < n; ++j) perm[j] = int64_t(f.perm[size_t(j)]);
+    });
+}
+
+// coru::corutv (corutv.hpp:79-100). u rows(a)×ell, t ell×ell, v cols(a)×ell.
+// flags[0] = lower, flags[1] = conditioning_warning.
+int ref_corutv(const double* a, int64_t m, int64_t n, int64_t ell, int q, int variant,
+               uint64_t seed, uint64_t stream, double* u, double* t, double* v, int* flags) {
+    return guarded([&] {
+        if (ell < 0) throw std::invalid_argument("corutv: ell must be >= 1");
+        coru::UtvApprox f = coru::corutv(wrap(a, m, n), size_t(ell), q,
+                                         variant == 0 ? coru::DVariant::exact : coru::DVariant::approx,
+                                         {seed, stream});
+        put(f.u, u);
+        put(f.t, t);
+        put(f.v, v);
+        flags[0] = f.lower;
+        flags[1] = f.conditioning_warning;
+    });
+}
+
+// Same steps as coru::corutv's exact-D, m >= n branch (corutv.hpp:49-65, 89-97), with the two
+// A-products and the transpose row-parallel over `threads` threads: bit-identical to ref_corutv.
+// QR, QRCP and the Gaussian are the reference's own serial functions.
+int ref_corutv_mt(const double* a_, int64_t m, int64_t n, int64_t ell, int q, uint64_t seed,
+                  uint64_t stream, int threads, double* u, double* t, double* v, int* flags) {
+    return guarded([&] {
+        const Matrix a = wrap(a_, m, n);
+        coru::detail::check_corutv_params(a, size_t(ell));
+        if (q < 0) throw std::invalid_argument("corutv: q must be >= 0");
+        if (m < n) throw std::invalid_argument("ref_corutv_mt: m >= n only");
+        const Matrix at = transposed_rows(a, threads);
+        Matrix c2 = coru::gaussian(a.cols(), size_t(ell), {seed, stream});
+        Matrix c1(a.rows(), size_t(ell));
+        for (int i = 0; i <= q; ++i) {
+            c1 = matmul_rows(a, c2, threads);
+            c2 = matmul_rows(at, c1, threads);
+        }
+        coru::QrFactors f1 = coru::householder_qr(c1);
+        coru::QrFactors f2 = coru::householder_qr(c2);
+        const bool warn = std::abs(f1.r(size_t(ell) - 1, size_t(ell) - 1)) <= 1e-14 * std::abs(f1.r(0, 0));
+        // D = (Q1^T A) Q2 (corutv.hpp:90)
+        const Matrix d = coru::matmul(matmul_rows(f1.q.transposed(), a, threads), f2.q);
+        coru::QrcpFactors cp = coru::qrcp(d);
+        put(matmul_rows(f1.q, cp.q, threads), u);
+        put(cp.r, t);
+        Matrix vv(a.cols(), size_t(ell));
+        for (size_t j = 0; j < size_t(ell); ++j)
+            for (size_t i = 0; i < a.cols(); ++i) vv(i, j) = f2.q(i, cp.perm[j]);
+        put(vv, v);
+        flags[0] = 0;
+        flags[1] = warn;
+    });
+}
+
+// `count` independent coru::corutv calls (seeds {seed, stream0 + i}) fanned out over `threads`
+// std::threads — the reference's own concurrency model, trial-level fan-out of unchanged
+// decompositions (parallel.hpp:23-36, used at coru_cli.cpp:171-177). A is shared read-only
+// (Matrix is safe to share, matrix.hpp:14-15). Returns sum_i sum_j |t_jj| as a checksum.
+double ref_corutv_batch(const double* a_, int64_t m, int64_t n, int64_t ell, int q, uint64_t seed,
+                        uint64_t stream0, int count, int threads) {
+    const Matrix a = wrap(a_, m, n);
+    std::vector<double> sums(size_t(count), 0.0);
+    std::atomic<int> next{0};
+    auto worker = [&] {
+        for (int i; (i = next.fetch_add(1)) < count;) {
+            coru::UtvApprox f = coru::corutv(a, size_t(ell), q, coru::DVariant::exact, {seed, stream0 + uint64_t(i)});
+            double s = 0;
+            for (double e : coru::singular_estimates(f)) s += e;
+            sums[size_t(i)] = s;
+        }
+    };
+    std::vector<std::thread> pool;
+    for (int t = 0; t < std::max(1, threads); ++t) pool.emplace_back(worker);
+    for (auto& th : pool) th.join();
+    double tot = 0;
+    for (double s : sums) tot += s;
+    return tot;
+}
+
+// coru::detail::sketch_bases (corutv.hpp:49-65)
+int ref_sketch_bases(const double* a, int64_t m, int64_t n, int64_t ell, int q, uint64_t seed,
+                     uint64_t stream, double* q1, double* q2, double* c1, double* c2_prev, int* warn) {
+    return guarded([&] {
+        coru::detail::SketchBases sb = coru::detail::sketch_bases(wrap(a, m, n), size_t(ell), q, {seed, stream});
+        put(sb.q1, q1);
+        put(sb.q2, q2);
+        put(sb.c1, c1);
+        put(sb.c2_prev, c2_prev);
+        *warn = sb.conditioning_warning;
+    });
+}
+
+// Test-matrix generators of the reference suite (testgen.hpp:48-81).
+int ref_gen_fast_decay(int64_t n, int64_t k, uint64_t seed, uint64_t stream, double* out) {
+    return guarded([&] { put(coru::gen_fast_decay(size_t(n), size_t(k), {seed, stream}), out); });
+}
+int ref_gen_noisy_lowrank(int64_t n, int64_t k, double gap, uint64_t seed, uint64_t stream, double* out) {
+    return guarded([&] { put(coru::gen_noisy_lowrank(size_t(n), size_t(k), gap, {seed, stream}), out); });
+}
+
+// coru::frobenius_norm (matrix.hpp:133-137)
+double ref_frobenius(const double* a, int64_t m, int64_t n) { return coru::frobenius_norm(wrap(a, m, n)); }
+
+}  // extern "C"

@@ -1,0 +1,926 @@
+// C-ABI (include/coru_gpu.h) and host orchestration of CoR-UTV on B200.
+//
+// The step order is the reference's (corutv.hpp:49-100):
+//   Φ = gaussian(n, ell, seed)                        host, bit-exact (rng_host.cpp), one H2D
+//   q+1 x { B1 = A·B2 ; B2 = A^T·B1 }                  gemm (op N / op T: A^T is never formed)
+//   Q1,R1 = TSQR(B1) ; Q2 = TSQR(B2)                    tsqr.cu (R-tree, explicit Q)
+//   warning = |R1(ell,ell)| <= 1e-14 |R1(1,1)|
+//   D = Q1^T (A Q2)                                     two gemm calls; W = A·Q2 is m x ell
+//   Q_M, T, perm = QRCP(D) ; U = Q1·Q_M ; V = Q2·P       qrcp.cu + gemm + gather
+// With a communicator (A row-sharded over ranks) the A^T-products and D are summed with
+// ncclAllReduce, the B1 TSQR tree gets a cross-rank top level (ncclAllGather of the ell x ell R's,
+// redundant top QR on every rank), and everything ell x ell or n x ell is computed redundantly
+// and bit-identically on every rank (all kernels are atomic-free and fixed-order).
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <thread>
+#include <utility>
+#include <vector>
+
+#include "../../include/coru_gpu.h"
+#include "gemm.cuh"
+#include "qrcp.cuh"
+#include "tsqr.cuh"
+
+namespace coru_gpu {
+template <typename OutT>
+void gaussian_host(int64_t rows, int64_t cols, uint64_t seed, uint64_t stream, OutT* out, int64_t ldo, int threads);
+}  // namespace coru_gpu
+
+using namespace coru_gpu;
+
+namespace {
+
+thread_local std::string g_err;
+thread_local int64_t g_launches = 0;
+
+int fail(int code, const std::string& msg) {
+    g_err = msg;
+    return code;
+}
+
+#define CORU_CUDA(expr)                                                                                      \
+    do {                                                                                                     \
+        cudaError_t e_ = (expr);                                                                             \
+        if (e_ != cudaSuccess) return fail(CORU_ECUDA, std::string(#expr) + ": " + cudaGetErrorString(e_));  \
+    } while (0)
+
+#define CORU_TRY(expr)                  \
+    do {                                \
+        int rc_ = (expr);               \
+        if (rc_ != CORU_OK) return rc_; \
+    } while (0)
+
+// ---- NCCL, loaded at run time ------------------------------------------------------------------
+struct Nccl {
+    void* h = nullptr;
+    ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+    ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+    ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+    ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                              cudaStream_t) = nullptr;
+    ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
+    const char* (*GetErrorString)(ncclResult_t) = nullptr;
+    std::string err;
+};
+
+Nccl* nccl() {
+    static Nccl api;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        for (const char* nm : {"libnccl.so.2", "libnccl.so"})
+            if ((api.h = dlopen(nm, RTLD_NOW | RTLD_GLOBAL))) break;
+        if (!api.h) {
+            api.err = std::string("dlopen libnccl.so.2 failed: ") + dlerror();
+            return;
+        }
+#define LOAD(sym) api.sym = reinterpret_cast<decltype(api.sym)>(dlsym(api.h, "nccl" #sym))
+        LOAD(GetUniqueId);
+        LOAD(CommInitRank);
+        LOAD(CommDestroy);
+        LOAD(AllReduce);
+        LOAD(AllGather);
+        LOAD(GetErrorString);
+#undef LOAD
+        if (!api.GetUniqueId || !api.CommInitRank || !api.AllReduce || !api.AllGather || !api.GetErrorString) {
+            api.err = "libnccl is missing required symbols";
+            api.h = nullptr;
+        }
+    });
+    return api.h ? &api : nullptr;
+}
+
+#define CORU_NCCL(expr)                                                                               \
+    do {                                                                                              \
+        ncclResult_t r_ = (expr);                                                                     \
+        if (r_ != ncclSuccess) return fail(CORU_ENCCL, std::string(#expr) + ": " + nccl()->GetErrorString(r_)); \
+    } while (0)
+
+template <typename T>
+ncclDataType_t nccl_type() {
+    return sizeof(T) == 8 ? ncclFloat64 : ncclFloat32;
+}
+
+int64_t round_up(int64_t x, int64_t a) { return (x + a - 1) / a * a; }
+
+// Bump allocator: a measuring pass (base == nullptr) then a carving pass over the arena.
+struct Carver {
+    char* base = nullptr;
+    size_t off = 0;
+    template <typename T>
+    T* take(int64_t n) {
+        off = (off + 255) / 256 * 256;
+        T* p = base ? reinterpret_cast<T*>(base + off) : nullptr;
+        off += size_t(std::max<int64_t>(n, 0)) * sizeof(T);
+        return p;
+    }
+};
+
+}  // namespace
+
+struct coru_ctx {
+    int device = 0;
+    cudaStream_t own_stream = nullptr;
+    cudaStream_t stream = nullptr;
+    int num_sms = 148;
+    int max_smem = 227 * 1024;
+    int host_threads = 1;
+    char* arena = nullptr;
+    size_t arena_bytes = 0;
+    char* pinned = nullptr;
+    size_t pinned_bytes = 0;
+    ncclComm_t comm = nullptr;
+    int rank = 0, world = 1;
+    std::mutex mu;
+    // A-pass profiling (bench evidence): CUDA events recorded on the launching stream around every
+    // GEMM that streams the caller's A, plus their algorithmic flop and byte counts.
+    bool prof = false;
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> prof_events;
+    size_t prof_used = 0;
+    double prof_flops = 0, prof_bytes = 0;
+};
+
+namespace {
+
+int ensure_arena(coru_ctx* c, size_t bytes) {
+    if (bytes <= c->arena_bytes) return CORU_OK;
+    if (c->arena) {
+        CORU_CUDA(cudaStreamSynchronize(c->stream));
+        cudaFree(c->arena);
+        c->arena = nullptr;
+        c->arena_bytes = 0;
+    }
+    const size_t want = bytes + bytes / 8 + (1 << 20);
+    if (cudaMalloc(&c->arena, want) != cudaSuccess) {
+        cudaGetLastError();
+        return fail(CORU_ENOMEM, "cudaMalloc of " + std::to_string(want) + " workspace bytes failed");
+    }
+    c->arena_bytes = want;
+    return CORU_OK;
+}
+
+int ensure_pinned(coru_ctx* c, size_t bytes) {
+    if (bytes <= c->pinned_bytes) return CORU_OK;
+    if (c->pinned) {
+        CORU_CUDA(cudaStreamSynchronize(c->stream));
+        cudaFreeHost(c->pinned);
+        c->pinned = nullptr;
+        c->pinned_bytes = 0;
+    }
+    if (cudaMallocHost(&c->pinned, bytes) != cudaSuccess) {
+        cudaGetLastError();
+        return fail(CORU_ENOMEM, "cudaMallocHost of " + std::to_string(bytes) + " bytes failed");
+    }
+    c->pinned_bytes = bytes;
+    return CORU_OK;
+}
+
+// check_corutv_params (corutv.hpp:67-71) + the q check (corutv.hpp:81), same messages.
+int check_params(int64_t m, int64_t n, int64_t ell, int q) {
+    if (m < 1 || n < 1) return fail(CORU_EINVAL, "Matrix: dimensions must be positive");
+    if (ell < 1) return fail(CORU_EINVAL, "corutv: ell must be >= 1");
+    if (ell >= std::min(m, n)) return fail(CORU_EINVAL, "corutv: ell must be < min(rows, cols)");
+    if (q < 0) return fail(CORU_EINVAL, "corutv: q must be >= 0");
+    return CORU_OK;
+}
+
+// ---- per-dtype kernel dispatch ------------------------------------------------------------------
+template <typename T>
+int64_t gemm_ws(Op op, int64_t Mo, int64_t K, int N, int sms);
+template <>
+int64_t gemm_ws<double>(Op op, int64_t Mo, int64_t K, int N, int sms) {
+    return plan_gemm_f64(op, Mo, K, N, sms).ws_elems;
+}
+template <>
+int64_t gemm_ws<float>(Op, int64_t, int64_t, int, int) {
+    return 0;
+}
+
+template <typename T>
+int gemm(coru_ctx* c, Op op, const T* A, int64_t lda, const T* X, int64_t ldx, T* C, int64_t ldc, int64_t Mo,
+         int64_t K, int N, T* ws, int64_t ws_elems);
+int prof_begin(coru_ctx* c, cudaEvent_t* stop) {
+    if (c->prof_used == c->prof_events.size()) {
+        cudaEvent_t a, b;
+        CORU_CUDA(cudaEventCreate(&a));
+        CORU_CUDA(cudaEventCreate(&b));
+        c->prof_events.emplace_back(a, b);
+    }
+    auto& ev = c->prof_events[c->prof_used++];
+    CORU_CUDA(cudaEventRecord(ev.first, c->stream));
+    *stop = ev.second;
+    return CORU_OK;
+}
+
+template <>
+int gemm<double>(coru_ctx* c, Op op, const double* A, int64_t lda, const double* X, int64_t ldx, double* C,
+                 int64_t ldc, int64_t Mo, int64_t K, int N, double* ws, int64_t ws_elems) {
+    GemmPlan p = plan_gemm_f64(op, Mo, K, N, c->num_sms);
+    if (p.ws_elems > ws_elems) return fail(CORU_ECUDA, "internal: gemm workspace too small");
+    cudaEvent_t stop = nullptr;
+    if (c->prof) CORU_TRY(prof_begin(c, &stop));
+    CORU_CUDA(gemm_f64(op, A, lda, X, ldx, C, ldc, Mo, K, N, p, ws, c->stream));
+    if (stop) {
+        CORU_CUDA(cudaEventRecord(stop, c->stream));
+        c->prof_flops += 2.0 * double(Mo) * double(K) * double(N);
+        c->prof_bytes += 8.0 * double(Mo) * double(K);
+    }
+    g_launches += p.splits > 1 ? 2 : 1;
+    return CORU_OK;
+}
+template <>
+int gemm<float>(coru_ctx*, Op, const float*, int64_t, const float*, int64_t, float*, int64_t, int64_t, int64_t, int,
+                float*, int64_t) {
+    return fail(CORU_ENOTSUP, "fp32 A-pass kernels are not in this build yet (DESIGN.md: fp32 / C5)");
+}
+
+template <typename T>
+struct TsqrBufs {
+    TsqrPlan plan;
+    T *v = nullptr, *beta = nullptr, *rarena = nullptr, *scratch = nullptr;
+    void carve(Carver& cv, int64_t rows, int d, int max_smem) {
+        plan = plan_tsqr(rows, d, sizeof(T), max_smem);
+        v = cv.take<T>(plan.v_elems);
+        beta = cv.take<T>(plan.beta_elems);
+        rarena = cv.take<T>(plan.r_elems);
+        int64_t maxrows = 0;
+        for (size_t l = 1; l < plan.levels.size(); ++l) maxrows = std::max<int64_t>(maxrows, plan.levels[l].rows);
+        scratch = cv.take<T>(tsqr_scratch_elems(plan) + 2 * maxrows * d);
+    }
+    int factor(const T* B, int64_t ldb, T* r_out, cudaStream_t st) {
+        CORU_CUDA(tsqr_factor<T>(plan, B, ldb, v, beta, rarena, r_out, st));
+        g_launches += int64_t(plan.levels.size());
+        return CORU_OK;
+    }
+    int form_q(const T* q_top, T* Q, int64_t ldq, cudaStream_t st) {
+        CORU_CUDA(tsqr_form_q<T>(plan, q_top, v, beta, scratch, Q, ldq, st));
+        g_launches += int64_t(plan.levels.size());
+        return CORU_OK;
+    }
+};
+
+enum class Mode { Full, Sketch, Project };
+
+// One decomposition request, already mapped onto A' (= A, or A^T for the ULV orientation).
+template <typename T>
+struct Request {
+    const T* A = nullptr;
+    int64_t lda = 0;
+    bool trans = false;     // run on A' = A^T (corutv.hpp:82-87), zero-copy via the op flag
+    int64_t rows = 0;       // rows of A' held by this rank
+    int64_t cols = 0;       // cols of A'
+    int d = 0;
+    int q = 0;
+    uint64_t seed = 0, stream = 0;
+    Mode mode = Mode::Full;
+    // Full: U' (rows x d), T' (d x d), V' (cols x d) — device, caller's buffers.
+    T* u = nullptr;
+    int64_t ldu = 0;
+    T* t = nullptr;
+    int64_t ldt = 0;
+    bool t_transpose = false;
+    T* v = nullptr;
+    int64_t ldv = 0;
+    int64_t* perm_host = nullptr;
+    int* warn_host = nullptr;
+    // Sketch: Q1, Q2, C1, C2prev (device, may be null except Q1/Q2).
+    T *q1 = nullptr, *q2 = nullptr, *c1 = nullptr, *c2p = nullptr;
+    int64_t ldq1 = 0, ldq2 = 0, ldc1 = 0, ldc2 = 0;
+    Op op_a() const { return trans ? Op::T : Op::N; }   // A'·X
+    Op op_at() const { return trans ? Op::N : Op::T; }  // A'^T·Y
+};
+
+template <typename T>
+struct Work {
+    T *b2 = nullptr, *b2prev = nullptr, *b1 = nullptr, *q1 = nullptr, *q2 = nullptr, *gws = nullptr;
+    int64_t gws_elems = 0;
+    TsqrBufs<T> ts1, ts2, tstop;
+    T *rstack = nullptr, *qtop = nullptr, *r1loc = nullptr, *r1 = nullptr, *r2 = nullptr;
+    T *m = nullptr, *qm = nullptr, *tm = nullptr, *qrcp_scr = nullptr;
+    int64_t* perm = nullptr;
+    int* flag = nullptr;
+
+    void layout(Carver& cv, const coru_ctx* c, const Request<T>& r, int dp) {
+        const int64_t R = r.rows, N = r.cols;
+        const int d = r.d, sms = c->num_sms;
+        b2 = cv.take<T>(N * dp);
+        b2prev = r.c2p ? cv.take<T>(N * dp) : nullptr;
+        b1 = cv.take<T>(R * dp);
+        q1 = cv.take<T>(R * dp);
+        q2 = cv.take<T>(N * dp);
+        gws_elems = std::max({gemm_ws<T>(r.op_a(), R, N, d, sms), gemm_ws<T>(r.op_at(), N, R, d, sms),
+                              gemm_ws<T>(Op::T, d, R, d, sms), gemm_ws<T>(Op::N, R, d, d, sms)});
+        gws = cv.take<T>(gws_elems);
+        ts1.carve(cv, R, d, c->max_smem);
+        ts2.carve(cv, N, d, c->max_smem);
+        if (c->world > 1) {
+            rstack = cv.take<T>(int64_t(c->world) * d * d);
+            tstop.carve(cv, int64_t(c->world) * d, d, c->max_smem);
+            qtop = cv.take<T>(int64_t(c->world) * d * d);
+        }
+        r1loc = cv.take<T>(int64_t(d) * d);
+        r1 = cv.take<T>(int64_t(d) * d);
+        r2 = cv.take<T>(int64_t(d) * d);
+        m = cv.take<T>(int64_t(d) * dp);
+        qm = cv.take<T>(int64_t(dp) * dp);
+        tm = cv.take<T>(int64_t(d) * d);
+        qrcp_scr = cv.take<T>(qrcp_scratch_elems(d));
+        perm = cv.take<int64_t>(d);
+        flag = cv.take<int>(4);
+    }
+};
+
+template <typename T>
+int allreduce(coru_ctx* c, T* buf, size_t count) {
+    if (c->world <= 1) return CORU_OK;
+    CORU_NCCL(nccl()->AllReduce(buf, buf, count, nccl_type<T>(), ncclSum, c->comm, c->stream));
+    return CORU_OK;
+}
+
+// The hot path. Enqueues everything on c->stream and synchronises once at the end (the flag and
+// the pivots are host outputs).
+template <typename T>
+int run(coru_ctx* c, const Request<T>& r, size_t extra_arena_off = 0) {
+    const int d = r.d;
+    const int dp = int(round_up(d, 8));
+    const int64_t R = r.rows, N = r.cols;
+    cudaStream_t st = c->stream;
+    Work<T> w;
+    Carver meas{nullptr, extra_arena_off};
+    w.layout(meas, c, r, dp);
+    CORU_TRY(ensure_arena(c, meas.off));
+    Carver cv{c->arena, extra_arena_off};
+    w.layout(cv, c, r, dp);
+
+    // Φ = gaussian(cols, ell, seed) on the host, padded to dp columns, one H2D (corutv.hpp:51).
+    const size_t phi_bytes = size_t(N) * dp * sizeof(T);
+    CORU_TRY(ensure_pinned(c, phi_bytes));
+    CORU_CUDA(cudaStreamSynchronize(st));  // the pinned staging buffer is reused across calls
+    T* phi = reinterpret_cast<T*>(c->pinned);
+    if (dp != d) std::memset(phi, 0, phi_bytes);
+    gaussian_host<T>(N, d, r.seed, r.stream, phi, dp, c->host_threads);
+    CORU_CUDA(cudaMemcpyAsync(w.b2, phi, phi_bytes, cudaMemcpyHostToDevice, st));
+    CORU_CUDA(cudaMemsetAsync(w.q1, 0, size_t(R) * dp * sizeof(T), st));
+    CORU_CUDA(cudaMemsetAsync(w.q2, 0, size_t(N) * dp * sizeof(T), st));
+
+    // Sketch and power rounds (corutv.hpp:54-58): c1 = a·c2 ; c2_prev = c2 ; c2 = a^T·c1.
+    for (int i = 0; i <= r.q; ++i) {
+        CORU_TRY(gemm<T>(c, r.op_a(), r.A, r.lda, w.b2, dp, w.b1, dp, R, N, d, w.gws, w.gws_elems));
+        if (i == r.q && w.b2prev)
+            CORU_CUDA(cudaMemcpyAsync(w.b2prev, w.b2, size_t(N) * dp * sizeof(T), cudaMemcpyDeviceToDevice, st));
+        CORU_TRY(gemm<T>(c, r.op_at(), r.A, r.lda, w.b1, dp, w.b2, dp, N, R, d, w.gws, w.gws_elems));
+        CORU_TRY(allreduce<T>(c, w.b2, size_t(N) * dp));
+    }
+
+    // Q1, R1 = QR(c1) through the TSQR tree (corutv.hpp:59), cross-rank top level when sharded.
+    if (c->world > 1) {
+        CORU_TRY(w.ts1.factor(w.b1, dp, w.r1loc, st));
+        CORU_NCCL(nccl()->AllGather(w.r1loc, w.rstack, size_t(d) * d, nccl_type<T>(), c->comm, st));
+        CORU_TRY(w.tstop.factor(w.rstack, d, w.r1, st));
+        CORU_TRY(w.tstop.form_q(nullptr, w.qtop, d, st));
+        CORU_TRY(w.ts1.form_q(w.qtop + int64_t(c->rank) * d * d, w.q1, dp, st));
+    } else {
+        CORU_TRY(w.ts1.factor(w.b1, dp, w.r1, st));
+        CORU_TRY(w.ts1.form_q(nullptr, w.q1, dp, st));
+    }
+    CORU_CUDA(conditioning_flag<T>(w.r1, d, d, w.flag, st));  // corutv.hpp:61-64
+    ++g_launches;
+    // Q2 = QR(c2) (corutv.hpp:60): c2 is replicated, so every rank computes the same tree.
+    CORU_TRY(w.ts2.factor(w.b2, dp, w.r2, st));
+    CORU_TRY(w.ts2.form_q(nullptr, w.q2, dp, st));
+
+    if (r.mode == Mode::Sketch) {
+        CORU_CUDA(copy_block<T>(w.q1, dp, r.q1, r.ldq1, R, d, st));
+        CORU_CUDA(copy_block<T>(w.q2, dp, r.q2, r.ldq2, N, d, st));
+        g_launches += 2;
+        if (r.c1) {
+            CORU_CUDA(copy_block<T>(w.b1, dp, r.c1, r.ldc1, R, d, st));
+            ++g_launches;
+        }
+        if (r.c2p) {
+            CORU_CUDA(copy_block<T>(w.b2prev, dp, r.c2p, r.ldc2, N, d, st));
+            ++g_launches;
+        }
+        int flag = 0;
+        CORU_CUDA(cudaMemcpyAsync(&flag, w.flag, sizeof(int), cudaMemcpyDeviceToHost, st));
+        CORU_CUDA(cudaStreamSynchronize(st));
+        if (r.warn_host) *r.warn_host = flag;
+        return CORU_OK;
+    }
+
+    // D = (Q1^T a) q2 (corutv.hpp:90) as Q1^T (A'·Q2): W = A'·Q2 reuses the B1 buffer.
+    T* W = w.b1;
+    CORU_TRY(gemm<T>(c, r.op_a(), r.A, r.lda, w.q2, dp, W, dp, R, N, d, w.gws, w.gws_elems));
+    {
+        const bool p = c->prof;  // Q1^T·W is m x d x d, not an A-pass
+        c->prof = false;
+        const int rc = gemm<T>(c, Op::T, w.q1, dp, W, dp, w.m, dp, d, R, d, w.gws, w.gws_elems);
+        c->prof = p;
+        CORU_TRY(rc);
+    }
+    CORU_TRY(allreduce<T>(c, w.m, size_t(d) * dp));
+
+    // QRCP of the core (corutv.hpp:93), then the lift (corutv.hpp:94-97).
+    CORU_CUDA(cudaMemsetAsync(w.qm, 0, size_t(dp) * dp * sizeof(T), st));
+    CORU_CUDA(qrcp<T>(w.m, dp, d, w.qm, dp, w.tm, d, w.perm, w.qrcp_scr, c->max_smem, st));
+    ++g_launches;
+    {
+        const bool p = c->prof;  // U = Q1·Q_M is m x d x d, not an A-pass
+        c->prof = false;
+        const int rc = gemm<T>(c, Op::N, w.q1, dp, w.qm, dp, r.u, r.ldu, R, d, d, w.gws, w.gws_elems);
+        c->prof = p;
+        CORU_TRY(rc);
+    }
+    CORU_CUDA(gather_columns<T>(w.q2, dp, w.perm, N, d, r.v, r.ldv, st));
+    ++g_launches;
+    if (r.t_transpose) CORU_CUDA(transpose_square<T>(w.tm, d, r.t, int(r.ldt), d, st));
+    else CORU_CUDA(copy_block<T>(w.tm, d, r.t, r.ldt, d, d, st));
+    ++g_launches;
+
+    int flag = 0;
+    CORU_CUDA(cudaMemcpyAsync(&flag, w.flag, sizeof(int), cudaMemcpyDeviceToHost, st));
+    if (r.perm_host) CORU_CUDA(cudaMemcpyAsync(r.perm_host, w.perm, sizeof(int64_t) * d, cudaMemcpyDeviceToHost, st));
+    CORU_CUDA(cudaStreamSynchronize(st));
+    if (r.warn_host) *r.warn_host = flag;
+    return CORU_OK;
+}
+
+int enter(coru_ctx* c) {
+    if (!c) return fail(CORU_EINVAL, "null context");
+    CORU_CUDA(cudaSetDevice(c->device));
+    return CORU_OK;
+}
+
+template <typename T>
+int corutv_dev(coru_ctx* c, const T* A, int64_t m_local, int64_t m, int64_t n, int64_t lda, int64_t ell, int q,
+               int variant, uint64_t seed, uint64_t stream, coru_utv* out) {
+    CORU_TRY(check_params(m, n, ell, q));
+    if (variant != CORU_D_EXACT)
+        return fail(CORU_ENOTSUP, "DVariant::approx (pinv core, corutv.hpp:91-92) is outside this build's scope");
+    if (!out || !A) return fail(CORU_EINVAL, "null argument");
+    if (c->world <= 1 && m_local != m) return fail(CORU_EINVAL, "m_local != m without a communicator");
+    if (lda < n) return fail(CORU_EINVAL, "lda < n");
+    Request<T> r;
+    r.A = A;
+    r.lda = lda;
+    r.d = int(ell);
+    r.q = q;
+    r.seed = seed;
+    r.stream = stream;
+    r.perm_host = out->perm;
+    r.warn_host = &out->conditioning_warning;
+    if (m < n) {
+        if (c->world > 1) return fail(CORU_ENOTSUP, "row-sharded ULV (rows < cols) is not supported");
+        // corutv(a^T) then {v, t^T, u, lower = true} (corutv.hpp:82-87).
+        r.trans = true;
+        r.rows = n;
+        r.cols = m;
+        r.u = static_cast<T*>(out->v);
+        r.ldu = out->ldv;
+        r.v = static_cast<T*>(out->u);
+        r.ldv = out->ldu;
+        r.t = static_cast<T*>(out->t);
+        r.ldt = out->ldt;
+        r.t_transpose = true;
+        out->lower = 1;
+    } else {
+        r.rows = m_local;
+        r.cols = n;
+        r.u = static_cast<T*>(out->u);
+        r.ldu = out->ldu;
+        r.v = static_cast<T*>(out->v);
+        r.ldv = out->ldv;
+        r.t = static_cast<T*>(out->t);
+        r.ldt = out->ldt;
+        out->lower = 0;
+    }
+    return run<T>(c, r);
+}
+
+// Host-buffer entry: upload A into the arena head, run, download. Single GPU.
+template <typename T>
+int corutv_host(coru_ctx* c, const T* A, int64_t m, int64_t n, int64_t ell, int q, int variant, uint64_t seed,
+                uint64_t stream, T* U, T* Tt, T* V, int64_t* perm, int* lower, int* warn) {
+    CORU_TRY(check_params(m, n, ell, q));
+    if (variant != CORU_D_EXACT)
+        return fail(CORU_ENOTSUP, "DVariant::approx (pinv core, corutv.hpp:91-92) is outside this build's scope");
+    if (!A || !U || !Tt || !V) return fail(CORU_EINVAL, "null argument");
+    if (c->world > 1) return fail(CORU_EINVAL, "host-buffer entry is single-GPU; use the _dev entry per rank");
+    // Head of the arena: A, U, T, V and a flag, then the decomposition workspace.
+    Carver head{nullptr, 0};
+    auto lay = [&](Carver& cv, T*& a, T*& u, T*& t, T*& v, int*& f) {
+        a = cv.template take<T>(m * n);
+        u = cv.template take<T>(m * ell);
+        t = cv.template take<T>(ell * ell);
+        v = cv.template take<T>(n * ell);
+        f = cv.template take<int>(4);
+    };
+    T *a_d, *u_d, *t_d, *v_d;
+    int* f_d;
+    lay(head, a_d, u_d, t_d, v_d, f_d);
+    const size_t head_bytes = (head.off + 255) / 256 * 256;
+    // Reserve the head plus a generous guess; run() grows the arena if needed, so size it first.
+    {
+        Request<T> probe;
+        probe.rows = m >= n ? m : n;
+        probe.cols = m >= n ? n : m;
+        probe.d = int(ell);
+        Work<T> w;
+        Carver meas{nullptr, head_bytes};
+        w.layout(meas, c, probe, int(round_up(ell, 8)));
+        CORU_TRY(ensure_arena(c, meas.off));
+    }
+    Carver cv{c->arena, 0};
+    lay(cv, a_d, u_d, t_d, v_d, f_d);
+    cudaStream_t st = c->stream;
+    CORU_CUDA(cudaMemcpyAsync(a_d, A, sizeof(T) * m * n, cudaMemcpyHostToDevice, st));
+    CORU_CUDA(any_nonfinite<T>(a_d, m * n, f_d, st));
+    ++g_launches;
+    coru_utv out{u_d, ell, t_d, ell, v_d, ell, perm, 0, 0};
+    Request<T> r;
+    r.A = a_d;
+    r.lda = n;
+    r.d = int(ell);
+    r.q = q;
+    r.seed = seed;
+    r.stream = stream;
+    r.perm_host = perm;
+    r.warn_host = &out.conditioning_warning;
+    if (m < n) {
+        r.trans = true;
+        r.rows = n;
+        r.cols = m;
+        r.u = v_d;
+        r.ldu = ell;
+        r.v = u_d;
+        r.ldv = ell;
+        r.t = t_d;
+        r.ldt = ell;
+        r.t_transpose = true;
+    } else {
+        r.rows = m;
+        r.cols = n;
+        r.u = u_d;
+        r.ldu = ell;
+        r.v = v_d;
+        r.ldv = ell;
+        r.t = t_d;
+        r.ldt = ell;
+    }
+    CORU_TRY(run<T>(c, r, head_bytes));
+    int bad = 0;
+    CORU_CUDA(cudaMemcpyAsync(&bad, f_d, sizeof(int), cudaMemcpyDeviceToHost, st));
+    CORU_CUDA(cudaMemcpyAsync(U, u_d, sizeof(T) * m * ell, cudaMemcpyDeviceToHost, st));
+    CORU_CUDA(cudaMemcpyAsync(Tt, t_d, sizeof(T) * ell * ell, cudaMemcpyDeviceToHost, st));
+    CORU_CUDA(cudaMemcpyAsync(V, v_d, sizeof(T) * n * ell, cudaMemcpyDeviceToHost, st));
+    CORU_CUDA(cudaStreamSynchronize(st));
+    if (bad) return fail(CORU_EINVAL, "Matrix: non-finite entry");
+    if (lower) *lower = m < n ? 1 : 0;
+    if (warn) *warn = out.conditioning_warning;
+    return CORU_OK;
+}
+
+}  // namespace
+
+// ==== exported C-ABI =========================================================================
+extern "C" {
+
+int coru_abi_version(void) { return CORU_GPU_ABI_VERSION; }
+const char* coru_last_error(void) { return g_err.c_str(); }
+
+int64_t coru_launch_count(int reset) {
+    const int64_t v = g_launches;
+    if (reset) g_launches = 0;
+    return v;
+}
+
+int coru_ctx_create(int device, coru_ctx** out) {
+    if (!out) return fail(CORU_EINVAL, "null out");
+    *out = nullptr;
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0) {
+        cudaGetLastError();
+        return fail(CORU_ECUDA, "no CUDA device visible (coru_gpu has no CPU fallback)");
+    }
+    if (device < 0 || device >= n) return fail(CORU_EINVAL, "device index out of range");
+    cudaDeviceProp prop;
+    CORU_CUDA(cudaGetDeviceProperties(&prop, device));
+    if (prop.major != 10) return fail(CORU_ECUDA, std::string("device is not sm_100 (B200): ") + prop.name);
+    CORU_CUDA(cudaSetDevice(device));
+    auto* c = new coru_ctx;
+    c->device = device;
+    c->num_sms = prop.multiProcessorCount;
+    c->max_smem = int(prop.sharedMemPerBlockOptin);
+    c->host_threads = int(std::max(1u, std::min(16u, std::thread::hardware_concurrency())));
+    if (cudaStreamCreateWithFlags(&c->own_stream, cudaStreamNonBlocking) != cudaSuccess) {
+        delete c;
+        return fail(CORU_ECUDA, "cudaStreamCreate failed");
+    }
+    c->stream = c->own_stream;
+    *out = c;
+    return CORU_OK;
+}
+
+void coru_ctx_destroy(coru_ctx* c) {
+    if (!c) return;
+    cudaSetDevice(c->device);
+    if (c->stream) cudaStreamSynchronize(c->stream);
+    if (c->comm && nccl() && nccl()->CommDestroy) nccl()->CommDestroy(c->comm);
+    if (c->arena) cudaFree(c->arena);
+    if (c->pinned) cudaFreeHost(c->pinned);
+    if (c->own_stream) cudaStreamDestroy(c->own_stream);
+    for (auto& e : c->prof_events) {
+        cudaEventDestroy(e.first);
+        cudaEventDestroy(e.second);
+    }
+    delete c;
+}
+
+int coru_ctx_set_stream(coru_ctx* c, void* s) {
+    if (!c) return fail(CORU_EINVAL, "null context");
+    std::lock_guard<std::mutex> lk(c->mu);
+    c->stream = s ? static_cast<cudaStream_t>(s) : c->own_stream;
+    return CORU_OK;
+}
+
+int coru_ctx_set_profiling(coru_ctx* c, int enable) {
+    if (!c) return fail(CORU_EINVAL, "null context");
+    std::lock_guard<std::mutex> lk(c->mu);
+    c->prof = enable != 0;
+    c->prof_used = 0;
+    c->prof_flops = c->prof_bytes = 0;
+    return CORU_OK;
+}
+
+int coru_ctx_profile_apass(coru_ctx* c, double* total_ms, int64_t* launches, double* flops, double* bytes) {
+    CORU_TRY(enter(c));
+    std::lock_guard<std::mutex> lk(c->mu);
+    double ms = 0;
+    for (size_t i = 0; i < c->prof_used; ++i) {
+        float t = 0;
+        CORU_CUDA(cudaEventSynchronize(c->prof_events[i].second));
+        CORU_CUDA(cudaEventElapsedTime(&t, c->prof_events[i].first, c->prof_events[i].second));
+        ms += t;
+    }
+    if (total_ms) *total_ms = ms;
+    if (launches) *launches = int64_t(c->prof_used);
+    if (flops) *flops = c->prof_flops;
+    if (bytes) *bytes = c->prof_bytes;
+    c->prof_used = 0;
+    c->prof_flops = c->prof_bytes = 0;
+    return CORU_OK;
+}
+
+int coru_ctx_set_host_threads(coru_ctx* c, int threads) {
+    if (!c || threads < 1) return fail(CORU_EINVAL, "bad argument");
+    std::lock_guard<std::mutex> lk(c->mu);
+    c->host_threads = threads;
+    return CORU_OK;
+}
+
+int coru_comm_unique_id(unsigned char id[128]) {
+    Nccl* api = nccl();
+    if (!api) return fail(CORU_ENCCL, "NCCL unavailable");
+    ncclUniqueId u;
+    CORU_NCCL(api->GetUniqueId(&u));
+    static_assert(sizeof(u) == 128, "ncclUniqueId is 128 bytes");
+    std::memcpy(id, &u, 128);
+    return CORU_OK;
+}
+
+int coru_ctx_init_comm(coru_ctx* c, int rank, int world, const unsigned char id[128]) {
+    CORU_TRY(enter(c));
+    if (world < 1 || rank < 0 || rank >= world) return fail(CORU_EINVAL, "bad rank/world");
+    std::lock_guard<std::mutex> lk(c->mu);
+    if (world == 1) {
+        c->rank = 0;
+        c->world = 1;
+        return CORU_OK;
+    }
+    Nccl* api = nccl();
+    if (!api) return fail(CORU_ENCCL, "NCCL unavailable");
+    ncclUniqueId u;
+    std::memcpy(&u, id, 128);
+    CORU_NCCL(api->CommInitRank(&c->comm, world, u, rank));
+    c->rank = rank;
+    c->world = world;
+    return CORU_OK;
+}
+
+void coru_shard_rows(int64_t m, int rank, int world, int64_t* row0, int64_t* rows) {
+    // Contiguous, balanced row blocks: rank g owns [g*m/G, (g+1)*m/G).
+    const int64_t a = m * rank / world, b = m * (rank + 1) / world;
+    if (row0) *row0 = a;
+    if (rows) *rows = b - a;
+}
+
+int coru_corutv_f64_dev(coru_ctx* c, const double* A, int64_t m_local, int64_t m, int64_t n, int64_t lda,
+                        int64_t ell, int q, int variant, uint64_t seed, uint64_t stream, coru_utv* out) {
+    CORU_TRY(enter(c));
+    std::lock_guard<std::mutex> lk(c->mu);
+    return corutv_dev<double>(c, A, m_local, m, n, lda, ell, q, variant, seed, stream, out);
+}
+
+int coru_corutv_f32_dev(coru_ctx* c, const float* A, int64_t m_local, int64_t m, int64_t n, int64_t lda,
+                        int64_t ell, int q, int variant, uint64_t seed, uint64_t stream, coru_utv* out) {
+    CORU_TRY(enter(c));
+    std::lock_guard<std::mutex> lk(c->mu);
+    return corutv_dev<float>(c, A, m_local, m, n, lda, ell, q, variant, seed, stream, out);
+}
+
+int coru_corutv_f64(coru_ctx* c, const double* A, int64_t m, int64_t n, int64_t ell, int q, int variant,
+                    uint64_t seed, uint64_t stream, double* U, double* T, double* V, int64_t* perm, int* lower,
+                    int* warn) {
+    CORU_TRY(enter(c));
+    std::lock_guard<std::mutex> lk(c->mu);
+    return corutv_host<double>(c, A, m, n, ell, q, variant, seed, stream, U, T, V, perm, lower, warn);
+}
+
+int coru_corutv_f32(coru_ctx* c, const float* A, int64_t m, int64_t n, int64_t ell, int q, int variant,
+                    uint64_t seed, uint64_t stream, float* U, float* T, float* V, int64_t* perm, int* lower,
+                    int* warn) {
+    CORU_TRY(enter(c));
+    std::lock_guard<std::mutex> lk(c->mu);
+    return corutv_host<float>(c, A, m, n, ell, q, variant, seed, stream, U, T, V, perm, lower, warn);
+}
+
+int coru_sketch_bases_f64_dev(coru_ctx* c, const double* A, int64_t m_local, int64_t m, int64_t n, int64_t lda,
+                              int64_t ell, int q, uint64_t seed, uint64_t stream, double* Q1, int64_t ldq1,
+                              double* Q2, int64_t ldq2, double* C1, int64_t ldc1, double* C2prev, int64_t ldc2,
+                              int* warn) {
+    CORU_TRY(enter(c));
+    std::lock_guard<std::mutex> lk(c->mu);
+    CORU_TRY(check_params(m, n, ell, q));
+    if (!A || !Q1 || !Q2) return fail(CORU_EINVAL, "null argument");
+    if (c->world <= 1 && m_local != m) return fail(CORU_EINVAL, "m_local != m without a communicator");
+    Request<double> r;
+    r.A = A;
+    r.lda = lda;
+    r.rows = m_local;
+    r.cols = n;
+    r.d = int(ell);
+    r.q = q;
+    r.seed = seed;
+    r.stream = stream;
+    r.mode = Mode::Sketch;
+    r.q1 = Q1;
+    r.ldq1 = ldq1;
+    r.q2 = Q2;
+    r.ldq2 = ldq2;
+    r.c1 = C1;
+    r.ldc1 = ldc1;
+    r.c2p = C2prev;
+    r.ldc2 = ldc2;
+    r.warn_host = warn;
+    return run<double>(c, r);
+}
+
+int coru_sketch_bases_f64(coru_ctx* c, const double* A, int64_t m, int64_t n, int64_t ell, int q, uint64_t seed,
+                          uint64_t stream, double* Q1, double* Q2, double* C1, double* C2prev, int* warn) {
+    CORU_TRY(enter(c));
+    std::lock_guard<std::mutex> lk(c->mu);
+    CORU_TRY(check_params(m, n, ell, q));
+    if (!A || !Q1 || !Q2) return fail(CORU_EINVAL, "null argument");
+    Carver head{nullptr, 0};
+    double *a_d = head.take<double>(m * n), *q1_d = head.take<double>(m * ell), *q2_d = head.take<double>(n * ell),
+           *c1_d = head.take<double>(m * ell), *c2_d = head.take<double>(n * ell);
+    const size_t head_bytes = (head.off + 255) / 256 * 256;
+    Request<double> r;
+    r.rows = m;
+    r.cols = n;
+    r.d = int(ell);
+    r.q = q;
+    r.seed = seed;
+    r.stream = stream;
+    r.mode = Mode::Sketch;
+    r.c2p = reinterpret_cast<double*>(1);  // request the c2_prev buffer in the layout
+    {
+        Work<double> w;
+        Carver meas{nullptr, head_bytes};
+        w.layout(meas, c, r, int(round_up(ell, 8)));
+        CORU_TRY(ensure_arena(c, meas.off));
+    }
+    Carver cv{c->arena, 0};
+    a_d = cv.take<double>(m * n);
+    q1_d = cv.take<double>(m * ell);
+    q2_d = cv.take<double>(n * ell);
+    c1_d = cv.take<double>(m * ell);
+    c2_d = cv.take<double>(n * ell);
+    cudaStream_t st = c->stream;
+    CORU_CUDA(cudaMemcpyAsync(a_d, A, sizeof(double) * m * n, cudaMemcpyHostToDevice, st));
+    r.A = a_d;
+    r.lda = n;
+    r.q1 = q1_d;
+    r.ldq1 = ell;
+    r.q2 = q2_d;
+    r.ldq2 = ell;
+    r.c1 = c1_d;
+    r.ldc1 = ell;
+    r.c2p = c2_d;
+    r.ldc2 = ell;
+    r.warn_host = warn;
+    CORU_TRY(run<double>(c, r, head_bytes));
+    CORU_CUDA(cudaMemcpyAsync(Q1, q1_d, sizeof(double) * m * ell, cudaMemcpyDeviceToHost, st));
+    CORU_CUDA(cudaMemcpyAsync(Q2, q2_d, sizeof(double) * n * ell, cudaMemcpyDeviceToHost, st));
+    if (C1) CORU_CUDA(cudaMemcpyAsync(C1, c1_d, sizeof(double) * m * ell, cudaMemcpyDeviceToHost, st));
+    if (C2prev) CORU_CUDA(cudaMemcpyAsync(C2prev, c2_d, sizeof(double) * n * ell, cudaMemcpyDeviceToHost, st));
+    CORU_CUDA(cudaStreamSynchronize(st));
+    return CORU_OK;
+}
+
+int coru_project_f64_dev(coru_ctx* c, const double* A, int64_t m_local, int64_t n, int64_t lda, const double* Q1,
+                         int64_t ldq1, const double* Q2, int64_t ldq2, int64_t ell, double* D, int64_t ldd) {
+    CORU_TRY(enter(c));
+    std::lock_guard<std::mutex> lk(c->mu);
+    if (ell < 1 || !A || !Q1 || !Q2 || !D) return fail(CORU_EINVAL, "bad argument");
+    const int d = int(ell);
+    Carver meas{nullptr, 0};
+    auto lay = [&](Carver& cv, double*& W, double*& Mb, double*& ws, int64_t& wse) {
+        W = cv.take<double>(m_local * ell);
+        Mb = cv.take<double>(ell * ell);
+        wse = std::max(gemm_ws<double>(Op::N, m_local, n, d, c->num_sms), gemm_ws<double>(Op::T, d, m_local, d, c->num_sms));
+        ws = cv.take<double>(wse);
+    };
+    double *W, *Mb, *ws;
+    int64_t wse;
+    lay(meas, W, Mb, ws, wse);
+    CORU_TRY(ensure_arena(c, meas.off));
+    Carver cv{c->arena, 0};
+    lay(cv, W, Mb, ws, wse);
+    CORU_TRY(gemm<double>(c, Op::N, A, lda, Q2, ldq2, W, d, m_local, n, d, ws, wse));
+    CORU_TRY(gemm<double>(c, Op::T, Q1, ldq1, W, d, Mb, d, d, m_local, d, ws, wse));
+    CORU_TRY(allreduce<double>(c, Mb, size_t(d) * d));
+    CORU_CUDA(copy_block<double>(Mb, d, D, ldd, d, d, c->stream));
+    ++g_launches;
+    CORU_CUDA(cudaStreamSynchronize(c->stream));
+    return CORU_OK;
+}
+
+int coru_gaussian(int64_t rows, int64_t cols, uint64_t seed, uint64_t stream, double* out, int threads) {
+    if (rows < 1 || cols < 1 || !out) return fail(CORU_EINVAL, "Matrix: dimensions must be positive");
+    gaussian_host<double>(rows, cols, seed, stream, out, cols, threads);
+    return CORU_OK;
+}
+
+int coru_gemm_f64_dev(coru_ctx* c, int op, const double* A, int64_t lda, const double* X, int64_t ldx, double* C,
+                      int64_t ldc, int64_t rows, int64_t K, int64_t N) {
+    CORU_TRY(enter(c));
+    std::lock_guard<std::mutex> lk(c->mu);
+    if (rows < 1 || K < 1 || N < 1 || N > 4096 || (op != 0 && op != 1)) return fail(CORU_EINVAL, "bad gemm shape");
+    if (ldx % 2 != 0 || reinterpret_cast<uintptr_t>(X) % 16 != 0)
+        return fail(CORU_EINVAL, "X must be 16-byte aligned with an even leading dimension");
+    const Op o = op ? Op::T : Op::N;
+    const int64_t wse = gemm_ws<double>(o, rows, K, int(N), c->num_sms);
+    CORU_TRY(ensure_arena(c, size_t(wse) * 8 + 256));
+    CORU_TRY(gemm<double>(c, o, A, lda, X, ldx, C, ldc, rows, K, int(N), reinterpret_cast<double*>(c->arena), wse));
+    CORU_CUDA(cudaStreamSynchronize(c->stream));
+    return CORU_OK;
+}
+
+int coru_tsqr_f64_dev(coru_ctx* c, const double* B, int64_t ldb, int64_t m, int64_t n, double* Q, int64_t ldq,
+                      double* R, int64_t ldr) {
+    CORU_TRY(enter(c));
+    std::lock_guard<std::mutex> lk(c->mu);
+    if (n < 1 || m <= n) return fail(CORU_EINVAL, "householder_qr: requires rows > cols for TSQR");
+    TsqrBufs<double> tb;
+    Carver meas{nullptr, 0};
+    tb.carve(meas, m, int(n), c->max_smem);
+    double* r = meas.take<double>(n * n);
+    CORU_TRY(ensure_arena(c, meas.off));
+    Carver cv{c->arena, 0};
+    tb.carve(cv, m, int(n), c->max_smem);
+    r = cv.take<double>(n * n);
+    CORU_TRY(tb.factor(B, ldb, r, c->stream));
+    CORU_TRY(tb.form_q(nullptr, Q, ldq, c->stream));
+    CORU_CUDA(copy_block<double>(r, n, R, ldr, n, int(n), c->stream));
+    ++g_launches;
+    CORU_CUDA(cudaStreamSynchronize(c->stream));
+    return CORU_OK;
+}
+
+int coru_qrcp_f64_dev(coru_ctx* c, const double* M, int64_t ldm, int64_t n, double* Q, int64_t ldq, double* R,
+                      int64_t ldr, int64_t* perm) {
+    CORU_TRY(enter(c));
+    std::lock_guard<std::mutex> lk(c->mu);
+    if (n < 1 || n > 544) return fail(CORU_EINVAL, "qrcp: 1 <= n <= 544");
+    Carver meas{nullptr, 0};
+    meas.take<double>(qrcp_scratch_elems(int(n)));
+    meas.take<int64_t>(n);
+    CORU_TRY(ensure_arena(c, meas.off));
+    Carver cv{c->arena, 0};
+    double* scr = cv.take<double>(qrcp_scratch_elems(int(n)));
+    int64_t* p = cv.take<int64_t>(n);
+    CORU_CUDA(qrcp<double>(M, int(ldm), int(n), Q, int(ldq), R, int(ldr), p, scr, c->max_smem, c->stream));
+    ++g_launches;
+    CORU_CUDA(cudaMemcpyAsync(perm, p, sizeof(int64_t) * n, cudaMemcpyDeviceToHost, c->stream));
+    CORU_CUDA(cudaStreamSynchronize(c->stream));
+    return CORU_OK;
+}
+
+}  // extern "C"

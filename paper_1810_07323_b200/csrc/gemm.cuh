@@ -1,0 +1,26 @@
+// Skinny A-pass GEMMs of CoR-UTV.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace coru_gpu {
+
+// C[Mo x N] = op(A) · X where
+//   op = N : op(A) = A   (A is Mo x K, row-major, lda)          — B1 = A·B2, W = A·Q2, U = Q1·Q_M
+//   op = T : op(A) = A^T (A is K x Mo, row-major, lda; no copy) — B2 = A^T·B1, M = Q1^T·W
+// X is K x N row-major (ldx), C is Mo x N row-major (ldc). N is the (padded) sketch width.
+// Deterministic: split-K partials are reduced in a fixed order; no floating-point atomics.
+enum class Op { N = 0, T = 1 };
+
+struct GemmPlan {
+    int bm = 0, bn = 0, splits = 1;
+    int64_t ws_elems = 0;  // workspace (partials) needed, in elements
+};
+
+GemmPlan plan_gemm_f64(Op op, int64_t Mo, int64_t K, int N, int num_sms);
+// `ws` must hold plan.ws_elems doubles when plan.splits > 1.
+cudaError_t gemm_f64(Op op, const double* A, int64_t lda, const double* X, int64_t ldx, double* C,
+                     int64_t ldc, int64_t Mo, int64_t K, int N, const GemmPlan& plan, double* ws,
+                     cudaStream_t stream);
+
+}  // namespace coru_gpu

@@ -1,0 +1,314 @@
+// Businger–Golub QRCP of the d x d core M = Q1^T A Q2 (qr.hpp:106-143, called at corutv.hpp:93),
+// then the lift U = Q1·Q_M (GEMM, elsewhere) and V = Q2·P (gather here, corutv.hpp:95-97).
+//
+// One CTA; M lives column-major in shared memory when it fits (else in an L2-resident global
+// scratch). Per pivot step: block argmax of the downdated squared norms with the reference's
+// tie rule (strict >, so the lowest index wins, qr.hpp:122-123), column swap, reflector
+// (make_reflector recipe), then warps update their trailing columns and downdate
+// colsq[c] -= w(j,c)^2 with the 1e-6 recompute guard (qr.hpp:133-139). The norm updates use
+// uncontracted __dmul_rn/__dsub_rn so the downdate rounds like the reference.
+// Q_M is accumulated backwards onto I exactly like accumulate_q (qr.hpp:60-72).
+#include <algorithm>
+
+#include "common.cuh"
+#include "qrcp.cuh"
+
+namespace coru_gpu {
+
+namespace {
+
+constexpr int kThreads = 256;
+constexpr int kWarps = kThreads / 32;
+constexpr int kQPer = 17;  // Q_M column held as 17 values per lane: d <= 544
+
+template <typename T> __device__ __forceinline__ T mul_rn(T a, T b);
+template <> __device__ __forceinline__ double mul_rn<double>(double a, double b) { return __dmul_rn(a, b); }
+template <> __device__ __forceinline__ float mul_rn<float>(float a, float b) { return __fmul_rn(a, b); }
+template <typename T> __device__ __forceinline__ T add_rn(T a, T b);
+template <> __device__ __forceinline__ double add_rn<double>(double a, double b) { return __dadd_rn(a, b); }
+template <> __device__ __forceinline__ float add_rn<float>(float a, float b) { return __fadd_rn(a, b); }
+template <typename T> __device__ __forceinline__ T tsqrt(T x);
+template <> __device__ __forceinline__ double tsqrt<double>(double x) { return sqrt(x); }
+template <> __device__ __forceinline__ float tsqrt<float>(float x) { return sqrtf(x); }
+
+template <typename T>
+__device__ __forceinline__ T warp_sumsq(const T* col, int lo, int hi, int lane) {
+    T s = 0;
+    for (int i = lo + lane; i < hi; i += 32) s = add_rn(s, mul_rn(col[i], col[i]));
+    return warp_sum(s);
+}
+
+template <typename T>
+__global__ void __launch_bounds__(kThreads) k_qrcp(const T* __restrict__ M, int ldm, int d, T* __restrict__ Q, int ldq,
+                                                   T* __restrict__ Tout, int ldt, int64_t* __restrict__ perm_out,
+                                                   T* __restrict__ gscratch, int use_smem) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    // smem layout: colsq[d], base[d], beta[d] (T), perm[d] (int), piv (int), then W if it fits.
+    T* colsq = reinterpret_cast<T*>(smem_raw);
+    T* base = colsq + d;
+    T* beta = base + d;
+    int* perm = reinterpret_cast<int*>(beta + d);
+    int* piv_s = perm + d;
+    const int ldw = d | 1;
+    T* W = use_smem ? reinterpret_cast<T*>(smem_raw + (((3 * d * sizeof(T) + (d + 1) * 4) + 15) / 16) * 16)
+                    : gscratch;
+    for (int e = tid; e < d * d; e += kThreads) {
+        const int r = e / d, c = e % d;
+        W[c * ldw + r] = M[r * ldm + c];
+    }
+    for (int c = tid; c < d; c += kThreads) perm[c] = c;
+    __syncthreads();
+    // Initial squared norms (qr.hpp:115-119).
+    for (int c = warp; c < d; c += kWarps) {
+        const T s = warp_sumsq(W + c * ldw, 0, d, lane);
+        if (lane == 0) colsq[c] = base[c] = s;
+    }
+    __syncthreads();
+    for (int j = 0; j < d; ++j) {
+        // Argmax with lowest-index ties (qr.hpp:121-123), warp 0: each lane keeps the first
+        // maximum of its strided scan; the merge prefers the larger value, then the lower index.
+        if (warp == 0) {
+            T bv = T(0);
+            int bi = -1;
+            for (int c = j + lane; c < d; c += 32) {
+                const T v = colsq[c];
+                if (bi < 0 || v > bv) { bv = v; bi = c; }
+            }
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                const T ov = __shfl_xor_sync(0xffffffffu, bv, o);
+                const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+                if (oi >= 0 && (bi < 0 || ov > bv || (ov == bv && oi < bi))) { bv = ov; bi = oi; }
+            }
+            if (lane == 0) *piv_s = bi;
+        }
+        __syncthreads();
+        const int piv = *piv_s;
+        if (piv != j) {  // swap columns j, piv (qr.hpp:124-129)
+            for (int i = tid; i < d; i += kThreads) {
+                const T x = W[j * ldw + i];
+                W[j * ldw + i] = W[piv * ldw + i];
+                W[piv * ldw + i] = x;
+            }
+            if (tid == 0) {
+                T x = colsq[j]; colsq[j] = colsq[piv]; colsq[piv] = x;
+                x = base[j]; base[j] = base[piv]; base[piv] = x;
+                const int p = perm[j]; perm[j] = perm[piv]; perm[piv] = p;
+            }
+            __syncthreads();
+        }
+        // Reflector for column j (make_reflector, qr.hpp:32-45), warp 0.
+        if (warp == 0) {
+            T* col = W + j * ldw;
+            const T sig = warp_sumsq(col, j + 1, d, lane);
+            const T x0 = col[j];
+            T b = 0;
+            if (sig != T(0)) {
+                const T mu = tsqrt(add_rn(mul_rn(x0, x0), sig));
+                const T v0 = (x0 <= T(0)) ? x0 - mu : -sig / (x0 + mu);
+                b = T(2) * v0 * v0 / (sig + v0 * v0);
+                for (int i = j + 1 + lane; i < d; i += 32) col[i] /= v0;
+                __syncwarp();
+                if (lane == 0) col[j] = mu;
+            }
+            if (lane == 0) beta[j] = b;
+        }
+        __syncthreads();
+        // Trailing update + downdate (qr.hpp:131-139).
+        const T bj = beta[j];
+        const T* vcol = W + j * ldw;
+        for (int c = j + 1 + warp; c < d; c += kWarps) {
+            T* col = W + c * ldw;
+            if (bj != T(0)) {
+                T s = 0;
+                for (int i = j + 1 + lane; i < d; i += 32) s += vcol[i] * col[i];
+                s = warp_sum(s);
+                s += col[j];
+                s *= bj;
+                for (int i = j + 1 + lane; i < d; i += 32) col[i] -= s * vcol[i];
+                __syncwarp();
+                if (lane == 0) col[j] -= s;
+                __syncwarp();
+            }
+            T cs = 0;
+            if (lane == 0) {
+                const T w = col[j];
+                cs = colsq[c] - mul_rn(w, w);
+            }
+            cs = __shfl_sync(0xffffffffu, cs, 0);
+            bool small = false;
+            if (lane == 0) small = cs < T(1e-6) * base[c];
+            small = __shfl_sync(0xffffffffu, small, 0);
+            if (small) {
+                const T s = warp_sumsq(col, j + 1, d, lane);
+                if (lane == 0) colsq[c] = base[c] = s;
+            } else if (lane == 0) {
+                colsq[c] = cs;
+            }
+        }
+        __syncthreads();
+    }
+    // T = upper triangle (qr.hpp:74-79), perm out.
+    for (int e = tid; e < d * d; e += kThreads) {
+        const int r = e / d, c = e % d;
+        Tout[r * ldt + c] = (r <= c) ? W[c * ldw + r] : T(0);
+    }
+    for (int c = tid; c < d; c += kThreads) perm_out[c] = perm[c];
+    __syncthreads();
+    // Q_M: apply reflectors backwards onto I (qr.hpp:60-72); column c of Q owned by one warp.
+    // Reuse the strictly-lower part of W (the reflectors) and a per-warp column in registers.
+    for (int c = warp; c < d; c += kWarps) {
+        T q[kQPer];
+#pragma unroll
+        for (int u = 0; u < kQPer; ++u) {
+            const int i = lane + 32 * u;
+            q[u] = (i == c) ? T(1) : T(0);
+        }
+        for (int j = d - 1; j >= 0; --j) {
+            const T bj = beta[j];
+            if (bj == T(0)) continue;
+            const T* vcol = W + j * ldw;
+            T s = 0;
+#pragma unroll
+            for (int u = 0; u < kQPer; ++u) {
+                const int i = lane + 32 * u;
+                if (i > j && i < d) s += vcol[i] * q[u];
+            }
+            s = warp_sum(s);
+            T qsel = 0;
+#pragma unroll
+            for (int u = 0; u < kQPer; ++u)
+                if (u == (j >> 5)) qsel = q[u];
+            const T qj = __shfl_sync(0xffffffffu, qsel, j & 31);
+            s += qj;
+            s *= bj;
+#pragma unroll
+            for (int u = 0; u < kQPer; ++u) {
+                const int i = lane + 32 * u;
+                if (i > j && i < d) q[u] -= s * vcol[i];
+                if (i == j) q[u] -= s;
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < kQPer; ++u) {
+            const int i = lane + 32 * u;
+            if (i < d) Q[i * ldq + c] = q[u];
+        }
+    }
+}
+
+template <typename T>
+__global__ void k_gather_columns(const T* __restrict__ Q2, int64_t ldq, const int64_t* __restrict__ perm, int64_t n,
+                                 int d, T* __restrict__ V, int64_t ldv) {
+    const int64_t total = n * d;
+    for (int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < total; e += int64_t(gridDim.x) * blockDim.x) {
+        const int64_t i = e / d;
+        const int j = int(e % d);
+        V[i * ldv + j] = Q2[i * ldq + perm[j]];
+    }
+}
+
+template <typename T>
+__global__ void k_conditioning_flag(const T* R, int ldr, int d, int* flag) {
+    const double r00 = fabs(double(R[0]));
+    const double rll = fabs(double(R[(d - 1) * ldr + (d - 1)]));
+    *flag = rll <= 1e-14 * r00;
+}
+
+template <typename T>
+__global__ void k_copy_block(const T* __restrict__ src, int64_t lds, T* __restrict__ dst, int64_t ldd, int64_t rows,
+                             int cols) {
+    const int64_t total = rows * cols;
+    for (int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < total; e += int64_t(gridDim.x) * blockDim.x) {
+        const int64_t r = e / cols;
+        const int c = int(e % cols);
+        dst[r * ldd + c] = src[r * lds + c];
+    }
+}
+
+template <typename T>
+__global__ void k_any_nonfinite(const T* __restrict__ A, int64_t n, int* flag) {
+    int bad = 0;
+    for (int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < n; e += int64_t(gridDim.x) * blockDim.x)
+        bad |= !isfinite(A[e]);
+    bad = __syncthreads_or(bad);
+    if (bad && threadIdx.x == 0) *flag = 1;  // benign race: every writer stores 1
+}
+
+template <typename T>
+__global__ void k_transpose_square(const T* __restrict__ src, int lds, T* __restrict__ dst, int ldd, int d) {
+    for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < d * d; e += gridDim.x * blockDim.x) {
+        const int r = e / d, c = e % d;
+        dst[r * ldd + c] = src[c * lds + r];
+    }
+}
+
+size_t qrcp_smem_bytes(int d, size_t eb, bool with_w) {
+    size_t head = ((3 * d * eb + (d + 1) * 4) + 15) / 16 * 16;
+    return head + (with_w ? size_t(d | 1) * d * eb : 0);
+}
+
+int grid_for(int64_t total) { return int(std::min<int64_t>((total + 255) / 256, 148 * 16)); }
+
+}  // namespace
+
+int64_t qrcp_scratch_elems(int d) { return int64_t(d | 1) * d; }
+
+template <typename T>
+cudaError_t qrcp(const T* M, int ldm, int d, T* Q, int ldq, T* Tout, int ldt, int64_t* perm, T* scratch,
+                 int max_smem, cudaStream_t st) {
+    if (d > 32 * kQPer) return cudaErrorInvalidValue;
+    const bool fits = qrcp_smem_bytes(d, sizeof(T), true) <= size_t(max_smem);
+    const size_t sm = qrcp_smem_bytes(d, sizeof(T), fits);
+    cudaFuncSetAttribute(k_qrcp<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
+    k_qrcp<T><<<1, kThreads, sm, st>>>(M, ldm, d, Q, ldq, Tout, ldt, perm, scratch, fits ? 1 : 0);
+    return cudaGetLastError();
+}
+
+template <typename T>
+cudaError_t gather_columns(const T* Q2, int64_t ldq, const int64_t* perm, int64_t n, int d, T* V, int64_t ldv,
+                           cudaStream_t st) {
+    k_gather_columns<T><<<grid_for(n * d), 256, 0, st>>>(Q2, ldq, perm, n, d, V, ldv);
+    return cudaGetLastError();
+}
+
+template <typename T>
+cudaError_t conditioning_flag(const T* R, int ldr, int d, int* flag, cudaStream_t st) {
+    k_conditioning_flag<T><<<1, 1, 0, st>>>(R, ldr, d, flag);
+    return cudaGetLastError();
+}
+
+template <typename T>
+cudaError_t copy_block(const T* src, int64_t lds, T* dst, int64_t ldd, int64_t rows, int cols, cudaStream_t st) {
+    k_copy_block<T><<<grid_for(rows * cols), 256, 0, st>>>(src, lds, dst, ldd, rows, cols);
+    return cudaGetLastError();
+}
+
+template <typename T>
+cudaError_t any_nonfinite(const T* A, int64_t n, int* flag, cudaStream_t st) {
+    cudaError_t e = cudaMemsetAsync(flag, 0, sizeof(int), st);
+    if (e != cudaSuccess) return e;
+    k_any_nonfinite<T><<<grid_for(n), 256, 0, st>>>(A, n, flag);
+    return cudaGetLastError();
+}
+
+template <typename T>
+cudaError_t transpose_square(const T* src, int lds, T* dst, int ldd, int d, cudaStream_t st) {
+    k_transpose_square<T><<<grid_for(int64_t(d) * d), 256, 0, st>>>(src, lds, dst, ldd, d);
+    return cudaGetLastError();
+}
+
+#define CORU_INST(T)                                                                                              \
+    template cudaError_t qrcp<T>(const T*, int, int, T*, int, T*, int, int64_t*, T*, int, cudaStream_t);          \
+    template cudaError_t gather_columns<T>(const T*, int64_t, const int64_t*, int64_t, int, T*, int64_t,          \
+                                           cudaStream_t);                                                         \
+    template cudaError_t conditioning_flag<T>(const T*, int, int, int*, cudaStream_t);                            \
+    template cudaError_t copy_block<T>(const T*, int64_t, T*, int64_t, int64_t, int, cudaStream_t);               \
+    template cudaError_t transpose_square<T>(const T*, int, T*, int, int, cudaStream_t);                        \
+    template cudaError_t any_nonfinite<T>(const T*, int64_t, int*, cudaStream_t);
+CORU_INST(double)
+CORU_INST(float)
+#undef CORU_INST
+
+}  // namespace coru_gpu

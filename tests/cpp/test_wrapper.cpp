@@ -1,0 +1,88 @@
+// C++ caller of the drop-in header (include/coru_gpu.hpp), written the way a reference caller
+// uses coru::corutv (proj/tests/test_corutv.cpp:31-55, 98-108). Exit 0 = all checks passed.
+#include <cmath>
+#include <cstdio>
+#include <stdexcept>
+
+#include "coru_gpu.hpp"
+
+using namespace coru_gpu;
+
+static int failures = 0;
+#define CHECK(c)                                                   \
+    do {                                                           \
+        if (!(c)) {                                                \
+            std::fprintf(stderr, "CHECK failed %s:%d: %s\n", __FILE__, __LINE__, #c); \
+            ++failures;                                            \
+        }                                                          \
+    } while (0)
+
+static double orth_res(const Matrix& q) {
+    double s = 0;
+    for (std::size_t i = 0; i < q.cols(); ++i)
+        for (std::size_t j = 0; j < q.cols(); ++j) {
+            double g = 0;
+            for (std::size_t r = 0; r < q.rows(); ++r) g += q(r, i) * q(r, j);
+            g -= (i == j);
+            s += g * g;
+        }
+    return std::sqrt(s);
+}
+
+static Matrix exact_rank(std::size_t m, std::size_t n, std::size_t r, RngSeed seed) {
+    Matrix g1 = gaussian(m, r, substream(seed, 0)), g2 = gaussian(n, r, substream(seed, 1)), a(m, n);
+    for (std::size_t i = 0; i < m; ++i)
+        for (std::size_t j = 0; j < n; ++j)
+            for (std::size_t k = 0; k < r; ++k) a(i, j) += g1(i, k) * g2(j, k);
+    return a;
+}
+
+static double recon_err(const Matrix& a, const UtvApprox& f) {
+    double e = 0, na = 0;
+    for (std::size_t i = 0; i < a.rows(); ++i)
+        for (std::size_t j = 0; j < a.cols(); ++j) {
+            double s = 0;
+            for (std::size_t p = 0; p < f.ell; ++p)
+                for (std::size_t q = 0; q < f.ell; ++q) s += f.u(i, p) * f.t(p, q) * f.v(j, q);
+            e += (a(i, j) - s) * (a(i, j) - s);
+            na += a(i, j) * a(i, j);
+        }
+    return std::sqrt(e / na);
+}
+
+int main() {
+    // bad parameters -> std::invalid_argument (test_corutv.cpp:31-36)
+    const Matrix g = gaussian(10, 8, {1, 0});
+    for (auto [ell, q] : {std::pair<std::size_t, int>{0, 0}, {8, 0}, {3, -1}}) {
+        bool threw = false;
+        try {
+            corutv(g, ell, q, DVariant::exact, {1, 0});
+        } catch (const std::invalid_argument&) {
+            threw = true;
+        }
+        CHECK(threw);
+    }
+    // exact rank-5 recovery (test_corutv.cpp:38-42)
+    const Matrix a = exact_rank(30, 20, 5, {3, 0});
+    UtvApprox f = corutv(a, 5, 0, DVariant::exact, {4, 0});
+    CHECK(recon_err(a, f) <= 1e-8);
+    CHECK(!f.lower);
+    CHECK(orth_res(f.u) <= 1e-12 * 5 && orth_res(f.v) <= 1e-12 * 5);
+    for (std::size_t i = 0; i < 5; ++i)
+        for (std::size_t j = 0; j < i; ++j) CHECK(f.t(i, j) == 0.0);
+    const auto est = singular_estimates(f);
+    for (std::size_t j = 0; j + 1 < est.size(); ++j) CHECK(est[j] >= est[j + 1]);
+    // wide input -> ULV (test_corutv.cpp:98-108)
+    const Matrix w = exact_rank(20, 35, 4, {11, 0});
+    UtvApprox fw = corutv(w, 8, 1, DVariant::exact, {12, 0});
+    CHECK(fw.lower);
+    CHECK(fw.u.rows() == 20 && fw.v.rows() == 35);
+    for (std::size_t i = 0; i < 8; ++i)
+        for (std::size_t j = i + 1; j < 8; ++j) CHECK(fw.t(i, j) == 0.0);
+    CHECK(recon_err(w, fw) <= 1e-8);
+    // sketch stage (test_corutv.cpp:57-65 uses it directly)
+    SketchBases sb = sketch_bases(a, 5, 1, {4, 0});
+    CHECK(orth_res(sb.q1) <= 1e-12 * 5 && orth_res(sb.q2) <= 1e-12 * 5);
+    std::printf("%s: %d failures\n", failures ? "FAIL" : "OK", failures);
+    return failures ? 1 : 0;
+}

@@ -1,0 +1,30 @@
+"""Golden fixtures generated from the compiled reference (see make_golden.py)."""
+import os
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+
+
+def corutv_cases():
+    z = np.load(os.path.join(HERE, "corutv_ref_cases.npz"))
+    out = []
+    for name in z["names"]:
+        name = str(name)
+        ell, q, seed, stream = (int(x) for x in z[f"{name}/params"])
+        lower, warn = (bool(x) for x in z[f"{name}/flags"])
+        a = z[f"A/{str(z[f'{name}/Akey'])}"]
+        out.append(dict(name=name, A=a, ell=ell, q=q, seed=seed, stream=stream, U=z[f"{name}/U"],
+                        T=z[f"{name}/T"], V=z[f"{name}/V"], lower=lower, warning=warn))
+    return out
+
+
+def sketch_case():
+    z = np.load(os.path.join(HERE, "corutv_ref_cases.npz"))
+    a = next(c["A"] for c in corutv_cases() if c["name"] == "fast_decay_60_q1")
+    return dict(A=a, ell=15, q=1, seed=8, stream=0, Q1=z["sketch_60/Q1"], Q2=z["sketch_60/Q2"],
+                C1=z["sketch_60/C1"], C2prev=z["sketch_60/C2prev"], warning=bool(z["sketch_60/flag"][0]))
+
+
+def kat():
+    return dict(np.load(os.path.join(HERE, "kernels_ref_kat.npz")))

@@ -1,0 +1,111 @@
+"""Generate tests/golden/*.npz from the reference itself (oracle/_ref/libcoru_ref.so, compiled from
+/root/reference/proj/include by oracle/Makefile). Run here, where /root/reference exists:
+
+    make -C oracle && python tests/golden/make_golden.py
+
+The cases are the reference's own hot-path tests (proj/tests/test_corutv.cpp, test_matcore.cpp),
+with their matrices built by the reference's generators (testgen.hpp) and seeds. The fixtures pin
+(1) the plain-C oracle restatement bit-for-bit and (2) the GPU path within tolerance, on machines
+where the reference tree is absent.
+"""
+import os
+import sys
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, os.path.dirname(os.path.dirname(HERE)))
+
+from oracle import Reference  # noqa: E402
+
+R = Reference()
+
+
+def exact_rank_matrix(m, n, r, seed, stream=0):
+    # test_corutv.cpp:16-19: matmul(gaussian(m, r, substream(seed, 0)), gaussian(n, r, substream(seed, 1))^T)
+    g1 = R.gaussian(m, r, seed, stream + 0)
+    g2 = R.gaussian(n, r, seed, stream + 1)
+    return R.matmul(g1, np.ascontiguousarray(g2.T))
+
+
+def main():
+    cases = []  # (name, A, ell, q, seed, stream)
+    cases.append(("exact_rank_30x20_r5", exact_rank_matrix(30, 20, 5, 3), 5, 0, 4, 0))      # :38-42
+    fd80 = R.gen_fast_decay(80, 8, 5)
+    cases.append(("fast_decay_80_q0", fd80, 20, 0, 6, 0))                                   # :44-55
+    cases.append(("fast_decay_80_q2", fd80, 20, 2, 6, 0))
+    cases.append(("fast_decay_60_q1", R.gen_fast_decay(60, 6, 7), 15, 1, 8, 0))             # :57-65
+    nl400 = R.gen_noisy_lowrank(400, 20, 0.01, 12345)
+    cases.append(("noisy_lowrank_400_q0_s1000", nl400, 40, 0, 1000, 0))                     # :67-75
+    cases.append(("noisy_lowrank_400_q2", nl400, 40, 2, 2024, 0))                            # :77-85
+    cases.append(("wide_20x35_ulv", exact_rank_matrix(20, 35, 4, 11), 8, 1, 12, 0))         # :98-108
+    cases.append(("fast_decay_50_q1", R.gen_fast_decay(50, 5, 13), 12, 1, 14, 0))           # :110-116
+    d = np.zeros((6, 5)); d[0, 0], d[1, 1], d[2, 2] = 5.0, 3.0, 1.0
+    cases.append(("diag531_6x5", d, 3, 2, 15, 0))                                            # :133-144
+    cases.append(("rank1_12x9", exact_rank_matrix(12, 9, 1, 16), 2, 0, 17, 0))              # :146-148
+    fd120 = R.gen_fast_decay(120, 5, 26)
+    cases.append(("fast_decay_120_q0", fd120, 30, 0, 27, 0))                                 # :198-206
+    cases.append(("fast_decay_120_q6", fd120, 30, 6, 27, 0))
+    nl150 = R.gen_noisy_lowrank(150, 10, 0.01, 23)
+    cases.append(("noisy_lowrank_150_q0", nl150, 20, 0, 200, 0))                             # :208-220
+    cases.append(("noisy_lowrank_150_q2", nl150, 20, 2, 200, 0))
+
+    out = {}
+    names = []
+    mats = {}  # each distinct input stored once
+    for name, a, ell, q, seed, stream in cases:
+        f = R.corutv(a, ell, q, 0, seed, stream)
+        names.append(name)
+        key = next((k for k, v in mats.items() if v.shape == a.shape and np.array_equal(v, a)), None)
+        if key is None:
+            key = f"mat{len(mats)}"
+            mats[key] = a
+            out[f"A/{key}"] = a
+        out[f"{name}/Akey"] = np.array(key)
+        out[f"{name}/params"] = np.array([ell, q, seed, stream], np.int64)
+        out[f"{name}/U"], out[f"{name}/T"], out[f"{name}/V"] = f.u, f.t, f.v
+        out[f"{name}/flags"] = np.array([f.lower, f.conditioning_warning], np.int64)
+    # sketch_bases (test_corutv.cpp:61) on fast_decay_60
+    q1, q2, c1, c2p, w = R.sketch_bases(R.gen_fast_decay(60, 6, 7), 15, 1, 8, 0)
+    out["sketch_60/Q1"], out["sketch_60/Q2"], out["sketch_60/C1"], out["sketch_60/C2prev"] = q1, q2, c1, c2p
+    out["sketch_60/flag"] = np.array([w], np.int64)
+    out["names"] = np.array(names)
+    np.savez_compressed(os.path.join(HERE, "corutv_ref_cases.npz"), **out)
+
+    # RNG / QR / QRCP known answers (test_matcore.cpp:21-117, 207-230)
+    kat = {}
+    kat["xoshiro_42_0"] = R.xoshiro_words(42, 0, 64)
+    kat["xoshiro_0_0"] = R.xoshiro_words(0, 0, 16)  # all-zero SplitMix guard path (rng.hpp:47-48)
+    kat["gaussian_4x4_1_0"] = R.gaussian(4, 4, 1, 0)
+    kat["gaussian_4x4_1_1"] = R.gaussian(4, 4, 1, 1)
+    kat["gaussian_7x9_42_3"] = R.gaussian(7, 9, 42, 3)
+    kat["gaussian_100x100_42_0"] = R.gaussian(100, 100, 42, 0)
+    kat["gaussian_1x5_7_0"] = R.gaussian(1, 5, 7, 0)  # odd count: the spare is dropped
+    g = R.gaussian(50, 20, 31, 0)
+    kat["qr_in"] = g
+    kat["qr_q"], kat["qr_r"] = R.householder_qr(g)
+    q, r = R.householder_qr(np.array([[3.0], [4.0]]))
+    kat["qr34_q"], kat["qr34_r"] = q, r
+    rd = np.zeros((5, 3))
+    for i in range(5):
+        rd[i, 0] = rd[i, 2] = i + 1.0
+    kat["qr_rankdef_in"] = rd
+    kat["qr_rankdef_q"], kat["qr_rankdef_r"] = R.householder_qr(rd)
+    dd = np.diag([1.0, 5.0, 3.0])
+    kat["qrcp_diag_q"], kat["qrcp_diag_r"], kat["qrcp_diag_perm"] = R.qrcp(dd)
+    u9, v6 = R.gaussian(9, 1, 41, 0), R.gaussian(6, 1, 41, 1)
+    r1 = R.matmul(u9, np.ascontiguousarray(v6.T))
+    kat["qrcp_rank1_in"] = r1
+    kat["qrcp_rank1_q"], kat["qrcp_rank1_r"], kat["qrcp_rank1_perm"] = R.qrcp(r1)
+    for trial in range(12):                                        # test_matcore.cpp:102-117
+        m = 8 + (trial * 7) % 30
+        n = 2 + (trial * 5) % (min(m, 15) - 1)
+        a = R.gaussian(m, n, trial, 7)
+        kat[f"qrcp_trial{trial}_in"] = a
+        kat[f"qrcp_trial{trial}_q"], kat[f"qrcp_trial{trial}_r"], kat[f"qrcp_trial{trial}_perm"] = R.qrcp(a)
+    np.savez_compressed(os.path.join(HERE, "kernels_ref_kat.npz"), **kat)
+    print("wrote", len(names), "corutv cases and", len(kat), "kernel KAT arrays")
+
+
+if __name__ == "__main__":
+    main()

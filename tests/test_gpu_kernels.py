@@ -1,0 +1,101 @@
+"""Kernel-level parity of the sm_100a kernels against the CPU oracle (gpu marker).
+
+Tolerances:
+* GEMM (K1/K2): the reference contract for any alternative matmul is 1e-12 relative per entry
+  (matrix.hpp:112-114), stated norm-wise |C - C_ref| <= 1e-12·(|A||X|) because
+  relative-per-entry is ill-posed where the sum cancels.
+* TSQR: Q R = B to 1e-12·||B||, ||Q^T Q - I|| <= 1e-12·d, diag R >= 0, and agreement with the
+  reference Householder Q/R (unique for full-rank input) to 1e-10 relative.
+* QRCP: identical pivots, |diag T| to 1e-12 relative, reconstruction M P = Q T.
+"""
+import numpy as np
+import pytest
+
+from conftest import orth_residual
+
+pytestmark = pytest.mark.gpu
+
+
+def _t(x):
+    import torch
+    return torch.from_numpy(np.ascontiguousarray(x)).cuda()
+
+
+@pytest.mark.parametrize("m,n,d", [(1000, 1000, 25), (4000, 4000, 60), (777, 1234, 17), (3001, 129, 110),
+                                   (64, 64, 8), (5, 3000, 2), (20000, 2000, 110), (2000, 3000, 220)])
+@pytest.mark.parametrize("op", [0, 1])
+def test_gemm_matches_oracle(ctx, oracle, m, n, d, op):
+    import paper_1810_07323_b200 as cg
+    rng = np.random.default_rng(m * 7 + n + d + op)
+    a = rng.standard_normal((m, n))
+    x = rng.standard_normal((m if op else n, d))
+    # leading dimension of X must be even for 16-B cp.async rows: pad to a multiple of 8
+    dp = (d + 7) // 8 * 8
+    xp = np.zeros((x.shape[0], dp)); xp[:, :d] = x
+    c = cg.gemm(_t(a), _t(xp)[:, :d], op=op, ctx=ctx).cpu().numpy()
+    want = oracle.matmul(a, x) if op == 0 else oracle.matmul_tn(a, x)
+    bound = (np.abs(a) @ np.abs(x)) if op == 0 else (np.abs(a).T @ np.abs(x))
+    assert np.all(np.abs(c - want) <= 1e-12 * bound + 1e-300)
+
+
+def test_gemm_odd_lda_and_views(ctx, oracle):
+    """A with odd leading dimension (8-byte cp.async path) and a column view of a wider matrix."""
+    import torch
+    import paper_1810_07323_b200 as cg
+    rng = np.random.default_rng(5)
+    big = rng.standard_normal((301, 157))
+    a = big[:, :149]
+    x = rng.standard_normal((149, 8))
+    ta = _t(big)[:, :149]
+    for op, xx, want in [(0, x, oracle.matmul(a, x))]:
+        c = cg.gemm(ta, _t(xx), op=op, ctx=ctx).cpu().numpy()
+        assert np.all(np.abs(c - want) <= 1e-12 * (np.abs(a) @ np.abs(xx)))
+    y = rng.standard_normal((301, 8))
+    c = cg.gemm(ta, _t(y), op=1, ctx=ctx).cpu().numpy()
+    assert np.all(np.abs(c - oracle.matmul_tn(a, y)) <= 1e-12 * (np.abs(a).T @ np.abs(y)))
+
+
+@pytest.mark.parametrize("m,d", [(4000, 60), (1000, 25), (200000, 110), (2000, 110), (61, 60), (300, 1),
+                                 (5000, 220), (257, 128)])
+def test_tsqr_matches_reference_householder(ctx, oracle, m, d):
+    import paper_1810_07323_b200 as cg
+    rng = np.random.default_rng(m + d)
+    b = rng.standard_normal((m, d))
+    q, r = cg.tsqr(_t(b), ctx=ctx)
+    q, r = q.cpu().numpy(), r.cpu().numpy()
+    assert np.all(np.diag(r) >= 0)
+    assert np.all(np.tril(r, -1) == 0.0)
+    assert np.linalg.norm(q @ r - b) <= 1e-12 * np.linalg.norm(b)
+    assert orth_residual(q) <= 1e-12 * d
+    if m * d <= 4000 * 110:
+        qo, ro = oracle.householder_qr(b)
+        assert np.linalg.norm(q - qo) <= 1e-10 * np.sqrt(d)
+        assert np.linalg.norm(r - ro) <= 1e-10 * np.linalg.norm(ro)
+
+
+def test_qrcp_known_answers(ctx):
+    """test_matcore.cpp:71-80: diag(1,5,3) -> perm[0] = 1 and |R| = (5,3,1)."""
+    import paper_1810_07323_b200 as cg
+    a = np.diag([1.0, 5.0, 3.0])
+    q, r, perm = cg.qrcp(_t(a), ctx=ctx)
+    r = r.cpu().numpy()
+    assert perm[0] == 1
+    assert np.allclose(np.abs(np.diag(r)), [5, 3, 1], rtol=1e-14)
+
+
+@pytest.mark.parametrize("n,seed", [(25, 1), (60, 2), (110, 3), (220, 4), (7, 5), (1, 6), (160, 7)])
+def test_qrcp_matches_oracle(ctx, oracle, n, seed):
+    import paper_1810_07323_b200 as cg
+    rng = np.random.default_rng(seed)
+    # graded columns so pivots are well separated
+    a = rng.standard_normal((n, n)) * np.logspace(0, -3, n)[rng.permutation(n)]
+    q, r, perm = cg.qrcp(_t(a), ctx=ctx)
+    q, r = q.cpu().numpy(), r.cpu().numpy()
+    qo, ro, po = oracle.qrcp(a)
+    assert np.array_equal(perm, po)
+    assert np.all(np.tril(r, -1) == 0.0)
+    assert np.allclose(np.abs(np.diag(r)), np.abs(np.diag(ro)), rtol=1e-12, atol=1e-300)
+    assert np.linalg.norm(q @ r - a[:, perm]) <= 1e-12 * np.linalg.norm(a)
+    assert orth_residual(q) <= 1e-12 * n
+    # sign convention: the last diagonal keeps its sign (no reflector when sigma == 0, qr.hpp:37)
+    assert np.sign(r[-1, -1]) == np.sign(ro[-1, -1])

@@ -1,0 +1,113 @@
+"""The CPU oracle pinned against the reference (CPU; no GPU needed).
+
+The plain-C restatement (oracle/coru_oracle.c) must reproduce the compiled reference bit-for-bit:
+checked against the committed golden fixtures (always) and against oracle/_ref live when it is
+present. This is what entitles the GPU parity tests to use the oracle as the checker.
+"""
+import numpy as np
+import pytest
+
+from golden import corutv_cases, kat, sketch_case
+
+
+def test_rng_words_and_gaussian_bitexact(oracle):
+    k = kat()
+    assert np.array_equal(oracle.xoshiro_words(42, 0, 64), k["xoshiro_42_0"])
+    assert np.array_equal(oracle.xoshiro_words(0, 0, 16), k["xoshiro_0_0"])
+    for key, (r, c, s, st) in {"gaussian_4x4_1_0": (4, 4, 1, 0), "gaussian_4x4_1_1": (4, 4, 1, 1),
+                               "gaussian_7x9_42_3": (7, 9, 42, 3), "gaussian_100x100_42_0": (100, 100, 42, 0),
+                               "gaussian_1x5_7_0": (1, 5, 7, 0)}.items():
+        assert np.array_equal(oracle.gaussian(r, c, s, st), k[key]), key
+
+
+def test_gaussian_properties(oracle):
+    """test_matcore.cpp:207-230: determinism, distinct streams differ, moments."""
+    a = oracle.gaussian(4, 4, 1, 0)
+    assert np.array_equal(a, oracle.gaussian(4, 4, 1, 0))
+    assert np.abs(a - oracle.gaussian(4, 4, 1, 1)).max() > 0
+    g = oracle.gaussian(100, 100, 42, 0)
+    assert abs(g.mean()) <= 0.05 and 0.9 <= g.var(ddof=1) <= 1.1
+
+
+def test_qr_qrcp_bitexact(oracle):
+    k = kat()
+    q, r = oracle.householder_qr(k["qr_in"])
+    assert np.array_equal(q, k["qr_q"]) and np.array_equal(r, k["qr_r"])
+    q, r = oracle.householder_qr(np.array([[3.0], [4.0]]))
+    assert np.array_equal(q, k["qr34_q"]) and np.array_equal(r, k["qr34_r"])
+    assert abs(r[0, 0]) == pytest.approx(5.0) and abs(q[0, 0]) == pytest.approx(0.6)
+    q, r = oracle.householder_qr(k["qr_rankdef_in"])
+    assert np.array_equal(q, k["qr_rankdef_q"]) and np.array_equal(r, k["qr_rankdef_r"])
+    for name in ["qrcp_diag", "qrcp_rank1"] + [f"qrcp_trial{t}" for t in range(12)]:
+        src = np.diag([1.0, 5.0, 3.0]) if name == "qrcp_diag" else k[f"{name}_in"]
+        q, r, p = oracle.qrcp(src)
+        assert np.array_equal(q, k[f"{name}_q"]) and np.array_equal(r, k[f"{name}_r"]), name
+        assert np.array_equal(p, k[f"{name}_perm"]), name
+    assert oracle.qrcp(np.diag([1.0, 5.0, 3.0]))[2][0] == 1  # test_matcore.cpp:71-80
+
+
+def test_householder_rejects_wide(oracle):
+    with pytest.raises(ValueError):
+        oracle.householder_qr(np.zeros((3, 4)))
+
+
+@pytest.mark.parametrize("case", corutv_cases(), ids=lambda c: c["name"])
+def test_corutv_bitexact_vs_golden(oracle, case):
+    f = oracle.corutv(case["A"], case["ell"], case["q"], 0, case["seed"], case["stream"])
+    assert np.array_equal(f.u, case["U"])
+    assert np.array_equal(f.t, case["T"])
+    assert np.array_equal(f.v, case["V"])
+    assert f.lower == case["lower"] and f.conditioning_warning == case["warning"]
+
+
+def test_corutv_threads_do_not_change_bits(oracle):
+    case = corutv_cases()[1]
+    f1 = oracle.corutv(case["A"], case["ell"], case["q"], 0, case["seed"], 0, threads=1)
+    f8 = oracle.corutv(case["A"], case["ell"], case["q"], 0, case["seed"], 0, threads=8)
+    assert np.array_equal(f1.u, f8.u) and np.array_equal(f1.t, f8.t) and np.array_equal(f1.v, f8.v)
+
+
+def test_sketch_bases_bitexact(oracle):
+    c = sketch_case()
+    q1, q2, c1, c2p, w = oracle.sketch_bases(c["A"], c["ell"], c["q"], c["seed"], c["stream"])
+    for got, key in [(q1, "Q1"), (q2, "Q2"), (c1, "C1"), (c2p, "C2prev")]:
+        assert np.array_equal(got, c[key]), key
+    assert w == c["warning"]
+
+
+def test_bad_parameters(oracle):
+    a = oracle.gaussian(10, 8, 1, 0)
+    for ell, q in [(0, 0), (8, 0), (3, -1)]:
+        with pytest.raises(ValueError):
+            oracle.corutv(a, ell, q, seed=1)
+
+
+def test_oracle_matches_live_reference(oracle, reference):
+    """When oracle/_ref is built (this container), compare against the reference directly."""
+    rng = np.random.default_rng(7)
+    for (m, n, d, q) in [(200, 150, 12, 0), (150, 200, 10, 1), (300, 120, 30, 2)]:
+        a = rng.standard_normal((m, n))
+        f = oracle.corutv(a, d, q, 0, 42, 3)
+        g = reference.corutv(a, d, q, 0, 42, 3)
+        assert np.array_equal(f.u, g.u) and np.array_equal(f.t, g.t) and np.array_equal(f.v, g.v)
+        assert f.conditioning_warning == g.conditioning_warning
+
+
+def test_reference_threaded_driver_bitexact(reference):
+    rng = np.random.default_rng(8)
+    a = rng.standard_normal((500, 300))
+    f = reference.corutv(a, 20, 1, 0, 5, 0, threads=1)
+    g = reference.corutv(a, 20, 1, 0, 5, 0, threads=4)
+    assert np.array_equal(f.u, g.u) and np.array_equal(f.t, g.t) and np.array_equal(f.v, g.v)
+
+
+def test_fp32_restatement_tracks_fp64(oracle):
+    """fp32 restatement: |diag T| within the fp32 tolerance (1e-3 absolute), the
+    leading k = 20 (signal) estimates to 1e-5 relative."""
+    from workloads import make_host
+    a = make_host("C1", 300, 300)
+    f64 = oracle.corutv(a, 25, 0, seed=42)
+    f32 = oracle.corutv(a.astype(np.float32), 25, 0, seed=42)
+    d64, d32 = np.abs(np.diag(f64.t)), np.abs(np.diag(f32.t))
+    assert np.max(np.abs(d64 - d32)) <= 1e-3
+    assert np.max(np.abs(d64 - d32)[:20] / d64[:20]) <= 1e-5
