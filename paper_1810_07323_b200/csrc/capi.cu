@@ -243,23 +243,24 @@ int gemm<float>(coru_ctx*, Op, const float*, int64_t, const float*, int64_t, flo
 template <typename T>
 struct TsqrBufs {
     TsqrPlan plan;
-    T *v = nullptr, *beta = nullptr, *rarena = nullptr, *scratch = nullptr;
-    void carve(Carver& cv, int64_t rows, int d, int max_smem) {
-        plan = plan_tsqr(rows, d, sizeof(T), max_smem);
+    T *v = nullptr, *beta = nullptr, *tarena = nullptr, *rarena = nullptr, *scratch = nullptr;
+    int max_smem = 0;
+    void carve(Carver& cv, int64_t rows, int d, int smem) {
+        max_smem = smem;
+        plan = plan_tsqr(rows, d, sizeof(T), smem);
         v = cv.take<T>(plan.v_elems);
         beta = cv.take<T>(plan.beta_elems);
+        tarena = cv.take<T>(plan.t_elems);
         rarena = cv.take<T>(plan.r_elems);
-        int64_t maxrows = 0;
-        for (size_t l = 1; l < plan.levels.size(); ++l) maxrows = std::max<int64_t>(maxrows, plan.levels[l].rows);
-        scratch = cv.take<T>(tsqr_scratch_elems(plan) + 2 * maxrows * d);
+        scratch = cv.take<T>(tsqr_scratch_elems(plan));
     }
     int factor(const T* B, int64_t ldb, T* r_out, cudaStream_t st) {
-        CORU_CUDA(tsqr_factor<T>(plan, B, ldb, v, beta, rarena, r_out, st));
+        CORU_CUDA(tsqr_factor<T>(plan, B, ldb, v, beta, tarena, rarena, r_out, st));
         g_launches += int64_t(plan.levels.size());
         return CORU_OK;
     }
     int form_q(const T* q_top, T* Q, int64_t ldq, cudaStream_t st) {
-        CORU_CUDA(tsqr_form_q<T>(plan, q_top, v, beta, scratch, Q, ldq, st));
+        CORU_CUDA(tsqr_form_q<T>(plan, q_top, v, beta, tarena, scratch, Q, ldq, max_smem, st));
         g_launches += int64_t(plan.levels.size());
         return CORU_OK;
     }

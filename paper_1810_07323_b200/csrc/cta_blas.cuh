@@ -1,0 +1,188 @@
+// CTA-level dense kernels on shared-memory operands, used by the blocked Householder kernels
+// (TSQR panels, compact-WY updates, QRCP's Q accumulation).
+//
+// cta_gemm: C(i,j) <op>= sum_k A(i,k)·B(k,j) for i < M, j < N, k < K, with A/B/C given as
+// accessor functors (so implicit unit-diagonal / zero-padded reflector storage needs no copy).
+// Threads own TM x TN register tiles; when the tiles cannot occupy the CTA the K range is split
+// and the partial tiles are reduced through shared memory in a fixed order (deterministic).
+#pragma once
+#include "common.cuh"
+
+namespace coru_gpu {
+
+template <int TM, int TN, typename T, class FA, class FB, class FC>
+__device__ __forceinline__ void cta_gemm(int M, int N, int K, FA A, FB B, FC C, T* scratch, int scratch_elems) {
+    const int tid = threadIdx.x, nt = blockDim.x;
+    const int tm = (M + TM - 1) / TM, tn = (N + TN - 1) / TN, tiles = tm * tn;
+    if (tiles == 0 || K <= 0) return;
+    // split-K factor: fill the CTA, keep >= 8 k per split, respect the scratch capacity
+    int S = 1;
+    if (tiles * 2 <= nt) {
+        S = min(nt / tiles, max(1, K / 8));
+        const int cap = scratch_elems / max(1, tiles * TM * TN);
+        S = max(1, min(S, cap));
+    }
+    const int work = tiles * S;
+    for (int w = tid; w < work; w += nt) {
+        const int tile = w % tiles, s = w / tiles;
+        const int i0 = (tile / tn) * TM, j0 = (tile % tn) * TN;
+        const int k0 = int((int64_t(K) * s) / S), k1 = int((int64_t(K) * (s + 1)) / S);
+        T acc[TM][TN];
+#pragma unroll
+        for (int a = 0; a < TM; ++a)
+#pragma unroll
+            for (int b = 0; b < TN; ++b) acc[a][b] = T(0);
+        for (int k = k0; k < k1; ++k) {
+            T av[TM], bv[TN];
+#pragma unroll
+            for (int a = 0; a < TM; ++a) av[a] = (i0 + a < M) ? A(i0 + a, k) : T(0);
+#pragma unroll
+            for (int b = 0; b < TN; ++b) bv[b] = (j0 + b < N) ? B(k, j0 + b) : T(0);
+#pragma unroll
+            for (int a = 0; a < TM; ++a)
+#pragma unroll
+                for (int b = 0; b < TN; ++b) acc[a][b] += av[a] * bv[b];
+        }
+        if (S == 1) {
+#pragma unroll
+            for (int a = 0; a < TM; ++a)
+#pragma unroll
+                for (int b = 0; b < TN; ++b)
+                    if (i0 + a < M && j0 + b < N) C(i0 + a, j0 + b, acc[a][b]);
+        } else {
+            T* p = scratch + (int64_t(s) * tiles + tile) * (TM * TN);
+#pragma unroll
+            for (int a = 0; a < TM; ++a)
+#pragma unroll
+                for (int b = 0; b < TN; ++b) p[a * TN + b] = acc[a][b];
+        }
+    }
+    if (S > 1) {
+        __syncthreads();
+        for (int e = tid; e < tiles * TM * TN; e += nt) {
+            const int tile = e / (TM * TN), r = e % (TM * TN);
+            const int i = (tile / tn) * TM + r / TN, j = (tile % tn) * TN + r % TN;
+            T v = scratch[e];
+            for (int s = 1; s < S; ++s) v += scratch[int64_t(s) * tiles * TM * TN + e];
+            if (i < M && j < N) C(i, j, v);
+        }
+    }
+}
+
+// FP64 tensor-core CTA GEMM on shared (or global) operands with explicit element strides:
+//   C(i,j) = alpha * sum_k A(i,k) B(k,j) + (accumulate ? C(i,j) : 0)
+//   A(i,k) = A[i*ars + k*acs], B(k,j) = B[k*brs + j*bcs], C(i,j) = C[i*crs + j*ccs]
+// Warps own 16x8 DMMA tiles (m16n8k8); when the tiles cannot occupy the warps the K range is
+// split and the partial tiles are reduced in a fixed order through `scratch` (deterministic).
+// Must be called by every thread of the CTA; inputs must be visible (synchronised) on entry and
+// outputs are visible to all threads only after the caller's next __syncthreads().
+__device__ __forceinline__ void cta_mm_f64(int M, int N, int K, const double* A, int ars, int acs, const double* B,
+                                           int brs, int bcs, double* C, int crs, int ccs, double alpha,
+                                           bool accumulate, double* scratch, int scratch_elems) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    const int g = lane >> 2, t = lane & 3;
+    const int tm = (M + 15) >> 4, tn = (N + 7) >> 3, tiles = tm * tn;
+    if (tiles == 0 || K <= 0) return;
+    const int ksteps = (K + 7) >> 3;
+    int S = 1;
+    if (tiles < nw) {
+        S = min(nw / tiles, max(1, ksteps / 4));
+        S = max(1, min(S, scratch_elems / (tiles * 128)));
+    }
+    for (int w = warp; w < tiles * S; w += nw) {
+        const int tile = w % tiles, s = w / tiles;
+        const int i0 = (tile / tn) << 4, j0 = (tile % tn) << 3;
+        const int ks0 = (ksteps * s) / S, ks1 = (ksteps * (s + 1)) / S;
+        double acc[4] = {0.0, 0.0, 0.0, 0.0};
+        const int ia = i0 + g, ib = i0 + g + 8, jb = j0 + g;
+        for (int ks = ks0; ks < ks1; ++ks) {
+            const int k0 = (ks << 3) + t, k1 = k0 + 4;
+            double a[4], b[2];
+            a[0] = (ia < M && k0 < K) ? A[ia * ars + k0 * acs] : 0.0;
+            a[1] = (ib < M && k0 < K) ? A[ib * ars + k0 * acs] : 0.0;
+            a[2] = (ia < M && k1 < K) ? A[ia * ars + k1 * acs] : 0.0;
+            a[3] = (ib < M && k1 < K) ? A[ib * ars + k1 * acs] : 0.0;
+            b[0] = (jb < N && k0 < K) ? B[k0 * brs + jb * bcs] : 0.0;
+            b[1] = (jb < N && k1 < K) ? B[k1 * brs + jb * bcs] : 0.0;
+            dmma_16x8x8(acc, a, b);
+        }
+        if (S == 1) {
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                const int i = i0 + g + ((e >> 1) << 3), j = j0 + 2 * t + (e & 1);
+                if (i < M && j < N) {
+                    double* c = C + i * crs + j * ccs;
+                    *c = accumulate ? *c + alpha * acc[e] : alpha * acc[e];
+                }
+            }
+        } else {
+            double* p = scratch + (s * tiles + tile) * 128 + lane * 4;
+#pragma unroll
+            for (int e = 0; e < 4; ++e) p[e] = acc[e];
+        }
+    }
+    if (S > 1) {
+        __syncthreads();
+        for (int e = threadIdx.x; e < tiles * 128; e += blockDim.x) {
+            const int tile = e >> 7, ln = (e >> 2) & 31, el = e & 3;
+            const int i = ((tile / tn) << 4) + (ln >> 2) + ((el >> 1) << 3);
+            const int j = ((tile % tn) << 3) + 2 * (ln & 3) + (el & 1);
+            double v = scratch[e];
+            for (int s = 1; s < S; ++s) v += scratch[s * tiles * 128 + e];
+            if (i < M && j < N) {
+                double* c = C + i * crs + j * ccs;
+                *c = accumulate ? *c + alpha * v : alpha * v;
+            }
+        }
+    }
+}
+
+// Same contract for any T on the CUDA cores (fp32 path; small fp64 shapes).
+template <typename T>
+__device__ __forceinline__ void cta_mm_simt(int M, int N, int K, const T* A, int ars, int acs, const T* B, int brs,
+                                            int bcs, T* C, int crs, int ccs, T alpha, bool accumulate, T* scratch,
+                                            int scratch_elems) {
+    cta_gemm<2, 2, T>(
+        M, N, K, [=] __device__(int i, int k) { return A[i * ars + k * acs]; },
+        [=] __device__(int k, int j) { return B[k * brs + j * bcs]; },
+        [=] __device__(int i, int j, T v) {
+            T* c = C + i * crs + j * ccs;
+            *c = accumulate ? *c + alpha * v : alpha * v;
+        },
+        scratch, scratch_elems);
+}
+
+__device__ __forceinline__ void cta_mm(int M, int N, int K, const double* A, int ars, int acs, const double* B, int brs,
+                                       int bcs, double* C, int crs, int ccs, double alpha, bool accumulate,
+                                       double* scratch, int scratch_elems) {
+    cta_mm_f64(M, N, K, A, ars, acs, B, brs, bcs, C, crs, ccs, alpha, accumulate, scratch, scratch_elems);
+}
+__device__ __forceinline__ void cta_mm(int M, int N, int K, const float* A, int ars, int acs, const float* B, int brs,
+                                       int bcs, float* C, int crs, int ccs, float alpha, bool accumulate,
+                                       float* scratch, int scratch_elems) {
+    cta_mm_simt<float>(M, N, K, A, ars, acs, B, brs, bcs, C, crs, ccs, alpha, accumulate, scratch, scratch_elems);
+}
+
+// Forward compact-WY T factor (LAPACK dlarft convention): H_0 H_1 ... H_{k-1} = I - V T V^T with
+// T upper triangular, T(j,j) = beta_j and T(0:j, j) = -beta_j T(0:j, 0:j) G(0:j, j), where
+// G(a,b) = v_a^T v_b (a < b) is given in shared memory (ldg). One warp; lanes over rows of T.
+template <typename T>
+__device__ __forceinline__ void warp_larft(int k, const T* G, int ldg, const T* beta, T* Tm, int ldt) {
+    const int lane = threadIdx.x & 31;
+    for (int b = 0; b < k; ++b) {
+        const T bb = beta[b];
+        // rows a < b, each lane handles a = lane, lane + 32, ...
+        for (int a = lane; a < b; a += 32) {
+            T s = 0;
+            for (int c = a; c < b; ++c) s += Tm[a * ldt + c] * G[c * ldg + b];
+            Tm[a * ldt + b] = -bb * s;
+        }
+        if (lane == 0) {
+            Tm[b * ldt + b] = bb;
+            for (int a = b + 1; a < k; ++a) Tm[a * ldt + b] = T(0);
+        }
+        __syncwarp();
+    }
+}
+
+}  // namespace coru_gpu

@@ -7,19 +7,32 @@
 // (make_reflector recipe), then warps update their trailing columns and downdate
 // colsq[c] -= w(j,c)^2 with the 1e-6 recompute guard (qr.hpp:133-139). The norm updates use
 // uncontracted __dmul_rn/__dsub_rn so the downdate rounds like the reference.
-// Q_M is accumulated backwards onto I exactly like accumulate_q (qr.hpp:60-72).
+// Q_M = H_0...H_{d-1} (accumulate_q, qr.hpp:60-72) is formed in compact-WY form with CTA GEMMs.
 #include <algorithm>
 
 #include "common.cuh"
+#include "cta_blas.cuh"
 #include "qrcp.cuh"
 
 namespace coru_gpu {
 
 namespace {
 
-constexpr int kThreads = 256;
+constexpr int kThreads = 512;
 constexpr int kWarps = kThreads / 32;
-constexpr int kQPer = 17;  // Q_M column held as 17 values per lane: d <= 544
+constexpr int kQrcpGemmScratch = 4096;
+
+// reflector a at row k (implicit unit diagonal) in the column-major working matrix
+template <typename T>
+__device__ __forceinline__ T qvval(const T* W, int ldw, int a, int k) {
+    return k > a ? W[a * ldw + k] : (k == a ? T(1) : T(0));
+}
+__host__ __device__ inline int64_t qrcp_w_elems(int d) { return int64_t(d | 1) * d; }
+__host__ __device__ inline int qrcp_ldx(int d) {
+    int ld = d;
+    while (ld % 16 != 8) ++ld;
+    return ld;
+}
 
 template <typename T> __device__ __forceinline__ T mul_rn(T a, T b);
 template <> __device__ __forceinline__ double mul_rn<double>(double a, double b) { return __dmul_rn(a, b); }
@@ -156,46 +169,25 @@ __global__ void __launch_bounds__(kThreads) k_qrcp(const T* __restrict__ M, int 
     }
     for (int c = tid; c < d; c += kThreads) perm_out[c] = perm[c];
     __syncthreads();
-    // Q_M: apply reflectors backwards onto I (qr.hpp:60-72); column c of Q owned by one warp.
-    // Reuse the strictly-lower part of W (the reflectors) and a per-warp column in registers.
-    for (int c = warp; c < d; c += kWarps) {
-        T q[kQPer];
-#pragma unroll
-        for (int u = 0; u < kQPer; ++u) {
-            const int i = lane + 32 * u;
-            q[u] = (i == c) ? T(1) : T(0);
-        }
-        for (int j = d - 1; j >= 0; --j) {
-            const T bj = beta[j];
-            if (bj == T(0)) continue;
-            const T* vcol = W + j * ldw;
-            T s = 0;
-#pragma unroll
-            for (int u = 0; u < kQPer; ++u) {
-                const int i = lane + 32 * u;
-                if (i > j && i < d) s += vcol[i] * q[u];
-            }
-            s = warp_sum(s);
-            T qsel = 0;
-#pragma unroll
-            for (int u = 0; u < kQPer; ++u)
-                if (u == (j >> 5)) qsel = q[u];
-            const T qj = __shfl_sync(0xffffffffu, qsel, j & 31);
-            s += qj;
-            s *= bj;
-#pragma unroll
-            for (int u = 0; u < kQPer; ++u) {
-                const int i = lane + 32 * u;
-                if (i > j && i < d) q[u] -= s * vcol[i];
-                if (i == j) q[u] -= s;
-            }
-        }
-#pragma unroll
-        for (int u = 0; u < kQPer; ++u) {
-            const int i = lane + 32 * u;
-            if (i < d) Q[i * ldq + c] = q[u];
-        }
-    }
+    // Q_M = H_0 ... H_{d-1} = I - V T V^T (accumulate_q, qr.hpp:60-72, in compact-WY form):
+    // explicit V, G = V^T V, T by the forward recurrence, Y = T V^T, Q = I - V Y (DMMA CTA GEMMs).
+    const int ldx = qrcp_ldx(d);
+    T* Vx = gscratch + qrcp_w_elems(d);
+    T* G = Vx + int64_t(d) * ldx;
+    T* Tm = G + d * d;
+    T* Y = Tm + d * d;
+    T* gs = Y + d * d;
+    for (int a = warp; a < d; a += kWarps)
+        for (int r = lane; r < ldx; r += 32) Vx[a * ldx + r] = r > a && r < d ? W[a * ldw + r] : T(r == a ? 1 : 0);
+    for (int e = tid; e < d * d; e += kThreads) Q[(e / d) * ldq + e % d] = T(e / d == e % d ? 1 : 0);
+    __syncthreads();
+    cta_mm(d, d, d, Vx, ldx, 1, Vx, 1, ldx, G, d, 1, T(1), false, gs, kQrcpGemmScratch);
+    __syncthreads();
+    if (warp == 0) warp_larft<T>(d, G, d, beta, Tm, d);
+    __syncthreads();
+    cta_mm(d, d, d, Tm, d, 1, Vx, ldx, 1, Y, d, 1, T(1), false, gs, kQrcpGemmScratch);
+    __syncthreads();
+    cta_mm(d, d, d, Vx, 1, ldx, Y, d, 1, Q, ldq, 1, T(-1), true, gs, kQrcpGemmScratch);
 }
 
 template <typename T>
@@ -253,12 +245,13 @@ int grid_for(int64_t total) { return int(std::min<int64_t>((total + 255) / 256, 
 
 }  // namespace
 
-int64_t qrcp_scratch_elems(int d) { return int64_t(d | 1) * d; }
+int64_t qrcp_scratch_elems(int d) {
+    return qrcp_w_elems(d) + int64_t(qrcp_ldx(d)) * d + 3 * int64_t(d) * d + kQrcpGemmScratch;
+}
 
 template <typename T>
 cudaError_t qrcp(const T* M, int ldm, int d, T* Q, int ldq, T* Tout, int ldt, int64_t* perm, T* scratch,
                  int max_smem, cudaStream_t st) {
-    if (d > 32 * kQPer) return cudaErrorInvalidValue;
     const bool fits = qrcp_smem_bytes(d, sizeof(T), true) <= size_t(max_smem);
     const size_t sm = qrcp_smem_bytes(d, sizeof(T), fits);
     cudaFuncSetAttribute(k_qrcp<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));

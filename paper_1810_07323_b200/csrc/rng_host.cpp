@@ -74,13 +74,22 @@ void gaussian_host(int64_t rows, int64_t cols, uint64_t seed, uint64_t stream, O
     std::vector<uint64_t> words(size_t(2 * pairs));
     Xoshiro x(seed, stream);
     for (auto& w : words) w = x.next();
-    auto put = [&](int64_t e, double v) { out[(e / cols) * ldo + e % cols] = static_cast<OutT>(v); };
+    // Pair p fills row-major elements 2p and 2p+1; (row, col) advance incrementally (no division
+    // in the loop — an int64 divide per element cost more than the transcendental functions).
     auto work = [&](int64_t p0, int64_t p1) {
+        int64_t e = 2 * p0, r = e / cols, c = e % cols;
+        auto put = [&](double v) {
+            out[r * ldo + c] = static_cast<OutT>(v);
+            if (++c == cols) {
+                c = 0;
+                ++r;
+            }
+        };
         for (int64_t p = p0; p < p1; ++p) {
-            double c, s;
-            box_muller(words[size_t(2 * p)], words[size_t(2 * p + 1)], c, s);
-            put(2 * p, c);
-            if (2 * p + 1 < total) put(2 * p + 1, s);
+            double cv, sv;
+            box_muller(words[size_t(2 * p)], words[size_t(2 * p + 1)], cv, sv);
+            put(cv);
+            if (2 * p + 1 < total) put(sv);
         }
     };
     if (threads <= 1 || pairs < 4096) {

@@ -16,10 +16,15 @@
 //
 // Q kernel: applies the stored reflectors backwards (accumulate_q order, qr.hpp:60-72) onto
 // [Q_above block; 0]; columns are independent, so warps never synchronise.
+//
+// Two implementations share the tree: the blocked one below (shared-memory block, panels +
+// compact WY) whenever a block of > 1.25 d rows fits shared memory, and the "wide" one (the
+// unblocked column pipeline, working block in L2) for sketch widths too wide for that.
 #include <algorithm>
 #include <cmath>
 
 #include "common.cuh"
+#include "cta_blas.cuh"
 #include "tsqr.cuh"
 
 namespace coru_gpu {
@@ -208,9 +213,268 @@ __global__ void __launch_bounds__(kThreads) k_hh_form_q(const T* __restrict__ Qi
     }
 }
 
-size_t factor_smem_bytes(int rbmax, int d, size_t eb) {
+
+// ============================================================================================
+// Blocked path (the block fits shared memory). Panels of kNB columns are factored with the column
+// pipeline held in registers (one warp per panel column, a column = kRPL values per lane), the
+// "reflector j ready" hand-off going through named hardware barriers (bar.arrive by the builder,
+// bar.sync by the later panel warps: no spinning). The panel's explicit reflectors V_p and its
+// compact-WY factor T_p (H_p0...H_p0+nb-1 = I - V_p T_p V_p^T, dlarft convention) then update the
+// trailing columns with three DMMA GEMMs, C <- C - V_p T_p^T (V_p^T C). The per-panel T_p are kept,
+// so Q is formed panel by panel (in reverse) with the same GEMM shape.
+// ============================================================================================
+constexpr int kBThreads = 512;
+constexpr int kNB = 16;       // panel width == warps that own a panel column
+constexpr int kRPL = 8;       // rows per lane held in registers: blocks of <= 256 rows
+constexpr int kMaxRowsBlocked = 32 * kRPL;
+constexpr int kGemmScratch = 2048;
+constexpr int kQChunk = 32;   // Q columns formed per pass
+
+__host__ __device__ inline int ld_mod(int rows, int residue) {
+    // smallest ld >= rows with ld % 16 == residue (bank-friendly fragment strides for 8-byte data)
+    int ld = rows;
+    while (ld % 16 != residue) ++ld;
+    return ld;
+}
+__host__ __device__ inline int npanels(int d) { return (d + kNB - 1) / kNB; }
+
+__device__ __forceinline__ void named_bar_sync(int id, int count) {
+    asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(count) : "memory");
+}
+__device__ __forceinline__ void named_bar_arrive(int id, int count) {
+    asm volatile("bar.arrive %0, %1;\n" ::"r"(id), "r"(count) : "memory");
+}
+
+template <typename T>
+struct BlockedSmem {
+    int d, ldw, ldvp;
+    T *W, *Vp, *beta, *Gp, *Tp, *Y, *Z, *scratch;
+    __device__ BlockedSmem(unsigned char* raw, int d_, int rb) : d(d_), ldw(ld_mod(rb, 4)), ldvp(ld_mod(rb, 8)) {
+        T* p = reinterpret_cast<T*>(raw);
+        W = p;
+        p += size_t(d) * ldw;
+        Vp = p;
+        p += size_t(kNB) * ldvp;
+        beta = p;
+        p += d + (d & 1);
+        Gp = p;
+        p += kNB * kNB;
+        Tp = p;
+        p += kNB * kNB;
+        Y = p;
+        p += size_t(kNB) * d;
+        Z = p;
+        p += size_t(kNB) * d;
+        scratch = p;
+    }
+    static size_t bytes(int d, int rb, size_t eb) {
+        return (size_t(d) * ld_mod(rb, 4) + size_t(kNB) * ld_mod(rb, 8) + d + (d & 1) + 2 * kNB * kNB +
+                2 * size_t(kNB) * d + kGemmScratch) *
+               eb;
+    }
+};
+
+template <typename T>
+__global__ void __launch_bounds__(kBThreads, 1)
+    k_qr_blocked(const T* __restrict__ X, int64_t ldx, int64_t rows, int nb, int d, T* __restrict__ V, int ldv,
+                 T* __restrict__ betas, T* __restrict__ Tg, T* __restrict__ Rout, int ldr) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int b = blockIdx.x;
+    const int64_t r0 = rows * b / nb, r1 = rows * (b + 1) / nb;
+    const int rb = int(r1 - r0);
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    BlockedSmem<T> S(smem_raw, d, rb);
+    T* W = S.W;
+    const int ldw = S.ldw, ldvp = S.ldvp;
+    T* Tb = Tg + int64_t(b) * npanels(d) * kNB * kNB;  // this block's panel T factors
+
+    // Load rows [r0, r1) (row-major, coalesced along columns) into column-major W.
+    for (int r = warp; r < rb; r += kBThreads / 32) {
+        const T* src = X + (r0 + r) * ldx;
+        for (int c = lane; c < d; c += 32) W[c * ldw + r] = src[c];
+    }
+    __syncthreads();
+
+    for (int p0 = 0, pi = 0; p0 < d; p0 += kNB, ++pi) {
+        const int nbp = min(kNB, d - p0);
+        // ---- panel factorisation: warp w owns column p0 + w; rows >= p0 in registers ----
+        if (warp < nbp) {
+            const int c = p0 + warp;
+            T x[kRPL];
+#pragma unroll
+            for (int u = 0; u < kRPL; ++u) {
+                const int r = lane + 32 * u;
+                x[u] = (r >= p0 && r < rb) ? W[c * ldw + r] : T(0);
+            }
+            for (int jj = 0; jj <= warp; ++jj) {
+                const int j = p0 + jj;
+                const int bar = 1 + jj, cnt = 32 * (nbp - jj);
+                if (jj < warp) {
+                    // apply H_j (built by warp jj) to my column   (apply_reflector, qr.hpp:49-57)
+                    named_bar_sync(bar, cnt);
+                    const T bj = S.beta[j];
+                    if (bj == T(0)) continue;
+                    const T* vj = S.Vp + jj * ldvp;
+                    T v[kRPL];
+                    T s = 0;
+#pragma unroll
+                    for (int u = 0; u < kRPL; ++u) {
+                        const int r = lane + 32 * u;
+                        v[u] = r < rb ? vj[r] : T(0);
+                        s += v[u] * x[u];
+                    }
+                    s = warp_sum(s) * bj;
+#pragma unroll
+                    for (int u = 0; u < kRPL; ++u) x[u] -= s * v[u];
+                } else {
+                    // build reflector j from my column   (make_reflector, qr.hpp:32-45)
+                    T sig = 0, x0 = 0;
+#pragma unroll
+                    for (int u = 0; u < kRPL; ++u) {
+                        const int r = lane + 32 * u;
+                        if (r > j) sig += x[u] * x[u];
+                        if (u == (j >> 5)) x0 = x[u];
+                    }
+                    sig = warp_sum(sig);
+                    x0 = __shfl_sync(0xffffffffu, x0, j & 31);
+                    T bj = 0, v0 = 1;
+                    if (sig != T(0)) {
+                        const T mu = tsqrt(x0 * x0 + sig);
+                        v0 = (x0 <= T(0)) ? x0 - mu : -sig / (x0 + mu);
+                        bj = T(2) * v0 * v0 / (sig + v0 * v0);
+#pragma unroll
+                        for (int u = 0; u < kRPL; ++u) {
+                            const int r = lane + 32 * u;
+                            if (r > j) x[u] /= v0;
+                            if (r == j) x[u] = mu;
+                        }
+                    }
+                    T* vj = S.Vp + jj * ldvp;
+#pragma unroll
+                    for (int u = 0; u < kRPL; ++u) {
+                        const int r = lane + 32 * u;
+                        if (r >= p0 && r < rb) W[c * ldw + r] = x[u];
+                        // explicit reflector: 0 above j, 1 at j, v below (0 past rb and in the padding)
+                        if (r < ldvp) vj[r] = (r > j && r < rb) ? x[u] : (r == j ? T(1) : T(0));
+                    }
+                    if (lane == 0) S.beta[j] = bj;
+                    if (jj + 1 < nbp) named_bar_arrive(bar, cnt);
+                }
+            }
+        }
+        __syncthreads();
+        const int K = rb - p0;
+        // ---- panel T factor: G = V_p^T V_p, T_p by the forward recurrence ----
+        cta_mm(nbp, nbp, K, S.Vp + p0, ldvp, 1, S.Vp + p0, 1, ldvp, S.Gp, kNB, 1, T(1), false, S.scratch, kGemmScratch);
+        __syncthreads();
+        if (warp == 0) {
+            warp_larft<T>(nbp, S.Gp, kNB, S.beta + p0, S.Tp, kNB);
+            T* Tpg = Tb + pi * kNB * kNB;
+            for (int e = lane; e < kNB * kNB; e += 32) Tpg[e] = S.Tp[e];
+        }
+        __syncthreads();
+        // ---- trailing update of columns [p0+nbp, d): C <- C - V_p T_p^T (V_p^T C), rows >= p0 ----
+        const int c0 = p0 + nbp, nc = d - c0;
+        if (nc > 0) {
+            T* C = W + c0 * ldw + p0;
+            cta_mm(nbp, nc, K, S.Vp + p0, ldvp, 1, C, 1, ldw, S.Y, d, 1, T(1), false, S.scratch, kGemmScratch);
+            __syncthreads();
+            cta_mm(nbp, nc, nbp, S.Tp, 1, kNB, S.Y, d, 1, S.Z, d, 1, T(1), false, S.scratch, kGemmScratch);
+            __syncthreads();
+            cta_mm(K, nc, nbp, S.Vp + p0, 1, ldvp, S.Z, d, 1, C, 1, ldw, T(-1), true, S.scratch, kGemmScratch);
+            __syncthreads();
+        }
+    }
+
+    // R (upper, exact zeros below) -> Rout rows [b*d, (b+1)*d); reflectors and betas to global.
+    for (int e = tid; e < d * d; e += kBThreads) {
+        const int r = e / d, c = e % d;
+        Rout[(int64_t(b) * d + r) * ldr + c] = (r <= c) ? W[c * ldw + r] : T(0);
+    }
+    for (int c = tid; c < d; c += kBThreads) betas[int64_t(b) * d + c] = S.beta[c];
+    T* Vb = V + int64_t(b) * d * ldv;
+    for (int c = warp; c < d; c += kBThreads / 32)
+        for (int r = lane; r < rb; r += 32) Vb[int64_t(c) * ldv + r] = W[c * ldw + r];
+}
+
+template <typename T>
+struct FormQSmem {
+    int ldvs, lde;
+    T *Vs, *E, *Y, *Z, *Tp, *scratch;
+    __device__ FormQSmem(unsigned char* raw, int d, int rb) : ldvs(ld_mod(rb, 8)), lde(ld_mod(rb, 4)) {
+        T* p = reinterpret_cast<T*>(raw);
+        Vs = p;
+        p += size_t(d) * ldvs;
+        E = p;
+        p += size_t(kQChunk) * lde;
+        Y = p;
+        p += kNB * kQChunk;
+        Z = p;
+        p += kNB * kQChunk;
+        Tp = p;
+        p += kNB * kNB;
+        scratch = p;
+    }
+    static size_t bytes(int d, int rb, size_t eb) {
+        return (size_t(d) * ld_mod(rb, 8) + size_t(kQChunk) * ld_mod(rb, 4) + 2 * kNB * kQChunk + kNB * kNB +
+                kGemmScratch) *
+               eb;
+    }
+};
+
+// Q block b = H_0 ... H_{d-1} [Qin_b; 0]  (Qin null => identity), by panels in reverse:
+//   E <- E - V_p (T_p (V_p^T E)),  p = P-1 ... 0, on column chunks of E.
+template <typename T>
+__global__ void __launch_bounds__(kBThreads, 1)
+    k_qr_blocked_form_q(const T* __restrict__ Qin, int ldqin, int64_t rows, int nb, int d, const T* __restrict__ V,
+                        int ldv, const T* __restrict__ Tg, T* __restrict__ Qout, int64_t ldqout) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int b = blockIdx.x;
+    const int64_t r0 = rows * b / nb, r1 = rows * (b + 1) / nb;
+    const int rb = int(r1 - r0);
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    FormQSmem<T> S(smem_raw, d, rb);
+    const T* Vb = V + int64_t(b) * d * ldv;
+    const T* Tb = Tg + int64_t(b) * npanels(d) * kNB * kNB;
+    const T* Qb = Qin ? Qin + int64_t(b) * d * ldqin : nullptr;
+    // explicit reflectors (0 above the diagonal, 1 on it) staged column-major
+    for (int c = warp; c < d; c += kBThreads / 32)
+        for (int r = lane; r < S.ldvs; r += 32)
+            S.Vs[c * S.ldvs + r] = (r > c && r < rb) ? Vb[int64_t(c) * ldv + r] : T(r == c ? 1 : 0);
+    for (int q0 = 0; q0 < d; q0 += kQChunk) {
+        const int nq = min(kQChunk, d - q0);
+        for (int e = tid; e < nq * rb; e += kBThreads) {
+            const int j = e / rb, i = e % rb;
+            S.E[j * S.lde + i] = i < d ? (Qb ? Qb[i * ldqin + q0 + j] : T(i == q0 + j ? 1 : 0)) : T(0);
+        }
+        __syncthreads();
+        for (int pi = npanels(d) - 1; pi >= 0; --pi) {
+            const int p0 = pi * kNB, nbp = min(kNB, d - p0), K = rb - p0;
+            const T* Vp = S.Vs + p0 * S.ldvs + p0;  // V_p rows >= p0
+            if (tid < kNB * kNB) S.Tp[tid] = Tb[pi * kNB * kNB + tid];
+            cta_mm(nbp, nq, K, Vp, S.ldvs, 1, S.E + p0, 1, S.lde, S.Y, kQChunk, 1, T(1), false, S.scratch,
+                   kGemmScratch);
+            __syncthreads();
+            cta_mm(nbp, nq, nbp, S.Tp, kNB, 1, S.Y, kQChunk, 1, S.Z, kQChunk, 1, T(1), false, S.scratch,
+                   kGemmScratch);
+            __syncthreads();
+            cta_mm(K, nq, nbp, Vp, 1, S.ldvs, S.Z, kQChunk, 1, S.E + p0, 1, S.lde, T(-1), true, S.scratch,
+                   kGemmScratch);
+            __syncthreads();
+        }
+        T* Qo = Qout + r0 * ldqout + q0;
+        for (int e = tid; e < nq * rb; e += kBThreads) {
+            const int i = e / nq, j = e % nq;
+            Qo[int64_t(i) * ldqout + j] = S.E[j * S.lde + i];
+        }
+        __syncthreads();
+    }
+}
+
+size_t wide_factor_smem_bytes(int rbmax, int d, size_t eb) {
     return ((d * 4 + 15) / 16) * 16 + ((d + 1) / 2) * 2 * eb + size_t(rbmax | 1) * d * eb;
 }
+
 
 }  // namespace
 
@@ -219,61 +483,87 @@ TsqrPlan plan_tsqr(int64_t m, int d, size_t eb, int max_smem) {
     p.m = m;
     p.d = d;
     p.elem_bytes = eb;
-    // Largest block that fits shared memory; prefer ~4d..512 rows per block.
-    int rb_smem = 0;
-    for (int rb = 2048; rb > d; rb -= 1)
-        if (factor_smem_bytes(rb, d, eb) <= size_t(max_smem)) { rb_smem = rb; break; }
-    const bool smem = rb_smem >= 2 * d + 2;
-    int target = smem ? std::min(rb_smem, std::max(4 * d, 256)) : std::max(4 * d, 256);
+    // Largest block the blocked kernels take (<= 256 rows, both kernels' working sets in smem).
+    int rb_blocked = 0;
+    for (int rb = kMaxRowsBlocked; rb > d; --rb)
+        if (BlockedSmem<double>::bytes(d, rb, eb) <= size_t(max_smem) &&
+            FormQSmem<double>::bytes(d, rb, eb) <= size_t(max_smem)) {
+            rb_blocked = rb;
+            break;
+        }
+    // Largest block the unblocked kernels hold in smem (else they work in L2).
+    int rb_wide = 0;
+    for (int rb = 2048; rb > d; --rb)
+        if (wide_factor_smem_bytes(rb, d, eb) <= size_t(max_smem)) {
+            rb_wide = rb;
+            break;
+        }
+    const bool blocked_ok = rb_blocked >= d + 1 + d / 4;  // at least a 1.25x reduction per level
+    const int target = blocked_ok ? rb_blocked : (rb_wide >= 2 * d + 2 ? std::min(rb_wide, std::max(4 * d, 256))
+                                                                           : std::max(4 * d, 256));
     int64_t rows = m;
-    int64_t voff = 0, boff = 0, roff = 0;
+    int64_t voff = 0, boff = 0, roff = 0, toff = 0;
     for (;;) {
         TsqrLevel L;
         L.rows = rows;
-        L.smem = smem;
-        int64_t nb = (rows + target - 1) / target;
-        nb = std::min<int64_t>(nb, rows / (d + 1));  // every block strictly taller than d
-        if (nb < 1) nb = 1;
+        // every block strictly taller than d (so the tree always shrinks), at most `target` rows
+        int64_t nb = std::max<int64_t>(1, (rows + target - 1) / target);
+        nb = std::max<int64_t>(1, std::min<int64_t>(nb, rows / (d + 1)));
         L.nb = int(nb);
         L.rbmax = int((rows + nb - 1) / nb);
-        if (L.smem && factor_smem_bytes(L.rbmax, d, eb) > size_t(max_smem)) L.smem = false;
+        L.blocked = blocked_ok && L.rbmax <= rb_blocked;
+        L.smem = L.blocked || wide_factor_smem_bytes(L.rbmax, d, eb) <= size_t(max_smem);
         L.ldv = L.rbmax + (L.rbmax % 2);
         L.v_off = voff;
         L.beta_off = boff;
         L.r_off = roff;
+        L.t_off = toff;
         voff += int64_t(L.nb) * d * L.ldv;
         boff += int64_t(L.nb) * d;
         roff += int64_t(L.nb) * d * d;
+        if (L.blocked) toff += int64_t(L.nb) * npanels(d) * kNB * kNB;
         p.levels.push_back(L);
         if (L.nb == 1) break;
-        rows = int64_t(L.nb) * d;
+        rows = int64_t(L.nb) * d;  // < previous rows: each block has > d rows
     }
+    p.blocked = !p.levels.empty() && p.levels[0].blocked;
     p.v_elems = voff;
     p.beta_elems = boff;
     p.r_elems = roff;
+    p.t_elems = toff;
     return p;
 }
 
 int64_t tsqr_scratch_elems(const TsqrPlan& p) {
-    int64_t s = 0;
-    for (auto& L : p.levels)
-        if (!L.smem) s = std::max<int64_t>(s, int64_t(L.nb) * p.d * L.ldv);
-    return s;
+    int64_t work = 0, maxrows = 0;
+    for (size_t l = 0; l < p.levels.size(); ++l) {
+        const TsqrLevel& L = p.levels[l];
+        if (!L.blocked && !L.smem) work = std::max<int64_t>(work, int64_t(L.nb) * p.d * L.ldv);
+        if (l >= 1) maxrows = std::max<int64_t>(maxrows, L.rows);
+    }
+    return work + 2 * maxrows * p.d;
 }
 
 template <typename T>
-cudaError_t tsqr_factor(const TsqrPlan& p, const T* B, int64_t ldb, T* V, T* beta, T* R, T* r_out,
+cudaError_t tsqr_factor(const TsqrPlan& p, const T* B, int64_t ldb, T* V, T* beta, T* Tarena, T* R, T* r_out,
                         cudaStream_t st) {
     const int d = p.d;
     const T* X = B;
     int64_t ldx = ldb;
     for (size_t l = 0; l < p.levels.size(); ++l) {
         const TsqrLevel& L = p.levels[l];
-        const size_t sm = L.smem ? factor_smem_bytes(L.rbmax, d, sizeof(T)) : factor_smem_bytes(0, d, sizeof(T));
-        cudaFuncSetAttribute(k_hh_factor<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
         T* Rl = (l + 1 == p.levels.size()) ? r_out : R + L.r_off;
-        k_hh_factor<T><<<L.nb, kThreads, sm, st>>>(X, ldx, L.rows, L.nb, d, V + L.v_off, L.ldv,
-                                                    beta + L.beta_off, Rl, d, L.smem ? 1 : 0);
+        if (L.blocked) {
+            const size_t sm = BlockedSmem<T>::bytes(d, L.rbmax, sizeof(T));
+            cudaFuncSetAttribute(k_qr_blocked<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
+            k_qr_blocked<T><<<L.nb, kBThreads, sm, st>>>(X, ldx, L.rows, L.nb, d, V + L.v_off, L.ldv,
+                                                          beta + L.beta_off, Tarena + L.t_off, Rl, d);
+        } else {
+            const size_t sm = L.smem ? wide_factor_smem_bytes(L.rbmax, d, sizeof(T)) : wide_factor_smem_bytes(0, d, sizeof(T));
+            cudaFuncSetAttribute(k_hh_factor<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
+            k_hh_factor<T><<<L.nb, kThreads, sm, st>>>(X, ldx, L.rows, L.nb, d, V + L.v_off, L.ldv,
+                                                        beta + L.beta_off, Rl, d, L.smem ? 1 : 0);
+        }
         cudaError_t e = cudaGetLastError();
         if (e != cudaSuccess) return e;
         X = Rl;
@@ -283,15 +573,16 @@ cudaError_t tsqr_factor(const TsqrPlan& p, const T* B, int64_t ldb, T* V, T* bet
 }
 
 template <typename T>
-cudaError_t tsqr_form_q(const TsqrPlan& p, const T* q_top, T* V, T* beta, T* scratch, T* Q, int64_t ldq,
-                        cudaStream_t st) {
+cudaError_t tsqr_form_q(const TsqrPlan& p, const T* q_top, T* V, T* beta, T* Tarena, T* scratch, T* Q, int64_t ldq,
+                        int max_smem, cudaStream_t st) {
     const int d = p.d;
-    // Level l's output Q (rows_l x d) is the Qin of level l-1. Intermediate Qs go to scratch
-    // space carved from the R arena region sizes: reuse a ping-pong pair in `scratch` tail.
-    // Layout: scratch holds [global-L2 working blocks | ping | pong].
-    const int64_t work = tsqr_scratch_elems(p);
-    int64_t maxrows = 0;
-    for (size_t l = 1; l < p.levels.size(); ++l) maxrows = std::max<int64_t>(maxrows, p.levels[l].rows);
+    // scratch = [wide-path working blocks | ping | pong]
+    int64_t work = 0, maxrows = 0;
+    for (size_t l = 0; l < p.levels.size(); ++l) {
+        const TsqrLevel& L = p.levels[l];
+        if (!L.blocked && !L.smem) work = std::max<int64_t>(work, int64_t(L.nb) * d * L.ldv);
+        if (l >= 1) maxrows = std::max<int64_t>(maxrows, L.rows);
+    }
     T* ping = scratch + work;
     T* pong = ping + maxrows * d;
     const T* qin = q_top;
@@ -300,10 +591,17 @@ cudaError_t tsqr_form_q(const TsqrPlan& p, const T* q_top, T* V, T* beta, T* scr
         const TsqrLevel& L = p.levels[size_t(l)];
         T* out = (l == 0) ? Q : ((p.levels.size() - 1 - size_t(l)) % 2 == 0 ? ping : pong);
         const int64_t ldo = (l == 0) ? ldq : d;
-        const size_t sm = L.smem ? size_t(L.rbmax | 1) * d * sizeof(T) : 0;
-        cudaFuncSetAttribute(k_hh_form_q<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
-        k_hh_form_q<T><<<L.nb, kThreads, sm, st>>>(qin, ldqin, L.rows, L.nb, d, V + L.v_off, L.ldv,
-                                                    beta + L.beta_off, out, ldo, scratch, L.smem ? 1 : 0);
+        if (L.blocked) {
+            const size_t sm = FormQSmem<T>::bytes(d, L.rbmax, sizeof(T));
+            cudaFuncSetAttribute(k_qr_blocked_form_q<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
+            k_qr_blocked_form_q<T><<<L.nb, kBThreads, sm, st>>>(qin, ldqin, L.rows, L.nb, d, V + L.v_off, L.ldv,
+                                                                 Tarena + L.t_off, out, ldo);
+        } else {
+            const size_t sm = L.smem ? size_t(L.rbmax | 1) * d * sizeof(T) : 0;
+            cudaFuncSetAttribute(k_hh_form_q<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
+            k_hh_form_q<T><<<L.nb, kThreads, sm, st>>>(qin, ldqin, L.rows, L.nb, d, V + L.v_off, L.ldv,
+                                                        beta + L.beta_off, out, ldo, scratch, L.smem ? 1 : 0);
+        }
         cudaError_t e = cudaGetLastError();
         if (e != cudaSuccess) return e;
         qin = out;
@@ -312,14 +610,13 @@ cudaError_t tsqr_form_q(const TsqrPlan& p, const T* q_top, T* V, T* beta, T* scr
     return cudaSuccess;
 }
 
-// scratch must hold tsqr_scratch_elems(p) + 2 * max_{l>=1} rows_l * d elements.
-template cudaError_t tsqr_factor<double>(const TsqrPlan&, const double*, int64_t, double*, double*, double*,
+template cudaError_t tsqr_factor<double>(const TsqrPlan&, const double*, int64_t, double*, double*, double*, double*,
                                          double*, cudaStream_t);
-template cudaError_t tsqr_factor<float>(const TsqrPlan&, const float*, int64_t, float*, float*, float*, float*,
+template cudaError_t tsqr_factor<float>(const TsqrPlan&, const float*, int64_t, float*, float*, float*, float*, float*,
                                         cudaStream_t);
-template cudaError_t tsqr_form_q<double>(const TsqrPlan&, const double*, double*, double*, double*, double*,
-                                         int64_t, cudaStream_t);
-template cudaError_t tsqr_form_q<float>(const TsqrPlan&, const float*, float*, float*, float*, float*, int64_t,
-                                        cudaStream_t);
+template cudaError_t tsqr_form_q<double>(const TsqrPlan&, const double*, double*, double*, double*, double*, double*,
+                                         int64_t, int, cudaStream_t);
+template cudaError_t tsqr_form_q<float>(const TsqrPlan&, const float*, float*, float*, float*, float*, float*, int64_t,
+                                        int, cudaStream_t);
 
 }  // namespace coru_gpu

@@ -16,6 +16,8 @@ struct TsqrLevel {
     int64_t v_off = 0;     // offset (elements) of this level's reflector store in the V arena
     int64_t beta_off = 0;  // offset of the betas
     int64_t r_off = 0;     // offset of the stacked R (nb*d x d, ld = d) output in the R arena
+    int64_t t_off = 0;     // offset of the per-block compact-WY T factors (blocked path)
+    bool blocked = false;  // panel-blocked compact-WY kernels (else the unblocked column pipeline)
     bool smem = true;      // working block lives in shared memory (else in the V arena, L2)
 };
 
@@ -23,7 +25,8 @@ struct TsqrPlan {
     int64_t m = 0;
     int d = 0;
     std::vector<TsqrLevel> levels;
-    int64_t v_elems = 0, beta_elems = 0, r_elems = 0;
+    bool blocked = false;  // level 0 uses the blocked kernels
+    int64_t v_elems = 0, beta_elems = 0, r_elems = 0, t_elems = 0;
     size_t elem_bytes = 8;
 };
 
@@ -32,16 +35,17 @@ TsqrPlan plan_tsqr(int64_t m, int d, size_t elem_bytes, int max_smem_bytes);
 // Factor B (m x d, row-major, ldb) through the tree. R (d x d, row-major, upper, exact zeros
 // below) is written to r_out (ld = d) — on device.
 template <typename T>
-cudaError_t tsqr_factor(const TsqrPlan& p, const T* B, int64_t ldb, T* v_arena, T* beta_arena, T* r_arena,
-                        T* r_out, cudaStream_t st);
+cudaError_t tsqr_factor(const TsqrPlan& p, const T* B, int64_t ldb, T* v_arena, T* beta_arena, T* t_arena,
+                        T* r_arena, T* r_out, cudaStream_t st);
 
 // Form the explicit Q (m x d, row-major, ldq) from a factored tree. If q_top is non-null it is the
 // d x d (row-major, ld = d) block that multiplies the tree's top-level Q from the right — used for
 // the cross-rank top level (Q_g = Q_local_tree · Q_global[g*d:(g+1)*d, :]); null means identity.
 template <typename T>
-cudaError_t tsqr_form_q(const TsqrPlan& p, const T* q_top, T* v_arena, T* beta_arena, T* scratch, T* Q,
-                        int64_t ldq, cudaStream_t st);
+cudaError_t tsqr_form_q(const TsqrPlan& p, const T* q_top, T* v_arena, T* beta_arena, T* t_arena, T* scratch, T* Q,
+                        int64_t ldq, int max_smem, cudaStream_t st);
 
+// scratch of tsqr_form_q: working blocks (wide path), T-product buffers and two level buffers.
 int64_t tsqr_scratch_elems(const TsqrPlan& p);
 
 }  // namespace coru_gpu
