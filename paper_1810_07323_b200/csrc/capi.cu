@@ -128,6 +128,8 @@ struct coru_ctx {
     int device = 0;
     cudaStream_t own_stream = nullptr;
     cudaStream_t stream = nullptr;
+    cudaStream_t aux = nullptr;  // second stream: the two TSQR trees run concurrently
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     int num_sms = 148;
     int max_smem = 227 * 1024;
     int host_threads = 1;
@@ -371,30 +373,46 @@ int run(coru_ctx* c, const Request<T>& r, size_t extra_arena_off = 0) {
     CORU_CUDA(cudaMemsetAsync(w.q2, 0, size_t(N) * dp * sizeof(T), st));
 
     // Sketch and power rounds (corutv.hpp:54-58): c1 = a·c2 ; c2_prev = c2 ; c2 = a^T·c1.
+    // The two QRs are independent and latency-bound (one CTA per tree block), so they run on two
+    // streams: single-GPU, QR(c1) starts on the aux stream as soon as the last c1 exists and
+    // overlaps the last A^T pass; with a communicator QR(c1) stays on the main stream (its
+    // all-gather must keep the NCCL issue order) and QR(c2) goes to the aux stream.
+    const bool sharded = c->world > 1;
     for (int i = 0; i <= r.q; ++i) {
         CORU_TRY(gemm<T>(c, r.op_a(), r.A, r.lda, w.b2, dp, w.b1, dp, R, N, d, w.gws, w.gws_elems));
+        if (i == r.q && !sharded) {
+            CORU_CUDA(cudaEventRecord(c->ev_fork, st));
+            CORU_CUDA(cudaStreamWaitEvent(c->aux, c->ev_fork, 0));
+            CORU_TRY(w.ts1.factor(w.b1, dp, w.r1, c->aux));  // Q1, R1 = QR(c1) (corutv.hpp:59)
+            CORU_TRY(w.ts1.form_q(nullptr, w.q1, dp, c->aux));
+            CORU_CUDA(conditioning_flag<T>(w.r1, d, d, w.flag, c->aux));  // corutv.hpp:61-64
+            ++g_launches;
+        }
         if (i == r.q && w.b2prev)
             CORU_CUDA(cudaMemcpyAsync(w.b2prev, w.b2, size_t(N) * dp * sizeof(T), cudaMemcpyDeviceToDevice, st));
         CORU_TRY(gemm<T>(c, r.op_at(), r.A, r.lda, w.b1, dp, w.b2, dp, N, R, d, w.gws, w.gws_elems));
         CORU_TRY(allreduce<T>(c, w.b2, size_t(N) * dp));
     }
-
-    // Q1, R1 = QR(c1) through the TSQR tree (corutv.hpp:59), cross-rank top level when sharded.
-    if (c->world > 1) {
+    if (sharded) {
+        // Q2 = QR(c2) (corutv.hpp:60): c2 is replicated, every rank computes the same tree (aux).
+        CORU_CUDA(cudaEventRecord(c->ev_fork, st));
+        CORU_CUDA(cudaStreamWaitEvent(c->aux, c->ev_fork, 0));
+        CORU_TRY(w.ts2.factor(w.b2, dp, w.r2, c->aux));
+        CORU_TRY(w.ts2.form_q(nullptr, w.q2, dp, c->aux));
+        // Q1, R1: local tree, all-gather of the R_g, redundant top level, local Q (main stream).
         CORU_TRY(w.ts1.factor(w.b1, dp, w.r1loc, st));
         CORU_NCCL(nccl()->AllGather(w.r1loc, w.rstack, size_t(d) * d, nccl_type<T>(), c->comm, st));
         CORU_TRY(w.tstop.factor(w.rstack, d, w.r1, st));
         CORU_TRY(w.tstop.form_q(nullptr, w.qtop, d, st));
         CORU_TRY(w.ts1.form_q(w.qtop + int64_t(c->rank) * d * d, w.q1, dp, st));
+        CORU_CUDA(conditioning_flag<T>(w.r1, d, d, w.flag, st));
+        ++g_launches;
     } else {
-        CORU_TRY(w.ts1.factor(w.b1, dp, w.r1, st));
-        CORU_TRY(w.ts1.form_q(nullptr, w.q1, dp, st));
+        CORU_TRY(w.ts2.factor(w.b2, dp, w.r2, st));  // Q2 = QR(c2) (corutv.hpp:60)
+        CORU_TRY(w.ts2.form_q(nullptr, w.q2, dp, st));
     }
-    CORU_CUDA(conditioning_flag<T>(w.r1, d, d, w.flag, st));  // corutv.hpp:61-64
-    ++g_launches;
-    // Q2 = QR(c2) (corutv.hpp:60): c2 is replicated, so every rank computes the same tree.
-    CORU_TRY(w.ts2.factor(w.b2, dp, w.r2, st));
-    CORU_TRY(w.ts2.form_q(nullptr, w.q2, dp, st));
+    CORU_CUDA(cudaEventRecord(c->ev_join, c->aux));
+    CORU_CUDA(cudaStreamWaitEvent(st, c->ev_join, 0));
 
     if (r.mode == Mode::Sketch) {
         CORU_CUDA(copy_block<T>(w.q1, dp, r.q1, r.ldq1, R, d, st));
@@ -543,6 +561,13 @@ int corutv_host(coru_ctx* c, const T* A, int64_t m, int64_t n, int64_t ell, int 
     CORU_CUDA(cudaMemcpyAsync(a_d, A, sizeof(T) * m * n, cudaMemcpyHostToDevice, st));
     CORU_CUDA(any_nonfinite<T>(a_d, m * n, f_d, st));
     ++g_launches;
+    {
+        // The Matrix constructor rejects non-finite entries before any work (matrix.hpp:29-31).
+        int bad = 0;
+        CORU_CUDA(cudaMemcpyAsync(&bad, f_d, sizeof(int), cudaMemcpyDeviceToHost, st));
+        CORU_CUDA(cudaStreamSynchronize(st));
+        if (bad) return fail(CORU_EINVAL, "Matrix: non-finite entry");
+    }
     coru_utv out{u_d, ell, t_d, ell, v_d, ell, perm, 0, 0};
     Request<T> r;
     r.A = a_d;
@@ -575,13 +600,10 @@ int corutv_host(coru_ctx* c, const T* A, int64_t m, int64_t n, int64_t ell, int 
         r.ldt = ell;
     }
     CORU_TRY(run<T>(c, r, head_bytes));
-    int bad = 0;
-    CORU_CUDA(cudaMemcpyAsync(&bad, f_d, sizeof(int), cudaMemcpyDeviceToHost, st));
     CORU_CUDA(cudaMemcpyAsync(U, u_d, sizeof(T) * m * ell, cudaMemcpyDeviceToHost, st));
     CORU_CUDA(cudaMemcpyAsync(Tt, t_d, sizeof(T) * ell * ell, cudaMemcpyDeviceToHost, st));
     CORU_CUDA(cudaMemcpyAsync(V, v_d, sizeof(T) * n * ell, cudaMemcpyDeviceToHost, st));
     CORU_CUDA(cudaStreamSynchronize(st));
-    if (bad) return fail(CORU_EINVAL, "Matrix: non-finite entry");
     if (lower) *lower = m < n ? 1 : 0;
     if (warn) *warn = out.conditioning_warning;
     return CORU_OK;
@@ -624,6 +646,12 @@ int coru_ctx_create(int device, coru_ctx** out) {
         return fail(CORU_ECUDA, "cudaStreamCreate failed");
     }
     c->stream = c->own_stream;
+    if (cudaStreamCreateWithFlags(&c->aux, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming) != cudaSuccess) {
+        coru_ctx_destroy(c);
+        return fail(CORU_ECUDA, "stream/event creation failed");
+    }
     *out = c;
     return CORU_OK;
 }
@@ -635,6 +663,12 @@ void coru_ctx_destroy(coru_ctx* c) {
     if (c->comm && nccl() && nccl()->CommDestroy) nccl()->CommDestroy(c->comm);
     if (c->arena) cudaFree(c->arena);
     if (c->pinned) cudaFreeHost(c->pinned);
+    if (c->aux) {
+        cudaStreamSynchronize(c->aux);
+        cudaStreamDestroy(c->aux);
+    }
+    if (c->ev_fork) cudaEventDestroy(c->ev_fork);
+    if (c->ev_join) cudaEventDestroy(c->ev_join);
     if (c->own_stream) cudaStreamDestroy(c->own_stream);
     for (auto& e : c->prof_events) {
         cudaEventDestroy(e.first);

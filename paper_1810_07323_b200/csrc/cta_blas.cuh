@@ -165,21 +165,36 @@ __device__ __forceinline__ void cta_mm(int M, int N, int K, const float* A, int 
 
 // Forward compact-WY T factor (LAPACK dlarft convention): H_0 H_1 ... H_{k-1} = I - V T V^T with
 // T upper triangular, T(j,j) = beta_j and T(0:j, j) = -beta_j T(0:j, 0:j) G(0:j, j), where
-// G(a,b) = v_a^T v_b (a < b) is given in shared memory (ldg). One warp; lanes over rows of T.
+// G(a,b) = v_a^T v_b (a < b) is given (ldg). One warp. For k <= 16 each row of T gets two lanes
+// (the c-range split in halves, one shuffle to combine), which halves the serial chain.
 template <typename T>
 __device__ __forceinline__ void warp_larft(int k, const T* G, int ldg, const T* beta, T* Tm, int ldt) {
     const int lane = threadIdx.x & 31;
+    if (k <= 16) {
+        const int a = lane >> 1, half = lane & 1;
+        for (int b = 0; b < k; ++b) {
+            T s = 0;
+            if (a < b) {
+                const int mid = (a + b) >> 1;
+                const int c0 = half ? mid : a, c1 = half ? b : mid;
+                for (int c = c0; c < c1; ++c) s += Tm[a * ldt + c] * G[c * ldg + b];
+            }
+            s += __shfl_xor_sync(0xffffffffu, s, 1);
+            if (half == 0 && a < k) Tm[a * ldt + b] = a < b ? -beta[b] * s : (a == b ? beta[b] : T(0));
+            __syncwarp();
+        }
+        return;
+    }
     for (int b = 0; b < k; ++b) {
         const T bb = beta[b];
-        // rows a < b, each lane handles a = lane, lane + 32, ...
-        for (int a = lane; a < b; a += 32) {
-            T s = 0;
-            for (int c = a; c < b; ++c) s += Tm[a * ldt + c] * G[c * ldg + b];
-            Tm[a * ldt + b] = -bb * s;
-        }
-        if (lane == 0) {
-            Tm[b * ldt + b] = bb;
-            for (int a = b + 1; a < k; ++a) Tm[a * ldt + b] = T(0);
+        for (int a = lane; a < k; a += 32) {
+            if (a < b) {
+                T s = 0;
+                for (int c = a; c < b; ++c) s += Tm[a * ldt + c] * G[c * ldg + b];
+                Tm[a * ldt + b] = -bb * s;
+            } else {
+                Tm[a * ldt + b] = a == b ? bb : T(0);
+            }
         }
         __syncwarp();
     }

@@ -18,7 +18,8 @@ namespace coru_gpu {
 
 namespace {
 
-constexpr int kThreads = 512;
+constexpr int kThreads = 1024;
+constexpr int kG = 8;  // lanes per column group in the trailing update
 constexpr int kWarps = kThreads / 32;
 constexpr int kQrcpGemmScratch = 4096;
 
@@ -51,18 +52,34 @@ __device__ __forceinline__ T warp_sumsq(const T* col, int lo, int hi, int lane) 
     return warp_sum(s);
 }
 
+// Sum over the kG lanes of a column group (xor butterfly: every lane of the group gets the bits).
+template <typename T>
+__device__ __forceinline__ T group_sum(T v) {
+#pragma unroll
+    for (int o = kG / 2; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+template <typename T>
+__device__ __forceinline__ T group_sumsq(const T* col, int lo, int hi, int gl) {
+    T s = 0;
+    for (int i = lo + gl; i < hi; i += kG) s = add_rn(s, mul_rn(col[i], col[i]));
+    return group_sum(s);
+}
+
 template <typename T>
 __global__ void __launch_bounds__(kThreads) k_qrcp(const T* __restrict__ M, int ldm, int d, T* __restrict__ Q, int ldq,
                                                    T* __restrict__ Tout, int ldt, int64_t* __restrict__ perm_out,
                                                    T* __restrict__ gscratch, int use_smem) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int grp = tid / kG, gl = tid % kG;  // column groups of kG lanes
+    constexpr int kGroups = kThreads / kG;
     // smem layout: colsq[d], base[d], beta[d] (T), perm[d] (int), piv (int), then W if it fits.
     T* colsq = reinterpret_cast<T*>(smem_raw);
     T* base = colsq + d;
     T* beta = base + d;
     int* perm = reinterpret_cast<int*>(beta + d);
-    int* piv_s = perm + d;
     const int ldw = d | 1;
     T* W = use_smem ? reinterpret_cast<T*>(smem_raw + (((3 * d * sizeof(T) + (d + 1) * 4) + 15) / 16) * 16)
                     : gscratch;
@@ -73,15 +90,17 @@ __global__ void __launch_bounds__(kThreads) k_qrcp(const T* __restrict__ M, int 
     for (int c = tid; c < d; c += kThreads) perm[c] = c;
     __syncthreads();
     // Initial squared norms (qr.hpp:115-119).
-    for (int c = warp; c < d; c += kWarps) {
-        const T s = warp_sumsq(W + c * ldw, 0, d, lane);
-        if (lane == 0) colsq[c] = base[c] = s;
+    for (int rr = 0; rr < (d + kGroups - 1) / kGroups; ++rr) {  // warp-uniform rounds
+        const int c = grp + rr * kGroups;
+        const T s = group_sumsq(W + (c < d ? c : 0) * ldw, 0, d, gl);
+        if (c < d && gl == 0) colsq[c] = base[c] = s;
     }
     __syncthreads();
     for (int j = 0; j < d; ++j) {
-        // Argmax with lowest-index ties (qr.hpp:121-123), warp 0: each lane keeps the first
-        // maximum of its strided scan; the merge prefers the larger value, then the lower index.
+        // ---- phase A (warp 0): pivot, swap, reflector ----
         if (warp == 0) {
+            // argmax with lowest-index ties (qr.hpp:121-123): each lane keeps the first maximum
+            // of its strided scan; the merge prefers the larger value, then the lower index.
             T bv = T(0);
             int bi = -1;
             for (int c = j + lane; c < d; c += 32) {
@@ -94,25 +113,21 @@ __global__ void __launch_bounds__(kThreads) k_qrcp(const T* __restrict__ M, int 
                 const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
                 if (oi >= 0 && (bi < 0 || ov > bv || (ov == bv && oi < bi))) { bv = ov; bi = oi; }
             }
-            if (lane == 0) *piv_s = bi;
-        }
-        __syncthreads();
-        const int piv = *piv_s;
-        if (piv != j) {  // swap columns j, piv (qr.hpp:124-129)
-            for (int i = tid; i < d; i += kThreads) {
-                const T x = W[j * ldw + i];
-                W[j * ldw + i] = W[piv * ldw + i];
-                W[piv * ldw + i] = x;
+            const int piv = __shfl_sync(0xffffffffu, bi, 0);  // one pivot for the warp (NaN-safe)
+            if (piv != j) {  // swap columns j, piv (qr.hpp:124-129)
+                for (int i = lane; i < d; i += 32) {
+                    const T x = W[j * ldw + i];
+                    W[j * ldw + i] = W[piv * ldw + i];
+                    W[piv * ldw + i] = x;
+                }
+                if (lane == 0) {
+                    T x = colsq[j]; colsq[j] = colsq[piv]; colsq[piv] = x;
+                    x = base[j]; base[j] = base[piv]; base[piv] = x;
+                    const int p = perm[j]; perm[j] = perm[piv]; perm[piv] = p;
+                }
+                __syncwarp();
             }
-            if (tid == 0) {
-                T x = colsq[j]; colsq[j] = colsq[piv]; colsq[piv] = x;
-                x = base[j]; base[j] = base[piv]; base[piv] = x;
-                const int p = perm[j]; perm[j] = perm[piv]; perm[piv] = p;
-            }
-            __syncthreads();
-        }
-        // Reflector for column j (make_reflector, qr.hpp:32-45), warp 0.
-        if (warp == 0) {
+            // reflector for column j (make_reflector, qr.hpp:32-45)
             T* col = W + j * ldw;
             const T sig = warp_sumsq(col, j + 1, d, lane);
             const T x0 = col[j];
@@ -128,37 +143,36 @@ __global__ void __launch_bounds__(kThreads) k_qrcp(const T* __restrict__ M, int 
             if (lane == 0) beta[j] = b;
         }
         __syncthreads();
-        // Trailing update + downdate (qr.hpp:131-139).
+        // ---- phase B (column groups): trailing update + downdate (qr.hpp:131-139) ----
         const T bj = beta[j];
         const T* vcol = W + j * ldw;
-        for (int c = j + 1 + warp; c < d; c += kWarps) {
-            T* col = W + c * ldw;
+        // Rounds are warp-uniform: groups past the last column compute on column j and never write,
+        // so every shuffle and __syncwarp sees the full warp.
+        const int rounds = (d - (j + 1) + kGroups - 1) / kGroups;
+        for (int rr = 0; rr < rounds; ++rr) {
+            const int c = j + 1 + grp + rr * kGroups;
+            const bool act = c < d;
+            T* col = W + (act ? c : j) * ldw;
             if (bj != T(0)) {
                 T s = 0;
-                for (int i = j + 1 + lane; i < d; i += 32) s += vcol[i] * col[i];
-                s = warp_sum(s);
+                for (int i = j + 1 + gl; i < d; i += kG) s += vcol[i] * col[i];
+                s = group_sum(s);
                 s += col[j];
                 s *= bj;
-                for (int i = j + 1 + lane; i < d; i += 32) col[i] -= s * vcol[i];
+                if (act) {
+                    for (int i = j + 1 + gl; i < d; i += kG) col[i] -= s * vcol[i];
+                    if (gl == 0) col[j] -= s;
+                }
                 __syncwarp();
-                if (lane == 0) col[j] -= s;
-                __syncwarp();
             }
-            T cs = 0;
-            if (lane == 0) {
-                const T w = col[j];
-                cs = colsq[c] - mul_rn(w, w);
+            const T w = col[j];
+            const T cs = (act ? colsq[c] : T(0)) - mul_rn(w, w);
+            const bool need = act && cs < T(1e-6) * base[act ? c : j];
+            if (__any_sync(0xffffffffu, need)) {
+                const T s2 = group_sumsq(col, j + 1, d, gl);
+                if (need && gl == 0) colsq[c] = base[c] = s2;
             }
-            cs = __shfl_sync(0xffffffffu, cs, 0);
-            bool small = false;
-            if (lane == 0) small = cs < T(1e-6) * base[c];
-            small = __shfl_sync(0xffffffffu, small, 0);
-            if (small) {
-                const T s = warp_sumsq(col, j + 1, d, lane);
-                if (lane == 0) colsq[c] = base[c] = s;
-            } else if (lane == 0) {
-                colsq[c] = cs;
-            }
+            if (act && !need && gl == 0) colsq[c] = cs;
         }
         __syncthreads();
     }
@@ -169,25 +183,33 @@ __global__ void __launch_bounds__(kThreads) k_qrcp(const T* __restrict__ M, int 
     }
     for (int c = tid; c < d; c += kThreads) perm_out[c] = perm[c];
     __syncthreads();
-    // Q_M = H_0 ... H_{d-1} = I - V T V^T (accumulate_q, qr.hpp:60-72, in compact-WY form):
-    // explicit V, G = V^T V, T by the forward recurrence, Y = T V^T, Q = I - V Y (DMMA CTA GEMMs).
+    // Q_M = H_0 ... H_{d-1} I (accumulate_q, qr.hpp:60-72) by 16-column panels in reverse,
+    // E <- E - V_p T_p (V_p^T E) with each panel's compact-WY T_p (DMMA CTA GEMMs).
     const int ldx = qrcp_ldx(d);
-    T* Vx = gscratch + qrcp_w_elems(d);
-    T* G = Vx + int64_t(d) * ldx;
-    T* Tm = G + d * d;
-    T* Y = Tm + d * d;
-    T* gs = Y + d * d;
+    T* Vx = gscratch + qrcp_w_elems(d);         // explicit reflectors, column-major d x ldx
+    T* G = Vx + int64_t(d) * ldx;                // 16 x 16 panel Gram matrix
+    T* Tp = G + 256;                             // 16 x 16 panel T
+    T* Y = Tp + 256;                             // 16 x d
+    T* Z = Y + 16 * d;                           // 16 x d
+    T* gs = Z + 16 * d;
     for (int a = warp; a < d; a += kWarps)
         for (int r = lane; r < ldx; r += 32) Vx[a * ldx + r] = r > a && r < d ? W[a * ldw + r] : T(r == a ? 1 : 0);
     for (int e = tid; e < d * d; e += kThreads) Q[(e / d) * ldq + e % d] = T(e / d == e % d ? 1 : 0);
     __syncthreads();
-    cta_mm(d, d, d, Vx, ldx, 1, Vx, 1, ldx, G, d, 1, T(1), false, gs, kQrcpGemmScratch);
-    __syncthreads();
-    if (warp == 0) warp_larft<T>(d, G, d, beta, Tm, d);
-    __syncthreads();
-    cta_mm(d, d, d, Tm, d, 1, Vx, ldx, 1, Y, d, 1, T(1), false, gs, kQrcpGemmScratch);
-    __syncthreads();
-    cta_mm(d, d, d, Vx, 1, ldx, Y, d, 1, Q, ldq, 1, T(-1), true, gs, kQrcpGemmScratch);
+    for (int p0 = ((d - 1) / 16) * 16; p0 >= 0; p0 -= 16) {
+        const int nbp = min(16, d - p0), K = d - p0;
+        const T* Vp = Vx + p0 * ldx + p0;  // rows >= p0 of the panel's reflectors
+        cta_mm(nbp, nbp, K, Vp, ldx, 1, Vp, 1, ldx, G, 16, 1, T(1), false, gs, kQrcpGemmScratch);
+        __syncthreads();
+        if (warp == 0) warp_larft<T>(nbp, G, 16, beta + p0, Tp, 16);
+        // Y = V_p^T E(rows >= p0)
+        cta_mm(nbp, d, K, Vp, ldx, 1, Q + p0 * ldq, ldq, 1, Y, d, 1, T(1), false, gs, kQrcpGemmScratch);
+        __syncthreads();
+        cta_mm(nbp, d, nbp, Tp, 16, 1, Y, d, 1, Z, d, 1, T(1), false, gs, kQrcpGemmScratch);
+        __syncthreads();
+        cta_mm(K, d, nbp, Vp, 1, ldx, Z, d, 1, Q + p0 * ldq, ldq, 1, T(-1), true, gs, kQrcpGemmScratch);
+        __syncthreads();
+    }
 }
 
 template <typename T>
@@ -246,7 +268,7 @@ int grid_for(int64_t total) { return int(std::min<int64_t>((total + 255) / 256, 
 }  // namespace
 
 int64_t qrcp_scratch_elems(int d) {
-    return qrcp_w_elems(d) + int64_t(qrcp_ldx(d)) * d + 3 * int64_t(d) * d + kQrcpGemmScratch;
+    return qrcp_w_elems(d) + int64_t(qrcp_ldx(d)) * d + 512 + 32 * int64_t(d) + kQrcpGemmScratch;
 }
 
 template <typename T>

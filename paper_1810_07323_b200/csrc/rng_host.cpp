@@ -4,14 +4,22 @@
 //   the all-zero guard (rng.hpp:41-61), uniform_open01 = ((x>>11)+1)·2^-53 (rng.hpp:64), Box–Muller
 //   r = sqrt(-2 ln u1), θ = 2π·u2, r·cos θ first then the spare r·sin θ (rng.hpp:86-98), row-major
 //   fill (rng.hpp:107-112).
+//
 // Φ stays on the host on purpose: bit-exactness is defined by the host libm's log/sin/cos, which
-// the device's math library does not reproduce. The serial part is only the xoshiro word stream
-// (~1 ns/word); the transcendental Box–Muller transform is split over host threads, each pair
-// being a pure function of its two words, so the output is identical for any thread count.
-// Compiled with -ffp-contract=off (no FMA contraction on the host).
+// the device math library does not reproduce. Both halves are parallel and exact:
+//   * the xoshiro256++ transition is linear over GF(2)^256, so every worker jumps straight to its
+//     first word with precomputed M^(2^i) (popcount(offset) 256x256 bit mat-vecs) and then runs
+//     the ordinary recurrence — the word stream is identical to the serial one;
+//   * each Box–Muller pair is a pure function of its two words.
+// Workers come from a persistent pool (no thread creation per call). Compiled with
+// -ffp-contract=off (no FMA contraction on the host).
+#include <atomic>
 #include <cmath>
+#include <condition_variable>
 #include <cstdint>
 #include <cstring>
+#include <functional>
+#include <mutex>
 #include <thread>
 #include <vector>
 
@@ -27,56 +35,180 @@ inline uint64_t splitmix_next(uint64_t& s) {
 }
 inline uint64_t rotl(uint64_t x, int k) { return (x << k) | (x >> (64 - k)); }
 
-struct Xoshiro {
+struct State {
     uint64_t s[4];
-    Xoshiro(uint64_t seed, uint64_t stream) {
-        uint64_t a = seed, b = stream;
-        bool zero = true;
-        for (auto& w : s) {
-            w = splitmix_next(a) ^ splitmix_next(b);
-            zero = zero && w == 0;
-        }
-        if (zero) s[0] = 1;
-    }
-    uint64_t next() {
-        const uint64_t r = rotl(s[0] + s[3], 23) + s[0];
-        const uint64_t t = s[1] << 17;
-        s[2] ^= s[0];
-        s[3] ^= s[1];
-        s[1] ^= s[2];
-        s[0] ^= s[3];
-        s[2] ^= t;
-        s[3] = rotl(s[3], 45);
-        return r;
-    }
 };
+
+inline State seed_state(uint64_t seed, uint64_t stream) {
+    State st;
+    uint64_t a = seed, b = stream;
+    bool zero = true;
+    for (auto& w : st.s) {
+        w = splitmix_next(a) ^ splitmix_next(b);
+        zero = zero && w == 0;
+    }
+    if (zero) st.s[0] = 1;
+    return st;
+}
+
+inline uint64_t next_word(State& st) {
+    uint64_t* s = st.s;
+    const uint64_t r = rotl(s[0] + s[3], 23) + s[0];
+    const uint64_t t = s[1] << 17;
+    s[2] ^= s[0];
+    s[3] ^= s[1];
+    s[1] ^= s[2];
+    s[0] ^= s[3];
+    s[2] ^= t;
+    s[3] = rotl(s[3], 45);
+    return r;
+}
+
+// 256x256 GF(2) matrix, row i = bit mask over the 256 state bits feeding output bit i.
+struct Gf2 {
+    uint64_t row[256][4];
+};
+
+inline int bit(const State& v, int i) { return int((v.s[i >> 6] >> (i & 63)) & 1u); }
+
+State mul(const Gf2& m, const State& v) {
+    State out{{0, 0, 0, 0}};
+    for (int i = 0; i < 256; ++i) {
+        const uint64_t p = (m.row[i][0] & v.s[0]) ^ (m.row[i][1] & v.s[1]) ^ (m.row[i][2] & v.s[2]) ^
+                           (m.row[i][3] & v.s[3]);
+        if (__builtin_parityll(p)) out.s[i >> 6] |= uint64_t(1) << (i & 63);
+    }
+    return out;
+}
+
+Gf2 square(const Gf2& a) {
+    // (A·A) row i = XOR of rows k of A for every bit k set in A's row i.
+    Gf2 c;
+    std::memset(&c, 0, sizeof(c));
+    for (int i = 0; i < 256; ++i)
+        for (int k = 0; k < 256; ++k)
+            if ((a.row[i][k >> 6] >> (k & 63)) & 1u)
+                for (int w = 0; w < 4; ++w) c.row[i][w] ^= a.row[k][w];
+    return c;
+}
+
+constexpr int kJumpBits = 48;  // offsets below 2^48 words
+
+// jump[i] = M^(2^i) for the state transition M of one xoshiro256++ step.
+const std::vector<Gf2>& jump_table() {
+    static std::vector<Gf2> table = [] {
+        std::vector<Gf2> t(kJumpBits);
+        Gf2& m = t[0];
+        std::memset(&m, 0, sizeof(m));
+        for (int j = 0; j < 256; ++j) {  // column j = M e_j
+            State e{{0, 0, 0, 0}};
+            e.s[j >> 6] = uint64_t(1) << (j & 63);
+            next_word(e);
+            for (int i = 0; i < 256; ++i)
+                if (bit(e, i)) m.row[i][j >> 6] |= uint64_t(1) << (j & 63);
+        }
+        for (int k = 1; k < kJumpBits; ++k) t[k] = square(t[k - 1]);
+        return t;
+    }();
+    return table;
+}
+
+State jump(State s, uint64_t k) {
+    const auto& t = jump_table();
+    for (int i = 0; i < kJumpBits && k; ++i, k >>= 1)
+        if (k & 1u) s = mul(t[size_t(i)], s);
+    return s;
+}
 
 inline double open01(uint64_t w) { return static_cast<double>((w >> 11) + 1) * 0x1.0p-53; }
 
-// Pair p -> (r cos θ, r sin θ) from words 2p, 2p+1.
-inline void box_muller(uint64_t w1, uint64_t w2, double& c, double& s) {
-    const double u1 = open01(w1), u2 = open01(w2);
-    const double r = std::sqrt(-2.0 * std::log(u1));
-    const double theta = 2.0 * 3.141592653589793 * u2;  // 2·std::numbers::pi·u2
-    s = r * std::sin(theta);
-    c = r * std::cos(theta);
+// Persistent worker pool: run(n, f) calls f(0..n-1) on n workers (the caller is worker 0).
+class Pool {
+public:
+    void run(int n, const std::function<void(int)>& f) {
+        if (n <= 1) {
+            f(0);
+            return;
+        }
+        std::unique_lock<std::mutex> call(call_mu_);  // one dispatch at a time
+        ensure(n - 1);
+        {
+            std::lock_guard<std::mutex> lk(mu_);
+            job_ = &f;
+            active_ = n - 1;
+            pending_ = n - 1;
+            ++gen_;
+        }
+        cv_.notify_all();
+        f(0);
+        std::unique_lock<std::mutex> lk(mu_);
+        done_cv_.wait(lk, [&] { return pending_ == 0; });
+        job_ = nullptr;
+    }
+    ~Pool() {
+        {
+            std::lock_guard<std::mutex> lk(mu_);
+            stop_ = true;
+            ++gen_;
+        }
+        cv_.notify_all();
+        for (auto& t : threads_) t.join();
+    }
+
+private:
+    void ensure(int workers) {
+        while (int(threads_.size()) < workers) {
+            const int id = int(threads_.size()) + 1;
+            threads_.emplace_back([this, id] { loop(id); });
+        }
+    }
+    void loop(int id) {
+        uint64_t seen = 0;
+        for (;;) {
+            const std::function<void(int)>* job;
+            {
+                std::unique_lock<std::mutex> lk(mu_);
+                cv_.wait(lk, [&] { return stop_ || gen_ != seen; });
+                if (stop_) return;
+                seen = gen_;
+                if (id > active_) continue;
+                job = job_;
+            }
+            (*job)(id);
+            std::lock_guard<std::mutex> lk(mu_);
+            if (--pending_ == 0) done_cv_.notify_all();
+        }
+    }
+    std::mutex call_mu_, mu_;
+    std::condition_variable cv_, done_cv_;
+    std::vector<std::thread> threads_;
+    const std::function<void(int)>* job_ = nullptr;
+    int active_ = 0, pending_ = 0;
+    uint64_t gen_ = 0;
+    bool stop_ = false;
+};
+
+Pool& pool() {
+    static Pool p;
+    return p;
 }
 
 }  // namespace
 
-// Writes rows x cols Gaussians. Element e (row-major index) goes to out[(e / cols) * ldo + e % cols]
-// converted to OutT (fp32 rounds the fp64 value). threads <= 1 runs serially.
+// Writes rows x cols Gaussians; element e (row-major index) goes to out[(e / cols) * ldo + e % cols]
+// converted to OutT (fp32 rounds the fp64 value). Identical output for any thread count.
 template <typename OutT>
 void gaussian_host(int64_t rows, int64_t cols, uint64_t seed, uint64_t stream, OutT* out, int64_t ldo,
                    int threads) {
     const int64_t total = rows * cols;
     const int64_t pairs = (total + 1) / 2;
-    std::vector<uint64_t> words(size_t(2 * pairs));
-    Xoshiro x(seed, stream);
-    for (auto& w : words) w = x.next();
-    // Pair p fills row-major elements 2p and 2p+1; (row, col) advance incrementally (no division
-    // in the loop — an int64 divide per element cost more than the transcendental functions).
-    auto work = [&](int64_t p0, int64_t p1) {
+    const State s0 = seed_state(seed, stream);
+    int nt = threads < 1 ? 1 : threads;
+    if (pairs < 8192) nt = 1;
+    if (nt > 1) jump_table();  // build once, outside the timed fan-out
+    pool().run(nt, [&](int t) {
+        const int64_t p0 = pairs * t / nt, p1 = pairs * (t + 1) / nt;
+        State st = t == 0 ? s0 : jump(s0, uint64_t(2 * p0));
         int64_t e = 2 * p0, r = e / cols, c = e % cols;
         auto put = [&](double v) {
             out[r * ldo + c] = static_cast<OutT>(v);
@@ -86,19 +218,15 @@ void gaussian_host(int64_t rows, int64_t cols, uint64_t seed, uint64_t stream, O
             }
         };
         for (int64_t p = p0; p < p1; ++p) {
-            double cv, sv;
-            box_muller(words[size_t(2 * p)], words[size_t(2 * p + 1)], cv, sv);
-            put(cv);
+            const double u1 = open01(next_word(st));
+            const double u2 = open01(next_word(st));
+            const double rad = std::sqrt(-2.0 * std::log(u1));
+            const double theta = 2.0 * 3.141592653589793 * u2;  // 2·std::numbers::pi·u2
+            const double sv = rad * std::sin(theta);
+            put(rad * std::cos(theta));
             if (2 * p + 1 < total) put(sv);
         }
-    };
-    if (threads <= 1 || pairs < 4096) {
-        work(0, pairs);
-        return;
-    }
-    std::vector<std::thread> pool;
-    for (int t = 0; t < threads; ++t) pool.emplace_back(work, pairs * t / threads, pairs * (t + 1) / threads);
-    for (auto& th : pool) th.join();
+    });
 }
 
 template void gaussian_host<double>(int64_t, int64_t, uint64_t, uint64_t, double*, int64_t, int);

@@ -288,11 +288,26 @@ __global__ void __launch_bounds__(kBThreads, 1)
     const int ldw = S.ldw, ldvp = S.ldvp;
     T* Tb = Tg + int64_t(b) * npanels(d) * kNB * kNB;  // this block's panel T factors
 
-    // Load rows [r0, r1) (row-major, coalesced along columns) into column-major W.
-    for (int r = warp; r < rb; r += kBThreads / 32) {
-        const T* src = X + (r0 + r) * ldx;
-        for (int c = lane; c < d; c += 32) W[c * ldw + r] = src[c];
-    }
+    // Load rows [r0, r1) (row-major, coalesced along columns) into column-major W; four rows in
+    // flight per warp for memory-level parallelism.
+    for (int cb = 0; cb < d; cb += 128)
+        for (int r = warp * 4; r < rb; r += (kBThreads / 32) * 4) {
+            T v[4][4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+#pragma unroll
+                for (int h = 0; h < 4; ++h) {
+                    const int c = cb + lane + 32 * h;
+                    v[q][h] = (r + q < rb && c < d) ? X[(r0 + r + q) * ldx + c] : T(0);
+                }
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+#pragma unroll
+                for (int h = 0; h < 4; ++h) {
+                    const int c = cb + lane + 32 * h;
+                    if (r + q < rb && c < d) W[c * ldw + r + q] = v[q][h];
+                }
+        }
     __syncthreads();
 
     for (int p0 = 0, pi = 0; p0 < d; p0 += kNB, ++pi) {
@@ -315,38 +330,49 @@ __global__ void __launch_bounds__(kBThreads, 1)
                     const T bj = S.beta[j];
                     if (bj == T(0)) continue;
                     const T* vj = S.Vp + jj * ldvp;
-                    T v[kRPL];
-                    T s = 0;
+                    T v[kRPL], pr[kRPL];
 #pragma unroll
                     for (int u = 0; u < kRPL; ++u) {
                         const int r = lane + 32 * u;
                         v[u] = r < rb ? vj[r] : T(0);
-                        s += v[u] * x[u];
+                        pr[u] = v[u] * x[u];
                     }
-                    s = warp_sum(s) * bj;
+                    // pairwise (tree) sum: short dependency chain on the critical path
+#pragma unroll
+                    for (int h = kRPL / 2; h > 0; h >>= 1)
+#pragma unroll
+                        for (int u = 0; u < h; ++u) pr[u] += pr[u + h];
+                    const T s = warp_sum(pr[0]) * bj;
 #pragma unroll
                     for (int u = 0; u < kRPL; ++u) x[u] -= s * v[u];
                 } else {
                     // build reflector j from my column   (make_reflector, qr.hpp:32-45)
-                    T sig = 0, x0 = 0;
+                    T sq[kRPL];
 #pragma unroll
                     for (int u = 0; u < kRPL; ++u) {
                         const int r = lane + 32 * u;
-                        if (r > j) sig += x[u] * x[u];
-                        if (u == (j >> 5)) x0 = x[u];
+                        sq[u] = r > j ? x[u] * x[u] : T(0);
+                        if (r == j) W[c * ldw + j] = x[u];  // x0 through smem: no dynamic register index
                     }
-                    sig = warp_sum(sig);
-                    x0 = __shfl_sync(0xffffffffu, x0, j & 31);
-                    T bj = 0, v0 = 1;
+#pragma unroll
+                    for (int h = kRPL / 2; h > 0; h >>= 1)
+#pragma unroll
+                        for (int u = 0; u < h; ++u) sq[u] += sq[u + h];
+                    const T sig = warp_sum(sq[0]);
+                    __syncwarp();
+                    const T x0 = W[c * ldw + j];
+                    T bj = 0;
                     if (sig != T(0)) {
                         const T mu = tsqrt(x0 * x0 + sig);
-                        v0 = (x0 <= T(0)) ? x0 - mu : -sig / (x0 + mu);
+                        const T v0 = (x0 <= T(0)) ? x0 - mu : -sig / (x0 + mu);
                         bj = T(2) * v0 * v0 / (sig + v0 * v0);
+                        // v = x / v0 (qr.hpp:42); one reciprocal then independent products keeps the
+                        // division off the per-element critical path (<= 1 ulp from x / v0).
+                        const T rv = T(1) / v0;
 #pragma unroll
                         for (int u = 0; u < kRPL; ++u) {
                             const int r = lane + 32 * u;
-                            if (r > j) x[u] /= v0;
-                            if (r == j) x[u] = mu;
+                            x[u] = r > j ? x[u] * rv : (r == j ? mu : x[u]);
                         }
                     }
                     T* vj = S.Vp + jj * ldvp;
@@ -423,7 +449,8 @@ struct FormQSmem {
 };
 
 // Q block b = H_0 ... H_{d-1} [Qin_b; 0]  (Qin null => identity), by panels in reverse:
-//   E <- E - V_p (T_p (V_p^T E)),  p = P-1 ... 0, on column chunks of E.
+//   E <- E - V_p (T_p (V_p^T E)),  p = P-1 ... 0. Columns of Q are independent, so each CTA
+//   forms one kQChunk-wide column chunk (grid = blocks x chunks) to spread a level over more SMs.
 template <typename T>
 __global__ void __launch_bounds__(kBThreads, 1)
     k_qr_blocked_form_q(const T* __restrict__ Qin, int ldqin, int64_t rows, int nb, int d, const T* __restrict__ V,
@@ -441,7 +468,8 @@ __global__ void __launch_bounds__(kBThreads, 1)
     for (int c = warp; c < d; c += kBThreads / 32)
         for (int r = lane; r < S.ldvs; r += 32)
             S.Vs[c * S.ldvs + r] = (r > c && r < rb) ? Vb[int64_t(c) * ldv + r] : T(r == c ? 1 : 0);
-    for (int q0 = 0; q0 < d; q0 += kQChunk) {
+    {
+        const int q0 = blockIdx.y * kQChunk;  // this CTA's column chunk of Q
         const int nq = min(kQChunk, d - q0);
         for (int e = tid; e < nq * rb; e += kBThreads) {
             const int j = e / rb, i = e % rb;
@@ -467,7 +495,6 @@ __global__ void __launch_bounds__(kBThreads, 1)
             const int i = e / nq, j = e % nq;
             Qo[int64_t(i) * ldqout + j] = S.E[j * S.lde + i];
         }
-        __syncthreads();
     }
 }
 
@@ -594,7 +621,8 @@ cudaError_t tsqr_form_q(const TsqrPlan& p, const T* q_top, T* V, T* beta, T* Tar
         if (L.blocked) {
             const size_t sm = FormQSmem<T>::bytes(d, L.rbmax, sizeof(T));
             cudaFuncSetAttribute(k_qr_blocked_form_q<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
-            k_qr_blocked_form_q<T><<<L.nb, kBThreads, sm, st>>>(qin, ldqin, L.rows, L.nb, d, V + L.v_off, L.ldv,
+            const dim3 grid(unsigned(L.nb), unsigned((d + kQChunk - 1) / kQChunk));
+            k_qr_blocked_form_q<T><<<grid, kBThreads, sm, st>>>(qin, ldqin, L.rows, L.nb, d, V + L.v_off, L.ldv,
                                                                  Tarena + L.t_off, out, ldo);
         } else {
             const size_t sm = L.smem ? size_t(L.rbmax | 1) * d * sizeof(T) : 0;

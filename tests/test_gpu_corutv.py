@@ -97,6 +97,10 @@ def test_bad_parameters(ctx):
     bad[2, 3] = np.nan
     with pytest.raises(cg.CoruInvalidArgument):  # matrix.hpp:29-31
         cg.corutv(bad, 3, 0, seed=cg.RngSeed(1, 0), ctx=ctx)
+    # the device entry does not validate (like corutv itself) but must terminate on NaN input
+    import torch
+    f = cg.corutv(torch.from_numpy(bad).cuda(), 3, 0, seed=cg.RngSeed(1, 0), ctx=ctx)
+    assert f.t.shape == (3, 3)
 
 
 def test_determinism_bitwise(ctx):

@@ -7,7 +7,7 @@ import paper_1810_07323_b200 as cg
 ctx = cg.Context(0)
 b = torch.randn(4000, 60, dtype=torch.float64, device="cuda")
 m = torch.randn(60, 60, dtype=torch.float64, device="cuda")
-for _ in range(2):
+for _ in range(4):
     q, r = cg.tsqr(b, ctx=ctx)
     cg.qrcp(m, ctx=ctx)
 torch.cuda.synchronize()
