@@ -126,6 +126,8 @@ int coru_gaussian(int64_t rows, int64_t cols, uint64_t seed, uint64_t stream, do
 /* C (rows x N) = op(A) · X, op 0: A (rows x K), op 1: A^T with A (K x rows); device row-major. */
 int coru_gemm_f64_dev(coru_ctx* ctx, int op, const double* A, int64_t lda, const double* X, int64_t ldx,
                       double* C, int64_t ldc, int64_t rows, int64_t K, int64_t N);
+int coru_gemm_f32_dev(coru_ctx* ctx, int op, const float* A, int64_t lda, const float* X, int64_t ldx, float* C,
+                      int64_t ldc, int64_t rows, int64_t K, int64_t N);
 /* householder_qr (qr.hpp:85-99) via TSQR: B (m x n, m > n) -> Q (m x n), R (n x n). Device. */
 int coru_tsqr_f64_dev(coru_ctx* ctx, const double* B, int64_t ldb, int64_t m, int64_t n, double* Q, int64_t ldq,
                       double* R, int64_t ldr);

@@ -153,6 +153,7 @@ def load_library():
     L.coru_project_f64_dev.argtypes = [p, p, i64, i64, i64, p, i64, p, i64, i64, p, i64]
     L.coru_gaussian.argtypes = [i64, i64, u64, u64, p, i32]
     L.coru_gemm_f64_dev.argtypes = [p, i32, p, i64, p, i64, p, i64, i64, i64, i64]
+    L.coru_gemm_f32_dev.argtypes = [p, i32, p, i64, p, i64, p, i64, i64, i64, i64]
     L.coru_tsqr_f64_dev.argtypes = [p, p, i64, i64, i64, p, i64, p, i64]
     L.coru_qrcp_f64_dev.argtypes = [p, p, i64, i64, p, i64, p, i64, p]
     _lib = L
@@ -387,16 +388,16 @@ def singular_estimates(f: UtvApprox) -> np.ndarray:
 
 # kernel-level entry points (parity tests / benchmarks) ----------------------------------------
 def gemm(a, x, op: int = 0, ctx: Optional[Context] = None, out=None):
-    """C = op(a)·x on the A-pass kernel (op 0: a·x, op 1: a^T·x); CUDA fp64 tensors."""
+    """C = op(a)·x on the A-pass kernel (op 0: a·x, op 1: a^T·x); CUDA fp64 or fp32 tensors."""
     import torch
     ctx = ctx or default_context(a.device.index or 0)
     rows = a.shape[0] if op == 0 else a.shape[1]
     K = a.shape[1] if op == 0 else a.shape[0]
     N = x.shape[1]
-    c = out if out is not None else torch.empty((rows, N), dtype=torch.float64, device=a.device)
+    c = out if out is not None else torch.empty((rows, N), dtype=a.dtype, device=a.device)
+    fn = ctx.lib.coru_gemm_f64_dev if a.dtype == torch.float64 else ctx.lib.coru_gemm_f32_dev
     _torch_sync_stream(ctx, a)
-    _check(ctx.lib.coru_gemm_f64_dev(ctx.h, op, a.data_ptr(), a.stride(0), x.data_ptr(), x.stride(0),
-                                     c.data_ptr(), c.stride(0), rows, K, N))
+    _check(fn(ctx.h, op, a.data_ptr(), a.stride(0), x.data_ptr(), x.stride(0), c.data_ptr(), c.stride(0), rows, K, N))
     return c
 
 

@@ -200,8 +200,8 @@ int64_t gemm_ws<double>(Op op, int64_t Mo, int64_t K, int N, int sms) {
     return plan_gemm_f64(op, Mo, K, N, sms).ws_elems;
 }
 template <>
-int64_t gemm_ws<float>(Op, int64_t, int64_t, int, int) {
-    return 0;
+int64_t gemm_ws<float>(Op op, int64_t Mo, int64_t K, int N, int sms) {
+    return plan_gemm_f32(op, Mo, K, N, sms).ws_elems;
 }
 
 template <typename T>
@@ -237,9 +237,20 @@ int gemm<double>(coru_ctx* c, Op op, const double* A, int64_t lda, const double*
     return CORU_OK;
 }
 template <>
-int gemm<float>(coru_ctx*, Op, const float*, int64_t, const float*, int64_t, float*, int64_t, int64_t, int64_t, int,
-                float*, int64_t) {
-    return fail(CORU_ENOTSUP, "fp32 A-pass kernels are not in this build yet (DESIGN.md: fp32 / C5)");
+int gemm<float>(coru_ctx* c, Op op, const float* A, int64_t lda, const float* X, int64_t ldx, float* C, int64_t ldc,
+                int64_t Mo, int64_t K, int N, float* ws, int64_t ws_elems) {
+    GemmPlan p = plan_gemm_f32(op, Mo, K, N, c->num_sms);
+    if (p.ws_elems > ws_elems) return fail(CORU_ECUDA, "internal: gemm workspace too small");
+    cudaEvent_t stop = nullptr;
+    if (c->prof) CORU_TRY(prof_begin(c, &stop));
+    CORU_CUDA(gemm_f32(op, A, lda, X, ldx, C, ldc, Mo, K, N, p, ws, c->stream));
+    if (stop) {
+        CORU_CUDA(cudaEventRecord(stop, c->stream));
+        c->prof_flops += 2.0 * double(Mo) * double(K) * double(N);
+        c->prof_bytes += 4.0 * double(Mo) * double(K);
+    }
+    g_launches += p.splits > 1 ? 2 : 1;
+    return CORU_OK;
 }
 
 template <typename T>
@@ -914,6 +925,19 @@ int coru_gemm_f64_dev(coru_ctx* c, int op, const double* A, int64_t lda, const d
     const int64_t wse = gemm_ws<double>(o, rows, K, int(N), c->num_sms);
     CORU_TRY(ensure_arena(c, size_t(wse) * 8 + 256));
     CORU_TRY(gemm<double>(c, o, A, lda, X, ldx, C, ldc, rows, K, int(N), reinterpret_cast<double*>(c->arena), wse));
+    CORU_CUDA(cudaStreamSynchronize(c->stream));
+    return CORU_OK;
+}
+
+int coru_gemm_f32_dev(coru_ctx* c, int op, const float* A, int64_t lda, const float* X, int64_t ldx, float* C,
+                      int64_t ldc, int64_t rows, int64_t K, int64_t N) {
+    CORU_TRY(enter(c));
+    std::lock_guard<std::mutex> lk(c->mu);
+    if (rows < 1 || K < 1 || N < 1 || (op != 0 && op != 1)) return fail(CORU_EINVAL, "bad gemm shape");
+    const Op o = op ? Op::T : Op::N;
+    const int64_t wse = gemm_ws<float>(o, rows, K, int(N), c->num_sms);
+    CORU_TRY(ensure_arena(c, size_t(wse) * 4 + 256));
+    CORU_TRY(gemm<float>(c, o, A, lda, X, ldx, C, ldc, rows, K, int(N), reinterpret_cast<float*>(c->arena), wse));
     CORU_CUDA(cudaStreamSynchronize(c->stream));
     return CORU_OK;
 }

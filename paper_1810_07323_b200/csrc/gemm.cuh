@@ -23,4 +23,8 @@ cudaError_t gemm_f64(Op op, const double* A, int64_t lda, const double* X, int64
                      int64_t ldc, int64_t Mo, int64_t K, int N, const GemmPlan& plan, double* ws,
                      cudaStream_t stream);
 
+GemmPlan plan_gemm_f32(Op op, int64_t Mo, int64_t K, int N, int num_sms);
+cudaError_t gemm_f32(Op op, const float* A, int64_t lda, const float* X, int64_t ldx, float* C, int64_t ldc,
+                     int64_t Mo, int64_t K, int N, const GemmPlan& plan, float* ws, cudaStream_t stream);
+
 }  // namespace coru_gpu

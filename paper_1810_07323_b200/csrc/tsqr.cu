@@ -418,19 +418,166 @@ __global__ void __launch_bounds__(kBThreads, 1)
         Rout[(int64_t(b) * d + r) * ldr + c] = (r <= c) ? W[c * ldw + r] : T(0);
     }
     for (int c = tid; c < d; c += kBThreads) betas[int64_t(b) * d + c] = S.beta[c];
+    // explicit reflectors (0 above the diagonal, 1 on it) for the Q kernel
     T* Vb = V + int64_t(b) * d * ldv;
     for (int c = warp; c < d; c += kBThreads / 32)
-        for (int r = lane; r < rb; r += 32) Vb[int64_t(c) * ldv + r] = W[c * ldw + r];
+        for (int r = lane; r < rb; r += 32) Vb[int64_t(c) * ldv + r] = r > c ? W[c * ldw + r] : T(r == c ? 1 : 0);
+}
+
+// Same algorithm with the working block in global memory (L2) — blocks too tall or too wide for
+// shared memory (wide sketches, e.g. d = 220 fp64 or d = 520 fp32). The panel columns are
+// updated in place in L2 (four independent loads in flight per lane), the panel reflectors and
+// all small factors stay in shared memory, and the trailing update is the same three CTA GEMMs.
+template <typename T>
+struct BigSmem {
+    int ldvp;
+    T *Vp, *beta, *Gp, *Tp, *Y, *Z, *scratch;
+    __device__ BigSmem(unsigned char* raw, int d, int rb) : ldvp(ld_mod(rb, 8)) {
+        T* p = reinterpret_cast<T*>(raw);
+        Vp = p;
+        p += size_t(kNB) * ldvp;
+        beta = p;
+        p += d + (d & 1);
+        Gp = p;
+        p += kNB * kNB;
+        Tp = p;
+        p += kNB * kNB;
+        Y = p;
+        p += size_t(kNB) * d;
+        Z = p;
+        p += size_t(kNB) * d;
+        scratch = p;
+    }
+    static size_t bytes(int d, int rb, size_t eb) {
+        return (size_t(kNB) * ld_mod(rb, 8) + d + (d & 1) + 2 * kNB * kNB + 2 * size_t(kNB) * d + kGemmScratch) * eb;
+    }
+};
+
+template <typename T>
+__global__ void __launch_bounds__(kBThreads, 1)
+    k_qr_blocked_g(const T* __restrict__ X, int64_t ldx, int64_t rows, int nb, int d, T* __restrict__ V, int ldv,
+                   T* __restrict__ betas, T* __restrict__ Tg, T* __restrict__ Rout, int ldr) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int b = blockIdx.x;
+    const int64_t r0 = rows * b / nb, r1 = rows * (b + 1) / nb;
+    const int rb = int(r1 - r0);
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    BigSmem<T> S(smem_raw, d, rb);
+    const int ldvp = S.ldvp;
+    T* W = V + int64_t(b) * d * ldv;  // column-major working block (ld = ldv) in global memory
+    T* Tb = Tg + int64_t(b) * npanels(d) * kNB * kNB;
+    for (int cb = 0; cb < d; cb += 128)
+        for (int r = warp * 4; r < rb; r += (kBThreads / 32) * 4) {
+            T v[4][4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+#pragma unroll
+                for (int h = 0; h < 4; ++h) {
+                    const int c = cb + lane + 32 * h;
+                    v[q][h] = (r + q < rb && c < d) ? X[(r0 + r + q) * ldx + c] : T(0);
+                }
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+#pragma unroll
+                for (int h = 0; h < 4; ++h) {
+                    const int c = cb + lane + 32 * h;
+                    if (r + q < rb && c < d) W[int64_t(c) * ldv + r + q] = v[q][h];
+                }
+        }
+    __syncthreads();
+
+    for (int p0 = 0, pi = 0; p0 < d; p0 += kNB, ++pi) {
+        const int nbp = min(kNB, d - p0);
+        if (warp < nbp) {
+            const int c = p0 + warp;
+            T* col = W + int64_t(c) * ldv;
+            for (int jj = 0; jj <= warp; ++jj) {
+                const int j = p0 + jj;
+                const int bar = 1 + jj, cnt = 32 * (nbp - jj);
+                if (jj < warp) {
+                    named_bar_sync(bar, cnt);
+                    const T bj = S.beta[j];
+                    if (bj == T(0)) continue;
+                    const T* vj = S.Vp + jj * ldvp;
+                    T s0 = 0, s1 = 0, s2 = 0, s3 = 0;
+                    int i = j + lane;
+                    for (; i + 96 < rb; i += 128) {
+                        s0 += vj[i] * col[i];
+                        s1 += vj[i + 32] * col[i + 32];
+                        s2 += vj[i + 64] * col[i + 64];
+                        s3 += vj[i + 96] * col[i + 96];
+                    }
+                    for (; i < rb; i += 32) s0 += vj[i] * col[i];
+                    const T s = warp_sum((s0 + s1) + (s2 + s3)) * bj;
+                    for (int i2 = j + lane; i2 < rb; i2 += 32) col[i2] -= s * vj[i2];
+                    __syncwarp();
+                } else {
+                    T q0 = 0, q1 = 0;
+                    int i = j + 1 + lane;
+                    for (; i + 32 < rb; i += 64) {
+                        q0 += col[i] * col[i];
+                        q1 += col[i + 32] * col[i + 32];
+                    }
+                    for (; i < rb; i += 32) q0 += col[i] * col[i];
+                    const T sig = warp_sum(q0 + q1);
+                    const T x0 = col[j];
+                    T bj = 0;
+                    if (sig != T(0)) {
+                        const T mu = tsqrt(x0 * x0 + sig);
+                        const T v0 = (x0 <= T(0)) ? x0 - mu : -sig / (x0 + mu);
+                        bj = T(2) * v0 * v0 / (sig + v0 * v0);
+                        const T rv = T(1) / v0;
+                        for (int i2 = j + 1 + lane; i2 < rb; i2 += 32) col[i2] *= rv;
+                        __syncwarp();
+                        if (lane == 0) col[j] = mu;
+                    }
+                    __syncwarp();
+                    T* vj = S.Vp + jj * ldvp;
+                    for (int i2 = lane; i2 < ldvp; i2 += 32)
+                        vj[i2] = (i2 > j && i2 < rb) ? col[i2] : T(i2 == j ? 1 : 0);
+                    if (lane == 0) S.beta[j] = bj;
+                    __threadfence_block();
+                    if (jj + 1 < nbp) named_bar_arrive(bar, cnt);
+                }
+            }
+        }
+        __syncthreads();
+        const int K = rb - p0;
+        cta_mm(nbp, nbp, K, S.Vp + p0, ldvp, 1, S.Vp + p0, 1, ldvp, S.Gp, kNB, 1, T(1), false, S.scratch, kGemmScratch);
+        __syncthreads();
+        if (warp == 0) {
+            warp_larft<T>(nbp, S.Gp, kNB, S.beta + p0, S.Tp, kNB);
+            T* Tpg = Tb + pi * kNB * kNB;
+            for (int e = lane; e < kNB * kNB; e += 32) Tpg[e] = S.Tp[e];
+        }
+        __syncthreads();
+        const int c0 = p0 + nbp, nc = d - c0;
+        if (nc > 0) {
+            T* C = W + int64_t(c0) * ldv + p0;
+            cta_mm(nbp, nc, K, S.Vp + p0, ldvp, 1, C, 1, ldv, S.Y, d, 1, T(1), false, S.scratch, kGemmScratch);
+            __syncthreads();
+            cta_mm(nbp, nc, nbp, S.Tp, 1, kNB, S.Y, d, 1, S.Z, d, 1, T(1), false, S.scratch, kGemmScratch);
+            __syncthreads();
+            cta_mm(K, nc, nbp, S.Vp + p0, 1, ldvp, S.Z, d, 1, C, 1, ldv, T(-1), true, S.scratch, kGemmScratch);
+            __syncthreads();
+        }
+    }
+    for (int e = tid; e < d * d; e += kBThreads) {
+        const int r = e / d, c = e % d;
+        Rout[(int64_t(b) * d + r) * ldr + c] = (r <= c) ? W[int64_t(c) * ldv + r] : T(0);
+    }
+    for (int c = tid; c < d; c += kBThreads) betas[int64_t(b) * d + c] = S.beta[c];
+    __syncthreads();
+    for (int c = warp; c < d; c += kBThreads / 32)  // explicit reflectors in place
+        for (int r = lane; r <= c && r < rb; r += 32) W[int64_t(c) * ldv + r] = T(r == c ? 1 : 0);
 }
 
 template <typename T>
 struct FormQSmem {
     int ldvs, lde;
     T *Vs, *E, *Y, *Z, *Tp, *scratch;
-    __device__ FormQSmem(unsigned char* raw, int d, int rb) : ldvs(ld_mod(rb, 8)), lde(ld_mod(rb, 4)) {
+    __device__ FormQSmem(unsigned char* raw, int d, int rb, bool stage) : ldvs(ld_mod(rb, 8)), lde(ld_mod(rb, 4)) {
         T* p = reinterpret_cast<T*>(raw);
-        Vs = p;
-        p += size_t(d) * ldvs;
         E = p;
         p += size_t(kQChunk) * lde;
         Y = p;
@@ -440,10 +587,12 @@ struct FormQSmem {
         Tp = p;
         p += kNB * kNB;
         scratch = p;
+        p += kGemmScratch;
+        Vs = stage ? p : nullptr;
     }
-    static size_t bytes(int d, int rb, size_t eb) {
-        return (size_t(d) * ld_mod(rb, 8) + size_t(kQChunk) * ld_mod(rb, 4) + 2 * kNB * kQChunk + kNB * kNB +
-                kGemmScratch) *
+    static size_t bytes(int d, int rb, size_t eb, bool stage) {
+        return (size_t(kQChunk) * ld_mod(rb, 4) + 2 * kNB * kQChunk + kNB * kNB + kGemmScratch +
+                (stage ? size_t(d) * ld_mod(rb, 8) : 0)) *
                eb;
     }
 };
@@ -451,50 +600,50 @@ struct FormQSmem {
 // Q block b = H_0 ... H_{d-1} [Qin_b; 0]  (Qin null => identity), by panels in reverse:
 //   E <- E - V_p (T_p (V_p^T E)),  p = P-1 ... 0. Columns of Q are independent, so each CTA
 //   forms one kQChunk-wide column chunk (grid = blocks x chunks) to spread a level over more SMs.
+//   V is the explicit reflector matrix (column-major, ldv), staged in shared memory when it fits.
 template <typename T>
 __global__ void __launch_bounds__(kBThreads, 1)
     k_qr_blocked_form_q(const T* __restrict__ Qin, int ldqin, int64_t rows, int nb, int d, const T* __restrict__ V,
-                        int ldv, const T* __restrict__ Tg, T* __restrict__ Qout, int64_t ldqout) {
+                        int ldv, const T* __restrict__ Tg, T* __restrict__ Qout, int64_t ldqout, int stage) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int b = blockIdx.x;
     const int64_t r0 = rows * b / nb, r1 = rows * (b + 1) / nb;
     const int rb = int(r1 - r0);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    FormQSmem<T> S(smem_raw, d, rb);
+    FormQSmem<T> S(smem_raw, d, rb, stage != 0);
     const T* Vb = V + int64_t(b) * d * ldv;
     const T* Tb = Tg + int64_t(b) * npanels(d) * kNB * kNB;
     const T* Qb = Qin ? Qin + int64_t(b) * d * ldqin : nullptr;
-    // explicit reflectors (0 above the diagonal, 1 on it) staged column-major
-    for (int c = warp; c < d; c += kBThreads / 32)
-        for (int r = lane; r < S.ldvs; r += 32)
-            S.Vs[c * S.ldvs + r] = (r > c && r < rb) ? Vb[int64_t(c) * ldv + r] : T(r == c ? 1 : 0);
-    {
-        const int q0 = blockIdx.y * kQChunk;  // this CTA's column chunk of Q
-        const int nq = min(kQChunk, d - q0);
-        for (int e = tid; e < nq * rb; e += kBThreads) {
-            const int j = e / rb, i = e % rb;
-            S.E[j * S.lde + i] = i < d ? (Qb ? Qb[i * ldqin + q0 + j] : T(i == q0 + j ? 1 : 0)) : T(0);
-        }
+    const T* Vx = Vb;
+    int ldx = ldv;
+    if (stage) {
+        for (int c = warp; c < d; c += kBThreads / 32)
+            for (int r = lane; r < rb; r += 32) S.Vs[c * S.ldvs + r] = Vb[int64_t(c) * ldv + r];
+        Vx = S.Vs;
+        ldx = S.ldvs;
+    }
+    const int q0 = blockIdx.y * kQChunk;  // this CTA's column chunk of Q
+    const int nq = min(kQChunk, d - q0);
+    for (int e = tid; e < nq * rb; e += kBThreads) {
+        const int j = e / rb, i = e % rb;
+        S.E[j * S.lde + i] = i < d ? (Qb ? Qb[i * ldqin + q0 + j] : T(i == q0 + j ? 1 : 0)) : T(0);
+    }
+    __syncthreads();
+    for (int pi = npanels(d) - 1; pi >= 0; --pi) {
+        const int p0 = pi * kNB, nbp = min(kNB, d - p0), K = rb - p0;
+        const T* Vp = Vx + p0 * ldx + p0;  // V_p rows >= p0
+        if (tid < kNB * kNB) S.Tp[tid] = Tb[pi * kNB * kNB + tid];
+        cta_mm(nbp, nq, K, Vp, ldx, 1, S.E + p0, 1, S.lde, S.Y, kQChunk, 1, T(1), false, S.scratch, kGemmScratch);
         __syncthreads();
-        for (int pi = npanels(d) - 1; pi >= 0; --pi) {
-            const int p0 = pi * kNB, nbp = min(kNB, d - p0), K = rb - p0;
-            const T* Vp = S.Vs + p0 * S.ldvs + p0;  // V_p rows >= p0
-            if (tid < kNB * kNB) S.Tp[tid] = Tb[pi * kNB * kNB + tid];
-            cta_mm(nbp, nq, K, Vp, S.ldvs, 1, S.E + p0, 1, S.lde, S.Y, kQChunk, 1, T(1), false, S.scratch,
-                   kGemmScratch);
-            __syncthreads();
-            cta_mm(nbp, nq, nbp, S.Tp, kNB, 1, S.Y, kQChunk, 1, S.Z, kQChunk, 1, T(1), false, S.scratch,
-                   kGemmScratch);
-            __syncthreads();
-            cta_mm(K, nq, nbp, Vp, 1, S.ldvs, S.Z, kQChunk, 1, S.E + p0, 1, S.lde, T(-1), true, S.scratch,
-                   kGemmScratch);
-            __syncthreads();
-        }
-        T* Qo = Qout + r0 * ldqout + q0;
-        for (int e = tid; e < nq * rb; e += kBThreads) {
-            const int i = e / nq, j = e % nq;
-            Qo[int64_t(i) * ldqout + j] = S.E[j * S.lde + i];
-        }
+        cta_mm(nbp, nq, nbp, S.Tp, kNB, 1, S.Y, kQChunk, 1, S.Z, kQChunk, 1, T(1), false, S.scratch, kGemmScratch);
+        __syncthreads();
+        cta_mm(K, nq, nbp, Vp, 1, ldx, S.Z, kQChunk, 1, S.E + p0, 1, S.lde, T(-1), true, S.scratch, kGemmScratch);
+        __syncthreads();
+    }
+    T* Qo = Qout + r0 * ldqout + q0;
+    for (int e = tid; e < nq * rb; e += kBThreads) {
+        const int i = e / nq, j = e % nq;
+        Qo[int64_t(i) * ldqout + j] = S.E[j * S.lde + i];
     }
 }
 
@@ -510,24 +659,27 @@ TsqrPlan plan_tsqr(int64_t m, int d, size_t eb, int max_smem) {
     p.m = m;
     p.d = d;
     p.elem_bytes = eb;
-    // Largest block the blocked kernels take (<= 256 rows, both kernels' working sets in smem).
+    const size_t cap = size_t(max_smem);
+    // Largest block for the shared-memory blocked kernels (<= 256 rows, register panels).
     int rb_blocked = 0;
     for (int rb = kMaxRowsBlocked; rb > d; --rb)
-        if (BlockedSmem<double>::bytes(d, rb, eb) <= size_t(max_smem) &&
-            FormQSmem<double>::bytes(d, rb, eb) <= size_t(max_smem)) {
+        if (BlockedSmem<double>::bytes(d, rb, eb) <= cap && FormQSmem<double>::bytes(d, rb, eb, true) <= cap) {
             rb_blocked = rb;
             break;
         }
-    // Largest block the unblocked kernels hold in smem (else they work in L2).
-    int rb_wide = 0;
-    for (int rb = 2048; rb > d; --rb)
-        if (wide_factor_smem_bytes(rb, d, eb) <= size_t(max_smem)) {
-            rb_wide = rb;
+    // Largest block for the global-working-set blocked kernels (panel reflectors + Q chunk in smem).
+    int rb_big = 0;
+    for (int rb = 4096; rb > d; --rb)
+        if (BigSmem<double>::bytes(d, rb, eb) <= cap && FormQSmem<double>::bytes(d, rb, eb, false) <= cap) {
+            rb_big = rb;
             break;
         }
     const bool blocked_ok = rb_blocked >= d + 1 + d / 4;  // at least a 1.25x reduction per level
-    const int target = blocked_ok ? rb_blocked : (rb_wide >= 2 * d + 2 ? std::min(rb_wide, std::max(4 * d, 256))
-                                                                           : std::max(4 * d, 256));
+    const bool big_ok = rb_big >= 2 * d + 2;
+    int target;
+    if (blocked_ok) target = rb_blocked;
+    else if (big_ok) target = std::min(rb_big, std::max(4 * d, 1024));
+    else target = std::max(4 * d, 256);
     int64_t rows = m;
     int64_t voff = 0, boff = 0, roff = 0, toff = 0;
     for (;;) {
@@ -538,8 +690,16 @@ TsqrPlan plan_tsqr(int64_t m, int d, size_t eb, int max_smem) {
         nb = std::max<int64_t>(1, std::min<int64_t>(nb, rows / (d + 1)));
         L.nb = int(nb);
         L.rbmax = int((rows + nb - 1) / nb);
-        L.blocked = blocked_ok && L.rbmax <= rb_blocked;
-        L.smem = L.blocked || wide_factor_smem_bytes(L.rbmax, d, eb) <= size_t(max_smem);
+        if (blocked_ok && L.rbmax <= rb_blocked) {
+            L.kind = TsqrLevel::kBlockedSmem;
+        } else if (rb_big > d && L.rbmax <= rb_big) {
+            L.kind = TsqrLevel::kBlockedGlobal;
+        } else {
+            L.kind = TsqrLevel::kWide;
+        }
+        L.blocked = L.kind != TsqrLevel::kWide;
+        L.smem = L.kind == TsqrLevel::kBlockedSmem ||
+                 (L.kind == TsqrLevel::kWide && wide_factor_smem_bytes(L.rbmax, d, eb) <= cap);
         L.ldv = L.rbmax + (L.rbmax % 2);
         L.v_off = voff;
         L.beta_off = boff;
@@ -558,6 +718,7 @@ TsqrPlan plan_tsqr(int64_t m, int d, size_t eb, int max_smem) {
     p.beta_elems = boff;
     p.r_elems = roff;
     p.t_elems = toff;
+    p.max_smem = max_smem;
     return p;
 }
 
@@ -580,11 +741,16 @@ cudaError_t tsqr_factor(const TsqrPlan& p, const T* B, int64_t ldb, T* V, T* bet
     for (size_t l = 0; l < p.levels.size(); ++l) {
         const TsqrLevel& L = p.levels[l];
         T* Rl = (l + 1 == p.levels.size()) ? r_out : R + L.r_off;
-        if (L.blocked) {
+        if (L.kind == TsqrLevel::kBlockedSmem) {
             const size_t sm = BlockedSmem<T>::bytes(d, L.rbmax, sizeof(T));
             cudaFuncSetAttribute(k_qr_blocked<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
             k_qr_blocked<T><<<L.nb, kBThreads, sm, st>>>(X, ldx, L.rows, L.nb, d, V + L.v_off, L.ldv,
                                                           beta + L.beta_off, Tarena + L.t_off, Rl, d);
+        } else if (L.kind == TsqrLevel::kBlockedGlobal) {
+            const size_t sm = BigSmem<T>::bytes(d, L.rbmax, sizeof(T));
+            cudaFuncSetAttribute(k_qr_blocked_g<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
+            k_qr_blocked_g<T><<<L.nb, kBThreads, sm, st>>>(X, ldx, L.rows, L.nb, d, V + L.v_off, L.ldv,
+                                                            beta + L.beta_off, Tarena + L.t_off, Rl, d);
         } else {
             const size_t sm = L.smem ? wide_factor_smem_bytes(L.rbmax, d, sizeof(T)) : wide_factor_smem_bytes(0, d, sizeof(T));
             cudaFuncSetAttribute(k_hh_factor<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
@@ -619,11 +785,12 @@ cudaError_t tsqr_form_q(const TsqrPlan& p, const T* q_top, T* V, T* beta, T* Tar
         T* out = (l == 0) ? Q : ((p.levels.size() - 1 - size_t(l)) % 2 == 0 ? ping : pong);
         const int64_t ldo = (l == 0) ? ldq : d;
         if (L.blocked) {
-            const size_t sm = FormQSmem<T>::bytes(d, L.rbmax, sizeof(T));
+            const bool stage = FormQSmem<T>::bytes(d, L.rbmax, sizeof(T), true) <= size_t(max_smem);
+            const size_t sm = FormQSmem<T>::bytes(d, L.rbmax, sizeof(T), stage);
             cudaFuncSetAttribute(k_qr_blocked_form_q<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
             const dim3 grid(unsigned(L.nb), unsigned((d + kQChunk - 1) / kQChunk));
             k_qr_blocked_form_q<T><<<grid, kBThreads, sm, st>>>(qin, ldqin, L.rows, L.nb, d, V + L.v_off, L.ldv,
-                                                                 Tarena + L.t_off, out, ldo);
+                                                                 Tarena + L.t_off, out, ldo, stage ? 1 : 0);
         } else {
             const size_t sm = L.smem ? size_t(L.rbmax | 1) * d * sizeof(T) : 0;
             cudaFuncSetAttribute(k_hh_form_q<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));

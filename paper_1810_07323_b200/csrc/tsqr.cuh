@@ -17,6 +17,8 @@ struct TsqrLevel {
     int64_t beta_off = 0;  // offset of the betas
     int64_t r_off = 0;     // offset of the stacked R (nb*d x d, ld = d) output in the R arena
     int64_t t_off = 0;     // offset of the per-block compact-WY T factors (blocked path)
+    enum Kind { kBlockedSmem = 0, kBlockedGlobal = 1, kWide = 2 };
+    Kind kind = kBlockedSmem;  // which kernel pair factors / forms Q for this level
     bool blocked = false;  // panel-blocked compact-WY kernels (else the unblocked column pipeline)
     bool smem = true;      // working block lives in shared memory (else in the V arena, L2)
 };
@@ -27,6 +29,7 @@ struct TsqrPlan {
     std::vector<TsqrLevel> levels;
     bool blocked = false;  // level 0 uses the blocked kernels
     int64_t v_elems = 0, beta_elems = 0, r_elems = 0, t_elems = 0;
+    int max_smem = 0;
     size_t elem_bytes = 8;
 };
 

@@ -182,3 +182,26 @@ def test_cpp_wrapper_program(ctx):
         subprocess.run(["make", "-C", os.path.join(here, "cpp")], check=True)
     r = subprocess.run([exe], capture_output=True, text=True, timeout=300)
     assert r.returncode == 0, r.stdout + r.stderr
+
+
+@pytest.mark.parametrize("name,m,n", [("C1", 1000, 1000), ("C5", 3000, 3000)])
+def test_fp32_parity_vs_fp32_oracle(ctx, oracle, name, m, n):
+    """fp32 path against the fp32 restatement of the reference: relative
+    reconstruction error to 1e-4, |diag T| to 1e-3 (BASELINE.json north_star, fp32)."""
+    import paper_1810_07323_b200 as cg
+    from workloads import CONFIGS, make_host
+    c = CONFIGS[name]
+    d, q = (c.d, c.q) if name == "C1" else (104, 2)
+    a = make_host(name, m, n).astype(np.float32)
+    f = cg.corutv(a, d, q, seed=cg.RngSeed(42, 0), ctx=ctx)
+    o = oracle.corutv(a, d, q, seed=42, threads=16)
+    a64 = a.astype(np.float64)
+    e_gpu = rel_recon_error(a64, f.u.astype(np.float64), f.t.astype(np.float64), f.v.astype(np.float64))
+    e_ora = rel_recon_error(a64, o.u.astype(np.float64), o.t.astype(np.float64), o.v.astype(np.float64))
+    dg = np.abs(np.abs(np.diag(f.t)).astype(np.float64) - np.abs(np.diag(o.t)).astype(np.float64))
+    _record(f"fp32_{name}_{m}x{n}", err_gpu=e_gpu, err_oracle=e_ora, rel_err_diff=abs(e_gpu - e_ora) / e_ora,
+            diag_absdiff=dg.max(), orth_u=orth_residual(f.u.astype(np.float64)),
+            orth_v=orth_residual(f.v.astype(np.float64)))
+    assert abs(e_gpu - e_ora) <= 1e-4 * e_ora
+    assert dg.max() <= 1e-3
+    assert np.all(np.tril(f.t, -1) == 0.0)

@@ -99,3 +99,19 @@ def test_qrcp_matches_oracle(ctx, oracle, n, seed):
     assert orth_residual(q) <= 1e-12 * n
     # sign convention: the last diagonal keeps its sign (no reflector when sigma == 0, qr.hpp:37)
     assert np.sign(r[-1, -1]) == np.sign(ro[-1, -1])
+
+
+@pytest.mark.parametrize("m,n,d,op", [(1000, 1000, 25, 0), (1000, 1000, 25, 1), (4097, 3001, 130, 0),
+                                      (4097, 3001, 130, 1), (300, 5000, 520, 0), (5000, 300, 520, 1)])
+def test_gemm_f32_matches_oracle(ctx, oracle, m, n, d, op):
+    """fp32 A-pass: exact fp32 FMA accumulation; bound |C - C_ref| <= K·2^-23·(|A||X|) (fp32 unit
+    roundoff times the reduction length, the standard forward error bound of a dot product)."""
+    import paper_1810_07323_b200 as cg
+    rng = np.random.default_rng(m + n + d + op)
+    a = rng.standard_normal((m, n)).astype(np.float32)
+    x = rng.standard_normal((m if op else n, d)).astype(np.float32)
+    c = cg.gemm(_t(a), _t(x), op=op, ctx=ctx).cpu().numpy()
+    want = oracle.matmul(a, x) if op == 0 else oracle.matmul_tn(a, x)
+    K = n if op == 0 else m
+    bound = ((np.abs(a) @ np.abs(x)) if op == 0 else (np.abs(a).T @ np.abs(x))).astype(np.float64)
+    assert np.all(np.abs(c.astype(np.float64) - want) <= K * 2.0 ** -23 * bound + 1e-30)
