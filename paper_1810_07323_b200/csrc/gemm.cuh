@@ -13,8 +13,10 @@ namespace coru_gpu {
 enum class Op { N = 0, T = 1 };
 
 struct GemmPlan {
-    int bm = 0, bn = 0, splits = 1;
-    int64_t ws_elems = 0;  // workspace (partials) needed, in elements
+    int bm = 0, bn = 0, splits = 1;  // fp64: splits = stream-K CTA count
+    int max_seg = 1;                 // fp64 stream-K: max CTAs sharing one tile
+    bool fixup = false;              // fp64 stream-K: some tile is split across CTAs
+    int64_t ws_elems = 0;            // workspace (partials) needed, in elements
 };
 
 GemmPlan plan_gemm_f64(Op op, int64_t Mo, int64_t K, int N, int num_sms);

@@ -16,10 +16,20 @@
 
 namespace coru_gpu {
 
+#ifdef CORU_QRCP_PROFILE
+__device__ long long g_qrcp_phase[4];  // cycles: phase A, phase B, Q formation, total
+#define QPROF_T(v) long long v = clock64()
+#define QPROF_ADD(i, t0) if (threadIdx.x == 0) g_qrcp_phase[i] += clock64() - (t0)
+#else
+#define QPROF_T(v)
+#define QPROF_ADD(i, t0)
+#endif
+
 namespace {
 
 constexpr int kThreads = 1024;
 constexpr int kG = 8;  // lanes per column group in the trailing update
+constexpr int kQRPL = 8;  // Q_M rows per lane in the register path (d <= 256)
 constexpr int kWarps = kThreads / 32;
 constexpr int kQrcpGemmScratch = 4096;
 
@@ -67,6 +77,35 @@ __device__ __forceinline__ T group_sumsq(const T* col, int lo, int hi, int gl) {
     return group_sum(s);
 }
 
+template <typename T, int RPL>
+__device__ __forceinline__ void q_columns(const T* W, int ldw, const T* beta, int d, T* Q, int ldq, int warp, int lane) {
+    for (int c = warp; c < d; c += kWarps) {
+        T q[RPL];
+#pragma unroll
+        for (int u = 0; u < RPL; ++u) q[u] = T(lane + 32 * u == c ? 1 : 0);
+        for (int j = d - 1; j >= 0; --j) {
+            const T bj = beta[j];
+            if (bj == T(0)) continue;
+            T v[RPL];
+            T s = 0;
+#pragma unroll
+            for (int u = 0; u < RPL; ++u) {
+                const int i = lane + 32 * u;
+                v[u] = i > j && i < d ? W[j * ldw + i] : T(i == j ? 1 : 0);
+                s += v[u] * q[u];
+            }
+            s = warp_sum(s) * bj;
+#pragma unroll
+            for (int u = 0; u < RPL; ++u) q[u] -= s * v[u];
+        }
+#pragma unroll
+        for (int u = 0; u < RPL; ++u) {
+            const int i = lane + 32 * u;
+            if (i < d) Q[i * ldq + c] = q[u];
+        }
+    }
+}
+
 template <typename T>
 __global__ void __launch_bounds__(kThreads) k_qrcp(const T* __restrict__ M, int ldm, int d, T* __restrict__ Q, int ldq,
                                                    T* __restrict__ Tout, int ldt, int64_t* __restrict__ perm_out,
@@ -96,7 +135,9 @@ __global__ void __launch_bounds__(kThreads) k_qrcp(const T* __restrict__ M, int 
         if (c < d && gl == 0) colsq[c] = base[c] = s;
     }
     __syncthreads();
+    QPROF_T(t_all);
     for (int j = 0; j < d; ++j) {
+        QPROF_T(t_a);
         // ---- phase A (warp 0): pivot, swap, reflector ----
         if (warp == 0) {
             // argmax with lowest-index ties (qr.hpp:121-123): each lane keeps the first maximum
@@ -143,6 +184,8 @@ __global__ void __launch_bounds__(kThreads) k_qrcp(const T* __restrict__ M, int 
             if (lane == 0) beta[j] = b;
         }
         __syncthreads();
+        QPROF_ADD(0, t_a);
+        QPROF_T(t_b);
         // ---- phase B (column groups): trailing update + downdate (qr.hpp:131-139) ----
         const T bj = beta[j];
         const T* vcol = W + j * ldw;
@@ -154,9 +197,14 @@ __global__ void __launch_bounds__(kThreads) k_qrcp(const T* __restrict__ M, int 
             const bool act = c < d;
             T* col = W + (act ? c : j) * ldw;
             if (bj != T(0)) {
-                T s = 0;
-                for (int i = j + 1 + gl; i < d; i += kG) s += vcol[i] * col[i];
-                s = group_sum(s);
+                T s0 = 0, s1 = 0;
+                int i = j + 1 + gl;
+                for (; i + kG < d; i += 2 * kG) {
+                    s0 += vcol[i] * col[i];
+                    s1 += vcol[i + kG] * col[i + kG];
+                }
+                if (i < d) s0 += vcol[i] * col[i];
+                T s = group_sum(s0 + s1);
                 s += col[j];
                 s *= bj;
                 if (act) {
@@ -175,7 +223,9 @@ __global__ void __launch_bounds__(kThreads) k_qrcp(const T* __restrict__ M, int 
             if (act && !need && gl == 0) colsq[c] = cs;
         }
         __syncthreads();
+        QPROF_ADD(1, t_b);
     }
+    QPROF_T(t_q);
     // T = upper triangle (qr.hpp:74-79), perm out.
     for (int e = tid; e < d * d; e += kThreads) {
         const int r = e / d, c = e % d;
@@ -183,6 +233,18 @@ __global__ void __launch_bounds__(kThreads) k_qrcp(const T* __restrict__ M, int 
     }
     for (int c = tid; c < d; c += kThreads) perm_out[c] = perm[c];
     __syncthreads();
+    if (d <= 64) {
+        // Q_M = H_0 ... H_{d-1} I exactly in accumulate_q's order (qr.hpp:60-72): every column of
+        // Q is independent, so warp w carries columns w, w+32, ... in registers (RPL = ceil(d/32)
+        // rows per lane) through the d reflectors; the reflectors are read from W.
+        if (d <= 32) q_columns<T, 1>(W, ldw, beta, d, Q, ldq, warp, lane);
+        else if (d <= 64) q_columns<T, 2>(W, ldw, beta, d, Q, ldq, warp, lane);
+        else if (d <= 128) q_columns<T, 4>(W, ldw, beta, d, Q, ldq, warp, lane);
+        else q_columns<T, 8>(W, ldw, beta, d, Q, ldq, warp, lane);
+        QPROF_ADD(2, t_q);
+        QPROF_ADD(3, t_all);
+        return;
+    }
     // Q_M = H_0 ... H_{d-1} I (accumulate_q, qr.hpp:60-72) by 16-column panels in reverse,
     // E <- E - V_p T_p (V_p^T E) with each panel's compact-WY T_p (DMMA CTA GEMMs).
     const int ldx = qrcp_ldx(d);
@@ -210,6 +272,8 @@ __global__ void __launch_bounds__(kThreads) k_qrcp(const T* __restrict__ M, int 
         cta_mm(K, d, nbp, Vp, 1, ldx, Z, d, 1, Q + p0 * ldq, ldq, 1, T(-1), true, gs, kQrcpGemmScratch);
         __syncthreads();
     }
+    QPROF_ADD(2, t_q);
+    QPROF_ADD(3, t_all);
 }
 
 template <typename T>
