@@ -69,6 +69,13 @@ int coru_ctx_set_host_threads(coru_ctx* ctx, int threads);
  * calls coru_ctx_init_comm. NCCL is loaded at run time (libnccl.so.2). */
 int coru_comm_unique_id(unsigned char id[128]);
 int coru_ctx_init_comm(coru_ctx* ctx, int rank, int world, const unsigned char id[128]);
+/* In-process alternative to NCCL: ranks are host threads of one process (one context each, on one
+ * GPU or on peer-accessible GPUs); collectives are a stream sync + host barrier + fixed-order
+ * device sum, deterministic and identical on every rank. */
+typedef struct coru_threadcomm coru_threadcomm;
+coru_threadcomm* coru_threadcomm_create(int world);
+void coru_threadcomm_destroy(coru_threadcomm* group);
+int coru_ctx_init_threadcomm(coru_ctx* ctx, coru_threadcomm* group, int rank);
 /* Rows [*row0, *row0 + *rows) of an m-row matrix belong to `rank` of `world`. */
 void coru_shard_rows(int64_t m, int rank, int world, int64_t* row0, int64_t* rows);
 

@@ -140,6 +140,11 @@ def load_library():
     L.coru_ctx_set_profiling.argtypes = [p, i32]
     L.coru_ctx_profile_apass.argtypes = [p, C.POINTER(C.c_double), C.POINTER(i64), C.POINTER(C.c_double),
                                          C.POINTER(C.c_double)]
+    L.coru_threadcomm_create.argtypes = [i32]
+    L.coru_threadcomm_create.restype = p
+    L.coru_threadcomm_destroy.argtypes = [p]
+    L.coru_threadcomm_destroy.restype = None
+    L.coru_ctx_init_threadcomm.argtypes = [p, p, i32]
     L.coru_shard_rows.argtypes = [i64, i32, i32, C.POINTER(i64), C.POINTER(i64)]
     L.coru_shard_rows.restype = None
     for sfx in ("f64", "f32"):
@@ -226,10 +231,37 @@ class Context:
         _check(load_library().coru_comm_unique_id(buf))
         return bytes(buf)
 
+    def init_threadcomm(self, group: "ThreadGroup", rank: int):
+        """Join an in-process collective group (ranks = host threads, one context each)."""
+        _check(self.lib.coru_ctx_init_threadcomm(self.h, group.h, rank))
+        self.rank, self.world = rank, group.world
+
     def init_comm(self, rank: int, world: int, uid: bytes):
         buf = (C.c_ubyte * 128).from_buffer_copy(uid)
         _check(self.lib.coru_ctx_init_comm(self.h, rank, world, buf))
         self.rank, self.world = rank, world
+
+
+class ThreadGroup:
+    """coru_threadcomm: the in-process alternative to NCCL for row-sharded decompositions."""
+
+    def __init__(self, world: int):
+        self.lib = load_library()
+        self.world = world
+        self.h = self.lib.coru_threadcomm_create(world)
+        if not self.h:
+            raise CoruInvalidArgument("world must be >= 1")
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.lib.coru_threadcomm_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
 
 _default_ctx: dict[int, Context] = {}

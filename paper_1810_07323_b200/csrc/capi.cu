@@ -17,6 +17,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstring>
+#include <condition_variable>
 #include <mutex>
 #include <string>
 #include <thread>
@@ -124,6 +125,38 @@ struct Carver {
 
 }  // namespace
 
+// In-process collective group: ranks are host threads (each with its own context, on one GPU or
+// on peer-accessible GPUs). A collective = stream sync + host barrier + fixed-order device sum /
+// copies, so it is deterministic and no kernel ever waits on another kernel.
+struct coru_threadcomm {
+    int world = 1;
+    std::mutex mu;
+    std::condition_variable cv;
+    int arrived = 0;
+    uint64_t generation = 0;
+    std::vector<const void*> slots;
+    bool failed = false;  // a rank failed: every pending and future barrier returns false
+    explicit coru_threadcomm(int w) : world(w), slots(size_t(w), nullptr) {}
+    bool barrier() {
+        std::unique_lock<std::mutex> lk(mu);
+        if (failed) return false;
+        const uint64_t gen = generation;
+        if (++arrived == world) {
+            arrived = 0;
+            ++generation;
+            cv.notify_all();
+        } else {
+            cv.wait(lk, [&] { return generation != gen || failed; });
+        }
+        return !failed;
+    }
+    void abort() {
+        std::lock_guard<std::mutex> lk(mu);
+        failed = true;
+        cv.notify_all();
+    }
+};
+
 struct coru_ctx {
     int device = 0;
     cudaStream_t own_stream = nullptr;
@@ -138,6 +171,9 @@ struct coru_ctx {
     char* pinned = nullptr;
     size_t pinned_bytes = 0;
     ncclComm_t comm = nullptr;
+    coru_threadcomm* tcomm = nullptr;  // in-process backend (instead of NCCL)
+    void* tscratch = nullptr;          // its reduction scratch
+    size_t tscratch_bytes = 0;
     int rank = 0, world = 1;
     std::mutex mu;
     // A-pass profiling (bench evidence): CUDA events recorded on the launching stream around every
@@ -351,16 +387,86 @@ struct Work {
 };
 
 template <typename T>
+__global__ void k_sum_slots(const T* const* slots, int world, T* out, size_t count) {
+    for (size_t e = size_t(blockIdx.x) * blockDim.x + threadIdx.x; e < count; e += size_t(gridDim.x) * blockDim.x) {
+        T s = slots[0][e];
+        for (int r = 1; r < world; ++r) s += slots[r][e];  // rank order: identical bytes on every rank
+        out[e] = s;
+    }
+}
+
+template <typename T>
+int thread_allreduce(coru_ctx* c, T* buf, size_t count) {
+    coru_threadcomm* g = c->tcomm;
+    const size_t bytes = count * sizeof(T) + size_t(g->world) * sizeof(void*);
+    if (c->tscratch_bytes < bytes) {
+        CORU_CUDA(cudaStreamSynchronize(c->stream));
+        if (c->tscratch) cudaFree(c->tscratch);
+        c->tscratch = nullptr;
+        c->tscratch_bytes = 0;
+        if (cudaMalloc(&c->tscratch, bytes) != cudaSuccess) return fail(CORU_ENOMEM, "thread-comm scratch");
+        c->tscratch_bytes = bytes;
+    }
+    CORU_CUDA(cudaStreamSynchronize(c->stream));
+    g->slots[size_t(c->rank)] = buf;
+    if (!g->barrier()) return fail(CORU_ECUDA, "a peer rank of the thread group failed");
+    const T** dslots = reinterpret_cast<const T**>(static_cast<char*>(c->tscratch) + count * sizeof(T));
+    CORU_CUDA(cudaMemcpyAsync(dslots, g->slots.data(), size_t(g->world) * sizeof(void*), cudaMemcpyHostToDevice,
+                              c->stream));
+    T* tmp = static_cast<T*>(c->tscratch);
+    const int blocks = int(std::min<size_t>((count + 255) / 256, 148 * 8));
+    k_sum_slots<T><<<std::max(blocks, 1), 256, 0, c->stream>>>(dslots, g->world, tmp, count);
+    ++g_launches;
+    CORU_CUDA(cudaGetLastError());
+    CORU_CUDA(cudaStreamSynchronize(c->stream));
+    if (!g->barrier()) return fail(CORU_ECUDA, "a peer rank of the thread group failed");
+    CORU_CUDA(cudaMemcpyAsync(buf, tmp, count * sizeof(T), cudaMemcpyDeviceToDevice, c->stream));
+    return CORU_OK;
+}
+
+template <typename T>
+int thread_allgather(coru_ctx* c, const T* send, T* recv, size_t count) {
+    coru_threadcomm* g = c->tcomm;
+    CORU_CUDA(cudaStreamSynchronize(c->stream));
+    g->slots[size_t(c->rank)] = send;
+    if (!g->barrier()) return fail(CORU_ECUDA, "a peer rank of the thread group failed");
+    for (int r = 0; r < g->world; ++r)
+        CORU_CUDA(cudaMemcpyAsync(recv + size_t(r) * count, g->slots[size_t(r)], count * sizeof(T),
+                                  cudaMemcpyDeviceToDevice, c->stream));
+    CORU_CUDA(cudaStreamSynchronize(c->stream));
+    if (!g->barrier()) return fail(CORU_ECUDA, "a peer rank of the thread group failed");
+    return CORU_OK;
+}
+
+template <typename T>
 int allreduce(coru_ctx* c, T* buf, size_t count) {
     if (c->world <= 1) return CORU_OK;
+    if (c->tcomm) return thread_allreduce<T>(c, buf, count);
     CORU_NCCL(nccl()->AllReduce(buf, buf, count, nccl_type<T>(), ncclSum, c->comm, c->stream));
     return CORU_OK;
 }
 
+template <typename T>
+int allgather(coru_ctx* c, const T* send, T* recv, size_t count) {
+    if (c->tcomm) return thread_allgather<T>(c, send, recv, count);
+    CORU_NCCL(nccl()->AllGather(send, recv, count, nccl_type<T>(), c->comm, c->stream));
+    return CORU_OK;
+}
+
+template <typename T>
+int run_impl(coru_ctx* c, const Request<T>& r, size_t extra_arena_off);
+
 // The hot path. Enqueues everything on c->stream and synchronises once at the end (the flag and
-// the pivots are host outputs).
+// the pivots are host outputs). A failing rank of an in-process group releases its peers.
 template <typename T>
 int run(coru_ctx* c, const Request<T>& r, size_t extra_arena_off = 0) {
+    const int rc = run_impl<T>(c, r, extra_arena_off);
+    if (rc != CORU_OK && c->tcomm) c->tcomm->abort();
+    return rc;
+}
+
+template <typename T>
+int run_impl(coru_ctx* c, const Request<T>& r, size_t extra_arena_off) {
     const int d = r.d;
     const int dp = int(round_up(d, 8));
     const int64_t R = r.rows, N = r.cols;
@@ -412,7 +518,7 @@ int run(coru_ctx* c, const Request<T>& r, size_t extra_arena_off = 0) {
         CORU_TRY(w.ts2.form_q(nullptr, w.q2, dp, c->aux));
         // Q1, R1: local tree, all-gather of the R_g, redundant top level, local Q (main stream).
         CORU_TRY(w.ts1.factor(w.b1, dp, w.r1loc, st));
-        CORU_NCCL(nccl()->AllGather(w.r1loc, w.rstack, size_t(d) * d, nccl_type<T>(), c->comm, st));
+        CORU_TRY(allgather<T>(c, w.r1loc, w.rstack, size_t(d) * d));
         CORU_TRY(w.tstop.factor(w.rstack, d, w.r1, st));
         CORU_TRY(w.tstop.form_q(nullptr, w.qtop, d, st));
         CORU_TRY(w.ts1.form_q(w.qtop + int64_t(c->rank) * d * d, w.q1, dp, st));
@@ -672,6 +778,7 @@ void coru_ctx_destroy(coru_ctx* c) {
     cudaSetDevice(c->device);
     if (c->stream) cudaStreamSynchronize(c->stream);
     if (c->comm && nccl() && nccl()->CommDestroy) nccl()->CommDestroy(c->comm);
+    if (c->tscratch) cudaFree(c->tscratch);
     if (c->arena) cudaFree(c->arena);
     if (c->pinned) cudaFreeHost(c->pinned);
     if (c->aux) {
@@ -756,6 +863,23 @@ int coru_ctx_init_comm(coru_ctx* c, int rank, int world, const unsigned char id[
     CORU_NCCL(api->CommInitRank(&c->comm, world, u, rank));
     c->rank = rank;
     c->world = world;
+    return CORU_OK;
+}
+
+coru_threadcomm* coru_threadcomm_create(int world) {
+    if (world < 1) return nullptr;
+    return new coru_threadcomm(world);
+}
+
+void coru_threadcomm_destroy(coru_threadcomm* g) { delete g; }
+
+int coru_ctx_init_threadcomm(coru_ctx* c, coru_threadcomm* g, int rank) {
+    CORU_TRY(enter(c));
+    if (!g || rank < 0 || rank >= g->world) return fail(CORU_EINVAL, "bad thread group / rank");
+    std::lock_guard<std::mutex> lk(c->mu);
+    c->tcomm = g;
+    c->rank = rank;
+    c->world = g->world;
     return CORU_OK;
 }
 

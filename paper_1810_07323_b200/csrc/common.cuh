@@ -1,11 +1,34 @@
 // Shared device helpers for the CoR-UTV sm_100a kernels.
 #pragma once
 #include <cstdint>
+#include <mutex>
+#include <set>
+#include <utility>
 #include <cuda_runtime.h>
 
 namespace coru_gpu {
 
 constexpr int kWarp = 32;
+
+// Raise a kernel's dynamic shared-memory limit to the device maximum, once per (kernel, device).
+// The attribute is process-global: setting it per launch to the launch's own size races between
+// host threads (a concurrent smaller setting makes a larger launch fail), and the limit does not
+// affect occupancy — the launch's actual size does.
+inline void allow_max_smem(const void* kernel) {
+    static std::mutex mu;
+    static std::set<std::pair<const void*, int>> done;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> lk(mu);
+    if (!done.insert({kernel, dev}).second) return;
+    int v = 0;
+    cudaDeviceGetAttribute(&v, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, v);
+}
+template <typename K>
+inline void allow_max_smem(K* kernel) {
+    allow_max_smem(reinterpret_cast<const void*>(kernel));
+}
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));

@@ -165,10 +165,10 @@ cudaError_t gemm_f32(Op op, const float* A, int64_t lda, const float* X, int64_t
     const dim3 grid(unsigned((Mo + kBM - 1) / kBM), unsigned((N + kBN - 1) / kBN), unsigned(p.splits));
     const size_t smem = size_t(kStages) * kStageFloats * sizeof(float);
     if (op == Op::N) {
-        cudaFuncSetAttribute(k_gemm_f32<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+        allow_max_smem(k_gemm_f32<false>);
         k_gemm_f32<false><<<grid, kThreads, smem, st>>>(A, lda, X, ldx, out, ldo, sstride, Mo, K, N, kps);
     } else {
-        cudaFuncSetAttribute(k_gemm_f32<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+        allow_max_smem(k_gemm_f32<true>);
         k_gemm_f32<true><<<grid, kThreads, smem, st>>>(A, lda, X, ldx, out, ldo, sstride, Mo, K, N, kps);
     }
     cudaError_t e = cudaGetLastError();

@@ -262,11 +262,11 @@ cudaError_t launch(const double* A, int64_t lda, const double* X, int64_t ldx, d
     const bool vec = (lda % 2 == 0) && (reinterpret_cast<uintptr_t>(A) % 16 == 0);
     if (vec) {
         auto k = k_gemm_f64<WM, WN, TRANS, 2>;
-        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, S::bytes);
+        allow_max_smem(k);
         k<<<p.splits, S::NT, S::bytes, st>>>(A, lda, X, ldx, C, ldc, Mo, K, N, ktiles, iters, p.splits, ws, p.max_seg);
     } else {
         auto k = k_gemm_f64<WM, WN, TRANS, 1>;
-        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, S::bytes);
+        allow_max_smem(k);
         k<<<p.splits, S::NT, S::bytes, st>>>(A, lda, X, ldx, C, ldc, Mo, K, N, ktiles, iters, p.splits, ws, p.max_seg);
     }
     cudaError_t e = cudaGetLastError();

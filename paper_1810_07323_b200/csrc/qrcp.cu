@@ -340,7 +340,7 @@ cudaError_t qrcp(const T* M, int ldm, int d, T* Q, int ldq, T* Tout, int ldt, in
                  int max_smem, cudaStream_t st) {
     const bool fits = qrcp_smem_bytes(d, sizeof(T), true) <= size_t(max_smem);
     const size_t sm = qrcp_smem_bytes(d, sizeof(T), fits);
-    cudaFuncSetAttribute(k_qrcp<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
+    allow_max_smem(k_qrcp<T>);
     k_qrcp<T><<<1, kThreads, sm, st>>>(M, ldm, d, Q, ldq, Tout, ldt, perm, scratch, fits ? 1 : 0);
     return cudaGetLastError();
 }

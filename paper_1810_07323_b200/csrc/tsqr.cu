@@ -743,17 +743,17 @@ cudaError_t tsqr_factor(const TsqrPlan& p, const T* B, int64_t ldb, T* V, T* bet
         T* Rl = (l + 1 == p.levels.size()) ? r_out : R + L.r_off;
         if (L.kind == TsqrLevel::kBlockedSmem) {
             const size_t sm = BlockedSmem<T>::bytes(d, L.rbmax, sizeof(T));
-            cudaFuncSetAttribute(k_qr_blocked<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
+            allow_max_smem(k_qr_blocked<T>);
             k_qr_blocked<T><<<L.nb, kBThreads, sm, st>>>(X, ldx, L.rows, L.nb, d, V + L.v_off, L.ldv,
                                                           beta + L.beta_off, Tarena + L.t_off, Rl, d);
         } else if (L.kind == TsqrLevel::kBlockedGlobal) {
             const size_t sm = BigSmem<T>::bytes(d, L.rbmax, sizeof(T));
-            cudaFuncSetAttribute(k_qr_blocked_g<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
+            allow_max_smem(k_qr_blocked_g<T>);
             k_qr_blocked_g<T><<<L.nb, kBThreads, sm, st>>>(X, ldx, L.rows, L.nb, d, V + L.v_off, L.ldv,
                                                             beta + L.beta_off, Tarena + L.t_off, Rl, d);
         } else {
             const size_t sm = L.smem ? wide_factor_smem_bytes(L.rbmax, d, sizeof(T)) : wide_factor_smem_bytes(0, d, sizeof(T));
-            cudaFuncSetAttribute(k_hh_factor<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
+            allow_max_smem(k_hh_factor<T>);
             k_hh_factor<T><<<L.nb, kThreads, sm, st>>>(X, ldx, L.rows, L.nb, d, V + L.v_off, L.ldv,
                                                         beta + L.beta_off, Rl, d, L.smem ? 1 : 0);
         }
@@ -787,13 +787,13 @@ cudaError_t tsqr_form_q(const TsqrPlan& p, const T* q_top, T* V, T* beta, T* Tar
         if (L.blocked) {
             const bool stage = FormQSmem<T>::bytes(d, L.rbmax, sizeof(T), true) <= size_t(max_smem);
             const size_t sm = FormQSmem<T>::bytes(d, L.rbmax, sizeof(T), stage);
-            cudaFuncSetAttribute(k_qr_blocked_form_q<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
+            allow_max_smem(k_qr_blocked_form_q<T>);
             const dim3 grid(unsigned(L.nb), unsigned((d + kQChunk - 1) / kQChunk));
             k_qr_blocked_form_q<T><<<grid, kBThreads, sm, st>>>(qin, ldqin, L.rows, L.nb, d, V + L.v_off, L.ldv,
                                                                  Tarena + L.t_off, out, ldo, stage ? 1 : 0);
         } else {
             const size_t sm = L.smem ? size_t(L.rbmax | 1) * d * sizeof(T) : 0;
-            cudaFuncSetAttribute(k_hh_form_q<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
+            allow_max_smem(k_hh_form_q<T>);
             k_hh_form_q<T><<<L.nb, kThreads, sm, st>>>(qin, ldqin, L.rows, L.nb, d, V + L.v_off, L.ldv,
                                                         beta + L.beta_off, out, ldo, scratch, L.smem ? 1 : 0);
         }
