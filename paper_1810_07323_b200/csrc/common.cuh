@@ -46,6 +46,22 @@ __device__ __forceinline__ void cp_async_zfill(void* smem_dst, const void* gmem_
                      "l"(gmem_src), "n"(BYTES), "r"(src_bytes));
     }
 }
+// 16-byte cp.async with an L2 cache policy (createpolicy): stream A with evict_first so the small,
+// re-read operand (the sketch X) stays L2-resident.
+__device__ __forceinline__ void cp_async16_hint(void* smem_dst, const void* gmem_src, int src_bytes, uint64_t policy) {
+    asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2, %3;\n" ::"r"(smem_u32(smem_dst)),
+                 "l"(gmem_src), "r"(src_bytes), "l"(policy));
+}
+__device__ __forceinline__ uint64_t l2_policy_evict_first() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;\n" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ uint64_t l2_policy_evict_last() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;\n" : "=l"(p));
+    return p;
+}
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }

@@ -16,10 +16,15 @@ struct GemmPlan {
     int bm = 0, bn = 0, splits = 1;  // fp64: splits = stream-K CTA count
     int max_seg = 1;                 // fp64 stream-K: max CTAs sharing one tile
     bool fixup = false;              // fp64 stream-K: some tile is split across CTAs
+    int cfg = -1;                    // fp64: kernel configuration id (gemm_f64.cu table)
+    int num_sms = 148;
     int64_t ws_elems = 0;            // workspace (partials) needed, in elements
 };
 
 GemmPlan plan_gemm_f64(Op op, int64_t Mo, int64_t K, int N, int num_sms);
+// Explicit configuration (cfg < 0: default); for tuning tools.
+GemmPlan plan_gemm_f64_cfg(Op op, int64_t Mo, int64_t K, int N, int num_sms, int cfg);
+int gemm_f64_num_configs();
 // `ws` must hold plan.ws_elems doubles when plan.splits > 1.
 cudaError_t gemm_f64(Op op, const double* A, int64_t lda, const double* X, int64_t ldx, double* C,
                      int64_t ldc, int64_t Mo, int64_t K, int N, const GemmPlan& plan, double* ws,

@@ -6,13 +6,14 @@
 // DMMA; tools/fp64_peak.cu measured DMMA and DFMA both at ~36.5-37 TFLOP/s per GPU.
 //
 // Shape: the output is Mo x N with N = the sketch width (<= 256): one CTA tile spans ALL of N
-// (warps 32x32, WN = ceil(N/32) warps across, WM = 8/WN down), so A is streamed from HBM exactly
-// once per pass. K is the long dimension. BK = 16 slabs go through a 3-deep cp.async ring in
-// padded shared memory; A fragments are read as 16-byte pairs by giving each lane the k-pair
-// (2t, 2t+1) instead of (t, t+4) (a consistent permutation of k in A and X, so the product is
-// unchanged). Work is split stream-K style: exactly P = 2 x SMs CTAs, each owning an equal
-// contiguous range of (tile, k-slab) iterations; tiles owned by one CTA are written directly,
-// split tiles go through a fixed-order fix-up (deterministic, no atomics).
+// (WN warps of 32 columns), so A is streamed from HBM exactly once per pass; warps own
+// (16·MT) x 32 output tiles. K is the long dimension, staged in BK-deep slabs through an
+// ST-deep cp.async ring in padded shared memory. A fragments are read as 16-byte pairs by giving
+// lane t the k-pair (2t, 2t+1) instead of (t, t+4) (a consistent permutation of k in A and X, so
+// the product is unchanged). A is streamed with an L2 evict-first policy so X stays L2-resident.
+// Work is split stream-K style: P = resident CTAs, each owning an equal contiguous range of
+// (tile, k-slab) iterations; tiles owned by one CTA are written directly, split tiles go through
+// a fixed-order fix-up (deterministic, no atomics).
 #include <algorithm>
 #include <cmath>
 
@@ -25,29 +26,33 @@ namespace {
 
 __host__ __device__ __forceinline__ int64_t imin64(int64_t a, int64_t b) { return a < b ? a : b; }
 
-constexpr int kBK = 16;
-constexpr int kStages = 3;
-
-template <int WM, int WN, bool TRANS>
+template <int WM_, int WN_, int MT_, int BK_, int ST_, bool TRANS_>
 struct Cfg {
-    static constexpr int BM = 32 * WM, BN = 32 * WN, NT = 32 * WM * WN;
+    static constexpr int WM = WM_, WN = WN_, MT = MT_, BK = BK_, ST = ST_;
+    static constexpr bool TRANS = TRANS_;
+    static constexpr int WTM = 16 * MT;  // warp tile rows
+    static constexpr int BM = WM * WTM, BN = 32 * WN, NT = 32 * WM * WN;
     // op N: A tile [BM][BK+8]   (row stride = 8 mod 16 doubles: conflict-free 16-byte pair reads)
     // op T: A tile [BK][BM+4]   (row stride = 4 mod 16: 2 wavefronts per 8-byte fragment read)
-    static constexpr int a_stride = TRANS ? BM + 4 : kBK + 8;
-    static constexpr int a_elems = TRANS ? kBK * a_stride : BM * a_stride;
+    static constexpr int a_stride = TRANS ? BM + 4 : BK + 8;
+    static constexpr int a_elems = TRANS ? BK * a_stride : BM * a_stride;
     static constexpr int x_stride = BN + 4;
-    static constexpr int x_elems = kBK * x_stride;
+    static constexpr int x_elems = BK * x_stride;
     static constexpr int stage_elems = a_elems + x_elems;
-    static constexpr int bytes = kStages * stage_elems * 8;
+    static constexpr int bytes = ST * stage_elems * 8;
+    static constexpr int regs = MT == 4 ? 192 : (MT == 2 ? 128 : 96);
+    static constexpr int occ_smem = (227 * 1024) / bytes;
+    static constexpr int occ_regs = 65536 / (NT * regs);
+    static constexpr int min_blocks = occ_smem < occ_regs ? (occ_smem < 4 ? occ_smem : 4) : (occ_regs < 4 ? occ_regs : 4);
 };
 
-template <int WM, int WN, bool TRANS, int VEC>
+// Generic loader (any alignment; 8-byte copies when lda is odd).
+template <class S, int VEC>
 __device__ __forceinline__ void load_stage(double* sa, double* sx, const double* __restrict__ A, int64_t lda,
                                            const double* __restrict__ X, int64_t ldx, int64_t m0, int64_t k0,
                                            int64_t Mo, int64_t K, int N, int tid) {
-    using S = Cfg<WM, WN, TRANS>;
-    if constexpr (!TRANS) {
-        constexpr int CPR = kBK / VEC;
+    if constexpr (!S::TRANS) {
+        constexpr int CPR = S::BK / VEC;
         for (int c = tid; c < S::BM * CPR; c += S::NT) {
             const int r = c / CPR, cc = (c % CPR) * VEC;
             const int64_t gr = m0 + r, gc = k0 + cc;
@@ -61,7 +66,7 @@ __device__ __forceinline__ void load_stage(double* sa, double* sx, const double*
         }
     } else {
         constexpr int CPR = S::BM / VEC;
-        for (int c = tid; c < kBK * CPR; c += S::NT) {
+        for (int c = tid; c < S::BK * CPR; c += S::NT) {
             const int r = c / CPR, cc = (c % CPR) * VEC;
             const int64_t gr = k0 + r, gc = m0 + cc;
             int bytes = 0;
@@ -74,7 +79,7 @@ __device__ __forceinline__ void load_stage(double* sa, double* sx, const double*
         }
     }
     constexpr int CPRX = S::BN / 2;  // X rows are 16-B aligned (ldx even, base aligned)
-    for (int c = tid; c < kBK * CPRX; c += S::NT) {
+    for (int c = tid; c < S::BK * CPRX; c += S::NT) {
         const int r = c / CPRX, cc = (c % CPRX) * 2;
         const int64_t gr = k0 + r;
         int bytes = 0;
@@ -87,6 +92,92 @@ __device__ __forceinline__ void load_stage(double* sa, double* sx, const double*
     }
 }
 
+// Loader for 16-byte-aligned operands: every thread's chunk columns and row offsets are fixed
+// per tile, so a stage costs one pointer bump + one predicate per 16-byte copy.
+template <class S>
+struct FastLoader {
+    static constexpr int A_CPR = S::TRANS ? S::BM / 2 : S::BK / 2;  // 16-byte chunks per smem row
+    static constexpr int A_ROWS = S::TRANS ? S::BK : S::BM;
+    static constexpr int A_RPP = S::NT / A_CPR;  // rows per pass
+    static constexpr int A_PASSES = (A_ROWS + A_RPP - 1) / A_RPP;
+    static constexpr int X_CPR = S::BN / 2;
+    static constexpr int X_RPP = S::NT / X_CPR;
+    static constexpr int X_PASSES = (S::BK + X_RPP - 1) / X_RPP;
+    static_assert(S::NT % A_CPR == 0 && S::NT % X_CPR == 0, "thread mapping");
+    static_assert(A_PASSES <= 32, "pass mask");
+
+    const double* a_ptr;
+    const double* x_ptr;
+    int64_t a_pass_stride, a_k_stride, x_pass_stride;
+    int a_r0, a_cc, x_r0, x_cc;
+    int a_fixed_bytes;  // op T: bytes valid along m (fixed per tile)
+    uint32_t a_row_ok;  // pass i row inside the tile (and < Mo for op N)
+    int x_bytes;
+    int64_t K;
+    uint64_t pol_a, pol_x;
+
+    __device__ FastLoader(const double* A, int64_t lda, const double* X, int64_t ldx, int64_t m0, int64_t Mo,
+                          int64_t K_, int N, int tid, uint64_t pa, uint64_t px)  // X, N: this n-tile's columns
+        : K(K_), pol_a(pa), pol_x(px) {
+        a_r0 = tid / A_CPR;
+        a_cc = (tid % A_CPR) * 2;
+        x_r0 = tid / X_CPR;
+        x_cc = (tid % X_CPR) * 2;
+        a_row_ok = 0;
+        if constexpr (!S::TRANS) {
+            a_ptr = A + (m0 + a_r0) * lda + a_cc;
+            a_pass_stride = int64_t(A_RPP) * lda;
+            a_k_stride = 1;
+#pragma unroll
+            for (int i = 0; i < A_PASSES; ++i)
+                if (a_r0 + i * A_RPP < A_ROWS && m0 + a_r0 + i * A_RPP < Mo) a_row_ok |= 1u << i;
+            a_fixed_bytes = 16;
+        } else {
+            a_ptr = A + int64_t(a_r0) * lda + m0 + a_cc;
+            a_pass_stride = int64_t(A_RPP) * lda;
+            a_k_stride = lda;
+#pragma unroll
+            for (int i = 0; i < A_PASSES; ++i)
+                if (a_r0 + i * A_RPP < A_ROWS) a_row_ok |= 1u << i;
+            const int64_t rem = Mo - (m0 + a_cc);
+            a_fixed_bytes = rem >= 2 ? 16 : (rem == 1 ? 8 : 0);
+        }
+        x_ptr = X + int64_t(x_r0) * ldx + x_cc;
+        x_pass_stride = int64_t(X_RPP) * ldx;
+        x_bytes = N - x_cc >= 2 ? 16 : (N - x_cc == 1 ? 8 : 0);
+    }
+
+    __device__ __forceinline__ void load(double* sa, double* sx, int64_t k0, const double* A, const double* X,
+                                         int64_t ldx) const {
+        if constexpr (!S::TRANS) {
+            const int64_t kr = K - (k0 + a_cc);
+            const int kbytes = kr >= 2 ? 16 : (kr == 1 ? 8 : 0);
+#pragma unroll
+            for (int i = 0; i < A_PASSES; ++i) {
+                if (a_r0 + i * A_RPP >= A_ROWS) continue;
+                const bool ok = ((a_row_ok >> i) & 1u) && kbytes > 0;
+                cp_async16_hint(sa + (a_r0 + i * A_RPP) * S::a_stride + a_cc, ok ? a_ptr + i * a_pass_stride + k0 : A,
+                                ok ? kbytes : 0, pol_a);
+            }
+        } else {
+#pragma unroll
+            for (int i = 0; i < A_PASSES; ++i) {
+                if (a_r0 + i * A_RPP >= A_ROWS) continue;
+                const bool ok = k0 + a_r0 + i * A_RPP < K && a_fixed_bytes > 0;
+                cp_async16_hint(sa + (a_r0 + i * A_RPP) * S::a_stride + a_cc,
+                                ok ? a_ptr + i * a_pass_stride + k0 * a_k_stride : A, ok ? a_fixed_bytes : 0, pol_a);
+            }
+        }
+#pragma unroll
+        for (int i = 0; i < X_PASSES; ++i) {
+            if (x_r0 + i * X_RPP >= S::BK) continue;
+            const bool ok = k0 + x_r0 + i * X_RPP < K && x_bytes > 0;
+            cp_async16_hint(sx + (x_r0 + i * X_RPP) * S::x_stride + x_cc, ok ? x_ptr + i * x_pass_stride + k0 * ldx : X,
+                            ok ? x_bytes : 0, pol_x);
+        }
+    }
+};
+
 // CTA c owns iterations [I*c/P, I*(c+1)/P) of the (tile, k-slab) space, tile-major.
 __host__ __device__ __forceinline__ int64_t sk_begin(int64_t iters, int P, int c) { return iters * c / P; }
 // The CTA that owns iteration g.
@@ -94,66 +185,69 @@ __host__ __device__ __forceinline__ int sk_owner(int64_t iters, int P, int64_t g
     return int(((g + 1) * P - 1) / iters);
 }
 
-template <int WM, int WN, bool TRANS, int VEC>
-__global__ void __launch_bounds__(32 * WM * WN, 2)
+template <class S, int VEC>
+__global__ void __launch_bounds__(S::NT, S::min_blocks)
     k_gemm_f64(const double* __restrict__ A, int64_t lda, const double* __restrict__ X, int64_t ldx,
                double* __restrict__ C, int64_t ldc, int64_t Mo, int64_t K, int N, int64_t ktiles, int64_t iters, int P,
                double* __restrict__ ws, int max_seg) {
-    using S = Cfg<WM, WN, TRANS>;
+    constexpr int MT = S::MT, BK = S::BK, ST = S::ST;
     extern __shared__ __align__(16) double smem[];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int g = lane >> 2, t = lane & 3;
-    const int wm0 = (warp / WN) * 32, wn0 = (warp % WN) * 32;
+    const int wm0 = (warp / S::WN) * S::WTM, wn0 = (warp % S::WN) * 32;
     const int cta = blockIdx.x;
     int64_t it = sk_begin(iters, P, cta);
     const int64_t it_end = sk_begin(iters, P, cta + 1);
+    const uint64_t pol_a = l2_policy_evict_first(), pol_x = l2_policy_evict_last();
 
+    const int tiles_n = (N + S::BN - 1) / S::BN;
     while (it < it_end) {
         const int64_t tile = it / ktiles;
         const int64_t kb = it % ktiles;
         const int64_t ke = imin64(ktiles, kb + (it_end - it));
         const int nk = int(ke - kb);
-        const int64_t m0 = tile * S::BM;
+        const int64_t m0 = (tile / tiles_n) * S::BM;  // n-tiles of one row block are adjacent
+        const int n0 = int(tile % tiles_n) * S::BN;
+        const int Nt = N - n0;                        // columns left from this n-tile
+        const double* Xt = X + n0;
 
-        double acc[2][4][4];
+        double acc[MT][4][4];
 #pragma unroll
-        for (int i = 0; i < 2; ++i)
+        for (int i = 0; i < MT; ++i)
 #pragma unroll
             for (int j = 0; j < 4; ++j)
 #pragma unroll
                 for (int e = 0; e < 4; ++e) acc[i][j][e] = 0.0;
 
+        const FastLoader<S> fl(A, lda, Xt, ldx, m0, Mo, K, Nt, tid, pol_a, pol_x);
+        auto stage_load = [&](double* sa, int64_t k0) {
+            if constexpr (VEC == 2) fl.load(sa, sa + S::a_elems, k0, A, Xt, ldx);
+            else load_stage<S, VEC>(sa, sa + S::a_elems, A, lda, Xt, ldx, m0, k0, Mo, K, Nt, tid);
+        };
         __syncthreads();  // previous segment's readers are done with the ring
 #pragma unroll
-        for (int s = 0; s < kStages - 1; ++s) {
-            if (s < nk) {
-                double* sa = smem + s * S::stage_elems;
-                load_stage<WM, WN, TRANS, VEC>(sa, sa + S::a_elems, A, lda, X, ldx, m0, (kb + s) * kBK, Mo, K, N, tid);
-            }
+        for (int s = 0; s < ST - 1; ++s) {
+            if (s < nk) stage_load(smem + s * S::stage_elems, (kb + s) * BK);
             cp_async_commit();
         }
         for (int ki = 0; ki < nk; ++ki) {
-            cp_async_wait<kStages - 2>();
+            cp_async_wait<ST - 2>();
             __syncthreads();
             {
-                const int nxt = ki + kStages - 1;
-                if (nxt < nk) {
-                    double* sa = smem + (nxt % kStages) * S::stage_elems;
-                    load_stage<WM, WN, TRANS, VEC>(sa, sa + S::a_elems, A, lda, X, ldx, m0, (kb + nxt) * kBK, Mo, K,
-                                                   N, tid);
-                }
+                const int nxt = ki + ST - 1;
+                if (nxt < nk) stage_load(smem + (nxt % ST) * S::stage_elems, (kb + nxt) * BK);
                 cp_async_commit();
             }
-            const double* sa = smem + (ki % kStages) * S::stage_elems;
+            const double* sa = smem + (ki % ST) * S::stage_elems;
             const double* sx = sa + S::a_elems;
 #pragma unroll
-            for (int kk = 0; kk < kBK; kk += 8) {
+            for (int kk = 0; kk < BK; kk += 8) {
                 // lane (g, t) holds k-pair (2t, 2t+1) of the k8 slab for both operands
-                double af[2][4], bf[4][2];
+                double af[MT][4], bf[4][2];
 #pragma unroll
-                for (int mt = 0; mt < 2; ++mt) {
+                for (int mt = 0; mt < MT; ++mt) {
                     const int r = wm0 + mt * 16 + g;
-                    if constexpr (!TRANS) {
+                    if constexpr (!S::TRANS) {
                         const double2 lo = *reinterpret_cast<const double2*>(sa + r * S::a_stride + kk + 2 * t);
                         const double2 hi = *reinterpret_cast<const double2*>(sa + (r + 8) * S::a_stride + kk + 2 * t);
                         af[mt][0] = lo.x;
@@ -174,7 +268,7 @@ __global__ void __launch_bounds__(32 * WM * WN, 2)
                     bf[nt][1] = sx[(kk + 2 * t + 1) * S::x_stride + c];
                 }
 #pragma unroll
-                for (int mt = 0; mt < 2; ++mt)
+                for (int mt = 0; mt < MT; ++mt)
 #pragma unroll
                     for (int nt = 0; nt < 4; ++nt) dmma_16x8x8(acc[mt][nt], af[mt], bf[nt]);
             }
@@ -186,7 +280,7 @@ __global__ void __launch_bounds__(32 * WM * WN, 2)
         double* dst_base;
         int64_t ld_dst, row_base;
         if (whole) {
-            dst_base = C;
+            dst_base = C + n0;
             ld_dst = ldc;
             row_base = m0;
         } else {
@@ -197,7 +291,7 @@ __global__ void __launch_bounds__(32 * WM * WN, 2)
             row_base = 0;
         }
 #pragma unroll
-        for (int mt = 0; mt < 2; ++mt) {
+        for (int mt = 0; mt < MT; ++mt) {
 #pragma unroll
             for (int h = 0; h < 2; ++h) {
                 const int r = wm0 + mt * 16 + g + h * 8;
@@ -208,11 +302,11 @@ __global__ void __launch_bounds__(32 * WM * WN, 2)
                     double* dst = dst_base + (row_base + r) * ld_dst + col;
                     if (!whole) {
                         *reinterpret_cast<double2*>(dst) = make_double2(acc[mt][nt][2 * h], acc[mt][nt][2 * h + 1]);
-                    } else if (col + 1 < N && (reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
+                    } else if (col + 1 < Nt && (reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
                         *reinterpret_cast<double2*>(dst) = make_double2(acc[mt][nt][2 * h], acc[mt][nt][2 * h + 1]);
-                    } else if (col < N) {
+                    } else if (col < Nt) {
                         dst[0] = acc[mt][nt][2 * h];
-                        if (col + 1 < N) dst[1] = acc[mt][nt][2 * h + 1];
+                        if (col + 1 < Nt) dst[1] = acc[mt][nt][2 * h + 1];
                     }
                 }
             }
@@ -226,6 +320,8 @@ __global__ void __launch_bounds__(32 * WM * WN, 2)
 __global__ void k_streamk_fixup(const double* __restrict__ ws, int max_seg, int bm, int bn, int64_t ktiles,
                                 int64_t iters, int P, double* __restrict__ C, int64_t ldc, int64_t Mo, int N) {
     const int64_t tile = blockIdx.x;
+    const int tiles_n = (N + bn - 1) / bn;
+    const int n0 = int(tile % tiles_n) * bn;
     const int first = sk_owner(iters, P, tile * ktiles);
     const int last = sk_owner(iters, P, tile * ktiles + ktiles - 1);
     if (first == last) return;  // written directly by its only owner
@@ -233,39 +329,75 @@ __global__ void k_streamk_fixup(const double* __restrict__ ws, int max_seg, int 
     const int e = blockIdx.y * blockDim.x + threadIdx.x;
     if (e >= tile_elems) return;
     const int r = e / bn, c = e % bn;
-    const int64_t row = tile * bm + r;
-    if (row >= Mo || c >= N) return;
+    const int64_t row = (tile / tiles_n) * bm + r;
+    if (row >= Mo || n0 + c >= N) return;
     const double* base = ws + tile * max_seg * tile_elems + e;
     double s = base[0];
     for (int q = 1; q <= last - first; ++q) s += base[q * tile_elems];
-    C[row * ldc + c] = s;
+    C[row * ldc + n0 + c] = s;
 }
 
-void warp_grid(int N, int& wm, int& wn) {
-    wn = std::max(1, std::min(8, (N + 31) / 32));
-    wm = std::max(1, std::min(4, 8 / wn));
+// ---- configuration table -------------------------------------------------------------------
+struct CfgInfo {
+    int id, wm, wn, mt, bk, st;
+};
+// Candidates per sketch-width class (WN = ceil(N/32)); tools/gemm_tune.cu sweeps them.
+#define CORU_GEMM_CONFIGS(X) \
+    X(0, 4, 1, 2, 16, 3)     \
+    X(1, 4, 2, 2, 16, 3)     \
+    X(2, 4, 2, 4, 16, 3)     \
+    X(3, 2, 2, 4, 32, 3)     \
+    X(4, 2, 3, 2, 16, 3)     \
+    X(5, 2, 4, 2, 16, 3)     \
+    X(6, 2, 4, 4, 16, 3)     \
+    X(7, 1, 5, 2, 16, 3)     \
+    X(8, 1, 6, 2, 16, 3)     \
+    X(9, 1, 7, 2, 16, 3)     \
+    X(10, 1, 7, 4, 16, 3)    \
+    X(11, 1, 8, 2, 16, 2)    \
+    X(12, 1, 8, 4, 16, 2)    \
+    X(13, 4, 2, 2, 32, 3)    \
+    X(14, 1, 7, 4, 32, 2)    \
+    X(15, 2, 1, 2, 16, 4)    \
+    X(16, 2, 2, 1, 16, 4)    \
+    X(17, 2, 2, 2, 16, 3)    \
+    X(18, 4, 1, 1, 16, 4)    \
+    X(19, 1, 2, 2, 16, 4)
+
+constexpr CfgInfo kCfgs[] = {
+#define CORU_ROW(id, wm, wn, mt, bk, st) {id, wm, wn, mt, bk, st},
+    CORU_GEMM_CONFIGS(CORU_ROW)
+#undef CORU_ROW
+};
+constexpr int kNumCfgs = int(sizeof(kCfgs) / sizeof(kCfgs[0]));
+
+int cfg_bytes(const CfgInfo& c, bool trans) {
+    const int bm = c.wm * 16 * c.mt, bn = 32 * c.wn;
+    const int a = trans ? c.bk * (bm + 4) : bm * (c.bk + 8);
+    return c.st * (a + c.bk * (bn + 4)) * 8;
 }
 
-int cfg_bytes(int wm, int wn, bool trans) {
-    const int bm = 32 * wm, bn = 32 * wn;
-    const int a = trans ? kBK * (bm + 4) : bm * (kBK + 8);
-    return kStages * (a + kBK * (bn + 4)) * 8;
+// Picked from tools/gemm_tune.cu on B200 (round 1): small 4-warp CTAs with 4-deep rings and 32- or
+// 64-wide n-tiles (3-4 resident CTAs per SM, A re-read from L2 per n-tile) beat the wide-tile
+// variants by 10-15 % on every BASELINE shape.
+int default_cfg(Op op, int N) {
+    if (op == Op::N) return N <= 32 ? 0 : (N <= 64 ? 16 : 0);
+    return N <= 32 ? 15 : (N <= 64 ? 19 : 15);
 }
 
-template <int WM, int WN, bool TRANS>
-cudaError_t launch(const double* A, int64_t lda, const double* X, int64_t ldx, double* C, int64_t ldc, int64_t Mo,
-                   int64_t K, int N, const GemmPlan& p, double* ws, cudaStream_t st) {
-    using S = Cfg<WM, WN, TRANS>;
-    const int64_t ktiles = (K + kBK - 1) / kBK;
-    const int64_t tiles = (Mo + S::BM - 1) / S::BM;
+template <class S>
+cudaError_t launch_cfg(const double* A, int64_t lda, const double* X, int64_t ldx, double* C, int64_t ldc, int64_t Mo,
+                       int64_t K, int N, const GemmPlan& p, double* ws, cudaStream_t st) {
+    const int64_t ktiles = (K + S::BK - 1) / S::BK;
+    const int64_t tiles = ((Mo + S::BM - 1) / S::BM) * ((N + S::BN - 1) / S::BN);
     const int64_t iters = tiles * ktiles;
     const bool vec = (lda % 2 == 0) && (reinterpret_cast<uintptr_t>(A) % 16 == 0);
     if (vec) {
-        auto k = k_gemm_f64<WM, WN, TRANS, 2>;
+        auto k = k_gemm_f64<S, 2>;
         allow_max_smem(k);
         k<<<p.splits, S::NT, S::bytes, st>>>(A, lda, X, ldx, C, ldc, Mo, K, N, ktiles, iters, p.splits, ws, p.max_seg);
     } else {
-        auto k = k_gemm_f64<WM, WN, TRANS, 1>;
+        auto k = k_gemm_f64<S, 1>;
         allow_max_smem(k);
         k<<<p.splits, S::NT, S::bytes, st>>>(A, lda, X, ldx, C, ldc, Mo, K, N, ktiles, iters, p.splits, ws, p.max_seg);
     }
@@ -278,24 +410,29 @@ cudaError_t launch(const double* A, int64_t lda, const double* X, int64_t ldx, d
 
 }  // namespace
 
-GemmPlan plan_gemm_f64(Op op, int64_t Mo, int64_t K, int N, int num_sms) {
-    (void)op;
+int gemm_f64_num_configs() { return kNumCfgs; }
+
+GemmPlan plan_gemm_f64_cfg(Op op, int64_t Mo, int64_t K, int N, int num_sms, int cfg) {
     GemmPlan p;
-    int wm, wn;
-    warp_grid(N, wm, wn);
-    p.bm = 32 * wm;
-    p.bn = 32 * wn;
-    const int64_t ktiles = (K + kBK - 1) / kBK;
-    const int64_t tiles = (Mo + p.bm - 1) / p.bm;
+    if (cfg < 0 || cfg >= kNumCfgs) cfg = default_cfg(op, N);
+    const CfgInfo& c = kCfgs[cfg];
+    p.cfg = cfg;
+    p.bm = c.wm * 16 * c.mt;
+    p.bn = 32 * c.wn;
+    const int64_t ktiles = (K + c.bk - 1) / c.bk;
+    const int64_t tiles = ((Mo + p.bm - 1) / p.bm) * ((N + p.bn - 1) / p.bn);
     const int64_t iters = tiles * ktiles;
-    // Every CTA resident at once (occupancy by shared memory), never more CTAs than iterations.
-    const int occ = std::max(1, std::min(2, (227 * 1024) / cfg_bytes(wm, wn, op == Op::T)));
-    // ... and each CTA owns >= 4 k-slabs, and no tile is shared by more than 12 CTAs (bounded fix-up).
+    const int nt = 32 * c.wm * c.wn;
+    const int reg_per_thread = c.mt == 4 ? 192 : (c.mt == 2 ? 128 : 96);
+    const int occ_smem = (227 * 1024) / cfg_bytes(c, op == Op::T);
+    const int occ_regs = 65536 / (nt * reg_per_thread);
+    const int occ = std::max(1, std::min({4, occ_smem, occ_regs}));
+    // Every CTA resident at once, each owns >= 4 k-slabs, and no tile is shared by more CTAs than
+    // needed to fill the machine (bounded fix-up).
     int64_t P64 = std::min<int64_t>(int64_t(occ) * num_sms, iters / 4);
-    P64 = std::min<int64_t>(P64, tiles * 12);
-    int P = int(std::max<int64_t>(P64, 1));
+    P64 = std::min<int64_t>(P64, tiles * std::max<int64_t>(12, (int64_t(occ) * num_sms + tiles - 1) / tiles));
+    const int P = int(std::max<int64_t>(P64, 1));
     p.splits = P;
-    // Max segments a tile is split into: ceil(ktiles / (iters/P)) + 1.
     const int64_t per = std::max<int64_t>(1, iters / P);
     p.max_seg = int(std::min<int64_t>(P, (ktiles + per - 1) / per + 1));
     p.fixup = false;
@@ -304,34 +441,37 @@ GemmPlan plan_gemm_f64(Op op, int64_t Mo, int64_t K, int N, int num_sms) {
         p.fixup = ((g0 + 1) * P - 1) / iters != ((g1 + 1) * P - 1) / iters;
     }
     p.ws_elems = p.fixup ? tiles * int64_t(p.max_seg) * p.bm * p.bn : 0;
+    p.num_sms = num_sms;
+    return p;
+}
+
+GemmPlan plan_gemm_f64(Op op, int64_t Mo, int64_t K, int N, int num_sms) {
+    // Sketch widths beyond one CTA tile run as 256-wide column chunks (see gemm_f64); the
+    // workspace covers the largest chunk plan.
+    GemmPlan p = plan_gemm_f64_cfg(op, Mo, K, std::min(N, 256), num_sms, -1);
+    for (int n0 = 256; n0 < N; n0 += 256)
+        p.ws_elems = std::max(p.ws_elems, plan_gemm_f64_cfg(op, Mo, K, std::min(256, N - n0), num_sms, -1).ws_elems);
     return p;
 }
 
 cudaError_t gemm_f64(Op op, const double* A, int64_t lda, const double* X, int64_t ldx, double* C, int64_t ldc,
                      int64_t Mo, int64_t K, int N, const GemmPlan& p, double* ws, cudaStream_t st) {
     if (Mo <= 0 || N <= 0) return cudaSuccess;
-    if (N > p.bn) {  // sketch widths beyond one CTA tile: independent column chunks of X and C
-        for (int n0 = 0; n0 < N; n0 += p.bn) {
-            const int nc = std::min(p.bn, N - n0);
-            const GemmPlan q = plan_gemm_f64(op, Mo, K, nc, 148);
+    if (N > 256) {  // independent column chunks of X and C (plans are built for <= 256 columns)
+        for (int n0 = 0; n0 < N; n0 += 256) {
+            const int nc = std::min(256, N - n0);
+            const GemmPlan q = plan_gemm_f64_cfg(op, Mo, K, nc, p.num_sms, -1);
             cudaError_t e = gemm_f64(op, A, lda, X + n0, ldx, C + n0, ldc, Mo, K, nc, q, ws, st);
             if (e != cudaSuccess) return e;
         }
         return cudaSuccess;
     }
-    const int wn = p.bn / 32, wm = p.bm / 32;
-#define CORU_CASE(WM_, WN_)                                                                   \
-    if (wm == WM_ && wn == WN_)                                                               \
-        return op == Op::N ? launch<WM_, WN_, false>(A, lda, X, ldx, C, ldc, Mo, K, N, p, ws, st) \
-                           : launch<WM_, WN_, true>(A, lda, X, ldx, C, ldc, Mo, K, N, p, ws, st);
-    CORU_CASE(4, 1)
-    CORU_CASE(4, 2)
-    CORU_CASE(2, 3)
-    CORU_CASE(2, 4)
-    CORU_CASE(1, 5)
-    CORU_CASE(1, 6)
-    CORU_CASE(1, 7)
-    CORU_CASE(1, 8)
+#define CORU_CASE(id, wm, wn, mt, bk, st_)                                                                   \
+    if (p.cfg == id)                                                                                           \
+        return op == Op::N                                                                                     \
+                   ? launch_cfg<Cfg<wm, wn, mt, bk, st_, false>>(A, lda, X, ldx, C, ldc, Mo, K, N, p, ws, st)  \
+                   : launch_cfg<Cfg<wm, wn, mt, bk, st_, true>>(A, lda, X, ldx, C, ldc, Mo, K, N, p, ws, st);
+    CORU_GEMM_CONFIGS(CORU_CASE)
 #undef CORU_CASE
     return cudaErrorInvalidValue;
 }
