@@ -316,25 +316,29 @@ __global__ void __launch_bounds__(S::NT, S::min_blocks)
 }
 
 // Fix-up of the split tiles: C(tile) = sum of its segments in CTA order (fixed order).
-// grid = (tiles, element chunks of 256): every thread owns one element of one tile.
+// grid = (P - 1 CTA boundaries, element chunks of 256): block c handles the tile that CTA c starts
+// inside of, if CTA c is that tile's first boundary (so every split tile is summed exactly once).
 __global__ void k_streamk_fixup(const double* __restrict__ ws, int max_seg, int bm, int bn, int64_t ktiles,
                                 int64_t iters, int P, double* __restrict__ C, int64_t ldc, int64_t Mo, int N) {
-    const int64_t tile = blockIdx.x;
+    const int c = blockIdx.x + 1;
+    const int64_t g = sk_begin(iters, P, c);
+    if (g % ktiles == 0) return;  // CTA c starts on a tile boundary: nothing split here
+    const int64_t tile = g / ktiles;
+    const int first = sk_owner(iters, P, tile * ktiles);
+    if (first != c - 1) return;   // an earlier boundary already owns this tile's fix-up
+    const int last = sk_owner(iters, P, tile * ktiles + ktiles - 1);
     const int tiles_n = (N + bn - 1) / bn;
     const int n0 = int(tile % tiles_n) * bn;
-    const int first = sk_owner(iters, P, tile * ktiles);
-    const int last = sk_owner(iters, P, tile * ktiles + ktiles - 1);
-    if (first == last) return;  // written directly by its only owner
     const int64_t tile_elems = int64_t(bm) * bn;
     const int e = blockIdx.y * blockDim.x + threadIdx.x;
     if (e >= tile_elems) return;
-    const int r = e / bn, c = e % bn;
+    const int r = e / bn, cc = e % bn;
     const int64_t row = (tile / tiles_n) * bm + r;
-    if (row >= Mo || n0 + c >= N) return;
+    if (row >= Mo || n0 + cc >= N) return;
     const double* base = ws + tile * max_seg * tile_elems + e;
     double s = base[0];
     for (int q = 1; q <= last - first; ++q) s += base[q * tile_elems];
-    C[row * ldc + n0 + c] = s;
+    C[row * ldc + n0 + cc] = s;
 }
 
 // ---- configuration table -------------------------------------------------------------------
@@ -403,7 +407,7 @@ cudaError_t launch_cfg(const double* A, int64_t lda, const double* X, int64_t ld
     }
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess || !p.fixup) return e;
-    const dim3 grid(unsigned(tiles), unsigned((S::BM * S::BN + 255) / 256));
+    const dim3 grid(unsigned(std::max(1, p.splits - 1)), unsigned((S::BM * S::BN + 255) / 256));
     k_streamk_fixup<<<grid, 256, 0, st>>>(ws, p.max_seg, S::BM, S::BN, ktiles, iters, p.splits, C, ldc, Mo, N);
     return cudaGetLastError();
 }

@@ -674,8 +674,11 @@ TsqrPlan plan_tsqr(int64_t m, int d, size_t eb, int max_smem) {
             rb_big = rb;
             break;
         }
-    const bool blocked_ok = rb_blocked >= d + 1 + d / 4;  // at least a 1.25x reduction per level
     const bool big_ok = rb_big >= 2 * d + 2;
+    // The shared-memory kernels are fastest per block, but when they cannot reduce a level by at
+    // least 2x (wide sketches: d = 110 fits only ~168 rows) the tree gets deep and every level
+    // costs d sequential reflector steps; then the L2-resident kernels with ~1024-row blocks win.
+    const bool blocked_ok = rb_blocked >= 2 * d + 2 || (rb_blocked >= d + 1 + d / 4 && !big_ok);
     int target;
     if (blocked_ok) target = rb_blocked;
     else if (big_ok) target = std::min(rb_big, std::max(4 * d, 1024));
