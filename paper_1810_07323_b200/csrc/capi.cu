@@ -31,7 +31,8 @@
 
 namespace coru_gpu {
 template <typename OutT>
-void gaussian_host(int64_t rows, int64_t cols, uint64_t seed, uint64_t stream, OutT* out, int64_t ldo, int threads);
+void gaussian_host(int64_t rows, int64_t cols, uint64_t seed, uint64_t stream, OutT* out, int64_t ldo, int threads,
+                   int streaming);
 }  // namespace coru_gpu
 
 using namespace coru_gpu;
@@ -483,8 +484,7 @@ int run_impl(coru_ctx* c, const Request<T>& r, size_t extra_arena_off) {
     CORU_TRY(ensure_pinned(c, phi_bytes));
     CORU_CUDA(cudaStreamSynchronize(st));  // the pinned staging buffer is reused across calls
     T* phi = reinterpret_cast<T*>(c->pinned);
-    if (dp != d) std::memset(phi, 0, phi_bytes);
-    gaussian_host<T>(N, d, r.seed, r.stream, phi, dp, c->host_threads);
+    gaussian_host<T>(N, d, r.seed, r.stream, phi, dp, c->host_threads, 1);  // streaming stores, zero padding
     CORU_CUDA(cudaMemcpyAsync(w.b2, phi, phi_bytes, cudaMemcpyHostToDevice, st));
     CORU_CUDA(cudaMemsetAsync(w.q1, 0, size_t(R) * dp * sizeof(T), st));
     CORU_CUDA(cudaMemsetAsync(w.q2, 0, size_t(N) * dp * sizeof(T), st));
@@ -1034,7 +1034,7 @@ int coru_project_f64_dev(coru_ctx* c, const double* A, int64_t m_local, int64_t 
 
 int coru_gaussian(int64_t rows, int64_t cols, uint64_t seed, uint64_t stream, double* out, int threads) {
     if (rows < 1 || cols < 1 || !out) return fail(CORU_EINVAL, "Matrix: dimensions must be positive");
-    gaussian_host<double>(rows, cols, seed, stream, out, cols, threads);
+    gaussian_host<double>(rows, cols, seed, stream, out, cols, threads, 0);
     return CORU_OK;
 }
 

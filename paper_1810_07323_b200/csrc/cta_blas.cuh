@@ -76,10 +76,17 @@ __device__ __forceinline__ void cta_gemm(int M, int N, int K, FA A, FB B, FC C, 
 // split and the partial tiles are reduced in a fixed order through `scratch` (deterministic).
 // Must be called by every thread of the CTA; inputs must be visible (synchronised) on entry and
 // outputs are visible to all threads only after the caller's next __syncthreads().
+// warp0/nwarps: the participating warps (default: the whole CTA). With a subset, the split-K
+// reduction synchronises them through named barrier `bar_id` instead of __syncthreads.
 __device__ __forceinline__ void cta_mm_f64(int M, int N, int K, const double* A, int ars, int acs, const double* B,
                                            int brs, int bcs, double* C, int crs, int ccs, double alpha,
-                                           bool accumulate, double* scratch, int scratch_elems) {
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+                                           bool accumulate, double* scratch, int scratch_elems, int warp0 = 0,
+                                           int nwarps = -1, int bar_id = 15) {
+    const int lane = threadIdx.x & 31;
+    const int all = int(blockDim.x >> 5);
+    const int nw = nwarps < 0 ? all : nwarps;
+    const int warp = int(threadIdx.x >> 5) - warp0;
+    if (warp < 0 || warp >= nw) return;
     const int g = lane >> 2, t = lane & 3;
     const int tm = (M + 15) >> 4, tn = (N + 7) >> 3, tiles = tm * tn;
     if (tiles == 0 || K <= 0) return;
@@ -122,8 +129,9 @@ __device__ __forceinline__ void cta_mm_f64(int M, int N, int K, const double* A,
         }
     }
     if (S > 1) {
-        __syncthreads();
-        for (int e = threadIdx.x; e < tiles * 128; e += blockDim.x) {
+        if (nw == all) __syncthreads();
+        else asm volatile("bar.sync %0, %1;\n" ::"r"(bar_id), "r"(nw * 32) : "memory");
+        for (int e = warp * 32 + lane; e < tiles * 128; e += nw * 32) {
             const int tile = e >> 7, ln = (e >> 2) & 31, el = e & 3;
             const int i = ((tile / tn) << 4) + (ln >> 2) + ((el >> 1) << 3);
             const int j = ((tile % tn) << 3) + 2 * (ln & 3) + (el & 1);
@@ -154,8 +162,8 @@ __device__ __forceinline__ void cta_mm_simt(int M, int N, int K, const T* A, int
 
 __device__ __forceinline__ void cta_mm(int M, int N, int K, const double* A, int ars, int acs, const double* B, int brs,
                                        int bcs, double* C, int crs, int ccs, double alpha, bool accumulate,
-                                       double* scratch, int scratch_elems) {
-    cta_mm_f64(M, N, K, A, ars, acs, B, brs, bcs, C, crs, ccs, alpha, accumulate, scratch, scratch_elems);
+                                       double* scratch, int scratch_elems, int warp0 = 0, int nwarps = -1) {
+    cta_mm_f64(M, N, K, A, ars, acs, B, brs, bcs, C, crs, ccs, alpha, accumulate, scratch, scratch_elems, warp0, nwarps);
 }
 __device__ __forceinline__ void cta_mm(int M, int N, int K, const float* A, int ars, int acs, const float* B, int brs,
                                        int bcs, float* C, int crs, int ccs, float alpha, bool accumulate,
@@ -165,24 +173,42 @@ __device__ __forceinline__ void cta_mm(int M, int N, int K, const float* A, int 
 
 // Forward compact-WY T factor (LAPACK dlarft convention): H_0 H_1 ... H_{k-1} = I - V T V^T with
 // T upper triangular, T(j,j) = beta_j and T(0:j, j) = -beta_j T(0:j, 0:j) G(0:j, j), where
-// G(a,b) = v_a^T v_b (a < b) is given (ldg). One warp. For k <= 16 each row of T gets two lanes
-// (the c-range split in halves, one shuffle to combine), which halves the serial chain.
+// G(a,b) = v_a^T v_b (a < b) is given (ldg). One warp. For k <= 16 lane a owns row a of T in
+// registers (see below); wider panels use the generic shared-memory loop.
 template <typename T>
 __device__ __forceinline__ void warp_larft(int k, const T* G, int ldg, const T* beta, T* Tm, int ldt) {
     const int lane = threadIdx.x & 31;
     if (k <= 16) {
-        const int a = lane >> 1, half = lane & 1;
-        for (int b = 0; b < k; ++b) {
-            T s = 0;
-            if (a < b) {
-                const int mid = (a + b) >> 1;
-                const int c0 = half ? mid : a, c1 = half ? b : mid;
-                for (int c = c0; c < c1; ++c) s += Tm[a * ldt + c] * G[c * ldg + b];
+        // Lane a keeps row a of T in registers; the loops are fully unrolled so every register
+        // index is static, and column b of G is read as broadcast loads (no dependent smem chain).
+        // Row a is zero left of the diagonal, so the sum needs no predicate; columns b >= k are
+        // computed from clamped (finite or not, never stored) entries and discarded.
+        const int a = lane;
+        T row[16];
+#pragma unroll
+        for (int c = 0; c < 16; ++c) row[c] = T(0);
+#pragma unroll
+        for (int b = 0; b < 16; ++b) {
+            const T bb = beta[b < k ? b : k - 1];
+            // Branch-free: the newest entry row[b-1] enters last, so the per-column critical path is
+            // two dependent FMAs; fma(-bb, s, 0) rounds exactly like -bb * s.
+            T p0 = 0, p1 = 0;
+#pragma unroll
+            for (int c = 0; c + 1 < b; ++c) {
+                const T gv = G[c * ldg + b];
+                if (c & 1) p1 = fma(row[c], gv, p1);
+                else p0 = fma(row[c], gv, p0);
             }
-            s += __shfl_xor_sync(0xffffffffu, s, 1);
-            if (half == 0 && a < k) Tm[a * ldt + b] = a < b ? -beta[b] * s : (a == b ? beta[b] : T(0));
-            __syncwarp();
+            const T s = b > 0 ? fma(row[b - 1], G[(b - 1) * ldg + b], p0 + p1) : T(0);
+            const T coef = a < b ? -bb : T(0), diag = a == b ? bb : T(0);
+            row[b] = fma(coef, s, diag);
         }
+        if (a < k) {
+#pragma unroll
+            for (int c = 0; c < 16; ++c)
+                if (c < k) Tm[a * ldt + c] = row[c];
+        }
+        __syncwarp();
         return;
     }
     for (int b = 0; b < k; ++b) {

@@ -23,6 +23,8 @@
 #include <thread>
 #include <vector>
 
+#include <emmintrin.h>
+
 namespace coru_gpu {
 
 namespace {
@@ -195,11 +197,27 @@ Pool& pool() {
 
 }  // namespace
 
+// Non-temporal 8/4-byte store: the staging buffer is read next by a DMA engine, and a PCIe read of
+// lines left dirty in the CPU caches runs ~8x slower than one from memory (measured on the B200
+// box: 2 MB in ~340 us dirty vs ~43 us written with movnti).
+inline void store_stream(double* p, double v) {
+    long long b;
+    std::memcpy(&b, &v, 8);
+    _mm_stream_si64(reinterpret_cast<long long*>(p), b);
+}
+inline void store_stream(float* p, float v) {
+    int b;
+    std::memcpy(&b, &v, 4);
+    _mm_stream_si32(reinterpret_cast<int*>(p), b);
+}
+
 // Writes rows x cols Gaussians; element e (row-major index) goes to out[(e / cols) * ldo + e % cols]
 // converted to OutT (fp32 rounds the fp64 value). Identical output for any thread count.
+// streaming != 0: non-temporal stores, and the padding columns [cols, ldo) of every row are zeroed
+// (the buffer is a DMA source; see store_stream).
 template <typename OutT>
 void gaussian_host(int64_t rows, int64_t cols, uint64_t seed, uint64_t stream, OutT* out, int64_t ldo,
-                   int threads) {
+                   int threads, int streaming) {
     const int64_t total = rows * cols;
     const int64_t pairs = (total + 1) / 2;
     const State s0 = seed_state(seed, stream);
@@ -211,8 +229,14 @@ void gaussian_host(int64_t rows, int64_t cols, uint64_t seed, uint64_t stream, O
         State st = t == 0 ? s0 : jump(s0, uint64_t(2 * p0));
         int64_t e = 2 * p0, r = e / cols, c = e % cols;
         auto put = [&](double v) {
-            out[r * ldo + c] = static_cast<OutT>(v);
+            if (streaming) {
+                store_stream(out + r * ldo + c, static_cast<OutT>(v));
+            } else {
+                out[r * ldo + c] = static_cast<OutT>(v);
+            }
             if (++c == cols) {
+                if (streaming)
+                    for (int64_t z = cols; z < ldo; ++z) store_stream(out + r * ldo + z, OutT(0));
                 c = 0;
                 ++r;
             }
@@ -226,10 +250,11 @@ void gaussian_host(int64_t rows, int64_t cols, uint64_t seed, uint64_t stream, O
             put(rad * std::cos(theta));
             if (2 * p + 1 < total) put(sv);
         }
+        if (streaming) _mm_sfence();
     });
 }
 
-template void gaussian_host<double>(int64_t, int64_t, uint64_t, uint64_t, double*, int64_t, int);
-template void gaussian_host<float>(int64_t, int64_t, uint64_t, uint64_t, float*, int64_t, int);
+template void gaussian_host<double>(int64_t, int64_t, uint64_t, uint64_t, double*, int64_t, int, int);
+template void gaussian_host<float>(int64_t, int64_t, uint64_t, uint64_t, float*, int64_t, int, int);
 
 }  // namespace coru_gpu

@@ -29,6 +29,29 @@
 
 namespace coru_gpu {
 
+#ifdef CORU_QR_PROFILE
+__device__ long long g_qr_phase[12];  // cycles of block 0: load, panel chains, T factors, trailing, export
+__device__ __forceinline__ long long qrp_clock() {
+    long long v;
+    asm volatile("mov.u64 %0, %%clock64;" : "=l"(v)::"memory");
+    return v;
+}
+#define QRP_T(v) long long v = qrp_clock()
+#define QRP_NS(v) unsigned long long v; asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(v))
+#define QRP_NSADD(i, t0) if (threadIdx.x == 0 && blockIdx.x == 0) { unsigned long long t1_; asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1_)); g_qr_phase[i] += t1_ - (t0); }
+// per-thread register accumulators; block 0 / thread 0 flushes them once at the end
+#define QRP_DECL long long qrp_acc[8] = {0, 0, 0, 0, 0, 0, 0, 0}
+#define QRP_ADD(i, t0) qrp_acc[i] += qrp_clock() - (t0)
+#define QRP_FLUSH if (threadIdx.x == 0 && blockIdx.x == 0) for (int i_ = 0; i_ < 8; ++i_) g_qr_phase[i_] += qrp_acc[i_]
+#else
+#define QRP_T(v)
+#define QRP_ADD(i, t0)
+#define QRP_NS(v)
+#define QRP_NSADD(i, t0)
+#define QRP_DECL
+#define QRP_FLUSH
+#endif
+
 namespace {
 
 constexpr int kThreads = 256;
@@ -288,6 +311,10 @@ __global__ void __launch_bounds__(kBThreads, 1)
     const int ldw = S.ldw, ldvp = S.ldvp;
     T* Tb = Tg + int64_t(b) * npanels(d) * kNB * kNB;  // this block's panel T factors
 
+    QRP_DECL;
+    QRP_NS(ns_all);
+    QRP_T(t_all);
+    QRP_T(t_load);
     // Load rows [r0, r1) (row-major, coalesced along columns) into column-major W; four rows in
     // flight per warp for memory-level parallelism.
     for (int cb = 0; cb < d; cb += 128)
@@ -310,8 +337,10 @@ __global__ void __launch_bounds__(kBThreads, 1)
         }
     __syncthreads();
 
+    QRP_ADD(0, t_load);
     for (int p0 = 0, pi = 0; p0 < d; p0 += kNB, ++pi) {
         const int nbp = min(kNB, d - p0);
+        QRP_T(t_chain);
         // ---- panel factorisation: warp w owns column p0 + w; rows >= p0 in registers ----
         if (warp < nbp) {
             const int c = p0 + warp;
@@ -389,29 +418,46 @@ __global__ void __launch_bounds__(kBThreads, 1)
             }
         }
         __syncthreads();
+        QRP_ADD(1, t_chain);
+        QRP_T(t_tf);
         const int K = rb - p0;
+        const int c0 = p0 + nbp, nc = d - c0;
+        T* C = W + c0 * ldw + p0;
         // ---- panel T factor: G = V_p^T V_p, T_p by the forward recurrence ----
         cta_mm(nbp, nbp, K, S.Vp + p0, ldvp, 1, S.Vp + p0, 1, ldvp, S.Gp, kNB, 1, T(1), false, S.scratch, kGemmScratch);
+        QRP_ADD(6, t_tf);
         __syncthreads();
+        QRP_ADD(5, t_tf);
+        // The recurrence (one warp) overlaps Y = V_p^T C on the other warps (fp64 tensor path).
+        constexpr bool kOverlap = sizeof(T) == 8;
         if (warp == 0) {
             warp_larft<T>(nbp, S.Gp, kNB, S.beta + p0, S.Tp, kNB);
             T* Tpg = Tb + pi * kNB * kNB;
             for (int e = lane; e < kNB * kNB; e += 32) Tpg[e] = S.Tp[e];
+        } else if constexpr (kOverlap) {
+            if (nc > 0)
+                cta_mm_f64(nbp, nc, K, reinterpret_cast<const double*>(S.Vp + p0), ldvp, 1,
+                           reinterpret_cast<const double*>(C), 1, ldw, reinterpret_cast<double*>(S.Y), d, 1, 1.0,
+                           false, reinterpret_cast<double*>(S.scratch), kGemmScratch, 1, kBThreads / 32 - 1, 15);
         }
         __syncthreads();
+        QRP_ADD(2, t_tf);
+        QRP_T(t_tr);
         // ---- trailing update of columns [p0+nbp, d): C <- C - V_p T_p^T (V_p^T C), rows >= p0 ----
-        const int c0 = p0 + nbp, nc = d - c0;
         if (nc > 0) {
-            T* C = W + c0 * ldw + p0;
-            cta_mm(nbp, nc, K, S.Vp + p0, ldvp, 1, C, 1, ldw, S.Y, d, 1, T(1), false, S.scratch, kGemmScratch);
-            __syncthreads();
+            if constexpr (!kOverlap) {
+                cta_mm(nbp, nc, K, S.Vp + p0, ldvp, 1, C, 1, ldw, S.Y, d, 1, T(1), false, S.scratch, kGemmScratch);
+                __syncthreads();
+            }
             cta_mm(nbp, nc, nbp, S.Tp, 1, kNB, S.Y, d, 1, S.Z, d, 1, T(1), false, S.scratch, kGemmScratch);
             __syncthreads();
             cta_mm(K, nc, nbp, S.Vp + p0, 1, ldvp, S.Z, d, 1, C, 1, ldw, T(-1), true, S.scratch, kGemmScratch);
             __syncthreads();
         }
+        QRP_ADD(3, t_tr);
     }
 
+    QRP_T(t_exp);
     // R (upper, exact zeros below) -> Rout rows [b*d, (b+1)*d); reflectors and betas to global.
     for (int e = tid; e < d * d; e += kBThreads) {
         const int r = e / d, c = e % d;
@@ -422,6 +468,10 @@ __global__ void __launch_bounds__(kBThreads, 1)
     T* Vb = V + int64_t(b) * d * ldv;
     for (int c = warp; c < d; c += kBThreads / 32)
         for (int r = lane; r < rb; r += 32) Vb[int64_t(c) * ldv + r] = r > c ? W[c * ldw + r] : T(r == c ? 1 : 0);
+    QRP_ADD(4, t_exp);
+    QRP_ADD(7, t_all);
+    QRP_FLUSH;
+    QRP_NSADD(8, ns_all);
 }
 
 // Same algorithm with the working block in global memory (L2) — blocks too tall or too wide for
