@@ -59,10 +59,18 @@ const char* coru_last_error(void);
 
 int coru_ctx_create(int device, coru_ctx** out);
 void coru_ctx_destroy(coru_ctx* ctx);
-/* Run on the caller's cudaStream_t (NULL restores the context-owned stream). */
+/* Run on the caller's cudaStream_t (NULL restores the context-owned non-blocking stream; pass
+ * cudaStreamLegacy for the legacy default stream). */
 int coru_ctx_set_stream(coru_ctx* ctx, void* cuda_stream);
 /* Host threads used for the bit-exact Gaussian test matrix (default: hardware concurrency). */
 int coru_ctx_set_host_threads(coru_ctx* ctx, int threads);
+/* Where corutv draws Φ (corutv.hpp:51):
+ *   CORU_PHI_DEVICE (default): generated on the GPU — the reference's xoshiro256++ word stream
+ *     bit-for-bit, Box–Muller with the device log/sincos (entries within a few ulp of the host's);
+ *   CORU_PHI_HOST_EXACT: generated on the host with the host libm (bit-identical to the
+ *     reference's gaussian()) and copied in. */
+enum { CORU_PHI_DEVICE = 0, CORU_PHI_HOST_EXACT = 1 };
+int coru_ctx_set_phi_mode(coru_ctx* ctx, int mode);
 
 /* ---- multi-GPU: one process (and context) per GPU, A row-block sharded --------------------- */
 /* Rank 0 creates the id and distributes it (e.g. torch.distributed broadcast); every rank then
@@ -128,6 +136,10 @@ int coru_project_f64_dev(coru_ctx* ctx, const double* A, int64_t m_local, int64_
 
 /* ---- the test matrix Φ: gaussian(rows, cols, {seed, stream}) (rng.hpp:107-112), host --------- */
 int coru_gaussian(int64_t rows, int64_t cols, uint64_t seed, uint64_t stream, double* out, int threads);
+/* Device variant (CORU_PHI_DEVICE's generator): out is a device pointer with leading dimension
+ * ldo >= cols (padding columns are zeroed), enqueued on the context's stream. */
+int coru_gaussian_f64_dev(coru_ctx* ctx, int64_t rows, int64_t cols, uint64_t seed, uint64_t stream, double* out,
+                          int64_t ldo);
 
 /* ---- kernel-level entry points (parity tests and benchmarks of the A-pass kernels) ----------- */
 /* C (rows x N) = op(A) · X, op 0: A (rows x K), op 1: A^T with A (K x rows); device row-major. */

@@ -135,6 +135,7 @@ def load_library():
     L.coru_ctx_destroy.restype = None
     L.coru_ctx_set_stream.argtypes = [p, p]
     L.coru_ctx_set_host_threads.argtypes = [p, i32]
+    L.coru_ctx_set_phi_mode.argtypes = [p, i32]
     L.coru_comm_unique_id.argtypes = [p]
     L.coru_ctx_init_comm.argtypes = [p, i32, i32, p]
     L.coru_ctx_set_profiling.argtypes = [p, i32]
@@ -157,6 +158,7 @@ def load_library():
     L.coru_sketch_bases_f64.argtypes = [p, p, i64, i64, i64, i32, u64, u64, p, p, p, p, C.POINTER(i32)]
     L.coru_project_f64_dev.argtypes = [p, p, i64, i64, i64, p, i64, p, i64, i64, p, i64]
     L.coru_gaussian.argtypes = [i64, i64, u64, u64, p, i32]
+    L.coru_gaussian_f64_dev.argtypes = [p, i64, i64, u64, u64, p, i64]
     L.coru_gemm_f64_dev.argtypes = [p, i32, p, i64, p, i64, p, i64, i64, i64, i64]
     L.coru_gemm_f32_dev.argtypes = [p, i32, p, i64, p, i64, p, i64, i64, i64, i64]
     L.coru_tsqr_f64_dev.argtypes = [p, p, i64, i64, i64, p, i64, p, i64]
@@ -215,6 +217,14 @@ class Context:
 
     def set_host_threads(self, n: int):
         _check(self.lib.coru_ctx_set_host_threads(self.h, n))
+
+    PHI_DEVICE, PHI_HOST_EXACT = 0, 1
+
+    def set_phi_mode(self, mode: int):
+        """PHI_DEVICE (default): Φ generated on the GPU (reference word stream bit-for-bit, Box–Muller
+        values within a few ulp of the host libm's); PHI_HOST_EXACT: host-generated, bit-identical
+        to the reference's gaussian()."""
+        _check(self.lib.coru_ctx_set_phi_mode(self.h, mode))
 
     def set_profiling(self, on: bool):
         _check(self.lib.coru_ctx_set_profiling(self.h, 1 if on else 0))
@@ -286,9 +296,15 @@ def _np_dtype_suffix(dt) -> str:
     raise CoruInvalidArgument(f"unsupported dtype {dt}")
 
 
+_CUDA_STREAM_LEGACY = 0x1  # cudaStreamLegacy: torch's default stream reports handle 0
+
+
 def _torch_sync_stream(ctx: Context, a):
+    """Enqueue the library's work on torch's current stream (ordered with the tensors' producers
+    and consumers). Handle 0 would select the context's own non-blocking stream instead."""
     import torch
-    ctx.set_stream(torch.cuda.current_stream(a.device).cuda_stream)
+    h = torch.cuda.current_stream(a.device).cuda_stream
+    ctx.set_stream(h if h else _CUDA_STREAM_LEGACY)
 
 
 def corutv(a, ell: int, q: int, variant: DVariant = DVariant.exact, seed: RngSeed = RngSeed(),
@@ -387,6 +403,18 @@ def gaussian(rows: int, cols: int, seed: RngSeed = RngSeed(), threads: int = 1) 
     """rng.hpp:107-112 — host generator of the test matrix Φ, bit-exact with the reference."""
     out = np.empty((rows, cols), np.float64)
     _check(load_library().coru_gaussian(rows, cols, seed.seed, seed.stream, out.ctypes.data, threads))
+    return out
+
+
+def gaussian_device(rows: int, cols: int, seed: RngSeed = RngSeed(), ctx: "Context | None" = None, ld: int | None = None):
+    """Device generator of Φ (the CORU_PHI_DEVICE path): a (rows, ld) float64 CUDA tensor whose first
+    `cols` columns hold gaussian(rows, cols, seed) and the rest zeros."""
+    import torch
+    ctx = ctx or default_context()
+    ld = ld or cols
+    out = torch.empty((rows, ld), dtype=torch.float64, device=f"cuda:{ctx.device}")
+    _torch_sync_stream(ctx, out)
+    _check(ctx.lib.coru_gaussian_f64_dev(ctx.h, rows, cols, seed.seed, seed.stream, out.data_ptr(), ld))
     return out
 
 

@@ -27,6 +27,7 @@
 #include "../../include/coru_gpu.h"
 #include "gemm.cuh"
 #include "qrcp.cuh"
+#include "rng_dev.cuh"
 #include "tsqr.cuh"
 
 namespace coru_gpu {
@@ -167,6 +168,7 @@ struct coru_ctx {
     int num_sms = 148;
     int max_smem = 227 * 1024;
     int host_threads = 1;
+    int phi_mode = CORU_PHI_DEVICE;
     char* arena = nullptr;
     size_t arena_bytes = 0;
     char* pinned = nullptr;
@@ -479,13 +481,21 @@ int run_impl(coru_ctx* c, const Request<T>& r, size_t extra_arena_off) {
     Carver cv{c->arena, extra_arena_off};
     w.layout(cv, c, r, dp);
 
-    // Φ = gaussian(cols, ell, seed) on the host, padded to dp columns, one H2D (corutv.hpp:51).
-    const size_t phi_bytes = size_t(N) * dp * sizeof(T);
-    CORU_TRY(ensure_pinned(c, phi_bytes));
-    CORU_CUDA(cudaStreamSynchronize(st));  // the pinned staging buffer is reused across calls
-    T* phi = reinterpret_cast<T*>(c->pinned);
-    gaussian_host<T>(N, d, r.seed, r.stream, phi, dp, c->host_threads, 1);  // streaming stores, zero padding
-    CORU_CUDA(cudaMemcpyAsync(w.b2, phi, phi_bytes, cudaMemcpyHostToDevice, st));
+    // Φ = gaussian(cols, ell, seed), padded to dp columns (corutv.hpp:51): on the device, or on the
+    // host with the host libm (bit-exact) and one H2D.
+    if (c->phi_mode == CORU_PHI_DEVICE) {
+        uint64_t s4[4];
+        seed_state_words(r.seed, r.stream, s4);
+        CORU_CUDA(gaussian_dev<T>(N, d, s4, w.b2, dp, st));
+        ++g_launches;
+    } else {
+        const size_t phi_bytes = size_t(N) * dp * sizeof(T);
+        CORU_TRY(ensure_pinned(c, phi_bytes));
+        CORU_CUDA(cudaStreamSynchronize(st));  // the pinned staging buffer is reused across calls
+        T* phi = reinterpret_cast<T*>(c->pinned);
+        gaussian_host<T>(N, d, r.seed, r.stream, phi, dp, c->host_threads, 1);  // streaming stores, zero padding
+        CORU_CUDA(cudaMemcpyAsync(w.b2, phi, phi_bytes, cudaMemcpyHostToDevice, st));
+    }
     CORU_CUDA(cudaMemsetAsync(w.q1, 0, size_t(R) * dp * sizeof(T), st));
     CORU_CUDA(cudaMemsetAsync(w.q2, 0, size_t(N) * dp * sizeof(T), st));
 
@@ -837,6 +847,13 @@ int coru_ctx_set_host_threads(coru_ctx* c, int threads) {
     return CORU_OK;
 }
 
+int coru_ctx_set_phi_mode(coru_ctx* c, int mode) {
+    if (!c || (mode != CORU_PHI_DEVICE && mode != CORU_PHI_HOST_EXACT)) return fail(CORU_EINVAL, "bad argument");
+    std::lock_guard<std::mutex> lk(c->mu);
+    c->phi_mode = mode;
+    return CORU_OK;
+}
+
 int coru_comm_unique_id(unsigned char id[128]) {
     Nccl* api = nccl();
     if (!api) return fail(CORU_ENCCL, "NCCL unavailable");
@@ -1035,6 +1052,18 @@ int coru_project_f64_dev(coru_ctx* c, const double* A, int64_t m_local, int64_t 
 int coru_gaussian(int64_t rows, int64_t cols, uint64_t seed, uint64_t stream, double* out, int threads) {
     if (rows < 1 || cols < 1 || !out) return fail(CORU_EINVAL, "Matrix: dimensions must be positive");
     gaussian_host<double>(rows, cols, seed, stream, out, cols, threads, 0);
+    return CORU_OK;
+}
+
+int coru_gaussian_f64_dev(coru_ctx* c, int64_t rows, int64_t cols, uint64_t seed, uint64_t stream, double* out,
+                          int64_t ldo) {
+    CORU_TRY(enter(c));
+    std::lock_guard<std::mutex> lk(c->mu);
+    if (rows < 1 || cols < 1 || ldo < cols || !out) return fail(CORU_EINVAL, "Matrix: dimensions must be positive");
+    uint64_t s4[4];
+    seed_state_words(seed, stream, s4);
+    CORU_CUDA(gaussian_dev<double>(rows, cols, s4, out, ldo, c->stream));
+    ++g_launches;
     return CORU_OK;
 }
 

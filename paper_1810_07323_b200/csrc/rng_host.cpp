@@ -197,6 +197,17 @@ Pool& pool() {
 
 }  // namespace
 
+const uint64_t* jump_table_words(int* nbits) {
+    static_assert(sizeof(Gf2) == 256 * 4 * sizeof(uint64_t), "dense table");
+    *nbits = kJumpBits;
+    return &jump_table()[0].row[0][0];
+}
+
+void seed_state_words(uint64_t seed, uint64_t stream, uint64_t out[4]) {
+    const State s = seed_state(seed, stream);
+    for (int i = 0; i < 4; ++i) out[i] = s.s[i];
+}
+
 // Non-temporal 8/4-byte store: the staging buffer is read next by a DMA engine, and a PCIe read of
 // lines left dirty in the CPU caches runs ~8x slower than one from memory (measured on the B200
 // box: 2 MB in ~340 us dirty vs ~43 us written with movnti).

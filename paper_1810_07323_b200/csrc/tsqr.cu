@@ -30,7 +30,8 @@
 namespace coru_gpu {
 
 #ifdef CORU_QR_PROFILE
-__device__ long long g_qr_phase[12];  // cycles of block 0: load, panel chains, T factors, trailing, export
+__device__ long long g_qr_phase[12];
+__device__ long long g_qr_tl[3 * 256];  // block 0 chain timeline: arrive / wake / build-start per column  // cycles of block 0: load, panel chains, T factors, trailing, export
 __device__ __forceinline__ long long qrp_clock() {
     long long v;
     asm volatile("mov.u64 %0, %%clock64;" : "=l"(v)::"memory");
@@ -42,6 +43,7 @@ __device__ __forceinline__ long long qrp_clock() {
 // per-thread register accumulators; block 0 / thread 0 flushes them once at the end
 #define QRP_DECL long long qrp_acc[8] = {0, 0, 0, 0, 0, 0, 0, 0}
 #define QRP_ADD(i, t0) qrp_acc[i] += qrp_clock() - (t0)
+#define QRP_TL(k, j) if (blockIdx.x == 0 && lane == 0) g_qr_tl[(k) * 256 + (j)] = qrp_clock()
 #define QRP_FLUSH if (threadIdx.x == 0 && blockIdx.x == 0) for (int i_ = 0; i_ < 8; ++i_) g_qr_phase[i_] += qrp_acc[i_]
 #else
 #define QRP_T(v)
@@ -49,6 +51,7 @@ __device__ __forceinline__ long long qrp_clock() {
 #define QRP_NS(v)
 #define QRP_NSADD(i, t0)
 #define QRP_DECL
+#define QRP_TL(k, j)
 #define QRP_FLUSH
 #endif
 
@@ -356,6 +359,7 @@ __global__ void __launch_bounds__(kBThreads, 1)
                 if (jj < warp) {
                     // apply H_j (built by warp jj) to my column   (apply_reflector, qr.hpp:49-57)
                     named_bar_sync(bar, cnt);
+                    if (jj + 1 == warp) QRP_TL(1, j + 1);
                     const T bj = S.beta[j];
                     if (bj == T(0)) continue;
                     const T* vj = S.Vp + jj * ldvp;
@@ -376,6 +380,7 @@ __global__ void __launch_bounds__(kBThreads, 1)
                     for (int u = 0; u < kRPL; ++u) x[u] -= s * v[u];
                 } else {
                     // build reflector j from my column   (make_reflector, qr.hpp:32-45)
+                    QRP_TL(2, j);
                     T sq[kRPL];
 #pragma unroll
                     for (int u = 0; u < kRPL; ++u) {
@@ -413,6 +418,7 @@ __global__ void __launch_bounds__(kBThreads, 1)
                         if (r < ldvp) vj[r] = (r > j && r < rb) ? x[u] : (r == j ? T(1) : T(0));
                     }
                     if (lane == 0) S.beta[j] = bj;
+                    QRP_TL(0, j);
                     if (jj + 1 < nbp) named_bar_arrive(bar, cnt);
                 }
             }

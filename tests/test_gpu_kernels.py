@@ -115,3 +115,40 @@ def test_gemm_f32_matches_oracle(ctx, oracle, m, n, d, op):
     K = n if op == 0 else m
     bound = ((np.abs(a) @ np.abs(x)) if op == 0 else (np.abs(a).T @ np.abs(x))).astype(np.float64)
     assert np.all(np.abs(c.astype(np.float64) - want) <= K * 2.0 ** -23 * bound + 1e-30)
+
+
+def _ulp_diff(x, y):
+    xi = x.astype(np.float64).view(np.int64)
+    yi = y.astype(np.float64).view(np.int64)
+    return np.abs(xi - yi)
+
+
+@pytest.mark.parametrize("rows,cols,ld,seed,stream", [(7, 9, 9, 42, 3), (1, 5, 8, 7, 0), (4001, 61, 64, 5, 2),
+                                                      (100, 100, 100, 42, 0), (65536, 520, 520, 42, 7)])
+def test_device_gaussian_matches_host(ctx, rows, cols, ld, seed, stream):
+    """rng_dev.cu vs the bit-exact host generator (rng.hpp:107-112): same xoshiro256++ word stream
+    (any word slip would show as O(1) differences), Box–Muller values within 4 ulp (device
+    log/sincos vs host libm), padding columns exactly zero."""
+    import paper_1810_07323_b200 as cg
+    g = cg.gaussian_device(rows, cols, cg.RngSeed(seed, stream), ctx=ctx, ld=ld).cpu().numpy()
+    h = cg.gaussian(rows, cols, cg.RngSeed(seed, stream), threads=16)
+    assert np.all(g[:, cols:] == 0.0)
+    u = _ulp_diff(g[:, :cols], h)
+    assert u.max() <= 4, u.max()
+    assert np.mean(u > 0) < 0.3
+
+
+def test_device_phi_corutv_agrees_with_host_exact(oracle):
+    """The default (device Φ) and the bit-exact host-Φ modes give the same decomposition to the
+    fp64 parity tolerances on a well-conditioned case."""
+    import paper_1810_07323_b200 as cg
+    rng = np.random.default_rng(3)
+    a = rng.standard_normal((600, 500))
+    c_dev, c_host = cg.Context(0), cg.Context(0)
+    c_host.set_phi_mode(cg.Context.PHI_HOST_EXACT)
+    f1 = cg.corutv(a, 20, 0, seed=cg.RngSeed(4, 1), ctx=c_dev)
+    f2 = cg.corutv(a, 20, 0, seed=cg.RngSeed(4, 1), ctx=c_host)
+    assert np.array_equal(f1.perm, f2.perm)
+    assert np.max(np.abs(np.abs(np.diag(f1.t)) - np.abs(np.diag(f2.t)))) <= 1e-12 * abs(f2.t[0, 0])
+    ref = oracle.corutv(a, 20, 0, seed=4, stream=1)
+    assert np.max(np.abs(np.abs(np.diag(f2.t)) - np.abs(np.diag(ref.t)))) <= 1e-12 * abs(ref.t[0, 0])

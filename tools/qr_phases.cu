@@ -26,4 +26,9 @@ int main(int argc, char** argv) {
         printf("m=%ld d=%d levels=%zu factor %.1f us | block0 cycles (summed over levels): load %lld chain %lld Tfac %lld trailing %lld export %lld | G %lld G-nosync %lld | total %lld cyc %lld ns (%s)\n",
                m, d, p.levels.size(), ms * 1e3, z[0], z[1], z[2], z[3], z[4], z[5], z[6], z[7], z[8], cudaGetErrorString(cudaGetLastError()));
     }
+    long long tl[3 * 256];
+    cudaMemcpyFromSymbol(tl, coru_gpu::g_qr_tl, sizeof(tl));
+    printf("col: barrier-wake apply build (cycles), last level block 0\n");
+    for (int j = 1; j < d; ++j)
+        if (j % 16) printf("%d: %lld %lld %lld\n", j, tl[256 + j] - tl[j - 1], tl[512 + j] - tl[256 + j], tl[j] - tl[512 + j]);
 }
