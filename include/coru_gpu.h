@@ -71,6 +71,12 @@ int coru_ctx_set_host_threads(coru_ctx* ctx, int threads);
  *     reference's gaussian()) and copied in. */
 enum { CORU_PHI_DEVICE = 0, CORU_PHI_HOST_EXACT = 1 };
 int coru_ctx_set_phi_mode(coru_ctx* ctx, int mode);
+/* fp32 A-pass engine (the fp32 configuration; matmul at corutv.hpp:55,57,90):
+ *   CORU_F32_AUTO (default): tcgen05 3xTF32 tensor-core kernel (TMA + TMEM) for A-pass-sized
+ *     products, CUDA-core FFMA otherwise;  CORU_F32_SIMT / CORU_F32_TC: force one engine
+ *     (CORU_F32_TC still uses FFMA where the tensor-core kernel cannot take the shape). */
+enum { CORU_F32_AUTO = 0, CORU_F32_SIMT = 1, CORU_F32_TC = 2 };
+int coru_ctx_set_f32_path(coru_ctx* ctx, int mode);
 
 /* ---- multi-GPU: one process (and context) per GPU, A row-block sharded --------------------- */
 /* Rank 0 creates the id and distributes it (e.g. torch.distributed broadcast); every rank then

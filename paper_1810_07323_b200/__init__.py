@@ -136,6 +136,7 @@ def load_library():
     L.coru_ctx_set_stream.argtypes = [p, p]
     L.coru_ctx_set_host_threads.argtypes = [p, i32]
     L.coru_ctx_set_phi_mode.argtypes = [p, i32]
+    L.coru_ctx_set_f32_path.argtypes = [p, i32]
     L.coru_comm_unique_id.argtypes = [p]
     L.coru_ctx_init_comm.argtypes = [p, i32, i32, p]
     L.coru_ctx_set_profiling.argtypes = [p, i32]
@@ -225,6 +226,13 @@ class Context:
         values within a few ulp of the host libm's); PHI_HOST_EXACT: host-generated, bit-identical
         to the reference's gaussian()."""
         _check(self.lib.coru_ctx_set_phi_mode(self.h, mode))
+
+    F32_AUTO, F32_SIMT, F32_TC = 0, 1, 2
+
+    def set_f32_path(self, mode: int):
+        """fp32 A-pass engine: F32_AUTO (default: tcgen05 3xTF32 tensor cores for A-pass-sized
+        products), F32_SIMT (CUDA-core FFMA), F32_TC (tensor cores wherever the shape allows)."""
+        _check(self.lib.coru_ctx_set_f32_path(self.h, mode))
 
     def set_profiling(self, on: bool):
         _check(self.lib.coru_ctx_set_profiling(self.h, 1 if on else 0))

@@ -169,6 +169,7 @@ struct coru_ctx {
     int max_smem = 227 * 1024;
     int host_threads = 1;
     int phi_mode = CORU_PHI_DEVICE;
+    int f32_path = CORU_F32_AUTO;
     char* arena = nullptr;
     size_t arena_bytes = 0;
     char* pinned = nullptr;
@@ -240,7 +241,16 @@ int64_t gemm_ws<double>(Op op, int64_t Mo, int64_t K, int N, int sms) {
 }
 template <>
 int64_t gemm_ws<float>(Op op, int64_t Mo, int64_t K, int N, int sms) {
-    return plan_gemm_f32(op, Mo, K, N, sms).ws_elems;
+    const int64_t simt = plan_gemm_f32(op, Mo, K, N, sms).ws_elems;
+    return gemm_tc32_eligible(Mo, K, N) ? std::max(simt, gemm_tc32_ws_elems(Mo, K, N, sms)) : simt;
+}
+
+// The tensor-core fp32 path takes A-pass-sized products (A streamed once per N-chunk); small
+// products (the core, the lift) stay on the FFMA kernel.
+bool use_tc32(const coru_ctx* c, Op op, const float* A, int64_t lda, int64_t Mo, int64_t K, int N) {
+    if (c->f32_path == CORU_F32_SIMT) return false;
+    if (!gemm_tc32_supported(op, A, lda, Mo, K, N)) return false;
+    return c->f32_path == CORU_F32_TC || Mo * K >= (int64_t(1) << 22);
 }
 
 template <typename T>
@@ -272,23 +282,28 @@ int gemm<double>(coru_ctx* c, Op op, const double* A, int64_t lda, const double*
         c->prof_flops += 2.0 * double(Mo) * double(K) * double(N);
         c->prof_bytes += 8.0 * double(Mo) * double(K);
     }
-    g_launches += p.splits > 1 ? 2 : 1;
+    g_launches += 1;  // stream-K fix-up runs inside the GEMM
     return CORU_OK;
 }
 template <>
 int gemm<float>(coru_ctx* c, Op op, const float* A, int64_t lda, const float* X, int64_t ldx, float* C, int64_t ldc,
                 int64_t Mo, int64_t K, int N, float* ws, int64_t ws_elems) {
+    const bool tc = use_tc32(c, op, A, lda, Mo, K, N);
     GemmPlan p = plan_gemm_f32(op, Mo, K, N, c->num_sms);
-    if (p.ws_elems > ws_elems) return fail(CORU_ECUDA, "internal: gemm workspace too small");
+    const int64_t need = tc ? gemm_tc32_ws_elems(Mo, K, N, c->num_sms) : p.ws_elems;
+    if (need > ws_elems) return fail(CORU_ECUDA, "internal: gemm workspace too small");
     cudaEvent_t stop = nullptr;
     if (c->prof) CORU_TRY(prof_begin(c, &stop));
-    CORU_CUDA(gemm_f32(op, A, lda, X, ldx, C, ldc, Mo, K, N, p, ws, c->stream));
+    if (tc)
+        CORU_CUDA(gemm_tc32(op, A, lda, X, ldx, C, ldc, Mo, K, N, ws, c->num_sms, c->max_smem, c->stream));
+    else
+        CORU_CUDA(gemm_f32(op, A, lda, X, ldx, C, ldc, Mo, K, N, p, ws, c->stream));
     if (stop) {
         CORU_CUDA(cudaEventRecord(stop, c->stream));
         c->prof_flops += 2.0 * double(Mo) * double(K) * double(N);
         c->prof_bytes += 4.0 * double(Mo) * double(K);
     }
-    g_launches += p.splits > 1 ? 2 : 1;
+    g_launches += tc ? gemm_tc32_launches(Mo, K, N, c->num_sms) : (p.splits > 1 ? 2 : 1);
     return CORU_OK;
 }
 
@@ -851,6 +866,13 @@ int coru_ctx_set_phi_mode(coru_ctx* c, int mode) {
     if (!c || (mode != CORU_PHI_DEVICE && mode != CORU_PHI_HOST_EXACT)) return fail(CORU_EINVAL, "bad argument");
     std::lock_guard<std::mutex> lk(c->mu);
     c->phi_mode = mode;
+    return CORU_OK;
+}
+
+int coru_ctx_set_f32_path(coru_ctx* c, int mode) {
+    if (!c || mode < CORU_F32_AUTO || mode > CORU_F32_TC) return fail(CORU_EINVAL, "bad argument");
+    std::lock_guard<std::mutex> lk(c->mu);
+    c->f32_path = mode;
     return CORU_OK;
 }
 

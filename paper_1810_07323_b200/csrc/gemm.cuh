@@ -34,4 +34,13 @@ GemmPlan plan_gemm_f32(Op op, int64_t Mo, int64_t K, int N, int num_sms);
 cudaError_t gemm_f32(Op op, const float* A, int64_t lda, const float* X, int64_t ldx, float* C, int64_t ldc,
                      int64_t Mo, int64_t K, int N, const GemmPlan& plan, float* ws, cudaStream_t stream);
 
+// fp32 A-pass on tcgen05 tensor cores (3xTF32, TMA + TMEM; gemm_tc32.cu). `ws` must hold
+// gemm_tc32_ws_elems floats. Call only when gemm_tc32_supported().
+bool gemm_tc32_supported(Op op, const float* A, int64_t lda, int64_t Mo, int64_t K, int N);
+bool gemm_tc32_eligible(int64_t Mo, int64_t K, int N);
+int64_t gemm_tc32_ws_elems(int64_t Mo, int64_t K, int N, int num_sms);
+int gemm_tc32_launches(int64_t Mo, int64_t K, int N, int num_sms);
+cudaError_t gemm_tc32(Op op, const float* A, int64_t lda, const float* X, int64_t ldx, float* C, int64_t ldc,
+                      int64_t Mo, int64_t K, int N, float* ws, int num_sms, int max_smem, cudaStream_t st);
+
 }  // namespace coru_gpu

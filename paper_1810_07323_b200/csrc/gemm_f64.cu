@@ -12,9 +12,14 @@
 // lane t the k-pair (2t, 2t+1) instead of (t, t+4) (a consistent permutation of k in A and X, so
 // the product is unchanged). A is streamed with an L2 evict-first policy so X stays L2-resident.
 // Work is split stream-K style: P = resident CTAs, each owning an equal contiguous range of
-// (tile, k-slab) iterations; tiles owned by one CTA are written directly, split tiles go through
-// a fixed-order fix-up (deterministic, no atomics).
+// (tile, k-slab) iterations; tiles owned by one CTA are written directly. A split tile's segments
+// are written to a workspace slot each and published with a release flag (tagged with a per-launch
+// epoch); the CTA that owns the tile's LAST k-slab (the tile sits at the start of its range, so
+// every other segment belongs to a lower-index, already-dispatched CTA: no deadlock) sums the
+// segments in segment order after finishing its own range and writes C — the fix-up runs inside
+// the GEMM (no second launch), in a fixed order (deterministic, no floating-point atomics).
 #include <algorithm>
+#include <atomic>
 #include <cmath>
 
 #include "common.cuh"
@@ -178,6 +183,15 @@ struct FastLoader {
     }
 };
 
+__device__ __forceinline__ void st_release_gpu_u64(uint64_t* p, uint64_t v) {
+    asm volatile("st.release.gpu.global.u64 [%0], %1;\n" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ uint64_t ld_acquire_gpu_u64(const uint64_t* p) {
+    uint64_t v;
+    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];\n" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+
 // CTA c owns iterations [I*c/P, I*(c+1)/P) of the (tile, k-slab) space, tile-major.
 __host__ __device__ __forceinline__ int64_t sk_begin(int64_t iters, int P, int c) { return iters * c / P; }
 // The CTA that owns iteration g.
@@ -189,7 +203,7 @@ template <class S, int VEC>
 __global__ void __launch_bounds__(S::NT, S::min_blocks)
     k_gemm_f64(const double* __restrict__ A, int64_t lda, const double* __restrict__ X, int64_t ldx,
                double* __restrict__ C, int64_t ldc, int64_t Mo, int64_t K, int N, int64_t ktiles, int64_t iters, int P,
-               double* __restrict__ ws, int max_seg) {
+               double* __restrict__ ws, int max_seg, uint64_t* __restrict__ flags, uint64_t epoch) {
     constexpr int MT = S::MT, BK = S::BK, ST = S::ST;
     extern __shared__ __align__(16) double smem[];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -201,6 +215,8 @@ __global__ void __launch_bounds__(S::NT, S::min_blocks)
     const uint64_t pol_a = l2_policy_evict_first(), pol_x = l2_policy_evict_last();
 
     const int tiles_n = (N + S::BN - 1) / S::BN;
+    int64_t fix_tile = -1;  // split tile whose last k-slab this CTA owns: summed after the range
+    int fix_segs = 0;
     while (it < it_end) {
         const int64_t tile = it / ktiles;
         const int64_t kb = it % ktiles;
@@ -279,13 +295,14 @@ __global__ void __launch_bounds__(S::NT, S::min_blocks)
         const bool whole = kb == 0 && ke == ktiles;
         double* dst_base;
         int64_t ld_dst, row_base;
+        int seg = 0;
         if (whole) {
             dst_base = C + n0;
             ld_dst = ldc;
             row_base = m0;
         } else {
             const int first = sk_owner(iters, P, tile * ktiles);
-            const int seg = cta - first;
+            seg = cta - first;
             dst_base = ws + (tile * max_seg + seg) * int64_t(S::BM * S::BN);
             ld_dst = S::BN;
             row_base = 0;
@@ -311,34 +328,45 @@ __global__ void __launch_bounds__(S::NT, S::min_blocks)
                 }
             }
         }
+        if (!whole) {
+            if (ke == ktiles) {  // last segment: this CTA sums the tile once its range is done
+                fix_tile = tile;
+                fix_segs = seg + 1;
+            } else {             // publish the segment
+                __syncthreads();
+                if (tid == 0) {
+                    __threadfence();
+                    st_release_gpu_u64(flags + tile * max_seg + seg, epoch);
+                }
+            }
+        }
         it = tile * ktiles + ke;
     }
-}
-
-// Fix-up of the split tiles: C(tile) = sum of its segments in CTA order (fixed order).
-// grid = (P - 1 CTA boundaries, element chunks of 256): block c handles the tile that CTA c starts
-// inside of, if CTA c is that tile's first boundary (so every split tile is summed exactly once).
-__global__ void k_streamk_fixup(const double* __restrict__ ws, int max_seg, int bm, int bn, int64_t ktiles,
-                                int64_t iters, int P, double* __restrict__ C, int64_t ldc, int64_t Mo, int N) {
-    const int c = blockIdx.x + 1;
-    const int64_t g = sk_begin(iters, P, c);
-    if (g % ktiles == 0) return;  // CTA c starts on a tile boundary: nothing split here
-    const int64_t tile = g / ktiles;
-    const int first = sk_owner(iters, P, tile * ktiles);
-    if (first != c - 1) return;   // an earlier boundary already owns this tile's fix-up
-    const int last = sk_owner(iters, P, tile * ktiles + ktiles - 1);
-    const int tiles_n = (N + bn - 1) / bn;
-    const int n0 = int(tile % tiles_n) * bn;
-    const int64_t tile_elems = int64_t(bm) * bn;
-    const int e = blockIdx.y * blockDim.x + threadIdx.x;
-    if (e >= tile_elems) return;
-    const int r = e / bn, cc = e % bn;
-    const int64_t row = (tile / tiles_n) * bm + r;
-    if (row >= Mo || n0 + cc >= N) return;
-    const double* base = ws + tile * max_seg * tile_elems + e;
-    double s = base[0];
-    for (int q = 1; q <= last - first; ++q) s += base[q * tile_elems];
-    C[row * ldc + n0 + cc] = s;
+    if (fix_tile >= 0) {
+        // Fixed-order sum of the tile's segments (seg 0 .. fix_segs-1; the last one is ours).
+        if (tid == 0) {
+            for (int q = 0; q + 1 < fix_segs; ++q) {
+                const uint64_t* f = flags + fix_tile * max_seg + q;
+                if (ld_acquire_gpu_u64(f) != epoch) {
+                    const long long t0 = clock64();
+                    while (ld_acquire_gpu_u64(f) != epoch)
+                        if (clock64() - t0 > 16000000000LL) __trap();  // never hang the GPU
+                }
+            }
+        }
+        __syncthreads();
+        const int64_t m0 = (fix_tile / tiles_n) * S::BM;
+        const int n0 = int(fix_tile % tiles_n) * S::BN;
+        const int64_t te = int64_t(S::BM) * S::BN;
+        const double* base = ws + fix_tile * max_seg * te;
+        for (int e = tid; e < S::BM * S::BN; e += S::NT) {
+            const int r = e / S::BN, cc = e % S::BN;
+            if (m0 + r >= Mo || n0 + cc >= N) continue;
+            double v = __ldcg(base + e);
+            for (int q = 1; q < fix_segs; ++q) v += __ldcg(base + q * te + e);
+            C[(m0 + r) * ldc + n0 + cc] = v;
+        }
+    }
 }
 
 // ---- configuration table -------------------------------------------------------------------
@@ -396,19 +424,21 @@ cudaError_t launch_cfg(const double* A, int64_t lda, const double* X, int64_t ld
     const int64_t tiles = ((Mo + S::BM - 1) / S::BM) * ((N + S::BN - 1) / S::BN);
     const int64_t iters = tiles * ktiles;
     const bool vec = (lda % 2 == 0) && (reinterpret_cast<uintptr_t>(A) % 16 == 0);
+    // split-tile flags live after the partial tiles; a fresh epoch per launch (no reset needed)
+    uint64_t* flags = p.fixup ? reinterpret_cast<uint64_t*>(ws + tiles * int64_t(p.max_seg) * S::BM * S::BN) : nullptr;
+    static std::atomic<uint64_t> launch_counter{0};
+    const uint64_t epoch = 0xC0DEull << 48 | (++launch_counter & 0xFFFFFFFFFFFFull);
     if (vec) {
         auto k = k_gemm_f64<S, 2>;
         allow_max_smem(k);
-        k<<<p.splits, S::NT, S::bytes, st>>>(A, lda, X, ldx, C, ldc, Mo, K, N, ktiles, iters, p.splits, ws, p.max_seg);
+        k<<<p.splits, S::NT, S::bytes, st>>>(A, lda, X, ldx, C, ldc, Mo, K, N, ktiles, iters, p.splits, ws, p.max_seg,
+                                              flags, epoch);
     } else {
         auto k = k_gemm_f64<S, 1>;
         allow_max_smem(k);
-        k<<<p.splits, S::NT, S::bytes, st>>>(A, lda, X, ldx, C, ldc, Mo, K, N, ktiles, iters, p.splits, ws, p.max_seg);
+        k<<<p.splits, S::NT, S::bytes, st>>>(A, lda, X, ldx, C, ldc, Mo, K, N, ktiles, iters, p.splits, ws, p.max_seg,
+                                              flags, epoch);
     }
-    cudaError_t e = cudaGetLastError();
-    if (e != cudaSuccess || !p.fixup) return e;
-    const dim3 grid(unsigned(std::max(1, p.splits - 1)), unsigned((S::BM * S::BN + 255) / 256));
-    k_streamk_fixup<<<grid, 256, 0, st>>>(ws, p.max_seg, S::BM, S::BN, ktiles, iters, p.splits, C, ldc, Mo, N);
     return cudaGetLastError();
 }
 
@@ -444,7 +474,7 @@ GemmPlan plan_gemm_f64_cfg(Op op, int64_t Mo, int64_t K, int N, int num_sms, int
         const int64_t g0 = tile * ktiles, g1 = g0 + ktiles - 1;
         p.fixup = ((g0 + 1) * P - 1) / iters != ((g1 + 1) * P - 1) / iters;
     }
-    p.ws_elems = p.fixup ? tiles * int64_t(p.max_seg) * p.bm * p.bn : 0;
+    p.ws_elems = p.fixup ? tiles * int64_t(p.max_seg) * (int64_t(p.bm) * p.bn + 1) : 0;  // partials + flags
     p.num_sms = num_sms;
     return p;
 }

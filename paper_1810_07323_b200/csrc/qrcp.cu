@@ -9,6 +9,7 @@
 // uncontracted __dmul_rn/__dsub_rn so the downdate rounds like the reference.
 // Q_M = H_0...H_{d-1} (accumulate_q, qr.hpp:60-72) is formed in compact-WY form with CTA GEMMs.
 #include <algorithm>
+#include <climits>
 
 #include "common.cuh"
 #include "cta_blas.cuh"
@@ -276,6 +277,271 @@ __global__ void __launch_bounds__(kThreads) k_qrcp(const T* __restrict__ M, int 
     QPROF_ADD(3, t_all);
 }
 
+// ------------------------------------------------------------------------------------------------
+// Register-resident QRCP for d <= 128 (C1 d=25, C2 d=60, C3 d=110): the pivot loop is d sequential
+// steps, so the kernel is built around ONE block barrier per step.
+//
+// * Warp w owns columns c = w, w+NW, ... (CPW of them); lane l holds rows l, l+32, ... (RPL of
+//   them) of each in registers. Columns never move: the reference's physical swap (qr.hpp:124-129)
+//   is tracked as a position per column (pos), which is also what the tie rule compares (strict >
+//   over positions j..d-1 picks the lowest position among equal maxima, qr.hpp:121-123).
+// * After applying reflector j to its trailing columns (apply_reflector, qr.hpp:49-57) and
+//   downdating their squared norms with the 1e-6 recompute guard (qr.hpp:131-139), each warp
+//   builds the reflector of ITS best candidate for step j+1 (make_reflector, qr.hpp:32-45) into a
+//   double-buffered shared slot. After the barrier every warp picks the global winner among the NW
+//   candidates and reads its reflector: the pivot search, the reflector and the update of the next
+//   step need no second barrier.
+// * Scalar formulas use explicit _rn operations so nvcc does not contract them into FMAs that the
+//   reference (built without contraction) does not perform; reductions are tree-ordered.
+// * Q_M = H_0 ... H_{d-1} I (accumulate_q, qr.hpp:60-72): each warp carries its columns of I in
+//   registers through the d stored reflectors in reverse order.
+template <typename T, int RPL, int CPW, int NW>
+__global__ void __launch_bounds__(NW * 32) k_qrcp_reg(const T* __restrict__ M, int ldm, int d, T* __restrict__ Q,
+                                                      int ldq, T* __restrict__ Tout, int ldt,
+                                                      int64_t* __restrict__ perm_out) {
+    constexpr int R = RPL * 32;  // padded row count
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    T* cand_v = reinterpret_cast<T*>(smem_raw);        // [2][NW][R]  candidate reflectors
+    T* vst = cand_v + 2 * NW * R;                      // [d][R]      chosen reflectors (for Q)
+    T* cand_s = vst + size_t(d) * R;                   // [2][NW][3]  colsq, beta, diagonal
+    int* cand_i = reinterpret_cast<int*>(cand_s + 2 * NW * 3);  // [2][NW][2] position, column
+    T* betas = reinterpret_cast<T*>(cand_i + 2 * NW * 2 + 2);   // [d] (8-byte aligned: +2 ints)
+
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    T col[CPW][RPL];
+    T colsq[CPW], base[CPW];
+    int pos[CPW];
+#pragma unroll
+    for (int k = 0; k < CPW; ++k) {
+        const int c = warp + NW * k;
+        T s = 0;
+#pragma unroll
+        for (int u = 0; u < RPL; ++u) {
+            const int r = lane + 32 * u;
+            col[k][u] = (c < d && r < d) ? M[int64_t(r) * ldm + c] : T(0);
+            s = add_rn(s, mul_rn(col[k][u], col[k][u]));
+        }
+        s = warp_sum(s);  // initial squared norms (qr.hpp:115-119)
+        colsq[k] = base[k] = s;
+        pos[k] = c < d ? c : INT_MAX;  // INT_MAX: padding column, never active
+    }
+
+    // Builds this warp's candidate for step jn among its columns at positions >= jn and writes it
+    // to slot `sl`. Warp-uniform control flow throughout (colsq/pos are identical on all lanes).
+    auto candidate = [&](int jn, int sl) {
+        int kb = -1;
+        T bv = T(0);
+        int bp = INT_MAX;
+#pragma unroll
+        for (int k = 0; k < CPW; ++k) {
+            if (pos[k] >= jn && pos[k] < d) {
+                if (kb < 0 || colsq[k] > bv || (colsq[k] == bv && pos[k] < bp)) { kb = k; bv = colsq[k]; bp = pos[k]; }
+            }
+        }
+        T* cs = cand_s + (sl * NW + warp) * 3;
+        int* ci = cand_i + (sl * NW + warp) * 2;
+        if (kb < 0) {
+            if (lane == 0) { ci[0] = INT_MAX; ci[1] = -1; }
+            return;
+        }
+        T x[RPL];
+#pragma unroll
+        for (int u = 0; u < RPL; ++u) {
+            x[u] = col[0][u];
+#pragma unroll
+            for (int k = 1; k < CPW; ++k) x[u] = (k == kb) ? col[k][u] : x[u];
+        }
+        T sig = 0, x0 = 0;
+#pragma unroll
+        for (int u = 0; u < RPL; ++u) {
+            const int r = lane + 32 * u;
+            if (r > jn) sig = add_rn(sig, mul_rn(x[u], x[u]));
+            if (r == jn) x0 = x[u];
+        }
+        sig = warp_sum(sig);
+        x0 = __shfl_sync(0xffffffffu, x0, jn & 31);
+        T* v = cand_v + (sl * NW + warp) * R;
+        T beta = 0, diag = x0;
+        if (sig != T(0)) {  // make_reflector (qr.hpp:32-45); sigma == 0 leaves the diagonal (qr.hpp:37)
+            const T mu = tsqrt(add_rn(mul_rn(x0, x0), sig));
+            const T v0 = (x0 <= T(0)) ? add_rn(x0, -mu) : -sig / add_rn(x0, mu);
+            const T v0sq = mul_rn(v0, v0);
+            beta = mul_rn(T(2) * v0, v0) / add_rn(sig, v0sq);
+            diag = mu;
+#pragma unroll
+            for (int u = 0; u < RPL; ++u) {
+                const int r = lane + 32 * u;
+                v[r] = r > jn ? x[u] / v0 : T(r == jn ? 1 : 0);
+            }
+        } else {
+#pragma unroll
+            for (int u = 0; u < RPL; ++u) v[lane + 32 * u] = T(0);
+        }
+        if (lane == 0) {
+            cs[0] = bv; cs[1] = beta; cs[2] = diag;
+            ci[0] = bp; ci[1] = warp + NW * kb;
+        }
+    };
+
+    candidate(0, 0);
+    __syncthreads();
+    for (int j = 0; j < d; ++j) {
+        const int sl = j & 1;
+        // ---- global pivot: the best of the NW candidates (larger colsq, then lower position) ----
+        T wv = T(0);
+        int wp = INT_MAX, ww = -1;
+        if (lane < NW) {
+            const int p = cand_i[(sl * NW + lane) * 2];
+            if (p != INT_MAX) { wv = cand_s[(sl * NW + lane) * 3]; wp = p; ww = lane; }
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            const T ov = __shfl_xor_sync(0xffffffffu, wv, o);
+            const int op = __shfl_xor_sync(0xffffffffu, wp, o);
+            const int ow = __shfl_xor_sync(0xffffffffu, ww, o);
+            if (ow >= 0 && (ww < 0 || ov > wv || (ov == wv && op < wp))) { wv = ov; wp = op; ww = ow; }
+        }
+        // lane 0's choice for the whole CTA: with NaN norms the butterfly need not agree across
+        // lanes, and every later branch must stay warp-uniform (shuffles inside)
+        ww = __shfl_sync(0xffffffffu, ww, 0);
+        wp = __shfl_sync(0xffffffffu, wp, 0);
+        const T* cs = cand_s + (sl * NW + ww) * 3;
+        const T beta = cs[1], diag = cs[2];
+        const int wcol = cand_i[(sl * NW + ww) * 2 + 1];
+        const T* vsrc = cand_v + (sl * NW + ww) * R;
+        T v[RPL];
+#pragma unroll
+        for (int u = 0; u < RPL; ++u) v[u] = vsrc[lane + 32 * u];
+        // ---- bookkeeping of the swap (qr.hpp:124-129) ----
+#pragma unroll
+        for (int k = 0; k < CPW; ++k) if (pos[k] == j) pos[k] = wp;
+        if (warp == (wcol % NW)) {
+            const int kw = wcol / NW;
+#pragma unroll
+            for (int k = 0; k < CPW; ++k) {
+                if (k == kw) {
+                    pos[k] = j;
+#pragma unroll
+                    for (int u = 0; u < RPL; ++u)
+                        if (lane + 32 * u == j) col[k][u] = diag;  // R(j,j) = mu (or x0 when sigma == 0)
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < RPL; ++u) vst[j * R + lane + 32 * u] = v[u];
+            if (lane == 0) { betas[j] = beta; perm_out[j] = wcol; }
+        }
+        // ---- apply H_j to the trailing columns and downdate their norms (qr.hpp:131-139) ----
+        if (beta != T(0)) {
+            T s[CPW];
+#pragma unroll
+            for (int k = 0; k < CPW; ++k) {
+                s[k] = 0;
+#pragma unroll
+                for (int u = 0; u < RPL; ++u) s[k] += v[u] * col[k][u];
+            }
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+                for (int k = 0; k < CPW; ++k) s[k] += __shfl_xor_sync(0xffffffffu, s[k], o);
+#pragma unroll
+            for (int k = 0; k < CPW; ++k) {
+                if (pos[k] > j && pos[k] < d) {
+                    const T sb = s[k] * beta;
+#pragma unroll
+                    for (int u = 0; u < RPL; ++u) col[k][u] = add_rn(col[k][u], -mul_rn(sb, v[u]));
+                }
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < CPW; ++k) {
+            T w = 0;
+#pragma unroll
+            for (int u = 0; u < RPL; ++u) if (lane + 32 * u == j) w = col[k][u];
+            w = __shfl_sync(0xffffffffu, w, j & 31);
+            if (pos[k] > j && pos[k] < d) {
+                colsq[k] = add_rn(colsq[k], -mul_rn(w, w));
+                if (colsq[k] < T(1e-6) * base[k]) {  // recompute guard (qr.hpp:135-139)
+                    T s2 = 0;
+#pragma unroll
+                    for (int u = 0; u < RPL; ++u)
+                        if (lane + 32 * u > j) s2 = add_rn(s2, mul_rn(col[k][u], col[k][u]));
+                    colsq[k] = base[k] = warp_sum(s2);
+                }
+            }
+        }
+        if (j + 1 < d) candidate(j + 1, sl ^ 1);
+        __syncthreads();
+    }
+    // ---- T = upper triangle (qr.hpp:74-79) ----
+#pragma unroll
+    for (int k = 0; k < CPW; ++k) {
+        const int p = pos[k];
+        if (p < d) {
+#pragma unroll
+            for (int u = 0; u < RPL; ++u) {
+                const int r = lane + 32 * u;
+                if (r < d) Tout[int64_t(r) * ldt + p] = r <= p ? col[k][u] : T(0);
+            }
+        }
+    }
+    // ---- Q_M (accumulate_q order: reflectors d-1 .. 0 applied to each column of I) ----
+#pragma unroll
+    for (int k = 0; k < CPW; ++k)
+#pragma unroll
+        for (int u = 0; u < RPL; ++u) col[k][u] = T(lane + 32 * u == warp + NW * k ? 1 : 0);
+    for (int j = d - 1; j >= 0; --j) {
+        const T bj = betas[j];
+        if (bj == T(0)) continue;
+        T v[RPL];
+#pragma unroll
+        for (int u = 0; u < RPL; ++u) v[u] = vst[j * R + lane + 32 * u];
+        T s[CPW];
+#pragma unroll
+        for (int k = 0; k < CPW; ++k) {
+            s[k] = 0;
+#pragma unroll
+            for (int u = 0; u < RPL; ++u) s[k] += v[u] * col[k][u];
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+            for (int k = 0; k < CPW; ++k) s[k] += __shfl_xor_sync(0xffffffffu, s[k], o);
+#pragma unroll
+        for (int k = 0; k < CPW; ++k) {
+            const T sb = s[k] * bj;
+#pragma unroll
+            for (int u = 0; u < RPL; ++u) col[k][u] = add_rn(col[k][u], -mul_rn(sb, v[u]));
+        }
+    }
+#pragma unroll
+    for (int k = 0; k < CPW; ++k) {
+        const int c = warp + NW * k;
+        if (c < d) {
+#pragma unroll
+            for (int u = 0; u < RPL; ++u) {
+                const int r = lane + 32 * u;
+                if (r < d) Q[int64_t(r) * ldq + c] = col[k][u];
+            }
+        }
+    }
+}
+
+template <typename T, int RPL, int CPW, int NW>
+size_t qrcp_reg_smem(int d) {
+    constexpr int R = RPL * 32;
+    return (size_t(2) * NW * R + size_t(d) * R + 2 * NW * 3) * sizeof(T) + (2 * NW * 2 + 2) * sizeof(int) +
+           size_t(d) * sizeof(T);
+}
+
+template <typename T, int RPL, int CPW, int NW>
+cudaError_t launch_qrcp_reg(const T* M, int ldm, int d, T* Q, int ldq, T* Tout, int ldt, int64_t* perm,
+                            cudaStream_t st) {
+    allow_max_smem(k_qrcp_reg<T, RPL, CPW, NW>);
+    k_qrcp_reg<T, RPL, CPW, NW><<<1, NW * 32, qrcp_reg_smem<T, RPL, CPW, NW>(d), st>>>(M, ldm, d, Q, ldq, Tout, ldt,
+                                                                                      perm);
+    return cudaGetLastError();
+}
+
 template <typename T>
 __global__ void k_gather_columns(const T* __restrict__ Q2, int64_t ldq, const int64_t* __restrict__ perm, int64_t n,
                                  int d, T* __restrict__ V, int64_t ldv) {
@@ -338,6 +604,9 @@ int64_t qrcp_scratch_elems(int d) {
 template <typename T>
 cudaError_t qrcp(const T* M, int ldm, int d, T* Q, int ldq, T* Tout, int ldt, int64_t* perm, T* scratch,
                  int max_smem, cudaStream_t st) {
+    if (d <= 32) return launch_qrcp_reg<T, 1, 2, 16>(M, ldm, d, Q, ldq, Tout, ldt, perm, st);
+    if (d <= 64) return launch_qrcp_reg<T, 2, 4, 16>(M, ldm, d, Q, ldq, Tout, ldt, perm, st);
+    if (d <= 128) return launch_qrcp_reg<T, 4, 8, 16>(M, ldm, d, Q, ldq, Tout, ldt, perm, st);
     const bool fits = qrcp_smem_bytes(d, sizeof(T), true) <= size_t(max_smem);
     const size_t sm = qrcp_smem_bytes(d, sizeof(T), fits);
     allow_max_smem(k_qrcp<T>);

@@ -38,6 +38,20 @@ def test_gemm_matches_oracle(ctx, oracle, m, n, d, op):
     assert np.all(np.abs(c - want) <= 1e-12 * bound + 1e-300)
 
 
+@pytest.mark.parametrize("m,n,d,op", [(4000, 4000, 60, 0), (4000, 4000, 60, 1), (1000, 1000, 25, 1),
+                                      (20000, 2000, 110, 1), (3001, 129, 110, 0)])
+def test_gemm_streamk_fixup_deterministic(ctx, m, n, d, op):
+    """Split tiles are summed inside the GEMM by the CTA owning their last k-slab, in segment order:
+    repeated launches (fresh epochs over the same workspace) are bitwise identical."""
+    import paper_1810_07323_b200 as cg
+    rng = np.random.default_rng(m + n + d)
+    a = _t(rng.standard_normal((m, n)))
+    x = _t(rng.standard_normal((m if op else n, (d + 7) // 8 * 8)))[:, :d]
+    c0 = cg.gemm(a, x, op=op, ctx=ctx).cpu().numpy()
+    for _ in range(3):
+        assert np.array_equal(cg.gemm(a, x, op=op, ctx=ctx).cpu().numpy(), c0)
+
+
 def test_gemm_odd_lda_and_views(ctx, oracle):
     """A with odd leading dimension (8-byte cp.async path) and a column view of a wider matrix."""
     import torch
@@ -101,6 +115,38 @@ def test_qrcp_matches_oracle(ctx, oracle, n, seed):
     assert np.sign(r[-1, -1]) == np.sign(ro[-1, -1])
 
 
+@pytest.mark.parametrize("n,kind", [(8, "hadamard"), (32, "hadamard"), (64, "hadamard"), (50, "dup"), (100, "dup"),
+                                    (33, "zero"), (128, "zero"), (60, "rank5")])
+def test_qrcp_ties_and_degenerate(ctx, oracle, n, kind):
+    """Tie rule (strict >, lowest position wins, qr.hpp:121-123) and degenerate columns (sigma == 0
+    leaves the diagonal unreflected, qr.hpp:37): the pivot order must equal the reference's."""
+    import paper_1810_07323_b200 as cg
+    rng = np.random.default_rng(n)
+    if kind == "hadamard":  # every column has the same norm: pure tie-breaking
+        h = np.array([[1.0]])
+        while h.shape[0] < n:
+            h = np.block([[h, h], [h, -h]])
+        a = h[:n, :n].copy()
+    elif kind == "dup":  # duplicated columns: equal norms, and exact cancellation after one of them
+        b = rng.standard_normal((n, n // 2))
+        a = np.concatenate([b, b], axis=1)[:, rng.permutation(n)]
+    elif kind == "zero":
+        a = rng.standard_normal((n, n))
+        a[:, rng.choice(n, n // 3, replace=False)] = 0.0
+    else:
+        a = rng.standard_normal((n, 5)) @ rng.standard_normal((5, n))
+    q, r, perm = cg.qrcp(_t(a), ctx=ctx)
+    q, r = q.cpu().numpy(), r.cpu().numpy()
+    qo, ro, po = oracle.qrcp(a)
+    # past the numerical rank the pivots are decided by rounding noise
+    k = {"rank5": 5, "dup": n // 2}.get(kind, n)
+    assert np.array_equal(perm[:k], po[:k])
+    assert np.all(np.tril(r, -1) == 0.0)
+    assert np.linalg.norm(q @ r - a[:, perm]) <= 1e-12 * np.linalg.norm(a) * n
+    assert orth_residual(q) <= 1e-12 * n
+    assert np.allclose(np.abs(np.diag(r))[:k], np.abs(np.diag(ro))[:k], rtol=1e-10, atol=1e-12 * np.abs(ro[0, 0]))
+
+
 @pytest.mark.parametrize("m,n,d,op", [(1000, 1000, 25, 0), (1000, 1000, 25, 1), (4097, 3001, 130, 0),
                                       (4097, 3001, 130, 1), (300, 5000, 520, 0), (5000, 300, 520, 1)])
 def test_gemm_f32_matches_oracle(ctx, oracle, m, n, d, op):
@@ -115,6 +161,31 @@ def test_gemm_f32_matches_oracle(ctx, oracle, m, n, d, op):
     K = n if op == 0 else m
     bound = ((np.abs(a) @ np.abs(x)) if op == 0 else (np.abs(a).T @ np.abs(x))).astype(np.float64)
     assert np.all(np.abs(c.astype(np.float64) - want) <= K * 2.0 ** -23 * bound + 1e-30)
+
+
+@pytest.mark.parametrize("m,n,d,op", [(1000, 1000, 25, 0), (1000, 1000, 25, 1), (4097, 3001, 130, 0),
+                                      (4097, 3001, 130, 1), (300, 5000, 520, 0), (5000, 300, 520, 1),
+                                      (129, 131, 16, 0), (131, 129, 16, 1), (2000, 777, 384, 0),
+                                      (777, 2000, 400, 1), (1280, 4096, 520, 0), (4096, 1280, 520, 1)])
+def test_gemm_f32_tensor_core_matches_oracle(m, n, d, op, oracle):
+    """tcgen05 3xTF32 A-pass (gemm_tc32.cu) against the fp32 restatement of matmul (matrix.hpp:115-131).
+    Bound: per product the split v = hi + lo loses the lo·lo term and the TF32 truncation of the lo
+    parts (<= 2^-19 |a||x|), plus the fp32 accumulation over K (K·2^-22 covers both sides' sums):
+    |C - C_ref| <= (2^-19 + K·2^-22)·(|A||X|). Typical errors are far smaller (checked too)."""
+    import paper_1810_07323_b200 as cg
+    ctx = cg.Context(0)
+    ctx.set_f32_path(ctx.F32_TC)
+    rng = np.random.default_rng(m + n + d + op)
+    a = rng.standard_normal((m, n)).astype(np.float32)
+    x = rng.standard_normal((m if op else n, d)).astype(np.float32)
+    c = cg.gemm(_t(a), _t(x), op=op, ctx=ctx).cpu().numpy().astype(np.float64)
+    want = oracle.matmul(a, x) if op == 0 else oracle.matmul_tn(a, x)
+    K = n if op == 0 else m
+    bound = ((np.abs(a) @ np.abs(x)) if op == 0 else (np.abs(a).T @ np.abs(x))).astype(np.float64)
+    err = np.abs(c - want)
+    assert np.all(err <= (2.0 ** -19 + K * 2.0 ** -22) * bound + 1e-30)
+    assert np.median(err / bound) < 2.0 ** -22
+    ctx.close()
 
 
 def _ulp_diff(x, y):
