@@ -16,13 +16,14 @@
 //   warps 4..7  converters: row t of the A tile (smem) -> hi/lo -> TMEM columns of stage s
 //               (tcgen05.st 32x32b: thread t owns TMEM lane t = output row t); later the epilogue
 //   warp 1      MMA issuer (one thread): per K=8 step, 3 (or 6 when nc > 256) tcgen05.mma with
-//               A from TMEM ("ts" form) and X from smem (MN-major SW128 descriptor); tcgen05.commit
+//               A from TMEM ("ts" form) and X from smem (K-major SW128 descriptor); tcgen05.commit
 //               frees the stage (smem + TMEM slot) and finally signals the accumulator.
 //   warp 2      TMEM allocator (512 columns: accumulator [0, nc), A slots at 384 + 64 s).
-// X^hi / X^lo are produced once per pass by k_split_x into a pre-tiled layout
-// [chunk][32-column atom][k][32] so that one 3-D TMA per operand loads a whole stage. A is read
-// exactly once per N-chunk; no A^T is formed (op T reads row-major A as the MN-major operand and
-// the converter reads it down columns).
+// X^hi / X^lo are produced once per pass by k_split_xt, transposed (K-major: row n of the chunk
+// holds X(:, n) contiguously; tools/tc_probe.cu showed the MN-major tf32 B operand with the plain
+// 128-byte swizzle is not what the tensor core reads, while K-major SW128 is exact). A is read
+// exactly once per N-chunk and no A^T is formed: op T loads row-major A tiles as [k][128] and the
+// converter reads them down columns.
 //
 // Deterministic: fixed MMA order; split-K partials reduced in a fixed order (no atomics).
 #include <algorithm>
@@ -95,8 +96,8 @@ __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence:
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory"); }
 
 // Shared-memory matrix descriptor, SWIZZLE_128B (layout type 2), Blackwell version bit 46.
-// For the MN-major operand: LBO = byte stride between 32-element MN atoms, SBO = byte stride
-// between 8-row K groups (cute make_umma_desc<Major::MN> canonical form).
+// K-major operand: SBO = byte stride between 8-row groups (1024 for dense 128-byte rows), LBO
+// unused by the swizzled K-major form.
 __device__ __forceinline__ uint64_t sdesc_sw128(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
     uint64_t d = uint64_t((saddr & 0x3FFFFu) >> 4);
     d |= uint64_t((lbo >> 4) & 0x3FFFu) << 16;
@@ -105,9 +106,9 @@ __device__ __forceinline__ uint64_t sdesc_sw128(uint32_t saddr, uint32_t lbo, ui
     d |= uint64_t(2) << 61;
     return d;
 }
-// Instruction descriptor: D f32, A/B tf32, A K-major (TMEM), B MN-major, M = 128, N = n.
+// Instruction descriptor: D f32, A/B tf32, both K-major, M = 128, N = n.
 __host__ __device__ constexpr uint32_t idesc_tf32(int n) {
-    return (1u << 4) | (2u << 7) | (2u << 10) | (1u << 16) | (uint32_t(n >> 3) << 17) | (uint32_t(kBM >> 4) << 24);
+    return (1u << 4) | (2u << 7) | (2u << 10) | (uint32_t(n >> 3) << 17) | (uint32_t(kBM >> 4) << 24);
 }
 __device__ __forceinline__ void mma_tf32_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uint32_t idesc,
                                             uint32_t accum) {
@@ -160,7 +161,7 @@ struct TcArgs {
     int N;        // true columns of C
     int nc;       // columns per N-chunk (multiple of 16, <= kAccCols)
     int n1;       // first MMA's N (<= 256); the second covers nc - n1
-    int atoms;    // 32-column atoms per chunk in the pre-tiled X
+    int xboxes;   // TMA boxes per X tile (box rows = nc / xboxes <= 256)
     int nch;      // N-chunks
     int mtiles;
     int stages;
@@ -177,7 +178,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     extern __shared__ __align__(16) unsigned char smem_raw[];
     // 1024-byte alignment for the SW128 atoms
     unsigned char* sm = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    const int xbytes = kBK * p.atoms * 32 * 4;              // one X operand tile per stage
+    const int xbytes = p.nc * kBK * 4;                      // one X operand tile per stage
     const int stage_bytes = kATileBytes + 2 * xbytes;       // multiple of 1024
     uint64_t* bars = reinterpret_cast<uint64_t*>(sm + p.stages * stage_bytes);
     uint64_t* full = bars;                   // [stages] TMA landed
@@ -232,8 +233,11 @@ __global__ void __launch_bounds__(kTcThreads, 1)
                     tma_load_2d(st, &tmA, k0, int(m0), &full[s]);
                 else
                     tma_load_2d(st, &tmA, int(m0), k0, &full[s]);
-                tma_load_3d(st + kATileBytes, &tmXh, 0, k0, chunk * p.atoms, &full[s]);
-                tma_load_3d(st + kATileBytes + xbytes, &tmXl, 0, k0, chunk * p.atoms, &full[s]);
+                const int br = p.nc / p.xboxes;
+                for (int b = 0; b < p.xboxes; ++b) {
+                    tma_load_2d(st + kATileBytes + b * br * 128, &tmXh, k0, chunk * p.nc + b * br, &full[s]);
+                    tma_load_2d(st + kATileBytes + xbytes + b * br * 128, &tmXl, k0, chunk * p.nc + b * br, &full[s]);
+                }
             }
             __syncwarp();
         }
@@ -242,7 +246,6 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         const uint32_t id1 = idesc_tf32(p.n1);
         const int n2 = p.nc - p.n1;
         const uint32_t id2 = idesc_tf32(n2 > 0 ? n2 : 16);
-        const uint32_t lbo = kBK * 128;  // atom stride in the X tile
         for (int i = 0; i < nk; ++i) {
             const int s = i % p.stages;
             const uint32_t ph = (i / p.stages) & 1;
@@ -257,15 +260,16 @@ __global__ void __launch_bounds__(kTcThreads, 1)
                 for (int ks = 0; ks < kBK / 8; ++ks) {
                     const uint32_t ahi = aslot + 8 * ks, alo = ahi + 32;
                     const uint32_t acc0 = (i > 0 || ks > 0) ? 1u : 0u;
-                    const uint64_t bh = sdesc_sw128(xh + 1024 * ks, lbo, 1024);
-                    const uint64_t bl = sdesc_sw128(xl + 1024 * ks, lbo, 1024);
+                    // K-major SW128: rows of 128 B (32 k), 8-row groups 1024 B apart, K step = +32 B
+                    const uint64_t bh = sdesc_sw128(xh + 32 * ks, 16, 1024);
+                    const uint64_t bl = sdesc_sw128(xl + 32 * ks, 16, 1024);
                     mma_tf32_ts(tmem, alo, bh, id1, acc0);
                     mma_tf32_ts(tmem, ahi, bl, id1, 1u);
                     mma_tf32_ts(tmem, ahi, bh, id1, 1u);
                     if (n2 > 0) {
-                        const uint32_t off = (p.n1 / 32) * lbo;
-                        const uint64_t bh2 = sdesc_sw128(xh + off + 1024 * ks, lbo, 1024);
-                        const uint64_t bl2 = sdesc_sw128(xl + off + 1024 * ks, lbo, 1024);
+                        const uint32_t off = p.n1 * 128;
+                        const uint64_t bh2 = sdesc_sw128(xh + off + 32 * ks, 16, 1024);
+                        const uint64_t bl2 = sdesc_sw128(xl + off + 32 * ks, 16, 1024);
                         mma_tf32_ts(tmem + p.n1, alo, bh2, id2, acc0);
                         mma_tf32_ts(tmem + p.n1, ahi, bl2, id2, 1u);
                         mma_tf32_ts(tmem + p.n1, ahi, bh2, id2, 1u);
@@ -351,23 +355,29 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     }
 }
 
-// X (K x N, ld ldx) -> hi / lo parts in the pre-tiled layout [chunk][atom][k][32], zero padded.
-__global__ void k_split_x(const float* __restrict__ X, int64_t ldx, int64_t K, int N, int nc, int atoms, int nch,
-                          float* __restrict__ Xh, float* __restrict__ Xl) {
-    const int64_t total = int64_t(nch) * atoms * K * 32;
-    for (int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < total; e += int64_t(gridDim.x) * blockDim.x) {
-        const int c = int(e & 31);
-        int64_t r = e >> 5;
-        const int64_t k = r % K;
-        r /= K;
-        const int a = int(r % atoms);
-        const int h = int(r / atoms);
-        const int cc = a * 32 + c;
-        const int col = h * nc + cc;
-        const float x = (cc < nc && col < N) ? X[k * ldx + col] : 0.f;
-        const float hi = __uint_as_float(tf32_rna(x));
-        Xh[e] = hi;
-        Xl[e] = x - hi;
+// X (K x N, ld ldx) -> hi / lo parts, transposed: XT[h * nc + n][k] = X[k][h * nc + n] (row
+// stride ldk), zero for columns >= N. 32 x 32 tiles through shared memory (coalesced both ways).
+__global__ void k_split_xt(const float* __restrict__ X, int64_t ldx, int64_t K, int N, int rows_out, int64_t ldk,
+                           float* __restrict__ Xh, float* __restrict__ Xl) {
+    __shared__ float tile[32][33];
+    const int64_t k0 = int64_t(blockIdx.x) * 32;
+    const int n0 = blockIdx.y * 32;
+    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 8 threads
+    for (int r = ty; r < 32; r += 8) {
+        const int64_t k = k0 + r;
+        const int n = n0 + tx;
+        tile[r][tx] = (k < K && n < N) ? X[k * ldx + n] : 0.f;
+    }
+    __syncthreads();
+    for (int r = ty; r < 32; r += 8) {
+        const int n = n0 + r;
+        const int64_t k = k0 + tx;
+        if (n < rows_out && k < K) {
+            const float x = tile[tx][r];
+            const float hi = __uint_as_float(tf32_rna(x));
+            Xh[int64_t(n) * ldk + k] = hi;
+            Xl[int64_t(n) * ldk + k] = x - hi;
+        }
     }
 }
 
@@ -406,7 +416,7 @@ bool make_map(CUtensorMap* m, const void* base, int rank, const cuuint64_t* dims
 }
 
 struct TcShape {
-    int nch, nc, n1, atoms, stages, splits, mtiles, kt_per_split;
+    int nch, nc, n1, xboxes, stages, splits, mtiles, kt_per_split;
     size_t smem;
 };
 
@@ -416,8 +426,8 @@ TcShape tc_shape(int64_t Mo, int64_t K, int N, int num_sms, int max_smem) {
     s.nch = (n16 + kAccCols - 1) / kAccCols;
     s.nc = ((n16 / 16 + s.nch - 1) / s.nch) * 16;
     s.n1 = std::min(s.nc, 256);
-    s.atoms = (s.nc + 31) / 32;
-    const size_t stage = size_t(kATileBytes) + 2 * size_t(kBK) * s.atoms * 32 * 4;
+    s.xboxes = (s.nc + 255) / 256;
+    const size_t stage = size_t(kATileBytes) + 2 * size_t(s.nc) * kBK * 4;
     s.stages = int(std::min<size_t>(kMaxStages, (size_t(max_smem) - 1024 - 256) / stage));
     s.smem = 1024 + s.stages * stage + 256;
     s.mtiles = int((Mo + kBM - 1) / kBM);
@@ -452,20 +462,22 @@ bool gemm_tc32_supported(Op op, const float* A, int64_t lda, int64_t Mo, int64_t
 
 int64_t gemm_tc32_ws_elems(int64_t Mo, int64_t K, int N, int num_sms) {
     const TcShape s = tc_shape(Mo, K, N, num_sms, 227 * 1024);
-    const int64_t x = int64_t(s.nch) * s.atoms * 32 * K;  // one pre-tiled operand
+    const int64_t x = int64_t(s.nch) * s.nc * ((K + 3) / 4 * 4);  // one transposed operand
     return 2 * x + (s.splits > 1 ? int64_t(s.splits) * Mo * N : 0) + 64;
 }
 
 cudaError_t gemm_tc32(Op op, const float* A, int64_t lda, const float* X, int64_t ldx, float* C, int64_t ldc,
                       int64_t Mo, int64_t K, int N, float* ws, int num_sms, int max_smem, cudaStream_t st) {
     const TcShape s = tc_shape(Mo, K, N, num_sms, max_smem);
-    const int64_t xe = int64_t(s.nch) * s.atoms * 32 * K;
+    const int64_t ldk = (K + 3) / 4 * 4;  // TMA row stride must be a multiple of 16 bytes
+    const int rows_out = s.nch * s.nc;
+    const int64_t xe = int64_t(rows_out) * ldk;
     float* xh = ws;
     float* xl = ws + xe;
     float* part = ws + 2 * xe;
     {
-        const int blocks = int(std::min<int64_t>((xe + 255) / 256, int64_t(num_sms) * 16));
-        k_split_x<<<blocks, 256, 0, st>>>(X, ldx, K, N, s.nc, s.atoms, s.nch, xh, xl);
+        const dim3 grid(unsigned((K + 31) / 32), unsigned((rows_out + 31) / 32));
+        k_split_xt<<<grid, 256, 0, st>>>(X, ldx, K, N, rows_out, ldk, xh, xl);
         cudaError_t e = cudaGetLastError();
         if (e != cudaSuccess) return e;
     }
@@ -482,11 +494,11 @@ cudaError_t gemm_tc32(Op op, const float* A, int64_t lda, const float* X, int64_
         if (!make_map(&ta, A, 2, dims, str, box, CU_TENSOR_MAP_SWIZZLE_NONE)) return cudaErrorInvalidValue;
     }
     {
-        const cuuint64_t dims[3] = {32, cuuint64_t(K), cuuint64_t(s.nch) * s.atoms};
-        const cuuint64_t str[2] = {128, cuuint64_t(K) * 128};
-        const cuuint32_t box[3] = {32, kBK, cuuint32_t(s.atoms)};
-        if (!make_map(&txh, xh, 3, dims, str, box, CU_TENSOR_MAP_SWIZZLE_128B)) return cudaErrorInvalidValue;
-        if (!make_map(&txl, xl, 3, dims, str, box, CU_TENSOR_MAP_SWIZZLE_128B)) return cudaErrorInvalidValue;
+        const cuuint64_t dims[2] = {cuuint64_t(K), cuuint64_t(rows_out)};
+        const cuuint64_t str[1] = {cuuint64_t(ldk) * 4};
+        const cuuint32_t box[2] = {kBK, cuuint32_t(s.nc / s.xboxes)};
+        if (!make_map(&txh, xh, 2, dims, str, box, CU_TENSOR_MAP_SWIZZLE_128B)) return cudaErrorInvalidValue;
+        if (!make_map(&txl, xl, 2, dims, str, box, CU_TENSOR_MAP_SWIZZLE_128B)) return cudaErrorInvalidValue;
     }
     TcArgs a{};
     a.Mo = Mo;
@@ -494,7 +506,7 @@ cudaError_t gemm_tc32(Op op, const float* A, int64_t lda, const float* X, int64_
     a.N = N;
     a.nc = s.nc;
     a.n1 = s.n1;
-    a.atoms = s.atoms;
+    a.xboxes = s.xboxes;
     a.nch = s.nch;
     a.mtiles = s.mtiles;
     a.stages = s.stages;
