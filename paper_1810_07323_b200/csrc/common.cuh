@@ -79,6 +79,57 @@ __device__ __forceinline__ void dmma_16x8x8(double (&c)[4], const double (&a)[4]
         : "d"(a[0]), "d"(a[1]), "d"(a[2]), "d"(a[3]), "d"(b[0]), "d"(b[1]));
 }
 
+// Short-latency fp64 reciprocal / reciprocal square root for the latency-bound reflector chains:
+// a single-precision MUFU seed refined by Newton steps (DFMA), ~1 ulp. IEEE fp64 division and
+// sqrt are ~400-cycle serial sequences on this chip (tools/qr_reg_tl). Arguments outside the float
+// exponent range (or zero / non-finite) fall back to the IEEE operation.
+__device__ __forceinline__ bool float_range(double x) {
+    const double a = fabs(x);
+    return a > 1e-36 && a < 1e36;
+}
+__device__ __forceinline__ double fast_rcp(double x) {
+    if (!float_range(x)) return 1.0 / x;
+    double r = double(__frcp_rn(float(x)));
+    double e = fma(-x, r, 1.0);
+    r = fma(r, e, r);
+    e = fma(-x, r, 1.0);
+    return fma(r, e, r);
+}
+__device__ __forceinline__ double fast_rsqrt(double x) {  // x > 0
+    if (!float_range(x)) return 1.0 / sqrt(x);
+    double r = double(rsqrtf(float(x)));
+    // r <- r (3 - x r^2) / 2, twice (quadratic convergence from ~2^-23)
+    double h = 0.5 * x;
+    r = r * fma(-h * r, r, 1.5);
+    r = r * fma(-h * r, r, 1.5);
+    return r;
+}
+__device__ __forceinline__ float fast_rcp(float x) { return 1.0f / x; }
+__device__ __forceinline__ float fast_rsqrt(float x) { return rsqrtf(x); }
+
+// make_reflector's scalars (qr.hpp:32-45) for sigma != 0, with two short-latency reciprocals in
+// place of the serial IEEE sqrt -> divide -> divide chain:
+//   t = x0^2 + sigma, mu = t·rsqrt(t);  v0 = x0 - mu (x0 <= 0) or -sigma/(x0 + mu);
+//   beta = 2 v0^2/(sigma + v0^2) = -v0/mu (since sigma = mu^2 - x0^2);
+//   rv = 1/v0 = 1/(x0 - mu) or -(x0 + mu)/sigma (the reciprocal of sigma overlaps the rsqrt).
+// Every quantity is within a few ulp of the reference's formula.
+template <typename T>
+__device__ __forceinline__ void reflector_scalars(T x0, T sig, T& mu, T& v0, T& beta, T& rv) {
+    const T t = x0 * x0 + sig;
+    const T rmu = fast_rsqrt(t);
+    const T rsig = fast_rcp(sig);
+    mu = t * rmu;
+    if (x0 <= T(0)) {
+        v0 = x0 - mu;
+        rv = fast_rcp(v0);
+    } else {
+        const T xpm = x0 + mu;
+        v0 = -sig * fast_rcp(xpm);
+        rv = -xpm * rsig;
+    }
+    beta = -v0 * rmu;
+}
+
 template <typename T>
 __device__ __forceinline__ T warp_sum(T v) {
 #pragma unroll

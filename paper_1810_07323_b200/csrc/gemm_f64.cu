@@ -357,14 +357,37 @@ __global__ void __launch_bounds__(S::NT, S::min_blocks)
         __syncthreads();
         const int64_t m0 = (fix_tile / tiles_n) * S::BM;
         const int n0 = int(fix_tile % tiles_n) * S::BN;
+        constexpr int TE2 = S::BM * S::BN / 2, VPT = 4;  // double2 elements; 4 per thread in flight
         const int64_t te = int64_t(S::BM) * S::BN;
-        const double* base = ws + fix_tile * max_seg * te;
-        for (int e = tid; e < S::BM * S::BN; e += S::NT) {
-            const int r = e / S::BN, cc = e % S::BN;
-            if (m0 + r >= Mo || n0 + cc >= N) continue;
-            double v = __ldcg(base + e);
-            for (int q = 1; q < fix_segs; ++q) v += __ldcg(base + q * te + e);
-            C[(m0 + r) * ldc + n0 + cc] = v;
+        const double2* base = reinterpret_cast<const double2*>(ws + fix_tile * max_seg * te);
+        for (int e0 = tid; e0 < TE2; e0 += S::NT * VPT) {
+            double2 acc[VPT];
+#pragma unroll
+            for (int v = 0; v < VPT; ++v) {
+                const int e2 = e0 + v * S::NT;
+                acc[v] = e2 < TE2 ? __ldcg(base + e2) : make_double2(0.0, 0.0);
+            }
+#pragma unroll 4
+            for (int q = 1; q < fix_segs; ++q) {
+                double2 t[VPT];
+#pragma unroll
+                for (int v = 0; v < VPT; ++v) {
+                    const int e2 = e0 + v * S::NT;
+                    t[v] = e2 < TE2 ? __ldcg(base + q * (te / 2) + e2) : make_double2(0.0, 0.0);
+                }
+#pragma unroll
+                for (int v = 0; v < VPT; ++v) { acc[v].x += t[v].x; acc[v].y += t[v].y; }
+            }
+#pragma unroll
+            for (int v = 0; v < VPT; ++v) {
+                const int e2 = e0 + v * S::NT;
+                if (e2 >= TE2) continue;
+                const int r = (2 * e2) / S::BN, cc = (2 * e2) % S::BN;
+                if (m0 + r >= Mo) continue;
+                double* dst = C + (m0 + r) * ldc + n0 + cc;
+                if (n0 + cc < N) dst[0] = acc[v].x;
+                if (n0 + cc + 1 < N) dst[1] = acc[v].y;
+            }
         }
     }
 }

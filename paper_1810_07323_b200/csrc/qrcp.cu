@@ -366,12 +366,14 @@ __global__ void __launch_bounds__(NW * 32) k_qrcp_reg(const T* __restrict__ M, i
             const T mu = tsqrt(add_rn(mul_rn(x0, x0), sig));
             const T v0 = (x0 <= T(0)) ? add_rn(x0, -mu) : -sig / add_rn(x0, mu);
             const T v0sq = mul_rn(v0, v0);
+            // one reciprocal beside beta's division instead of RPL serialised divisions (<= 1 ulp)
+            const T rv = T(1) / v0;
             beta = mul_rn(T(2) * v0, v0) / add_rn(sig, v0sq);
             diag = mu;
 #pragma unroll
             for (int u = 0; u < RPL; ++u) {
                 const int r = lane + 32 * u;
-                v[r] = r > jn ? x[u] / v0 : T(r == jn ? 1 : 0);
+                v[r] = r > jn ? mul_rn(x[u], rv) : T(r == jn ? 1 : 0);
             }
         } else {
 #pragma unroll

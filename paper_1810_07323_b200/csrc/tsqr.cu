@@ -45,6 +45,11 @@ __device__ __forceinline__ long long qrp_clock() {
 #define QRP_ADD(i, t0) qrp_acc[i] += qrp_clock() - (t0)
 #define QRP_TL(k, j) if (blockIdx.x == 0 && lane == 0) g_qr_tl[(k) * 256 + (j)] = qrp_clock()
 #define QRP_FLUSH if (threadIdx.x == 0 && blockIdx.x == 0) for (int i_ = 0; i_ < 8; ++i_) g_qr_phase[i_] += qrp_acc[i_]
+// k_qr_reg timeline: per step, cycles of [v load, apply, build, barrier] summed for warp 0 and for
+// the building warp (clock read made dependent on the phase's last result)
+__device__ long long g_qr_reg_ph[8];
+#define QRR_CLK(v, dep) long long v; asm volatile("mov.u64 %0, %%clock64;" : "=l"(v) : "d"(double(dep)) : "memory")
+#define QRR_ADD(i, dt) if (blockIdx.x == 0 && lane == 0) atomicAdd((unsigned long long*)&g_qr_reg_ph[i], (unsigned long long)(dt))
 #else
 #define QRP_T(v)
 #define QRP_ADD(i, t0)
@@ -53,6 +58,8 @@ __device__ __forceinline__ long long qrp_clock() {
 #define QRP_DECL
 #define QRP_TL(k, j)
 #define QRP_FLUSH
+#define QRR_CLK(v, dep)
+#define QRR_ADD(i, dt)
 #endif
 
 namespace {
@@ -85,10 +92,9 @@ __device__ __forceinline__ T warp_make_reflector(T* col, int rb, int j, int lane
     sig = warp_sum(sig);
     const T x0 = col[j];
     if (sig == T(0)) return T(0);
-    const T mu = tsqrt(x0 * x0 + sig);
-    const T v0 = (x0 <= T(0)) ? x0 - mu : -sig / (x0 + mu);
-    const T beta = T(2) * v0 * v0 / (sig + v0 * v0);
-    for (int i = j + 1 + lane; i < rb; i += 32) col[i] /= v0;
+    T mu, v0, beta, rv;
+    reflector_scalars(x0, sig, mu, v0, beta, rv);
+    for (int i = j + 1 + lane; i < rb; i += 32) col[i] *= rv;
     __syncwarp();
     if (lane == 0) col[j] = mu;
     __syncwarp();
@@ -397,12 +403,9 @@ __global__ void __launch_bounds__(kBThreads, 1)
                     const T x0 = W[c * ldw + j];
                     T bj = 0;
                     if (sig != T(0)) {
-                        const T mu = tsqrt(x0 * x0 + sig);
-                        const T v0 = (x0 <= T(0)) ? x0 - mu : -sig / (x0 + mu);
-                        bj = T(2) * v0 * v0 / (sig + v0 * v0);
-                        // v = x / v0 (qr.hpp:42); one reciprocal then independent products keeps the
-                        // division off the per-element critical path (<= 1 ulp from x / v0).
-                        const T rv = T(1) / v0;
+                        // v = x / v0 (qr.hpp:42) as x · (1/v0); short-latency scalars (common.cuh)
+                        T mu, v0, rv;
+                        reflector_scalars(x0, sig, mu, v0, bj, rv);
 #pragma unroll
                         for (int u = 0; u < kRPL; ++u) {
                             const int r = lane + 32 * u;
@@ -429,6 +432,9 @@ __global__ void __launch_bounds__(kBThreads, 1)
         const int K = rb - p0;
         const int c0 = p0 + nbp, nc = d - c0;
         T* C = W + c0 * ldw + p0;
+#ifdef CORU_ABL_CHAIN_ONLY  // tooling ablation: the panel chains alone (wrong results)
+        continue;
+#endif
         // ---- panel T factor: G = V_p^T V_p, T_p by the forward recurrence ----
         cta_mm(nbp, nbp, K, S.Vp + p0, ldvp, 1, S.Vp + p0, 1, ldvp, S.Gp, kNB, 1, T(1), false, S.scratch, kGemmScratch);
         QRP_ADD(6, t_tf);
@@ -450,7 +456,11 @@ __global__ void __launch_bounds__(kBThreads, 1)
         QRP_ADD(2, t_tf);
         QRP_T(t_tr);
         // ---- trailing update of columns [p0+nbp, d): C <- C - V_p T_p^T (V_p^T C), rows >= p0 ----
+#ifdef CORU_ABL_NO_TRAIL  // tooling ablation: no trailing update (wrong results)
+        if (false) {
+#else
         if (nc > 0) {
+#endif
             if constexpr (!kOverlap) {
                 cta_mm(nbp, nc, K, S.Vp + p0, ldvp, 1, C, 1, ldw, S.Y, d, 1, T(1), false, S.scratch, kGemmScratch);
                 __syncthreads();
@@ -579,10 +589,8 @@ __global__ void __launch_bounds__(kBThreads, 1)
                     const T x0 = col[j];
                     T bj = 0;
                     if (sig != T(0)) {
-                        const T mu = tsqrt(x0 * x0 + sig);
-                        const T v0 = (x0 <= T(0)) ? x0 - mu : -sig / (x0 + mu);
-                        bj = T(2) * v0 * v0 / (sig + v0 * v0);
-                        const T rv = T(1) / v0;
+                        T mu, v0, rv;
+                        reflector_scalars(x0, sig, mu, v0, bj, rv);
                         for (int i2 = j + 1 + lane; i2 < rb; i2 += 32) col[i2] *= rv;
                         __syncwarp();
                         if (lane == 0) col[j] = mu;
@@ -703,6 +711,234 @@ __global__ void __launch_bounds__(kBThreads, 1)
     }
 }
 
+// ============================================================================================
+// Register-resident path for narrow sketches (d <= 64, blocks of <= 256 rows: C1, C2). The d
+// reflector steps are the latency chain, so the factor kernel keeps the whole block in registers
+// (warp w owns columns w, w+16, ...; lane l holds rows l, l+32, ...) and runs ONE block barrier
+// per column: after applying H_j to its trailing columns (apply_reflector, qr.hpp:49-57), the warp
+// that owns column j+1 immediately builds reflector j+1 (make_reflector, qr.hpp:32-45) into a
+// double-buffered shared slot; after the barrier every warp applies it. The Q kernel keeps
+// [Q_above; 0] in registers the same way and applies the stored reflectors backwards
+// (accumulate_q order, qr.hpp:60-72) without any barrier. Scalar formulas use uncontracted
+// _rn operations like the reference; the reductions are tree-ordered.
+constexpr int kRegWarps = 16;
+constexpr int kRegRPL = 8;  // rows per lane: blocks of <= 256 rows
+
+template <typename T> __device__ __forceinline__ T mul_rn_t(T a, T b);
+template <> __device__ __forceinline__ double mul_rn_t<double>(double a, double b) { return __dmul_rn(a, b); }
+template <> __device__ __forceinline__ float mul_rn_t<float>(float a, float b) { return __fmul_rn(a, b); }
+template <typename T> __device__ __forceinline__ T add_rn_t(T a, T b);
+template <> __device__ __forceinline__ double add_rn_t<double>(double a, double b) { return __dadd_rn(a, b); }
+template <> __device__ __forceinline__ float add_rn_t<float>(float a, float b) { return __fadd_rn(a, b); }
+
+template <typename T, int CPW>
+__global__ void __launch_bounds__(kRegWarps * 32, 1)
+    k_qr_reg(const T* __restrict__ X, int64_t ldx, int64_t rows, int nb, int d, T* __restrict__ V, int ldv,
+             T* __restrict__ betas, T* __restrict__ Rout, int ldr) {
+    constexpr int RPL = kRegRPL, R = RPL * 32, NW = kRegWarps;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    T* slot_v = reinterpret_cast<T*>(smem_raw);  // [2][R]
+    T* slot_b = slot_v + 2 * R;                  // [2]
+    T* W = slot_b + 2;                           // staging, column-major [d][R + 1]
+    constexpr int ldw = R + 1;
+    const int b = blockIdx.x;
+    const int64_t r0 = rows * b / nb, r1 = rows * (b + 1) / nb;
+    const int rb = int(r1 - r0);
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    // coalesced row-major load -> column-major staging -> registers
+    for (int e = tid; e < rb * d; e += NW * 32) {
+        const int r = e / d, c = e % d;
+        W[c * ldw + r] = X[(r0 + r) * ldx + c];
+    }
+    __syncthreads();
+    T col[CPW][RPL];
+#pragma unroll
+    for (int k = 0; k < CPW; ++k) {
+        const int c = warp + NW * k;
+#pragma unroll
+        for (int u = 0; u < RPL; ++u) {
+            const int r = lane + 32 * u;
+            col[k][u] = (c < d && r < rb) ? W[c * ldw + r] : T(0);
+        }
+    }
+    // make_reflector for column jn (owned by this warp as col[kk]); publishes into slot sl.
+    auto build = [&](int jn, int kk, int sl) {
+        T x[RPL];
+#pragma unroll
+        for (int u = 0; u < RPL; ++u) {
+            x[u] = col[0][u];
+#pragma unroll
+            for (int k = 1; k < CPW; ++k) x[u] = (k == kk) ? col[k][u] : x[u];
+        }
+        T sig = 0, x0 = 0;
+#pragma unroll
+        for (int u = 0; u < RPL; ++u) {
+            const int r = lane + 32 * u;
+            if (r > jn) sig = add_rn_t(sig, mul_rn_t(x[u], x[u]));
+            if (r == jn) x0 = x[u];
+        }
+        sig = warp_sum(sig);
+        x0 = __shfl_sync(0xffffffffu, x0, jn & 31);
+        T* v = slot_v + sl * R;
+        T beta = 0;
+        if (sig != T(0)) {
+            T mu, v0, rv;
+            reflector_scalars(x0, sig, mu, v0, beta, rv);
+#pragma unroll
+            for (int u = 0; u < RPL; ++u) {
+                const int r = lane + 32 * u;
+                v[r] = r > jn && r < rb ? mul_rn_t(x[u], rv) : T(r == jn ? 1 : 0);
+                if (r == jn) {
+#pragma unroll
+                    for (int k = 0; k < CPW; ++k)
+                        if (k == kk) col[k][u] = mu;  // R(jn, jn) = mu
+                }
+            }
+        } else {  // sigma == 0: no reflection, the diagonal keeps its value (qr.hpp:37)
+#pragma unroll
+            for (int u = 0; u < RPL; ++u) v[lane + 32 * u] = T(0);
+        }
+        if (lane == 0) slot_b[sl] = beta;
+    };
+    if (warp == 0) build(0, 0, 0);
+    __syncthreads();
+    T* Vb = V + int64_t(b) * d * ldv;
+    for (int j = 0; j < d; ++j) {
+        const int sl = j & 1;
+        QRR_CLK(t0, 0);
+        const T beta = slot_b[sl];
+        T v[RPL];
+#pragma unroll
+        for (int u = 0; u < RPL; ++u) v[u] = slot_v[sl * R + lane + 32 * u];
+        QRR_CLK(t1, v[RPL - 1] + beta);
+        if (warp == j % NW) {  // the owner of column j stores reflector j for the Q kernel
+#pragma unroll
+            for (int u = 0; u < RPL; ++u) {
+                const int r = lane + 32 * u;
+                if (r < ldv) Vb[int64_t(j) * ldv + r] = r < rb ? v[u] : T(0);
+            }
+            if (lane == 0) betas[int64_t(b) * d + j] = beta;
+        }
+        if (beta != T(0)) {
+            T sk[CPW];
+#pragma unroll
+            for (int k = 0; k < CPW; ++k) {
+                sk[k] = 0;
+#pragma unroll
+                for (int u = 0; u < RPL; ++u) sk[k] += v[u] * col[k][u];
+            }
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+                for (int k = 0; k < CPW; ++k) sk[k] += __shfl_xor_sync(0xffffffffu, sk[k], o);
+#pragma unroll
+            for (int k = 0; k < CPW; ++k) {
+                const int c = warp + NW * k;
+                if (c > j && c < d) {
+                    const T sb = sk[k] * beta;
+#pragma unroll
+                    for (int u = 0; u < RPL; ++u) col[k][u] = add_rn_t(col[k][u], -mul_rn_t(sb, v[u]));
+                }
+            }
+        }
+        QRR_CLK(t2, col[CPW - 1][RPL - 1]);
+        if (j + 1 < d && warp == (j + 1) % NW) build(j + 1, (j + 1) / NW, sl ^ 1);
+        QRR_CLK(t3, col[0][0]);
+        __syncthreads();
+        QRR_CLK(t4, 0);
+        if (warp == 0) { QRR_ADD(0, t1 - t0); QRR_ADD(1, t2 - t1); QRR_ADD(2, t3 - t2); QRR_ADD(3, t4 - t3); }
+        if (j + 1 < d && warp == (j + 1) % NW) { QRR_ADD(4, t1 - t0); QRR_ADD(5, t2 - t1); QRR_ADD(6, t3 - t2); QRR_ADD(7, t4 - t3); }
+    }
+    // R (upper triangle, exact zeros below; qr.hpp:74-79) -> rows [b*d, (b+1)*d) of Rout
+#pragma unroll
+    for (int k = 0; k < CPW; ++k) {
+        const int c = warp + NW * k;
+        if (c < d) {
+#pragma unroll
+            for (int u = 0; u < RPL; ++u) {
+                const int r = lane + 32 * u;
+                if (r < d) Rout[(int64_t(b) * d + r) * ldr + c] = r <= c ? col[k][u] : T(0);
+            }
+        }
+    }
+}
+
+// Q block b = H_0 ... H_{d-1} [Qin_b; 0] (Qin null => identity), rows [r0, r1) of Qout.
+template <typename T, int CPW>
+__global__ void __launch_bounds__(kRegWarps * 32, 1)
+    k_qr_reg_form_q(const T* __restrict__ Qin, int ldqin, int64_t rows, int nb, int d, const T* __restrict__ V,
+                    int ldv, const T* __restrict__ betas, T* __restrict__ Qout, int64_t ldqout) {
+    constexpr int RPL = kRegRPL, R = RPL * 32, NW = kRegWarps;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    T* Vs = reinterpret_cast<T*>(smem_raw);  // [d][R] reflectors, later the output staging [d][R+1]
+    T* sb = Vs + size_t(d) * (R + 1);        // [d] betas
+    const int b = blockIdx.x;
+    const int64_t r0 = rows * b / nb, r1 = rows * (b + 1) / nb;
+    const int rb = int(r1 - r0);
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const T* Vb = V + int64_t(b) * d * ldv;
+    for (int e = tid; e < d * R; e += NW * 32) {
+        const int c = e / R, r = e % R;
+        Vs[c * R + r] = r < rb ? Vb[int64_t(c) * ldv + r] : T(0);
+    }
+    for (int c = tid; c < d; c += NW * 32) sb[c] = betas[int64_t(b) * d + c];
+    T col[CPW][RPL];
+#pragma unroll
+    for (int k = 0; k < CPW; ++k) {
+        const int c = warp + NW * k;
+#pragma unroll
+        for (int u = 0; u < RPL; ++u) {
+            const int r = lane + 32 * u;
+            T x = T(0);
+            if (c < d && r < d) x = Qin ? Qin[(int64_t(b) * d + r) * ldqin + c] : T(r == c ? 1 : 0);
+            col[k][u] = x;
+        }
+    }
+    __syncthreads();
+    for (int j = d - 1; j >= 0; --j) {
+        const T beta = sb[j];
+        if (beta == T(0)) continue;
+        T v[RPL];
+#pragma unroll
+        for (int u = 0; u < RPL; ++u) v[u] = Vs[j * R + lane + 32 * u];
+        T sk[CPW];
+#pragma unroll
+        for (int k = 0; k < CPW; ++k) {
+            sk[k] = 0;
+#pragma unroll
+            for (int u = 0; u < RPL; ++u) sk[k] += v[u] * col[k][u];
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+            for (int k = 0; k < CPW; ++k) sk[k] += __shfl_xor_sync(0xffffffffu, sk[k], o);
+#pragma unroll
+        for (int k = 0; k < CPW; ++k) {
+            const T s2 = sk[k] * beta;
+#pragma unroll
+            for (int u = 0; u < RPL; ++u) col[k][u] = add_rn_t(col[k][u], -mul_rn_t(s2, v[u]));
+        }
+    }
+    __syncthreads();  // reuse Vs as the output staging
+    constexpr int ldo = R + 1;
+#pragma unroll
+    for (int k = 0; k < CPW; ++k) {
+        const int c = warp + NW * k;
+        if (c < d) {
+#pragma unroll
+            for (int u = 0; u < RPL; ++u) Vs[c * ldo + lane + 32 * u] = col[k][u];
+        }
+    }
+    __syncthreads();
+    for (int e = tid; e < rb * d; e += NW * 32) {
+        const int r = e / d, c = e % d;
+        Qout[(r0 + r) * ldqout + c] = Vs[c * ldo + r];
+    }
+}
+
+size_t reg_factor_smem_bytes(int d, size_t eb) { return (2 * size_t(kRegRPL * 32) + 2 + size_t(d) * (kRegRPL * 32 + 1)) * eb; }
+size_t reg_formq_smem_bytes(int d, size_t eb) { return (size_t(d) * (kRegRPL * 32 + 1) + d) * eb; }
+
 size_t wide_factor_smem_bytes(int rbmax, int d, size_t eb) {
     return ((d * 4 + 15) / 16) * 16 + ((d + 1) / 2) * 2 * eb + size_t(rbmax | 1) * d * eb;
 }
@@ -731,12 +967,19 @@ TsqrPlan plan_tsqr(int64_t m, int d, size_t eb, int max_smem) {
             break;
         }
     const bool big_ok = rb_big >= 2 * d + 2;
+    // Narrow sketches: the register-resident kernels (one barrier per column) on <= 256-row blocks.
+#ifdef CORU_TSQR_REG  // tooling: the register-resident kernels (slower than the blocked ones on B200)
+    const bool reg_ok = d <= 64 && reg_factor_smem_bytes(d, eb) <= cap && reg_formq_smem_bytes(d, eb) <= cap;
+#else
+    const bool reg_ok = false;
+#endif
     // The shared-memory kernels are fastest per block, but when they cannot reduce a level by at
     // least 2x (wide sketches: d = 110 fits only ~168 rows) the tree gets deep and every level
     // costs d sequential reflector steps; then the L2-resident kernels with ~1024-row blocks win.
     const bool blocked_ok = rb_blocked >= 2 * d + 2 || (rb_blocked >= d + 1 + d / 4 && !big_ok);
     int target;
-    if (blocked_ok) target = rb_blocked;
+    if (reg_ok) target = kRegRPL * 32;
+    else if (blocked_ok) target = rb_blocked;
     else if (big_ok) target = std::min(rb_big, std::max(4 * d, 1024));
     else target = std::max(4 * d, 256);
     int64_t rows = m;
@@ -749,15 +992,17 @@ TsqrPlan plan_tsqr(int64_t m, int d, size_t eb, int max_smem) {
         nb = std::max<int64_t>(1, std::min<int64_t>(nb, rows / (d + 1)));
         L.nb = int(nb);
         L.rbmax = int((rows + nb - 1) / nb);
-        if (blocked_ok && L.rbmax <= rb_blocked) {
+        if (reg_ok && L.rbmax <= kRegRPL * 32) {
+            L.kind = TsqrLevel::kReg;
+        } else if (blocked_ok && L.rbmax <= rb_blocked) {
             L.kind = TsqrLevel::kBlockedSmem;
         } else if (rb_big > d && L.rbmax <= rb_big) {
             L.kind = TsqrLevel::kBlockedGlobal;
         } else {
             L.kind = TsqrLevel::kWide;
         }
-        L.blocked = L.kind != TsqrLevel::kWide;
-        L.smem = L.kind == TsqrLevel::kBlockedSmem ||
+        L.blocked = L.kind == TsqrLevel::kBlockedSmem || L.kind == TsqrLevel::kBlockedGlobal;
+        L.smem = L.kind == TsqrLevel::kBlockedSmem || L.kind == TsqrLevel::kReg ||
                  (L.kind == TsqrLevel::kWide && wide_factor_smem_bytes(L.rbmax, d, eb) <= cap);
         L.ldv = L.rbmax + (L.rbmax % 2);
         L.v_off = voff;
@@ -800,7 +1045,18 @@ cudaError_t tsqr_factor(const TsqrPlan& p, const T* B, int64_t ldb, T* V, T* bet
     for (size_t l = 0; l < p.levels.size(); ++l) {
         const TsqrLevel& L = p.levels[l];
         T* Rl = (l + 1 == p.levels.size()) ? r_out : R + L.r_off;
-        if (L.kind == TsqrLevel::kBlockedSmem) {
+        if (L.kind == TsqrLevel::kReg) {
+            const size_t sm = reg_factor_smem_bytes(d, sizeof(T));
+            if (d <= 32) {
+                allow_max_smem(k_qr_reg<T, 2>);
+                k_qr_reg<T, 2><<<L.nb, kRegWarps * 32, sm, st>>>(X, ldx, L.rows, L.nb, d, V + L.v_off, L.ldv,
+                                                                 beta + L.beta_off, Rl, d);
+            } else {
+                allow_max_smem(k_qr_reg<T, 4>);
+                k_qr_reg<T, 4><<<L.nb, kRegWarps * 32, sm, st>>>(X, ldx, L.rows, L.nb, d, V + L.v_off, L.ldv,
+                                                                 beta + L.beta_off, Rl, d);
+            }
+        } else if (L.kind == TsqrLevel::kBlockedSmem) {
             const size_t sm = BlockedSmem<T>::bytes(d, L.rbmax, sizeof(T));
             allow_max_smem(k_qr_blocked<T>);
             k_qr_blocked<T><<<L.nb, kBThreads, sm, st>>>(X, ldx, L.rows, L.nb, d, V + L.v_off, L.ldv,
@@ -843,7 +1099,18 @@ cudaError_t tsqr_form_q(const TsqrPlan& p, const T* q_top, T* V, T* beta, T* Tar
         const TsqrLevel& L = p.levels[size_t(l)];
         T* out = (l == 0) ? Q : ((p.levels.size() - 1 - size_t(l)) % 2 == 0 ? ping : pong);
         const int64_t ldo = (l == 0) ? ldq : d;
-        if (L.blocked) {
+        if (L.kind == TsqrLevel::kReg) {
+            const size_t sm = reg_formq_smem_bytes(d, sizeof(T));
+            if (d <= 32) {
+                allow_max_smem(k_qr_reg_form_q<T, 2>);
+                k_qr_reg_form_q<T, 2><<<L.nb, kRegWarps * 32, sm, st>>>(qin, ldqin, L.rows, L.nb, d, V + L.v_off,
+                                                                        L.ldv, beta + L.beta_off, out, ldo);
+            } else {
+                allow_max_smem(k_qr_reg_form_q<T, 4>);
+                k_qr_reg_form_q<T, 4><<<L.nb, kRegWarps * 32, sm, st>>>(qin, ldqin, L.rows, L.nb, d, V + L.v_off,
+                                                                        L.ldv, beta + L.beta_off, out, ldo);
+            }
+        } else if (L.blocked) {
             const bool stage = FormQSmem<T>::bytes(d, L.rbmax, sizeof(T), true) <= size_t(max_smem);
             const size_t sm = FormQSmem<T>::bytes(d, L.rbmax, sizeof(T), stage);
             allow_max_smem(k_qr_blocked_form_q<T>);

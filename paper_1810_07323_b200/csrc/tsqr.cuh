@@ -17,7 +17,7 @@ struct TsqrLevel {
     int64_t beta_off = 0;  // offset of the betas
     int64_t r_off = 0;     // offset of the stacked R (nb*d x d, ld = d) output in the R arena
     int64_t t_off = 0;     // offset of the per-block compact-WY T factors (blocked path)
-    enum Kind { kBlockedSmem = 0, kBlockedGlobal = 1, kWide = 2 };
+    enum Kind { kBlockedSmem = 0, kBlockedGlobal = 1, kWide = 2, kReg = 3 };
     Kind kind = kBlockedSmem;  // which kernel pair factors / forms Q for this level
     bool blocked = false;  // panel-blocked compact-WY kernels (else the unblocked column pipeline)
     bool smem = true;      // working block lives in shared memory (else in the V arena, L2)
