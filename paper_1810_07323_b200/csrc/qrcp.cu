@@ -363,12 +363,9 @@ __global__ void __launch_bounds__(NW * 32) k_qrcp_reg(const T* __restrict__ M, i
         T* v = cand_v + (sl * NW + warp) * R;
         T beta = 0, diag = x0;
         if (sig != T(0)) {  // make_reflector (qr.hpp:32-45); sigma == 0 leaves the diagonal (qr.hpp:37)
-            const T mu = tsqrt(add_rn(mul_rn(x0, x0), sig));
-            const T v0 = (x0 <= T(0)) ? add_rn(x0, -mu) : -sig / add_rn(x0, mu);
-            const T v0sq = mul_rn(v0, v0);
-            // one reciprocal beside beta's division instead of RPL serialised divisions (<= 1 ulp)
-            const T rv = T(1) / v0;
-            beta = mul_rn(T(2) * v0, v0) / add_rn(sig, v0sq);
+            // make_reflector's scalars with short-latency reciprocals (common.cuh), few ulp
+            T mu, v0, rv;
+            reflector_scalars(x0, sig, mu, v0, beta, rv);
             diag = mu;
 #pragma unroll
             for (int u = 0; u < RPL; ++u) {
@@ -390,23 +387,23 @@ __global__ void __launch_bounds__(NW * 32) k_qrcp_reg(const T* __restrict__ M, i
     for (int j = 0; j < d; ++j) {
         const int sl = j & 1;
         // ---- global pivot: the best of the NW candidates (larger colsq, then lower position) ----
+        // (position, warp) packed in one key: a smaller key is a lower position; empty = INT_MAX
         T wv = T(0);
-        int wp = INT_MAX, ww = -1;
+        int key = INT_MAX;
         if (lane < NW) {
             const int p = cand_i[(sl * NW + lane) * 2];
-            if (p != INT_MAX) { wv = cand_s[(sl * NW + lane) * 3]; wp = p; ww = lane; }
+            if (p != INT_MAX) { wv = cand_s[(sl * NW + lane) * 3]; key = (p << 5) | lane; }
         }
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
+        for (int o = NW / 2; o > 0; o >>= 1) {  // lanes [0, NW) only
             const T ov = __shfl_xor_sync(0xffffffffu, wv, o);
-            const int op = __shfl_xor_sync(0xffffffffu, wp, o);
-            const int ow = __shfl_xor_sync(0xffffffffu, ww, o);
-            if (ow >= 0 && (ww < 0 || ov > wv || (ov == wv && op < wp))) { wv = ov; wp = op; ww = ow; }
+            const int ok = __shfl_xor_sync(0xffffffffu, key, o);
+            if (ok != INT_MAX && (key == INT_MAX || ov > wv || (ov == wv && ok < key))) { wv = ov; key = ok; }
         }
         // lane 0's choice for the whole CTA: with NaN norms the butterfly need not agree across
         // lanes, and every later branch must stay warp-uniform (shuffles inside)
-        ww = __shfl_sync(0xffffffffu, ww, 0);
-        wp = __shfl_sync(0xffffffffu, wp, 0);
+        key = __shfl_sync(0xffffffffu, key, 0);
+        const int ww = key & 31, wp = key >> 5;
         const T* cs = cand_s + (sl * NW + ww) * 3;
         const T beta = cs[1], diag = cs[2];
         const int wcol = cand_i[(sl * NW + ww) * 2 + 1];
@@ -441,10 +438,7 @@ __global__ void __launch_bounds__(NW * 32) k_qrcp_reg(const T* __restrict__ M, i
 #pragma unroll
                 for (int u = 0; u < RPL; ++u) s[k] += v[u] * col[k][u];
             }
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1)
-#pragma unroll
-                for (int k = 0; k < CPW; ++k) s[k] += __shfl_xor_sync(0xffffffffu, s[k], o);
+            warp_allreduce_vec<CPW>(s, lane);
 #pragma unroll
             for (int k = 0; k < CPW; ++k) {
                 if (pos[k] > j && pos[k] < d) {
@@ -504,10 +498,7 @@ __global__ void __launch_bounds__(NW * 32) k_qrcp_reg(const T* __restrict__ M, i
 #pragma unroll
             for (int u = 0; u < RPL; ++u) s[k] += v[u] * col[k][u];
         }
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1)
-#pragma unroll
-            for (int k = 0; k < CPW; ++k) s[k] += __shfl_xor_sync(0xffffffffu, s[k], o);
+        warp_allreduce_vec<CPW>(s, lane);
 #pragma unroll
         for (int k = 0; k < CPW; ++k) {
             const T sb = s[k] * bj;
