@@ -77,6 +77,10 @@ int coru_ctx_set_phi_mode(coru_ctx* ctx, int mode);
  *     (CORU_F32_TC still uses FFMA where the tensor-core kernel cannot take the shape). */
 enum { CORU_F32_AUTO = 0, CORU_F32_SIMT = 1, CORU_F32_TC = 2 };
 int coru_ctx_set_f32_path(coru_ctx* ctx, int mode);
+/* QR of wide sketches (more than 128 columns; householder_qr at corutv.hpp:59-60): 1 (default) =
+ * CholeskyQR2 in fp64 with a device-side fall-back to the Householder tree when the sketch is
+ * ill-conditioned (estimated cond > 1e6) or the Cholesky breaks down; 0 = Householder tree only. */
+int coru_ctx_set_wide_qr(coru_ctx* ctx, int enable);
 
 /* ---- multi-GPU: one process (and context) per GPU, A row-block sharded --------------------- */
 /* Rank 0 creates the id and distributes it (e.g. torch.distributed broadcast); every rank then

@@ -137,6 +137,7 @@ def load_library():
     L.coru_ctx_set_host_threads.argtypes = [p, i32]
     L.coru_ctx_set_phi_mode.argtypes = [p, i32]
     L.coru_ctx_set_f32_path.argtypes = [p, i32]
+    L.coru_ctx_set_wide_qr.argtypes = [p, i32]
     L.coru_comm_unique_id.argtypes = [p]
     L.coru_ctx_init_comm.argtypes = [p, i32, i32, p]
     L.coru_ctx_set_profiling.argtypes = [p, i32]
@@ -233,6 +234,11 @@ class Context:
         """fp32 A-pass engine: F32_AUTO (default: tcgen05 3xTF32 tensor cores for A-pass-sized
         products), F32_SIMT (CUDA-core FFMA), F32_TC (tensor cores wherever the shape allows)."""
         _check(self.lib.coru_ctx_set_f32_path(self.h, mode))
+
+    def set_wide_qr(self, on: bool):
+        """QR of sketches wider than 128 columns: CholeskyQR2 in fp64 with a device-side Householder
+        fall-back (default), or the Householder tree only."""
+        _check(self.lib.coru_ctx_set_wide_qr(self.h, 1 if on else 0))
 
     def set_profiling(self, on: bool):
         _check(self.lib.coru_ctx_set_profiling(self.h, 1 if on else 0))

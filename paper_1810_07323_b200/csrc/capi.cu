@@ -27,6 +27,7 @@
 #include "../../include/coru_gpu.h"
 #include "gemm.cuh"
 #include "qrcp.cuh"
+#include "cholqr.cuh"
 #include "rng_dev.cuh"
 #include "tsqr.cuh"
 
@@ -170,6 +171,7 @@ struct coru_ctx {
     int host_threads = 1;
     int phi_mode = CORU_PHI_DEVICE;
     int f32_path = CORU_F32_AUTO;
+    bool wide_qr = true;  // CholeskyQR2 (fp64) for sketches wider than 128 columns, Householder fall-back
     char* arena = nullptr;
     size_t arena_bytes = 0;
     char* pinned = nullptr;
@@ -311,23 +313,44 @@ template <typename T>
 struct TsqrBufs {
     TsqrPlan plan;
     T *v = nullptr, *beta = nullptr, *tarena = nullptr, *rarena = nullptr, *scratch = nullptr;
-    int max_smem = 0;
-    void carve(Carver& cv, int64_t rows, int d, int smem) {
+    int max_smem = 0, sms = 148;
+    // Wide sketches: CholeskyQR2 in fp64 first; the Householder tree is gated on its status.
+    bool chol = false;
+    CholQrPlan cp;
+    double* cws = nullptr;
+    int* status = nullptr;
+    void carve(Carver& cv, int64_t rows, int d, int smem, int num_sms = 148, bool allow_chol = false) {
         max_smem = smem;
+        sms = num_sms;
         plan = plan_tsqr(rows, d, sizeof(T), smem);
         v = cv.take<T>(plan.v_elems);
         beta = cv.take<T>(plan.beta_elems);
         tarena = cv.take<T>(plan.t_elems);
         rarena = cv.take<T>(plan.r_elems);
         scratch = cv.take<T>(tsqr_scratch_elems(plan));
+        chol = allow_chol && cholqr_applicable(rows, d, smem);
+        if (chol) {
+            cp = plan_cholqr(rows, d, sizeof(T), num_sms);
+            cws = cv.take<double>(cholqr_ws_doubles(cp));
+            status = cv.take<int>(1);
+        }
     }
     int factor(const T* B, int64_t ldb, T* r_out, cudaStream_t st) {
-        CORU_CUDA(tsqr_factor<T>(plan, B, ldb, v, beta, tarena, rarena, r_out, st));
+        if (chol) {
+            CORU_CUDA(cholqr_factor<T>(cp, B, ldb, cws, status, r_out, max_smem, sms, st));
+            g_launches += cholqr_launches(plan.d);
+        }
+        CORU_CUDA(tsqr_factor<T>(plan, B, ldb, v, beta, tarena, rarena, r_out, st, chol ? status : nullptr));
         g_launches += int64_t(plan.levels.size());
         return CORU_OK;
     }
     int form_q(const T* q_top, T* Q, int64_t ldq, cudaStream_t st) {
-        CORU_CUDA(tsqr_form_q<T>(plan, q_top, v, beta, tarena, scratch, Q, ldq, max_smem, st));
+        if (chol) {
+            if (q_top) return fail(CORU_ECUDA, "internal: CholeskyQR2 tree with a top-level Q");
+            CORU_CUDA(cholqr_form_q<T>(cp, cws, Q, ldq, sms, st));
+            ++g_launches;
+        }
+        CORU_CUDA(tsqr_form_q<T>(plan, q_top, v, beta, tarena, scratch, Q, ldq, max_smem, st, chol ? status : nullptr));
         g_launches += int64_t(plan.levels.size());
         return CORU_OK;
     }
@@ -385,8 +408,9 @@ struct Work {
         gws_elems = std::max({gemm_ws<T>(r.op_a(), R, N, d, sms), gemm_ws<T>(r.op_at(), N, R, d, sms),
                               gemm_ws<T>(Op::T, d, R, d, sms), gemm_ws<T>(Op::N, R, d, d, sms)});
         gws = cv.take<T>(gws_elems);
-        ts1.carve(cv, R, d, c->max_smem);
-        ts2.carve(cv, N, d, c->max_smem);
+        // CholeskyQR2 for wide sketches, except for Q1 when sharded (its tree's top level is cross-rank)
+        ts1.carve(cv, R, d, c->max_smem, sms, c->world == 1 && c->wide_qr);
+        ts2.carve(cv, N, d, c->max_smem, sms, c->wide_qr);
         if (c->world > 1) {
             rstack = cv.take<T>(int64_t(c->world) * d * d);
             tstop.carve(cv, int64_t(c->world) * d, d, c->max_smem);
@@ -876,6 +900,13 @@ int coru_ctx_set_f32_path(coru_ctx* c, int mode) {
     return CORU_OK;
 }
 
+int coru_ctx_set_wide_qr(coru_ctx* c, int enable) {
+    if (!c) return fail(CORU_EINVAL, "null context");
+    std::lock_guard<std::mutex> lk(c->mu);
+    c->wide_qr = enable != 0;
+    return CORU_OK;
+}
+
 int coru_comm_unique_id(unsigned char id[128]) {
     Nccl* api = nccl();
     if (!api) return fail(CORU_ENCCL, "NCCL unavailable");
@@ -1124,11 +1155,11 @@ int coru_tsqr_f64_dev(coru_ctx* c, const double* B, int64_t ldb, int64_t m, int6
     if (n < 1 || m <= n) return fail(CORU_EINVAL, "householder_qr: requires rows > cols for TSQR");
     TsqrBufs<double> tb;
     Carver meas{nullptr, 0};
-    tb.carve(meas, m, int(n), c->max_smem);
+    tb.carve(meas, m, int(n), c->max_smem, c->num_sms, c->wide_qr);
     double* r = meas.take<double>(n * n);
     CORU_TRY(ensure_arena(c, meas.off));
     Carver cv{c->arena, 0};
-    tb.carve(cv, m, int(n), c->max_smem);
+    tb.carve(cv, m, int(n), c->max_smem, c->num_sms, c->wide_qr);
     r = cv.take<double>(n * n);
     CORU_TRY(tb.factor(B, ldb, r, c->stream));
     CORU_TRY(tb.form_q(nullptr, Q, ldq, c->stream));

@@ -23,7 +23,10 @@ inline void allow_max_smem(const void* kernel) {
     if (!done.insert({kernel, dev}).second) return;
     int v = 0;
     cudaDeviceGetAttribute(&v, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    cudaFuncAttributes fa{};
+    if (cudaFuncGetAttributes(&fa, kernel) == cudaSuccess) v -= int(fa.sharedSizeBytes);  // static smem counts too
     cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, v);
+    cudaGetLastError();  // never leave a stale error for the caller's launch check
 }
 template <typename K>
 inline void allow_max_smem(K* kernel) {

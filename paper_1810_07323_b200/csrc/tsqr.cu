@@ -119,7 +119,8 @@ __device__ __forceinline__ void warp_apply_reflector(const T* vcol, T beta, int 
 template <typename T>
 __global__ void __launch_bounds__(kThreads) k_hh_factor(const T* __restrict__ X, int64_t ldx, int64_t rows, int nb,
                                                         int d, T* __restrict__ V, int ldv, T* __restrict__ betas,
-                                                        T* __restrict__ Rout, int ldr, int use_smem) {
+                                                        T* __restrict__ Rout, int ldr, int use_smem, const int* __restrict__ gate) {
+    if (gate && *gate == 0) return;  // CholeskyQR2 already produced this QR (cholqr.cu)
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int b = blockIdx.x;
     const int64_t r0 = rows * b / nb, r1 = rows * (b + 1) / nb;
@@ -197,7 +198,8 @@ template <typename T>
 __global__ void __launch_bounds__(kThreads) k_hh_form_q(const T* __restrict__ Qin, int ldqin, int64_t rows, int nb,
                                                         int d, const T* __restrict__ V, int ldv,
                                                         const T* __restrict__ betas, T* __restrict__ Qout,
-                                                        int64_t ldqout, T* __restrict__ gscratch, int use_smem) {
+                                                        int64_t ldqout, T* __restrict__ gscratch, int use_smem, const int* __restrict__ gate) {
+    if (gate && *gate == 0) return;  // CholeskyQR2 already produced this QR (cholqr.cu)
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int b = blockIdx.x;
     const int64_t r0 = rows * b / nb, r1 = rows * (b + 1) / nb;
@@ -309,7 +311,8 @@ struct BlockedSmem {
 template <typename T>
 __global__ void __launch_bounds__(kBThreads, 1)
     k_qr_blocked(const T* __restrict__ X, int64_t ldx, int64_t rows, int nb, int d, T* __restrict__ V, int ldv,
-                 T* __restrict__ betas, T* __restrict__ Tg, T* __restrict__ Rout, int ldr) {
+                 T* __restrict__ betas, T* __restrict__ Tg, T* __restrict__ Rout, int ldr, const int* __restrict__ gate) {
+    if (gate && *gate == 0) return;  // CholeskyQR2 already produced this QR (cholqr.cu)
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int b = blockIdx.x;
     const int64_t r0 = rows * b / nb, r1 = rows * (b + 1) / nb;
@@ -522,7 +525,8 @@ struct BigSmem {
 template <typename T>
 __global__ void __launch_bounds__(kBThreads, 1)
     k_qr_blocked_g(const T* __restrict__ X, int64_t ldx, int64_t rows, int nb, int d, T* __restrict__ V, int ldv,
-                   T* __restrict__ betas, T* __restrict__ Tg, T* __restrict__ Rout, int ldr) {
+                   T* __restrict__ betas, T* __restrict__ Tg, T* __restrict__ Rout, int ldr, const int* __restrict__ gate) {
+    if (gate && *gate == 0) return;  // CholeskyQR2 already produced this QR (cholqr.cu)
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int b = blockIdx.x;
     const int64_t r0 = rows * b / nb, r1 = rows * (b + 1) / nb;
@@ -668,7 +672,8 @@ struct FormQSmem {
 template <typename T>
 __global__ void __launch_bounds__(kBThreads, 1)
     k_qr_blocked_form_q(const T* __restrict__ Qin, int ldqin, int64_t rows, int nb, int d, const T* __restrict__ V,
-                        int ldv, const T* __restrict__ Tg, T* __restrict__ Qout, int64_t ldqout, int stage) {
+                        int ldv, const T* __restrict__ Tg, T* __restrict__ Qout, int64_t ldqout, int stage, const int* __restrict__ gate) {
+    if (gate && *gate == 0) return;  // CholeskyQR2 already produced this QR (cholqr.cu)
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int b = blockIdx.x;
     const int64_t r0 = rows * b / nb, r1 = rows * (b + 1) / nb;
@@ -734,7 +739,8 @@ template <> __device__ __forceinline__ float add_rn_t<float>(float a, float b) {
 template <typename T, int CPW>
 __global__ void __launch_bounds__(kRegWarps * 32, 1)
     k_qr_reg(const T* __restrict__ X, int64_t ldx, int64_t rows, int nb, int d, T* __restrict__ V, int ldv,
-             T* __restrict__ betas, T* __restrict__ Rout, int ldr) {
+             T* __restrict__ betas, T* __restrict__ Rout, int ldr, const int* __restrict__ gate) {
+    if (gate && *gate == 0) return;  // CholeskyQR2 already produced this QR (cholqr.cu)
     constexpr int RPL = kRegRPL, R = RPL * 32, NW = kRegWarps;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     T* slot_v = reinterpret_cast<T*>(smem_raw);  // [2][R]
@@ -867,7 +873,8 @@ __global__ void __launch_bounds__(kRegWarps * 32, 1)
 template <typename T, int CPW>
 __global__ void __launch_bounds__(kRegWarps * 32, 1)
     k_qr_reg_form_q(const T* __restrict__ Qin, int ldqin, int64_t rows, int nb, int d, const T* __restrict__ V,
-                    int ldv, const T* __restrict__ betas, T* __restrict__ Qout, int64_t ldqout) {
+                    int ldv, const T* __restrict__ betas, T* __restrict__ Qout, int64_t ldqout, const int* __restrict__ gate) {
+    if (gate && *gate == 0) return;  // CholeskyQR2 already produced this QR (cholqr.cu)
     constexpr int RPL = kRegRPL, R = RPL * 32, NW = kRegWarps;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     T* Vs = reinterpret_cast<T*>(smem_raw);  // [d][R] reflectors, later the output staging [d][R+1]
@@ -1038,7 +1045,7 @@ int64_t tsqr_scratch_elems(const TsqrPlan& p) {
 
 template <typename T>
 cudaError_t tsqr_factor(const TsqrPlan& p, const T* B, int64_t ldb, T* V, T* beta, T* Tarena, T* R, T* r_out,
-                        cudaStream_t st) {
+                        cudaStream_t st, const int* gate) {
     const int d = p.d;
     const T* X = B;
     int64_t ldx = ldb;
@@ -1050,27 +1057,27 @@ cudaError_t tsqr_factor(const TsqrPlan& p, const T* B, int64_t ldb, T* V, T* bet
             if (d <= 32) {
                 allow_max_smem(k_qr_reg<T, 2>);
                 k_qr_reg<T, 2><<<L.nb, kRegWarps * 32, sm, st>>>(X, ldx, L.rows, L.nb, d, V + L.v_off, L.ldv,
-                                                                 beta + L.beta_off, Rl, d);
+                                                                 beta + L.beta_off, Rl, d, gate);
             } else {
                 allow_max_smem(k_qr_reg<T, 4>);
                 k_qr_reg<T, 4><<<L.nb, kRegWarps * 32, sm, st>>>(X, ldx, L.rows, L.nb, d, V + L.v_off, L.ldv,
-                                                                 beta + L.beta_off, Rl, d);
+                                                                 beta + L.beta_off, Rl, d, gate);
             }
         } else if (L.kind == TsqrLevel::kBlockedSmem) {
             const size_t sm = BlockedSmem<T>::bytes(d, L.rbmax, sizeof(T));
             allow_max_smem(k_qr_blocked<T>);
             k_qr_blocked<T><<<L.nb, kBThreads, sm, st>>>(X, ldx, L.rows, L.nb, d, V + L.v_off, L.ldv,
-                                                          beta + L.beta_off, Tarena + L.t_off, Rl, d);
+                                                          beta + L.beta_off, Tarena + L.t_off, Rl, d, gate);
         } else if (L.kind == TsqrLevel::kBlockedGlobal) {
             const size_t sm = BigSmem<T>::bytes(d, L.rbmax, sizeof(T));
             allow_max_smem(k_qr_blocked_g<T>);
             k_qr_blocked_g<T><<<L.nb, kBThreads, sm, st>>>(X, ldx, L.rows, L.nb, d, V + L.v_off, L.ldv,
-                                                            beta + L.beta_off, Tarena + L.t_off, Rl, d);
+                                                            beta + L.beta_off, Tarena + L.t_off, Rl, d, gate);
         } else {
             const size_t sm = L.smem ? wide_factor_smem_bytes(L.rbmax, d, sizeof(T)) : wide_factor_smem_bytes(0, d, sizeof(T));
             allow_max_smem(k_hh_factor<T>);
             k_hh_factor<T><<<L.nb, kThreads, sm, st>>>(X, ldx, L.rows, L.nb, d, V + L.v_off, L.ldv,
-                                                        beta + L.beta_off, Rl, d, L.smem ? 1 : 0);
+                                                        beta + L.beta_off, Rl, d, L.smem ? 1 : 0, gate);
         }
         cudaError_t e = cudaGetLastError();
         if (e != cudaSuccess) return e;
@@ -1082,7 +1089,7 @@ cudaError_t tsqr_factor(const TsqrPlan& p, const T* B, int64_t ldb, T* V, T* bet
 
 template <typename T>
 cudaError_t tsqr_form_q(const TsqrPlan& p, const T* q_top, T* V, T* beta, T* Tarena, T* scratch, T* Q, int64_t ldq,
-                        int max_smem, cudaStream_t st) {
+                        int max_smem, cudaStream_t st, const int* gate) {
     const int d = p.d;
     // scratch = [wide-path working blocks | ping | pong]
     int64_t work = 0, maxrows = 0;
@@ -1104,11 +1111,11 @@ cudaError_t tsqr_form_q(const TsqrPlan& p, const T* q_top, T* V, T* beta, T* Tar
             if (d <= 32) {
                 allow_max_smem(k_qr_reg_form_q<T, 2>);
                 k_qr_reg_form_q<T, 2><<<L.nb, kRegWarps * 32, sm, st>>>(qin, ldqin, L.rows, L.nb, d, V + L.v_off,
-                                                                        L.ldv, beta + L.beta_off, out, ldo);
+                                                                        L.ldv, beta + L.beta_off, out, ldo, gate);
             } else {
                 allow_max_smem(k_qr_reg_form_q<T, 4>);
                 k_qr_reg_form_q<T, 4><<<L.nb, kRegWarps * 32, sm, st>>>(qin, ldqin, L.rows, L.nb, d, V + L.v_off,
-                                                                        L.ldv, beta + L.beta_off, out, ldo);
+                                                                        L.ldv, beta + L.beta_off, out, ldo, gate);
             }
         } else if (L.blocked) {
             const bool stage = FormQSmem<T>::bytes(d, L.rbmax, sizeof(T), true) <= size_t(max_smem);
@@ -1116,12 +1123,12 @@ cudaError_t tsqr_form_q(const TsqrPlan& p, const T* q_top, T* V, T* beta, T* Tar
             allow_max_smem(k_qr_blocked_form_q<T>);
             const dim3 grid(unsigned(L.nb), unsigned((d + kQChunk - 1) / kQChunk));
             k_qr_blocked_form_q<T><<<grid, kBThreads, sm, st>>>(qin, ldqin, L.rows, L.nb, d, V + L.v_off, L.ldv,
-                                                                 Tarena + L.t_off, out, ldo, stage ? 1 : 0);
+                                                                 Tarena + L.t_off, out, ldo, stage ? 1 : 0, gate);
         } else {
             const size_t sm = L.smem ? size_t(L.rbmax | 1) * d * sizeof(T) : 0;
             allow_max_smem(k_hh_form_q<T>);
             k_hh_form_q<T><<<L.nb, kThreads, sm, st>>>(qin, ldqin, L.rows, L.nb, d, V + L.v_off, L.ldv,
-                                                        beta + L.beta_off, out, ldo, scratch, L.smem ? 1 : 0);
+                                                        beta + L.beta_off, out, ldo, scratch, L.smem ? 1 : 0, gate);
         }
         cudaError_t e = cudaGetLastError();
         if (e != cudaSuccess) return e;
@@ -1132,12 +1139,12 @@ cudaError_t tsqr_form_q(const TsqrPlan& p, const T* q_top, T* V, T* beta, T* Tar
 }
 
 template cudaError_t tsqr_factor<double>(const TsqrPlan&, const double*, int64_t, double*, double*, double*, double*,
-                                         double*, cudaStream_t);
+                                         double*, cudaStream_t, const int*);
 template cudaError_t tsqr_factor<float>(const TsqrPlan&, const float*, int64_t, float*, float*, float*, float*, float*,
-                                        cudaStream_t);
+                                        cudaStream_t, const int*);
 template cudaError_t tsqr_form_q<double>(const TsqrPlan&, const double*, double*, double*, double*, double*, double*,
-                                         int64_t, int, cudaStream_t);
+                                         int64_t, int, cudaStream_t, const int*);
 template cudaError_t tsqr_form_q<float>(const TsqrPlan&, const float*, float*, float*, float*, float*, float*, int64_t,
-                                        int, cudaStream_t);
+                                        int, cudaStream_t, const int*);
 
 }  // namespace coru_gpu

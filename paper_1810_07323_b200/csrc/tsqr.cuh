@@ -38,15 +38,17 @@ TsqrPlan plan_tsqr(int64_t m, int d, size_t elem_bytes, int max_smem_bytes);
 // Factor B (m x d, row-major, ldb) through the tree. R (d x d, row-major, upper, exact zeros
 // below) is written to r_out (ld = d) — on device.
 template <typename T>
+// gate (device int, may be null): when it reads 0 the kernels return at once (CholeskyQR2 already
+// produced this QR, cholqr.cu).
 cudaError_t tsqr_factor(const TsqrPlan& p, const T* B, int64_t ldb, T* v_arena, T* beta_arena, T* t_arena,
-                        T* r_arena, T* r_out, cudaStream_t st);
+                        T* r_arena, T* r_out, cudaStream_t st, const int* gate = nullptr);
 
 // Form the explicit Q (m x d, row-major, ldq) from a factored tree. If q_top is non-null it is the
 // d x d (row-major, ld = d) block that multiplies the tree's top-level Q from the right — used for
 // the cross-rank top level (Q_g = Q_local_tree · Q_global[g*d:(g+1)*d, :]); null means identity.
 template <typename T>
 cudaError_t tsqr_form_q(const TsqrPlan& p, const T* q_top, T* v_arena, T* beta_arena, T* t_arena, T* scratch, T* Q,
-                        int64_t ldq, int max_smem, cudaStream_t st);
+                        int64_t ldq, int max_smem, cudaStream_t st, const int* gate = nullptr);
 
 // scratch of tsqr_form_q: working blocks (wide path), T-product buffers and two level buffers.
 int64_t tsqr_scratch_elems(const TsqrPlan& p);

@@ -97,6 +97,33 @@ def test_qrcp_known_answers(ctx):
     assert np.allclose(np.abs(np.diag(r)), [5, 3, 1], rtol=1e-14)
 
 
+@pytest.mark.parametrize("m,d,cond,wide", [(5000, 220, 1e2, True), (5000, 220, 1e2, False), (20000, 520, 50.0, True),
+                                          (3000, 130, 1e3, True), (4000, 220, 1e12, True), (1500, 300, 1e9, True)])
+def test_wide_qr_cholqr2_and_fallback(m, d, cond, wide, oracle):
+    """Wide sketches (d > 128): CholeskyQR2 in fp64 (cholqr.cu) when well-conditioned, the gated
+    Householder tree otherwise (cond 1e9 and 1e12 exceed the 1e6 switch): Q R = B to 1e-12,
+    orthonormality 1e-12·d, positive diagonal, R equal to the reference Householder R."""
+    import paper_1810_07323_b200 as cg
+    ctx = cg.Context(0)
+    ctx.set_wide_qr(wide)
+    rng = np.random.default_rng(m + d)
+    x, _ = np.linalg.qr(rng.standard_normal((m, d)))
+    y, _ = np.linalg.qr(rng.standard_normal((d, d)))
+    b = (x * np.logspace(0, -np.log10(cond), d)) @ y.T
+    q, r = cg.tsqr(_t(b), ctx=ctx)
+    q, r = q.cpu().numpy(), r.cpu().numpy()
+    assert np.all(np.diag(r) > 0)
+    assert np.all(np.tril(r, -1) == 0.0)
+    assert np.linalg.norm(q @ r - b) <= 1e-12 * np.linalg.norm(b)
+    assert orth_residual(q) <= 1e-12 * d
+    if cond <= 1e3:
+        # unique QR: agrees with the reference Householder factors to rounding (x cond)
+        ro = oracle.householder_qr(b)[1] if m * d <= 5000 * 300 else None
+        if ro is not None:
+            assert np.linalg.norm(r - ro) <= 1e-12 * cond * np.linalg.norm(ro)
+    ctx.close()
+
+
 @pytest.mark.parametrize("n,seed", [(25, 1), (60, 2), (110, 3), (220, 4), (7, 5), (1, 6), (160, 7)])
 def test_qrcp_matches_oracle(ctx, oracle, n, seed):
     import paper_1810_07323_b200 as cg
