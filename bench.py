@@ -187,15 +187,15 @@ def ncu_traffic(config_name):
 
 
 # ---- CPU baselines ----------------------------------------------------------------------------------
-def cpu_baseline_sample(cfg, a_host):
+def cpu_baseline_sample(cfg, a_host, variant=0):
     """The compiled reference (oracle/_ref) on ONE host core: bounded sample of whole decompositions."""
     from oracle import Reference, has_reference, Oracle
     if has_reference():
         ref, kind = Reference(), "reference"
-        run = lambda s: ref.corutv(a_host, cfg.d, cfg.q, 0, 42, s)  # noqa: E731
+        run = lambda s: ref.corutv(a_host, cfg.d, cfg.q, variant, 42, s)  # noqa: E731
     else:
         ora, kind = Oracle(), "port"
-        run = lambda s: ora.corutv(a_host, cfg.d, cfg.q, 0, 42, s, threads=1)  # noqa: E731
+        run = lambda s: ora.corutv(a_host, cfg.d, cfg.q, variant, 42, s, threads=1)  # noqa: E731
     times = []
     budget = 12.0
     t_all = time.perf_counter()
@@ -254,6 +254,7 @@ def run_reference_arm(args, cfg):
 def config_block(cfg, args, l2):
     return {"workload": f"{cfg.name}: {cfg.dtype} {cfg.m}x{cfg.n}, {cfg.desc}, d={cfg.d}, q={cfg.q}, k={cfg.k}",
             "m": cfg.m, "n": cfg.n, "d": cfg.d, "q": cfg.q, "k": cfg.k, "seed": "RngSeed{42, step}",
+            "variant": args.variant, "passes_over_A": 2 * cfg.q + (3 if args.variant == "exact" else 2),
             "parallelism": f"row-sharded x{args.gpus}" if args.gpus > 1 else "single GPU", "l2": l2}
 
 
@@ -296,7 +297,8 @@ def run_ours(args, cfg):
     import ctypes as C
 
     def step(s):
-        cg._check(fn(ctx.h, a.data_ptr(), m_local, cfg.m, n, a.stride(0), d, cfg.q, 0, 42, s, C.byref(out)))
+        cg._check(fn(ctx.h, a.data_ptr(), m_local, cfg.m, n, a.stride(0), d, cfg.q, args.variant_id, 42, s,
+                      C.byref(out)))
 
     def barrier():
         if world > 1:
@@ -368,7 +370,7 @@ def run_ours(args, cfg):
 
     cpu = None
     if world == 1 and rank == 0 and not args.no_cpu_baseline:
-        cpu = cpu_baseline_sample(cfg, make_host(cfg.name))
+        cpu = cpu_baseline_sample(cfg, make_host(cfg.name), args.variant_id)
 
     if rank == 0:
         line = {
@@ -406,8 +408,9 @@ def run_e2e(args, cfg, ctx, a, world, rank, local, dev, barrier):
         fn = getattr(lib, f"coru_corutv_{sfx}")
 
         def step(s):
-            cg._check(fn(ctx.h, a_host.data_ptr(), cfg.m, n, d, cfg.q, 0, 42, 500_000 + s, u_h.data_ptr(),
-                         t_h.data_ptr(), v_h.data_ptr(), perm.ctypes.data, C.byref(lower), C.byref(warn)))
+            cg._check(fn(ctx.h, a_host.data_ptr(), cfg.m, n, d, cfg.q, args.variant_id, 42, 500_000 + s,
+                         u_h.data_ptr(), t_h.data_ptr(), v_h.data_ptr(), perm.ctypes.data, C.byref(lower),
+                         C.byref(warn)))
     else:
         a_dev = torch.empty_like(a)
         u = torch.empty((m_local, d), dtype=dt, device=dev)
@@ -421,8 +424,8 @@ def run_e2e(args, cfg, ctx, a, world, rank, local, dev, barrier):
         def step(s):
             with torch.cuda.stream(s_):
                 a_dev.copy_(a_host, non_blocking=True)
-            cg._check(fn(ctx.h, a_dev.data_ptr(), m_local, cfg.m, n, a_dev.stride(0), d, cfg.q, 0, 42, 500_000 + s,
-                         C.byref(out)))
+            cg._check(fn(ctx.h, a_dev.data_ptr(), m_local, cfg.m, n, a_dev.stride(0), d, cfg.q, args.variant_id, 42,
+                         500_000 + s, C.byref(out)))
             with torch.cuda.stream(s_):
                 u_h.copy_(u, non_blocking=True)
                 t_h.copy_(t, non_blocking=True)
@@ -459,7 +462,10 @@ def main():
     ap.add_argument("--config", default="C2q1", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--variant", default="exact", choices=["exact", "approx"],
+                    help="DVariant (corutv.hpp:17); the BASELINE metric is quoted on exact")
     args = ap.parse_args()
+    args.variant_id = 0 if args.variant == "exact" else 1
     cfg = CONFIGS[args.config]
     if args.impl == "reference":
         return run_reference_arm(args, cfg)

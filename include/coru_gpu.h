@@ -46,7 +46,8 @@ enum coru_status {
     CORU_ENOTSUP = 5  /* valid in the reference, not provided by this build */
 };
 
-/* DVariant (corutv.hpp:17). Only CORU_D_EXACT is in the hot-path scope. */
+/* DVariant (corutv.hpp:17): exact = D from one more pass over A (corutv.hpp:90); approx = D from the
+ * sketches, (Q1^T C1)·pinv(Q2^T C2prev) (corutv.hpp:91-92), with the pinv computed in fp64. */
 enum coru_variant { CORU_D_EXACT = 0, CORU_D_APPROX = 1 };
 
 /* Opaque per-device context: stream, workspace arena, pinned staging, optional communicator.
@@ -163,6 +164,11 @@ int coru_tsqr_f64_dev(coru_ctx* ctx, const double* B, int64_t ldb, int64_t m, in
 /* qrcp (qr.hpp:106-143) of a square n x n matrix: Q, R (n x n), perm (host, n). Device. */
 int coru_qrcp_f64_dev(coru_ctx* ctx, const double* M, int64_t ldm, int64_t n, double* Q, int64_t ldq, double* R,
                       int64_t ldr, int64_t* perm);
+
+/* pinv (svd.hpp:167-187) of a square n x n matrix via the one-sided Jacobi SVD (svd.hpp:31-134), the
+ * core of DVariant::approx (corutv.hpp:91-92). Device Y, P (row-major); *converged (host, may be
+ * NULL) = the number of Jacobi sweeps used, 0 when the 60-sweep cap was hit. */
+int coru_pinv_f64_dev(coru_ctx* ctx, const double* Y, int64_t ldy, int64_t n, double* P, int64_t ldp, int* converged);
 
 /* A-pass profiling: when enabled, CUDA events are recorded on the launching stream around every
  * GEMM that streams the caller's A (the sketch, power and projection passes). The read call

@@ -63,6 +63,9 @@ class Oracle:
         L.oracle_gaussian.argtypes = [_i64, _i64, _u64, _u64, _p]
         L.oracle_xoshiro_words.argtypes = [_u64, _u64, _i64, _p]
         L.oracle_max_threads.restype = _int
+        L.oracle_pinv_f64.argtypes = [_p, _i64, _p]
+        L.oracle_jacobi_svd_square.argtypes = [_p, _i64, _p, _p, _p]
+        L.oracle_jacobi_svd_square.restype = _int
         for sfx in ("f64", "f32"):
             getattr(L, f"oracle_matmul_{sfx}").argtypes = [_p, _i64, _i64, _p, _i64, _p, _int]
             getattr(L, f"oracle_matmul_tn_{sfx}").argtypes = [_p, _i64, _i64, _p, _i64, _p, _int]
@@ -119,6 +122,22 @@ class Oracle:
             raise CoruError("qrcp: requires rows >= cols")
         return q, r, perm
 
+    def pinv(self, a):
+        """pinv of a square matrix (svd.hpp:167-187), fp64 Jacobi SVD."""
+        a = np.ascontiguousarray(a, np.float64); n = a.shape[0]
+        assert a.shape == (n, n)
+        out = np.empty((n, n))
+        self.lib.oracle_pinv_f64(_ptr(a), n, _ptr(out))
+        return out
+
+    def jacobi_svd_square(self, a):
+        """detail::jacobi_svd_square (svd.hpp:31-134) on a square a: (u, sigma, v, converged)."""
+        a = np.ascontiguousarray(a, np.float64); n = a.shape[0]
+        acm = np.ascontiguousarray(a.T)
+        u = np.empty((n, n)); v = np.empty((n, n)); s = np.empty(n)
+        conv = self.lib.oracle_jacobi_svd_square(_ptr(acm), n, _ptr(u), _ptr(s), _ptr(v))
+        return u, s, v, bool(conv)
+
     def sketch_bases(self, a, ell, q, seed, stream=0, threads=1):
         a = np.ascontiguousarray(a); m, n = a.shape; dt = a.dtype
         q1 = np.empty((m, ell), dt); q2 = np.empty((n, ell), dt)
@@ -139,8 +158,6 @@ class Oracle:
             _ptr(a), m, n, ell, q, variant, seed, stream, threads, _ptr(u), _ptr(t), _ptr(v), _ptr(flags), _ptr(perm))
         if rc == 1:
             raise CoruError("corutv: bad parameters")
-        if rc == 3:
-            raise NotImplementedError("DVariant::approx is outside the hot-path scope")
         return Utv(u, t, v, bool(flags[0]), bool(flags[1]), perm)
 
 
@@ -157,6 +174,8 @@ class Reference:
         L.ref_matmul.argtypes = [_p, _i64, _i64, _p, _i64, _p]
         L.ref_householder_qr.argtypes = [_p, _i64, _i64, _p, _p]
         L.ref_qrcp.argtypes = [_p, _i64, _i64, _p, _p, _p]
+        L.ref_svd.argtypes = [_p, _i64, _i64, _p, _p, _p, _p]
+        L.ref_pinv.argtypes = [_p, _i64, _i64, _p]
         L.ref_corutv.argtypes = [_p, _i64, _i64, _i64, _int, _int, _u64, _u64, _p, _p, _p, _p]
         L.ref_corutv_mt.argtypes = [_p, _i64, _i64, _i64, _int, _u64, _u64, _int, _p, _p, _p, _p]
         L.ref_sketch_bases.argtypes = [_p, _i64, _i64, _i64, _int, _u64, _u64, _p, _p, _p, _p, _p]
@@ -188,6 +207,18 @@ class Reference:
         c = np.empty((a.shape[0], b.shape[1]))
         self._check(self.lib.ref_matmul(_ptr(a), a.shape[0], a.shape[1], _ptr(b), b.shape[1], _ptr(c)))
         return c
+
+    def svd(self, a):
+        a = np.ascontiguousarray(a, np.float64); m, n = a.shape; r = min(m, n)
+        u = np.empty((m, r)); s = np.empty(r); v = np.empty((n, r)); conv = np.zeros(1, np.int32)
+        self._check(self.lib.ref_svd(_ptr(a), m, n, _ptr(u), _ptr(s), _ptr(v), _ptr(conv)))
+        return u, s, v, bool(conv[0])
+
+    def pinv(self, a):
+        a = np.ascontiguousarray(a, np.float64); m, n = a.shape
+        out = np.empty((n, m))
+        self._check(self.lib.ref_pinv(_ptr(a), m, n, _ptr(out)))
+        return out
 
     def householder_qr(self, a):
         a = np.ascontiguousarray(a, np.float64); m, n = a.shape

@@ -88,6 +88,138 @@ void oracle_gaussian(int64_t rows, int64_t cols, uint64_t seed, uint64_t stream,
     }
 }
 
+/* ---- SVD / pseudo-inverse of a square matrix (svd.hpp), fp64 ---------------------------- */
+
+/* detail::jacobi_svd_square (svd.hpp:31-134). `a` (n×n) is COLUMN-major and is overwritten
+ * with the rotated columns. Outputs: u, v row-major n×n, sigma[n] non-increasing.
+ * One-sided cyclic Jacobi by (j,k) row order; a pair rotates when
+ * |c_j·c_k| > 1e-14·sqrt(sq_j·sq_k) (:51-57); converged after a sweep with no rotation, capped at
+ * 60 sweeps (:44); columns stable-sorted by descending squared norm (:79-82); zero-sigma u
+ * columns completed from the canonical basis (:98-121). Returns 1 if converged. */
+int oracle_jacobi_svd_square(double* a, int64_t n, double* u, double* sigma, double* v) {
+    const double kTol = 1e-14;
+    const int kMaxSweeps = 60;
+    double* vw = (double*)calloc((size_t)(n * n), sizeof(double));
+    double* sq = (double*)malloc(sizeof(double) * (size_t)n);
+    for (int64_t j = 0; j < n; ++j) vw[j * n + j] = 1.0;
+    for (int64_t j = 0; j < n; ++j) {
+        double s = 0.0;
+        const double* c = a + j * n;
+        for (int64_t i = 0; i < n; ++i) s += c[i] * c[i];
+        sq[j] = s;
+    }
+    int converged = 0;
+    for (int sweep = 0; sweep < kMaxSweeps && !converged; ++sweep) {
+        int rotated = 0;
+        for (int64_t j = 0; j + 1 < n; ++j) {
+            for (int64_t k = j + 1; k < n; ++k) {
+                double* cj = a + j * n;
+                double* ck = a + k * n;
+                if (sq[j] == 0.0 || sq[k] == 0.0) continue;
+                double gamma = 0.0;
+                for (int64_t i = 0; i < n; ++i) gamma += cj[i] * ck[i];
+                if (fabs(gamma) <= kTol * sqrt(sq[j] * sq[k])) continue;
+                const double zeta = (sq[k] - sq[j]) / (2.0 * gamma);
+                if (!isfinite(zeta)) continue;
+                const double t = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
+                const double c = 1.0 / sqrt(1.0 + t * t);
+                const double s = c * t;
+                double* vj = vw + j * n;
+                double* vk = vw + k * n;
+                for (int64_t i = 0; i < n; ++i) {
+                    const double x = cj[i], y = ck[i];
+                    cj[i] = c * x - s * y;
+                    ck[i] = s * x + c * y;
+                }
+                for (int64_t i = 0; i < n; ++i) {
+                    const double x = vj[i], y = vk[i];
+                    vj[i] = c * x - s * y;
+                    vk[i] = s * x + c * y;
+                }
+                double sj = 0.0, sk = 0.0;
+                for (int64_t i = 0; i < n; ++i) {
+                    sj += cj[i] * cj[i];
+                    sk += ck[i] * ck[i];
+                }
+                sq[j] = sj;
+                sq[k] = sk;
+                rotated = 1;
+            }
+        }
+        if (!rotated) converged = 1;
+    }
+    /* stable sort by descending sq (insertion sort keeps equal keys in index order) */
+    int64_t* order = (int64_t*)malloc(sizeof(int64_t) * (size_t)n);
+    for (int64_t j = 0; j < n; ++j) {
+        int64_t p = j;
+        while (p > 0 && sq[order[p - 1]] < sq[j]) {
+            order[p] = order[p - 1];
+            --p;
+        }
+        order[p] = j;
+    }
+    memset(u, 0, sizeof(double) * (size_t)(n * n));
+    for (int64_t j = 0; j < n; ++j) {
+        const int64_t src = order[j];
+        const double sg = sqrt(sq[src]);
+        sigma[j] = sg;
+        for (int64_t i = 0; i < n; ++i) v[i * n + j] = vw[src * n + i];
+        if (sg > 0.0)
+            for (int64_t i = 0; i < n; ++i) u[i * n + j] = a[src * n + i] / sg;
+    }
+    /* zero-sigma completion (svd.hpp:98-121) */
+    double* cand = (double*)malloc(sizeof(double) * (size_t)n);
+    double* best = (double*)malloc(sizeof(double) * (size_t)n);
+    for (int64_t j = 0; j < n; ++j) {
+        if (sigma[j] > 0.0) continue;
+        double best_res = -1.0;
+        for (int64_t e = 0; e < n; ++e) {
+            memset(cand, 0, sizeof(double) * (size_t)n);
+            cand[e] = 1.0;
+            for (int pass = 0; pass < 2; ++pass)
+                for (int64_t c = 0; c < j; ++c) {
+                    double dot = 0.0;
+                    for (int64_t i = 0; i < n; ++i) dot += cand[i] * u[i * n + c];
+                    for (int64_t i = 0; i < n; ++i) cand[i] -= dot * u[i * n + c];
+                }
+            double res = 0.0;
+            for (int64_t i = 0; i < n; ++i) res += cand[i] * cand[i];
+            if (res > best_res) {
+                best_res = res;
+                memcpy(best, cand, sizeof(double) * (size_t)n);
+            }
+        }
+        const double nrm = sqrt(best_res);
+        for (int64_t i = 0; i < n; ++i) u[i * n + j] = best[i] / nrm;
+    }
+    free(cand); free(best); free(order); free(vw); free(sq);
+    return converged;
+}
+
+/* pinv(a) (svd.hpp:167-187) for a square n×n row-major a: svd (the square branch, :150-155),
+ * singular values <= n·eps·sigma_1 dropped, then matmul(v·diag(1/sigma), u^T) in i-k-j order. */
+void oracle_pinv_f64(const double* a, int64_t n, double* out) {
+    double* acm = (double*)malloc(sizeof(double) * (size_t)(n * n));
+    double* u = (double*)malloc(sizeof(double) * (size_t)(n * n));
+    double* v = (double*)malloc(sizeof(double) * (size_t)(n * n));
+    double* sg = (double*)malloc(sizeof(double) * (size_t)n);
+    for (int64_t i = 0; i < n; ++i)
+        for (int64_t j = 0; j < n; ++j) acm[j * n + i] = a[i * n + j];
+    oracle_jacobi_svd_square(acm, n, u, sg, v);
+    const double cut = (double)n * 2.220446049250313080847e-16 * sg[0];
+    for (int64_t j = 0; j < n; ++j) {
+        const double inv = sg[j] > cut ? 1.0 / sg[j] : 0.0;
+        for (int64_t i = 0; i < n; ++i) v[i * n + j] *= inv; /* vs(i,j) = v(i,j)·inv */
+    }
+    memset(out, 0, sizeof(double) * (size_t)(n * n));
+    for (int64_t i = 0; i < n; ++i)
+        for (int64_t k = 0; k < n; ++k) {
+            const double vik = v[i * n + k];
+            for (int64_t j = 0; j < n; ++j) out[i * n + j] += vik * u[j * n + k]; /* u^T(k,j) */
+        }
+    free(acm); free(u); free(v); free(sg);
+}
+
 /* ---- type-generic linear algebra ---------------------------------------------------- */
 
 #define T double

@@ -194,15 +194,17 @@ int FN(oracle_sketch_bases_)(const T* a, int64_t m, int64_t n, int64_t ell, int 
     return 0;
 }
 
-/* corutv, exact-D variant (corutv.hpp:79-100). u m×ell, t ell×ell, v n×ell;
- * flags[0] = lower, flags[1] = conditioning_warning, perm_out (optional) = QRCP pivots.
- * Returns 1 for the reference's std::invalid_argument cases, 3 for DVariant::approx
- * (its pinv/Jacobi-SVD core is outside the hot-path scope). */
+/* corutv (corutv.hpp:79-100), variant 0 = DVariant::exact, 1 = DVariant::approx.
+ * u m×ell, t ell×ell, v n×ell; flags[0] = lower, flags[1] = conditioning_warning, perm_out
+ * (optional) = QRCP pivots. Returns 1 for the reference's std::invalid_argument cases.
+ * approx (corutv.hpp:91-92): d = (q1^T·c1)·pinv(q2^T·c2_prev); the pinv (Jacobi SVD, svd.hpp)
+ * runs in fp64 for both instantiations (the reference's tolerances are fp64 constants) and is
+ * rounded to T; the two products around it run in T. */
 int FN(oracle_corutv_)(const T* a, int64_t m, int64_t n, int64_t ell, int q, int variant,
                        uint64_t seed, uint64_t stream, int threads, T* u, T* t, T* v, int* flags,
                        int64_t* perm_out) {
     if (ell < 1 || ell >= (m < n ? m : n) || q < 0) return 1;
-    if (variant != 0) return 3;
+    if (variant != 0 && variant != 1) return 1;
     if (m < n) {
         /* corutv(a^T) and swap (corutv.hpp:82-87) */
         T* at = (T*)malloc(sizeof(T) * (size_t)(m * n));
@@ -219,21 +221,39 @@ int FN(oracle_corutv_)(const T* a, int64_t m, int64_t n, int64_t ell, int q, int
     T* q1 = (T*)malloc(sizeof(T) * (size_t)(m * ell));
     T* q2 = (T*)malloc(sizeof(T) * (size_t)(n * ell));
     int warn = 0;
-    FN(oracle_sketch_bases_)(a, m, n, ell, q, seed, stream, threads, q1, q2, NULL, NULL, &warn);
-    /* d = (q1^T·a)·q2 (corutv.hpp:90): q1^T·a is the tn product of (a-as-m×n, q1). Its row l
-     * accumulates q1(i,l)·a(i,.) over i increasing — matmul(q1.transposed(), a)'s order. */
-    T* q1ta = (T*)calloc((size_t)(ell * n), sizeof(T));
-#pragma omp parallel for schedule(static) num_threads(threads) if (threads > 1)
-    for (int64_t l = 0; l < ell; ++l) {
-        T* row = q1ta + l * n;
-        for (int64_t i = 0; i < m; ++i) {
-            const T w = q1[i * ell + l];
-            const T* ai = a + i * n;
-            for (int64_t j = 0; j < n; ++j) row[j] += w * ai[j];
-        }
-    }
     T* d = (T*)malloc(sizeof(T) * (size_t)(ell * ell));
-    FN(mm_)(q1ta, ell, n, q2, ell, d, 1);
+    T* q1ta = NULL;
+    if (variant == 1) {
+        T* c1 = (T*)malloc(sizeof(T) * (size_t)(m * ell));
+        T* c2p = (T*)malloc(sizeof(T) * (size_t)(n * ell));
+        FN(oracle_sketch_bases_)(a, m, n, ell, q, seed, stream, threads, q1, q2, c1, c2p, &warn);
+        T* y1 = (T*)malloc(sizeof(T) * (size_t)(ell * ell));
+        T* y2 = (T*)malloc(sizeof(T) * (size_t)(ell * ell));
+        FN(mm_tn_)(q1, m, ell, c1, ell, y1, threads);  /* q1^T·c1: matmul(q1.transposed(), c1) */
+        FN(mm_tn_)(q2, n, ell, c2p, ell, y2, threads); /* q2^T·c2_prev */
+        double* yd = (double*)malloc(sizeof(double) * (size_t)(ell * ell));
+        double* pd = (double*)malloc(sizeof(double) * (size_t)(ell * ell));
+        for (int64_t i = 0; i < ell * ell; ++i) yd[i] = (double)y2[i];
+        oracle_pinv_f64(yd, ell, pd);
+        for (int64_t i = 0; i < ell * ell; ++i) y2[i] = (T)pd[i];
+        FN(mm_)(y1, ell, ell, y2, ell, d, 1);          /* (q1^T c1)·pinv(q2^T c2_prev) */
+        free(c1); free(c2p); free(y1); free(y2); free(yd); free(pd);
+    } else {
+        FN(oracle_sketch_bases_)(a, m, n, ell, q, seed, stream, threads, q1, q2, NULL, NULL, &warn);
+        /* d = (q1^T·a)·q2 (corutv.hpp:90): q1^T·a is the tn product of (a-as-m×n, q1). Its row l
+         * accumulates q1(i,l)·a(i,.) over i increasing — matmul(q1.transposed(), a)'s order. */
+        q1ta = (T*)calloc((size_t)(ell * n), sizeof(T));
+#pragma omp parallel for schedule(static) num_threads(threads) if (threads > 1)
+        for (int64_t l = 0; l < ell; ++l) {
+            T* row = q1ta + l * n;
+            for (int64_t i = 0; i < m; ++i) {
+                const T w = q1[i * ell + l];
+                const T* ai = a + i * n;
+                for (int64_t j = 0; j < n; ++j) row[j] += w * ai[j];
+            }
+        }
+        FN(mm_)(q1ta, ell, n, q2, ell, d, 1);
+    }
     T* qm = (T*)malloc(sizeof(T) * (size_t)(ell * ell));
     int64_t* perm = (int64_t*)malloc(sizeof(int64_t) * (size_t)ell);
     FN(oracle_qrcp_)(d, ell, ell, qm, t, perm);          /* corutv.hpp:93 */

@@ -131,6 +131,22 @@ int ref_qrcp(const double* a, int64_t m, int64_t n, double* q, double* r, int64_
     });
 }
 
+// coru::svd (svd.hpp:141-161): u m×r, sigma[r], v n×r with r = min(m, n); returns converged in *conv.
+int ref_svd(const double* a, int64_t m, int64_t n, double* u, double* sigma, double* v, int* conv) {
+    return guarded([&] {
+        coru::SvdFactors f = coru::svd(wrap(a, m, n));
+        put(f.u, u);
+        put(f.v, v);
+        for (size_t j = 0; j < f.sigma.size(); ++j) sigma[j] = f.sigma[j];
+        *conv = f.converged ? 1 : 0;
+    });
+}
+
+// coru::pinv(a) (svd.hpp:184-187): n×m.
+int ref_pinv(const double* a, int64_t m, int64_t n, double* out) {
+    return guarded([&] { put(coru::pinv(wrap(a, m, n)), out); });
+}
+
 // coru::corutv (corutv.hpp:79-100). u rows(a)×ell, t ell×ell, v cols(a)×ell.
 // flags[0] = lower, flags[1] = conditioning_warning.
 int ref_corutv(const double* a, int64_t m, int64_t n, int64_t ell, int q, int variant,

@@ -165,6 +165,7 @@ def load_library():
     L.coru_gemm_f32_dev.argtypes = [p, i32, p, i64, p, i64, p, i64, i64, i64, i64]
     L.coru_tsqr_f64_dev.argtypes = [p, p, i64, i64, i64, p, i64, p, i64]
     L.coru_qrcp_f64_dev.argtypes = [p, p, i64, i64, p, i64, p, i64, p]
+    L.coru_pinv_f64_dev.argtypes = [p, p, i64, i64, p, i64, C.POINTER(i32)]
     _lib = L
     return L
 
@@ -499,3 +500,17 @@ def qrcp(mat, ctx: Optional[Context] = None):
     _check(ctx.lib.coru_qrcp_f64_dev(ctx.h, mat.data_ptr(), mat.stride(0), n, q.data_ptr(), n, r.data_ptr(), n,
                                      perm.ctypes.data))
     return q, r, perm
+
+
+def pinv(mat, ctx: Optional[Context] = None):
+    """pinv (svd.hpp:167-187) of a square CUDA fp64 tensor -> (p, sweeps); sweeps = Jacobi sweeps
+    used, 0 when the 60-sweep cap was hit (SvdFactors::converged == false)."""
+    import torch
+    ctx = ctx or default_context(mat.device.index or 0)
+    n = mat.shape[0]
+    assert mat.shape == (n, n) and mat.dtype == torch.float64 and mat.is_cuda
+    out = torch.empty((n, n), dtype=torch.float64, device=mat.device)
+    conv = C.c_int(0)
+    _torch_sync_stream(ctx, mat)
+    _check(ctx.lib.coru_pinv_f64_dev(ctx.h, mat.data_ptr(), mat.stride(0), n, out.data_ptr(), n, C.byref(conv)))
+    return out, int(conv.value)

@@ -29,6 +29,7 @@
 #include "qrcp.cuh"
 #include "cholqr.cuh"
 #include "rng_dev.cuh"
+#include "svd.cuh"
 #include "tsqr.cuh"
 
 namespace coru_gpu {
@@ -370,6 +371,7 @@ struct Request {
     int q = 0;
     uint64_t seed = 0, stream = 0;
     Mode mode = Mode::Full;
+    int variant = CORU_D_EXACT;  // Full: how D is formed (corutv.hpp:89-92)
     // Full: U' (rows x d), T' (d x d), V' (cols x d) — device, caller's buffers.
     T* u = nullptr;
     int64_t ldu = 0;
@@ -394,6 +396,8 @@ struct Work {
     TsqrBufs<T> ts1, ts2, tstop;
     T *rstack = nullptr, *qtop = nullptr, *r1loc = nullptr, *r1 = nullptr, *r2 = nullptr;
     T *m = nullptr, *qm = nullptr, *tm = nullptr, *qrcp_scr = nullptr;
+    T *y1 = nullptr, *y2 = nullptr, *pinv = nullptr;  // approx-D core
+    double* pws = nullptr;
     int64_t* perm = nullptr;
     int* flag = nullptr;
 
@@ -401,12 +405,14 @@ struct Work {
         const int64_t R = r.rows, N = r.cols;
         const int d = r.d, sms = c->num_sms;
         b2 = cv.take<T>(N * dp);
-        b2prev = r.c2p ? cv.take<T>(N * dp) : nullptr;
+        const bool approx = r.mode == Mode::Full && r.variant == CORU_D_APPROX;
+        b2prev = (r.c2p || approx) ? cv.take<T>(N * dp) : nullptr;
         b1 = cv.take<T>(R * dp);
         q1 = cv.take<T>(R * dp);
         q2 = cv.take<T>(N * dp);
         gws_elems = std::max({gemm_ws<T>(r.op_a(), R, N, d, sms), gemm_ws<T>(r.op_at(), N, R, d, sms),
-                              gemm_ws<T>(Op::T, d, R, d, sms), gemm_ws<T>(Op::N, R, d, d, sms)});
+                              gemm_ws<T>(Op::T, d, R, d, sms), gemm_ws<T>(Op::N, R, d, d, sms),
+                              gemm_ws<T>(Op::T, d, N, d, sms), gemm_ws<T>(Op::N, d, d, d, sms)});
         gws = cv.take<T>(gws_elems);
         // CholeskyQR2 for wide sketches, except for Q1 when sharded (its tree's top level is cross-rank)
         ts1.carve(cv, R, d, c->max_smem, sms, c->world == 1 && c->wide_qr);
@@ -423,6 +429,12 @@ struct Work {
         qm = cv.take<T>(int64_t(dp) * dp);
         tm = cv.take<T>(int64_t(d) * d);
         qrcp_scr = cv.take<T>(qrcp_scratch_elems(d));
+        if (approx) {
+            y1 = cv.take<T>(int64_t(d) * dp);
+            y2 = cv.take<T>(int64_t(d) * dp);
+            pinv = cv.take<T>(int64_t(d) * dp);
+            pws = cv.take<double>(pinv_ws_doubles(d));
+        }
         perm = cv.take<int64_t>(d);
         flag = cv.take<int>(4);
     }
@@ -599,17 +611,33 @@ int run_impl(coru_ctx* c, const Request<T>& r, size_t extra_arena_off) {
         return CORU_OK;
     }
 
-    // D = (Q1^T a) q2 (corutv.hpp:90) as Q1^T (A'·Q2): W = A'·Q2 reuses the B1 buffer.
-    T* W = w.b1;
-    CORU_TRY(gemm<T>(c, r.op_a(), r.A, r.lda, w.q2, dp, W, dp, R, N, d, w.gws, w.gws_elems));
-    {
+    if (r.variant == CORU_D_APPROX) {
+        // D = (Q1^T c1)·pinv(Q2^T c2_prev) (corutv.hpp:91-92): no further pass over A. Q1^T c1 is
+        // summed over ranks; Q2, c2_prev and so the pinv are replicated (identical bytes).
+        const bool p = c->prof;
+        c->prof = false;
+        int rc = gemm<T>(c, Op::T, w.q1, dp, w.b1, dp, w.y1, dp, d, R, d, w.gws, w.gws_elems);
+        if (rc == CORU_OK) rc = allreduce<T>(c, w.y1, size_t(d) * dp);
+        if (rc == CORU_OK) rc = gemm<T>(c, Op::T, w.q2, dp, w.b2prev, dp, w.y2, dp, d, N, d, w.gws, w.gws_elems);
+        if (rc == CORU_OK) {
+            const cudaError_t e = pinv_square<T>(w.y2, dp, d, w.pinv, dp, w.pws, nullptr, c->max_smem, st);
+            if (e != cudaSuccess) rc = fail(CORU_ECUDA, std::string("pinv_square: ") + cudaGetErrorString(e));
+            g_launches += kPinvLaunches;
+        }
+        if (rc == CORU_OK) rc = gemm<T>(c, Op::N, w.y1, dp, w.pinv, dp, w.m, dp, d, d, d, w.gws, w.gws_elems);
+        c->prof = p;
+        CORU_TRY(rc);
+    } else {
+        // D = (Q1^T a) q2 (corutv.hpp:90) as Q1^T (A'·Q2): W = A'·Q2 reuses the B1 buffer.
+        T* W = w.b1;
+        CORU_TRY(gemm<T>(c, r.op_a(), r.A, r.lda, w.q2, dp, W, dp, R, N, d, w.gws, w.gws_elems));
         const bool p = c->prof;  // Q1^T·W is m x d x d, not an A-pass
         c->prof = false;
         const int rc = gemm<T>(c, Op::T, w.q1, dp, W, dp, w.m, dp, d, R, d, w.gws, w.gws_elems);
         c->prof = p;
         CORU_TRY(rc);
+        CORU_TRY(allreduce<T>(c, w.m, size_t(d) * dp));
     }
-    CORU_TRY(allreduce<T>(c, w.m, size_t(d) * dp));
 
     // QRCP of the core (corutv.hpp:93), then the lift (corutv.hpp:94-97).
     CORU_CUDA(cudaMemsetAsync(w.qm, 0, size_t(dp) * dp * sizeof(T), st));
@@ -646,8 +674,7 @@ template <typename T>
 int corutv_dev(coru_ctx* c, const T* A, int64_t m_local, int64_t m, int64_t n, int64_t lda, int64_t ell, int q,
                int variant, uint64_t seed, uint64_t stream, coru_utv* out) {
     CORU_TRY(check_params(m, n, ell, q));
-    if (variant != CORU_D_EXACT)
-        return fail(CORU_ENOTSUP, "DVariant::approx (pinv core, corutv.hpp:91-92) is outside this build's scope");
+    if (variant != CORU_D_EXACT && variant != CORU_D_APPROX) return fail(CORU_EINVAL, "corutv: unknown DVariant");
     if (!out || !A) return fail(CORU_EINVAL, "null argument");
     if (c->world <= 1 && m_local != m) return fail(CORU_EINVAL, "m_local != m without a communicator");
     if (lda < n) return fail(CORU_EINVAL, "lda < n");
@@ -658,6 +685,7 @@ int corutv_dev(coru_ctx* c, const T* A, int64_t m_local, int64_t m, int64_t n, i
     r.q = q;
     r.seed = seed;
     r.stream = stream;
+    r.variant = variant;
     r.perm_host = out->perm;
     r.warn_host = &out->conditioning_warning;
     if (m < n) {
@@ -693,8 +721,7 @@ template <typename T>
 int corutv_host(coru_ctx* c, const T* A, int64_t m, int64_t n, int64_t ell, int q, int variant, uint64_t seed,
                 uint64_t stream, T* U, T* Tt, T* V, int64_t* perm, int* lower, int* warn) {
     CORU_TRY(check_params(m, n, ell, q));
-    if (variant != CORU_D_EXACT)
-        return fail(CORU_ENOTSUP, "DVariant::approx (pinv core, corutv.hpp:91-92) is outside this build's scope");
+    if (variant != CORU_D_EXACT && variant != CORU_D_APPROX) return fail(CORU_EINVAL, "corutv: unknown DVariant");
     if (!A || !U || !Tt || !V) return fail(CORU_EINVAL, "null argument");
     if (c->world > 1) return fail(CORU_EINVAL, "host-buffer entry is single-GPU; use the _dev entry per rank");
     // Head of the arena: A, U, T, V and a flag, then the decomposition workspace.
@@ -716,6 +743,7 @@ int corutv_host(coru_ctx* c, const T* A, int64_t m, int64_t n, int64_t ell, int 
         probe.rows = m >= n ? m : n;
         probe.cols = m >= n ? n : m;
         probe.d = int(ell);
+        probe.variant = variant;
         Work<T> w;
         Carver meas{nullptr, head_bytes};
         w.layout(meas, c, probe, int(round_up(ell, 8)));
@@ -742,6 +770,7 @@ int corutv_host(coru_ctx* c, const T* A, int64_t m, int64_t n, int64_t ell, int 
     r.q = q;
     r.seed = seed;
     r.stream = stream;
+    r.variant = variant;
     r.perm_host = perm;
     r.warn_host = &out.conditioning_warning;
     if (m < n) {
@@ -1145,6 +1174,22 @@ int coru_gemm_f32_dev(coru_ctx* c, int op, const float* A, int64_t lda, const fl
     CORU_TRY(ensure_arena(c, size_t(wse) * 4 + 256));
     CORU_TRY(gemm<float>(c, o, A, lda, X, ldx, C, ldc, rows, K, int(N), reinterpret_cast<float*>(c->arena), wse));
     CORU_CUDA(cudaStreamSynchronize(c->stream));
+    return CORU_OK;
+}
+
+int coru_pinv_f64_dev(coru_ctx* c, const double* Y, int64_t ldy, int64_t n, double* P, int64_t ldp, int* converged) {
+    CORU_TRY(enter(c));
+    std::lock_guard<std::mutex> lk(c->mu);
+    if (n < 1 || ldy < n || ldp < n) return fail(CORU_EINVAL, "pinv: bad shape");
+    CORU_TRY(ensure_arena(c, size_t(pinv_ws_doubles(int(n))) * sizeof(double) + 256));
+    double* ws = reinterpret_cast<double*>(c->arena);
+    int* conv_d = reinterpret_cast<int*>(ws + pinv_ws_doubles(int(n)));
+    CORU_CUDA(pinv_square<double>(Y, ldy, int(n), P, ldp, ws, conv_d, c->max_smem, c->stream));
+    g_launches += kPinvLaunches;
+    int conv = 0;
+    CORU_CUDA(cudaMemcpyAsync(&conv, conv_d, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+    CORU_CUDA(cudaStreamSynchronize(c->stream));
+    if (converged) *converged = conv;
     return CORU_OK;
 }
 

@@ -28,3 +28,21 @@ def sketch_case():
 
 def kat():
     return dict(np.load(os.path.join(HERE, "kernels_ref_kat.npz")))
+
+
+def approx_cases():
+    z = np.load(os.path.join(HERE, "approx_ref_cases.npz"))
+    out = []
+    for name in z["names"]:
+        name = str(name)
+        ell, q, seed, stream = (int(x) for x in z[f"{name}/params"])
+        lower, warn = (bool(x) for x in z[f"{name}/flags"])
+        out.append(dict(name=name, A=z[f"{name}/A"], ell=ell, q=q, seed=seed, stream=stream, U=z[f"{name}/U"],
+                        T=z[f"{name}/T"], V=z[f"{name}/V"], lower=lower, warning=warn))
+    return out
+
+
+def pinv_cases():
+    z = np.load(os.path.join(HERE, "approx_ref_cases.npz"))
+    return [dict(name=str(k), A=z[f"pinv/{k}/in"], P=z[f"pinv/{k}/out"], U=z[f"pinv/{k}/u"], S=z[f"pinv/{k}/s"],
+                 V=z[f"pinv/{k}/v"], converged=bool(z[f"pinv/{k}/conv"][0])) for k in z["pinv_names"]]

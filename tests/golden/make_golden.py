@@ -105,6 +105,57 @@ def main():
         kat[f"qrcp_trial{trial}_q"], kat[f"qrcp_trial{trial}_r"], kat[f"qrcp_trial{trial}_perm"] = R.qrcp(a)
     np.savez_compressed(os.path.join(HERE, "kernels_ref_kat.npz"), **kat)
     print("wrote", len(names), "corutv cases and", len(kat), "kernel KAT arrays")
+    approx_fixtures(cases)
+
+
+def approx_fixtures(cases):
+    """DVariant::approx (corutv.hpp:91-92) and its pinv core (svd.hpp:31-187)."""
+    ap = {}
+    anames = []
+    er = exact_rank_matrix(40, 30, 6, 9)                                                      # test_corutv.cpp:87-96
+    acases = [("approx_exact_rank_40x30_q0", er, 10, 0, 10, 0), ("approx_exact_rank_40x30_q2", er, 10, 2, 10, 0)]
+    pick = {"fast_decay_80_q0", "fast_decay_80_q2", "wide_20x35_ulv", "noisy_lowrank_150_q0",
+            "noisy_lowrank_150_q2", "fast_decay_120_q0", "diag531_6x5", "rank1_12x9"}
+    acases += [("approx_" + c[0],) + c[1:] for c in cases if c[0] in pick]
+    for name, a, ell, q, seed, stream in acases:
+        f = R.corutv(a, ell, q, 1, seed, stream)
+        anames.append(name)
+        ap[f"{name}/A"] = a
+        ap[f"{name}/params"] = np.array([ell, q, seed, stream], np.int64)
+        ap[f"{name}/U"], ap[f"{name}/T"], ap[f"{name}/V"] = f.u, f.t, f.v
+        ap[f"{name}/flags"] = np.array([f.lower, f.conditioning_warning], np.int64)
+    ap["names"] = np.array(anames)
+    # pinv / square Jacobi SVD known answers (test_matcore.cpp:119-205) and the cores the approx
+    # variant actually inverts: Q2^T·C2prev from the reference's own sketch_bases.
+    sq = {}
+    sq["diag3m2"] = np.array([[3.0, 0.0], [0.0, -2.0]])
+    sq["swap2"] = np.array([[0.0, 1.0], [1.0, 0.0]])
+    d2 = np.zeros((2, 2)); d2[0, 0] = 2.0
+    sq["diag2_0"] = d2
+    sq["zero3"] = np.zeros((3, 3))
+    stream = 0
+    for m in range(1, 5):                                                                    # :138-150 (square)
+        sq[f"gauss{m}x{m}"] = R.gaussian(m, m, 77, stream + 5 * (m - 1))
+    for trial, n in enumerate((7, 12, 25, 40)):
+        sq[f"gauss{n}_t{trial}"] = R.gaussian(n, n, trial + 1, 3)
+    u, v = R.gaussian(6, 2, 9, 0), R.gaussian(6, 2, 9, 1)                                    # :170-176
+    sq["rank2_6"] = R.matmul(u, np.ascontiguousarray(v.T))
+    g = R.gaussian(30, 30, 5, 5)
+    sq["graded30"] = g * (10.0 ** -(np.arange(30) / 2.0))
+    for name, a, ell, q, seed, stream in acases[:2] + [c for c in acases if c[0] in ("approx_fast_decay_80_q2", "approx_noisy_lowrank_150_q0")]:
+        if a.shape[0] < a.shape[1]:
+            continue
+        q1, q2, c1, c2p, _ = R.sketch_bases(a, ell, q, seed, stream)
+        sq[f"core_{name}"] = R.matmul(np.ascontiguousarray(q2.T), c2p)
+    for k, a in sq.items():
+        ap[f"pinv/{k}/in"] = a
+        ap[f"pinv/{k}/out"] = R.pinv(a)
+        uu, ss, vv, conv = R.svd(a)
+        ap[f"pinv/{k}/u"], ap[f"pinv/{k}/s"], ap[f"pinv/{k}/v"] = uu, ss, vv
+        ap[f"pinv/{k}/conv"] = np.array([conv], np.int64)
+    ap["pinv_names"] = np.array(list(sq))
+    np.savez_compressed(os.path.join(HERE, "approx_ref_cases.npz"), **ap)
+    print("wrote", len(anames), "approx corutv cases and", len(sq), "pinv cases")
 
 
 if __name__ == "__main__":

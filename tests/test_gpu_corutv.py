@@ -91,8 +91,9 @@ def test_bad_parameters(ctx):
     for ell, q in [(0, 0), (8, 0), (3, -1)]:
         with pytest.raises(cg.CoruInvalidArgument):
             cg.corutv(a, ell, q, seed=cg.RngSeed(1, 0), ctx=ctx)
-    with pytest.raises(NotImplementedError):
-        cg.corutv(a, 3, 0, cg.DVariant.approx, cg.RngSeed(1, 0), ctx=ctx)
+    for ell, q in [(0, 0), (8, 0), (3, -1)]:  # the approx variant validates the same way
+        with pytest.raises(cg.CoruInvalidArgument):
+            cg.corutv(a, ell, q, cg.DVariant.approx, cg.RngSeed(1, 0), ctx=ctx)
     bad = a.copy()
     bad[2, 3] = np.nan
     with pytest.raises(cg.CoruInvalidArgument):  # matrix.hpp:29-31

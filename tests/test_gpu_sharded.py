@@ -13,7 +13,7 @@ from conftest import orth_residual
 pytestmark = pytest.mark.gpu
 
 
-def _run_sharded(a_dev, d, q, world, seed=42):
+def _run_sharded(a_dev, d, q, world, seed=42, variant=0):
     import torch
     import paper_1810_07323_b200 as cg
     m, n = a_dev.shape
@@ -28,7 +28,7 @@ def _run_sharded(a_dev, d, q, world, seed=42):
             r0, rows = cg.shard_rows(m, rank, world)
             a_r = a_dev[r0:r0 + rows].contiguous()
             torch.cuda.synchronize()
-            f = cg.corutv(a_r, d, q, seed=cg.RngSeed(seed, 0), ctx=ctx, m_global=m)
+            f = cg.corutv(a_r, d, q, cg.DVariant(variant), seed=cg.RngSeed(seed, 0), ctx=ctx, m_global=m)
             torch.cuda.synchronize()
             out[rank] = f
         except Exception as e:  # surfaced below (the group releases the other ranks)
@@ -75,3 +75,29 @@ def test_sharded_matches_single_gpu(ctx, world, m, n, d, q):
     # determinism of the sharded path itself
     again = _run_sharded(a_dev, d, q, world)
     assert torch.equal(again[0].t, parts[0].t) and torch.equal(torch.cat([f.u for f in again]), torch.cat([f.u for f in parts]))
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_sharded_approx_matches_single_gpu(ctx, world):
+    """DVariant::approx sharded: Q1^T C1 is all-reduced, the pinv of Q2^T C2prev is replicated."""
+    import torch
+    import paper_1810_07323_b200 as cg
+    m, n, d, q = 4000, 2000, 40, 1
+    rng = np.random.default_rng(world)
+    r = 2 * d
+    x, _ = np.linalg.qr(rng.standard_normal((m, r)))
+    y, _ = np.linalg.qr(rng.standard_normal((n, r)))
+    a = (x * np.logspace(0, -2, r)) @ y.T + 1e-7 * rng.standard_normal((m, n))
+    a_dev = torch.from_numpy(a).cuda()
+    single = cg.corutv(a_dev, d, q, cg.DVariant.approx, seed=cg.RngSeed(42, 0), ctx=ctx)
+    parts = _run_sharded(a_dev, d, q, world, variant=1)
+    for f in parts[1:]:
+        assert torch.equal(f.t, parts[0].t) and torch.equal(f.v, parts[0].v)
+    u = torch.cat([f.u for f in parts]).cpu().numpy()
+    t, v = parts[0].t.cpu().numpy(), parts[0].v.cpu().numpy()
+    assert orth_residual(u) <= 1e-12 * d and orth_residual(v) <= 1e-12 * d
+    su, st, sv = single.u.cpu().numpy(), single.t.cpu().numpy(), single.v.cpu().numpy()
+    e_sh = np.linalg.norm(a - u @ t @ v.T) / np.linalg.norm(a)
+    e_1 = np.linalg.norm(a - su @ st @ sv.T) / np.linalg.norm(a)
+    assert abs(e_sh - e_1) <= 1e-8 * e_1
+    assert np.max(np.abs(np.abs(np.diag(t)) - np.abs(np.diag(st)))) <= 1e-8 * abs(st[0, 0])

@@ -7,7 +7,7 @@ present. This is what entitles the GPU parity tests to use the oracle as the che
 import numpy as np
 import pytest
 
-from golden import corutv_cases, kat, sketch_case
+from golden import approx_cases, corutv_cases, kat, pinv_cases, sketch_case
 
 
 def test_rng_words_and_gaussian_bitexact(oracle):
@@ -60,6 +60,49 @@ def test_corutv_bitexact_vs_golden(oracle, case):
     assert f.lower == case["lower"] and f.conditioning_warning == case["warning"]
 
 
+@pytest.mark.parametrize("case", approx_cases(), ids=lambda c: c["name"])
+def test_corutv_approx_bitexact_vs_golden(oracle, case):
+    """DVariant::approx (corutv.hpp:91-92): sketch products, pinv (svd.hpp) and the core product."""
+    f = oracle.corutv(case["A"], case["ell"], case["q"], 1, case["seed"], case["stream"])
+    assert np.array_equal(f.u, case["U"])
+    assert np.array_equal(f.t, case["T"])
+    assert np.array_equal(f.v, case["V"])
+    assert f.lower == case["lower"] and f.conditioning_warning == case["warning"]
+
+
+@pytest.mark.parametrize("case", pinv_cases(), ids=lambda c: c["name"])
+def test_pinv_and_jacobi_svd_bitexact_vs_golden(oracle, case):
+    """pinv (svd.hpp:167-187) and the square one-sided Jacobi SVD (svd.hpp:31-134, 141-161)."""
+    assert np.array_equal(oracle.pinv(case["A"]), case["P"])
+    u, s, v, conv = oracle.jacobi_svd_square(case["A"])
+    assert np.array_equal(s, case["S"]) and np.array_equal(u, case["U"]) and np.array_equal(v, case["V"])
+    assert conv == case["converged"]
+
+
+def test_pinv_properties(oracle):
+    """test_matcore.cpp:178-205: diagonal / zero / orthonormal inputs and the Penrose identities."""
+    p = oracle.pinv(np.diag([2.0, 0.0]))
+    assert p[0, 0] == 0.5 and p[1, 1] == 0.0
+    assert np.max(np.abs(oracle.pinv(np.zeros((3, 3))))) == 0.0
+    q, _ = oracle.householder_qr(oracle.gaussian(8, 8, 13, 0))
+    assert np.max(np.abs(oracle.pinv(q) - q.T)) <= 1e-12
+    a = oracle.gaussian(10, 10, 17, 0)
+    ap = oracle.pinv(a)
+    sc = np.linalg.norm(a)
+    assert np.linalg.norm(a @ ap @ a - a) <= 1e-10 * sc
+    assert np.linalg.norm(ap @ a @ ap - ap) <= 1e-9 * sc
+
+
+def test_approx_agrees_with_exact_on_exact_rank(oracle):
+    """test_corutv.cpp:87-96: approx-D and exact-D reconstructions agree on an exact-rank matrix."""
+    c = approx_cases()[0]
+    a = c["A"]
+    for q in (0, 2):
+        e = oracle.corutv(a, 10, q, 0, 10, 0)
+        p = oracle.corutv(a, 10, q, 1, 10, 0)
+        assert np.linalg.norm(e.u @ e.t @ e.v.T - p.u @ p.t @ p.v.T) <= 1e-6 * np.linalg.norm(a)
+
+
 def test_corutv_threads_do_not_change_bits(oracle):
     case = corutv_cases()[1]
     f1 = oracle.corutv(case["A"], case["ell"], case["q"], 0, case["seed"], 0, threads=1)
@@ -91,6 +134,12 @@ def test_oracle_matches_live_reference(oracle, reference):
         g = reference.corutv(a, d, q, 0, 42, 3)
         assert np.array_equal(f.u, g.u) and np.array_equal(f.t, g.t) and np.array_equal(f.v, g.v)
         assert f.conditioning_warning == g.conditioning_warning
+        f = oracle.corutv(a, d, q, 1, 42, 3)
+        g = reference.corutv(a, d, q, 1, 42, 3)
+        assert np.array_equal(f.u, g.u) and np.array_equal(f.t, g.t) and np.array_equal(f.v, g.v)
+    for n in (1, 3, 16, 33, 64):
+        a = rng.standard_normal((n, n)) * (0.5 ** np.arange(n))
+        assert np.array_equal(oracle.pinv(a), reference.pinv(a))
 
 
 def test_reference_threaded_driver_bitexact(reference):
