@@ -83,26 +83,29 @@ __device__ __forceinline__ void dmma_16x8x8(double (&c)[4], const double (&a)[4]
 }
 
 // Short-latency fp64 reciprocal / reciprocal square root for the latency-bound reflector chains:
-// a single-precision MUFU seed refined by Newton steps (DFMA), ~1 ulp. IEEE fp64 division and
-// sqrt are ~400-cycle serial sequences on this chip (tools/qr_reg_tl). Arguments outside the float
-// exponent range (or zero / non-finite) fall back to the IEEE operation.
-__device__ __forceinline__ bool float_range(double x) {
+// the fp64 MUFU seed (MUFU.RCP64H / MUFU.RSQ64H, from the PTX .approx.ftz.f64 forms) refined by
+// Newton steps (DFMA). Measured on B200 (tools/lat2_probe.cu): 54 / 63 cycles dependent latency
+// against ~200 for the float-seeded form and ~400 for IEEE division / sqrt; rcp within 1 ulp of
+// IEEE, rsqrt within 1.4 ulp. Zero, subnormal, huge and non-finite arguments take the IEEE path.
+__device__ __forceinline__ bool mufu64_range(double x) {
     const double a = fabs(x);
-    return a > 1e-36 && a < 1e36;
+    return a > 1e-300 && a < 1e300;
 }
 __device__ __forceinline__ double fast_rcp(double x) {
-    if (!float_range(x)) return 1.0 / x;
-    double r = double(__frcp_rn(float(x)));
+    if (!mufu64_range(x)) return 1.0 / x;
+    double r;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
     double e = fma(-x, r, 1.0);
     r = fma(r, e, r);
     e = fma(-x, r, 1.0);
     return fma(r, e, r);
 }
 __device__ __forceinline__ double fast_rsqrt(double x) {  // x > 0
-    if (!float_range(x)) return 1.0 / sqrt(x);
-    double r = double(rsqrtf(float(x)));
-    // r <- r (3 - x r^2) / 2, twice (quadratic convergence from ~2^-23)
-    double h = 0.5 * x;
+    if (!mufu64_range(x)) return 1.0 / sqrt(x);
+    double r;
+    asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+    // r <- r (3 - x r^2) / 2, twice (quadratic convergence from the MUFU seed)
+    const double h = 0.5 * x;
     r = r * fma(-h * r, r, 1.5);
     r = r * fma(-h * r, r, 1.5);
     return r;

@@ -3,7 +3,7 @@
 // The reference's Jacobi SVD (svd.hpp:31-134) rotates column pairs in cyclic row order
 // (0,1),(0,2),...,(1,2),...: d(d-1)/2 strictly sequential rotations per sweep. Here the pairs of a
 // sweep are visited in round-robin (tournament) order instead: each of the d-1 steps of a sweep
-// is d/2 disjoint pairs, rotated concurrently, one warp per pair. Every rotation uses the
+// is d/2 disjoint pairs, rotated concurrently, one lane group (4-32 lanes) per pair. Every rotation uses the
 // reference's formulas (threshold 1e-14·sqrt(sq_j·sq_k), zeta, t, c, s, recomputed squared norms)
 // and the same convergence rule (a sweep without a rotation, at most 60 sweeps); the converged
 // factorisation equals the cyclic one up to rounding and the signs of singular-vector pairs,
@@ -44,20 +44,37 @@ size_t jacobi_smem(int d, bool cols_in_smem) {
     return b;
 }
 
-template <typename T>
-__global__ void __launch_bounds__(kJacThreadsMax, 1)
+// Sum over the G lanes of a lane group (xor offsets stay inside aligned groups); every lane of
+// the group ends with the same bits.
+template <int G>
+__device__ __forceinline__ double group_sum(double v) {
+#pragma unroll
+    for (int o = G / 2; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+// One CTA. A lane group of G lanes rotates one column pair; a warp carries 32/G pairs, so the
+// per-pair scalar work (threshold, zeta, t, c, s) is issued once for 32/G pairs.
+// E > 0: the columns live in shared memory and each lane keeps its E entries of the four columns
+// of its pair (a_j, a_k, v_j, v_k) in registers for the whole rotation (one load round, one store
+// round); E = 0: columns in the global workspace (wide cores), streamed per loop.
+template <typename T, int G, int E>
+__global__ void __launch_bounds__(E > 0 ? 512 : kJacThreadsMax, 1)
     k_jacobi_svd(const T* __restrict__ Y, int64_t ldy, int d, double* ws, int cols_in_smem, int* converged_out) {
+    constexpr int kPairsPerWarp = kWarp / G;
     const int kJacThreads = blockDim.x, kJacWarps = kJacThreads >> 5;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     double* sq = reinterpret_cast<double*>(smem_raw);
     int* ord = reinterpret_cast<int*>(sq + d);
     const size_t head = (size_t(d) * sizeof(double) + size_t(d) * sizeof(int) + 15) / 16 * 16;
     PinvWs w(ws, d);
-    double* a = cols_in_smem ? reinterpret_cast<double*>(smem_raw + head) : w.a;
+    double* a = (E > 0 || cols_in_smem) ? reinterpret_cast<double*>(smem_raw + head) : w.a;
     double* v = a + int64_t(d) * d;
     __shared__ int s_rot;
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int gl = lane % G;                             // lane within the group
+    const int slots = kJacWarps * kPairsPerWarp;
     // column-major working copy (svd.hpp:152-154: a_cm[j·n + i] = a(i, j)) and V = I
     for (int e = tid; e < d * d; e += kJacThreads) {
         const int i = e / d, j = e - i * d;
@@ -65,65 +82,115 @@ __global__ void __launch_bounds__(kJacThreadsMax, 1)
         v[int64_t(j) * d + i] = (i == j) ? 1.0 : 0.0;
     }
     __syncthreads();
-    for (int j = warp; j < d; j += kJacWarps) {  // svd.hpp:38-43
-        const double* c = a + int64_t(j) * d;
+    for (int b = warp * kPairsPerWarp; b < d; b += slots) {  // svd.hpp:38-43 (whole warps join the shuffles)
+        const int j = b + lane / G;
         double s = 0.0;
-        for (int i = lane; i < d; i += kWarp) s += c[i] * c[i];
-        s = warp_sum(s);
-        if (lane == 0) sq[j] = s;
+        if (j < d) {
+            const double* c = a + int64_t(j) * d;
+            for (int i = gl; i < d; i += G) s += c[i] * c[i];
+        }
+        s = group_sum<G>(s);
+        if (j < d && gl == 0) sq[j] = s;
     }
 
     const int np = d + (d & 1);  // an odd d gets a dummy player
+    const int npairs = np / 2, mod = np - 1;
     int converged = 0;
     for (int sweep = 0; sweep < kMaxSweeps; ++sweep) {
         if (tid == 0) s_rot = 0;
         __syncthreads();
-        for (int step = 0; step + 1 < np; ++step) {
-            for (int p = warp; p < np / 2; p += kJacWarps) {
+        for (int step = 0; step < mod; ++step) {
+            // every lane runs the same trip count so the group shuffles stay converged
+            for (int p0 = warp * kPairsPerWarp; p0 < npairs; p0 += slots) {
+                const int p = p0 + lane / G;
                 // round-robin: position 0 fixed, positions 1..np-1 rotate by `step`
-                const int x = p == 0 ? 0 : (p - 1 + step) % (np - 1) + 1;
-                const int y = (np - 2 - p + step) % (np - 1) + 1;
+                int x = p - 1 + step, y = np - 2 - p + step;
+                x = x >= mod ? x - mod : x;
+                y = y >= mod ? y - mod : y;
+                x = p == 0 ? 0 : x + 1;
+                y += 1;
                 const int j = min(x, y), k = max(x, y);
-                if (k >= d) continue;
-                const double sqj = sq[j], sqk = sq[k];
-                if (sqj == 0.0 || sqk == 0.0) continue;  // svd.hpp:50
-                double* cj = a + int64_t(j) * d;
-                double* ck = a + int64_t(k) * d;
+                bool act = p < npairs && k < d;
+                const double sqj = act ? sq[j] : 0.0, sqk = act ? sq[k] : 0.0;
+                act = act && sqj != 0.0 && sqk != 0.0;  // svd.hpp:50
+                double* cj = a + int64_t(act ? j : 0) * d;
+                double* ck = a + int64_t(act ? k : 0) * d;
+                double* vj = v + int64_t(act ? j : 0) * d;
+                double* vk = v + int64_t(act ? k : 0) * d;
                 double g = 0.0;
-                for (int i = lane; i < d; i += kWarp) g += cj[i] * ck[i];
-                g = warp_sum(g);  // butterfly: identical on every lane
-                // svd.hpp:53-60 with short-latency reciprocals / square roots (Newton-refined
-                // MUFU seeds, ~1 ulp) in place of the serial IEEE divide and sqrt chain
+                [[maybe_unused]] double xr[E > 0 ? E : 1], yr[E > 0 ? E : 1], pr[E > 0 ? E : 1], qr[E > 0 ? E : 1];
+                if constexpr (E > 0) {
+#pragma unroll
+                    for (int e = 0; e < E; ++e) {
+                        const int i = gl + e * G;
+                        const bool in = act && i < d;
+                        xr[e] = in ? cj[i] : 0.0;
+                        yr[e] = in ? ck[i] : 0.0;
+                        pr[e] = in ? vj[i] : 0.0;
+                        qr[e] = in ? vk[i] : 0.0;
+                    }
+#pragma unroll
+                    for (int e = 0; e < E; ++e) g += xr[e] * yr[e];
+                } else {
+                    if (act)
+                        for (int i = gl; i < d; i += G) g += cj[i] * ck[i];
+                }
+                g = group_sum<G>(g);
+                // svd.hpp:53-60. Same rotation, evaluated with one chain of short-latency MUFU-seeded
+                // reciprocals: with D = sq_k - sq_j, zeta = D/(2g) and
+                //   t = sign(zeta)/(|zeta| + sqrt(1 + zeta^2)) = sign(zeta)·2|g|/(|D| + sqrt(D^2 + 4g^2)),
+                // the threshold |g| <= 1e-14·sqrt(sq_j·sq_k) compared in squares, and the reference's
+                // "zeta not finite -> skip" as |D| > 2|g|·DBL_MAX.
                 const double pjk = sqj * sqk;
-                if (fabs(g) <= (pjk > 0.0 ? 1e-14 * pjk * fast_rsqrt(pjk) : 0.0)) continue;
-                const double zeta = (sqk - sqj) * fast_rcp(2.0 * g);
-                if (!isfinite(zeta)) continue;
-                const double h = 1.0 + zeta * zeta;
-                const double t =
-                    isinf(h) ? 0.0 : (zeta >= 0.0 ? 1.0 : -1.0) * fast_rcp(fabs(zeta) + h * fast_rsqrt(h));
-                const double c = fast_rsqrt(1.0 + t * t);
-                const double s = c * t;
+                const double ag = fabs(g);
+                const bool tiny = (pjk > 1e-280 && pjk < 1e280 && ag < 1e140) ? g * g <= 1e-28 * pjk
+                                                                              : ag <= 1e-14 * sqrt(pjk);
+                const double D = sqk - sqj;
+                act = act && !tiny && !(fabs(D) > 2.0 * ag * DBL_MAX);
                 double sj = 0.0, sk = 0.0;
-                for (int i = lane; i < d; i += kWarp) {
-                    const double xv = cj[i], yv = ck[i];
-                    const double nx = c * xv - s * yv, ny = s * xv + c * yv;
-                    cj[i] = nx;
-                    ck[i] = ny;
-                    sj += nx * nx;
-                    sk += ny * ny;
+                if (act) {
+                    const double qq = D * D + 4.0 * g * g;
+                    const double r = mufu64_range(qq) ? qq * fast_rsqrt(qq) : sqrt(qq);
+                    const double sgn = (D == 0.0 || (D > 0.0) == (g > 0.0)) ? 1.0 : -1.0;
+                    const double t = sgn * (2.0 * ag) * fast_rcp(fabs(D) + r);  // r = inf -> t = 0 (ref :58)
+                    const double c = fast_rsqrt(1.0 + t * t);
+                    const double s = c * t;
+                    if constexpr (E > 0) {
+#pragma unroll
+                        for (int e = 0; e < E; ++e) {
+                            const int i = gl + e * G;
+                            const double nx = c * xr[e] - s * yr[e], ny = s * xr[e] + c * yr[e];
+                            const double nv = c * pr[e] - s * qr[e], nw = s * pr[e] + c * qr[e];
+                            sj += nx * nx;
+                            sk += ny * ny;
+                            if (i < d) {
+                                cj[i] = nx;
+                                ck[i] = ny;
+                                vj[i] = nv;
+                                vk[i] = nw;
+                            }
+                        }
+                    } else {
+                        for (int i = gl; i < d; i += G) {
+                            const double xv = cj[i], yv = ck[i];
+                            const double nx = c * xv - s * yv, ny = s * xv + c * yv;
+                            cj[i] = nx;
+                            ck[i] = ny;
+                            sj += nx * nx;
+                            sk += ny * ny;
+                        }
+                        for (int i = gl; i < d; i += G) {
+                            const double xv = vj[i], yv = vk[i];
+                            vj[i] = c * xv - s * yv;
+                            vk[i] = s * xv + c * yv;
+                        }
+                    }
                 }
-                double* vj = v + int64_t(j) * d;
-                double* vk = v + int64_t(k) * d;
-                for (int i = lane; i < d; i += kWarp) {
-                    const double xv = vj[i], yv = vk[i];
-                    vj[i] = c * xv - s * yv;
-                    vk[i] = s * xv + c * yv;
-                }
-                double r2[2] = {sj, sk};
-                warp_allreduce_vec<2>(r2, lane);
-                if (lane == 0) {
-                    sq[j] = r2[0];
-                    sq[k] = r2[1];
+                sj = group_sum<G>(sj);
+                sk = group_sum<G>(sk);
+                if (act && gl == 0) {
+                    sq[j] = sj;
+                    sq[k] = sk;
                     s_rot = 1;
                 }
             }
@@ -213,10 +280,20 @@ cudaError_t pinv_square(const T* Y, int64_t ldy, int d, T* P, int64_t ldp, doubl
                         cudaStream_t st) {
     const bool in_smem = jacobi_smem(d, true) <= size_t(max_smem);
     const size_t smem = jacobi_smem(d, in_smem);
-    allow_max_smem(k_jacobi_svd<T>);
-    // one warp per concurrent pair of a round-robin step (d/2 pairs), at most 32 warps
-    const int warps = std::min(32, std::max(1, (d + 1) / 2));
-    k_jacobi_svd<T><<<1, warps * kWarp, smem, st>>>(Y, ldy, d, ws, in_smem ? 1 : 0, converged);
+    // G lanes per column pair, at most 8 column entries per lane (register path when the columns
+    // fit shared memory); enough warps for the d/2 pairs of a round-robin step
+    const int pairs = (d + 1) / 2;
+    const int cols = in_smem ? 1 : 0;
+    auto launch = [&](auto kern, int G, int max_warps) {
+        const int ppw = kWarp / G;
+        const int warps = std::min(max_warps, std::max(1, (pairs + ppw - 1) / ppw));
+        allow_max_smem(kern);
+        kern<<<1, warps * kWarp, smem, st>>>(Y, ldy, d, ws, cols, converged);
+    };
+    if (in_smem && d <= 32) launch(k_jacobi_svd<T, 4, 8>, 4, 16);
+    else if (in_smem && d <= 64) launch(k_jacobi_svd<T, 8, 8>, 8, 16);
+    else if (in_smem && d <= 128) launch(k_jacobi_svd<T, 16, 8>, 16, 16);
+    else launch(k_jacobi_svd<T, 32, 0>, 32, 32);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     const dim3 grid((d + kAsmTile - 1) / kAsmTile, (d + kAsmTile - 1) / kAsmTile);
