@@ -12,6 +12,7 @@
 // redundant top QR on every rank), and everything ell x ell or n x ell is computed redundantly
 // and bit-identically on every rank (all kernels are atomic-free and fixed-order).
 #include <dlfcn.h>
+#include <cstdlib>
 #include <nccl.h>
 
 #include <algorithm>
@@ -556,9 +557,10 @@ int run_impl(coru_ctx* c, const Request<T>& r, size_t extra_arena_off) {
     // overlaps the last A^T pass; with a communicator QR(c1) stays on the main stream (its
     // all-gather must keep the NCCL issue order) and QR(c2) goes to the aux stream.
     const bool sharded = c->world > 1;
+    const bool early_qr1 = !sharded && getenv("CORU_QR1_EARLY") != nullptr;  // tooling: overlap QR(c1) with the last A^T pass
     for (int i = 0; i <= r.q; ++i) {
         CORU_TRY(gemm<T>(c, r.op_a(), r.A, r.lda, w.b2, dp, w.b1, dp, R, N, d, w.gws, w.gws_elems));
-        if (i == r.q && !sharded) {
+        if (i == r.q && early_qr1) {
             CORU_CUDA(cudaEventRecord(c->ev_fork, st));
             CORU_CUDA(cudaStreamWaitEvent(c->aux, c->ev_fork, 0));
             CORU_TRY(w.ts1.factor(w.b1, dp, w.r1, c->aux));  // Q1, R1 = QR(c1) (corutv.hpp:59)
@@ -586,6 +588,16 @@ int run_impl(coru_ctx* c, const Request<T>& r, size_t extra_arena_off) {
         CORU_CUDA(conditioning_flag<T>(w.r1, d, d, w.flag, st));
         ++g_launches;
     } else {
+        if (!early_qr1) {
+            // QR(c1) on the aux stream, concurrent with QR(c2): both trees start once the last
+            // A^T pass is done (overlapping that pass only slows it; QR(c2) is the critical path)
+            CORU_CUDA(cudaEventRecord(c->ev_fork, st));
+            CORU_CUDA(cudaStreamWaitEvent(c->aux, c->ev_fork, 0));
+            CORU_TRY(w.ts1.factor(w.b1, dp, w.r1, c->aux));  // Q1, R1 = QR(c1) (corutv.hpp:59)
+            CORU_TRY(w.ts1.form_q(nullptr, w.q1, dp, c->aux));
+            CORU_CUDA(conditioning_flag<T>(w.r1, d, d, w.flag, c->aux));  // corutv.hpp:61-64
+            ++g_launches;
+        }
         CORU_TRY(w.ts2.factor(w.b2, dp, w.r2, st));  // Q2 = QR(c2) (corutv.hpp:60)
         CORU_TRY(w.ts2.form_q(nullptr, w.q2, dp, st));
     }

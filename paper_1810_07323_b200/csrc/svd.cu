@@ -16,6 +16,8 @@
 #include <algorithm>
 #include <cfloat>
 
+#include <cooperative_groups.h>
+
 #include "common.cuh"
 #include "svd.cuh"
 
@@ -26,7 +28,8 @@ constexpr int kJacThreadsMax = 1024;
 constexpr int kMaxSweeps = 60;  // svd.hpp:35
 
 struct PinvWs {
-    double *a, *v, *vs, *ut, *rank;
+    double *a, *v, *vs, *ut, *rank, *sq;  // rank[0] = kept rank; sq: squared norms (grid kernel)
+    int *rot, *ord;                       // grid kernel: per-sweep "rotated" flags, sort order
     __host__ __device__ PinvWs(double* ws, int d) {
         const int64_t dd = int64_t(d) * d;
         a = ws;
@@ -34,6 +37,9 @@ struct PinvWs {
         vs = v + dd;
         ut = vs + dd;
         rank = ut + dd;
+        sq = rank + 8;
+        rot = reinterpret_cast<int*>(sq + d);
+        ord = rot + kMaxSweeps;
     }
 };
 
@@ -237,6 +243,148 @@ __global__ void __launch_bounds__(E > 0 ? 512 : kJacThreadsMax, 1)
     }
 }
 
+// Wide cores (columns beyond shared memory, d <= 32·kGridE): the same round-robin sweeps spread
+// over a cooperative grid, one warp per pair with the pair's four columns in registers (kGridE
+// entries per lane), one grid-wide barrier per step. Columns and norms live in the L2-resident
+// workspace and are read with ld.global.cg (other SMs wrote them in the previous step).
+constexpr int kGridE = 17;
+constexpr int kGridWarps = 4;
+template <typename T>
+__global__ void __launch_bounds__(kGridWarps * 32)
+    k_jacobi_grid(const T* __restrict__ Y, int64_t ldy, int d, double* ws, int* converged_out) {
+    namespace cgs = cooperative_groups;
+    cgs::grid_group grid = cgs::this_grid();
+    PinvWs w(ws, d);
+    double* a = w.a;
+    double* v = w.v;
+    const int lane = threadIdx.x & 31;
+    const int gw = int(blockIdx.x) * kGridWarps + int(threadIdx.x >> 5);
+    const int nw = int(gridDim.x) * kGridWarps;
+    const int64_t gt = int64_t(blockIdx.x) * blockDim.x + threadIdx.x, nt = int64_t(gridDim.x) * blockDim.x;
+    for (int64_t e = gt; e < int64_t(d) * d; e += nt) {
+        const int i = int(e / d), j = int(e - int64_t(i) * d);
+        a[int64_t(j) * d + i] = double(Y[int64_t(i) * ldy + j]);
+        v[int64_t(j) * d + i] = (i == j) ? 1.0 : 0.0;
+    }
+    if (gt < kMaxSweeps) w.rot[gt] = 0;
+    grid.sync();
+    for (int j = gw; j < d; j += nw) {  // svd.hpp:38-43
+        const double* c = a + int64_t(j) * d;
+        double sacc = 0.0;
+        for (int i = lane; i < d; i += kWarp) {
+            const double x = __ldcg(c + i);
+            sacc += x * x;
+        }
+        sacc = warp_sum(sacc);
+        if (lane == 0) w.sq[j] = sacc;
+    }
+    grid.sync();
+    const int np = d + (d & 1), npairs = np / 2, mod = np - 1;
+    int converged = 0;
+    for (int sweep = 0; sweep < kMaxSweeps; ++sweep) {
+        for (int step = 0; step < mod; ++step) {
+            for (int p = gw; p < npairs; p += nw) {
+                int x = p - 1 + step, y = np - 2 - p + step;
+                x = x >= mod ? x - mod : x;
+                y = y >= mod ? y - mod : y;
+                x = p == 0 ? 0 : x + 1;
+                y += 1;
+                const int j = min(x, y), k = max(x, y);
+                if (k >= d) continue;
+                const double sqj = __ldcg(w.sq + j), sqk = __ldcg(w.sq + k);
+                if (sqj == 0.0 || sqk == 0.0) continue;  // svd.hpp:50
+                double* cj = a + int64_t(j) * d;
+                double* ck = a + int64_t(k) * d;
+                double* vj = v + int64_t(j) * d;
+                double* vk = v + int64_t(k) * d;
+                double xr[kGridE], yr[kGridE], pr[kGridE], qr[kGridE];
+                double g = 0.0;
+#pragma unroll
+                for (int e = 0; e < kGridE; ++e) {
+                    const int i = lane + e * kWarp;
+                    const bool in = i < d;
+                    xr[e] = in ? __ldcg(cj + i) : 0.0;
+                    yr[e] = in ? __ldcg(ck + i) : 0.0;
+                    pr[e] = in ? __ldcg(vj + i) : 0.0;
+                    qr[e] = in ? __ldcg(vk + i) : 0.0;
+                }
+#pragma unroll
+                for (int e = 0; e < kGridE; ++e) g += xr[e] * yr[e];
+                g = warp_sum(g);
+                const double pjk = sqj * sqk;
+                const double ag = fabs(g);
+                const bool tiny = (pjk > 1e-280 && pjk < 1e280 && ag < 1e140) ? g * g <= 1e-28 * pjk
+                                                                              : ag <= 1e-14 * sqrt(pjk);
+                const double D = sqk - sqj;
+                if (tiny || fabs(D) > 2.0 * ag * DBL_MAX) continue;  // svd.hpp:53-56
+                const double qq = D * D + 4.0 * g * g;
+                const double r = mufu64_range(qq) ? qq * fast_rsqrt(qq) : sqrt(qq);
+                const double sgn = (D == 0.0 || (D > 0.0) == (g > 0.0)) ? 1.0 : -1.0;
+                const double t = sgn * (2.0 * ag) * fast_rcp(fabs(D) + r);
+                const double c = fast_rsqrt(1.0 + t * t);
+                const double s = c * t;
+                double sj = 0.0, sk = 0.0;
+#pragma unroll
+                for (int e = 0; e < kGridE; ++e) {
+                    const int i = lane + e * kWarp;
+                    const double nx = c * xr[e] - s * yr[e], ny = s * xr[e] + c * yr[e];
+                    const double nv = c * pr[e] - s * qr[e], nq = s * pr[e] + c * qr[e];
+                    sj += nx * nx;
+                    sk += ny * ny;
+                    if (i < d) {
+                        __stcg(cj + i, nx);
+                        __stcg(ck + i, ny);
+                        __stcg(vj + i, nv);
+                        __stcg(vk + i, nq);
+                    }
+                }
+                double r2[2] = {sj, sk};
+                warp_allreduce_vec<2>(r2, lane);
+                if (lane == 0) {
+                    __stcg(w.sq + j, r2[0]);
+                    __stcg(w.sq + k, r2[1]);
+                    __stcg(w.rot + sweep, 1);
+                }
+            }
+            grid.sync();
+        }
+        if (__ldcg(w.rot + sweep) == 0) {  // read by every thread after the sweep's last barrier
+            converged = sweep + 1;
+            break;
+        }
+    }
+    // stable descending order (svd.hpp:79-82), then the scaled factors for the assembly
+    for (int64_t j = gt; j < d; j += nt) {
+        const double x = __ldcg(w.sq + j);
+        int rnk = 0;
+        for (int i = 0; i < d; ++i) {
+            const double y = __ldcg(w.sq + i);
+            rnk += (y > x) || (y == x && i < j);
+        }
+        w.ord[rnk] = int(j);
+    }
+    grid.sync();
+    const double cut = double(d) * DBL_EPSILON * sqrt(__ldcg(w.sq + __ldcg(w.ord)));
+    for (int r = gw; r < d; r += nw) {
+        const int src = __ldcg(w.ord + r);
+        const double sigma = sqrt(__ldcg(w.sq + src));
+        const double inv = sigma > cut ? 1.0 / sigma : 0.0;
+        if (inv == 0.0) continue;
+        const double* vc = v + int64_t(src) * d;
+        const double* ac = a + int64_t(src) * d;
+        for (int i = lane; i < d; i += kWarp) {
+            w.vs[int64_t(r) * d + i] = __ldcg(vc + i) * inv;
+            w.ut[int64_t(r) * d + i] = __ldcg(ac + i) / sigma;
+        }
+    }
+    if (gt == 0) {
+        int rk = 0;
+        while (rk < d && sqrt(__ldcg(w.sq + __ldcg(w.ord + rk))) > cut) ++rk;
+        w.rank[0] = double(rk);
+        if (converged_out) *converged_out = converged;
+    }
+}
+
 // P(i, l) = sum_{r < rank} vs(r, i)·ut(r, l), r increasing (matmul(vs, uᵀ), svd.hpp:180).
 constexpr int kAsmTile = 32;
 template <typename T>
@@ -273,7 +421,7 @@ __global__ void __launch_bounds__(256) k_pinv_assemble(const double* ws, int d, 
 
 }  // namespace
 
-int64_t pinv_ws_doubles(int d) { return 4 * int64_t(d) * d + 8; }
+int64_t pinv_ws_doubles(int d) { return 4 * int64_t(d) * d + 8 + d + (kMaxSweeps + d + 1) / 2 + 8; }
 
 template <typename T>
 cudaError_t pinv_square(const T* Y, int64_t ldy, int d, T* P, int64_t ldp, double* ws, int* converged, int max_smem,
@@ -293,7 +441,20 @@ cudaError_t pinv_square(const T* Y, int64_t ldy, int d, T* P, int64_t ldp, doubl
     if (in_smem && d <= 32) launch(k_jacobi_svd<T, 4, 8>, 4, 16);
     else if (in_smem && d <= 64) launch(k_jacobi_svd<T, 8, 8>, 8, 16);
     else if (in_smem && d <= 128) launch(k_jacobi_svd<T, 16, 8>, 16, 16);
-    else launch(k_jacobi_svd<T, 32, 0>, 32, 32);
+    else if (d <= kWarp * kGridE) {
+        // cooperative grid: one warp per pair of a step, every CTA co-resident
+        int dev = 0, sms = 0, per_sm = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_jacobi_grid<T>, kGridWarps * kWarp, 0);
+        const int want = (pairs + kGridWarps - 1) / kGridWarps;
+        const int blocks = std::max(1, std::min(want, std::max(1, per_sm) * sms));
+        int dd = d;
+        void* args[] = {(void*)&Y, (void*)&ldy, (void*)&dd, (void*)&ws, (void*)&converged};
+        cudaError_t e = cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(k_jacobi_grid<T>), dim3(blocks),
+                                                    dim3(kGridWarps * kWarp), args, 0, st);
+        if (e != cudaSuccess) return e;
+    } else launch(k_jacobi_svd<T, 32, 0>, 32, 32);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     const dim3 grid((d + kAsmTile - 1) / kAsmTile, (d + kAsmTile - 1) / kAsmTile);

@@ -20,6 +20,7 @@
 // Two implementations share the tree: the blocked one below (shared-memory block, panels +
 // compact WY) whenever a block of > 1.25 d rows fits shared memory, and the "wide" one (the
 // unblocked column pipeline, working block in L2) for sketch widths too wide for that.
+#include <cstdlib>
 #include <algorithm>
 #include <cmath>
 
@@ -989,6 +990,7 @@ TsqrPlan plan_tsqr(int64_t m, int d, size_t eb, int max_smem) {
     else if (blocked_ok) target = rb_blocked;
     else if (big_ok) target = std::min(rb_big, std::max(4 * d, 1024));
     else target = std::max(4 * d, 256);
+    if (const char* e = getenv("CORU_TSQR_TARGET")) target = std::max(atoi(e), d + 1);  // tooling: tree shape sweeps
     int64_t rows = m;
     int64_t voff = 0, boff = 0, roff = 0, toff = 0;
     for (;;) {

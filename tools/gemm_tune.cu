@@ -1,5 +1,6 @@
 // Sweep the FP64 A-pass GEMM configurations on the BASELINE shapes (tooling only).
 #include <cstdio>
+#include <cstdlib>
 #include <vector>
 #include <cuda_runtime.h>
 #include "../paper_1810_07323_b200/csrc/gemm.cuh"
@@ -11,8 +12,11 @@ __global__ void fill(double* p, size_t n, double s) {
 int main() {
     struct Shape { long m, n; int d; const char* name; };
     Shape shapes[] = {{4000, 4000, 60, "C2"}, {200000, 2000, 110, "C3"}, {32768, 32768, 220, "C4"}};
+    const int only = getenv("TUNE_ONLY") ? atoi(getenv("TUNE_ONLY")) : -1;
+    int si = -1;
     int sms; cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
     for (auto& s : shapes) {
+        if (only >= 0 && ++si != only) continue;
         double *A, *X, *Y, *C, *ws;
         const int dp = (s.d + 7) / 8 * 8;
         cudaMalloc(&A, size_t(s.m) * s.n * 8);
