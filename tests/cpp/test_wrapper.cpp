@@ -83,6 +83,26 @@ int main() {
     // sketch stage (test_corutv.cpp:57-65 uses it directly)
     SketchBases sb = sketch_bases(a, 5, 1, {4, 0});
     CHECK(orth_res(sb.q1) <= 1e-12 * 5 && orth_res(sb.q2) <= 1e-12 * 5);
+    // approx-D agrees with exact-D on an exact-rank matrix (test_corutv.cpp:87-96)
+    const Matrix er = exact_rank(40, 30, 6, {9, 0});
+    for (int q : {0, 2}) {
+        UtvApprox e = corutv(er, 10, q, DVariant::exact, {10, 0});
+        UtvApprox p = corutv(er, 10, q, DVariant::approx, {10, 0});
+        CHECK(p.variant == DVariant::approx);
+        double diff = 0, nrm = 0;
+        for (std::size_t i = 0; i < 40; ++i)
+            for (std::size_t j = 0; j < 30; ++j) {
+                double se = 0, sp = 0;
+                for (std::size_t k = 0; k < 10; ++k)
+                    for (std::size_t l = k; l < 10; ++l) {
+                        se += e.u(i, k) * e.t(k, l) * e.v(j, l);
+                        sp += p.u(i, k) * p.t(k, l) * p.v(j, l);
+                    }
+                diff += (se - sp) * (se - sp);
+                nrm += er(i, j) * er(i, j);
+            }
+        CHECK(std::sqrt(diff) <= 1e-6 * std::sqrt(nrm));
+    }
     std::printf("%s: %d failures\n", failures ? "FAIL" : "OK", failures);
     return failures ? 1 : 0;
 }
