@@ -495,7 +495,7 @@ int thread_allgather(coru_ctx* c, const T* send, T* recv, size_t count) {
 
 template <typename T>
 int allreduce(coru_ctx* c, T* buf, size_t count) {
-    if (c->world <= 1) return CORU_OK;
+    if (c->world <= 1 && !c->comm) return CORU_OK;
     if (c->tcomm) return thread_allreduce<T>(c, buf, count);
     CORU_NCCL(nccl()->AllReduce(buf, buf, count, nccl_type<T>(), ncclSum, c->comm, c->stream));
     return CORU_OK;
@@ -962,7 +962,9 @@ int coru_ctx_init_comm(coru_ctx* c, int rank, int world, const unsigned char id[
     CORU_TRY(enter(c));
     if (world < 1 || rank < 0 || rank >= world) return fail(CORU_EINVAL, "bad rank/world");
     std::lock_guard<std::mutex> lk(c->mu);
-    if (world == 1) {
+    // world 1 needs no communicator; CORU_NCCL_WORLD1 (tests) builds one anyway so the NCCL plumbing
+    // (dlopen, init, all-reduce on the library's stream) runs on a single-GPU box
+    if (world == 1 && !getenv("CORU_NCCL_WORLD1")) {
         c->rank = 0;
         c->world = 1;
         return CORU_OK;

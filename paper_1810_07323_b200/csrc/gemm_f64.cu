@@ -440,6 +440,11 @@ int default_cfg(Op op, int N) {
     return N <= 32 ? 15 : (N <= 64 ? 19 : 15);
 }
 
+// Fix-up flag epochs: ONE process-wide counter for every configuration. (Per-configuration
+// counters let two GEMMs of different configurations that reuse a workspace carry the same epoch,
+// so a stale flag of the earlier one could pass for a fresh publish of the later one.)
+std::atomic<uint64_t> g_gemm_epoch{0};
+
 template <class S>
 cudaError_t launch_cfg(const double* A, int64_t lda, const double* X, int64_t ldx, double* C, int64_t ldc, int64_t Mo,
                        int64_t K, int N, const GemmPlan& p, double* ws, cudaStream_t st) {
@@ -449,8 +454,7 @@ cudaError_t launch_cfg(const double* A, int64_t lda, const double* X, int64_t ld
     const bool vec = (lda % 2 == 0) && (reinterpret_cast<uintptr_t>(A) % 16 == 0);
     // split-tile flags live after the partial tiles; a fresh epoch per launch (no reset needed)
     uint64_t* flags = p.fixup ? reinterpret_cast<uint64_t*>(ws + tiles * int64_t(p.max_seg) * S::BM * S::BN) : nullptr;
-    static std::atomic<uint64_t> launch_counter{0};
-    const uint64_t epoch = 0xC0DEull << 48 | (++launch_counter & 0xFFFFFFFFFFFFull);
+    const uint64_t epoch = 0xC0DEull << 48 | (++g_gemm_epoch & 0xFFFFFFFFFFFFull);
     if (vec) {
         auto k = k_gemm_f64<S, 2>;
         allow_max_smem(k);

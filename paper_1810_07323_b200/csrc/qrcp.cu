@@ -10,6 +10,9 @@
 // Q_M = H_0...H_{d-1} (accumulate_q, qr.hpp:60-72) is formed in compact-WY form with CTA GEMMs.
 #include <algorithm>
 #include <climits>
+#include <cstdlib>
+
+#include <cooperative_groups.h>
 
 #include "common.cuh"
 #include "cta_blas.cuh"
@@ -535,6 +538,305 @@ cudaError_t launch_qrcp_reg(const T* M, int ldm, int d, T* Q, int ldq, T* Tout, 
     return cudaGetLastError();
 }
 
+
+// ------------------------------------------------------------------------------------------------
+// Wide cores (C4 d=220, C5 d=520): the register-resident algorithm above spread over a cooperative
+// grid, one grid barrier per pivot step. Warp gw (of NWT grid-wide) owns columns gw, gw+NWT, ...
+// (CPW of them) in registers (RPL rows per lane). Per step every warp reads the CTA candidates of
+// the step (the best column of each CTA with its reflector already built, L2), picks the global
+// winner with the reference's rule (larger squared norm, then lower position, qr.hpp:121-123),
+// reads the winner's reflector, applies it to its trailing columns and downdates their norms with
+// the 1e-6 recompute guard (qr.hpp:131-139), then builds the reflector of its own best column for
+// the next step; the CTA's best warp publishes its candidate. Cross-CTA data moves through L2
+// (st.cg / ld.cg) and the grid barrier orders it. Same arithmetic as k_qrcp_reg.
+constexpr int kGridQW = 8;  // warps per CTA
+template <typename T, int RPL, int CPW>
+__global__ void __launch_bounds__(kGridQW * 32) k_qrcp_grid(const T* __restrict__ M, int ldm, int d, T* __restrict__ Q,
+                                                           int ldq, T* __restrict__ Tout, int ldt,
+                                                           int64_t* __restrict__ perm_out, T* __restrict__ gs) {
+    namespace cgs = cooperative_groups;
+    cgs::grid_group grid = cgs::this_grid();
+    constexpr int R = RPL * 32;
+    const int nblk = int(gridDim.x), NWT = nblk * kGridQW;
+    // global scratch: vst[d][R] | betas[d] | cand_v[2][nblk][R] | cand_s[2][nblk][3] | cand_i[2][nblk][2] (as T)
+    T* vst = gs;
+    T* betas = vst + int64_t(d) * R;
+    T* cand_v = betas + d;
+    T* cand_s = cand_v + int64_t(2) * nblk * R;
+    int* cand_i = reinterpret_cast<int*>(cand_s + 2 * nblk * 3);
+    __shared__ T wv_s[kGridQW];
+    __shared__ int wk_s[kGridQW], wc_s[kGridQW];
+    __shared__ T wb_s[kGridQW][2];
+    __shared__ __align__(16) T wvec[kGridQW][R];
+
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    const int gw = int(blockIdx.x) * kGridQW + wib;
+    T col[CPW][RPL];
+    T colsq[CPW], base[CPW];
+    int pos[CPW];
+#pragma unroll
+    for (int k = 0; k < CPW; ++k) {
+        const int c = gw + NWT * k;
+        T s = 0;
+#pragma unroll
+        for (int u = 0; u < RPL; ++u) {
+            const int r = lane + 32 * u;
+            col[k][u] = (c < d && r < d) ? M[int64_t(r) * ldm + c] : T(0);
+            s = add_rn(s, mul_rn(col[k][u], col[k][u]));
+        }
+        s = warp_sum(s);  // initial squared norms (qr.hpp:115-119)
+        colsq[k] = base[k] = s;
+        pos[k] = c < d ? c : INT_MAX;
+    }
+
+    // This warp's best column at positions >= jn, its reflector into wvec[wib]; then the CTA's best
+    // warp is published to slot sl. Called by every thread of the CTA.
+    auto candidate = [&](int jn, int sl) {
+        int kb = -1;
+        T bv = T(0);
+        int bp = INT_MAX;
+#pragma unroll
+        for (int k = 0; k < CPW; ++k)
+            if (pos[k] >= jn && pos[k] < d)
+                if (kb < 0 || colsq[k] > bv || (colsq[k] == bv && pos[k] < bp)) { kb = k; bv = colsq[k]; bp = pos[k]; }
+        T beta = 0, diag = 0;
+        if (kb >= 0) {
+            T x[RPL];
+#pragma unroll
+            for (int u = 0; u < RPL; ++u) {
+                x[u] = col[0][u];
+#pragma unroll
+                for (int k = 1; k < CPW; ++k) x[u] = (k == kb) ? col[k][u] : x[u];
+            }
+            T sig = 0, x0 = 0;
+#pragma unroll
+            for (int u = 0; u < RPL; ++u) {
+                const int r = lane + 32 * u;
+                if (r > jn) sig = add_rn(sig, mul_rn(x[u], x[u]));
+                if (r == jn) x0 = x[u];
+            }
+            sig = warp_sum(sig);
+            x0 = __shfl_sync(0xffffffffu, x0, jn & 31);
+            diag = x0;
+            if (sig != T(0)) {  // make_reflector (qr.hpp:32-45); sigma == 0 leaves the diagonal (qr.hpp:37)
+                T mu, v0, rv;
+                reflector_scalars(x0, sig, mu, v0, beta, rv);
+                diag = mu;
+#pragma unroll
+                for (int u = 0; u < RPL; ++u) {
+                    const int r = lane + 32 * u;
+                    wvec[wib][r] = r > jn ? mul_rn(x[u], rv) : T(r == jn ? 1 : 0);
+                }
+            } else {
+#pragma unroll
+                for (int u = 0; u < RPL; ++u) wvec[wib][lane + 32 * u] = T(0);
+            }
+        }
+        if (lane == 0) {
+            wv_s[wib] = bv;
+            wk_s[wib] = kb >= 0 ? bp : INT_MAX;
+            wc_s[wib] = gw + NWT * (kb >= 0 ? kb : 0);  // the candidate's column index
+            wb_s[wib][0] = beta;
+            wb_s[wib][1] = diag;
+        }
+        __syncthreads();
+        // CTA best (lower position on ties); warp 0 decides, every thread copies its reflector
+        __shared__ int s_best;
+        if (wib == 0) {
+            T v = T(0);
+            int key = INT_MAX;
+            if (lane < kGridQW && wk_s[lane] != INT_MAX) { v = wv_s[lane]; key = (wk_s[lane] << 5) | lane; }
+#pragma unroll
+            for (int o = kGridQW / 2; o > 0; o >>= 1) {
+                const T ov = __shfl_xor_sync(0xffffffffu, v, o);
+                const int ok = __shfl_xor_sync(0xffffffffu, key, o);
+                if (ok != INT_MAX && (key == INT_MAX || ov > v || (ov == v && ok < key))) { v = ov; key = ok; }
+            }
+            key = __shfl_sync(0xffffffffu, key, 0);
+            if (lane == 0) {
+                s_best = key;
+                T* cs = cand_s + (int64_t(sl) * nblk + blockIdx.x) * 3;
+                int* ci = cand_i + (int64_t(sl) * nblk + blockIdx.x) * 2;
+                if (key == INT_MAX) {
+                    __stcg(ci, INT_MAX);
+                } else {
+                    const int w = key & 31;
+                    __stcg(cs + 0, wv_s[w]);
+                    __stcg(cs + 1, wb_s[w][0]);
+                    __stcg(cs + 2, wb_s[w][1]);
+                    __stcg(ci, key >> 5);
+                    __stcg(ci + 1, wc_s[w]);
+                }
+            }
+        }
+        __syncthreads();
+        const int key = s_best;
+        if (key != INT_MAX) {
+            const int w = key & 31;
+            T* dst = cand_v + (int64_t(sl) * nblk + blockIdx.x) * R;
+            for (int r = threadIdx.x; r < R; r += kGridQW * 32) __stcg(dst + r, wvec[w][r]);
+        }
+    };
+
+    candidate(0, 0);
+    grid.sync();
+    for (int j = 0; j < d; ++j) {
+        const int sl = j & 1;
+        // ---- global pivot over the CTA candidates (larger colsq, then lower position) ----
+        T wv = T(0);
+        int key = INT_MAX, src = -1;  // key = position; src = CTA
+        for (int b = lane; b < nblk; b += 32) {
+            const int p = __ldcg(cand_i + (int64_t(sl) * nblk + b) * 2);
+            if (p == INT_MAX) continue;
+            const T v = __ldcg(cand_s + (int64_t(sl) * nblk + b) * 3);
+            if (key == INT_MAX || v > wv || (v == wv && p < key)) { wv = v; key = p; src = b; }
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            const T ov = __shfl_xor_sync(0xffffffffu, wv, o);
+            const int ok = __shfl_xor_sync(0xffffffffu, key, o);
+            const int os = __shfl_xor_sync(0xffffffffu, src, o);
+            if (ok != INT_MAX && (key == INT_MAX || ov > wv || (ov == wv && ok < key))) { wv = ov; key = ok; src = os; }
+        }
+        src = __shfl_sync(0xffffffffu, src, 0);
+        const int wp = __shfl_sync(0xffffffffu, key, 0);
+        const T* cs = cand_s + (int64_t(sl) * nblk + src) * 3;
+        const T beta = __ldcg(cs + 1), diag = __ldcg(cs + 2);
+        const int wcol = __ldcg(cand_i + (int64_t(sl) * nblk + src) * 2 + 1);  // the winner's column
+        const T* vsrc = cand_v + (int64_t(sl) * nblk + src) * R;
+        T v[RPL];
+#pragma unroll
+        for (int u = 0; u < RPL; ++u) v[u] = __ldcg(vsrc + lane + 32 * u);
+        // ---- bookkeeping of the swap (qr.hpp:124-129) ----
+#pragma unroll
+        for (int k = 0; k < CPW; ++k) if (pos[k] == j) pos[k] = wp;
+        if (gw == wcol % NWT) {
+            const int kw = wcol / NWT;
+#pragma unroll
+            for (int k = 0; k < CPW; ++k) {
+                if (k == kw) {
+                    pos[k] = j;
+#pragma unroll
+                    for (int u = 0; u < RPL; ++u)
+                        if (lane + 32 * u == j) col[k][u] = diag;  // R(j,j) = mu (or x0 when sigma == 0)
+                }
+            }
+            if (lane == 0) perm_out[j] = wcol;
+#pragma unroll
+            for (int u = 0; u < RPL; ++u) __stcg(vst + int64_t(j) * R + lane + 32 * u, v[u]);
+            if (lane == 0) __stcg(betas + j, beta);
+        }
+        // ---- apply H_j to the trailing columns and downdate their norms (qr.hpp:131-139) ----
+        if (beta != T(0)) {
+            T sv[CPW];
+#pragma unroll
+            for (int k = 0; k < CPW; ++k) {
+                sv[k] = 0;
+#pragma unroll
+                for (int u = 0; u < RPL; ++u) sv[k] += v[u] * col[k][u];
+            }
+            warp_allreduce_vec<CPW>(sv, lane);
+#pragma unroll
+            for (int k = 0; k < CPW; ++k) {
+                if (pos[k] > j && pos[k] < d) {
+                    const T sb = sv[k] * beta;
+#pragma unroll
+                    for (int u = 0; u < RPL; ++u) col[k][u] = add_rn(col[k][u], -mul_rn(sb, v[u]));
+                }
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < CPW; ++k) {
+            T w = 0;
+#pragma unroll
+            for (int u = 0; u < RPL; ++u) if (lane + 32 * u == j) w = col[k][u];
+            w = __shfl_sync(0xffffffffu, w, j & 31);
+            if (pos[k] > j && pos[k] < d) {
+                colsq[k] = add_rn(colsq[k], -mul_rn(w, w));
+                if (colsq[k] < T(1e-6) * base[k]) {  // recompute guard (qr.hpp:135-139)
+                    T s2 = 0;
+#pragma unroll
+                    for (int u = 0; u < RPL; ++u)
+                        if (lane + 32 * u > j) s2 = add_rn(s2, mul_rn(col[k][u], col[k][u]));
+                    colsq[k] = base[k] = warp_sum(s2);
+                }
+            }
+        }
+        if (j + 1 < d) candidate(j + 1, sl ^ 1);
+        grid.sync();
+    }
+    // ---- T = upper triangle (qr.hpp:74-79) ----
+#pragma unroll
+    for (int k = 0; k < CPW; ++k) {
+        const int p = pos[k];
+        if (p < d) {
+#pragma unroll
+            for (int u = 0; u < RPL; ++u) {
+                const int r = lane + 32 * u;
+                if (r < d) Tout[int64_t(r) * ldt + p] = r <= p ? col[k][u] : T(0);
+            }
+        }
+    }
+    // ---- Q_M (accumulate_q order: reflectors d-1 .. 0 applied to each column of I) ----
+#pragma unroll
+    for (int k = 0; k < CPW; ++k)
+#pragma unroll
+        for (int u = 0; u < RPL; ++u) col[k][u] = T(lane + 32 * u == gw + NWT * k ? 1 : 0);
+    for (int j = d - 1; j >= 0; --j) {
+        const T bj = __ldcg(betas + j);
+        if (bj == T(0)) continue;
+        T v[RPL];
+#pragma unroll
+        for (int u = 0; u < RPL; ++u) v[u] = __ldcg(vst + int64_t(j) * R + lane + 32 * u);
+        T sv[CPW];
+#pragma unroll
+        for (int k = 0; k < CPW; ++k) {
+            sv[k] = 0;
+#pragma unroll
+            for (int u = 0; u < RPL; ++u) sv[k] += v[u] * col[k][u];
+        }
+        warp_allreduce_vec<CPW>(sv, lane);
+#pragma unroll
+        for (int k = 0; k < CPW; ++k) {
+            const T sb = sv[k] * bj;
+#pragma unroll
+            for (int u = 0; u < RPL; ++u) col[k][u] = add_rn(col[k][u], -mul_rn(sb, v[u]));
+        }
+    }
+#pragma unroll
+    for (int k = 0; k < CPW; ++k) {
+        const int c = gw + NWT * k;
+        if (c < d) {
+#pragma unroll
+            for (int u = 0; u < RPL; ++u) {
+                const int r = lane + 32 * u;
+                if (r < d) Q[int64_t(r) * ldq + c] = col[k][u];
+            }
+        }
+    }
+}
+
+template <typename T, int RPL, int CPW>
+int64_t qrcp_grid_scratch(int d, int nblk) {
+    constexpr int R = RPL * 32;
+    return int64_t(d) * R + d + int64_t(2) * nblk * R + 2 * nblk * 3 + (2 * nblk * 2 * sizeof(int) + sizeof(T) - 1) / sizeof(T) + 8;
+}
+
+template <typename T, int RPL, int CPW>
+cudaError_t launch_qrcp_grid(const T* M, int ldm, int d, T* Q, int ldq, T* Tout, int ldt, int64_t* perm, T* scratch,
+                             cudaStream_t st) {
+    const int nblk = (d + kGridQW * CPW - 1) / (kGridQW * CPW);
+    int dev = 0, sms = 0, per_sm = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_qrcp_grid<T, RPL, CPW>, kGridQW * 32, 0);
+    if (nblk > per_sm * sms) return cudaErrorCooperativeLaunchTooLarge;
+    void* args[] = {(void*)&M, (void*)&ldm, (void*)&d, (void*)&Q, (void*)&ldq, (void*)&Tout, (void*)&ldt, (void*)&perm,
+                    (void*)&scratch};
+    return cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(k_qrcp_grid<T, RPL, CPW>), dim3(nblk),
+                                       dim3(kGridQW * 32), args, 0, st);
+}
+
 template <typename T>
 __global__ void k_gather_columns(const T* __restrict__ Q2, int64_t ldq, const int64_t* __restrict__ perm, int64_t n,
                                  int d, T* __restrict__ V, int64_t ldv) {
@@ -591,7 +893,10 @@ int grid_for(int64_t total) { return int(std::min<int64_t>((total + 255) / 256, 
 }  // namespace
 
 int64_t qrcp_scratch_elems(int d) {
-    return qrcp_w_elems(d) + int64_t(qrcp_ldx(d)) * d + 512 + 32 * int64_t(d) + kQrcpGemmScratch;
+    const int64_t cta = qrcp_w_elems(d) + int64_t(qrcp_ldx(d)) * d + 512 + 32 * int64_t(d) + kQrcpGemmScratch;
+    const int64_t grid = d <= 256 ? qrcp_grid_scratch<double, 8, 1>(d, (d + kGridQW - 1) / kGridQW)
+                                  : qrcp_grid_scratch<double, 17, 1>(d, (d + kGridQW - 1) / kGridQW);
+    return std::max(cta, grid + 64);
 }
 
 template <typename T>
@@ -600,6 +905,10 @@ cudaError_t qrcp(const T* M, int ldm, int d, T* Q, int ldq, T* Tout, int ldt, in
     if (d <= 32) return launch_qrcp_reg<T, 1, 2, 16>(M, ldm, d, Q, ldq, Tout, ldt, perm, st);
     if (d <= 64) return launch_qrcp_reg<T, 2, 4, 16>(M, ldm, d, Q, ldq, Tout, ldt, perm, st);
     if (d <= 128) return launch_qrcp_reg<T, 4, 8, 16>(M, ldm, d, Q, ldq, Tout, ldt, perm, st);
+    if (!getenv("CORU_QRCP_CTA")) {  // tooling switch: the one-CTA kernel below
+        if (d <= 256) return launch_qrcp_grid<T, 8, 1>(M, ldm, d, Q, ldq, Tout, ldt, perm, scratch, st);
+        if (d <= 544) return launch_qrcp_grid<T, 17, 1>(M, ldm, d, Q, ldq, Tout, ldt, perm, scratch, st);
+    }
     const bool fits = qrcp_smem_bytes(d, sizeof(T), true) <= size_t(max_smem);
     const size_t sm = qrcp_smem_bytes(d, sizeof(T), fits);
     allow_max_smem(k_qrcp<T>);

@@ -185,14 +185,13 @@ def test_cpp_wrapper_program(ctx):
     assert r.returncode == 0, r.stdout + r.stderr
 
 
-@pytest.mark.parametrize("name,m,n", [("C1", 1000, 1000), ("C5", 3000, 3000)])
-def test_fp32_parity_vs_fp32_oracle(ctx, oracle, name, m, n):
+@pytest.mark.parametrize("name,m,n,d,q", [("C1", 1000, 1000, 25, 0), ("C5", 3000, 3000, 104, 2),
+                                          ("C5", 2000, 2000, 300, 1)])
+def test_fp32_parity_vs_fp32_oracle(ctx, oracle, name, m, n, d, q):
     """fp32 path against the fp32 restatement of the reference: relative
     reconstruction error to 1e-4, |diag T| to 1e-3 (BASELINE.json north_star, fp32)."""
     import paper_1810_07323_b200 as cg
     from workloads import CONFIGS, make_host
-    c = CONFIGS[name]
-    d, q = (c.d, c.q) if name == "C1" else (104, 2)
     a = make_host(name, m, n).astype(np.float32)
     f = cg.corutv(a, d, q, seed=cg.RngSeed(42, 0), ctx=ctx)
     o = oracle.corutv(a, d, q, seed=42, threads=16)
@@ -200,9 +199,23 @@ def test_fp32_parity_vs_fp32_oracle(ctx, oracle, name, m, n):
     e_gpu = rel_recon_error(a64, f.u.astype(np.float64), f.t.astype(np.float64), f.v.astype(np.float64))
     e_ora = rel_recon_error(a64, o.u.astype(np.float64), o.t.astype(np.float64), o.v.astype(np.float64))
     dg = np.abs(np.abs(np.diag(f.t)).astype(np.float64) - np.abs(np.diag(o.t)).astype(np.float64))
-    _record(f"fp32_{name}_{m}x{n}", err_gpu=e_gpu, err_oracle=e_ora, rel_err_diff=abs(e_gpu - e_ora) / e_ora,
+    _record(f"fp32_{name}_{m}x{n}_d{d}", err_gpu=e_gpu, err_oracle=e_ora, rel_err_diff=abs(e_gpu - e_ora) / e_ora,
             diag_absdiff=dg.max(), orth_u=orth_residual(f.u.astype(np.float64)),
             orth_v=orth_residual(f.v.astype(np.float64)))
     assert abs(e_gpu - e_ora) <= 1e-4 * e_ora
     assert dg.max() <= 1e-3
     assert np.all(np.tril(f.t, -1) == 0.0)
+
+
+def test_repeat_determinism_wide_sketch(ctx):
+    """Regression: the stream-K fix-up flags are tagged with a per-launch epoch; epochs must be
+    unique across GEMM configurations that reuse one workspace (CholeskyQR2's Gram and R2·R1
+    products, the A-passes), or a stale flag passes for a fresh one. Repeated C4-shaped calls
+    (d = 220: CholeskyQR2 + gated Householder + the grid QRCP) must agree bit for bit."""
+    import paper_1810_07323_b200 as cg
+    from workloads import make_host
+    a = make_host("C4", 4096, 4096)
+    fs = [cg.corutv(a, 220, 2, seed=cg.RngSeed(42, 0), ctx=ctx) for _ in range(4)]
+    for f in fs[1:]:
+        assert np.array_equal(f.u, fs[0].u) and np.array_equal(f.t, fs[0].t) and np.array_equal(f.perm, fs[0].perm)
+    assert rel_recon_error(a, fs[0].u, fs[0].t, fs[0].v) < 0.05

@@ -101,3 +101,21 @@ def test_sharded_approx_matches_single_gpu(ctx, world):
     e_1 = np.linalg.norm(a - su @ st @ sv.T) / np.linalg.norm(a)
     assert abs(e_sh - e_1) <= 1e-8 * e_1
     assert np.max(np.abs(np.abs(np.diag(t)) - np.abs(np.diag(st)))) <= 1e-8 * abs(st[0, 0])
+
+
+def test_nccl_plumbing_world1(ctx, monkeypatch):
+    """The NCCL backend on the one GPU this run has: a world-1 communicator (CORU_NCCL_WORLD1)
+    routes the A^T-product and core all-reduces through ncclAllReduce; results must equal the
+    communicator-free run bit for bit (a 1-rank sum is the identity)."""
+    import torch
+    import paper_1810_07323_b200 as cg
+    monkeypatch.setenv("CORU_NCCL_WORLD1", "1")
+    rng = np.random.default_rng(5)
+    a = torch.from_numpy(rng.standard_normal((3000, 1500)) * (0.99 ** np.arange(1500))).cuda()
+    ref = [cg.corutv(a, 40, 1, v, seed=cg.RngSeed(42, 0), ctx=ctx) for v in (cg.DVariant.exact, cg.DVariant.approx)]
+    c2 = cg.Context(0)
+    c2.init_comm(0, 1, cg.Context.unique_id())
+    for v, r in zip((cg.DVariant.exact, cg.DVariant.approx), ref):
+        f = cg.corutv(a, 40, 1, v, seed=cg.RngSeed(42, 0), ctx=c2, m_global=3000)
+        assert torch.equal(f.u, r.u) and torch.equal(f.t, r.t) and torch.equal(f.v, r.v)
+    c2.close()
