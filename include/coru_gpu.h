@@ -170,6 +170,25 @@ int coru_qrcp_f64_dev(coru_ctx* ctx, const double* M, int64_t ldm, int64_t n, do
  * NULL) = the number of Jacobi sweeps used, 0 when the 60-sweep cap was hit. */
 int coru_pinv_f64_dev(coru_ctx* ctx, const double* Y, int64_t ldy, int64_t n, double* P, int64_t ldp, int* converged);
 
+/* ---- SVD-based baselines that share the CoR-UTV kernels (baselines.hpp:43-71), fp64 ----------- */
+/* svd (svd.hpp:141-161) of a square n x n matrix: U, V (n x n), S[n] non-increasing (device);
+ * *converged (host, may be NULL) = Jacobi sweeps used, 0 when the 60-sweep cap was hit. */
+int coru_svd_f64_dev(coru_ctx* ctx, const double* Y, int64_t ldy, int64_t n, double* U, int64_t ldu, double* S,
+                     double* V, int64_t ldv, int* converged);
+/* tsr_svd(a, ell, seed) (baselines.hpp:43-56): U m x ell, S[ell], V n x ell; Φ1, Φ2 from the
+ * sub-streams (stream, stream + 1). EINVAL "tsr_svd: ell out of range" unless 1 <= ell < min(m, n). */
+int coru_tsr_svd_f64_dev(coru_ctx* ctx, const double* A, int64_t m, int64_t n, int64_t lda, int64_t ell, uint64_t seed,
+                         uint64_t stream, double* U, int64_t ldu, double* S, double* V, int64_t ldv, int* converged);
+int coru_tsr_svd_f64(coru_ctx* ctx, const double* A, int64_t m, int64_t n, int64_t ell, uint64_t seed, uint64_t stream,
+                     double* U, double* S, double* V, int* converged);
+/* sor_svd(a, k, ell, q, seed) (baselines.hpp:61-71): L (m x n) = Q1·trunc_k(svd(Q1^T A Q2))·Q2^T with
+ * corutv's sketch (same seed -> same Q1, Q2). EINVAL as the reference: ell (corutv's checks),
+ * 1 <= k <= ell, q >= 0. */
+int coru_sor_svd_f64_dev(coru_ctx* ctx, const double* A, int64_t m, int64_t n, int64_t lda, int64_t k, int64_t ell,
+                         int q, uint64_t seed, uint64_t stream, double* L, int64_t ldl);
+int coru_sor_svd_f64(coru_ctx* ctx, const double* A, int64_t m, int64_t n, int64_t k, int64_t ell, int q, uint64_t seed,
+                     uint64_t stream, double* L);
+
 /* A-pass profiling: when enabled, CUDA events are recorded on the launching stream around every
  * GEMM that streams the caller's A (the sketch, power and projection passes). The read call
  * returns the summed device time, the number of A-passes, and their algorithmic flops

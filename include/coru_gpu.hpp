@@ -70,6 +70,13 @@ struct UtvApprox {  // corutv.hpp:23-34
     std::vector<std::int64_t> perm;  // QRCP pivots of the core (extra)
 };
 
+struct SvdFactors {  // svd.hpp:17-22
+    Matrix u;
+    std::vector<double> sigma;
+    Matrix v;
+    bool converged = true;
+};
+
 struct SketchBases {  // corutv.hpp:42-47
     Matrix q1, q2, c1, c2_prev;
     bool conditioning_warning = false;
@@ -130,6 +137,26 @@ inline Matrix gaussian(std::size_t rows, std::size_t cols, RngSeed seed) {
     detail::throw_status(coru_gaussian(std::int64_t(rows), std::int64_t(cols), seed.seed, seed.stream,
                                        m.data().data(), 1));
     return m;
+}
+
+// tsr_svd (baselines.hpp:43-56)
+inline SvdFactors tsr_svd(const Matrix& a, std::size_t ell, RngSeed seed) {
+    SvdFactors f{Matrix(a.rows(), ell), std::vector<double>(ell), Matrix(a.cols(), ell), true};
+    int conv = 0;
+    detail::throw_status(coru_tsr_svd_f64(detail::thread_context(), a.data().data(), std::int64_t(a.rows()),
+                                          std::int64_t(a.cols()), std::int64_t(ell), seed.seed, seed.stream,
+                                          f.u.data().data(), f.sigma.data(), f.v.data().data(), &conv));
+    f.converged = conv != 0;
+    return f;
+}
+
+// sor_svd (baselines.hpp:61-71)
+inline Matrix sor_svd(const Matrix& a, std::size_t k, std::size_t ell, int q, RngSeed seed) {
+    Matrix out(a.rows(), a.cols());
+    detail::throw_status(coru_sor_svd_f64(detail::thread_context(), a.data().data(), std::int64_t(a.rows()),
+                                          std::int64_t(a.cols()), std::int64_t(k), std::int64_t(ell), q, seed.seed,
+                                          seed.stream, out.data().data()));
+    return out;
 }
 
 // singular_estimates (corutv.hpp:113-117)

@@ -64,6 +64,10 @@ class Oracle:
         L.oracle_xoshiro_words.argtypes = [_u64, _u64, _i64, _p]
         L.oracle_max_threads.restype = _int
         L.oracle_pinv_f64.argtypes = [_p, _i64, _p]
+        L.oracle_svd_square_f64.argtypes = [_p, _i64, _p, _p, _p]
+        L.oracle_svd_square_f64.restype = _int
+        L.oracle_tsr_svd_f64.argtypes = [_p, _i64, _i64, _i64, _u64, _u64, _int, _p, _p, _p, _p]
+        L.oracle_sor_svd_f64.argtypes = [_p, _i64, _i64, _i64, _i64, _int, _u64, _u64, _int, _p]
         L.oracle_jacobi_svd_square.argtypes = [_p, _i64, _p, _p, _p]
         L.oracle_jacobi_svd_square.restype = _int
         for sfx in ("f64", "f32"):
@@ -130,6 +134,29 @@ class Oracle:
         self.lib.oracle_pinv_f64(_ptr(a), n, _ptr(out))
         return out
 
+    def svd_square(self, a):
+        """svd (svd.hpp:141-161) of a square matrix: (u, sigma, v, converged)."""
+        a = np.ascontiguousarray(a, np.float64); n = a.shape[0]
+        u = np.empty((n, n)); v = np.empty((n, n)); s = np.empty(n)
+        conv = self.lib.oracle_svd_square_f64(_ptr(a), n, _ptr(u), _ptr(s), _ptr(v))
+        return u, s, v, bool(conv)
+
+    def tsr_svd(self, a, ell, seed, stream=0, threads=1):
+        """tsr_svd (baselines.hpp:43-56) -> (u, sigma, v, converged)."""
+        a = np.ascontiguousarray(a, np.float64); m, n = a.shape
+        u = np.empty((m, ell)); s = np.empty(ell); v = np.empty((n, ell)); conv = np.zeros(1, np.int32)
+        if self.lib.oracle_tsr_svd_f64(_ptr(a), m, n, ell, seed, stream, threads, _ptr(u), _ptr(s), _ptr(v), _ptr(conv)):
+            raise CoruError("tsr_svd: ell out of range")
+        return u, s, v, bool(conv[0])
+
+    def sor_svd(self, a, k, ell, q, seed, stream=0, threads=1):
+        """sor_svd (baselines.hpp:61-71) -> m x n."""
+        a = np.ascontiguousarray(a, np.float64); m, n = a.shape
+        out = np.empty((m, n))
+        if self.lib.oracle_sor_svd_f64(_ptr(a), m, n, k, ell, q, seed, stream, threads, _ptr(out)):
+            raise CoruError("sor_svd: bad parameters")
+        return out
+
     def jacobi_svd_square(self, a):
         """detail::jacobi_svd_square (svd.hpp:31-134) on a square a: (u, sigma, v, converged)."""
         a = np.ascontiguousarray(a, np.float64); n = a.shape[0]
@@ -176,6 +203,8 @@ class Reference:
         L.ref_qrcp.argtypes = [_p, _i64, _i64, _p, _p, _p]
         L.ref_svd.argtypes = [_p, _i64, _i64, _p, _p, _p, _p]
         L.ref_pinv.argtypes = [_p, _i64, _i64, _p]
+        L.ref_tsr_svd.argtypes = [_p, _i64, _i64, _i64, _u64, _u64, _p, _p, _p, _p]
+        L.ref_sor_svd.argtypes = [_p, _i64, _i64, _i64, _i64, _int, _u64, _u64, _p]
         L.ref_corutv.argtypes = [_p, _i64, _i64, _i64, _int, _int, _u64, _u64, _p, _p, _p, _p]
         L.ref_corutv_mt.argtypes = [_p, _i64, _i64, _i64, _int, _u64, _u64, _int, _p, _p, _p, _p]
         L.ref_sketch_bases.argtypes = [_p, _i64, _i64, _i64, _int, _u64, _u64, _p, _p, _p, _p, _p]
@@ -213,6 +242,18 @@ class Reference:
         u = np.empty((m, r)); s = np.empty(r); v = np.empty((n, r)); conv = np.zeros(1, np.int32)
         self._check(self.lib.ref_svd(_ptr(a), m, n, _ptr(u), _ptr(s), _ptr(v), _ptr(conv)))
         return u, s, v, bool(conv[0])
+
+    def tsr_svd(self, a, ell, seed, stream=0):
+        a = np.ascontiguousarray(a, np.float64); m, n = a.shape
+        u = np.empty((m, ell)); s = np.empty(ell); v = np.empty((n, ell)); conv = np.zeros(1, np.int32)
+        self._check(self.lib.ref_tsr_svd(_ptr(a), m, n, ell, seed, stream, _ptr(u), _ptr(s), _ptr(v), _ptr(conv)))
+        return u, s, v, bool(conv[0])
+
+    def sor_svd(self, a, k, ell, q, seed, stream=0):
+        a = np.ascontiguousarray(a, np.float64); m, n = a.shape
+        out = np.empty((m, n))
+        self._check(self.lib.ref_sor_svd(_ptr(a), m, n, k, ell, q, seed, stream, _ptr(out)))
+        return out
 
     def pinv(self, a):
         a = np.ascontiguousarray(a, np.float64); m, n = a.shape

@@ -5,7 +5,9 @@
  *   - RNG: SplitMix64 / xoshiro256++ / Box–Muller Gaussian  (rng.hpp:13-112)
  *   - matmul i-k-j                                           (matrix.hpp:115-131)
  *   - householder_qr, qrcp, reflector helpers                (qr.hpp:32-143)
- *   - sketch_bases, corutv exact-D                           (corutv.hpp:49-100)
+ *   - sketch_bases, corutv exact-D and approx-D                (corutv.hpp:49-100)
+ *   - Jacobi SVD, pinv                                        (svd.hpp:31-187)
+ *   - sor_svd, tsr_svd baselines                              (baselines.hpp:43-71)
  * It is the parity checker for the CUDA path: only tests/, __graft_entry__.smoke() and
  * bench.py's cpu_baseline leg may load it (as liboracle.so via oracle/__init__.py).
  * Parity of this restatement is pinned bit-for-bit against the compiled reference
@@ -244,4 +246,110 @@ int oracle_max_threads(void) {
 #else
     return 1;
 #endif
+}
+
+/* ---- SVD-based baselines (baselines.hpp), fp64 ------------------------------------------ */
+
+static double* transpose_copy(const double* a, int64_t m, int64_t n) {
+    double* t = (double*)malloc(sizeof(double) * (size_t)(m * n));
+    for (int64_t i = 0; i < m; ++i)
+        for (int64_t j = 0; j < n; ++j) t[j * m + i] = a[i * n + j];
+    return t;
+}
+
+/* svd (svd.hpp:141-161) of a square n×n row-major a: u, v row-major n×n, sigma[n]. */
+int oracle_svd_square_f64(const double* a, int64_t n, double* u, double* sigma, double* v) {
+    double* acm = transpose_copy(a, n, n); /* a_cm[j·n + i] = a(i, j) */
+    const int conv = oracle_jacobi_svd_square(acm, n, u, sigma, v);
+    free(acm);
+    return conv;
+}
+
+/* tsr_svd (baselines.hpp:43-56): u m×ell, sigma[ell], v n×ell; *conv = svd(b).converged.
+ * Returns 1 for the reference's invalid_argument (ell < 1 or ell >= min(m, n)). */
+int oracle_tsr_svd_f64(const double* a, int64_t m, int64_t n, int64_t ell, uint64_t seed, uint64_t stream,
+                       int threads, double* u, double* sigma, double* v, int* conv) {
+    if (ell < 1 || ell >= (m < n ? m : n)) return 1;
+    double* phi1 = (double*)malloc(sizeof(double) * (size_t)(n * ell));
+    double* phi2 = (double*)malloc(sizeof(double) * (size_t)(m * ell));
+    oracle_gaussian(n, ell, seed, stream, phi1);      /* substream(seed, 0) */
+    oracle_gaussian(m, ell, seed, stream + 1, phi2);  /* substream(seed, 1) */
+    double* y1 = (double*)malloc(sizeof(double) * (size_t)(m * ell));
+    double* y2 = (double*)malloc(sizeof(double) * (size_t)(n * ell));
+    mm_f64(a, m, n, phi1, ell, y1, threads);          /* matmul(a, phi1) */
+    mm_tn_f64(a, m, n, phi2, ell, y2, threads);       /* matmul(a.transposed(), phi2) */
+    double* q1 = (double*)malloc(sizeof(double) * (size_t)(m * ell));
+    double* q2 = (double*)malloc(sizeof(double) * (size_t)(n * ell));
+    oracle_householder_qr_f64(y1, m, ell, q1, NULL);
+    oracle_householder_qr_f64(y2, n, ell, q2, NULL);
+    double* t1 = (double*)malloc(sizeof(double) * (size_t)(ell * ell));
+    double* t2 = (double*)malloc(sizeof(double) * (size_t)(ell * ell));
+    double* p2 = (double*)malloc(sizeof(double) * (size_t)(ell * ell));
+    double* b = (double*)malloc(sizeof(double) * (size_t)(ell * ell));
+    mm_tn_f64(q1, m, ell, y1, ell, t1, threads);      /* f1.q^T · y1 */
+    mm_tn_f64(q2, n, ell, phi1, ell, t2, threads);    /* f2.q^T · phi1 */
+    oracle_pinv_f64(t2, ell, p2);
+    mm_f64(t1, ell, ell, p2, ell, b, 1);
+    double* bu = (double*)malloc(sizeof(double) * (size_t)(ell * ell));
+    double* bv = (double*)malloc(sizeof(double) * (size_t)(ell * ell));
+    const int c = oracle_svd_square_f64(b, ell, bu, sigma, bv);
+    if (conv) *conv = c;
+    mm_f64(q1, m, ell, bu, ell, u, threads);          /* matmul(f1.q, bs.u) */
+    mm_f64(q2, n, ell, bv, ell, v, threads);          /* matmul(f2.q, bs.v) */
+    free(phi1); free(phi2); free(y1); free(y2); free(q1); free(q2);
+    free(t1); free(t2); free(p2); free(b); free(bu); free(bv);
+    return 0;
+}
+
+/* sor_svd (baselines.hpp:61-71): out m×n = q1 · svd_truncate(svd(q1^T a q2), k) · q2^T.
+ * Returns 1 for the reference's invalid_argument cases. */
+int oracle_sor_svd_f64(const double* a, int64_t m, int64_t n, int64_t k, int64_t ell, int q, uint64_t seed,
+                       uint64_t stream, int threads, double* out) {
+    if (m < n) { /* sor_svd(a^T)^T (baselines.hpp:63-66) */
+        double* at = transpose_copy(a, m, n);
+        double* ot = (double*)malloc(sizeof(double) * (size_t)(m * n));
+        const int rc = oracle_sor_svd_f64(at, n, m, k, ell, q, seed, stream, threads, ot);
+        if (rc == 0)
+            for (int64_t i = 0; i < n; ++i)
+                for (int64_t j = 0; j < m; ++j) out[j * n + i] = ot[i * m + j];
+        free(at); free(ot);
+        return rc;
+    }
+    if (ell < 1 || ell >= n || k < 1 || k > ell || q < 0) return 1; /* :67-69 */
+    double* q1 = (double*)malloc(sizeof(double) * (size_t)(m * ell));
+    double* q2 = (double*)malloc(sizeof(double) * (size_t)(n * ell));
+    int warn = 0;
+    oracle_sketch_bases_f64(a, m, n, ell, q, seed, stream, threads, q1, q2, NULL, NULL, &warn);
+    /* d = matmul(matmul(q1^T, a), q2) */
+    double* q1ta = (double*)calloc((size_t)(ell * n), sizeof(double));
+    for (int64_t l = 0; l < ell; ++l) {
+        double* row = q1ta + l * n;
+        for (int64_t i = 0; i < m; ++i) {
+            const double w = q1[i * ell + l];
+            const double* ai = a + i * n;
+            for (int64_t j = 0; j < n; ++j) row[j] += w * ai[j];
+        }
+    }
+    double* d = (double*)malloc(sizeof(double) * (size_t)(ell * ell));
+    mm_f64(q1ta, ell, n, q2, ell, d, 1);
+    double* du = (double*)malloc(sizeof(double) * (size_t)(ell * ell));
+    double* dv = (double*)malloc(sizeof(double) * (size_t)(ell * ell));
+    double* sg = (double*)malloc(sizeof(double) * (size_t)ell);
+    oracle_svd_square_f64(d, ell, du, sg, dv);
+    /* svd_truncate (baselines.hpp:14-20): us(i,j) = u(i,j)·sigma_j, j < k; matmul(us, v.left_cols(k)^T) */
+    double* us = (double*)malloc(sizeof(double) * (size_t)(ell * k));
+    double* vkt = (double*)malloc(sizeof(double) * (size_t)(k * ell));
+    for (int64_t i = 0; i < ell; ++i)
+        for (int64_t j = 0; j < k; ++j) us[i * k + j] = du[i * ell + j] * sg[j];
+    for (int64_t j = 0; j < k; ++j)
+        for (int64_t i = 0; i < ell; ++i) vkt[j * ell + i] = dv[i * ell + j];
+    double* core = (double*)malloc(sizeof(double) * (size_t)(ell * ell));
+    mm_f64(us, ell, k, vkt, ell, core, 1);
+    double* t = (double*)malloc(sizeof(double) * (size_t)(m * ell));
+    mm_f64(q1, m, ell, core, ell, t, threads);        /* matmul(sb.q1, truncated) */
+    double* q2t = transpose_copy(q2, n, ell);         /* sb.q2.transposed() */
+    mm_f64(t, m, ell, q2t, n, out, threads);
+    free(q1); free(q2); free(q1ta); free(d); free(du); free(dv); free(sg); free(us); free(vkt);
+    free(core); free(t); free(q2t);
+    return 0;
 }

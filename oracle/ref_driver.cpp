@@ -17,6 +17,7 @@
 #include <thread>
 #include <vector>
 
+#include "coru/baselines.hpp"
 #include "coru/corutv.hpp"
 #include "coru/norms.hpp"
 #include "coru/testgen.hpp"
@@ -145,6 +146,28 @@ int ref_svd(const double* a, int64_t m, int64_t n, double* u, double* sigma, dou
 // coru::pinv(a) (svd.hpp:184-187): n×m.
 int ref_pinv(const double* a, int64_t m, int64_t n, double* out) {
     return guarded([&] { put(coru::pinv(wrap(a, m, n)), out); });
+}
+
+// coru::tsr_svd (baselines.hpp:43-56): u m×ell, sigma[ell], v n×ell, *conv.
+int ref_tsr_svd(const double* a, int64_t m, int64_t n, int64_t ell, uint64_t seed, uint64_t stream, double* u,
+                double* sigma, double* v, int* conv) {
+    return guarded([&] {
+        if (ell < 0) throw std::invalid_argument("tsr_svd: ell out of range");
+        coru::SvdFactors f = coru::tsr_svd(wrap(a, m, n), size_t(ell), {seed, stream});
+        put(f.u, u);
+        put(f.v, v);
+        for (size_t j = 0; j < f.sigma.size(); ++j) sigma[j] = f.sigma[j];
+        *conv = f.converged ? 1 : 0;
+    });
+}
+
+// coru::sor_svd (baselines.hpp:61-71): out m×n.
+int ref_sor_svd(const double* a, int64_t m, int64_t n, int64_t k, int64_t ell, int q, uint64_t seed, uint64_t stream,
+                double* out) {
+    return guarded([&] {
+        if (ell < 0 || k < 0) throw std::invalid_argument("sor_svd: bad parameters");
+        put(coru::sor_svd(wrap(a, m, n), size_t(k), size_t(ell), q, {seed, stream}), out);
+    });
 }
 
 // coru::corutv (corutv.hpp:79-100). u rows(a)×ell, t ell×ell, v cols(a)×ell.

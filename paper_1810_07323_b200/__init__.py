@@ -166,6 +166,11 @@ def load_library():
     L.coru_tsqr_f64_dev.argtypes = [p, p, i64, i64, i64, p, i64, p, i64]
     L.coru_qrcp_f64_dev.argtypes = [p, p, i64, i64, p, i64, p, i64, p]
     L.coru_pinv_f64_dev.argtypes = [p, p, i64, i64, p, i64, C.POINTER(i32)]
+    L.coru_svd_f64_dev.argtypes = [p, p, i64, i64, p, i64, p, p, i64, C.POINTER(i32)]
+    L.coru_tsr_svd_f64_dev.argtypes = [p, p, i64, i64, i64, i64, u64, u64, p, i64, p, p, i64, C.POINTER(i32)]
+    L.coru_tsr_svd_f64.argtypes = [p, p, i64, i64, i64, u64, u64, p, p, p, C.POINTER(i32)]
+    L.coru_sor_svd_f64_dev.argtypes = [p, p, i64, i64, i64, i64, i64, i32, u64, u64, p, i64]
+    L.coru_sor_svd_f64.argtypes = [p, p, i64, i64, i64, i64, i32, u64, u64, p]
     _lib = L
     return L
 
@@ -514,3 +519,68 @@ def pinv(mat, ctx: Optional[Context] = None):
     _torch_sync_stream(ctx, mat)
     _check(ctx.lib.coru_pinv_f64_dev(ctx.h, mat.data_ptr(), mat.stride(0), n, out.data_ptr(), n, C.byref(conv)))
     return out, int(conv.value)
+
+
+@dataclass
+class SvdFactors:
+    """SvdFactors (svd.hpp:17-22): u, sigma (non-increasing), v, converged."""
+    u: object
+    sigma: object
+    v: object
+    converged: bool
+
+
+def svd(mat, ctx: Optional[Context] = None) -> SvdFactors:
+    """svd (svd.hpp:141-161) of a square CUDA fp64 tensor (the Jacobi kernel of the approx-D core)."""
+    import torch
+    ctx = ctx or default_context(mat.device.index or 0)
+    n = mat.shape[0]
+    assert mat.shape == (n, n) and mat.dtype == torch.float64 and mat.is_cuda
+    u = torch.empty((n, n), dtype=torch.float64, device=mat.device)
+    v = torch.empty((n, n), dtype=torch.float64, device=mat.device)
+    s = torch.empty(n, dtype=torch.float64, device=mat.device)
+    conv = C.c_int(0)
+    _torch_sync_stream(ctx, mat)
+    _check(ctx.lib.coru_svd_f64_dev(ctx.h, mat.data_ptr(), mat.stride(0), n, u.data_ptr(), n, s.data_ptr(),
+                                    v.data_ptr(), n, C.byref(conv)))
+    return SvdFactors(u, s, v, conv.value > 0)
+
+
+def tsr_svd(a, ell: int, seed: RngSeed = RngSeed(), ctx: Optional[Context] = None) -> SvdFactors:
+    """tsr_svd(a, ell, seed) (baselines.hpp:43-56); numpy (host entry) or CUDA torch (device entry)."""
+    ctx = ctx or default_context()
+    m, n = a.shape
+    conv = C.c_int(0)
+    if _is_torch(a):
+        import torch
+        assert a.dtype == torch.float64
+        u = torch.empty((m, ell), dtype=torch.float64, device=a.device)
+        v = torch.empty((n, ell), dtype=torch.float64, device=a.device)
+        s = torch.empty(ell, dtype=torch.float64, device=a.device)
+        _torch_sync_stream(ctx, a)
+        _check(ctx.lib.coru_tsr_svd_f64_dev(ctx.h, a.data_ptr(), m, n, a.stride(0), ell, seed.seed, seed.stream,
+                                            u.data_ptr(), ell, s.data_ptr(), v.data_ptr(), ell, C.byref(conv)))
+        return SvdFactors(u, s, v, bool(conv.value))
+    a = np.ascontiguousarray(a, np.float64)
+    u = np.empty((m, ell)); s = np.empty(ell); v = np.empty((n, ell))
+    _check(ctx.lib.coru_tsr_svd_f64(ctx.h, a.ctypes.data, m, n, ell, seed.seed, seed.stream, u.ctypes.data,
+                                    s.ctypes.data, v.ctypes.data, C.byref(conv)))
+    return SvdFactors(u, s, v, bool(conv.value))
+
+
+def sor_svd(a, k: int, ell: int, q: int, seed: RngSeed = RngSeed(), ctx: Optional[Context] = None):
+    """sor_svd(a, k, ell, q, seed) (baselines.hpp:61-71) -> the m x n rank-k approximation."""
+    ctx = ctx or default_context()
+    m, n = a.shape
+    if _is_torch(a):
+        import torch
+        assert a.dtype == torch.float64
+        out = torch.empty((m, n), dtype=torch.float64, device=a.device)
+        _torch_sync_stream(ctx, a)
+        _check(ctx.lib.coru_sor_svd_f64_dev(ctx.h, a.data_ptr(), m, n, a.stride(0), k, ell, q, seed.seed, seed.stream,
+                                            out.data_ptr(), n))
+        return out
+    a = np.ascontiguousarray(a, np.float64)
+    out = np.empty((m, n))
+    _check(ctx.lib.coru_sor_svd_f64(ctx.h, a.ctypes.data, m, n, k, ell, q, seed.seed, seed.stream, out.ctypes.data))
+    return out

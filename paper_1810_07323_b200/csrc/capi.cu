@@ -816,6 +816,266 @@ int corutv_host(coru_ctx* c, const T* A, int64_t m, int64_t n, int64_t ell, int 
     return CORU_OK;
 }
 
+
+// ==== SVD-based baselines (baselines.hpp:43-71), fp64 =========================================
+__global__ void k_transpose_rect(const double* __restrict__ src, int64_t lds, int64_t rows, int cols,
+                                 double* __restrict__ dst, int64_t ldd) {
+    // dst (cols x rows) = src (rows x cols)^T
+    const int64_t total = rows * cols;
+    for (int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < total; e += int64_t(gridDim.x) * blockDim.x) {
+        const int c = int(e / rows);
+        const int64_t r = e - int64_t(c) * rows;
+        dst[int64_t(c) * ldd + r] = src[r * lds + c];
+    }
+}
+
+// Φ = gaussian(rows, d, {seed, stream}) into out (ld dp, zero padding), per the context's Φ mode.
+int fill_phi(coru_ctx* c, int64_t rows, int d, int dp, uint64_t seed, uint64_t stream, double* out) {
+    if (c->phi_mode == CORU_PHI_DEVICE) {
+        uint64_t s4[4];
+        seed_state_words(seed, stream, s4);
+        CORU_CUDA(gaussian_dev<double>(rows, d, s4, out, dp, c->stream));
+        ++g_launches;
+        return CORU_OK;
+    }
+    const size_t bytes = size_t(rows) * dp * sizeof(double);
+    CORU_TRY(ensure_pinned(c, bytes));
+    CORU_CUDA(cudaStreamSynchronize(c->stream));  // the pinned staging buffer is reused
+    double* phi = reinterpret_cast<double*>(c->pinned);
+    gaussian_host<double>(rows, d, seed, stream, phi, dp, c->host_threads, 1);
+    CORU_CUDA(cudaMemcpyAsync(out, phi, bytes, cudaMemcpyHostToDevice, c->stream));
+    return CORU_OK;
+}
+
+// tsr_svd (baselines.hpp:43-56): two sketches (A·Φ1, A^T·Φ2), their QRs (two streams), the core
+// (Q1^T Y1)·pinv(Q2^T Φ1), its Jacobi SVD, the lift. Device A, U (m x ell), V (n x ell), S (ell).
+int tsr_impl(coru_ctx* c, const double* A, int64_t m, int64_t n, int64_t lda, int d, uint64_t seed, uint64_t stream,
+             double* U, int64_t ldu, double* S, double* V, int64_t ldv, int* conv_host, size_t off,
+             size_t* need = nullptr) {
+    const int dp = int(round_up(d, 8));
+    const int sms = c->num_sms;
+    struct Lay {
+        double *phi1, *phi2, *y1, *y2, *q1, *q2, *gws, *r1, *r2, *t1, *t2, *p, *b, *bu, *bv, *sig, *pws;
+        int* conv;
+        int64_t gwse;
+        TsqrBufs<double> ts1, ts2;
+    } l;
+    auto lay = [&](Carver& cv) {
+        l.phi1 = cv.take<double>(n * dp);
+        l.phi2 = cv.take<double>(m * dp);
+        l.y1 = cv.take<double>(m * dp);
+        l.y2 = cv.take<double>(n * dp);
+        l.q1 = cv.take<double>(m * dp);
+        l.q2 = cv.take<double>(n * dp);
+        l.gwse = std::max({gemm_ws<double>(Op::N, m, n, d, sms), gemm_ws<double>(Op::T, n, m, d, sms),
+                           gemm_ws<double>(Op::T, d, m, d, sms), gemm_ws<double>(Op::T, d, n, d, sms),
+                           gemm_ws<double>(Op::N, m, d, d, sms), gemm_ws<double>(Op::N, n, d, d, sms),
+                           gemm_ws<double>(Op::N, d, d, d, sms)});
+        l.gws = cv.take<double>(l.gwse);
+        l.ts1.carve(cv, m, d, c->max_smem, sms, c->wide_qr);
+        l.ts2.carve(cv, n, d, c->max_smem, sms, c->wide_qr);
+        l.r1 = cv.take<double>(int64_t(d) * d);
+        l.r2 = cv.take<double>(int64_t(d) * d);
+        l.t1 = cv.take<double>(int64_t(d) * dp);
+        l.t2 = cv.take<double>(int64_t(d) * dp);
+        l.p = cv.take<double>(int64_t(d) * dp);
+        l.b = cv.take<double>(int64_t(d) * dp);
+        l.bu = cv.take<double>(int64_t(d) * dp);
+        l.bv = cv.take<double>(int64_t(d) * dp);
+        l.sig = cv.take<double>(d);
+        l.pws = cv.take<double>(pinv_ws_doubles(d));
+        l.conv = cv.take<int>(4);
+    };
+    Carver meas{nullptr, off};
+    lay(meas);
+    if (need) {  // sizing pass: the caller reserves the arena before placing anything in it
+        *need = meas.off;
+        return CORU_OK;
+    }
+    CORU_TRY(ensure_arena(c, meas.off));
+    Carver cv{c->arena, off};
+    lay(cv);
+    cudaStream_t st = c->stream;
+    CORU_TRY(fill_phi(c, n, d, dp, seed, stream, l.phi1));      // substream(seed, 0)
+    CORU_TRY(fill_phi(c, m, d, dp, seed, stream + 1, l.phi2));  // substream(seed, 1)
+    CORU_CUDA(cudaMemsetAsync(l.q1, 0, size_t(m) * dp * sizeof(double), st));
+    CORU_CUDA(cudaMemsetAsync(l.q2, 0, size_t(n) * dp * sizeof(double), st));
+    // y1 = A·Φ1, y2 = A^T·Φ2 (A^T never formed)
+    CORU_TRY(gemm<double>(c, Op::N, A, lda, l.phi1, dp, l.y1, dp, m, n, d, l.gws, l.gwse));
+    CORU_TRY(gemm<double>(c, Op::T, A, lda, l.phi2, dp, l.y2, dp, n, m, d, l.gws, l.gwse));
+    CORU_CUDA(cudaEventRecord(c->ev_fork, st));
+    CORU_CUDA(cudaStreamWaitEvent(c->aux, c->ev_fork, 0));
+    CORU_TRY(l.ts1.factor(l.y1, dp, l.r1, c->aux));
+    CORU_TRY(l.ts1.form_q(nullptr, l.q1, dp, c->aux));
+    CORU_TRY(l.ts2.factor(l.y2, dp, l.r2, st));
+    CORU_TRY(l.ts2.form_q(nullptr, l.q2, dp, st));
+    CORU_CUDA(cudaEventRecord(c->ev_join, c->aux));
+    CORU_CUDA(cudaStreamWaitEvent(st, c->ev_join, 0));
+    const bool prof = c->prof;  // the rest are d-wide products, not A-passes
+    c->prof = false;
+    int rc = gemm<double>(c, Op::T, l.q1, dp, l.y1, dp, l.t1, dp, d, m, d, l.gws, l.gwse);      // Q1^T·y1
+    if (rc == CORU_OK) rc = gemm<double>(c, Op::T, l.q2, dp, l.phi1, dp, l.t2, dp, d, n, d, l.gws, l.gwse);  // Q2^T·Φ1
+    if (rc == CORU_OK) {
+        const cudaError_t e = pinv_square<double>(l.t2, dp, d, l.p, dp, l.pws, nullptr, c->max_smem, st);
+        if (e != cudaSuccess) rc = fail(CORU_ECUDA, std::string("pinv_square: ") + cudaGetErrorString(e));
+        g_launches += kPinvLaunches;
+    }
+    if (rc == CORU_OK) rc = gemm<double>(c, Op::N, l.t1, dp, l.p, dp, l.b, dp, d, d, d, l.gws, l.gwse);
+    if (rc == CORU_OK) {
+        const cudaError_t e = svd_square<double>(l.b, dp, d, l.bu, dp, l.sig, l.bv, dp, l.pws, l.conv, c->max_smem, st);
+        if (e != cudaSuccess) rc = fail(CORU_ECUDA, std::string("svd_square: ") + cudaGetErrorString(e));
+        g_launches += kSvdLaunches;
+    }
+    if (rc == CORU_OK) rc = gemm<double>(c, Op::N, l.q1, dp, l.bu, dp, U, ldu, m, d, d, l.gws, l.gwse);
+    if (rc == CORU_OK) rc = gemm<double>(c, Op::N, l.q2, dp, l.bv, dp, V, ldv, n, d, d, l.gws, l.gwse);
+    c->prof = prof;
+    CORU_TRY(rc);
+    CORU_CUDA(cudaMemcpyAsync(S, l.sig, sizeof(double) * d, cudaMemcpyDeviceToDevice, st));
+    int conv = 0;
+    CORU_CUDA(cudaMemcpyAsync(&conv, l.conv, sizeof(int), cudaMemcpyDeviceToHost, st));
+    CORU_CUDA(cudaStreamSynchronize(st));
+    if (conv_host) *conv_host = conv > 0 ? 1 : 0;
+    return CORU_OK;
+}
+
+int check_tsr(int64_t m, int64_t n, int64_t ell) {
+    if (m < 1 || n < 1) return fail(CORU_EINVAL, "Matrix: dimensions must be positive");
+    if (ell < 1 || ell >= std::min(m, n)) return fail(CORU_EINVAL, "tsr_svd: ell out of range");
+    return CORU_OK;
+}
+
+int check_sor(int64_t m, int64_t n, int64_t k, int64_t ell, int q) {
+    if (m < 1 || n < 1) return fail(CORU_EINVAL, "Matrix: dimensions must be positive");
+    // m < n recurses on the transpose (baselines.hpp:63-66), which has the same min(rows, cols)
+    if (ell < 1) return fail(CORU_EINVAL, "corutv: ell must be >= 1");
+    if (ell >= std::min(m, n)) return fail(CORU_EINVAL, "corutv: ell must be < min(rows, cols)");
+    if (k < 1 || k > ell) return fail(CORU_EINVAL, "sor_svd: requires 1 <= k <= ell");
+    if (q < 0) return fail(CORU_EINVAL, "sor_svd: q must be >= 0");
+    return CORU_OK;
+}
+
+// sor_svd (baselines.hpp:61-71): the CoR sketch stage, the exact core D = Q1^T A Q2, its Jacobi SVD
+// truncated to rank k, lifted to the m x n output L = Q1·C·Q2^T. For m < n the reference works on
+// A^T and transposes the result; here A^T is a flag and L = Q2'·C^T·Q1'^T is written directly.
+int sor_impl(coru_ctx* c, const double* A, int64_t m, int64_t n, int64_t lda, int k, int d, int q, uint64_t seed,
+             uint64_t stream, double* Lout, int64_t ldl, size_t off, size_t* need = nullptr) {
+    const bool trans = m < n;
+    const int64_t R = trans ? n : m, N = trans ? m : n;
+    const int dp = int(round_up(d, 8));
+    const int sms = c->num_sms;
+    const Op op_a = trans ? Op::T : Op::N;
+    const int64_t mX = trans ? N : R, nY = trans ? R : N;  // L = X·C·Y^T, X mX x d, Y nY x d
+    struct Lay {
+        double *q1, *q2, *w, *dm, *du, *dv, *sig, *core, *coret, *t, *yt, *gws, *pws;
+        int* conv;
+        int64_t gwse;
+    } l;
+    auto lay = [&](Carver& cv) {
+        l.q1 = cv.take<double>(R * dp);
+        l.q2 = cv.take<double>(N * dp);
+        l.w = cv.take<double>(R * dp);
+        l.dm = cv.take<double>(int64_t(d) * dp);
+        l.du = cv.take<double>(int64_t(d) * dp);
+        l.dv = cv.take<double>(int64_t(d) * dp);
+        l.sig = cv.take<double>(d);
+        l.core = cv.take<double>(int64_t(d) * dp);
+        l.coret = cv.take<double>(int64_t(d) * dp);
+        l.t = cv.take<double>(mX * dp);
+        l.yt = cv.take<double>(int64_t(d) * nY);
+        l.gwse = std::max({gemm_ws<double>(op_a, R, N, d, sms), gemm_ws<double>(Op::T, d, R, d, sms),
+                           gemm_ws<double>(Op::N, mX, d, d, sms), gemm_ws<double>(Op::N, mX, d, int(nY), sms)});
+        l.gws = cv.take<double>(l.gwse);
+        l.pws = cv.take<double>(pinv_ws_doubles(d));
+        l.conv = cv.take<int>(4);
+    };
+    Carver meas{nullptr, off};
+    lay(meas);
+    const size_t work_off = (meas.off + 255) / 256 * 256;
+    {
+        // the sketch stage carves its workspace after ours: size the arena for both up front
+        Request<double> probe;
+        probe.rows = R;
+        probe.cols = N;
+        probe.d = d;
+        probe.mode = Mode::Sketch;
+        Work<double> w;
+        Carver wm{nullptr, work_off};
+        w.layout(wm, c, probe, dp);
+        if (need) {
+            *need = wm.off;
+            return CORU_OK;
+        }
+        CORU_TRY(ensure_arena(c, wm.off));
+    }
+    Carver cv{c->arena, off};
+    lay(cv);
+    Request<double> r;  // detail::sketch_bases(a, ell, q, seed) (baselines.hpp:69)
+    r.A = A;
+    r.lda = lda;
+    r.trans = trans;
+    r.rows = R;
+    r.cols = N;
+    r.d = d;
+    r.q = q;
+    r.seed = seed;
+    r.stream = stream;
+    r.mode = Mode::Sketch;
+    r.q1 = l.q1;
+    r.ldq1 = dp;
+    r.q2 = l.q2;
+    r.ldq2 = dp;
+    int warn = 0;
+    r.warn_host = &warn;
+    CORU_TRY(run<double>(c, r, work_off));
+    cudaStream_t st = c->stream;
+    CORU_CUDA(cudaMemsetAsync(l.core, 0, size_t(d) * dp * sizeof(double), st));
+    // D = (Q1^T a) q2 (baselines.hpp:70) as Q1^T (A'·Q2)
+    CORU_TRY(gemm<double>(c, op_a, A, lda, l.q2, dp, l.w, dp, R, N, d, l.gws, l.gwse));
+    const bool prof = c->prof;
+    c->prof = false;
+    int rc = gemm<double>(c, Op::T, l.q1, dp, l.w, dp, l.dm, dp, d, R, d, l.gws, l.gwse);
+    if (rc == CORU_OK) {
+        cudaError_t e = svd_square<double>(l.dm, dp, d, l.du, dp, l.sig, l.dv, dp, l.pws, l.conv, c->max_smem, st);
+        if (e == cudaSuccess) e = svd_truncate_core<double>(l.pws, d, k, l.core, dp, st);
+        if (e != cudaSuccess) rc = fail(CORU_ECUDA, std::string("svd: ") + cudaGetErrorString(e));
+        g_launches += kSvdLaunches + 1;
+    }
+    const double* X = trans ? l.q2 : l.q1;
+    const double* Y = trans ? l.q1 : l.q2;
+    const double* Cm = l.core;
+    if (rc == CORU_OK && trans) {
+        const cudaError_t e = transpose_square<double>(l.core, dp, l.coret, dp, d, st);
+        if (e != cudaSuccess) rc = fail(CORU_ECUDA, cudaGetErrorString(e));
+        ++g_launches;
+        Cm = l.coret;
+    }
+    if (rc == CORU_OK) rc = gemm<double>(c, Op::N, X, dp, Cm, dp, l.t, dp, mX, d, d, l.gws, l.gwse);
+    if (rc == CORU_OK) {
+        const int blocks = int(std::min<int64_t>((nY * d + 255) / 256, int64_t(sms) * 16));
+        k_transpose_rect<<<std::max(blocks, 1), 256, 0, st>>>(Y, dp, nY, d, l.yt, nY);
+        ++g_launches;
+        const cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) rc = fail(CORU_ECUDA, cudaGetErrorString(e));
+    }
+    if (rc == CORU_OK) rc = gemm<double>(c, Op::N, l.t, dp, l.yt, nY, Lout, ldl, mX, d, int(nY), l.gws, l.gwse);
+    c->prof = prof;
+    CORU_TRY(rc);
+    CORU_CUDA(cudaStreamSynchronize(st));
+    return CORU_OK;
+}
+
+// Upload a host matrix into the arena head (validating finiteness like the Matrix constructor).
+int upload_checked(coru_ctx* c, const double* A, int64_t count, double* a_d, int* f_d) {
+    cudaStream_t st = c->stream;
+    CORU_CUDA(cudaMemcpyAsync(a_d, A, sizeof(double) * count, cudaMemcpyHostToDevice, st));
+    CORU_CUDA(any_nonfinite<double>(a_d, count, f_d, st));
+    ++g_launches;
+    int bad = 0;
+    CORU_CUDA(cudaMemcpyAsync(&bad, f_d, sizeof(int), cudaMemcpyDeviceToHost, st));
+    CORU_CUDA(cudaStreamSynchronize(st));
+    if (bad) return fail(CORU_EINVAL, "Matrix: non-finite entry");
+    return CORU_OK;
+}
 }  // namespace
 
 // ==== exported C-ABI =========================================================================
@@ -1204,6 +1464,115 @@ int coru_pinv_f64_dev(coru_ctx* c, const double* Y, int64_t ldy, int64_t n, doub
     CORU_CUDA(cudaMemcpyAsync(&conv, conv_d, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
     CORU_CUDA(cudaStreamSynchronize(c->stream));
     if (converged) *converged = conv;
+    return CORU_OK;
+}
+
+
+/* ---- SVD-based baselines (baselines.hpp:43-71) ---------------------------------------------- */
+int coru_svd_f64_dev(coru_ctx* c, const double* Y, int64_t ldy, int64_t n, double* U, int64_t ldu, double* S,
+                     double* V, int64_t ldv, int* converged) {
+    CORU_TRY(enter(c));
+    std::lock_guard<std::mutex> lk(c->mu);
+    if (n < 1 || ldy < n || ldu < n || ldv < n || !Y || !U || !S || !V) return fail(CORU_EINVAL, "svd: bad shape");
+    CORU_TRY(ensure_arena(c, size_t(pinv_ws_doubles(int(n))) * sizeof(double) + 256));
+    double* ws = reinterpret_cast<double*>(c->arena);
+    int* conv_d = reinterpret_cast<int*>(ws + pinv_ws_doubles(int(n)));
+    CORU_CUDA(svd_square<double>(Y, ldy, int(n), U, ldu, S, V, ldv, ws, conv_d, c->max_smem, c->stream));
+    g_launches += kSvdLaunches;
+    int conv = 0;
+    CORU_CUDA(cudaMemcpyAsync(&conv, conv_d, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+    CORU_CUDA(cudaStreamSynchronize(c->stream));
+    if (converged) *converged = conv;
+    return CORU_OK;
+}
+
+int coru_tsr_svd_f64_dev(coru_ctx* c, const double* A, int64_t m, int64_t n, int64_t lda, int64_t ell, uint64_t seed,
+                         uint64_t stream, double* U, int64_t ldu, double* S, double* V, int64_t ldv, int* converged) {
+    CORU_TRY(enter(c));
+    std::lock_guard<std::mutex> lk(c->mu);
+    CORU_TRY(check_tsr(m, n, ell));
+    if (!A || !U || !S || !V || lda < n) return fail(CORU_EINVAL, "bad argument");
+    if (c->world > 1) return fail(CORU_EINVAL, "tsr_svd: single-GPU entry");
+    size_t need = 0;
+    CORU_TRY(tsr_impl(c, A, m, n, lda, int(ell), seed, stream, U, ldu, S, V, ldv, converged, 0, &need));
+    CORU_TRY(ensure_arena(c, need));
+    return tsr_impl(c, A, m, n, lda, int(ell), seed, stream, U, ldu, S, V, ldv, converged, 0);
+}
+
+int coru_tsr_svd_f64(coru_ctx* c, const double* A, int64_t m, int64_t n, int64_t ell, uint64_t seed, uint64_t stream,
+                     double* U, double* S, double* V, int* converged) {
+    CORU_TRY(enter(c));
+    std::lock_guard<std::mutex> lk(c->mu);
+    CORU_TRY(check_tsr(m, n, ell));
+    if (!A || !U || !S || !V) return fail(CORU_EINVAL, "null argument");
+    if (c->world > 1) return fail(CORU_EINVAL, "host-buffer entry is single-GPU");
+    Carver head{nullptr, 0};
+    double *a_d, *u_d, *s_d, *v_d;
+    int* f_d;
+    auto lay = [&](Carver& cv) {
+        a_d = cv.take<double>(m * n);
+        u_d = cv.take<double>(m * ell);
+        s_d = cv.take<double>(ell);
+        v_d = cv.take<double>(n * ell);
+        f_d = cv.take<int>(4);
+    };
+    lay(head);
+    const size_t hb = (head.off + 255) / 256 * 256;
+    size_t need = 0;
+    CORU_TRY(tsr_impl(c, nullptr, m, n, n, int(ell), seed, stream, nullptr, ell, nullptr, nullptr, ell, nullptr, hb,
+                      &need));
+    CORU_TRY(ensure_arena(c, need));
+    Carver cv{c->arena, 0};
+    lay(cv);
+    CORU_TRY(upload_checked(c, A, m * n, a_d, f_d));
+    CORU_TRY(tsr_impl(c, a_d, m, n, n, int(ell), seed, stream, u_d, ell, s_d, v_d, ell, converged, hb));
+    cudaStream_t st = c->stream;
+    CORU_CUDA(cudaMemcpyAsync(U, u_d, sizeof(double) * m * ell, cudaMemcpyDeviceToHost, st));
+    CORU_CUDA(cudaMemcpyAsync(S, s_d, sizeof(double) * ell, cudaMemcpyDeviceToHost, st));
+    CORU_CUDA(cudaMemcpyAsync(V, v_d, sizeof(double) * n * ell, cudaMemcpyDeviceToHost, st));
+    CORU_CUDA(cudaStreamSynchronize(st));
+    return CORU_OK;
+}
+
+int coru_sor_svd_f64_dev(coru_ctx* c, const double* A, int64_t m, int64_t n, int64_t lda, int64_t k, int64_t ell,
+                         int q, uint64_t seed, uint64_t stream, double* L, int64_t ldl) {
+    CORU_TRY(enter(c));
+    std::lock_guard<std::mutex> lk(c->mu);
+    CORU_TRY(check_sor(m, n, k, ell, q));
+    if (!A || !L || lda < n || ldl < n) return fail(CORU_EINVAL, "bad argument");
+    if (c->world > 1) return fail(CORU_EINVAL, "sor_svd: single-GPU entry");
+    size_t need = 0;
+    CORU_TRY(sor_impl(c, A, m, n, lda, int(k), int(ell), q, seed, stream, L, ldl, 0, &need));
+    CORU_TRY(ensure_arena(c, need));
+    return sor_impl(c, A, m, n, lda, int(k), int(ell), q, seed, stream, L, ldl, 0);
+}
+
+int coru_sor_svd_f64(coru_ctx* c, const double* A, int64_t m, int64_t n, int64_t k, int64_t ell, int q, uint64_t seed,
+                     uint64_t stream, double* L) {
+    CORU_TRY(enter(c));
+    std::lock_guard<std::mutex> lk(c->mu);
+    CORU_TRY(check_sor(m, n, k, ell, q));
+    if (!A || !L) return fail(CORU_EINVAL, "null argument");
+    if (c->world > 1) return fail(CORU_EINVAL, "host-buffer entry is single-GPU");
+    Carver head{nullptr, 0};
+    double *a_d, *l_d;
+    int* f_d;
+    auto lay = [&](Carver& cv) {
+        a_d = cv.take<double>(m * n);
+        l_d = cv.take<double>(m * n);
+        f_d = cv.take<int>(4);
+    };
+    lay(head);
+    const size_t hb = (head.off + 255) / 256 * 256;
+    size_t need = 0;
+    CORU_TRY(sor_impl(c, nullptr, m, n, n, int(k), int(ell), q, seed, stream, nullptr, n, hb, &need));
+    CORU_TRY(ensure_arena(c, need));
+    Carver cv{c->arena, 0};
+    lay(cv);
+    CORU_TRY(upload_checked(c, A, m * n, a_d, f_d));
+    CORU_TRY(sor_impl(c, a_d, m, n, n, int(k), int(ell), q, seed, stream, l_d, n, hb));
+    CORU_CUDA(cudaMemcpyAsync(L, l_d, sizeof(double) * m * n, cudaMemcpyDeviceToHost, c->stream));
+    CORU_CUDA(cudaStreamSynchronize(c->stream));
     return CORU_OK;
 }
 

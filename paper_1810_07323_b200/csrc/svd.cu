@@ -27,9 +27,12 @@ namespace {
 constexpr int kJacThreadsMax = 1024;
 constexpr int kMaxSweeps = 60;  // svd.hpp:35
 
+// Workspace. After the sweeps, column r of the sorted factorisation is stored contiguously:
+//   pinv mode: vs[r] = v(:, src)/sigma (kept r only), ut[r] = a(:, src)/sigma = u(:, r)
+//   svd mode:  vs[r] = v(:, src), ut[r] = u(:, r) (0 where sigma == 0, completed later), sig[r]
 struct PinvWs {
-    double *a, *v, *vs, *ut, *rank, *sq;  // rank[0] = kept rank; sq: squared norms (grid kernel)
-    int *rot, *ord;                       // grid kernel: per-sweep "rotated" flags, sort order
+    double *a, *v, *vs, *ut, *rank, *sq, *sig;  // rank[0] = kept rank; sq: squared norms (grid kernel)
+    int *rot, *ord;                             // grid kernel: per-sweep "rotated" flags, sort order
     __host__ __device__ PinvWs(double* ws, int d) {
         const int64_t dd = int64_t(d) * d;
         a = ws;
@@ -38,7 +41,8 @@ struct PinvWs {
         ut = vs + dd;
         rank = ut + dd;
         sq = rank + 8;
-        rot = reinterpret_cast<int*>(sq + d);
+        sig = sq + d;
+        rot = reinterpret_cast<int*>(sig + d);
         ord = rot + kMaxSweeps;
     }
 };
@@ -66,7 +70,8 @@ __device__ __forceinline__ double group_sum(double v) {
 // round); E = 0: columns in the global workspace (wide cores), streamed per loop.
 template <typename T, int G, int E>
 __global__ void __launch_bounds__(E > 0 ? 512 : kJacThreadsMax, 1)
-    k_jacobi_svd(const T* __restrict__ Y, int64_t ldy, int d, double* ws, int cols_in_smem, int* converged_out) {
+    k_jacobi_svd(const T* __restrict__ Y, int64_t ldy, int d, double* ws, int cols_in_smem, int* converged_out,
+                 int svd_mode) {
     constexpr int kPairsPerWarp = kWarp / G;
     const int kJacThreads = blockDim.x, kJacWarps = kJacThreads >> 5;
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -226,10 +231,18 @@ __global__ void __launch_bounds__(E > 0 ? 512 : kJacThreadsMax, 1)
     for (int r = warp; r < d; r += kJacWarps) {
         const int src = ord[r];
         const double sigma = sqrt(sq[src]);
-        const double inv = sigma > cut ? 1.0 / sigma : 0.0;
-        if (inv == 0.0) continue;
         const double* vc = v + int64_t(src) * d;
         const double* ac = a + int64_t(src) * d;
+        if (svd_mode) {  // svd.hpp:84-95
+            for (int i = lane; i < d; i += kWarp) {
+                w.vs[int64_t(r) * d + i] = vc[i];
+                w.ut[int64_t(r) * d + i] = sigma > 0.0 ? ac[i] / sigma : 0.0;
+            }
+            if (lane == 0) w.sig[r] = sigma;
+            continue;
+        }
+        const double inv = sigma > cut ? 1.0 / sigma : 0.0;
+        if (inv == 0.0) continue;
         for (int i = lane; i < d; i += kWarp) {
             w.vs[int64_t(r) * d + i] = vc[i] * inv;
             w.ut[int64_t(r) * d + i] = ac[i] / sigma;
@@ -251,7 +264,7 @@ constexpr int kGridE = 17;
 constexpr int kGridWarps = 4;
 template <typename T>
 __global__ void __launch_bounds__(kGridWarps * 32)
-    k_jacobi_grid(const T* __restrict__ Y, int64_t ldy, int d, double* ws, int* converged_out) {
+    k_jacobi_grid(const T* __restrict__ Y, int64_t ldy, int d, double* ws, int* converged_out, int svd_mode) {
     namespace cgs = cooperative_groups;
     cgs::grid_group grid = cgs::this_grid();
     PinvWs w(ws, d);
@@ -368,10 +381,18 @@ __global__ void __launch_bounds__(kGridWarps * 32)
     for (int r = gw; r < d; r += nw) {
         const int src = __ldcg(w.ord + r);
         const double sigma = sqrt(__ldcg(w.sq + src));
-        const double inv = sigma > cut ? 1.0 / sigma : 0.0;
-        if (inv == 0.0) continue;
         const double* vc = v + int64_t(src) * d;
         const double* ac = a + int64_t(src) * d;
+        if (svd_mode) {  // svd.hpp:84-95
+            for (int i = lane; i < d; i += kWarp) {
+                w.vs[int64_t(r) * d + i] = __ldcg(vc + i);
+                w.ut[int64_t(r) * d + i] = sigma > 0.0 ? __ldcg(ac + i) / sigma : 0.0;
+            }
+            if (lane == 0) w.sig[r] = sigma;
+            continue;
+        }
+        const double inv = sigma > cut ? 1.0 / sigma : 0.0;
+        if (inv == 0.0) continue;
         for (int i = lane; i < d; i += kWarp) {
             w.vs[int64_t(r) * d + i] = __ldcg(vc + i) * inv;
             w.ut[int64_t(r) * d + i] = __ldcg(ac + i) / sigma;
@@ -419,13 +440,121 @@ __global__ void __launch_bounds__(256) k_pinv_assemble(const double* ws, int d, 
     }
 }
 
+
+// svd mode, after the sweeps: complete the u columns of zero singular values from the canonical
+// basis (svd.hpp:98-121: for each candidate e_i two Gram-Schmidt passes against the earlier
+// columns, the largest residual wins, the first on ties), then write U, sigma, V row-major.
+template <typename T>
+__global__ void __launch_bounds__(1024) k_svd_finalize(double* ws, int d, T* U, int64_t ldu, T* sigma, T* V,
+                                                       int64_t ldv) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    double* cand = reinterpret_cast<double*>(smem_raw);  // [32 warps][d]
+    __shared__ double s_res[32];
+    __shared__ int s_e[32];
+    PinvWs w(ws, d);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    double* cw = cand + int64_t(warp) * d;
+    for (int j = 0; j < d; ++j) {
+        if (w.sig[j] > 0.0) continue;  // uniform
+        double best = -1.0;
+        int be = d;
+        for (int e = warp; e < d; e += nw) {
+            for (int i = lane; i < d; i += kWarp) cw[i] = (i == e) ? 1.0 : 0.0;
+            __syncwarp();
+            for (int pass = 0; pass < 2; ++pass)
+                for (int c = 0; c < j; ++c) {
+                    const double* uc = w.ut + int64_t(c) * d;
+                    double dot = 0.0;
+                    for (int i = lane; i < d; i += kWarp) dot += cw[i] * uc[i];
+                    dot = warp_sum(dot);
+                    for (int i = lane; i < d; i += kWarp) cw[i] -= dot * uc[i];
+                    __syncwarp();
+                }
+            double res = 0.0;
+            for (int i = lane; i < d; i += kWarp) res += cw[i] * cw[i];
+            res = warp_sum(res);
+            if (res > best) { best = res; be = e; }  // e increasing: strict > keeps the first
+        }
+        if (lane == 0) { s_res[warp] = best; s_e[warp] = be; }
+        __syncthreads();
+        if (warp == 0) {
+            double b = lane < nw ? s_res[lane] : -2.0;
+            int e = lane < nw ? s_e[lane] : d;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                const double ob = __shfl_xor_sync(0xffffffffu, b, o);
+                const int oe = __shfl_xor_sync(0xffffffffu, e, o);
+                if (ob > b || (ob == b && oe < e)) { b = ob; e = oe; }
+            }
+            if (lane == 0) { s_res[0] = b; s_e[0] = e; }
+        }
+        __syncthreads();
+        const int e = s_e[0];
+        const double res = s_res[0];
+        if (warp == 0) {  // recompute the winner (same arithmetic) straight into u_j
+            double* uj = w.ut + int64_t(j) * d;
+            for (int i = lane; i < d; i += kWarp) uj[i] = (i == e) ? 1.0 : 0.0;
+            __syncwarp();
+            for (int pass = 0; pass < 2; ++pass)
+                for (int c = 0; c < j; ++c) {
+                    const double* uc = w.ut + int64_t(c) * d;
+                    double dot = 0.0;
+                    for (int i = lane; i < d; i += kWarp) dot += uj[i] * uc[i];
+                    dot = warp_sum(dot);
+                    for (int i = lane; i < d; i += kWarp) uj[i] -= dot * uc[i];
+                    __syncwarp();
+                }
+            const double nrm = sqrt(res);
+            for (int i = lane; i < d; i += kWarp) uj[i] /= nrm;
+        }
+        __syncthreads();
+    }
+    for (int64_t e = threadIdx.x; e < int64_t(d) * d; e += blockDim.x) {
+        const int i = int(e / d), r = int(e - int64_t(i) * d);
+        U[int64_t(i) * ldu + r] = T(w.ut[int64_t(r) * d + i]);
+        V[int64_t(i) * ldv + r] = T(w.vs[int64_t(r) * d + i]);
+    }
+    for (int r = threadIdx.x; r < d; r += blockDim.x) sigma[r] = T(w.sig[r]);
+}
+
+// svd_truncate's core (baselines.hpp:14-20): C(i, l) = sum_{r < k} (u(i, r)·sigma_r)·v(l, r), r increasing.
+template <typename T>
+__global__ void __launch_bounds__(256) k_svd_core(const double* ws, int d, int k, T* C, int64_t ldc) {
+    PinvWs w(const_cast<double*>(ws), d);
+    __shared__ double su[kAsmTile][kAsmTile + 1];
+    __shared__ double sv[kAsmTile][kAsmTile + 1];
+    const int i0 = blockIdx.y * kAsmTile, l0 = blockIdx.x * kAsmTile;
+    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+    double acc[4] = {0.0, 0.0, 0.0, 0.0};
+    for (int r0 = 0; r0 < k; r0 += kAsmTile) {
+        for (int rr = ty; rr < kAsmTile; rr += 8) {
+            const int r = r0 + rr;
+            const bool ok = r < k;
+            su[rr][tx] = (ok && i0 + tx < d) ? w.ut[int64_t(r) * d + i0 + tx] * w.sig[r] : 0.0;
+            sv[rr][tx] = (ok && l0 + tx < d) ? w.vs[int64_t(r) * d + l0 + tx] : 0.0;
+        }
+        __syncthreads();
+        const int rn = min(kAsmTile, k - r0);
+        for (int rr = 0; rr < rn; ++rr) {
+            const double vv = sv[rr][tx];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) acc[q] += su[rr][ty + 8 * q] * vv;
+        }
+        __syncthreads();
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        const int i = i0 + ty + 8 * q, l = l0 + tx;
+        if (i < d && l < d) C[int64_t(i) * ldc + l] = T(acc[q]);
+    }
+}
 }  // namespace
 
-int64_t pinv_ws_doubles(int d) { return 4 * int64_t(d) * d + 8 + d + (kMaxSweeps + d + 1) / 2 + 8; }
+int64_t pinv_ws_doubles(int d) { return 4 * int64_t(d) * d + 8 + 2 * int64_t(d) + (kMaxSweeps + d + 1) / 2 + 8; }
 
 template <typename T>
-cudaError_t pinv_square(const T* Y, int64_t ldy, int d, T* P, int64_t ldp, double* ws, int* converged, int max_smem,
-                        cudaStream_t st) {
+cudaError_t jacobi_run(const T* Y, int64_t ldy, int d, double* ws, int* converged, int max_smem, int svd_mode,
+                       cudaStream_t st) {
     const bool in_smem = jacobi_smem(d, true) <= size_t(max_smem);
     const size_t smem = jacobi_smem(d, in_smem);
     // G lanes per column pair, at most 8 column entries per lane (register path when the columns
@@ -436,7 +565,7 @@ cudaError_t pinv_square(const T* Y, int64_t ldy, int d, T* P, int64_t ldp, doubl
         const int ppw = kWarp / G;
         const int warps = std::min(max_warps, std::max(1, (pairs + ppw - 1) / ppw));
         allow_max_smem(kern);
-        kern<<<1, warps * kWarp, smem, st>>>(Y, ldy, d, ws, cols, converged);
+        kern<<<1, warps * kWarp, smem, st>>>(Y, ldy, d, ws, cols, converged, svd_mode);
     };
     if (in_smem && d <= 32) launch(k_jacobi_svd<T, 4, 8>, 4, 16);
     else if (in_smem && d <= 64) launch(k_jacobi_svd<T, 8, 8>, 8, 16);
@@ -450,15 +579,39 @@ cudaError_t pinv_square(const T* Y, int64_t ldy, int d, T* P, int64_t ldp, doubl
         const int want = (pairs + kGridWarps - 1) / kGridWarps;
         const int blocks = std::max(1, std::min(want, std::max(1, per_sm) * sms));
         int dd = d;
-        void* args[] = {(void*)&Y, (void*)&ldy, (void*)&dd, (void*)&ws, (void*)&converged};
+        void* args[] = {(void*)&Y, (void*)&ldy, (void*)&dd, (void*)&ws, (void*)&converged, (void*)&svd_mode};
         cudaError_t e = cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(k_jacobi_grid<T>), dim3(blocks),
                                                     dim3(kGridWarps * kWarp), args, 0, st);
         if (e != cudaSuccess) return e;
     } else launch(k_jacobi_svd<T, 32, 0>, 32, 32);
-    cudaError_t e = cudaGetLastError();
+    return cudaGetLastError();
+}
+
+template <typename T>
+cudaError_t pinv_square(const T* Y, int64_t ldy, int d, T* P, int64_t ldp, double* ws, int* converged, int max_smem,
+                        cudaStream_t st) {
+    cudaError_t e = jacobi_run<T>(Y, ldy, d, ws, converged, max_smem, 0, st);
     if (e != cudaSuccess) return e;
     const dim3 grid((d + kAsmTile - 1) / kAsmTile, (d + kAsmTile - 1) / kAsmTile);
     k_pinv_assemble<T><<<grid, 256, 0, st>>>(ws, d, P, ldp);
+    return cudaGetLastError();
+}
+
+template <typename T>
+cudaError_t svd_square(const T* Y, int64_t ldy, int d, T* U, int64_t ldu, T* sigma, T* V, int64_t ldv, double* ws,
+                       int* converged, int max_smem, cudaStream_t st) {
+    cudaError_t e = jacobi_run<T>(Y, ldy, d, ws, converged, max_smem, 1, st);
+    if (e != cudaSuccess) return e;
+    const size_t sm = size_t(kWarp) * d * sizeof(double);
+    allow_max_smem(k_svd_finalize<T>);
+    k_svd_finalize<T><<<1, 1024, sm, st>>>(ws, d, U, ldu, sigma, V, ldv);
+    return cudaGetLastError();
+}
+
+template <typename T>
+cudaError_t svd_truncate_core(const double* ws, int d, int k, T* C, int64_t ldc, cudaStream_t st) {
+    const dim3 grid((d + kAsmTile - 1) / kAsmTile, (d + kAsmTile - 1) / kAsmTile);
+    k_svd_core<T><<<grid, 256, 0, st>>>(ws, d, k, C, ldc);
     return cudaGetLastError();
 }
 
@@ -466,5 +619,8 @@ template cudaError_t pinv_square<double>(const double*, int64_t, int, double*, i
                                          cudaStream_t);
 template cudaError_t pinv_square<float>(const float*, int64_t, int, float*, int64_t, double*, int*, int,
                                         cudaStream_t);
+template cudaError_t svd_square<double>(const double*, int64_t, int, double*, int64_t, double*, double*, int64_t,
+                                        double*, int*, int, cudaStream_t);
+template cudaError_t svd_truncate_core<double>(const double*, int, int, double*, int64_t, cudaStream_t);
 
 }  // namespace coru_gpu

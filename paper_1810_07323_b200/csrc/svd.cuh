@@ -15,6 +15,18 @@ template <typename T>
 cudaError_t pinv_square(const T* Y, int64_t ldy, int d, T* P, int64_t ldp, double* ws, int* converged, int max_smem,
                         cudaStream_t st);
 int64_t pinv_ws_doubles(int d);
+
+// svd (svd.hpp:141-161) of a square d x d row-major Y: U, V (d x d row-major), sigma[d] non-increasing,
+// zero-sigma u columns completed from the canonical basis (svd.hpp:98-121). Same workspace as
+// pinv_square; afterwards `ws` still holds the sorted factors for svd_truncate_core.
+template <typename T>
+cudaError_t svd_square(const T* Y, int64_t ldy, int d, T* U, int64_t ldu, T* sigma, T* V, int64_t ldv, double* ws,
+                       int* converged, int max_smem, cudaStream_t st);
+// C (d x d, ldc) = u(:, 1:k)·diag(sigma_1..k)·v(:, 1:k)^T from the factors svd_square left in `ws`
+// (svd_truncate, baselines.hpp:14-20).
+template <typename T>
+cudaError_t svd_truncate_core(const double* ws, int d, int k, T* C, int64_t ldc, cudaStream_t st);
+constexpr int kSvdLaunches = 2;
 constexpr int kPinvLaunches = 2;
 
 }  // namespace coru_gpu

@@ -103,6 +103,27 @@ int main() {
             }
         CHECK(std::sqrt(diff) <= 1e-6 * std::sqrt(nrm));
     }
+    // baselines (test_baselines.cpp:99-112): sor_svd recovers exact rank-k input; bad k throws
+    {
+        const Matrix e5 = exact_rank(25, 18, 5, {22, 0});
+        const Matrix s5 = sor_svd(e5, 5, 8, 0, {23, 0});
+        double diff = 0, nrm = 0;
+        for (std::size_t i = 0; i < e5.data().size(); ++i) {
+            diff += (e5.data()[i] - s5.data()[i]) * (e5.data()[i] - s5.data()[i]);
+            nrm += e5.data()[i] * e5.data()[i];
+        }
+        CHECK(std::sqrt(diff) <= 1e-8 * std::sqrt(nrm));
+        bool threw = false;
+        try {
+            (void)sor_svd(e5, 9, 8, 0, {23, 0});
+        } catch (const std::invalid_argument&) {
+            threw = true;
+        }
+        CHECK(threw);
+        SvdFactors t = tsr_svd(e5, 6, {20, 3});
+        CHECK(orth_res(t.u) <= 1e-9 * std::sqrt(6.0) && orth_res(t.v) <= 1e-9 * std::sqrt(6.0));
+        for (std::size_t j = 0; j + 1 < t.sigma.size(); ++j) CHECK(t.sigma[j] >= t.sigma[j + 1]);
+    }
     std::printf("%s: %d failures\n", failures ? "FAIL" : "OK", failures);
     return failures ? 1 : 0;
 }

@@ -46,3 +46,24 @@ def pinv_cases():
     z = np.load(os.path.join(HERE, "approx_ref_cases.npz"))
     return [dict(name=str(k), A=z[f"pinv/{k}/in"], P=z[f"pinv/{k}/out"], U=z[f"pinv/{k}/u"], S=z[f"pinv/{k}/s"],
                  V=z[f"pinv/{k}/v"], converged=bool(z[f"pinv/{k}/conv"][0])) for k in z["pinv_names"]]
+
+
+def tsr_cases():
+    z = np.load(os.path.join(HERE, "baselines_ref_cases.npz"))
+    out = []
+    for name in z["tsr_names"]:
+        name = str(name)
+        ell, seed, stream = (int(x) for x in z[f"{name}/params"])
+        out.append(dict(name=name, A=z[f"{name}/A"], ell=ell, seed=seed, stream=stream, U=z[f"{name}/U"],
+                        S=z[f"{name}/S"], V=z[f"{name}/V"], converged=bool(z[f"{name}/conv"][0])))
+    return out
+
+
+def sor_cases():
+    z = np.load(os.path.join(HERE, "baselines_ref_cases.npz"))
+    out = []
+    for name in z["sor_names"]:
+        name = str(name)
+        k, ell, q, seed, stream = (int(x) for x in z[f"{name}/params"])
+        out.append(dict(name=name, A=z[f"{name}/A"], k=k, ell=ell, q=q, seed=seed, stream=stream, L=z[f"{name}/L"]))
+    return out

@@ -106,6 +106,36 @@ def main():
     np.savez_compressed(os.path.join(HERE, "kernels_ref_kat.npz"), **kat)
     print("wrote", len(names), "corutv cases and", len(kat), "kernel KAT arrays")
     approx_fixtures(cases)
+    baseline_fixtures()
+
+
+def baseline_fixtures():
+    """SOR-SVD / TSR-SVD (baselines.hpp:43-71) on the inputs of proj/tests/test_baselines.cpp."""
+    bl = {}
+    tsr = [("tsr_rank1_50x30", R.matmul(R.gaussian(50, 1, 17, 0), np.ascontiguousarray(R.gaussian(30, 1, 17, 1).T)),
+            2, 18, 0),                                                                          # :57-66
+           ("tsr_fast_decay_70", R.gen_fast_decay(70, 7, 19), 14, 20, 3),                      # :68-79
+           ("tsr_noisy_200", R.gen_noisy_lowrank(200, 10, 0.1, 21), 20, 400, 0),               # :81-97
+           ("tsr_wide_40x90", R.gaussian(40, 90, 31, 2) * (0.9 ** np.arange(90)), 12, 32, 0)]
+    for name, a, ell, seed, stream in tsr:
+        u, s, v, conv = R.tsr_svd(a, ell, seed, stream)
+        bl[f"{name}/A"], bl[f"{name}/params"] = a, np.array([ell, seed, stream], np.int64)
+        bl[f"{name}/U"], bl[f"{name}/S"], bl[f"{name}/V"] = u, s, v
+        bl[f"{name}/conv"] = np.array([conv], np.int64)
+    er = R.matmul(R.gaussian(25, 5, 22, 0), np.ascontiguousarray(R.gaussian(18, 5, 22, 1).T))
+    sor = [("sor_exact_rank_25x18", er, 5, 8, 0, 23, 0),                                      # :99-104
+           ("sor_fast_decay_60_k12", R.gen_fast_decay(60, 6, 24), 12, 12, 0, 25, 0),            # :106-112
+           ("sor_noisy_200", R.gen_noisy_lowrank(200, 10, 0.01, 26), 10, 20, 0, 500, 0),        # :114-124
+           ("sor_noisy_100", R.gen_noisy_lowrank(100, 10, 0.1, 5), 10, 20, 0, 6, 0),            # :45-55
+           ("sor_q2_90x60", R.gen_fast_decay(90, 9, 41)[:, :60].copy(), 6, 15, 2, 42, 1),
+           ("sor_wide_30x50", R.gaussian(30, 50, 43, 0) * (0.85 ** np.arange(50)), 4, 9, 1, 44, 0)]
+    for name, a, k, ell, q, seed, stream in sor:
+        bl[f"{name}/A"], bl[f"{name}/params"] = a, np.array([k, ell, q, seed, stream], np.int64)
+        bl[f"{name}/L"] = R.sor_svd(a, k, ell, q, seed, stream)
+    bl["tsr_names"] = np.array([t[0] for t in tsr])
+    bl["sor_names"] = np.array([t[0] for t in sor])
+    np.savez_compressed(os.path.join(HERE, "baselines_ref_cases.npz"), **bl)
+    print("wrote", len(tsr), "tsr_svd and", len(sor), "sor_svd cases")
 
 
 def approx_fixtures(cases):

@@ -7,7 +7,7 @@ present. This is what entitles the GPU parity tests to use the oracle as the che
 import numpy as np
 import pytest
 
-from golden import approx_cases, corutv_cases, kat, pinv_cases, sketch_case
+from golden import approx_cases, corutv_cases, kat, pinv_cases, sketch_case, sor_cases, tsr_cases
 
 
 def test_rng_words_and_gaussian_bitexact(oracle):
@@ -160,3 +160,25 @@ def test_fp32_restatement_tracks_fp64(oracle):
     d64, d32 = np.abs(np.diag(f64.t)), np.abs(np.diag(f32.t))
     assert np.max(np.abs(d64 - d32)) <= 1e-3
     assert np.max(np.abs(d64 - d32)[:20] / d64[:20]) <= 1e-5
+
+
+@pytest.mark.parametrize("case", tsr_cases(), ids=lambda c: c["name"])
+def test_tsr_svd_bitexact_vs_golden(oracle, case):
+    """tsr_svd (baselines.hpp:43-56): two sketches, two QRs, pinv core, square Jacobi SVD, lift."""
+    u, s, v, conv = oracle.tsr_svd(case["A"], case["ell"], case["seed"], case["stream"])
+    assert np.array_equal(u, case["U"]) and np.array_equal(s, case["S"]) and np.array_equal(v, case["V"])
+    assert conv == case["converged"]
+
+
+@pytest.mark.parametrize("case", sor_cases(), ids=lambda c: c["name"])
+def test_sor_svd_bitexact_vs_golden(oracle, case):
+    """sor_svd (baselines.hpp:61-71): sketch bases, exact core, truncated SVD, lifted m x n."""
+    out = oracle.sor_svd(case["A"], case["k"], case["ell"], case["q"], case["seed"], case["stream"])
+    assert np.array_equal(out, case["L"])
+
+
+def test_sor_svd_equals_corutv_reconstruction_at_k_ell(oracle):
+    """test_baselines.cpp:106-112: sor_svd(k = ell) == reconstruct(corutv) for the same seed."""
+    c = next(x for x in sor_cases() if x["name"] == "sor_fast_decay_60_k12")
+    f = oracle.corutv(c["A"], 12, 0, 0, 25, 0)
+    assert np.linalg.norm(c["L"] - f.u @ f.t @ f.v.T) <= 1e-9 * np.linalg.norm(c["A"])
