@@ -19,6 +19,7 @@ struct GemmPlan {
     int cfg = -1;                    // fp64: kernel configuration id (gemm_f64.cu table)
     int num_sms = 148;
     int64_t ws_elems = 0;            // workspace (partials) needed, in elements
+    int groups = 1;                  // fp64: grouped stream-K, one CTA group per n-tile (splits per group)
 };
 
 GemmPlan plan_gemm_f64(Op op, int64_t Mo, int64_t K, int N, int num_sms);

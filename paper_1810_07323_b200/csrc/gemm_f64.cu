@@ -21,6 +21,7 @@
 #include <algorithm>
 #include <atomic>
 #include <cmath>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "gemm.cuh"
@@ -203,27 +204,37 @@ template <class S, int VEC>
 __global__ void __launch_bounds__(S::NT, S::min_blocks)
     k_gemm_f64(const double* __restrict__ A, int64_t lda, const double* __restrict__ X, int64_t ldx,
                double* __restrict__ C, int64_t ldc, int64_t Mo, int64_t K, int N, int64_t ktiles, int64_t iters, int P,
-               double* __restrict__ ws, int max_seg, uint64_t* __restrict__ flags, uint64_t epoch) {
+               double* __restrict__ ws, int max_seg, uint64_t* __restrict__ flags, uint64_t epoch, int G, int apol) {
     constexpr int MT = S::MT, BK = S::BK, ST = S::ST;
     extern __shared__ __align__(16) double smem[];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int g = lane >> 2, t = lane & 3;
     const int wm0 = (warp / S::WN) * S::WTM, wn0 = (warp % S::WN) * 32;
-    const int cta = blockIdx.x;
+    // Grouped stream-K: G = n-tiles groups of P CTAs each; group g owns n-tile g of every row block
+    // and splits its (row block, k-slab) iterations stream-K style over its P CTAs. CTAs of equal
+    // rank in different groups walk the same A rows at the same time, so A comes from DRAM once
+    // and the other n-tiles read it from L2 (iters, P and `cta` below are per group).
+    const int grp = int(blockIdx.x) % G;
+    const int cta = int(blockIdx.x) / G;
     int64_t it = sk_begin(iters, P, cta);
     const int64_t it_end = sk_begin(iters, P, cta + 1);
-    const uint64_t pol_a = l2_policy_evict_first(), pol_x = l2_policy_evict_last();
+    // A: evict-first when one CTA is its only reader; with n-tile groups every A line has G readers
+    // within a short window, so it keeps the normal priority (apol: tooling override, -1 = auto).
+    const int ap = apol >= 0 ? apol : (G > 1 ? 1 : 0);
+    const uint64_t pol_a = ap == 0 ? l2_policy_evict_first() : (ap == 1 ? l2_policy_evict_normal() : l2_policy_evict_last());
+    const uint64_t pol_x = l2_policy_evict_last();
 
     const int tiles_n = (N + S::BN - 1) / S::BN;
     int64_t fix_tile = -1;  // split tile whose last k-slab this CTA owns: summed after the range
     int fix_segs = 0;
     while (it < it_end) {
-        const int64_t tile = it / ktiles;
+        const int64_t tile_m = it / ktiles;          // row block within the group
+        const int64_t tile = G > 1 ? tile_m * tiles_n + grp : tile_m;  // global tile id (ws / flags)
         const int64_t kb = it % ktiles;
         const int64_t ke = imin64(ktiles, kb + (it_end - it));
         const int nk = int(ke - kb);
-        const int64_t m0 = (tile / tiles_n) * S::BM;  // n-tiles of one row block are adjacent
-        const int n0 = int(tile % tiles_n) * S::BN;
+        const int64_t m0 = (G > 1 ? tile_m : tile / tiles_n) * S::BM;  // G == 1: n-tiles of a row block adjacent
+        const int n0 = (G > 1 ? grp : int(tile % tiles_n)) * S::BN;
         const int Nt = N - n0;                        // columns left from this n-tile
         const double* Xt = X + n0;
 
@@ -301,7 +312,7 @@ __global__ void __launch_bounds__(S::NT, S::min_blocks)
             ld_dst = ldc;
             row_base = m0;
         } else {
-            const int first = sk_owner(iters, P, tile * ktiles);
+            const int first = sk_owner(iters, P, tile_m * ktiles);
             seg = cta - first;
             dst_base = ws + (tile * max_seg + seg) * int64_t(S::BM * S::BN);
             ld_dst = S::BN;
@@ -340,7 +351,7 @@ __global__ void __launch_bounds__(S::NT, S::min_blocks)
                 }
             }
         }
-        it = tile * ktiles + ke;
+        it = tile_m * ktiles + ke;
     }
     if (fix_tile >= 0) {
         // Fixed-order sum of the tile's segments (seg 0 .. fix_segs-1; the last one is ours).
@@ -450,7 +461,9 @@ cudaError_t launch_cfg(const double* A, int64_t lda, const double* X, int64_t ld
                        int64_t K, int N, const GemmPlan& p, double* ws, cudaStream_t st) {
     const int64_t ktiles = (K + S::BK - 1) / S::BK;
     const int64_t tiles = ((Mo + S::BM - 1) / S::BM) * ((N + S::BN - 1) / S::BN);
-    const int64_t iters = tiles * ktiles;
+    const int G = p.groups;
+    static const int apol = getenv("CORU_GEMM_APOL") ? atoi(getenv("CORU_GEMM_APOL")) : -1;
+    const int64_t iters = (G > 1 ? (Mo + S::BM - 1) / S::BM : tiles) * ktiles;  // per group
     const bool vec = (lda % 2 == 0) && (reinterpret_cast<uintptr_t>(A) % 16 == 0);
     // split-tile flags live after the partial tiles; a fresh epoch per launch (no reset needed)
     uint64_t* flags = p.fixup ? reinterpret_cast<uint64_t*>(ws + tiles * int64_t(p.max_seg) * S::BM * S::BN) : nullptr;
@@ -458,13 +471,13 @@ cudaError_t launch_cfg(const double* A, int64_t lda, const double* X, int64_t ld
     if (vec) {
         auto k = k_gemm_f64<S, 2>;
         allow_max_smem(k);
-        k<<<p.splits, S::NT, S::bytes, st>>>(A, lda, X, ldx, C, ldc, Mo, K, N, ktiles, iters, p.splits, ws, p.max_seg,
-                                              flags, epoch);
+        k<<<p.splits * G, S::NT, S::bytes, st>>>(A, lda, X, ldx, C, ldc, Mo, K, N, ktiles, iters, p.splits, ws,
+                                                  p.max_seg, flags, epoch, G, apol);
     } else {
         auto k = k_gemm_f64<S, 1>;
         allow_max_smem(k);
-        k<<<p.splits, S::NT, S::bytes, st>>>(A, lda, X, ldx, C, ldc, Mo, K, N, ktiles, iters, p.splits, ws, p.max_seg,
-                                              flags, epoch);
+        k<<<p.splits * G, S::NT, S::bytes, st>>>(A, lda, X, ldx, C, ldc, Mo, K, N, ktiles, iters, p.splits, ws,
+                                                  p.max_seg, flags, epoch, G, apol);
     }
     return cudaGetLastError();
 }
@@ -481,8 +494,8 @@ GemmPlan plan_gemm_f64_cfg(Op op, int64_t Mo, int64_t K, int N, int num_sms, int
     p.bm = c.wm * 16 * c.mt;
     p.bn = 32 * c.wn;
     const int64_t ktiles = (K + c.bk - 1) / c.bk;
-    const int64_t tiles = ((Mo + p.bm - 1) / p.bm) * ((N + p.bn - 1) / p.bn);
-    const int64_t iters = tiles * ktiles;
+    const int64_t tiles_m = (Mo + p.bm - 1) / p.bm, tiles_n = (N + p.bn - 1) / p.bn;
+    const int64_t tiles = tiles_m * tiles_n;
     const int nt = 32 * c.wm * c.wn;
     const int reg_per_thread = c.mt == 4 ? 192 : (c.mt == 2 ? 128 : 96);
     const int occ_smem = (227 * 1024) / cfg_bytes(c, op == Op::T);
@@ -490,14 +503,22 @@ GemmPlan plan_gemm_f64_cfg(Op op, int64_t Mo, int64_t K, int N, int num_sms, int
     const int occ = std::max(1, std::min({4, occ_smem, occ_regs}));
     // Every CTA resident at once, each owns >= 4 k-slabs, and no tile is shared by more CTAs than
     // needed to fill the machine (bounded fix-up).
-    int64_t P64 = std::min<int64_t>(int64_t(occ) * num_sms, iters / 4);
-    P64 = std::min<int64_t>(P64, tiles * std::max<int64_t>(12, (int64_t(occ) * num_sms + tiles - 1) / tiles));
-    const int P = int(std::max<int64_t>(P64, 1));
+    // Grouped stream-K (several n-tiles): one CTA group per n-tile walking the row blocks in step,
+    // so A is read from DRAM once per pass instead of once per n-tile (k_gemm_f64).
+    static const bool grouped_env = getenv("CORU_GEMM_GROUPED") == nullptr || atoi(getenv("CORU_GEMM_GROUPED")) != 0;
+    const int64_t resident = int64_t(occ) * num_sms;
+    const int G = (grouped_env && tiles_n > 1 && resident / tiles_n >= 8) ? int(tiles_n) : 1;
+    p.groups = G;
+    const int64_t gtiles = G > 1 ? tiles_m : tiles;  // tiles per group
+    const int64_t iters = gtiles * ktiles;            // iterations per group
+    int64_t P64 = std::min<int64_t>(resident / G, iters / 4);
+    P64 = std::min<int64_t>(P64, gtiles * std::max<int64_t>(12, (resident / G + gtiles - 1) / gtiles));
+    const int P = int(std::max<int64_t>(P64, 1));     // CTAs per group
     p.splits = P;
     const int64_t per = std::max<int64_t>(1, iters / P);
     p.max_seg = int(std::min<int64_t>(P, (ktiles + per - 1) / per + 1));
     p.fixup = false;
-    for (int64_t tile = 0; tile < tiles && !p.fixup; ++tile) {
+    for (int64_t tile = 0; tile < gtiles && !p.fixup; ++tile) {
         const int64_t g0 = tile * ktiles, g1 = g0 + ktiles - 1;
         p.fixup = ((g0 + 1) * P - 1) / iters != ((g1 + 1) * P - 1) / iters;
     }
