@@ -168,6 +168,8 @@ struct coru_ctx {
     cudaStream_t stream = nullptr;
     cudaStream_t aux = nullptr;  // second stream: the two TSQR trees run concurrently
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+    static constexpr int kUploadChunks = 8;
+    cudaEvent_t ev_chunk[kUploadChunks] = {};  // host-entry upload pipeline (corutv_host)
     int num_sms = 148;
     int max_smem = 227 * 1024;
     int host_threads = 1;
@@ -372,6 +374,7 @@ struct Request {
     int q = 0;
     uint64_t seed = 0, stream = 0;
     Mode mode = Mode::Full;
+    bool first_done = false;  // the first power round (Φ, c1 = a·Φ, c2 = a^T·c1) is already in the workspace
     int variant = CORU_D_EXACT;  // Full: how D is formed (corutv.hpp:89-92)
     // Full: U' (rows x d), T' (d x d), V' (cols x d) — device, caller's buffers.
     T* u = nullptr;
@@ -508,6 +511,28 @@ int allgather(coru_ctx* c, const T* send, T* recv, size_t count) {
     return CORU_OK;
 }
 
+// Φ = gaussian(cols, ell, seed), padded to dp columns (corutv.hpp:51): on the device, or on the
+// host with the host libm (bit-exact) and one H2D.
+template <typename T>
+int gen_phi(coru_ctx* c, const Request<T>& r, T* out, int dp) {
+    const int64_t N = r.cols;
+    cudaStream_t st = c->stream;
+    if (c->phi_mode == CORU_PHI_DEVICE) {
+        uint64_t s4[4];
+        seed_state_words(r.seed, r.stream, s4);
+        CORU_CUDA(gaussian_dev<T>(N, r.d, s4, out, dp, st));
+        ++g_launches;
+        return CORU_OK;
+    }
+    const size_t phi_bytes = size_t(N) * dp * sizeof(T);
+    CORU_TRY(ensure_pinned(c, phi_bytes));
+    CORU_CUDA(cudaStreamSynchronize(st));  // the pinned staging buffer is reused across calls
+    T* phi = reinterpret_cast<T*>(c->pinned);
+    gaussian_host<T>(N, r.d, r.seed, r.stream, phi, dp, c->host_threads, 1);  // streaming stores, zero padding
+    CORU_CUDA(cudaMemcpyAsync(out, phi, phi_bytes, cudaMemcpyHostToDevice, st));
+    return CORU_OK;
+}
+
 template <typename T>
 int run_impl(coru_ctx* c, const Request<T>& r, size_t extra_arena_off);
 
@@ -535,19 +560,7 @@ int run_impl(coru_ctx* c, const Request<T>& r, size_t extra_arena_off) {
 
     // Φ = gaussian(cols, ell, seed), padded to dp columns (corutv.hpp:51): on the device, or on the
     // host with the host libm (bit-exact) and one H2D.
-    if (c->phi_mode == CORU_PHI_DEVICE) {
-        uint64_t s4[4];
-        seed_state_words(r.seed, r.stream, s4);
-        CORU_CUDA(gaussian_dev<T>(N, d, s4, w.b2, dp, st));
-        ++g_launches;
-    } else {
-        const size_t phi_bytes = size_t(N) * dp * sizeof(T);
-        CORU_TRY(ensure_pinned(c, phi_bytes));
-        CORU_CUDA(cudaStreamSynchronize(st));  // the pinned staging buffer is reused across calls
-        T* phi = reinterpret_cast<T*>(c->pinned);
-        gaussian_host<T>(N, d, r.seed, r.stream, phi, dp, c->host_threads, 1);  // streaming stores, zero padding
-        CORU_CUDA(cudaMemcpyAsync(w.b2, phi, phi_bytes, cudaMemcpyHostToDevice, st));
-    }
+    if (!r.first_done) CORU_TRY(gen_phi<T>(c, r, w.b2, dp));
     CORU_CUDA(cudaMemsetAsync(w.q1, 0, size_t(R) * dp * sizeof(T), st));
     CORU_CUDA(cudaMemsetAsync(w.q2, 0, size_t(N) * dp * sizeof(T), st));
 
@@ -557,8 +570,9 @@ int run_impl(coru_ctx* c, const Request<T>& r, size_t extra_arena_off) {
     // overlaps the last A^T pass; with a communicator QR(c1) stays on the main stream (its
     // all-gather must keep the NCCL issue order) and QR(c2) goes to the aux stream.
     const bool sharded = c->world > 1;
-    const bool early_qr1 = !sharded && getenv("CORU_QR1_EARLY") != nullptr;  // tooling: overlap QR(c1) with the last A^T pass
-    for (int i = 0; i <= r.q; ++i) {
+    // tooling: overlap QR(c1) with the last A^T pass
+    const bool early_qr1 = !sharded && getenv("CORU_QR1_EARLY") != nullptr && !(r.first_done && r.q == 0);
+    for (int i = r.first_done ? 1 : 0; i <= r.q; ++i) {
         CORU_TRY(gemm<T>(c, r.op_a(), r.A, r.lda, w.b2, dp, w.b1, dp, R, N, d, w.gws, w.gws_elems));
         if (i == r.q && early_qr1) {
             CORU_CUDA(cudaEventRecord(c->ev_fork, st));
@@ -728,6 +742,26 @@ int corutv_dev(coru_ctx* c, const T* A, int64_t m_local, int64_t m, int64_t n, i
     return run<T>(c, r);
 }
 
+template <typename T>
+__global__ void k_sum_chunks(const T* __restrict__ parts, int nparts, int64_t rows, int d, int ldp, int64_t stride,
+                             T* __restrict__ out, int ldo) {
+    const int64_t total = rows * d;
+    for (int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < total; e += int64_t(gridDim.x) * blockDim.x) {
+        const int64_t r = e / d;
+        const int cc = int(e - r * d);
+        T s = parts[r * ldp + cc];
+        for (int i = 1; i < nparts; ++i) s += parts[i * stride + r * ldp + cc];  // fixed chunk order
+        out[r * ldo + cc] = s;
+    }
+}
+template <typename T>
+cudaError_t sum_chunks(const T* parts, int nparts, int64_t rows, int d, int ldp, int64_t stride, T* out, int ldo,
+                       cudaStream_t st) {
+    const int blocks = int(std::min<int64_t>((rows * d + 255) / 256, 148 * 8));
+    k_sum_chunks<T><<<std::max(blocks, 1), 256, 0, st>>>(parts, nparts, rows, d, ldp, stride, out, ldo);
+    return cudaGetLastError();
+}
+
 // Host-buffer entry: upload A into the arena head, run, download. Single GPU.
 template <typename T>
 int corutv_host(coru_ctx* c, const T* A, int64_t m, int64_t n, int64_t ell, int q, int variant, uint64_t seed,
@@ -736,75 +770,126 @@ int corutv_host(coru_ctx* c, const T* A, int64_t m, int64_t n, int64_t ell, int 
     if (variant != CORU_D_EXACT && variant != CORU_D_APPROX) return fail(CORU_EINVAL, "corutv: unknown DVariant");
     if (!A || !U || !Tt || !V) return fail(CORU_EINVAL, "null argument");
     if (c->world > 1) return fail(CORU_EINVAL, "host-buffer entry is single-GPU; use the _dev entry per rank");
-    // Head of the arena: A, U, T, V and a flag, then the decomposition workspace.
+    const bool trans = m < n;
+    const int d = int(ell), dp = int(round_up(ell, 8));
+    // Upload pipeline (m >= n, A of 32 MB and more): A arrives in row chunks on the aux stream while
+    // the main stream validates each chunk and runs the first power round on it (c1 rows = A_i·Φ,
+    // partial c2 = A_i^T·c1_i, summed in chunk order), so the first two passes and the finiteness
+    // check hide under the H2D copy. Later rounds need all of A and start after the last chunk.
+    constexpr int C = coru_ctx::kUploadChunks;
+    const bool pipe = !trans && m >= int64_t(C) * 2 * (ell + 1) && size_t(m) * n * sizeof(T) >= (size_t(32) << 20) &&
+                      getenv("CORU_NO_UPLOAD_PIPE") == nullptr;
+    auto chunk_rows = [&](int i, int64_t& r0, int64_t& rows) {
+        r0 = m * i / C;
+        rows = m * (i + 1) / C - r0;
+    };
+    int64_t cwse = 0;
+    if (pipe)
+        for (int i = 0; i < C; ++i) {
+            int64_t r0, rows;
+            chunk_rows(i, r0, rows);
+            cwse = std::max({cwse, gemm_ws<T>(Op::N, rows, n, d, c->num_sms), gemm_ws<T>(Op::T, n, rows, d, c->num_sms)});
+        }
+    // Head of the arena: A, U, T, V and a flag (+ the pipeline's partial sketches and GEMM
+    // workspace), then the decomposition workspace.
     Carver head{nullptr, 0};
+    T* parts = nullptr;
+    T* cws = nullptr;
     auto lay = [&](Carver& cv, T*& a, T*& u, T*& t, T*& v, int*& f) {
         a = cv.template take<T>(m * n);
         u = cv.template take<T>(m * ell);
         t = cv.template take<T>(ell * ell);
         v = cv.template take<T>(n * ell);
         f = cv.template take<int>(4);
+        if (pipe) {
+            parts = cv.template take<T>(int64_t(C) * n * dp);
+            cws = cv.template take<T>(cwse);
+        }
     };
     T *a_d, *u_d, *t_d, *v_d;
     int* f_d;
     lay(head, a_d, u_d, t_d, v_d, f_d);
     const size_t head_bytes = (head.off + 255) / 256 * 256;
-    // Reserve the head plus a generous guess; run() grows the arena if needed, so size it first.
-    {
-        Request<T> probe;
-        probe.rows = m >= n ? m : n;
-        probe.cols = m >= n ? n : m;
-        probe.d = int(ell);
-        probe.variant = variant;
-        Work<T> w;
-        Carver meas{nullptr, head_bytes};
-        w.layout(meas, c, probe, int(round_up(ell, 8)));
-        CORU_TRY(ensure_arena(c, meas.off));
-    }
-    Carver cv{c->arena, 0};
-    lay(cv, a_d, u_d, t_d, v_d, f_d);
-    cudaStream_t st = c->stream;
-    CORU_CUDA(cudaMemcpyAsync(a_d, A, sizeof(T) * m * n, cudaMemcpyHostToDevice, st));
-    CORU_CUDA(any_nonfinite<T>(a_d, m * n, f_d, st));
-    ++g_launches;
-    {
-        // The Matrix constructor rejects non-finite entries before any work (matrix.hpp:29-31).
-        int bad = 0;
-        CORU_CUDA(cudaMemcpyAsync(&bad, f_d, sizeof(int), cudaMemcpyDeviceToHost, st));
-        CORU_CUDA(cudaStreamSynchronize(st));
-        if (bad) return fail(CORU_EINVAL, "Matrix: non-finite entry");
-    }
-    coru_utv out{u_d, ell, t_d, ell, v_d, ell, perm, 0, 0};
+    coru_utv out{nullptr, ell, nullptr, ell, nullptr, ell, perm, 0, 0};
     Request<T> r;
-    r.A = a_d;
     r.lda = n;
-    r.d = int(ell);
+    r.d = d;
     r.q = q;
     r.seed = seed;
     r.stream = stream;
     r.variant = variant;
     r.perm_host = perm;
     r.warn_host = &out.conditioning_warning;
-    if (m < n) {
-        r.trans = true;
-        r.rows = n;
-        r.cols = m;
-        r.u = v_d;
-        r.ldu = ell;
-        r.v = u_d;
-        r.ldv = ell;
-        r.t = t_d;
-        r.ldt = ell;
-        r.t_transpose = true;
+    r.rows = trans ? n : m;
+    r.cols = trans ? m : n;
+    r.trans = trans;
+    r.t_transpose = trans;
+    // Reserve the head plus the workspace before anything is placed in the arena.
+    {
+        Work<T> w;
+        Carver meas{nullptr, head_bytes};
+        w.layout(meas, c, r, dp);
+        CORU_TRY(ensure_arena(c, meas.off));
+    }
+    Carver cv{c->arena, 0};
+    lay(cv, a_d, u_d, t_d, v_d, f_d);
+    r.A = a_d;
+    r.u = trans ? v_d : u_d;
+    r.ldu = ell;
+    r.v = trans ? u_d : v_d;
+    r.ldv = ell;
+    r.t = t_d;
+    r.ldt = ell;
+    cudaStream_t st = c->stream;
+    if (pipe) {
+        Work<T> w;  // the exact carving run() will use
+        Carver wc{c->arena, head_bytes};
+        w.layout(wc, c, r, dp);
+        CORU_TRY(gen_phi<T>(c, r, w.b2, dp));
+        CORU_CUDA(cudaMemsetAsync(f_d, 0, sizeof(int), st));
+        CORU_CUDA(cudaEventRecord(c->ev_fork, st));  // the copies may overwrite the arena from here on
+        CORU_CUDA(cudaStreamWaitEvent(c->aux, c->ev_fork, 0));
+        for (int i = 0; i < C; ++i) {
+            int64_t r0, rows;
+            chunk_rows(i, r0, rows);
+            CORU_CUDA(cudaMemcpyAsync(a_d + r0 * n, A + r0 * n, sizeof(T) * rows * n, cudaMemcpyHostToDevice, c->aux));
+            CORU_CUDA(cudaEventRecord(c->ev_chunk[i], c->aux));
+        }
+        const bool prof = c->prof;  // partial passes: not A-pass launches
+        c->prof = false;
+        int rc = CORU_OK;
+        for (int i = 0; i < C && rc == CORU_OK; ++i) {
+            int64_t r0, rows;
+            chunk_rows(i, r0, rows);
+            const T* ai = a_d + r0 * n;
+            if (cudaStreamWaitEvent(st, c->ev_chunk[i], 0) != cudaSuccess ||
+                any_nonfinite_acc<T>(ai, rows * n, f_d, st) != cudaSuccess) {
+                rc = fail(CORU_ECUDA, "upload pipeline launch failed");
+                break;
+            }
+            ++g_launches;
+            rc = gemm<T>(c, Op::N, ai, n, w.b2, dp, w.b1 + r0 * dp, dp, rows, n, d, cws, cwse);  // c1 rows
+            if (rc == CORU_OK)
+                rc = gemm<T>(c, Op::T, ai, n, w.b1 + r0 * dp, dp, parts + int64_t(i) * n * dp, dp, n, rows, d, cws, cwse);
+        }
+        c->prof = prof;
+        CORU_TRY(rc);
+        if (q == 0 && w.b2prev)  // c2_prev = Φ for the approx core (corutv.hpp:56)
+            CORU_CUDA(cudaMemcpyAsync(w.b2prev, w.b2, sizeof(T) * n * dp, cudaMemcpyDeviceToDevice, st));
+        CORU_CUDA(sum_chunks<T>(parts, C, n, d, dp, int64_t(n) * dp, w.b2, dp, st));  // c2 = a^T·c1, chunk order
+        ++g_launches;
+        r.first_done = true;
     } else {
-        r.rows = m;
-        r.cols = n;
-        r.u = u_d;
-        r.ldu = ell;
-        r.v = v_d;
-        r.ldv = ell;
-        r.t = t_d;
-        r.ldt = ell;
+        CORU_CUDA(cudaMemcpyAsync(a_d, A, sizeof(T) * m * n, cudaMemcpyHostToDevice, st));
+        CORU_CUDA(any_nonfinite<T>(a_d, m * n, f_d, st));
+        ++g_launches;
+    }
+    {
+        // The Matrix constructor rejects non-finite entries (matrix.hpp:29-31); no output is written.
+        int bad = 0;
+        CORU_CUDA(cudaMemcpyAsync(&bad, f_d, sizeof(int), cudaMemcpyDeviceToHost, st));
+        CORU_CUDA(cudaStreamSynchronize(st));
+        if (bad) return fail(CORU_EINVAL, "Matrix: non-finite entry");
     }
     CORU_TRY(run<T>(c, r, head_bytes));
     CORU_CUDA(cudaMemcpyAsync(U, u_d, sizeof(T) * m * ell, cudaMemcpyDeviceToHost, st));
@@ -1115,7 +1200,12 @@ int coru_ctx_create(int device, coru_ctx** out) {
     c->stream = c->own_stream;
     if (cudaStreamCreateWithFlags(&c->aux, cudaStreamNonBlocking) != cudaSuccess ||
         cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
-        cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming) != cudaSuccess) {
+        cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming) != cudaSuccess ||
+        [&] {
+            for (auto& e : c->ev_chunk)
+                if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) return true;
+            return false;
+        }()) {
         coru_ctx_destroy(c);
         return fail(CORU_ECUDA, "stream/event creation failed");
     }
@@ -1137,6 +1227,8 @@ void coru_ctx_destroy(coru_ctx* c) {
     }
     if (c->ev_fork) cudaEventDestroy(c->ev_fork);
     if (c->ev_join) cudaEventDestroy(c->ev_join);
+    for (auto& e : c->ev_chunk)
+        if (e) cudaEventDestroy(e);
     if (c->own_stream) cudaStreamDestroy(c->own_stream);
     for (auto& e : c->prof_events) {
         cudaEventDestroy(e.first);

@@ -944,6 +944,12 @@ cudaError_t any_nonfinite(const T* A, int64_t n, int* flag, cudaStream_t st) {
 }
 
 template <typename T>
+cudaError_t any_nonfinite_acc(const T* A, int64_t n, int* flag, cudaStream_t st) {
+    k_any_nonfinite<T><<<grid_for(n), 256, 0, st>>>(A, n, flag);
+    return cudaGetLastError();
+}
+
+template <typename T>
 cudaError_t transpose_square(const T* src, int lds, T* dst, int ldd, int d, cudaStream_t st) {
     k_transpose_square<T><<<grid_for(int64_t(d) * d), 256, 0, st>>>(src, lds, dst, ldd, d);
     return cudaGetLastError();
@@ -956,7 +962,8 @@ cudaError_t transpose_square(const T* src, int lds, T* dst, int ldd, int d, cuda
     template cudaError_t conditioning_flag<T>(const T*, int, int, int*, cudaStream_t);                            \
     template cudaError_t copy_block<T>(const T*, int64_t, T*, int64_t, int64_t, int, cudaStream_t);               \
     template cudaError_t transpose_square<T>(const T*, int, T*, int, int, cudaStream_t);                        \
-    template cudaError_t any_nonfinite<T>(const T*, int64_t, int*, cudaStream_t);
+    template cudaError_t any_nonfinite<T>(const T*, int64_t, int*, cudaStream_t);                               \
+    template cudaError_t any_nonfinite_acc<T>(const T*, int64_t, int*, cudaStream_t);
 CORU_INST(double)
 CORU_INST(float)
 #undef CORU_INST

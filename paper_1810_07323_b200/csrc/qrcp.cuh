@@ -29,6 +29,9 @@ cudaError_t copy_block(const T* src, int64_t lds, T* dst, int64_t ldd, int64_t r
 // flag = 1 if any of the n entries is non-finite (the Matrix constructor check, matrix.hpp:29-31).
 template <typename T>
 cudaError_t any_nonfinite(const T* A, int64_t n, int* flag, cudaStream_t st);
+// Same check, accumulating into a flag the caller zeroed (chunked uploads).
+template <typename T>
+cudaError_t any_nonfinite_acc(const T* A, int64_t n, int* flag, cudaStream_t st);
 
 // Transpose a d x d row-major block: dst(i,j) = src(j,i)  (ULV orientation, corutv.hpp:84-86).
 template <typename T>

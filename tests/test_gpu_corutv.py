@@ -219,3 +219,32 @@ def test_repeat_determinism_wide_sketch(ctx):
     for f in fs[1:]:
         assert np.array_equal(f.u, fs[0].u) and np.array_equal(f.t, fs[0].t) and np.array_equal(f.perm, fs[0].perm)
     assert rel_recon_error(a, fs[0].u, fs[0].t, fs[0].v) < 0.05
+
+
+@pytest.mark.parametrize("variant,q", [(0, 1), (1, 0), (1, 1)])
+def test_host_entry_upload_pipeline(ctx, monkeypatch, variant, q):
+    """Host-buffer entry on a 128 MB A: the chunked upload runs the first power round under the
+    H2D copy (its A^T·c1 sums chunk partials, so bits differ from the device entry by rounding).
+    Deterministic; equal to the device entry with the pipeline off; same quality as the device
+    entry; a NaN in the last chunk is still rejected (matrix.hpp:29-31)."""
+    import torch
+    import paper_1810_07323_b200 as cg
+    from workloads import make_host
+    a = make_host("C2q1")
+    v = cg.DVariant(variant)
+    h1 = cg.corutv(a, 60, q, v, cg.RngSeed(42, 0), ctx=ctx)
+    h2 = cg.corutv(a, 60, q, v, cg.RngSeed(42, 0), ctx=ctx)
+    assert np.array_equal(h1.u, h2.u) and np.array_equal(h1.t, h2.t) and np.array_equal(h1.v, h2.v)
+    dv = cg.corutv(torch.from_numpy(a).cuda(), 60, q, v, cg.RngSeed(42, 0), ctx=ctx)
+    e_h = rel_recon_error(a, h1.u, h1.t, h1.v)
+    e_d = rel_recon_error(a, dv.u.cpu().numpy(), dv.t.cpu().numpy(), dv.v.cpu().numpy())
+    assert abs(e_h - e_d) <= 0.05 * e_d  # C2 floors are ~1e-3 relative (SURVEY.md §8c)
+    assert orth_residual(h1.u) <= 1e-12 * 60 and orth_residual(h1.v) <= 1e-12 * 60
+    monkeypatch.setenv("CORU_NO_UPLOAD_PIPE", "1")
+    h3 = cg.corutv(a, 60, q, v, cg.RngSeed(42, 0), ctx=ctx)
+    assert np.array_equal(h3.t, dv.t.cpu().numpy()) and np.array_equal(h3.u, dv.u.cpu().numpy())
+    monkeypatch.delenv("CORU_NO_UPLOAD_PIPE")
+    bad = a.copy()
+    bad[-1, -1] = np.inf
+    with pytest.raises(cg.CoruInvalidArgument):
+        cg.corutv(bad, 60, q, v, cg.RngSeed(42, 0), ctx=ctx)
