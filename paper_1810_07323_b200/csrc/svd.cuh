@@ -27,6 +27,6 @@ cudaError_t svd_square(const T* Y, int64_t ldy, int d, T* U, int64_t ldu, T* sig
 template <typename T>
 cudaError_t svd_truncate_core(const double* ws, int d, int k, T* C, int64_t ldc, cudaStream_t st);
 constexpr int kSvdLaunches = 2;
-constexpr int kPinvLaunches = 2;
+constexpr int kPinvLaunches = 5;  // widen, QRCP, Jacobi, fix, assemble
 
 }  // namespace coru_gpu
