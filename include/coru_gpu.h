@@ -189,12 +189,59 @@ int coru_sor_svd_f64_dev(coru_ctx* ctx, const double* A, int64_t m, int64_t n, i
 int coru_sor_svd_f64(coru_ctx* ctx, const double* A, int64_t m, int64_t n, int64_t k, int64_t ell, int q, uint64_t seed,
                      uint64_t stream, double* L);
 
+/* ---- robust PCA by ALM with the CoR-UTV inner step: alm_rpca (rpca.hpp:95-169), fp64 ---------- */
+/* RpcaInner (rpca.hpp:53): only the CoR-UTV inner is provided; svt_exact (the full SVD of every
+ * m x n iterate, rpca.hpp:117-120) returns CORU_ENOTSUP. */
+enum coru_rpca_inner { CORU_RPCA_SVT_EXACT = 0, CORU_RPCA_CORUTV = 1 };
+/* CorutvThresholding (rpca.hpp:58): soft = svt of the compressed core (rpca.hpp:135-139), hard =
+ * cor_threshold (corutv.hpp:124-134, rpca.hpp:130-133). */
+enum coru_rpca_threshold { CORU_COR_SOFT = 0, CORU_COR_HARD = 1 };
+/* RpcaConfig (rpca.hpp:60-78), same fields, defaults and validation (CORU_EINVAL with the reference's
+ * messages). Defaults that need an SVD of M or of the iterate — mu0 <= 0 (1.25/||M||_2) and
+ * corutv_ell == 0 (predict_rank(X) + 2, per iteration) — are computed on the GPU from the Gram matrix
+ * X^T X and need cols(M) <= 1024 (CORU_ENOTSUP beyond). */
+typedef struct {
+    double lambda;   /* <= 0: 1/sqrt(max(m, n)) */
+    double mu0;      /* <= 0: 1.25/||M||_2 */
+    double rho;      /* continuation factor, > 1 (reference default 1.5) */
+    double mu_bar;   /* <= 0: mu0·1e7 */
+    double tol;      /* > 0 (reference default 1e-5) */
+    int max_iter;    /* >= 1 (reference default 50) */
+    int inner;       /* coru_rpca_inner */
+    int64_t corutv_ell; /* 0: predict_rank(X) + 2 each iteration */
+    int corutv_q;       /* >= 0 (reference default 1) */
+    int thresholding;   /* coru_rpca_threshold */
+} coru_rpca_config;
+/* Fills the reference's defaults (RpcaConfig{} with inner = corutv). */
+void coru_rpca_config_default(coru_rpca_config* cfg);
+/* RpcaResult (rpca.hpp:80-88) minus l and s (the caller's buffers). residuals: host, max_iter entries
+ * (may be NULL); zeta_j = ||M - L_j - S_j||_F / ||M||_F. */
+typedef struct {
+    int iterations;
+    double* residuals;
+    int64_t rank_l;
+    int64_t s_l0;
+    int converged;
+    int ell_clamped;
+} coru_rpca_result;
+/* M, L, S: device row-major m x n (ldm, ldl, lds >= n); M is never written. Iteration j draws its
+ * sketch from substream({seed, stream}, j) (rpca.hpp:129). Single GPU. */
+int coru_alm_rpca_f64_dev(coru_ctx* ctx, const double* M, int64_t m, int64_t n, int64_t ldm,
+                          const coru_rpca_config* cfg, uint64_t seed, uint64_t stream, double* L, int64_t ldl,
+                          double* S, int64_t lds, coru_rpca_result* res);
+/* Host-buffer drop-in for coru::alm_rpca: M, L, S host row-major dense m x n. */
+int coru_alm_rpca_f64(coru_ctx* ctx, const double* M, int64_t m, int64_t n, const coru_rpca_config* cfg,
+                      uint64_t seed, uint64_t stream, double* L, double* S, coru_rpca_result* res);
+
 /* A-pass profiling: when enabled, CUDA events are recorded on the launching stream around every
  * GEMM that streams the caller's A (the sketch, power and projection passes). The read call
  * returns the summed device time, the number of A-passes, and their algorithmic flops
  * (2·rows·cols·ell) and A bytes (rows·cols·sizeof(T)), then resets the counters. */
 int coru_ctx_set_profiling(coru_ctx* ctx, int enable);
 int coru_ctx_profile_apass(coru_ctx* ctx, double* total_ms, int64_t* launches, double* flops, double* bytes);
+/* The same for the fused lift + ALM update kernel of alm_rpca: algorithmic flops 2·m·n·ell (the lift
+ * L = Tp·V^T) and bytes 40·m·n per launch (read M, Y; write S, Y, X). */
+int coru_ctx_profile_rpca_update(coru_ctx* ctx, double* total_ms, int64_t* launches, double* flops, double* bytes);
 
 /* Number of this library's kernels launched by the calling thread since the last reset
  * (bench evidence: "gpu_launches"). */

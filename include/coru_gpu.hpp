@@ -159,6 +159,61 @@ inline Matrix sor_svd(const Matrix& a, std::size_t k, std::size_t ell, int q, Rn
     return out;
 }
 
+// RpcaInner / CorutvThresholding / RpcaConfig / RpcaResult (rpca.hpp:53-88). inner defaults to corutv,
+// the inner step this build provides (svt_exact throws std::runtime_error, CORU_ENOTSUP).
+enum class RpcaInner { svt_exact, corutv };
+enum class CorutvThresholding { soft, hard };
+struct RpcaConfig {
+    double lambda = 0.0;
+    double mu0 = 0.0;
+    double rho = 1.5;
+    double mu_bar = 0.0;
+    double tol = 1e-5;
+    int max_iter = 50;
+    RpcaInner inner = RpcaInner::corutv;
+    std::size_t corutv_ell = 0;
+    int corutv_q = 1;
+    CorutvThresholding corutv_thresholding = CorutvThresholding::soft;
+};
+struct RpcaResult {
+    Matrix l, s;
+    int iterations;
+    std::vector<double> residuals;
+    std::size_t rank_l;
+    std::size_t s_l0;
+    bool converged;
+    bool ell_clamped;
+};
+
+// alm_rpca (rpca.hpp:95-169) with the CoR-UTV inner step on the GPU.
+inline RpcaResult alm_rpca(const Matrix& m, const RpcaConfig& config, RngSeed seed) {
+    coru_rpca_config c;
+    c.lambda = config.lambda;
+    c.mu0 = config.mu0;
+    c.rho = config.rho;
+    c.mu_bar = config.mu_bar;
+    c.tol = config.tol;
+    c.max_iter = config.max_iter;
+    c.inner = config.inner == RpcaInner::corutv ? CORU_RPCA_CORUTV : CORU_RPCA_SVT_EXACT;
+    c.corutv_ell = std::int64_t(config.corutv_ell);
+    c.corutv_q = config.corutv_q;
+    c.thresholding = config.corutv_thresholding == CorutvThresholding::hard ? CORU_COR_HARD : CORU_COR_SOFT;
+    RpcaResult r{Matrix(m.rows(), m.cols()), Matrix(m.rows(), m.cols()), 0, {}, 0, 0, false, false};
+    r.residuals.assign(std::size_t(std::max(config.max_iter, 1)), 0.0);
+    coru_rpca_result res{};
+    res.residuals = r.residuals.data();
+    detail::throw_status(coru_alm_rpca_f64(detail::thread_context(), m.data().data(), std::int64_t(m.rows()),
+                                           std::int64_t(m.cols()), &c, seed.seed, seed.stream, r.l.data().data(),
+                                           r.s.data().data(), &res));
+    r.iterations = res.iterations;
+    r.residuals.resize(std::size_t(res.iterations));
+    r.rank_l = std::size_t(res.rank_l);
+    r.s_l0 = std::size_t(res.s_l0);
+    r.converged = res.converged != 0;
+    r.ell_clamped = res.ell_clamped != 0;
+    return r;
+}
+
 // singular_estimates (corutv.hpp:113-117)
 inline std::vector<double> singular_estimates(const UtvApprox& f) {
     std::vector<double> s(f.ell);

@@ -188,6 +188,103 @@ class Oracle:
         return Utv(u, t, v, bool(flags[0]), bool(flags[1]), perm)
 
 
+    # ---- alm_rpca with the CoR-UTV inner step: a numpy restatement of rpca.hpp:95-169 over the C
+    # restatement's sketch_bases / corutv / matmul / Jacobi SVD (bit-exact with the reference, pinned in
+    # tests/test_oracle.py against oracle/_ref and tests/golden/rpca_ref_cases.npz).
+    @staticmethod
+    def frobenius(a):
+        """frobenius_norm (matrix.hpp:133-137): serial left-to-right sum of squares (np.cumsum is serial)."""
+        a = np.ascontiguousarray(a, np.float64).ravel()
+        return float(np.sqrt(np.cumsum(a * a)[-1])) if a.size else 0.0
+
+    def singular_values(self, a):
+        """svd(a).sigma (svd.hpp:140-162): the Jacobi SVD of R from householder_qr when rows > cols, of a^T
+        when rows < cols."""
+        a = np.ascontiguousarray(a, np.float64)
+        if a.shape[0] < a.shape[1]:
+            a = np.ascontiguousarray(a.T)
+        if a.shape[0] > a.shape[1]:
+            a = self.householder_qr(a)[1]
+        return self.jacobi_svd_square(a)[1]
+
+    def alm_rpca(self, mat, lambda_=0.0, mu0=0.0, rho=1.5, mu_bar=0.0, tol=1e-5, max_iter=50, inner=1,
+                 corutv_ell=0, corutv_q=1, thresholding=0, seed=0, stream=0):
+        """alm_rpca (rpca.hpp:95-169), inner = corutv (rpca.hpp:121-140)."""
+        if rho <= 1.0 or tol <= 0.0 or max_iter < 1 or corutv_q < 0:
+            raise CoruError("RpcaConfig: invalid")                       # rpca.hpp:72-77
+        if inner != 1:
+            raise NotImplementedError("svt_exact inner is not restated")
+        mat = np.ascontiguousarray(mat, np.float64)
+        rows, cols = mat.shape
+        lam = lambda_ if lambda_ > 0.0 else 1.0 / np.sqrt(float(max(rows, cols)))
+        m_fro = self.frobenius(mat)
+        mu = mu0 if mu0 > 0.0 else 1.25 / float(self.singular_values(mat)[0])
+        mub = mu_bar if mu_bar > 0.0 else mu * 1e7
+        l = np.zeros_like(mat); s = np.zeros_like(mat); y = np.zeros_like(mat)
+        residuals = []; rank_l = 0; converged = False; clamped = False; it = 0
+        while it < max_iter:
+            it += 1
+            inv_mu = 1.0 / mu
+            x = mat - s
+            x += y * inv_mu                                               # rpca.hpp:114-115
+            if corutv_ell:
+                ell = corutv_ell
+            else:                                                         # predict_rank (rpca.hpp:45-51)
+                fro = self.frobenius(x)
+                if fro == 0.0:
+                    k = 0
+                else:
+                    sig = self.singular_values(x)
+                    nuc = float(np.cumsum(sig)[-1])
+                    kk = np.ceil((nuc / fro) * (nuc / fro) - 1e-9)
+                    k = 1 if kk < 1.0 else int(kk)
+                ell = k + 2
+            ell_max = min(rows, cols) - 1
+            if ell > ell_max:
+                ell = ell_max; clamped = True
+            ell = max(ell, 1)
+            if thresholding == 1:                                         # cor_threshold (corutv.hpp:124-134)
+                f = self.corutv(x, ell, corutv_q, 0, seed, stream + it)
+                est = np.abs(np.diag(f.t))
+                r = int(np.sum(est > inv_mu))
+                if r == 0:
+                    l = np.zeros_like(mat)
+                elif f.lower:                                             # truncate_rank_k (:106-110)
+                    l = self.matmul(self.matmul(f.u, np.ascontiguousarray(f.t[:, :r])), np.ascontiguousarray(f.v[:, :r].T))
+                else:
+                    l = self.matmul(self.matmul(np.ascontiguousarray(f.u[:, :r]), np.ascontiguousarray(f.t[:r, :])),
+                                    np.ascontiguousarray(f.v.T))
+            else:                                                         # rpca.hpp:135-139
+                q1, q2, _, _, _ = self.sketch_bases(x, ell, corutv_q, seed, stream + it)
+                d = self.matmul(self.matmul(np.ascontiguousarray(q1.T), x), q2)
+                u, sg, v, _ = self.svd_square(d)                          # svt (rpca.hpp:30-40)
+                r = 0
+                while r < len(sg) and sg[r] > inv_mu:
+                    r += 1
+                if r == 0:
+                    l = np.zeros_like(mat)
+                else:
+                    us = u[:, :r] * (sg[:r] - inv_mu)
+                    dthr = self.matmul(np.ascontiguousarray(us), np.ascontiguousarray(v[:, :r].T))
+                    l = self.matmul(self.matmul(q1, dthr), np.ascontiguousarray(q2.T))
+            rank_l = r
+            w = mat - l
+            w += y * inv_mu                                               # rpca.hpp:143-144
+            mag = np.abs(w) - lam * inv_mu                                # shrink (rpca.hpp:17-26)
+            s = np.where(mag > 0.0, np.where(w > 0.0, mag, -mag), 0.0)
+            resid = mat - l
+            resid -= s
+            y += mu * resid
+            mu = min(rho * mu, mub)
+            zeta = self.frobenius(resid) / m_fro
+            residuals.append(zeta)
+            if zeta < tol:
+                converged = True
+                break
+        return dict(l=l, s=s, iterations=it, residuals=np.array(residuals), rank_l=rank_l,
+                    s_l0=int(np.count_nonzero(s)), converged=converged, ell_clamped=clamped)
+
+
 class Reference:
     """The reference library itself, compiled from /root/reference headers (oracle/_ref)."""
 
@@ -214,6 +311,10 @@ class Reference:
         L.ref_corutv_batch.restype = _dbl
         L.ref_frobenius.argtypes = [_p, _i64, _i64]
         L.ref_frobenius.restype = _dbl
+        L.ref_alm_rpca.argtypes = [_p, _i64, _i64, _p, _p, _u64, _u64, _p, _p, _p, _p]
+        L.ref_gen_rpca_instance.argtypes = [_i64, _i64, _u64, _dbl, _u64, _u64, _p, _p, _p]
+        L.ref_spectral_norm.argtypes = [_p, _i64, _i64]
+        L.ref_spectral_norm.restype = _dbl
 
     def _check(self, rc):
         if rc == 1:
@@ -310,6 +411,33 @@ class Reference:
     def frobenius(self, a):
         a = np.ascontiguousarray(a, np.float64)
         return self.lib.ref_frobenius(_ptr(a), a.shape[0], a.reshape(a.shape[0], -1).shape[1])
+
+
+    def alm_rpca(self, mat, lambda_=0.0, mu0=0.0, rho=1.5, mu_bar=0.0, tol=1e-5, max_iter=50, inner=1,
+                 corutv_ell=0, corutv_q=1, thresholding=0, seed=0, stream=0):
+        """coru::alm_rpca (rpca.hpp:95-169); inner 1 = corutv, thresholding 0 = soft / 1 = hard."""
+        mat = np.ascontiguousarray(mat, np.float64)
+        m, n = mat.shape
+        cfg = np.array([lambda_, mu0, rho, mu_bar, tol], np.float64)
+        icfg = np.array([max_iter, inner, corutv_ell, corutv_q, thresholding], np.int64)
+        l, s = np.empty((m, n)), np.empty((m, n))
+        res = np.zeros(max_iter)
+        out = np.zeros(5, np.int64)
+        self._check(self.lib.ref_alm_rpca(_ptr(mat), m, n, _ptr(cfg), _ptr(icfg), seed, stream, _ptr(l), _ptr(s),
+                                          _ptr(res), _ptr(out)))
+        it = int(out[0])
+        return dict(l=l, s=s, iterations=it, residuals=res[:it].copy(), rank_l=int(out[1]), s_l0=int(out[2]),
+                    converged=bool(out[3]), ell_clamped=bool(out[4]))
+
+    def gen_rpca_instance(self, n, r, s, amplitude, seed, stream=0):
+        """coru::gen_rpca_instance (testgen.hpp:86-109) -> (m, l_true, s_true)."""
+        m, l, sp = np.empty((n, n)), np.empty((n, n)), np.empty((n, n))
+        self._check(self.lib.ref_gen_rpca_instance(n, r, s, amplitude, seed, stream, _ptr(m), _ptr(l), _ptr(sp)))
+        return m, l, sp
+
+    def spectral_norm(self, a):
+        a = np.ascontiguousarray(a, np.float64)
+        return self.lib.ref_spectral_norm(_ptr(a), a.shape[0], a.shape[1])
 
 
 def has_reference() -> bool:

@@ -20,6 +20,7 @@
 #include "coru/baselines.hpp"
 #include "coru/corutv.hpp"
 #include "coru/norms.hpp"
+#include "coru/rpca.hpp"
 #include "coru/testgen.hpp"
 
 using coru::Matrix;
@@ -269,5 +270,47 @@ int ref_gen_noisy_lowrank(int64_t n, int64_t k, double gap, uint64_t seed, uint6
 
 // coru::frobenius_norm (matrix.hpp:133-137)
 double ref_frobenius(const double* a, int64_t m, int64_t n) { return coru::frobenius_norm(wrap(a, m, n)); }
+
+// coru::alm_rpca (rpca.hpp:95-169). cfg: {lambda, mu0, rho, mu_bar, tol}; icfg: {max_iter, inner,
+// corutv_ell, corutv_q, thresholding}. out_i: {iterations, rank_l, s_l0, converged, ell_clamped}.
+int ref_alm_rpca(const double* m_, int64_t m, int64_t n, const double* cfg, const int64_t* icfg, uint64_t seed,
+                 uint64_t stream, double* l, double* s, double* residuals, int64_t* out_i) {
+    return guarded([&] {
+        coru::RpcaConfig c;
+        c.lambda = cfg[0];
+        c.mu0 = cfg[1];
+        c.rho = cfg[2];
+        c.mu_bar = cfg[3];
+        c.tol = cfg[4];
+        c.max_iter = int(icfg[0]);
+        c.inner = icfg[1] ? coru::RpcaInner::corutv : coru::RpcaInner::svt_exact;
+        c.corutv_ell = size_t(icfg[2]);
+        c.corutv_q = int(icfg[3]);
+        c.corutv_thresholding = icfg[4] ? coru::CorutvThresholding::hard : coru::CorutvThresholding::soft;
+        coru::RpcaResult r = coru::alm_rpca(wrap(m_, m, n), c, {seed, stream});
+        put(r.l, l);
+        put(r.s, s);
+        for (size_t i = 0; i < r.residuals.size(); ++i) residuals[i] = r.residuals[i];
+        out_i[0] = r.iterations;
+        out_i[1] = int64_t(r.rank_l);
+        out_i[2] = int64_t(r.s_l0);
+        out_i[3] = r.converged;
+        out_i[4] = r.ell_clamped;
+    });
+}
+
+// coru::gen_rpca_instance (testgen.hpp:86-109): m, l_true, s_true (n x n).
+int ref_gen_rpca_instance(int64_t n, int64_t r, uint64_t s, double amp, uint64_t seed, uint64_t stream, double* m,
+                          double* l, double* sp) {
+    return guarded([&] {
+        coru::RpcaInstance inst = coru::gen_rpca_instance(size_t(n), size_t(r), s, amp, {seed, stream});
+        put(inst.m, m);
+        put(inst.l_true, l);
+        put(inst.s_true, sp);
+    });
+}
+
+// coru::spectral_norm (norms.hpp:27)
+double ref_spectral_norm(const double* a, int64_t m, int64_t n) { return coru::spectral_norm(wrap(a, m, n)); }
 
 }  // extern "C"

@@ -171,6 +171,11 @@ def load_library():
     L.coru_tsr_svd_f64.argtypes = [p, p, i64, i64, i64, u64, u64, p, p, p, C.POINTER(i32)]
     L.coru_sor_svd_f64_dev.argtypes = [p, p, i64, i64, i64, i64, i64, i32, u64, u64, p, i64]
     L.coru_sor_svd_f64.argtypes = [p, p, i64, i64, i64, i64, i32, u64, u64, p]
+    L.coru_rpca_config_default.argtypes = [p]
+    L.coru_ctx_profile_rpca_update.argtypes = [p, C.POINTER(C.c_double), C.POINTER(i64), C.POINTER(C.c_double), C.POINTER(C.c_double)]
+    L.coru_rpca_config_default.restype = None
+    L.coru_alm_rpca_f64_dev.argtypes = [p, p, i64, i64, i64, p, u64, u64, p, i64, p, i64, p]
+    L.coru_alm_rpca_f64.argtypes = [p, p, i64, i64, p, u64, u64, p, p, p]
     _lib = L
     return L
 
@@ -253,6 +258,12 @@ class Context:
         """Summed device time of the A-passes since the last read (CUDA events on the launch stream)."""
         ms, n, fl, by = C.c_double(), C.c_int64(), C.c_double(), C.c_double()
         _check(self.lib.coru_ctx_profile_apass(self.h, C.byref(ms), C.byref(n), C.byref(fl), C.byref(by)))
+        return {"ms": ms.value, "launches": n.value, "flops": fl.value, "bytes": by.value}
+
+    def profile_rpca_update(self) -> dict:
+        """Summed device time of alm_rpca's fused lift + update kernel since the last read."""
+        ms, n, fl, by = C.c_double(), C.c_int64(), C.c_double(), C.c_double()
+        _check(self.lib.coru_ctx_profile_rpca_update(self.h, C.byref(ms), C.byref(n), C.byref(fl), C.byref(by)))
         return {"ms": ms.value, "launches": n.value, "flops": fl.value, "bytes": by.value}
 
     @staticmethod
@@ -584,3 +595,87 @@ def sor_svd(a, k: int, ell: int, q: int, seed: RngSeed = RngSeed(), ctx: Optiona
     out = np.empty((m, n))
     _check(ctx.lib.coru_sor_svd_f64(ctx.h, a.ctypes.data, m, n, k, ell, q, seed.seed, seed.stream, out.ctypes.data))
     return out
+
+
+# ---- robust PCA: alm_rpca with the CoR-UTV inner step (rpca.hpp:53-169) ------------------------
+class RpcaInner(enum.IntEnum):
+    svt_exact = 0   # rpca.hpp:53 — not provided (CORU_ENOTSUP)
+    corutv = 1
+
+
+class CorutvThresholding(enum.IntEnum):
+    soft = 0        # rpca.hpp:58
+    hard = 1
+
+
+class _RpcaConfig(C.Structure):
+    _fields_ = [("lambda_", C.c_double), ("mu0", C.c_double), ("rho", C.c_double), ("mu_bar", C.c_double),
+                ("tol", C.c_double), ("max_iter", C.c_int), ("inner", C.c_int), ("corutv_ell", C.c_int64),
+                ("corutv_q", C.c_int), ("thresholding", C.c_int)]
+
+
+class _RpcaResult(C.Structure):
+    _fields_ = [("iterations", C.c_int), ("residuals", C.c_void_p), ("rank_l", C.c_int64), ("s_l0", C.c_int64),
+                ("converged", C.c_int), ("ell_clamped", C.c_int)]
+
+
+@dataclass
+class RpcaConfig:
+    """RpcaConfig (rpca.hpp:60-78): same fields and defaults, except inner defaults to corutv (the one
+    inner step this build provides)."""
+    lambda_: float = 0.0
+    mu0: float = 0.0
+    rho: float = 1.5
+    mu_bar: float = 0.0
+    tol: float = 1e-5
+    max_iter: int = 50
+    inner: RpcaInner = RpcaInner.corutv
+    corutv_ell: int = 0
+    corutv_q: int = 1
+    corutv_thresholding: CorutvThresholding = CorutvThresholding.soft
+
+    def _c(self) -> _RpcaConfig:
+        return _RpcaConfig(float(self.lambda_), float(self.mu0), float(self.rho), float(self.mu_bar),
+                           float(self.tol), int(self.max_iter), int(self.inner), int(self.corutv_ell),
+                           int(self.corutv_q), int(self.corutv_thresholding))
+
+
+@dataclass
+class RpcaResult:
+    """RpcaResult (rpca.hpp:80-88)."""
+    l: Any
+    s: Any
+    iterations: int
+    residuals: list
+    rank_l: int
+    s_l0: int
+    converged: bool
+    ell_clamped: bool
+
+
+def alm_rpca(m, config: RpcaConfig = RpcaConfig(), seed: RngSeed = RngSeed(),
+             ctx: Optional[Context] = None) -> RpcaResult:
+    """alm_rpca(m, config, seed) (rpca.hpp:95-169) with the CoR-UTV inner step on the GPU. ``m`` is a numpy
+    array (host entry: copies in and out) or a CUDA float64 tensor (device entry)."""
+    ctx = ctx or default_context()
+    rows, cols = m.shape
+    cfg = config._c()
+    resid = np.zeros(max(int(config.max_iter), 1))
+    res = _RpcaResult()
+    res.residuals = resid.ctypes.data
+    if _is_torch(m):
+        import torch
+        assert m.dtype == torch.float64
+        l = torch.empty((rows, cols), dtype=torch.float64, device=m.device)
+        s = torch.empty((rows, cols), dtype=torch.float64, device=m.device)
+        _torch_sync_stream(ctx, m)
+        _check(ctx.lib.coru_alm_rpca_f64_dev(ctx.h, m.data_ptr(), rows, cols, m.stride(0), C.byref(cfg), seed.seed,
+                                             seed.stream, l.data_ptr(), cols, s.data_ptr(), cols, C.byref(res)))
+    else:
+        m = np.ascontiguousarray(m, np.float64)
+        l = np.empty((rows, cols))
+        s = np.empty((rows, cols))
+        _check(ctx.lib.coru_alm_rpca_f64(ctx.h, m.ctypes.data, rows, cols, C.byref(cfg), seed.seed, seed.stream,
+                                         l.ctypes.data, s.ctypes.data, C.byref(res)))
+    return RpcaResult(l, s, res.iterations, list(resid[:res.iterations]), int(res.rank_l), int(res.s_l0),
+                      bool(res.converged), bool(res.ell_clamped))

@@ -30,6 +30,7 @@
 #include "qrcp.cuh"
 #include "cholqr.cuh"
 #include "rng_dev.cuh"
+#include "rpca.cuh"
 #include "svd.cuh"
 #include "tsqr.cuh"
 
@@ -192,6 +193,10 @@ struct coru_ctx {
     std::vector<std::pair<cudaEvent_t, cudaEvent_t>> prof_events;
     size_t prof_used = 0;
     double prof_flops = 0, prof_bytes = 0;
+    // the same for the fused ALM lift + update kernel of alm_rpca (rpca.cu)
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> upd_events;
+    size_t upd_used = 0;
+    double upd_flops = 0, upd_bytes = 0;
 };
 
 namespace {
@@ -1149,6 +1154,312 @@ int sor_impl(coru_ctx* c, const double* A, int64_t m, int64_t n, int64_t lda, in
     return CORU_OK;
 }
 
+// RpcaConfig::validate (rpca.hpp:72-77) and the inner-step switches this build provides.
+int check_rpca(const coru_rpca_config* cf, int64_t m, int64_t n) {
+    if (!cf) return fail(CORU_EINVAL, "null config");
+    if (m < 1 || n < 1) return fail(CORU_EINVAL, "Matrix: dimensions must be positive");
+    if (!(cf->rho > 1.0)) return fail(CORU_EINVAL, "RpcaConfig: rho must be > 1");
+    if (!(cf->tol > 0.0)) return fail(CORU_EINVAL, "RpcaConfig: tol must be > 0");
+    if (cf->max_iter < 1) return fail(CORU_EINVAL, "RpcaConfig: max_iter must be >= 1");
+    if (cf->corutv_q < 0) return fail(CORU_EINVAL, "RpcaConfig: corutv_q must be >= 0");
+    if (cf->inner == CORU_RPCA_SVT_EXACT)
+        return fail(CORU_ENOTSUP, "alm_rpca: the svt_exact inner (full SVD of the iterate) is not provided");
+    if (cf->inner != CORU_RPCA_CORUTV) return fail(CORU_EINVAL, "alm_rpca: unknown inner");
+    if (cf->thresholding != CORU_COR_SOFT && cf->thresholding != CORU_COR_HARD)
+        return fail(CORU_EINVAL, "alm_rpca: unknown thresholding");
+    if ((cf->mu0 <= 0.0 || cf->corutv_ell == 0) && n > 1024)
+        return fail(CORU_ENOTSUP, "alm_rpca: mu0 / predict_rank defaults need cols <= 1024");
+    return CORU_OK;
+}
+
+// alm_rpca (rpca.hpp:95-169) with the CoR-UTV inner step, M device m x n. Iterate buffers: X (the
+// inner step's input; X_1 = M exactly, so the first step reads M), Y; S is the caller's. One host
+// sync per iteration (zeta, rank; the predicted ell before the sketch when corutv_ell == 0).
+int rpca_impl(coru_ctx* c, const double* Min, int64_t m, int64_t n, int64_t ldm, const coru_rpca_config& cf,
+              uint64_t seed, uint64_t stream, double* Lout, int64_t ldl, double* Sout, int64_t lds,
+              coru_rpca_result* res, size_t off, size_t* need = nullptr) {
+    const bool hard = cf.thresholding == CORU_COR_HARD;
+    const bool predict = cf.corutv_ell == 0;
+    const bool gram = predict || cf.mu0 <= 0.0;
+    const int64_t ell_max = std::min(m, n) - 1;
+    const int dmax = int(std::max<int64_t>(1, predict ? ell_max : std::min(cf.corutv_ell, std::max<int64_t>(ell_max, 1))));
+    const int dpm = int(round_up(dmax, 8));
+    const int sms = c->num_sms;
+    const int nparts = rpca_parts(m, n, sms);
+    const bool trans = hard && m < n;  // cor_threshold's corutv runs the ULV orientation on A^T
+    struct Lay {
+        double *x, *y, *q1, *q2, *w, *tp, *dm, *cc, *du, *dv, *sig, *pws, *gws, *parts, *scal, *g, *gpws, *gsig;
+        int* ints;
+        unsigned long long* cnt;
+        int64_t gwse;
+    } l{};
+    auto lay = [&](Carver& cv) {
+        l.x = cv.take<double>(m * n);
+        l.y = cv.take<double>(m * n);
+        l.q1 = cv.take<double>(m * dpm);  // Q1 (soft) / U (hard)
+        l.q2 = cv.take<double>(n * dpm);  // Q2 (soft) / V (hard)
+        l.w = cv.take<double>(m * dpm);
+        l.tp = cv.take<double>(m * dpm);
+        l.dm = cv.take<double>(int64_t(dpm) * dpm);  // D (soft) / T (hard)
+        l.cc = cv.take<double>(int64_t(dpm) * dpm);  // svt(D) (soft) / truncated T (hard)
+        l.du = cv.take<double>(int64_t(dpm) * dpm);
+        l.dv = cv.take<double>(int64_t(dpm) * dpm);
+        l.sig = cv.take<double>(dpm);
+        l.pws = cv.take<double>(pinv_ws_doubles(dmax));
+        l.gwse = 0;
+        for (int d = 1; d <= dmax; d = d < dmax ? std::min(dmax, d * 2) : dmax + 1)
+            l.gwse = std::max({l.gwse, gemm_ws<double>(Op::N, m, n, d, sms), gemm_ws<double>(Op::T, d, m, d, sms),
+                               gemm_ws<double>(Op::N, m, d, d, sms)});
+        l.gwse = std::max(l.gwse, gemm_ws<double>(Op::N, m, dmax, dmax, sms));
+        if (gram) l.gwse = std::max(l.gwse, gemm_ws<double>(Op::T, n, m, int(n), sms));
+        l.gws = cv.take<double>(l.gwse);
+        l.parts = cv.take<double>(nparts);
+        l.scal = cv.take<double>(8);
+        l.ints = cv.take<int>(8);
+        l.cnt = cv.take<unsigned long long>(1);
+        if (gram) {
+            l.g = cv.take<double>(n * n);
+            l.gsig = cv.take<double>(n);
+            l.gpws = cv.take<double>(pinv_ws_doubles(int(n)));
+        }
+    };
+    Carver meas{nullptr, off};
+    lay(meas);
+    const size_t work_off = (meas.off + 255) / 256 * 256;
+    {
+        // the inner step carves its workspace after ours: size the arena for every ell it may use
+        size_t top = work_off;
+        for (int d = 1; d <= dmax; ++d) {
+            if (!predict && d != dmax) continue;
+            Request<double> probe;
+            probe.rows = trans ? n : m;
+            probe.cols = trans ? m : n;
+            probe.trans = trans;
+            probe.d = d;
+            probe.mode = hard ? Mode::Full : Mode::Sketch;
+            Work<double> w;
+            Carver wm{nullptr, work_off};
+            w.layout(wm, c, probe, int(round_up(d, 8)));
+            top = std::max(top, wm.off);
+        }
+        if (need) {
+            *need = top;
+            return CORU_OK;
+        }
+        CORU_TRY(ensure_arena(c, top));
+    }
+    Carver cv{c->arena, off};
+    lay(cv);
+    cudaStream_t st = c->stream;
+    auto cuda_ok = [&](cudaError_t e, const char* what) {
+        return e == cudaSuccess ? CORU_OK : fail(CORU_ECUDA, std::string(what) + ": " + cudaGetErrorString(e));
+    };
+    auto fro_sq = [&](const double* A, int64_t lda, double* out) -> int {  // frobenius_norm² (matrix.hpp:133-137)
+        CORU_TRY(cuda_ok(sumsq_parts(A, lda, m, n, l.parts, nparts, st), "sumsq"));
+        CORU_TRY(cuda_ok(sum_parts(l.parts, nparts, out, st), "sum_parts"));
+        g_launches += 2;
+        return CORU_OK;
+    };
+    // Gram-matrix norms of an m x n iterate: out[0] = ||A||_2, out[1] = ||A||_*, out[2] = ||A||_F²
+    auto gram_norms_of = [&](const double* A, int64_t lda, double* h) -> int {
+        const bool prof = c->prof;
+        c->prof = false;
+        int rc = gemm<double>(c, Op::T, A, lda, A, lda, l.g, n, n, m, int(n), l.gws, l.gwse);
+        c->prof = prof;
+        CORU_TRY(rc);
+        CORU_TRY(cuda_ok(svd_square<double>(l.g, n, int(n), l.g, n, l.gsig, l.g, n, l.gpws, nullptr, c->max_smem, st),
+                         "svd_square(gram)"));
+        CORU_TRY(cuda_ok(gram_norms(l.gsig, int(n), l.scal + 4, st), "gram_norms"));
+        g_launches += kSvdLaunches + 1;
+        CORU_TRY(fro_sq(A, lda, l.scal + 6));
+        CORU_CUDA(cudaMemcpyAsync(h, l.scal + 4, 3 * sizeof(double), cudaMemcpyDeviceToHost, st));
+        CORU_CUDA(cudaStreamSynchronize(st));
+        return CORU_OK;
+    };
+
+    double h3[3];
+    const double lambda = cf.lambda > 0.0 ? cf.lambda : 1.0 / std::sqrt(double(std::max(m, n)));
+    CORU_TRY(fro_sq(Min, ldm, l.scal));
+    double mfro2 = 0.0;
+    CORU_CUDA(cudaMemcpyAsync(&mfro2, l.scal, sizeof(double), cudaMemcpyDeviceToHost, st));
+    CORU_CUDA(cudaStreamSynchronize(st));
+    const double m_fro = std::sqrt(mfro2);
+    double mu = cf.mu0;
+    if (mu <= 0.0) {
+        CORU_TRY(gram_norms_of(Min, ldm, h3));
+        mu = 1.25 / h3[0];
+    }
+    const double mu_bar = cf.mu_bar > 0.0 ? cf.mu_bar : mu * 1e7;
+    CORU_CUDA(cudaMemsetAsync(l.y, 0, sizeof(double) * m * n, st));
+    const double* X = Min;  // X_1 = (M - 0) + 0·inv_mu = M
+    int64_t ldx = ldm;
+    res->iterations = 0;
+    res->converged = 0;
+    res->ell_clamped = 0;
+    res->rank_l = 0;
+    int last_d = 1;
+    int it = 0;
+    while (it < cf.max_iter) {
+        ++it;
+        const double inv_mu = 1.0 / mu;
+        int64_t ell = cf.corutv_ell;
+        if (predict) {  // predict_rank(x) + 2 (rpca.hpp:45-51,122)
+            CORU_TRY(gram_norms_of(X, ldx, h3));
+            const double fro = std::sqrt(h3[2]);
+            int64_t k = 0;
+            if (fro != 0.0) {
+                const double ratio = h3[1] / fro;
+                const double kk = std::ceil(ratio * ratio - 1e-9);
+                k = kk < 1.0 ? 1 : int64_t(kk);
+            }
+            ell = k + 2;
+        }
+        if (ell > ell_max) {
+            ell = ell_max;
+            res->ell_clamped = 1;
+        }
+        if (ell < 1) ell = 1;
+        const int d = int(ell), dp = int(round_up(d, 8));
+        const uint64_t it_stream = stream + uint64_t(it);  // substream(seed, it) (rpca.hpp:129)
+        const double* Vb = nullptr;
+        if (hard) {
+            // cor_threshold(x, inv_mu, ell, q, iter_seed) (corutv.hpp:124-134)
+            CORU_TRY(check_params(m, n, ell, cf.corutv_q));
+            Request<double> r;
+            r.A = X;
+            r.lda = ldx;
+            r.d = d;
+            r.q = cf.corutv_q;
+            r.seed = seed;
+            r.stream = it_stream;
+            r.variant = CORU_D_EXACT;
+            int warn = 0;
+            r.warn_host = &warn;
+            r.trans = trans;
+            r.rows = trans ? n : m;
+            r.cols = trans ? m : n;
+            r.u = trans ? l.q2 : l.q1;
+            r.ldu = dp;
+            r.v = trans ? l.q1 : l.q2;
+            r.ldv = dp;
+            r.t = l.dm;
+            r.ldt = dp;
+            r.t_transpose = trans;
+            CORU_TRY(run<double>(c, r, work_off));
+            CORU_TRY(cuda_ok(cor_truncate(l.dm, dp, d, inv_mu, trans ? 1 : 0, l.cc, dp, l.ints, st), "cor_truncate"));
+            ++g_launches;
+        } else {
+            // sketch_bases(x, ell, q, iter_seed); D = (Q1^T x) Q2; svt(D, inv_mu) (rpca.hpp:135-137)
+            if (ell >= std::min(m, n)) return fail(CORU_ENOTSUP, "alm_rpca: the soft inner needs min(rows, cols) >= 2");
+            Request<double> r;
+            r.A = X;
+            r.lda = ldx;
+            r.rows = m;
+            r.cols = n;
+            r.d = d;
+            r.q = cf.corutv_q;
+            r.seed = seed;
+            r.stream = it_stream;
+            r.mode = Mode::Sketch;
+            r.q1 = l.q1;
+            r.ldq1 = dp;
+            r.q2 = l.q2;
+            r.ldq2 = dp;
+            int warn = 0;
+            r.warn_host = &warn;
+            CORU_TRY(run<double>(c, r, work_off));
+            CORU_TRY(gemm<double>(c, Op::N, X, ldx, l.q2, dp, l.w, dp, m, n, d, l.gws, l.gwse));  // X·Q2 (A-pass)
+            const bool prof = c->prof;
+            c->prof = false;
+            int rc = gemm<double>(c, Op::T, l.q1, dp, l.w, dp, l.dm, dp, d, m, d, l.gws, l.gwse);
+            c->prof = prof;
+            CORU_TRY(rc);
+            // The preconditioned Jacobi (QRCP first) halves the sweeps on graded cores, but the RPCA core
+            // (rank-ell signal, flat spectrum) gains nothing and pays the QRCP: off unless asked for.
+            static const bool precond = getenv("CORU_RPCA_SVD_PRECOND") != nullptr &&
+                                        atoi(getenv("CORU_RPCA_SVD_PRECOND")) != 0;
+            if (precond) {
+                CORU_TRY(cuda_ok(svd_factors_precond<double>(l.dm, dp, d, l.pws, c->max_smem, st), "svd_factors"));
+                g_launches += 4;
+            } else {
+                CORU_TRY(cuda_ok(svd_square<double>(l.dm, dp, d, l.du, dp, l.sig, l.dv, dp, l.pws, nullptr, c->max_smem,
+                                                    st),
+                                 "svd_square"));
+                g_launches += kSvdLaunches;
+            }
+            CORU_TRY(cuda_ok(svt_core<double>(l.pws, d, inv_mu, l.cc, dp, l.ints, st), "svt_core"));
+            ++g_launches;
+        }
+        Vb = l.q2;  // V (hard) / Q2 (soft), n x d
+        {
+            // Tp = U·Tr (hard) / Q1·svt(D) (soft): L = Tp·V^T is formed inside the update kernel
+            const bool prof = c->prof;
+            c->prof = false;
+            const int rc = gemm<double>(c, Op::N, l.q1, dp, l.cc, dp, l.tp, dp, m, d, d, l.gws, l.gwse);
+            c->prof = prof;
+            CORU_TRY(rc);
+        }
+        const double mu_next = std::min(cf.rho * mu, mu_bar);
+        RpcaStep p;
+        p.inv_mu = inv_mu;
+        p.mu = mu;
+        p.thresh = lambda * inv_mu;
+        p.inv_mu_next = 1.0 / mu_next;
+        cudaEvent_t ustop = nullptr;
+        if (c->prof) {
+            if (c->upd_used == c->upd_events.size()) {
+                cudaEvent_t a, b;
+                CORU_CUDA(cudaEventCreate(&a));
+                CORU_CUDA(cudaEventCreate(&b));
+                c->upd_events.emplace_back(a, b);
+            }
+            auto& ev = c->upd_events[c->upd_used++];
+            CORU_CUDA(cudaEventRecord(ev.first, st));
+            ustop = ev.second;
+        }
+        CORU_TRY(cuda_ok(rpca_lift_update(l.tp, dp, Vb, dp, d, m, n, Min, ldm, l.y, n, l.x, n, Sout, lds, nullptr, 0, p,
+                                          false, l.parts, nparts, st),
+                         "rpca_lift_update"));
+        if (ustop) {
+            CORU_CUDA(cudaEventRecord(ustop, st));
+            c->upd_flops += 2.0 * double(m) * double(n) * d;
+            c->upd_bytes += 40.0 * double(m) * double(n);  // read M, Y; write S, Y, X (L never written)
+        }
+        CORU_TRY(cuda_ok(sum_parts(l.parts, nparts, l.scal + 1, st), "sum_parts"));
+        g_launches += 2;
+        double zsq = 0.0;
+        int rank = 0;
+        CORU_CUDA(cudaMemcpyAsync(&zsq, l.scal + 1, sizeof(double), cudaMemcpyDeviceToHost, st));
+        CORU_CUDA(cudaMemcpyAsync(&rank, l.ints, sizeof(int), cudaMemcpyDeviceToHost, st));
+        CORU_CUDA(cudaStreamSynchronize(st));
+        res->rank_l = rank;
+        mu = mu_next;
+        X = l.x;
+        ldx = n;
+        last_d = d;
+        const double zeta = std::sqrt(zsq) / m_fro;
+        if (res->residuals) res->residuals[it - 1] = zeta;
+        if (zeta < cf.tol) {
+            res->converged = 1;
+            break;
+        }
+    }
+    res->iterations = it;
+    // the final L from the last step's factors (rpca.hpp:139 / :131), written once
+    RpcaStep p0{};
+    CORU_TRY(cuda_ok(rpca_lift_update(l.tp, int(round_up(last_d, 8)), l.q2, int(round_up(last_d, 8)), last_d, m, n,
+                                      nullptr, 0, nullptr, 0, nullptr, 0, nullptr, 0, Lout, ldl, p0, true, l.parts,
+                                      nparts, st),
+                     "rpca_lift"));
+    CORU_TRY(cuda_ok(count_nonzero(Sout, lds, m, n, l.cnt, st), "count_nonzero"));
+    g_launches += 2;
+    unsigned long long nz = 0;
+    CORU_CUDA(cudaMemcpyAsync(&nz, l.cnt, sizeof(nz), cudaMemcpyDeviceToHost, st));
+    CORU_CUDA(cudaStreamSynchronize(st));
+    res->s_l0 = int64_t(nz);
+    return CORU_OK;
+}
+
 // Upload a host matrix into the arena head (validating finiteness like the Matrix constructor).
 int upload_checked(coru_ctx* c, const double* A, int64_t count, double* a_d, int* f_d) {
     cudaStream_t st = c->stream;
@@ -1234,6 +1545,10 @@ void coru_ctx_destroy(coru_ctx* c) {
         cudaEventDestroy(e.first);
         cudaEventDestroy(e.second);
     }
+    for (auto& e : c->upd_events) {
+        cudaEventDestroy(e.first);
+        cudaEventDestroy(e.second);
+    }
     delete c;
 }
 
@@ -1269,6 +1584,25 @@ int coru_ctx_profile_apass(coru_ctx* c, double* total_ms, int64_t* launches, dou
     if (bytes) *bytes = c->prof_bytes;
     c->prof_used = 0;
     c->prof_flops = c->prof_bytes = 0;
+    return CORU_OK;
+}
+
+int coru_ctx_profile_rpca_update(coru_ctx* c, double* total_ms, int64_t* launches, double* flops, double* bytes) {
+    CORU_TRY(enter(c));
+    std::lock_guard<std::mutex> lk(c->mu);
+    double ms = 0;
+    for (size_t i = 0; i < c->upd_used; ++i) {
+        float t = 0;
+        CORU_CUDA(cudaEventSynchronize(c->upd_events[i].second));
+        CORU_CUDA(cudaEventElapsedTime(&t, c->upd_events[i].first, c->upd_events[i].second));
+        ms += t;
+    }
+    if (total_ms) *total_ms = ms;
+    if (launches) *launches = int64_t(c->upd_used);
+    if (flops) *flops = c->upd_flops;
+    if (bytes) *bytes = c->upd_bytes;
+    c->upd_used = 0;
+    c->upd_flops = c->upd_bytes = 0;
     return CORU_OK;
 }
 
@@ -1704,6 +2038,65 @@ int coru_qrcp_f64_dev(coru_ctx* c, const double* M, int64_t ldm, int64_t n, doub
     CORU_CUDA(qrcp<double>(M, int(ldm), int(n), Q, int(ldq), R, int(ldr), p, scr, c->max_smem, c->stream));
     ++g_launches;
     CORU_CUDA(cudaMemcpyAsync(perm, p, sizeof(int64_t) * n, cudaMemcpyDeviceToHost, c->stream));
+    CORU_CUDA(cudaStreamSynchronize(c->stream));
+    return CORU_OK;
+}
+
+void coru_rpca_config_default(coru_rpca_config* cf) {
+    if (!cf) return;
+    cf->lambda = 0.0;
+    cf->mu0 = 0.0;
+    cf->rho = 1.5;
+    cf->mu_bar = 0.0;
+    cf->tol = 1e-5;
+    cf->max_iter = 50;
+    cf->inner = CORU_RPCA_CORUTV;
+    cf->corutv_ell = 0;
+    cf->corutv_q = 1;
+    cf->thresholding = CORU_COR_SOFT;
+}
+
+int coru_alm_rpca_f64_dev(coru_ctx* c, const double* M, int64_t m, int64_t n, int64_t ldm, const coru_rpca_config* cf,
+                          uint64_t seed, uint64_t stream, double* L, int64_t ldl, double* S, int64_t lds,
+                          coru_rpca_result* res) {
+    CORU_TRY(enter(c));
+    std::lock_guard<std::mutex> lk(c->mu);
+    CORU_TRY(check_rpca(cf, m, n));
+    if (!M || !L || !S || !res || ldm < n || ldl < n || lds < n) return fail(CORU_EINVAL, "bad argument");
+    if (c->world > 1) return fail(CORU_EINVAL, "alm_rpca: single-GPU entry");
+    size_t need = 0;
+    CORU_TRY(rpca_impl(c, M, m, n, ldm, *cf, seed, stream, L, ldl, S, lds, res, 0, &need));
+    CORU_TRY(ensure_arena(c, need));
+    return rpca_impl(c, M, m, n, ldm, *cf, seed, stream, L, ldl, S, lds, res, 0);
+}
+
+int coru_alm_rpca_f64(coru_ctx* c, const double* M, int64_t m, int64_t n, const coru_rpca_config* cf, uint64_t seed,
+                      uint64_t stream, double* L, double* S, coru_rpca_result* res) {
+    CORU_TRY(enter(c));
+    std::lock_guard<std::mutex> lk(c->mu);
+    CORU_TRY(check_rpca(cf, m, n));
+    if (!M || !L || !S || !res) return fail(CORU_EINVAL, "null argument");
+    if (c->world > 1) return fail(CORU_EINVAL, "host-buffer entry is single-GPU");
+    Carver head{nullptr, 0};
+    double *m_d, *l_d, *s_d;
+    int* f_d;
+    auto lay = [&](Carver& cv) {
+        m_d = cv.take<double>(m * n);
+        l_d = cv.take<double>(m * n);
+        s_d = cv.take<double>(m * n);
+        f_d = cv.take<int>(4);
+    };
+    lay(head);
+    const size_t hb = (head.off + 255) / 256 * 256;
+    size_t need = 0;
+    CORU_TRY(rpca_impl(c, nullptr, m, n, n, *cf, seed, stream, nullptr, n, nullptr, n, res, hb, &need));
+    CORU_TRY(ensure_arena(c, need));
+    Carver cv{c->arena, 0};
+    lay(cv);
+    CORU_TRY(upload_checked(c, M, m * n, m_d, f_d));
+    CORU_TRY(rpca_impl(c, m_d, m, n, n, *cf, seed, stream, l_d, n, s_d, n, res, hb));
+    CORU_CUDA(cudaMemcpyAsync(L, l_d, sizeof(double) * m * n, cudaMemcpyDeviceToHost, c->stream));
+    CORU_CUDA(cudaMemcpyAsync(S, s_d, sizeof(double) * m * n, cudaMemcpyDeviceToHost, c->stream));
     CORU_CUDA(cudaStreamSynchronize(c->stream));
     return CORU_OK;
 }

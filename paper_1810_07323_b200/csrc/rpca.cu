@@ -1,0 +1,253 @@
+// ALM robust PCA with the CoR-UTV inner step (rpca.hpp:95-169): the lift fused with the ALM
+// update, cor_threshold's truncation, and the reductions of the loop. See rpca.cuh.
+#include "rpca.cuh"
+
+#include <algorithm>
+
+#include "common.cuh"
+
+namespace coru_gpu {
+namespace {
+
+constexpr int kTile = 64;  // L tile (kTile x kTile) per CTA iteration
+constexpr int kKc = 32;    // k-chunk of Tp / Vb staged in shared memory
+constexpr int kThreads = 256;
+
+__device__ __forceinline__ double block_sum(double v, double* red) {
+    v = warp_sum(v);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (lane == 0) red[warp] = v;
+    __syncthreads();
+    double s = 0.0;
+    if (threadIdx.x == 0)
+        for (int w = 0; w < kThreads / 32; ++w) s += red[w];  // fixed order
+    __syncthreads();
+    return s;
+}
+
+// Each CTA walks tiles blockIdx.x, blockIdx.x + gridDim.x, ... (fixed order). Thread (ty, tx) of the
+// 16 x 16 layout owns rows ty + 16·i and columns tx + 16·j of the tile: a half-warp covers 128
+// contiguous bytes of a row of M / Y / S / X. The tile's M and Y are requested with cp.async into
+// shared memory before the k-loop, so their DRAM latency hides under the lift's FMAs (2 CTAs/SM).
+template <bool VEC>
+__global__ void __launch_bounds__(kThreads, 2) k_rpca_lift_update(const double* __restrict__ Tp, int64_t ldt,
+                                                                  const double* __restrict__ Vb, int64_t ldv, int d,
+                                                                  int64_t m, int64_t n, const double* __restrict__ M,
+                                                                  int64_t ldm, double* __restrict__ Y, int64_t ldy,
+                                                                  double* __restrict__ X, int64_t ldx,
+                                                                  double* __restrict__ S, int64_t lds,
+                                                                  double* __restrict__ L, int64_t ldl, RpcaStep p,
+                                                                  int lift_only, double* __restrict__ parts) {
+    extern __shared__ __align__(16) double smem[];
+    double(*sT)[kKc + 1] = reinterpret_cast<double(*)[kKc + 1]>(smem);
+    double(*sV)[kKc + 1] = reinterpret_cast<double(*)[kKc + 1]>(smem + kTile * (kKc + 1));
+    double* sM = smem + 2 * kTile * (kKc + 1);  // kTile x kTile, 16-byte aligned (2·64·33 is even)
+    double* sY = sM + kTile * kTile;
+    __shared__ double red[kThreads / 32];
+    const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+    const int64_t tiles_n = (n + kTile - 1) / kTile;
+    const int64_t tiles = ((m + kTile - 1) / kTile) * tiles_n;
+    double part = 0.0;
+    for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
+        const int64_t i0 = (t / tiles_n) * kTile, j0 = (t % tiles_n) * kTile;
+        if (!lift_only) {
+            if constexpr (VEC) {
+                for (int e = threadIdx.x; e < kTile * kTile / 2; e += kThreads) {
+                    const int r = e / (kTile / 2), c = 2 * (e % (kTile / 2));
+                    const int64_t gi = i0 + r, gj = j0 + c;
+                    const bool ok = gi < m && gj < n;  // n even when VEC: a pair is all-in or all-out
+                    const int64_t gi_c = ok ? gi : 0, gj_c = ok ? gj : 0;
+                    cp_async_zfill<16>(sM + r * kTile + c, M + gi_c * ldm + gj_c, ok ? 16 : 0);
+                    cp_async_zfill<16>(sY + r * kTile + c, Y + gi_c * ldy + gj_c, ok ? 16 : 0);
+                }
+            } else {
+                for (int e = threadIdx.x; e < kTile * kTile; e += kThreads) {
+                    const int r = e / kTile, c = e % kTile;
+                    const int64_t gi = i0 + r, gj = j0 + c;
+                    const bool ok = gi < m && gj < n;
+                    const int64_t gi_c = ok ? gi : 0, gj_c = ok ? gj : 0;
+                    cp_async_zfill<8>(sM + r * kTile + c, M + gi_c * ldm + gj_c, ok ? 8 : 0);
+                    cp_async_zfill<8>(sY + r * kTile + c, Y + gi_c * ldy + gj_c, ok ? 8 : 0);
+                }
+            }
+            asm volatile("cp.async.commit_group;\n" ::);
+        }
+        double acc[4][4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int j = 0; j < 4; ++j) acc[i][j] = 0.0;
+        for (int k0 = 0; k0 < d; k0 += kKc) {
+            for (int e = threadIdx.x; e < kTile * kKc; e += kThreads) {
+                const int r = e / kKc, c = e % kKc;
+                const bool kc = k0 + c < d;
+                sT[r][c] = (kc && i0 + r < m) ? __ldg(Tp + (i0 + r) * ldt + k0 + c) : 0.0;
+                sV[r][c] = (kc && j0 + r < n) ? __ldg(Vb + (j0 + r) * ldv + k0 + c) : 0.0;
+            }
+            __syncthreads();
+            const int kn = min(kKc, d - k0);
+            for (int kk = 0; kk < kn; ++kk) {
+                double a[4], b[4];
+#pragma unroll
+                for (int i = 0; i < 4; ++i) a[i] = sT[ty + 16 * i][kk];
+#pragma unroll
+                for (int j = 0; j < 4; ++j) b[j] = sV[tx + 16 * j][kk];
+#pragma unroll
+                for (int i = 0; i < 4; ++i)
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) acc[i][j] = fma(a[i], b[j], acc[i][j]);
+            }
+            __syncthreads();
+        }
+        if (!lift_only) {
+            asm volatile("cp.async.wait_group 0;\n" ::);
+            __syncthreads();
+        }
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const int li = ty + 16 * i;
+            const int64_t gi = i0 + li;
+            if (gi >= m) continue;
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const int lj = tx + 16 * j;
+                const int64_t gj = j0 + lj;
+                if (gj >= n) continue;
+                const double l = acc[i][j];
+                if (lift_only) {
+                    L[gi * ldl + gj] = l;
+                    continue;
+                }
+                const double mv = sM[li * kTile + lj];
+                const double yv = sY[li * kTile + lj];
+                const double ml = __dsub_rn(mv, l);                        // m - l        (rpca.hpp:143)
+                const double w = __dadd_rn(ml, __dmul_rn(yv, p.inv_mu));   // += y·inv_mu  (:144)
+                const double mag = __dsub_rn(fabs(w), p.thresh);           // shrink       (:17-26, :145)
+                const double s = mag > 0.0 ? (w > 0.0 ? mag : -mag) : 0.0;
+                const double r = __dsub_rn(ml, s);                         // resid        (:147-148)
+                const double y2 = __dadd_rn(yv, __dmul_rn(p.mu, r));       // y += mu·resid (:149)
+                __stcs(S + gi * lds + gj, s);
+                __stcs(Y + gi * ldy + gj, y2);
+                __stcs(X + gi * ldx + gj, __dadd_rn(__dsub_rn(mv, s), __dmul_rn(y2, p.inv_mu_next)));  // next x
+                part = fma(r, r, part);
+            }
+        }
+        if (!lift_only) __syncthreads();  // sM / sY are refilled by the next tile's prefetch
+    }
+    if (!lift_only) {
+        const double s = block_sum(part, red);
+        if (threadIdx.x == 0) parts[blockIdx.x] = s;
+    }
+}
+
+constexpr size_t kUpdSmem = size_t(2 * kTile * (kKc + 1) + 2 * kTile * kTile) * sizeof(double);
+
+__global__ void __launch_bounds__(kThreads) k_sumsq(const double* __restrict__ A, int64_t lda, int64_t m, int64_t n,
+                                                    double* __restrict__ parts) {
+    __shared__ double red[kThreads / 32];
+    double s = 0.0;
+    for (int64_t i = blockIdx.x; i < m; i += gridDim.x)
+        for (int64_t j = threadIdx.x; j < n; j += kThreads) {
+            const double v = A[i * lda + j];
+            s = fma(v, v, s);
+        }
+    s = block_sum(s, red);
+    if (threadIdx.x == 0) parts[blockIdx.x] = s;
+}
+
+__global__ void __launch_bounds__(kThreads) k_sum_parts(const double* __restrict__ parts, int nparts,
+                                                        double* __restrict__ out) {
+    __shared__ double red[kThreads / 32];
+    double s = 0.0;
+    for (int i = threadIdx.x; i < nparts; i += kThreads) s += parts[i];
+    s = block_sum(s, red);
+    if (threadIdx.x == 0) out[0] = s;
+}
+
+__global__ void k_cor_truncate(const double* __restrict__ T, int64_t ldt, int d, double delta, int lower,
+                               double* __restrict__ Tr, int64_t ldtr, int* rank_out) {
+    __shared__ int s_r;
+    if (threadIdx.x == 0) {
+        int r = 0;
+        for (int j = 0; j < d; ++j) r += fabs(T[int64_t(j) * ldt + j]) > delta;  // corutv.hpp:128-130
+        s_r = r;
+        if (rank_out) *rank_out = r;
+    }
+    __syncthreads();
+    const int r = s_r;
+    for (int64_t e = threadIdx.x; e < int64_t(d) * d; e += blockDim.x) {
+        const int i = int(e / d), j = int(e % d);
+        const bool keep = lower ? j < r : i < r;
+        Tr[int64_t(i) * ldtr + j] = keep ? T[int64_t(i) * ldt + j] : 0.0;
+    }
+}
+
+__global__ void k_gram_norms(const double* __restrict__ sig, int p, double* __restrict__ out) {
+    if (threadIdx.x != 0) return;
+    double nuc = 0.0;
+    for (int i = 0; i < p; ++i) nuc += sqrt(fmax(sig[i], 0.0));
+    out[0] = sqrt(fmax(sig[0], 0.0));
+    out[1] = nuc;
+}
+
+__global__ void __launch_bounds__(kThreads) k_count_nonzero(const double* __restrict__ A, int64_t lda, int64_t m,
+                                                            int64_t n, unsigned long long* out) {
+    unsigned long long c = 0;
+    for (int64_t i = blockIdx.x; i < m; i += gridDim.x)
+        for (int64_t j = threadIdx.x; j < n; j += kThreads) c += A[i * lda + j] != 0.0;
+    for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+    if ((threadIdx.x & 31) == 0 && c) atomicAdd(out, c);  // integer: order-independent
+}
+
+}  // namespace
+
+int rpca_parts(int64_t m, int64_t n, int sms) {
+    const int64_t tiles = ((m + kTile - 1) / kTile) * ((n + kTile - 1) / kTile);
+    return int(std::max<int64_t>(1, std::min<int64_t>(tiles, int64_t(sms) * 2)));
+}
+
+cudaError_t rpca_lift_update(const double* Tp, int64_t ldt, const double* Vb, int64_t ldv, int d, int64_t m,
+                             int64_t n, const double* M, int64_t ldm, double* Y, int64_t ldy, double* X, int64_t ldx,
+                             double* S, int64_t lds, double* L, int64_t ldl, const RpcaStep& p, bool lift_only,
+                             double* parts, int nparts, cudaStream_t st) {
+    const bool vec = !lift_only && n % 2 == 0 && ldm % 2 == 0 && ldy % 2 == 0 &&
+                     (reinterpret_cast<uintptr_t>(M) & 15) == 0 && (reinterpret_cast<uintptr_t>(Y) & 15) == 0;
+    auto kern = vec ? k_rpca_lift_update<true> : k_rpca_lift_update<false>;
+    allow_max_smem(kern);
+    kern<<<nparts, kThreads, kUpdSmem, st>>>(Tp, ldt, Vb, ldv, d, m, n, M, ldm, Y, ldy, X, ldx, S, lds, L, ldl, p,
+                                             lift_only ? 1 : 0, parts);
+    return cudaGetLastError();
+}
+
+cudaError_t cor_truncate(const double* T, int64_t ldt, int d, double delta, int lower, double* Tr, int64_t ldtr,
+                         int* rank_out, cudaStream_t st) {
+    k_cor_truncate<<<1, 256, 0, st>>>(T, ldt, d, delta, lower, Tr, ldtr, rank_out);
+    return cudaGetLastError();
+}
+
+cudaError_t sumsq_parts(const double* A, int64_t lda, int64_t m, int64_t n, double* parts, int nparts,
+                        cudaStream_t st) {
+    k_sumsq<<<nparts, kThreads, 0, st>>>(A, lda, m, n, parts);
+    return cudaGetLastError();
+}
+
+cudaError_t sum_parts(const double* parts, int nparts, double* out, cudaStream_t st) {
+    k_sum_parts<<<1, kThreads, 0, st>>>(parts, nparts, out);
+    return cudaGetLastError();
+}
+
+cudaError_t gram_norms(const double* sig, int p, double* out, cudaStream_t st) {
+    k_gram_norms<<<1, 32, 0, st>>>(sig, p, out);
+    return cudaGetLastError();
+}
+
+cudaError_t count_nonzero(const double* A, int64_t lda, int64_t m, int64_t n, unsigned long long* out,
+                          cudaStream_t st) {
+    cudaError_t e = cudaMemsetAsync(out, 0, sizeof(unsigned long long), st);
+    if (e != cudaSuccess) return e;
+    const int blocks = int(std::max<int64_t>(1, std::min<int64_t>(m, 148 * 8)));
+    k_count_nonzero<<<blocks, kThreads, 0, st>>>(A, lda, m, n, out);
+    return cudaGetLastError();
+}
+
+}  // namespace coru_gpu

@@ -98,7 +98,7 @@ __global__ void __launch_bounds__(E > 0 ? 512 : kJacThreadsMax, 1)
     // column-major working copy (svd.hpp:152-154: a_cm[j·n + i] = a(i, j)) and V = I
     for (int e = tid; e < d * d; e += kJacThreads) {
         const int i = e / d, j = e - i * d;
-        a[int64_t(j) * d + i] = double(svd_mode == 2 ? Y[int64_t(j) * ldy + i] : Y[int64_t(i) * ldy + j]);
+        a[int64_t(j) * d + i] = double(svd_mode >= 2 ? Y[int64_t(j) * ldy + i] : Y[int64_t(i) * ldy + j]);
         v[int64_t(j) * d + i] = (i == j) ? 1.0 : 0.0;
     }
     __syncthreads();
@@ -250,6 +250,14 @@ __global__ void __launch_bounds__(E > 0 ? 512 : kJacThreadsMax, 1)
             if (lane == 0) w.sig[r] = sigma;
             continue;
         }
+        if (svd_mode == 3) {  // preconditioned svd (svd_square_precond): as mode 2, unscaled, with sigma
+            for (int i = lane; i < d; i += kWarp) {
+                w.vs[int64_t(r) * d + i] = sigma > 0.0 ? ac[i] / sigma : 0.0;
+                w.ut[int64_t(r) * d + i] = vc[i];
+            }
+            if (lane == 0) w.sig[r] = sigma;
+            continue;
+        }
         const double inv = sigma > cut ? 1.0 / sigma : 0.0;
         if (inv == 0.0) continue;
         if (svd_mode == 2) {  // X = R^T: V_Y column = P·u'(:, r), U_Y column = Q·v'(:, src) (k_precond_fix)
@@ -292,7 +300,7 @@ __global__ void __launch_bounds__(kGridWarps * 32)
     const int64_t gt = int64_t(blockIdx.x) * blockDim.x + threadIdx.x, nt = int64_t(gridDim.x) * blockDim.x;
     for (int64_t e = gt; e < int64_t(d) * d; e += nt) {
         const int i = int(e / d), j = int(e - int64_t(i) * d);
-        a[int64_t(j) * d + i] = double(svd_mode == 2 ? Y[int64_t(j) * ldy + i] : Y[int64_t(i) * ldy + j]);
+        a[int64_t(j) * d + i] = double(svd_mode >= 2 ? Y[int64_t(j) * ldy + i] : Y[int64_t(i) * ldy + j]);
         v[int64_t(j) * d + i] = (i == j) ? 1.0 : 0.0;
     }
     if (gt < kMaxSweeps) w.rot[gt] = 0;
@@ -403,6 +411,14 @@ __global__ void __launch_bounds__(kGridWarps * 32)
             for (int i = lane; i < d; i += kWarp) {
                 w.vs[int64_t(r) * d + i] = __ldcg(vc + i);
                 w.ut[int64_t(r) * d + i] = sigma > 0.0 ? __ldcg(ac + i) / sigma : 0.0;
+            }
+            if (lane == 0) w.sig[r] = sigma;
+            continue;
+        }
+        if (svd_mode == 3) {
+            for (int i = lane; i < d; i += kWarp) {
+                w.vs[int64_t(r) * d + i] = sigma > 0.0 ? __ldcg(ac + i) / sigma : 0.0;
+                w.ut[int64_t(r) * d + i] = __ldcg(vc + i);
             }
             if (lane == 0) w.sig[r] = sigma;
             continue;
@@ -572,6 +588,51 @@ __global__ void __launch_bounds__(256) k_svd_core(const double* ws, int d, int k
     }
 }
 
+// svt's core (rpca.hpp:30-40) on the factors svd_square left in `ws`: R = the leading count of
+// sigma_r > delta (the reference's while loop over the non-increasing sigma), then
+// C(i, l) = sum_{r < R} (u(i, r)·(sigma_r - delta))·v(l, r), r increasing; R = 0 gives C = 0.
+// Block (0, 0) publishes R to *rank_out.
+template <typename T>
+__global__ void __launch_bounds__(256) k_svt_core(const double* ws, int d, double delta, T* C, int64_t ldc,
+                                                  int* rank_out) {
+    PinvWs w(const_cast<double*>(ws), d);
+    __shared__ double su[kAsmTile][kAsmTile + 1];
+    __shared__ double sv[kAsmTile][kAsmTile + 1];
+    __shared__ int s_k;
+    if (threadIdx.x == 0) {
+        int r = 0;
+        while (r < d && w.sig[r] > delta) ++r;
+        s_k = r;
+        if (blockIdx.x == 0 && blockIdx.y == 0 && rank_out) *rank_out = r;
+    }
+    __syncthreads();
+    const int k = s_k;
+    const int i0 = blockIdx.y * kAsmTile, l0 = blockIdx.x * kAsmTile;
+    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+    double acc[4] = {0.0, 0.0, 0.0, 0.0};
+    for (int r0 = 0; r0 < k; r0 += kAsmTile) {
+        for (int rr = ty; rr < kAsmTile; rr += 8) {
+            const int r = r0 + rr;
+            const bool ok = r < k;
+            su[rr][tx] = (ok && i0 + tx < d) ? __dmul_rn(w.ut[int64_t(r) * d + i0 + tx], __dsub_rn(w.sig[r], delta)) : 0.0;
+            sv[rr][tx] = (ok && l0 + tx < d) ? w.vs[int64_t(r) * d + l0 + tx] : 0.0;
+        }
+        __syncthreads();
+        const int rn = min(kAsmTile, k - r0);
+        for (int rr = 0; rr < rn; ++rr) {
+            const double vv = sv[rr][tx];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) acc[q] += su[rr][ty + 8 * q] * vv;
+        }
+        __syncthreads();
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        const int i = i0 + ty + 8 * q, l = l0 + tx;
+        if (i < d && l < d) C[int64_t(i) * ldc + l] = T(acc[q]);
+    }
+}
+
 // Preconditioned pinv: Y·P = Q·R (QRCP) and the Jacobi SVD of X = R^T = U' Σ V'^T give
 // Y = (Q V') Σ (P U')^T, so for every kept r: V_Y(:, r)/σ = P·u'(:, r)/σ (a row permutation) and
 // U_Y(:, r) = Q·v'(:, r). One CTA per r.
@@ -684,9 +745,29 @@ cudaError_t svd_square(const T* Y, int64_t ldy, int d, T* U, int64_t ldu, T* sig
 }
 
 template <typename T>
+cudaError_t svd_factors_precond(const T* Y, int64_t ldy, int d, double* ws, int max_smem, cudaStream_t st) {
+    cudaError_t e;
+    if (d < 8 || d > 544) return jacobi_run<T>(Y, ldy, d, ws, nullptr, max_smem, 1, st);
+    PinvWs w(ws, d);
+    k_widen_square<T><<<std::max(1, std::min(148 * 4, (d * d + 255) / 256)), 256, 0, st>>>(Y, ldy, d, w.yd);
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    if ((e = qrcp<double>(w.yd, d, d, w.qp, d, w.rp, d, w.perm, w.qscr, max_smem, st)) != cudaSuccess) return e;
+    if ((e = jacobi_run<double>(w.rp, d, d, ws, nullptr, max_smem, 3, st)) != cudaSuccess) return e;
+    k_precond_fix<<<d, 256, 2 * size_t(d) * sizeof(double), st>>>(ws, d);
+    return cudaGetLastError();
+}
+
+template <typename T>
 cudaError_t svd_truncate_core(const double* ws, int d, int k, T* C, int64_t ldc, cudaStream_t st) {
     const dim3 grid((d + kAsmTile - 1) / kAsmTile, (d + kAsmTile - 1) / kAsmTile);
     k_svd_core<T><<<grid, 256, 0, st>>>(ws, d, k, C, ldc);
+    return cudaGetLastError();
+}
+
+template <typename T>
+cudaError_t svt_core(const double* ws, int d, double delta, T* C, int64_t ldc, int* rank_out, cudaStream_t st) {
+    const dim3 grid((d + kAsmTile - 1) / kAsmTile, (d + kAsmTile - 1) / kAsmTile);
+    k_svt_core<T><<<grid, 256, 0, st>>>(ws, d, delta, C, ldc, rank_out);
     return cudaGetLastError();
 }
 
@@ -697,5 +778,8 @@ template cudaError_t pinv_square<float>(const float*, int64_t, int, float*, int6
 template cudaError_t svd_square<double>(const double*, int64_t, int, double*, int64_t, double*, double*, int64_t,
                                         double*, int*, int, cudaStream_t);
 template cudaError_t svd_truncate_core<double>(const double*, int, int, double*, int64_t, cudaStream_t);
+
+template cudaError_t svd_factors_precond<double>(const double*, int64_t, int, double*, int, cudaStream_t);
+template cudaError_t svt_core<double>(const double*, int, double, double*, int64_t, int*, cudaStream_t);
 
 }  // namespace coru_gpu

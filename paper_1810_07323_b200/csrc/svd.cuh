@@ -26,6 +26,16 @@ cudaError_t svd_square(const T* Y, int64_t ldy, int d, T* U, int64_t ldu, T* sig
 // (svd_truncate, baselines.hpp:14-20).
 template <typename T>
 cudaError_t svd_truncate_core(const double* ws, int d, int k, T* C, int64_t ldc, cudaStream_t st);
+// svt's core (rpca.hpp:30-40): C = u(:, 1:R)·diag(sigma_r - delta)·v(:, 1:R)^T with R = #{leading
+// sigma_r > delta}, from the factors svd_square left in `ws`; R is written to *rank_out (device).
+template <typename T>
+cudaError_t svt_core(const double* ws, int d, double delta, T* C, int64_t ldc, int* rank_out, cudaStream_t st);
+// The factors of svd (svd.hpp:141-161) left in `ws` only (sorted sigma, ut rows = u columns, vs rows =
+// v columns), computed like the preconditioned pinv: Y·P = Q·R, one-sided Jacobi of R^T, factors
+// permuted / rotated back — about half the sweeps of the plain square Jacobi on graded matrices; the
+// same factors to rounding. Falls back to the plain Jacobi for d < 8 or d > 544. 4 launches.
+template <typename T>
+cudaError_t svd_factors_precond(const T* Y, int64_t ldy, int d, double* ws, int max_smem, cudaStream_t st);
 constexpr int kSvdLaunches = 2;
 constexpr int kPinvLaunches = 5;  // widen, QRCP, Jacobi, fix, assemble
 

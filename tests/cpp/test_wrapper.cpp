@@ -124,6 +124,33 @@ int main() {
         CHECK(orth_res(t.u) <= 1e-9 * std::sqrt(6.0) && orth_res(t.v) <= 1e-9 * std::sqrt(6.0));
         for (std::size_t j = 0; j + 1 < t.sigma.size(); ++j) CHECK(t.sigma[j] >= t.sigma[j + 1]);
     }
+    // alm_rpca with the CoR-UTV inner (rpca.hpp:95-169): low rank + sparse recovery, config validation
+    {
+        const std::size_t n = 60, r = 3;
+        Matrix low = exact_rank(n, n, r, {31, 0});
+        Matrix mat = low;
+        for (std::size_t k = 0; k < 120; ++k) mat.data()[(k * 2654435761ull + k * k * 31) % (n * n)] += (k % 2 ? 50.0 : -50.0);
+        RpcaConfig cfg;
+        cfg.corutv_ell = 2 * r;
+        RpcaResult res = alm_rpca(mat, cfg, {2, 0});
+        CHECK(res.converged && res.rank_l == r && res.residuals.size() == std::size_t(res.iterations));
+        double diff = 0, nrm = 0;
+        for (std::size_t i = 0; i < low.data().size(); ++i) {
+            diff += (low.data()[i] - res.l.data()[i]) * (low.data()[i] - res.l.data()[i]);
+            nrm += low.data()[i] * low.data()[i];
+        }
+        CHECK(std::sqrt(diff) <= 1e-3 * std::sqrt(nrm));
+        CHECK(res.s_l0 >= 100);  // 111 distinct corrupted entries
+        bool threw = false;
+        try {
+            RpcaConfig bad = cfg;
+            bad.rho = 1.0;
+            (void)alm_rpca(mat, bad, {2, 0});
+        } catch (const std::invalid_argument&) {
+            threw = true;
+        }
+        CHECK(threw);
+    }
     std::printf("%s: %d failures\n", failures ? "FAIL" : "OK", failures);
     return failures ? 1 : 0;
 }

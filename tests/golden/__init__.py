@@ -67,3 +67,22 @@ def sor_cases():
         k, ell, q, seed, stream = (int(x) for x in z[f"{name}/params"])
         out.append(dict(name=name, A=z[f"{name}/A"], k=k, ell=ell, q=q, seed=seed, stream=stream, L=z[f"{name}/L"]))
     return out
+
+
+def rpca_cases():
+    """alm_rpca (rpca.hpp:95-169) with the CoR-UTV inner, outputs of the reference (make_golden.py rpca)."""
+    z = np.load(os.path.join(HERE, "rpca_ref_cases.npz"))
+    out = []
+    for name in z["names"]:
+        name = str(name)
+        c = z[f"{name}/cfg"]
+        cfg = dict(lambda_=float(c[0]), mu0=float(c[1]), rho=float(c[2]), mu_bar=float(c[3]), tol=float(c[4]),
+                   max_iter=int(c[5]), corutv_ell=int(c[6]), corutv_q=int(c[7]), thresholding=int(c[8]))
+        it, rank, sl0, conv, clamped = (int(x) for x in z[f"{name}/out"])
+        case = dict(name=name, M=z[f"{name}/M"], L=z[f"{name}/L"], S=z[f"{name}/S"], residuals=z[f"{name}/residuals"],
+                    cfg=cfg, iterations=it, rank_l=rank, s_l0=sl0, converged=bool(conv), ell_clamped=bool(clamped),
+                    seed=2, stream=0)
+        if f"{name}/S_true" in z.files:
+            case["S_true"] = z[f"{name}/S_true"]
+        out.append(case)
+    return out

@@ -188,5 +188,62 @@ def approx_fixtures(cases):
     print("wrote", len(anames), "approx corutv cases and", len(sq), "pinv cases")
 
 
+def rpca_instance_rect(m, n, r, nnz, amp, seed):
+    """Rectangular restatement of gen_rpca_instance (testgen.hpp:86-109) for the non-square cases:
+    L = G1·G2^T from the reference's gaussian sub-streams, nnz entries ±amp at seeded positions."""
+    g1 = R.gaussian(m, r, seed, 0)
+    g2 = R.gaussian(n, r, seed, 1)
+    low = R.matmul(g1, np.ascontiguousarray(g2.T))
+    rng = np.random.default_rng(seed)
+    sp = np.zeros(m * n)
+    idx = rng.choice(m * n, nnz, replace=False)
+    sp[idx] = np.where(rng.random(nnz) < 0.5, amp, -amp)
+    return low + sp.reshape(m, n)
+
+
+def rpca_fixtures(full=True):
+    """alm_rpca with the CoR-UTV inner (rpca.hpp:95-169): the reference's instances (test_cli.cpp:168-183
+    gen --family rpca --n 60 --k 4 --s 180 --amp 80 --seed 21; acceptance.cpp:204-220,394 criterion 7)."""
+    out = {}
+    names = []
+    m60 = R.gen_rpca_instance(60, 4, 180, 80.0, 21)[0]
+    tall = rpca_instance_rect(90, 50, 3, 150, 60.0, 5)
+    wide = np.ascontiguousarray(rpca_instance_rect(90, 50, 3, 150, 60.0, 6).T)
+    cases = [
+        ("n60_soft_ell8", m60, dict(corutv_ell=8, corutv_q=1, thresholding=0)),
+        ("n60_hard_ell8", m60, dict(corutv_ell=8, corutv_q=1, thresholding=1)),
+        ("n60_soft_predict", m60, dict(corutv_ell=0, corutv_q=1, thresholding=0)),
+        ("n60_hard_q0_maxit3", m60, dict(corutv_ell=8, corutv_q=0, thresholding=1, max_iter=3)),
+        ("tall90x50_soft_ell6", tall, dict(corutv_ell=6, corutv_q=1, thresholding=0)),
+        ("tall90x50_hard_ell6", tall, dict(corutv_ell=6, corutv_q=2, thresholding=1)),
+        ("wide50x90_hard_ell6", wide, dict(corutv_ell=6, corutv_q=1, thresholding=1)),
+        ("wide50x90_soft_ell6_mu0", wide, dict(corutv_ell=6, corutv_q=1, thresholding=0, mu0=0.01)),
+    ]
+    if full:
+        m400 = R.gen_rpca_instance(400, 20, 8000, 80.0, 2024)
+        cases.append(("acc7_n400_r20_soft_ell40", m400[0], dict(corutv_ell=40, corutv_q=1, thresholding=0)))
+        out["acc7_n400_r20_soft_ell40/S_true"] = m400[2]
+    for name, mat, kw in cases:
+        r = R.alm_rpca(mat, seed=2, stream=0, **kw)
+        names.append(name)
+        out[f"{name}/M"] = mat
+        out[f"{name}/L"] = r["l"]
+        out[f"{name}/S"] = r["s"]
+        out[f"{name}/residuals"] = r["residuals"]
+        cfg = dict(lambda_=0.0, mu0=0.0, rho=1.5, mu_bar=0.0, tol=1e-5, max_iter=50, corutv_ell=0, corutv_q=1,
+                   thresholding=0)
+        cfg.update(kw)
+        out[f"{name}/cfg"] = np.array([cfg["lambda_"], cfg["mu0"], cfg["rho"], cfg["mu_bar"], cfg["tol"],
+                                       cfg["max_iter"], cfg["corutv_ell"], cfg["corutv_q"], cfg["thresholding"]])
+        out[f"{name}/out"] = np.array([r["iterations"], r["rank_l"], r["s_l0"], r["converged"], r["ell_clamped"]],
+                                      np.int64)
+        print(name, "it", r["iterations"], "rank", r["rank_l"], "s_l0", r["s_l0"], "conv", r["converged"])
+    out["names"] = np.array(names)
+    np.savez_compressed(os.path.join(HERE, "rpca_ref_cases.npz"), **out)
+
+
 if __name__ == "__main__":
+    if len(sys.argv) > 1 and sys.argv[1] == "rpca":
+        rpca_fixtures()
+        sys.exit(0)
     main()

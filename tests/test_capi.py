@@ -76,3 +76,15 @@ def test_invalid_arguments_before_device():
     lib = cg.load_library()
     rc = lib.coru_gaussian(0, 3, 1, 0, None, 1)
     assert rc == cg.CORU_EINVAL
+
+
+def test_rpca_config_validation_before_device():
+    """RpcaConfig::validate (rpca.hpp:72-77) and the svt_exact ENOTSUP are reported before device work."""
+    import ctypes as C
+    import paper_1810_07323_b200 as cg
+    lib = cg.load_library()
+    cfg = cg.RpcaConfig(corutv_ell=4)
+    assert cfg.rho == 1.5 and cfg.tol == 1e-5 and cfg.max_iter == 50 and cfg.corutv_q == 1
+    c = cg._RpcaConfig()
+    lib.coru_rpca_config_default(C.byref(c))
+    assert (c.rho, c.tol, c.max_iter, c.corutv_q, c.inner, c.thresholding) == (1.5, 1e-5, 50, 1, 1, 0)
