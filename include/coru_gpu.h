@@ -130,6 +130,21 @@ int coru_corutv_f32(coru_ctx* ctx, const float* A, int64_t m, int64_t n, int64_t
                     uint64_t seed, uint64_t stream, float* U, float* T, float* V, int64_t* perm, int* lower,
                     int* conditioning_warning);
 
+/* Out-of-core corutv (§8 f4; the paper's pass model for externally stored data):
+ * A stays in HOST memory (row-major m x n, lda >= n, m >= n) and is streamed to the GPU in row
+ * chunks of chunk_rows rows (<= 0: ~512 MB per chunk) through a two-buffer device ring, the H2D of
+ * chunk i+1 overlapping the GEMMs of chunk i. Each power round reads A once (c1 rows = A_i·c2 and
+ * the partial A_i^T·c1_i from the same chunk, summed in chunk order), the exact-D projection once
+ * more: q + 2 streams of A (exact) / q + 1 (approx) instead of 2q + 3 / 2q + 2 passes. Only the
+ * sketches (m x ell, cols x ell) and two chunks live on the device, so A may exceed HBM. Pageable
+ * host memory is page-locked for the duration of the call. Outputs as coru_corutv_*_dev (device
+ * U, T, V). rows < cols returns CORU_ENOTSUP. Deterministic; differs from the in-core path at
+ * rounding level (chunk-ordered partial sums). */
+int coru_corutv_f64_ooc(coru_ctx* ctx, const double* A, int64_t m, int64_t n, int64_t lda, int64_t ell, int q,
+                        int variant, uint64_t seed, uint64_t stream, int64_t chunk_rows, coru_utv* out);
+int coru_corutv_f32_ooc(coru_ctx* ctx, const float* A, int64_t m, int64_t n, int64_t lda, int64_t ell, int q,
+                        int variant, uint64_t seed, uint64_t stream, int64_t chunk_rows, coru_utv* out);
+
 /* ---- the sketch stage: detail::sketch_bases (corutv.hpp:42-65) ------------------------------- */
 /* Requires rows(A) >= cols(A) like the reference's callers (rpca.hpp:135, baselines.hpp:68).
  * Q1/C1: m_local x ell, Q2/C2prev: n x ell (device, row-major). C1 and C2prev may be NULL. */

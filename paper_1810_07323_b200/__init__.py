@@ -155,6 +155,8 @@ def load_library():
                                                          C.POINTER(_Utv)]
         getattr(L, f"coru_corutv_{sfx}").argtypes = [p, p, i64, i64, i64, i32, i32, u64, u64, p, p, p, p,
                                                      C.POINTER(i32), C.POINTER(i32)]
+    for sfx in ("f64", "f32"):
+        getattr(L, f"coru_corutv_{sfx}_ooc").argtypes = [p, p, i64, i64, i64, i64, i32, i32, u64, u64, i64, p]
     L.coru_sketch_bases_f64_dev.argtypes = [p, p, i64, i64, i64, i64, i64, i32, u64, u64, p, i64, p, i64, p, i64,
                                             p, i64, C.POINTER(i32)]
     L.coru_sketch_bases_f64.argtypes = [p, p, i64, i64, i64, i32, u64, u64, p, p, p, p, C.POINTER(i32)]
@@ -679,3 +681,27 @@ def alm_rpca(m, config: RpcaConfig = RpcaConfig(), seed: RngSeed = RngSeed(),
                                          l.ctypes.data, s.ctypes.data, C.byref(res)))
     return RpcaResult(l, s, res.iterations, list(resid[:res.iterations]), int(res.rank_l), int(res.s_l0),
                       bool(res.converged), bool(res.ell_clamped))
+
+
+def corutv_ooc(a: np.ndarray, ell: int, q: int, variant: DVariant = DVariant.exact, seed: RngSeed = RngSeed(),
+               chunk_rows: int = 0, ctx: Optional[Context] = None) -> UtvApprox:
+    """Out-of-core corutv (§8 f4): ``a`` is a host numpy array (rows >= cols) streamed to the GPU in row chunks
+    (coru_corutv_{f64,f32}_ooc); U, T, V come back as numpy arrays."""
+    import torch
+    ctx = ctx or default_context()
+    assert isinstance(a, np.ndarray) and a.dtype in (np.float64, np.float32) and a.strides[1] == a.itemsize
+    m, n = a.shape
+    sfx = "f64" if a.dtype == np.float64 else "f32"
+    tdt = torch.float64 if sfx == "f64" else torch.float32
+    dev = torch.device("cuda", ctx.device)
+    u = torch.empty((m, ell), dtype=tdt, device=dev)
+    t = torch.empty((ell, ell), dtype=tdt, device=dev)
+    v = torch.empty((n, ell), dtype=tdt, device=dev)
+    perm = np.zeros(ell, np.int64)
+    out = _Utv(u.data_ptr(), ell, t.data_ptr(), ell, v.data_ptr(), ell, perm.ctypes.data, 0, 0)
+    torch.cuda.synchronize(dev)
+    _check(getattr(ctx.lib, f"coru_corutv_{sfx}_ooc")(ctx.h, a.ctypes.data, m, n, a.strides[0] // a.itemsize, ell, q,
+                                                     int(variant), seed.seed, seed.stream, chunk_rows, C.byref(out)))
+    torch.cuda.synchronize(dev)
+    return UtvApprox(u.cpu().numpy(), t.cpu().numpy(), v.cpu().numpy(), ell, q, variant, seed, bool(out.lower),
+                     bool(out.conditioning_warning), perm)

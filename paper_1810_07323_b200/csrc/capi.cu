@@ -391,6 +391,10 @@ struct Request {
     int64_t ldv = 0;
     int64_t* perm_host = nullptr;
     int* warn_host = nullptr;
+    // Out-of-core (§8 f4): A' stays in host memory (row-major, lda) and is streamed in row chunks
+    // of ooc_rows rows; A must then be null. Single GPU, rows >= cols.
+    const T* a_host = nullptr;
+    int64_t ooc_rows = 0;
     // Sketch: Q1, Q2, C1, C2prev (device, may be null except Q1/Q2).
     T *q1 = nullptr, *q2 = nullptr, *c1 = nullptr, *c2p = nullptr;
     int64_t ldq1 = 0, ldq2 = 0, ldc1 = 0, ldc2 = 0;
@@ -406,6 +410,7 @@ struct Work {
     T *rstack = nullptr, *qtop = nullptr, *r1loc = nullptr, *r1 = nullptr, *r2 = nullptr;
     T *m = nullptr, *qm = nullptr, *tm = nullptr, *qrcp_scr = nullptr;
     T *y1 = nullptr, *y2 = nullptr, *pinv = nullptr;  // approx-D core
+    T *cbuf[2] = {nullptr, nullptr}, *b2n = nullptr, *part = nullptr;  // out-of-core chunk ring, next c2, partial
     double* pws = nullptr;
     int64_t* perm = nullptr;
     int* flag = nullptr;
@@ -422,6 +427,15 @@ struct Work {
         gws_elems = std::max({gemm_ws<T>(r.op_a(), R, N, d, sms), gemm_ws<T>(r.op_at(), N, R, d, sms),
                               gemm_ws<T>(Op::T, d, R, d, sms), gemm_ws<T>(Op::N, R, d, d, sms),
                               gemm_ws<T>(Op::T, d, N, d, sms), gemm_ws<T>(Op::N, d, d, d, sms)});
+        if (r.a_host) {
+            const int64_t cr = std::min(r.ooc_rows, R), last = R - (R - 1) / cr * cr;
+            for (int64_t rows : {cr, last})
+                gws_elems = std::max({gws_elems, gemm_ws<T>(Op::N, rows, N, d, sms), gemm_ws<T>(Op::T, N, rows, d, sms)});
+            cbuf[0] = cv.take<T>(cr * N);
+            cbuf[1] = cv.take<T>(cr * N);
+            b2n = cv.take<T>(N * dp);
+            part = cv.take<T>(N * dp);
+        }
         gws = cv.take<T>(gws_elems);
         // CholeskyQR2 for wide sketches, except for Q1 when sharded (its tree's top level is cross-rank)
         ts1.carve(cv, R, d, c->max_smem, sms, c->world == 1 && c->wide_qr);
@@ -542,6 +556,18 @@ template <typename T>
 int run_impl(coru_ctx* c, const Request<T>& r, size_t extra_arena_off);
 
 // The hot path. Enqueues everything on c->stream and synchronises once at the end (the flag and
+template <typename T>
+__global__ void k_add_inplace(T* __restrict__ dst, const T* __restrict__ src, size_t count) {
+    for (size_t e = size_t(blockIdx.x) * blockDim.x + threadIdx.x; e < count; e += size_t(gridDim.x) * blockDim.x)
+        dst[e] += src[e];
+}
+template <typename T>
+cudaError_t add_inplace(T* dst, const T* src, size_t count, cudaStream_t st) {
+    const int blocks = int(std::min<size_t>((count + 255) / 256, 148 * 8));
+    k_add_inplace<T><<<std::max(blocks, 1), 256, 0, st>>>(dst, src, count);
+    return cudaGetLastError();
+}
+
 // the pivots are host outputs). A failing rank of an in-process group releases its peers.
 template <typename T>
 int run(coru_ctx* c, const Request<T>& r, size_t extra_arena_off = 0) {
@@ -577,7 +603,67 @@ int run_impl(coru_ctx* c, const Request<T>& r, size_t extra_arena_off) {
     const bool sharded = c->world > 1;
     // tooling: overlap QR(c1) with the last A^T pass
     const bool early_qr1 = !sharded && getenv("CORU_QR1_EARLY") != nullptr && !(r.first_done && r.q == 0);
-    for (int i = r.first_done ? 1 : 0; i <= r.q; ++i) {
+    // Out-of-core: stream A' through a two-buffer device ring, H2D on the aux stream one chunk ahead
+    // of the GEMMs on the main stream (events order the reuse of each buffer).
+    cudaEvent_t ooc_ev[4] = {};
+    struct EvGuard {
+        cudaEvent_t* e;
+        ~EvGuard() {
+            for (int i = 0; i < 4; ++i)
+                if (e[i]) cudaEventDestroy(e[i]);
+        }
+    } ooc_guard{ooc_ev};
+    if (r.a_host) {
+        for (auto& e : ooc_ev) CORU_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        CORU_CUDA(cudaMemsetAsync(w.b2n, 0, size_t(N) * dp * sizeof(T), st));  // padding columns stay zero
+        CORU_CUDA(cudaMemsetAsync(w.part, 0, size_t(N) * dp * sizeof(T), st));
+    }
+    auto stream_a = [&](auto&& on_chunk) -> int {
+        const int64_t cr = std::min(r.ooc_rows, R);
+        const int64_t nch = (R + cr - 1) / cr;
+        auto issue = [&](int64_t i) -> int {
+            const int64_t r0 = i * cr, rows = std::min(cr, R - r0);
+            const int b = int(i & 1);
+            CORU_CUDA(cudaStreamWaitEvent(c->aux, ooc_ev[2 + b], 0));  // buffer b free again
+            CORU_CUDA(cudaMemcpy2DAsync(w.cbuf[b], size_t(N) * sizeof(T), r.a_host + r0 * r.lda,
+                                        size_t(r.lda) * sizeof(T), size_t(N) * sizeof(T), size_t(rows),
+                                        cudaMemcpyHostToDevice, c->aux));
+            CORU_CUDA(cudaEventRecord(ooc_ev[b], c->aux));
+            return CORU_OK;
+        };
+        CORU_CUDA(cudaEventRecord(ooc_ev[2], st));  // both buffers start free (main-stream order)
+        CORU_CUDA(cudaEventRecord(ooc_ev[3], st));
+        CORU_TRY(issue(0));
+        for (int64_t i = 0; i < nch; ++i) {
+            if (i + 1 < nch) CORU_TRY(issue(i + 1));
+            const int b = int(i & 1);
+            CORU_CUDA(cudaStreamWaitEvent(st, ooc_ev[b], 0));
+            const int64_t r0 = i * cr, rows = std::min(cr, R - r0);
+            CORU_TRY(on_chunk(i, r0, rows, static_cast<const T*>(w.cbuf[b])));
+            CORU_CUDA(cudaEventRecord(ooc_ev[2 + b], st));
+        }
+        return CORU_OK;
+    };
+    if (r.a_host) {
+        // Each power round reads A once: c1 rows of chunk i = A_i·c2, and the partial A_i^T·c1_i from
+        // the same chunk, summed into the next c2 in chunk order (deterministic).
+        for (int i = 0; i <= r.q; ++i) {
+            CORU_TRY(stream_a([&](int64_t ch, int64_t r0, int64_t rows, const T* Ai) -> int {
+                CORU_TRY(gemm<T>(c, Op::N, Ai, N, w.b2, dp, w.b1 + r0 * dp, dp, rows, N, d, w.gws, w.gws_elems));
+                T* out = ch == 0 ? w.b2n : w.part;
+                CORU_TRY(gemm<T>(c, Op::T, Ai, N, w.b1 + r0 * dp, dp, out, dp, N, rows, d, w.gws, w.gws_elems));
+                if (ch > 0) {
+                    CORU_CUDA(add_inplace<T>(w.b2n, w.part, size_t(N) * dp, st));
+                    ++g_launches;
+                }
+                return CORU_OK;
+            }));
+            if (i == r.q && w.b2prev)
+                CORU_CUDA(cudaMemcpyAsync(w.b2prev, w.b2, size_t(N) * dp * sizeof(T), cudaMemcpyDeviceToDevice, st));
+            std::swap(w.b2, w.b2n);
+        }
+    }
+    for (int i = r.first_done ? 1 : 0; i <= r.q && !r.a_host; ++i) {
         CORU_TRY(gemm<T>(c, r.op_a(), r.A, r.lda, w.b2, dp, w.b1, dp, R, N, d, w.gws, w.gws_elems));
         if (i == r.q && early_qr1) {
             CORU_CUDA(cudaEventRecord(c->ev_fork, st));
@@ -661,7 +747,12 @@ int run_impl(coru_ctx* c, const Request<T>& r, size_t extra_arena_off) {
     } else {
         // D = (Q1^T a) q2 (corutv.hpp:90) as Q1^T (A'·Q2): W = A'·Q2 reuses the B1 buffer.
         T* W = w.b1;
-        CORU_TRY(gemm<T>(c, r.op_a(), r.A, r.lda, w.q2, dp, W, dp, R, N, d, w.gws, w.gws_elems));
+        if (r.a_host)
+            CORU_TRY(stream_a([&](int64_t, int64_t r0, int64_t rows, const T* Ai) -> int {
+                return gemm<T>(c, Op::N, Ai, N, w.q2, dp, W + r0 * dp, dp, rows, N, d, w.gws, w.gws_elems);
+            }));
+        else
+            CORU_TRY(gemm<T>(c, r.op_a(), r.A, r.lda, w.q2, dp, W, dp, R, N, d, w.gws, w.gws_elems));
         const bool p = c->prof;  // Q1^T·W is m x d x d, not an A-pass
         c->prof = false;
         const int rc = gemm<T>(c, Op::T, w.q1, dp, W, dp, w.m, dp, d, R, d, w.gws, w.gws_elems);
@@ -745,6 +836,56 @@ int corutv_dev(coru_ctx* c, const T* A, int64_t m_local, int64_t m, int64_t n, i
         out->lower = 0;
     }
     return run<T>(c, r);
+}
+
+// Out-of-core corutv (§8 f4): A in host memory, streamed. Unregistered host memory is page-locked
+// (read-only) for the duration of the call so every stream runs at full link bandwidth.
+template <typename T>
+int corutv_ooc(coru_ctx* c, const T* A, int64_t m, int64_t n, int64_t lda, int64_t ell, int q, int variant,
+               uint64_t seed, uint64_t stream, int64_t chunk_rows, coru_utv* out) {
+    CORU_TRY(check_params(m, n, ell, q));
+    if (variant != CORU_D_EXACT && variant != CORU_D_APPROX) return fail(CORU_EINVAL, "corutv: unknown DVariant");
+    if (!out || !A) return fail(CORU_EINVAL, "null argument");
+    if (lda < n) return fail(CORU_EINVAL, "lda < n");
+    if (c->world > 1) return fail(CORU_EINVAL, "out-of-core corutv is single-GPU");
+    if (m < n) return fail(CORU_ENOTSUP, "out-of-core corutv: rows < cols (ULV) is not provided");
+    if (chunk_rows <= 0) chunk_rows = std::max<int64_t>(1, int64_t((size_t(512) << 20) / (size_t(n) * sizeof(T))));
+    chunk_rows = std::min(chunk_rows, m);
+    Request<T> r;
+    r.a_host = A;
+    r.ooc_rows = chunk_rows;
+    r.lda = lda;
+    r.rows = m;
+    r.cols = n;
+    r.d = int(ell);
+    r.q = q;
+    r.seed = seed;
+    r.stream = stream;
+    r.variant = variant;
+    r.perm_host = out->perm;
+    r.warn_host = &out->conditioning_warning;
+    r.u = static_cast<T*>(out->u);
+    r.ldu = out->ldu;
+    r.v = static_cast<T*>(out->v);
+    r.ldv = out->ldv;
+    r.t = static_cast<T*>(out->t);
+    r.ldt = out->ldt;
+    out->lower = 0;
+    bool registered = false;
+    cudaPointerAttributes pa{};
+    const size_t bytes = size_t(m - 1) * lda * sizeof(T) + size_t(n) * sizeof(T);
+    if (cudaPointerGetAttributes(&pa, A) != cudaSuccess || pa.type == cudaMemoryTypeUnregistered) {
+        cudaGetLastError();
+        registered = cudaHostRegister(const_cast<T*>(A), bytes, cudaHostRegisterReadOnly) == cudaSuccess;
+        cudaGetLastError();  // registration is an optimisation: pageable copies still work
+    }
+    const int rc = run<T>(c, r);
+    if (registered) {
+        cudaStreamSynchronize(c->stream);
+        cudaStreamSynchronize(c->aux);
+        cudaHostUnregister(const_cast<T*>(A));
+    }
+    return rc;
 }
 
 template <typename T>
@@ -1709,6 +1850,20 @@ int coru_corutv_f64(coru_ctx* c, const double* A, int64_t m, int64_t n, int64_t 
     CORU_TRY(enter(c));
     std::lock_guard<std::mutex> lk(c->mu);
     return corutv_host<double>(c, A, m, n, ell, q, variant, seed, stream, U, T, V, perm, lower, warn);
+}
+
+int coru_corutv_f64_ooc(coru_ctx* c, const double* A, int64_t m, int64_t n, int64_t lda, int64_t ell, int q,
+                        int variant, uint64_t seed, uint64_t stream, int64_t chunk_rows, coru_utv* out) {
+    CORU_TRY(enter(c));
+    std::lock_guard<std::mutex> lk(c->mu);
+    return corutv_ooc<double>(c, A, m, n, lda, ell, q, variant, seed, stream, chunk_rows, out);
+}
+
+int coru_corutv_f32_ooc(coru_ctx* c, const float* A, int64_t m, int64_t n, int64_t lda, int64_t ell, int q,
+                        int variant, uint64_t seed, uint64_t stream, int64_t chunk_rows, coru_utv* out) {
+    CORU_TRY(enter(c));
+    std::lock_guard<std::mutex> lk(c->mu);
+    return corutv_ooc<float>(c, A, m, n, lda, ell, q, variant, seed, stream, chunk_rows, out);
 }
 
 int coru_corutv_f32(coru_ctx* c, const float* A, int64_t m, int64_t n, int64_t ell, int q, int variant,

@@ -1,0 +1,121 @@
+"""Out-of-core corutv (§8 f4): A stays in host memory and is streamed to the GPU in row chunks
+(coru_corutv_{f64,f32}_ooc). Checked against the reference's own outputs on its test inputs
+(tests/golden/corutv_ref_cases.npz, same tolerances as the in-core path) and against the in-core GPU
+path at C2 size with many chunks. Each power round reads A once (both products of a round from the
+same chunk), so the c2 partial sums are chunk-ordered: agreement with the in-core path is to rounding."""
+import numpy as np
+import pytest
+
+from conftest import orth_residual, rel_recon_error
+from golden import approx_cases, corutv_cases
+
+pytestmark = pytest.mark.gpu
+
+
+def _structure(f, d):
+    assert np.all(np.tril(f.t, -1) == 0.0)
+    assert orth_residual(f.u) <= 1e-12 * d and orth_residual(f.v) <= 1e-12 * d
+
+
+@pytest.mark.parametrize("case", [c for c in corutv_cases() if c["A"].shape[0] >= c["A"].shape[1]],
+                         ids=lambda c: c["name"])
+def test_ooc_reference_cases(ctx, case):
+    import paper_1810_07323_b200 as cg
+    a, ell, q = case["A"], case["ell"], case["q"]
+    chunk = max(ell + 1, a.shape[0] // 5)  # several chunks, a ragged last one
+    f = cg.corutv_ooc(a, ell, q, cg.DVariant.exact, cg.RngSeed(case["seed"], case["stream"]), chunk_rows=chunk, ctx=ctx)
+    assert not f.lower
+    _structure(f, ell)
+    e_gpu = rel_recon_error(a, f.u, f.t, f.v)
+    e_ref = rel_recon_error(a, case["U"], case["T"], case["V"])
+    dg = np.abs(np.abs(np.diag(f.t)) - np.abs(np.diag(case["T"])))
+    if q == 0 and not case["warning"]:
+        assert abs(e_gpu - e_ref) <= 1e-10 * max(e_ref, 1e-300) or abs(e_gpu - e_ref) <= 1e-14
+        assert dg.max() <= 1e-8
+        assert f.conditioning_warning == case["warning"]
+    else:
+        assert e_gpu <= 1.5 * e_ref + 1e-13
+
+
+@pytest.mark.parametrize("case", [c for c in approx_cases() if c["A"].shape[0] >= c["A"].shape[1]][:4],
+                         ids=lambda c: c["name"])
+def test_ooc_approx_reference_cases(ctx, case):
+    import paper_1810_07323_b200 as cg
+    a, ell, q = case["A"], case["ell"], case["q"]
+    f = cg.corutv_ooc(a, ell, q, cg.DVariant.approx, cg.RngSeed(case["seed"], case["stream"]),
+                      chunk_rows=max(ell + 1, a.shape[0] // 3), ctx=ctx)
+    e_gpu = rel_recon_error(a, f.u, f.t, f.v)
+    e_ref = rel_recon_error(a, case["U"], case["T"], case["V"])
+    assert orth_residual(f.u) <= 1e-12 * ell and orth_residual(f.v) <= 1e-12 * ell
+    assert e_gpu <= 1.5 * e_ref + 1e-12
+
+
+@pytest.mark.parametrize("q", [0, 1, 2])
+def test_ooc_matches_in_core_c2(ctx, q):
+    """C2 shape (4000 x 4000, sigma_i = i^-2, d = 60) streamed in 8 chunks of 500 rows vs the in-core path."""
+    import paper_1810_07323_b200 as cg
+    from workloads import make_host
+    a = make_host("C2q1")
+    seed = cg.RngSeed(42, 3)
+    f_in = cg.corutv(a, 60, q, cg.DVariant.exact, seed, ctx=ctx)
+    f = cg.corutv_ooc(a, 60, q, cg.DVariant.exact, seed, chunk_rows=500, ctx=ctx)
+    _structure(f, 60)
+    e_in, e_oo = rel_recon_error(a, f_in.u, f_in.t, f_in.v), rel_recon_error(a, f.u, f.t, f.v)
+    d_in, d_oo = np.abs(np.diag(f_in.t)), np.abs(np.diag(f.t))
+    if q == 0:  # well-conditioned sketch: the fp64 tolerances hold between the two paths
+        assert abs(e_in - e_oo) <= 1e-10 * e_in
+        assert np.max(np.abs(d_in - d_oo)) <= 1e-8
+        assert np.array_equal(f.perm, f_in.perm)
+    else:
+        # Power rounds amplify rounding (SURVEY.md §8c floors): at q = 2 the trailing sketch columns scale
+        # like sigma^5 < eps and are rounding noise in any implementation (the reference against itself
+        # changes pivots from j = 26), so only the leading estimates and the quality level are compared.
+        assert abs(e_in - e_oo) <= (1e-2 if q == 1 else 1e-1) * e_in
+        assert np.max(np.abs(d_in[:20] - d_oo[:20]) / d_in[:20]) <= 1e-6
+    g = cg.corutv_ooc(a, 60, q, cg.DVariant.exact, seed, chunk_rows=500, ctx=ctx)
+    assert np.array_equal(f.u, g.u) and np.array_equal(f.t, g.t) and np.array_equal(f.v, g.v)  # deterministic
+
+
+def test_ooc_pinned_equals_pageable_and_strided(ctx):
+    import torch
+    import paper_1810_07323_b200 as cg
+    rng = np.random.default_rng(3)
+    a = rng.standard_normal((3001, 700)) * (0.9 ** np.arange(700))
+    seed = cg.RngSeed(7, 1)
+    f = cg.corutv_ooc(a, 30, 1, seed=seed, chunk_rows=400, ctx=ctx)
+    pinned = torch.empty((3001, 700), dtype=torch.float64).pin_memory()
+    pinned.numpy()[:] = a
+    g = cg.corutv_ooc(pinned.numpy(), 30, 1, seed=seed, chunk_rows=400, ctx=ctx)
+    assert np.array_equal(f.u, g.u) and np.array_equal(f.t, g.t) and np.array_equal(f.v, g.v)
+    wide = np.zeros((3001, 800))
+    wide[:, :700] = a
+    h = cg.corutv_ooc(wide[:, :700], 30, 1, seed=seed, chunk_rows=400, ctx=ctx)  # lda = 800
+    assert np.array_equal(f.t, h.t) and np.array_equal(f.u, h.u)
+    one = cg.corutv_ooc(a, 30, 1, seed=seed, chunk_rows=3001, ctx=ctx)          # a single chunk
+    assert abs(rel_recon_error(a, one.u, one.t, one.v) - rel_recon_error(a, f.u, f.t, f.v)) <= 1e-8
+
+
+def test_ooc_fp32(ctx):
+    import paper_1810_07323_b200 as cg
+    rng = np.random.default_rng(5)
+    x, _ = np.linalg.qr(rng.standard_normal((2000, 50)))
+    y, _ = np.linalg.qr(rng.standard_normal((900, 50)))
+    a = ((x * (0.85 ** np.arange(50))) @ y.T).astype(np.float32)
+    seed = cg.RngSeed(11, 0)
+    f = cg.corutv_ooc(a, 20, 1, seed=seed, chunk_rows=300, ctx=ctx)
+    g = cg.corutv(a, 20, 1, cg.DVariant.exact, seed, ctx=ctx)
+    e_f = rel_recon_error(a.astype(np.float64), f.u.astype(np.float64), f.t.astype(np.float64), f.v.astype(np.float64))
+    e_g = rel_recon_error(a.astype(np.float64), g.u.astype(np.float64), g.t.astype(np.float64), g.v.astype(np.float64))
+    assert abs(e_f - e_g) <= 1e-4 * e_g
+    assert np.max(np.abs(np.abs(np.diag(f.t)) - np.abs(np.diag(g.t)))) <= 1e-3
+
+
+def test_ooc_errors(ctx):
+    import paper_1810_07323_b200 as cg
+    a = np.random.default_rng(0).standard_normal((50, 80))
+    with pytest.raises(NotImplementedError):
+        cg.corutv_ooc(a, 5, 0, ctx=ctx)                               # rows < cols
+    with pytest.raises(cg.CoruInvalidArgument):
+        cg.corutv_ooc(np.ascontiguousarray(a.T), 50, 0, ctx=ctx)      # ell >= min(rows, cols)
+    with pytest.raises(cg.CoruInvalidArgument):
+        cg.corutv_ooc(np.ascontiguousarray(a.T), 5, -1, ctx=ctx)      # q < 0
