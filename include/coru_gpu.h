@@ -43,7 +43,8 @@ enum coru_status {
     CORU_ECUDA = 2,   /* CUDA runtime / launch failure, or no sm_100 device */
     CORU_ENCCL = 3,   /* NCCL failure (multi-GPU) */
     CORU_ENOMEM = 4,  /* device or pinned-host allocation failed */
-    CORU_ENOTSUP = 5  /* valid in the reference, not provided by this build */
+    CORU_ENOTSUP = 5, /* valid in the reference, not provided by this build */
+    CORU_EIO = 6      /* coru::IoError (io.hpp): unreadable / malformed CORU file */
 };
 
 /* DVariant (corutv.hpp:17): exact = D from one more pass over A (corutv.hpp:90); approx = D from the
@@ -144,6 +145,16 @@ int coru_corutv_f64_ooc(coru_ctx* ctx, const double* A, int64_t m, int64_t n, in
                         int variant, uint64_t seed, uint64_t stream, int64_t chunk_rows, coru_utv* out);
 int coru_corutv_f32_ooc(coru_ctx* ctx, const float* A, int64_t m, int64_t n, int64_t lda, int64_t ell, int q,
                         int variant, uint64_t seed, uint64_t stream, int64_t chunk_rows, coru_utv* out);
+
+/* CORU binary matrix files (write_matrix_bin / read_matrix_bin, io.hpp:67-95): "CORU", rows, cols as
+ * u64 little-endian, then rows·cols fp64 little-endian row-major. The header reader validates the magic
+ * and the exact file size (CORU_EIO with the reference's messages). The file entry memory-maps the
+ * file and runs the out-of-core corutv on it directly (A never materialised in host RAM beyond the
+ * page cache); non-finite entries return CORU_EIO like read_matrix_bin. U, T, V: device buffers for
+ * rows x ell, ell x ell, cols x ell (rows >= cols). */
+int coru_read_matrix_bin_header(const char* path, int64_t* rows, int64_t* cols);
+int coru_corutv_f64_file(coru_ctx* ctx, const char* path, int64_t ell, int q, int variant, uint64_t seed,
+                         uint64_t stream, int64_t chunk_rows, coru_utv* out);
 
 /* ---- the sketch stage: detail::sketch_bases (corutv.hpp:42-65) ------------------------------- */
 /* Requires rows(A) >= cols(A) like the reference's callers (rpca.hpp:135, baselines.hpp:68).

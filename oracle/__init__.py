@@ -311,6 +311,8 @@ class Reference:
         L.ref_corutv_batch.restype = _dbl
         L.ref_frobenius.argtypes = [_p, _i64, _i64]
         L.ref_frobenius.restype = _dbl
+        L.ref_write_matrix_bin.argtypes = [C.c_char_p, _p, _i64, _i64]
+        L.ref_read_matrix_bin.argtypes = [C.c_char_p, _p, _p, _p]
         L.ref_alm_rpca.argtypes = [_p, _i64, _i64, _p, _p, _u64, _u64, _p, _p, _p, _p]
         L.ref_gen_rpca_instance.argtypes = [_i64, _i64, _u64, _dbl, _u64, _u64, _p, _p, _p]
         L.ref_spectral_norm.argtypes = [_p, _i64, _i64]
@@ -434,6 +436,18 @@ class Reference:
         m, l, sp = np.empty((n, n)), np.empty((n, n)), np.empty((n, n))
         self._check(self.lib.ref_gen_rpca_instance(n, r, s, amplitude, seed, stream, _ptr(m), _ptr(l), _ptr(sp)))
         return m, l, sp
+
+    def write_matrix_bin(self, path, a):
+        a = np.ascontiguousarray(a, np.float64)
+        self._check(self.lib.ref_write_matrix_bin(path.encode(), _ptr(a), a.shape[0], a.shape[1]))
+
+    def read_matrix_bin(self, path):
+        """read_matrix_bin (io.hpp:79-95); raises on malformed files like the reference (IoError)."""
+        mn = np.zeros(2, np.int64)
+        self._check(self.lib.ref_read_matrix_bin(path.encode(), _ptr(mn[:1]), _ptr(mn[1:]), None))
+        out = np.empty((int(mn[0]), int(mn[1])))
+        self._check(self.lib.ref_read_matrix_bin(path.encode(), _ptr(mn[:1]), _ptr(mn[1:]), _ptr(out)))
+        return out
 
     def spectral_norm(self, a):
         a = np.ascontiguousarray(a, np.float64)

@@ -21,6 +21,7 @@
 #include "coru/corutv.hpp"
 #include "coru/norms.hpp"
 #include "coru/rpca.hpp"
+#include "coru/io.hpp"
 #include "coru/testgen.hpp"
 
 using coru::Matrix;
@@ -312,5 +313,18 @@ int ref_gen_rpca_instance(int64_t n, int64_t r, uint64_t s, double amp, uint64_t
 
 // coru::spectral_norm (norms.hpp:27)
 double ref_spectral_norm(const double* a, int64_t m, int64_t n) { return coru::spectral_norm(wrap(a, m, n)); }
+
+// coru::write_matrix_bin / read_matrix_bin (io.hpp:67-95). Reader: rows/cols out, data (may be NULL).
+int ref_write_matrix_bin(const char* path, const double* a, int64_t m, int64_t n) {
+    return guarded([&] { coru::write_matrix_bin(path, wrap(a, m, n)); });
+}
+int ref_read_matrix_bin(const char* path, int64_t* m, int64_t* n, double* out) {
+    return guarded([&] {
+        Matrix x = coru::read_matrix_bin(path);
+        *m = int64_t(x.rows());
+        *n = int64_t(x.cols());
+        put(x, out);
+    });
+}
 
 }  // extern "C"

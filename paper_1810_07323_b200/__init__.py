@@ -45,7 +45,7 @@ __all__ = [
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _LIB_PATH = os.path.join(_HERE, "libcoru_gpu.so")
 
-CORU_OK, CORU_EINVAL, CORU_ECUDA, CORU_ENCCL, CORU_ENOMEM, CORU_ENOTSUP = range(6)
+CORU_OK, CORU_EINVAL, CORU_ECUDA, CORU_ENCCL, CORU_ENOMEM, CORU_ENOTSUP, CORU_EIO = range(7)
 
 
 class CoruError(RuntimeError):
@@ -157,6 +157,8 @@ def load_library():
                                                      C.POINTER(i32), C.POINTER(i32)]
     for sfx in ("f64", "f32"):
         getattr(L, f"coru_corutv_{sfx}_ooc").argtypes = [p, p, i64, i64, i64, i64, i32, i32, u64, u64, i64, p]
+    L.coru_read_matrix_bin_header.argtypes = [C.c_char_p, C.POINTER(i64), C.POINTER(i64)]
+    L.coru_corutv_f64_file.argtypes = [p, C.c_char_p, i64, i32, i32, u64, u64, i64, p]
     L.coru_sketch_bases_f64_dev.argtypes = [p, p, i64, i64, i64, i64, i64, i32, u64, u64, p, i64, p, i64, p, i64,
                                             p, i64, C.POINTER(i32)]
     L.coru_sketch_bases_f64.argtypes = [p, p, i64, i64, i64, i32, u64, u64, p, p, p, p, C.POINTER(i32)]
@@ -190,6 +192,8 @@ def _check(rc: int):
         raise CoruInvalidArgument(msg)
     if rc == CORU_ENOTSUP:
         raise NotImplementedError(msg)
+    if rc == CORU_EIO:
+        raise CoruIoError(msg)
     raise CoruError(rc, msg)
 
 
@@ -704,4 +708,43 @@ def corutv_ooc(a: np.ndarray, ell: int, q: int, variant: DVariant = DVariant.exa
                                                      int(variant), seed.seed, seed.stream, chunk_rows, C.byref(out)))
     torch.cuda.synchronize(dev)
     return UtvApprox(u.cpu().numpy(), t.cpu().numpy(), v.cpu().numpy(), ell, q, variant, seed, bool(out.lower),
+                     bool(out.conditioning_warning), perm)
+
+
+class CoruIoError(IOError):
+    """coru::IoError (io.hpp): unreadable or malformed CORU file (CORU_EIO)."""
+
+
+def write_matrix_bin(path: str, a: np.ndarray) -> None:
+    """write_matrix_bin (io.hpp:67-77): "CORU", rows, cols (u64 LE), fp64 LE row-major."""
+    import struct
+    a = np.ascontiguousarray(a, "<f8")
+    with open(path, "wb") as f:
+        f.write(b"CORU" + struct.pack("<QQ", a.shape[0], a.shape[1]))
+        f.write(a.tobytes())
+
+
+def read_matrix_bin_header(path: str) -> tuple[int, int]:
+    r, c = C.c_int64(), C.c_int64()
+    _check(load_library().coru_read_matrix_bin_header(path.encode(), C.byref(r), C.byref(c)))
+    return r.value, c.value
+
+
+def corutv_file(path: str, ell: int, q: int, variant: DVariant = DVariant.exact, seed: RngSeed = RngSeed(),
+                chunk_rows: int = 0, ctx: Optional[Context] = None) -> UtvApprox:
+    """corutv of a CORU binary matrix file, streamed out of core from the memory-mapped file."""
+    import torch
+    ctx = ctx or default_context()
+    m, n = read_matrix_bin_header(path)
+    dev = torch.device("cuda", ctx.device)
+    u = torch.empty((m, ell), dtype=torch.float64, device=dev)
+    t = torch.empty((ell, ell), dtype=torch.float64, device=dev)
+    v = torch.empty((n, ell), dtype=torch.float64, device=dev)
+    perm = np.zeros(ell, np.int64)
+    out = _Utv(u.data_ptr(), ell, t.data_ptr(), ell, v.data_ptr(), ell, perm.ctypes.data, 0, 0)
+    torch.cuda.synchronize(dev)
+    _check(ctx.lib.coru_corutv_f64_file(ctx.h, path.encode(), ell, q, int(variant), seed.seed, seed.stream, chunk_rows,
+                                        C.byref(out)))
+    torch.cuda.synchronize(dev)
+    return UtvApprox(u.cpu().numpy(), t.cpu().numpy(), v.cpu().numpy(), ell, q, variant, seed, False,
                      bool(out.conditioning_warning), perm)

@@ -12,6 +12,10 @@
 // redundant top QR on every rank), and everything ell x ell or n x ell is computed redundantly
 // and bit-identically on every rank (all kernels are atomic-free and fixed-order).
 #include <dlfcn.h>
+#include <fcntl.h>
+#include <sys/mman.h>
+#include <sys/stat.h>
+#include <unistd.h>
 #include <cstdlib>
 #include <nccl.h>
 
@@ -647,8 +651,13 @@ int run_impl(coru_ctx* c, const Request<T>& r, size_t extra_arena_off) {
     if (r.a_host) {
         // Each power round reads A once: c1 rows of chunk i = A_i·c2, and the partial A_i^T·c1_i from
         // the same chunk, summed into the next c2 in chunk order (deterministic).
+        CORU_CUDA(cudaMemsetAsync(w.flag + 1, 0, sizeof(int), st));
         for (int i = 0; i <= r.q; ++i) {
             CORU_TRY(stream_a([&](int64_t ch, int64_t r0, int64_t rows, const T* Ai) -> int {
+                if (i == 0) {  // finiteness, as the Matrix constructor / read_matrix_bin (matrix.hpp:29-31)
+                    CORU_CUDA(any_nonfinite_acc<T>(Ai, rows * N, w.flag + 1, st));
+                    ++g_launches;
+                }
                 CORU_TRY(gemm<T>(c, Op::N, Ai, N, w.b2, dp, w.b1 + r0 * dp, dp, rows, N, d, w.gws, w.gws_elems));
                 T* out = ch == 0 ? w.b2n : w.part;
                 CORU_TRY(gemm<T>(c, Op::T, Ai, N, w.b1 + r0 * dp, dp, out, dp, N, rows, d, w.gws, w.gws_elems));
@@ -658,6 +667,12 @@ int run_impl(coru_ctx* c, const Request<T>& r, size_t extra_arena_off) {
                 }
                 return CORU_OK;
             }));
+            if (i == 0) {
+                int bad = 0;
+                CORU_CUDA(cudaMemcpyAsync(&bad, w.flag + 1, sizeof(int), cudaMemcpyDeviceToHost, st));
+                CORU_CUDA(cudaStreamSynchronize(st));
+                if (bad) return fail(CORU_EINVAL, "Matrix: non-finite entry");
+            }
             if (i == r.q && w.b2prev)
                 CORU_CUDA(cudaMemcpyAsync(w.b2prev, w.b2, size_t(N) * dp * sizeof(T), cudaMemcpyDeviceToDevice, st));
             std::swap(w.b2, w.b2n);
@@ -1857,6 +1872,55 @@ int coru_corutv_f64_ooc(coru_ctx* c, const double* A, int64_t m, int64_t n, int6
     CORU_TRY(enter(c));
     std::lock_guard<std::mutex> lk(c->mu);
     return corutv_ooc<double>(c, A, m, n, lda, ell, q, variant, seed, stream, chunk_rows, out);
+}
+
+// CORU binary matrix (io.hpp:67-95): "CORU", rows, cols (u64 little-endian), rows·cols fp64 LE row-major.
+int coru_read_matrix_bin_header(const char* path, int64_t* rows, int64_t* cols) {
+    if (!path || !rows || !cols) return fail(CORU_EINVAL, "null argument");
+    const int fd = open(path, O_RDONLY);
+    if (fd < 0) return fail(CORU_EIO, std::string("cannot open ") + path);
+    struct stat stt {};
+    unsigned char h[20];
+    const bool ok = fstat(fd, &stt) == 0 && pread(fd, h, 20, 0) == 20;
+    close(fd);
+    auto u64 = [&](int o) {
+        uint64_t v = 0;
+        for (int b = 7; b >= 0; --b) v = (v << 8) | h[o + b];
+        return v;
+    };
+    if (!ok || stt.st_size < 20 || std::memcmp(h, "CORU", 4) != 0)
+        return fail(CORU_EIO, std::string(path) + ": not a CORU binary matrix");
+    const uint64_t r = u64(4), cc = u64(12);
+    if (r == 0 || cc == 0 || cc > (uint64_t(1) << 40) / r || uint64_t(stt.st_size) != 20 + 8 * r * cc)
+        return fail(CORU_EIO, std::string(path) + ": truncated or malformed CORU file");
+    *rows = int64_t(r);
+    *cols = int64_t(cc);
+    return CORU_OK;
+}
+
+int coru_corutv_f64_file(coru_ctx* c, const char* path, int64_t ell, int q, int variant, uint64_t seed,
+                         uint64_t stream, int64_t chunk_rows, coru_utv* out) {
+    CORU_TRY(enter(c));
+    int64_t m = 0, n = 0;
+    CORU_TRY(coru_read_matrix_bin_header(path, &m, &n));
+    const int fd = open(path, O_RDONLY);
+    if (fd < 0) return fail(CORU_EIO, std::string("cannot open ") + path);
+    const size_t len = 20 + size_t(m) * size_t(n) * 8;
+    void* base = mmap(nullptr, len, PROT_READ, MAP_PRIVATE, fd, 0);
+    close(fd);
+    if (base == MAP_FAILED) return fail(CORU_EIO, std::string("mmap failed: ") + path);
+    madvise(base, len, MADV_SEQUENTIAL);
+    // the payload starts at byte 20 (4 mod 8): it is only ever copied as bytes (cudaMemcpy2DAsync)
+    const double* A = reinterpret_cast<const double*>(static_cast<const char*>(base) + 20);
+    int rc;
+    {
+        std::lock_guard<std::mutex> lk(c->mu);
+        rc = corutv_ooc<double>(c, A, m, n, n, ell, q, variant, seed, stream, chunk_rows, out);
+    }
+    munmap(base, len);
+    if (rc == CORU_EINVAL && std::string(coru_last_error()) == "Matrix: non-finite entry")
+        return fail(CORU_EIO, std::string(path) + ": Matrix: non-finite entry");
+    return rc;
 }
 
 int coru_corutv_f32_ooc(coru_ctx* c, const float* A, int64_t m, int64_t n, int64_t lda, int64_t ell, int q,

@@ -247,3 +247,10 @@ if __name__ == "__main__":
         rpca_fixtures()
         sys.exit(0)
     main()
+
+
+def bin_fixtures():
+    """CORU binary files written by the reference's write_matrix_bin (io.hpp:67-77)."""
+    R.write_matrix_bin(os.path.join(HERE, "ref_matrix_3x2.bin"),
+                       np.array([[1.5, -2.0], [3.25, np.pi], [1e-300, -0.0]]))
+    R.write_matrix_bin(os.path.join(HERE, "ref_gaussian_64x24.bin"), R.gaussian(64, 24, 5, 0))

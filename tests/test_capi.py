@@ -88,3 +88,41 @@ def test_rpca_config_validation_before_device():
     c = cg._RpcaConfig()
     lib.coru_rpca_config_default(C.byref(c))
     assert (c.rho, c.tol, c.max_iter, c.corutv_q, c.inner, c.thresholding) == (1.5, 1e-5, 50, 1, 1, 0)
+
+
+def test_coru_bin_format_against_reference(tmp_path):
+    """write_matrix_bin / read_matrix_bin (io.hpp:67-95): the reference's own files (tests/golden/*.bin)
+    parse with the C-ABI header reader and the Python writer produces the reference's bytes."""
+    import os
+    import paper_1810_07323_b200 as cg
+    from golden import HERE
+    for name, shape in (("ref_matrix_3x2.bin", (3, 2)), ("ref_gaussian_64x24.bin", (64, 24))):
+        path = os.path.join(HERE, name)
+        assert cg.read_matrix_bin_header(path) == shape
+        raw = open(path, "rb").read()
+        a = np.frombuffer(raw[20:], "<f8").reshape(shape)
+        mine = tmp_path / name
+        cg.write_matrix_bin(str(mine), a)
+        assert mine.read_bytes() == raw                       # byte-identical to the reference's writer
+    bad = tmp_path / "bad.bin"
+    bad.write_bytes(b"CORX" + bytes(16) + bytes(8))
+    with pytest.raises(cg.CoruIoError):
+        cg.read_matrix_bin_header(str(bad))
+    trunc = tmp_path / "trunc.bin"
+    trunc.write_bytes(open(os.path.join(HERE, "ref_matrix_3x2.bin"), "rb").read()[:-1])
+    with pytest.raises(cg.CoruIoError):
+        cg.read_matrix_bin_header(str(trunc))
+    with pytest.raises(cg.CoruIoError):
+        cg.read_matrix_bin_header(str(tmp_path / "missing.bin"))
+
+
+def test_coru_bin_reference_reader_roundtrip(reference, tmp_path):
+    import paper_1810_07323_b200 as cg
+    a = np.random.default_rng(1).standard_normal((17, 9))
+    p = str(tmp_path / "a.bin")
+    cg.write_matrix_bin(p, a)
+    assert np.array_equal(reference.read_matrix_bin(p), a)
+    a[2, 3] = np.inf
+    cg.write_matrix_bin(p, a)
+    with pytest.raises(Exception):
+        reference.read_matrix_bin(p)                           # IoError: non-finite (io.hpp:90-94)
