@@ -48,6 +48,20 @@ __global__ void __launch_bounds__(kThreads, 2) k_rpca_lift_update(const double* 
     const int64_t tiles_n = (n + kTile - 1) / kTile;
     const int64_t tiles = ((m + kTile - 1) / kTile) * tiles_n;
     double part = 0.0;
+    // Tp / V chunks (kTile x kKc each) are loaded into registers one chunk ahead of the FMAs
+    constexpr int kPer = kTile * kKc / kThreads;
+    double pT[kPer], pV[kPer];
+    auto load_chunk = [&](int64_t tt, int k0) {
+        const int64_t ti0 = (tt / tiles_n) * kTile, tj0 = (tt % tiles_n) * kTile;
+#pragma unroll
+        for (int q = 0; q < kPer; ++q) {
+            const int e = threadIdx.x + q * kThreads;
+            const int r = e / kKc, c = e % kKc;
+            const bool kc = k0 + c < d;
+            pT[q] = (kc && ti0 + r < m) ? __ldg(Tp + (ti0 + r) * ldt + k0 + c) : 0.0;
+            pV[q] = (kc && tj0 + r < n) ? __ldg(Vb + (tj0 + r) * ldv + k0 + c) : 0.0;
+        }
+    };
     for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
         const int64_t i0 = (t / tiles_n) * kTile, j0 = (t % tiles_n) * kTile;
         if (!lift_only) {
@@ -77,14 +91,19 @@ __global__ void __launch_bounds__(kThreads, 2) k_rpca_lift_update(const double* 
         for (int i = 0; i < 4; ++i)
 #pragma unroll
             for (int j = 0; j < 4; ++j) acc[i][j] = 0.0;
+        if (t == int64_t(blockIdx.x)) load_chunk(t, 0);  // later tiles: issued before the previous epilogue
         for (int k0 = 0; k0 < d; k0 += kKc) {
-            for (int e = threadIdx.x; e < kTile * kKc; e += kThreads) {
-                const int r = e / kKc, c = e % kKc;
-                const bool kc = k0 + c < d;
-                sT[r][c] = (kc && i0 + r < m) ? __ldg(Tp + (i0 + r) * ldt + k0 + c) : 0.0;
-                sV[r][c] = (kc && j0 + r < n) ? __ldg(Vb + (j0 + r) * ldv + k0 + c) : 0.0;
+            __syncthreads();  // the previous chunk's FMAs are done with sT / sV
+#pragma unroll
+            for (int q = 0; q < kPer; ++q) {
+                const int e = threadIdx.x + q * kThreads;
+                sT[e / kKc][e % kKc] = pT[q];
+                sV[e / kKc][e % kKc] = pV[q];
             }
             __syncthreads();
+            // next chunk of this tile, or chunk 0 of the next tile: in flight under this chunk's FMAs
+            if (k0 + kKc < d) load_chunk(t, k0 + kKc);
+            else if (t + gridDim.x < tiles) load_chunk(t + gridDim.x, 0);
             const int kn = min(kKc, d - k0);
             for (int kk = 0; kk < kn; ++kk) {
                 double a[4], b[4];
@@ -97,7 +116,6 @@ __global__ void __launch_bounds__(kThreads, 2) k_rpca_lift_update(const double* 
 #pragma unroll
                     for (int j = 0; j < 4; ++j) acc[i][j] = fma(a[i], b[j], acc[i][j]);
             }
-            __syncthreads();
         }
         if (!lift_only) {
             asm volatile("cp.async.wait_group 0;\n" ::);
