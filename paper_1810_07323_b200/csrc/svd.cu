@@ -77,8 +77,8 @@ __device__ __forceinline__ double group_sum(double v) {
 // E > 0: the columns live in shared memory and each lane keeps its E entries of the four columns
 // of its pair (a_j, a_k, v_j, v_k) in registers for the whole rotation (one load round, one store
 // round); E = 0: columns in the global workspace (wide cores), streamed per loop.
-template <typename T, int G, int E>
-__global__ void __launch_bounds__(E > 0 ? 512 : kJacThreadsMax, 1)
+template <typename T, int G, int E, int MAXT = (E > 0 ? 512 : kJacThreadsMax)>
+__global__ void __launch_bounds__(MAXT, 1)
     k_jacobi_svd(const T* __restrict__ Y, int64_t ldy, int d, double* ws, int cols_in_smem, int* converged_out,
                  int svd_mode) {
     constexpr int kPairsPerWarp = kWarp / G;
@@ -678,6 +678,7 @@ template <typename T>
 cudaError_t jacobi_run(const T* Y, int64_t ldy, int d, double* ws, int* converged, int max_smem, int svd_mode,
                        cudaStream_t st) {
     const bool in_smem = jacobi_smem(d, true) <= size_t(max_smem);
+    static const int jac_variant = getenv("CORU_JACOBI_VARIANT") ? atoi(getenv("CORU_JACOBI_VARIANT")) : 1;
     const size_t smem = jacobi_smem(d, in_smem);
     // G lanes per column pair, at most 8 column entries per lane (register path when the columns
     // fit shared memory); enough warps for the d/2 pairs of a round-robin step
@@ -691,6 +692,11 @@ cudaError_t jacobi_run(const T* Y, int64_t ldy, int d, double* ws, int* converge
     };
     if (in_smem && d <= 32) launch(k_jacobi_svd<T, 4, 8>, 4, 16);
     else if (in_smem && d <= 64) launch(k_jacobi_svd<T, 8, 8>, 8, 16);
+    // 64 < d <= 128: 16 lanes per pair fit 32 pairs in 512 threads, so d > 64 takes two rounds per
+    // round-robin step; 20 warps (d <= 80, default) run a step in one (d = 80: -6 %); 8 lanes x 16
+    // entries (variant 2) is slower (longer per-lane chains).
+    else if (in_smem && d <= 80 && jac_variant == 1) launch(k_jacobi_svd<T, 16, 8, 640>, 16, 20);
+    else if (in_smem && d <= 128 && jac_variant == 2) launch(k_jacobi_svd<T, 8, 16, 512>, 8, 16);
     else if (in_smem && d <= 128) launch(k_jacobi_svd<T, 16, 8>, 16, 16);
     else if (d <= kWarp * kGridE) {
         // cooperative grid: one warp per pair of a step, every CTA co-resident
