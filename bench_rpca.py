@@ -55,6 +55,22 @@ def spectral_estimate(torch, m, iters=60):
     return float(np.sqrt(s))
 
 
+def ncu_update_traffic():
+    """DRAM bytes per launch of the fused update kernel from the committed ncu --set full summary."""
+    path = os.path.join(ROOT, "profiles", "r01_ncu_full_rpca_update.json")
+    try:
+        with open(path) as f:
+            d = json.load(f)
+        scale = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+        tot = 0.0
+        for k in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+            v, unit = d[k].split()
+            tot += float(v) * scale[unit]
+        return tot
+    except (OSError, KeyError, ValueError):
+        return None
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--n", type=int, default=8000)
@@ -140,8 +156,9 @@ def main():
             "share_of_step": ap_prof["ms"] / total_ms,
             "peak_source": "cuBLAS DGEMM 8192^3 burst measured in this run"}
     roof_upd = {"bound": "hbm", "achieved": up_gbs, "peak": hbm, "unit": "GB/s", "frac": up_gbs / hbm,
-                "traffic": None, "kernel": "k_rpca_lift_update (L = Tp·V^T in registers + shrink / multiplier / next "
-                "iterate; reads M, Y, writes S, Y, X)", "algorithmic_bytes_per_launch": up_bytes,
+                "traffic": ncu_update_traffic() if n == 8000 and r == 40 else None,
+                "kernel": "k_rpca_lift_update (L = Tp·V^T in registers + shrink / multiplier / next iterate; "
+                          "reads M, Y, writes S, Y, X)", "algorithmic_bytes_per_launch": up_bytes,
                 "avg_launch_ms": up_avg, "launches": up_prof["launches"], "share_of_step": up_prof["ms"] / total_ms,
                 "peak_source": psrc}
     cpu = None

@@ -139,8 +139,9 @@ int coru_corutv_f32(coru_ctx* ctx, const float* A, int64_t m, int64_t n, int64_t
  * more: q + 2 streams of A (exact) / q + 1 (approx) instead of 2q + 3 / 2q + 2 passes. Only the
  * sketches (m x ell, cols x ell) and two chunks live on the device, so A may exceed HBM. Pageable
  * host memory is page-locked for the duration of the call. Outputs as coru_corutv_*_dev (device
- * U, T, V). rows < cols returns CORU_ENOTSUP. Deterministic; differs from the in-core path at
- * rounding level (chunk-ordered partial sums). */
+ * U, T, V; host pointers are also accepted: the call then copies the factors back). rows < cols
+ * returns CORU_ENOTSUP. Deterministic; differs from the in-core path at rounding level
+ * (chunk-ordered partial sums). */
 int coru_corutv_f64_ooc(coru_ctx* ctx, const double* A, int64_t m, int64_t n, int64_t lda, int64_t ell, int q,
                         int variant, uint64_t seed, uint64_t stream, int64_t chunk_rows, coru_utv* out);
 int coru_corutv_f32_ooc(coru_ctx* ctx, const float* A, int64_t m, int64_t n, int64_t lda, int64_t ell, int q,
@@ -150,8 +151,8 @@ int coru_corutv_f32_ooc(coru_ctx* ctx, const float* A, int64_t m, int64_t n, int
  * u64 little-endian, then rows·cols fp64 little-endian row-major. The header reader validates the magic
  * and the exact file size (CORU_EIO with the reference's messages). The file entry memory-maps the
  * file and runs the out-of-core corutv on it directly (A never materialised in host RAM beyond the
- * page cache); non-finite entries return CORU_EIO like read_matrix_bin. U, T, V: device buffers for
- * rows x ell, ell x ell, cols x ell (rows >= cols). */
+ * page cache); non-finite entries return CORU_EIO like read_matrix_bin. U, T, V: device (or host)
+ * buffers for rows x ell, ell x ell, cols x ell (rows >= cols). */
 int coru_read_matrix_bin_header(const char* path, int64_t* rows, int64_t* cols);
 int coru_corutv_f64_file(coru_ctx* ctx, const char* path, int64_t ell, int q, int variant, uint64_t seed,
                          uint64_t stream, int64_t chunk_rows, coru_utv* out);

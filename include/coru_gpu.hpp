@@ -214,6 +214,41 @@ inline RpcaResult alm_rpca(const Matrix& m, const RpcaConfig& config, RngSeed se
     return r;
 }
 
+// Out-of-core corutv (§8 f4): A streamed from host memory in row chunks (rows >= cols); the same
+// UtvApprox as corutv. chunk_rows = 0: ~512 MB chunks.
+inline UtvApprox corutv_streamed(const Matrix& a, std::size_t ell, int q, DVariant variant, RngSeed seed,
+                                 std::int64_t chunk_rows = 0) {
+    if (ell < 1) throw std::invalid_argument("corutv: ell must be >= 1");
+    if (ell >= std::min(a.rows(), a.cols())) throw std::invalid_argument("corutv: ell must be < min(rows, cols)");
+    if (q < 0) throw std::invalid_argument("corutv: q must be >= 0");
+    UtvApprox f{Matrix(a.rows(), ell), Matrix(ell, ell), Matrix(a.cols(), ell), ell, q, variant, seed,
+                false, false, std::vector<std::int64_t>(ell)};
+    const std::int64_t l = std::int64_t(ell);
+    coru_utv out{f.u.data().data(), l, f.t.data().data(), l, f.v.data().data(), l, f.perm.data(), 0, 0};
+    detail::throw_status(coru_corutv_f64_ooc(detail::thread_context(), a.data().data(), std::int64_t(a.rows()),
+                                             std::int64_t(a.cols()), std::int64_t(a.cols()), l, q,
+                                             variant == DVariant::exact ? CORU_D_EXACT : CORU_D_APPROX, seed.seed,
+                                             seed.stream, chunk_rows, &out));
+    f.conditioning_warning = out.conditioning_warning != 0;
+    return f;
+}
+
+// corutv(read_matrix_bin(path), ...) without materialising the matrix (io.hpp:79-95 + corutv.hpp:79).
+inline UtvApprox corutv_file(const std::string& path, std::size_t ell, int q, DVariant variant, RngSeed seed,
+                             std::int64_t chunk_rows = 0) {
+    std::int64_t m = 0, n = 0;
+    detail::throw_status(coru_read_matrix_bin_header(path.c_str(), &m, &n));
+    UtvApprox f{Matrix(std::size_t(m), ell), Matrix(ell, ell), Matrix(std::size_t(n), ell), ell, q, variant, seed,
+                false, false, std::vector<std::int64_t>(ell)};
+    const std::int64_t l = std::int64_t(ell);
+    coru_utv out{f.u.data().data(), l, f.t.data().data(), l, f.v.data().data(), l, f.perm.data(), 0, 0};
+    detail::throw_status(coru_corutv_f64_file(detail::thread_context(), path.c_str(), l, q,
+                                              variant == DVariant::exact ? CORU_D_EXACT : CORU_D_APPROX, seed.seed,
+                                              seed.stream, chunk_rows, &out));
+    f.conditioning_warning = out.conditioning_warning != 0;
+    return f;
+}
+
 // singular_estimates (corutv.hpp:113-117)
 inline std::vector<double> singular_estimates(const UtvApprox& f) {
     std::vector<double> s(f.ell);

@@ -886,6 +886,30 @@ int corutv_ooc(coru_ctx* c, const T* A, int64_t m, int64_t n, int64_t lda, int64
     r.t = static_cast<T*>(out->t);
     r.ldt = out->ldt;
     out->lower = 0;
+    // Host output buffers (the C++ drop-in passes coru::Matrix storage): run into device scratch
+    // and copy back (U m x ell, T ell x ell, V n x ell with the caller's leading dimensions).
+    auto is_host = [](const void* ptr) {
+        cudaPointerAttributes a{};
+        if (cudaPointerGetAttributes(&a, ptr) != cudaSuccess) {
+            cudaGetLastError();
+            return true;
+        }
+        return a.type == cudaMemoryTypeUnregistered || a.type == cudaMemoryTypeHost;
+    };
+    T* dev_out = nullptr;
+    if (is_host(out->u) || is_host(out->t) || is_host(out->v)) {
+        const size_t elems = size_t(m) * ell + size_t(ell) * ell + size_t(n) * ell;
+        if (cudaMalloc(&dev_out, elems * sizeof(T)) != cudaSuccess) {
+            cudaGetLastError();
+            return fail(CORU_ENOMEM, "cudaMalloc of the out-of-core output buffers failed");
+        }
+        r.u = dev_out;
+        r.ldu = ell;
+        r.t = dev_out + size_t(m) * ell;
+        r.ldt = ell;
+        r.v = dev_out + size_t(m) * ell + size_t(ell) * ell;
+        r.ldv = ell;
+    }
     bool registered = false;
     cudaPointerAttributes pa{};
     const size_t bytes = size_t(m - 1) * lda * sizeof(T) + size_t(n) * sizeof(T);
@@ -894,7 +918,22 @@ int corutv_ooc(coru_ctx* c, const T* A, int64_t m, int64_t n, int64_t lda, int64
         registered = cudaHostRegister(const_cast<T*>(A), bytes, cudaHostRegisterReadOnly) == cudaSuccess;
         cudaGetLastError();  // registration is an optimisation: pageable copies still work
     }
-    const int rc = run<T>(c, r);
+    int rc = run<T>(c, r);
+    if (dev_out) {
+        if (rc == CORU_OK) {
+            auto back = [&](void* dst, int64_t ldd, const T* src, int64_t rows) -> cudaError_t {
+                return cudaMemcpy2DAsync(dst, size_t(ldd) * sizeof(T), src, size_t(ell) * sizeof(T),
+                                         size_t(ell) * sizeof(T), size_t(rows), cudaMemcpyDeviceToHost, c->stream);
+            };
+            cudaError_t e = back(out->u, out->ldu, r.u, m);
+            if (e == cudaSuccess) e = back(out->t, out->ldt, r.t, ell);
+            if (e == cudaSuccess) e = back(out->v, out->ldv, r.v, n);
+            if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
+            if (e != cudaSuccess) rc = fail(CORU_ECUDA, std::string("output copy: ") + cudaGetErrorString(e));
+        }
+        cudaStreamSynchronize(c->stream);
+        cudaFree(dev_out);
+    }
     if (registered) {
         cudaStreamSynchronize(c->stream);
         cudaStreamSynchronize(c->aux);

@@ -151,6 +151,27 @@ int main() {
         }
         CHECK(threw);
     }
+    // out-of-core (§8 f4): streamed from host memory and from a CORU .bin file (io.hpp:67-77)
+    {
+        const Matrix a = exact_rank(300, 120, 6, {41, 0});
+        UtvApprox in = corutv(a, 10, 1, DVariant::exact, {5, 0});
+        UtvApprox st = corutv_streamed(a, 10, 1, DVariant::exact, {5, 0}, 64);
+        CHECK(recon_err(a, st) <= 1e-10 && recon_err(a, in) <= 1e-10);
+        for (std::size_t j = 0; j < 10; ++j) CHECK(std::abs(std::abs(st.t(j, j)) - std::abs(in.t(j, j))) <= 1e-8 * std::abs(in.t(0, 0)));
+        const std::string path = "/tmp/coru_wrapper_test.bin";
+        if (FILE* fp = std::fopen(path.c_str(), "wb")) {
+            const std::uint64_t hdr[2] = {a.rows(), a.cols()};
+            std::fwrite("CORU", 1, 4, fp);
+            std::fwrite(hdr, 8, 2, fp);
+            std::fwrite(a.data().data(), 8, a.data().size(), fp);
+            std::fclose(fp);
+            UtvApprox fl = corutv_file(path, 10, 1, DVariant::exact, {5, 0}, 64);
+            CHECK(fl.t.data() == st.t.data() && fl.u.data() == st.u.data());
+            std::remove(path.c_str());
+        } else {
+            CHECK(false);
+        }
+    }
     std::printf("%s: %d failures\n", failures ? "FAIL" : "OK", failures);
     return failures ? 1 : 0;
 }
