@@ -119,6 +119,7 @@ ncclDataType_t nccl_type() {
 }
 
 int64_t round_up(int64_t x, int64_t a) { return (x + a - 1) / a * a; }
+constexpr int kTnMaxBlocks = 592;  // row blocks of the skinny Q^T·W kernel (tn_small)
 
 // Bump allocator: a measuring pass (base == nullptr) then a carving pass over the arena.
 struct Carver {
@@ -415,6 +416,7 @@ struct Work {
     T *m = nullptr, *qm = nullptr, *tm = nullptr, *qrcp_scr = nullptr;
     T *y1 = nullptr, *y2 = nullptr, *pinv = nullptr;  // approx-D core
     T *cbuf[2] = {nullptr, nullptr}, *b2n = nullptr, *part = nullptr;  // out-of-core chunk ring, next c2, partial
+    T* tnp = nullptr;  // partials of the skinny Q^T·W core products (d <= 64)
     double* pws = nullptr;
     int64_t* perm = nullptr;
     int* flag = nullptr;
@@ -453,6 +455,7 @@ struct Work {
         r1 = cv.take<T>(int64_t(d) * d);
         r2 = cv.take<T>(int64_t(d) * d);
         m = cv.take<T>(int64_t(d) * dp);
+        if (d <= 64) tnp = cv.take<T>(int64_t(kTnMaxBlocks) * d * d);
         qm = cv.take<T>(int64_t(dp) * dp);
         tm = cv.take<T>(int64_t(d) * d);
         qrcp_scr = cv.take<T>(qrcp_scratch_elems(d));
@@ -560,6 +563,82 @@ template <typename T>
 int run_impl(coru_ctx* c, const Request<T>& r, size_t extra_arena_off);
 
 // The hot path. Enqueues everything on c->stream and synchronises once at the end (the flag and
+// Skinny transposed product C (d x d) = Q^T·W for Q, W m x d (ld dp), d <= 64: the core
+// Q1^T·(A·Q2) and the approx-D cores Q1^T·c1, Q2^T·c2prev. The stream-K GEMM splits each of its one
+// or two output tiles over ~60 CTAs whose partials one owner sums serially (53 us at C2); here each
+// CTA reduces a row block into a private d x d partial (4x4 register tile per thread, rows staged
+// through shared memory) and one fixed-order pass sums the partials: deterministic, ~8 us.
+constexpr int kTnRows = 32;
+template <typename T>
+__global__ void __launch_bounds__(256) k_tn_partial(const T* __restrict__ Q, int64_t ldq, const T* __restrict__ W,
+                                                    int64_t ldw, int64_t m, int d, int64_t rows_per_blk,
+                                                    T* __restrict__ part) {
+    __shared__ __align__(16) T sQ[kTnRows][64];
+    __shared__ __align__(16) T sW[kTnRows][64];
+    const int ti = threadIdx.x >> 4, tj = threadIdx.x & 15;  // rows 4ti.., cols 4tj.. of the output
+    const int64_t r0 = int64_t(blockIdx.x) * rows_per_blk, r1 = min(m, r0 + rows_per_blk);
+    T acc[4][4] = {};
+    for (int64_t rb = r0; rb < r1; rb += kTnRows) {
+        for (int e = threadIdx.x; e < kTnRows * 64; e += 256) {
+            const int r = e >> 6, c = e & 63;
+            const bool ok = rb + r < r1 && c < d;
+            sQ[r][c] = ok ? Q[(rb + r) * ldq + c] : T(0);
+            sW[r][c] = ok ? W[(rb + r) * ldw + c] : T(0);
+        }
+        __syncthreads();
+#pragma unroll 4
+        for (int r = 0; r < kTnRows; ++r) {
+            T a[4], b[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                a[u] = sQ[r][4 * ti + u];
+                b[u] = sW[r][4 * tj + u];
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+#pragma unroll
+                for (int v = 0; v < 4; ++v) acc[u][v] = fma(a[u], b[v], acc[u][v]);
+        }
+        __syncthreads();
+    }
+    T* out = part + int64_t(blockIdx.x) * d * d;
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int v = 0; v < 4; ++v) {
+            const int i = 4 * ti + u, j = 4 * tj + v;
+            if (i < d && j < d) out[i * d + j] = acc[u][v];
+        }
+}
+template <typename T>
+__global__ void k_tn_reduce(const T* __restrict__ part, int nblk, int d, T* __restrict__ C, int64_t ldc) {
+    for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < d * d; e += gridDim.x * blockDim.x) {
+        T s = part[e];
+        for (int b = 1; b < nblk; ++b) s += part[int64_t(b) * d * d + e];  // fixed order
+        C[int64_t(e / d) * ldc + e % d] = s;
+    }
+}
+template <typename T>
+int tn_small(coru_ctx* c, const T* Q, int64_t ldq, const T* W, int64_t ldw, int64_t m, int d, T* C, int64_t ldc,
+             T* part) {
+    const int64_t want = (m + 63) / 64;
+    const int nblk = int(std::max<int64_t>(1, std::min<int64_t>(want, kTnMaxBlocks)));
+    const int64_t rpb = (m + nblk - 1) / nblk;
+    k_tn_partial<T><<<nblk, 256, 0, c->stream>>>(Q, ldq, W, ldw, m, d, rpb, part);
+    k_tn_reduce<T><<<(d * d + 255) / 256, 256, 0, c->stream>>>(part, nblk, d, C, ldc);
+    g_launches += 2;
+    CORU_CUDA(cudaGetLastError());
+    return CORU_OK;
+}
+// Q^T·W (d x d): the skinny kernel for d <= 64 (CORU_TN_SMALL=0 restores the GEMM), else the GEMM.
+template <typename T>
+int gemm_tn_core(coru_ctx* c, const T* Q, int64_t ldq, const T* W, int64_t ldw, int64_t m, int d, T* C, int64_t ldc,
+                 T* part, T* gws, int64_t gws_elems) {
+    static const bool on = getenv("CORU_TN_SMALL") == nullptr || atoi(getenv("CORU_TN_SMALL")) != 0;
+    if (on && part && d <= 64) return tn_small<T>(c, Q, ldq, W, ldw, m, d, C, ldc, part);
+    return gemm<T>(c, Op::T, Q, ldq, W, ldw, C, ldc, d, m, d, gws, gws_elems);
+}
+
 template <typename T>
 __global__ void k_add_inplace(T* __restrict__ dst, const T* __restrict__ src, size_t count) {
     for (size_t e = size_t(blockIdx.x) * blockDim.x + threadIdx.x; e < count; e += size_t(gridDim.x) * blockDim.x)
@@ -748,9 +827,9 @@ int run_impl(coru_ctx* c, const Request<T>& r, size_t extra_arena_off) {
         // summed over ranks; Q2, c2_prev and so the pinv are replicated (identical bytes).
         const bool p = c->prof;
         c->prof = false;
-        int rc = gemm<T>(c, Op::T, w.q1, dp, w.b1, dp, w.y1, dp, d, R, d, w.gws, w.gws_elems);
+        int rc = gemm_tn_core<T>(c, w.q1, dp, w.b1, dp, R, d, w.y1, dp, w.tnp, w.gws, w.gws_elems);
         if (rc == CORU_OK) rc = allreduce<T>(c, w.y1, size_t(d) * dp);
-        if (rc == CORU_OK) rc = gemm<T>(c, Op::T, w.q2, dp, w.b2prev, dp, w.y2, dp, d, N, d, w.gws, w.gws_elems);
+        if (rc == CORU_OK) rc = gemm_tn_core<T>(c, w.q2, dp, w.b2prev, dp, N, d, w.y2, dp, w.tnp, w.gws, w.gws_elems);
         if (rc == CORU_OK) {
             const cudaError_t e = pinv_square<T>(w.y2, dp, d, w.pinv, dp, w.pws, nullptr, c->max_smem, st);
             if (e != cudaSuccess) rc = fail(CORU_ECUDA, std::string("pinv_square: ") + cudaGetErrorString(e));
@@ -770,7 +849,7 @@ int run_impl(coru_ctx* c, const Request<T>& r, size_t extra_arena_off) {
             CORU_TRY(gemm<T>(c, r.op_a(), r.A, r.lda, w.q2, dp, W, dp, R, N, d, w.gws, w.gws_elems));
         const bool p = c->prof;  // Q1^T·W is m x d x d, not an A-pass
         c->prof = false;
-        const int rc = gemm<T>(c, Op::T, w.q1, dp, W, dp, w.m, dp, d, R, d, w.gws, w.gws_elems);
+        const int rc = gemm_tn_core<T>(c, w.q1, dp, W, dp, R, d, w.m, dp, w.tnp, w.gws, w.gws_elems);
         c->prof = p;
         CORU_TRY(rc);
         CORU_TRY(allreduce<T>(c, w.m, size_t(d) * dp));
