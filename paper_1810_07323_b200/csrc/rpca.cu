@@ -25,10 +25,13 @@ __device__ __forceinline__ double block_sum(double v, double* red) {
     return s;
 }
 
-// Each CTA walks tiles blockIdx.x, blockIdx.x + gridDim.x, ... (fixed order). Thread (ty, tx) of the
-// 16 x 16 layout owns rows ty + 16·i and columns tx + 16·j of the tile: a half-warp covers 128
-// contiguous bytes of a row of M / Y / S / X. The tile's M and Y are requested with cp.async into
-// shared memory before the k-loop, so their DRAM latency hides under the lift's FMAs (2 CTAs/SM).
+// Each CTA walks tiles blockIdx.x, blockIdx.x + gridDim.x, ... (fixed order). The lift L = Tp·V^T of
+// a 64 x 64 tile runs on the FP64 tensor cores (DMMA m16n8k8): warp (wm, wn) of the 4 x 2 layout
+// owns rows 16·wm.. and columns 32·wn.. (four 16 x 8 accumulators). Tp / V chunks (64 x 32) are
+// loaded into registers one chunk (and one tile) ahead of the MMAs and staged in shared memory with
+// a 36-double row stride (conflict-free fragment loads). Two CTAs per SM.
+constexpr int kLdT = kKc + 4;   // sT / sV row stride (doubles)
+constexpr int kLdM = kTile + 2; // sM / sY row stride (doubles; keeps 16-byte cp.async alignment)
 template <bool VEC>
 __global__ void __launch_bounds__(kThreads, 2) k_rpca_lift_update(const double* __restrict__ Tp, int64_t ldt,
                                                                   const double* __restrict__ Vb, int64_t ldv, int d,
@@ -39,16 +42,16 @@ __global__ void __launch_bounds__(kThreads, 2) k_rpca_lift_update(const double* 
                                                                   double* __restrict__ L, int64_t ldl, RpcaStep p,
                                                                   int lift_only, double* __restrict__ parts) {
     extern __shared__ __align__(16) double smem[];
-    double(*sT)[kKc + 1] = reinterpret_cast<double(*)[kKc + 1]>(smem);
-    double(*sV)[kKc + 1] = reinterpret_cast<double(*)[kKc + 1]>(smem + kTile * (kKc + 1));
-    double* sM = smem + 2 * kTile * (kKc + 1);  // kTile x kTile, 16-byte aligned (2·64·33 is even)
-    double* sY = sM + kTile * kTile;
+    double* sT = smem;                    // kTile x kLdT
+    double* sV = sT + kTile * kLdT;       // kTile x kLdT
+    double* sMY = sV + kTile * kLdT;      // [M, Y][kTile x kLdM] (16-byte aligned)
     __shared__ double red[kThreads / 32];
-    const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int g = lane >> 2, t4 = lane & 3;
+    const int wm = warp & 3, wn = warp >> 2;
     const int64_t tiles_n = (n + kTile - 1) / kTile;
     const int64_t tiles = ((m + kTile - 1) / kTile) * tiles_n;
     double part = 0.0;
-    // Tp / V chunks (kTile x kKc each) are loaded into registers one chunk ahead of the FMAs
     constexpr int kPer = kTile * kKc / kThreads;
     double pT[kPer], pV[kPer];
     auto load_chunk = [&](int64_t tt, int k0) {
@@ -62,59 +65,66 @@ __global__ void __launch_bounds__(kThreads, 2) k_rpca_lift_update(const double* 
             pV[q] = (kc && tj0 + r < n) ? __ldg(Vb + (tj0 + r) * ldv + k0 + c) : 0.0;
         }
     };
+    // M and Y of a tile are requested with cp.async at the start of the tile, so their DRAM latency
+    // hides under the MMAs (one buffer: two CTAs per SM beat one CTA with a double buffer).
+    auto prefetch_my = [&](int64_t tt, int buf) {
+        const int64_t ti0 = (tt / tiles_n) * kTile, tj0 = (tt % tiles_n) * kTile;
+        double* sM = sMY + buf * 2 * kTile * kLdM;
+        double* sY = sM + kTile * kLdM;
+        if constexpr (VEC) {
+            for (int e = threadIdx.x; e < kTile * kTile / 2; e += kThreads) {
+                const int r = e / (kTile / 2), c = 2 * (e % (kTile / 2));
+                const int64_t gi = ti0 + r, gj = tj0 + c;
+                const bool ok = gi < m && gj < n;  // n even when VEC: a pair is all-in or all-out
+                const int64_t gi_c = ok ? gi : 0, gj_c = ok ? gj : 0;
+                cp_async_zfill<16>(sM + r * kLdM + c, M + gi_c * ldm + gj_c, ok ? 16 : 0);
+                cp_async_zfill<16>(sY + r * kLdM + c, Y + gi_c * ldy + gj_c, ok ? 16 : 0);
+            }
+        } else {
+            for (int e = threadIdx.x; e < kTile * kTile; e += kThreads) {
+                const int r = e / kTile, c = e % kTile;
+                const int64_t gi = ti0 + r, gj = tj0 + c;
+                const bool ok = gi < m && gj < n;
+                const int64_t gi_c = ok ? gi : 0, gj_c = ok ? gj : 0;
+                cp_async_zfill<8>(sM + r * kLdM + c, M + gi_c * ldm + gj_c, ok ? 8 : 0);
+                cp_async_zfill<8>(sY + r * kLdM + c, Y + gi_c * ldy + gj_c, ok ? 8 : 0);
+            }
+        }
+        asm volatile("cp.async.commit_group;\n" ::);
+    };
     for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
         const int64_t i0 = (t / tiles_n) * kTile, j0 = (t % tiles_n) * kTile;
-        if (!lift_only) {
-            if constexpr (VEC) {
-                for (int e = threadIdx.x; e < kTile * kTile / 2; e += kThreads) {
-                    const int r = e / (kTile / 2), c = 2 * (e % (kTile / 2));
-                    const int64_t gi = i0 + r, gj = j0 + c;
-                    const bool ok = gi < m && gj < n;  // n even when VEC: a pair is all-in or all-out
-                    const int64_t gi_c = ok ? gi : 0, gj_c = ok ? gj : 0;
-                    cp_async_zfill<16>(sM + r * kTile + c, M + gi_c * ldm + gj_c, ok ? 16 : 0);
-                    cp_async_zfill<16>(sY + r * kTile + c, Y + gi_c * ldy + gj_c, ok ? 16 : 0);
-                }
-            } else {
-                for (int e = threadIdx.x; e < kTile * kTile; e += kThreads) {
-                    const int r = e / kTile, c = e % kTile;
-                    const int64_t gi = i0 + r, gj = j0 + c;
-                    const bool ok = gi < m && gj < n;
-                    const int64_t gi_c = ok ? gi : 0, gj_c = ok ? gj : 0;
-                    cp_async_zfill<8>(sM + r * kTile + c, M + gi_c * ldm + gj_c, ok ? 8 : 0);
-                    cp_async_zfill<8>(sY + r * kTile + c, Y + gi_c * ldy + gj_c, ok ? 8 : 0);
-                }
-            }
-            asm volatile("cp.async.commit_group;\n" ::);
-        }
+        const double* sM = sMY;
+        const double* sY = sM + kTile * kLdM;
+        if (!lift_only) prefetch_my(t, 0);
         double acc[4][4];
 #pragma unroll
-        for (int i = 0; i < 4; ++i)
+        for (int nb = 0; nb < 4; ++nb)
 #pragma unroll
-            for (int j = 0; j < 4; ++j) acc[i][j] = 0.0;
-        if (t == int64_t(blockIdx.x)) load_chunk(t, 0);  // later tiles: issued before the previous epilogue
+            for (int u = 0; u < 4; ++u) acc[nb][u] = 0.0;
+        if (t == int64_t(blockIdx.x)) load_chunk(t, 0);  // later tiles: issued under the previous MMAs
         for (int k0 = 0; k0 < d; k0 += kKc) {
-            __syncthreads();  // the previous chunk's FMAs are done with sT / sV
+            __syncthreads();  // the previous chunk's MMAs are done with sT / sV
 #pragma unroll
             for (int q = 0; q < kPer; ++q) {
                 const int e = threadIdx.x + q * kThreads;
-                sT[e / kKc][e % kKc] = pT[q];
-                sV[e / kKc][e % kKc] = pV[q];
+                sT[(e / kKc) * kLdT + e % kKc] = pT[q];
+                sV[(e / kKc) * kLdT + e % kKc] = pV[q];
             }
             __syncthreads();
-            // next chunk of this tile, or chunk 0 of the next tile: in flight under this chunk's FMAs
             if (k0 + kKc < d) load_chunk(t, k0 + kKc);
             else if (t + gridDim.x < tiles) load_chunk(t + gridDim.x, 0);
-            const int kn = min(kKc, d - k0);
-            for (int kk = 0; kk < kn; ++kk) {
-                double a[4], b[4];
+            const int ksteps = (min(kKc, d - k0) + 7) / 8;  // zero-padded columns past d add nothing
+            for (int ks = 0; ks < ksteps; ++ks) {
+                const int kb = ks * 8;
+                const double* ta = sT + (wm * 16 + g) * kLdT + kb + t4;
+                const double a[4] = {ta[0], ta[8 * kLdT], ta[4], ta[8 * kLdT + 4]};
 #pragma unroll
-                for (int i = 0; i < 4; ++i) a[i] = sT[ty + 16 * i][kk];
-#pragma unroll
-                for (int j = 0; j < 4; ++j) b[j] = sV[tx + 16 * j][kk];
-#pragma unroll
-                for (int i = 0; i < 4; ++i)
-#pragma unroll
-                    for (int j = 0; j < 4; ++j) acc[i][j] = fma(a[i], b[j], acc[i][j]);
+                for (int nb = 0; nb < 4; ++nb) {
+                    const double* vb = sV + (wn * 32 + nb * 8 + g) * kLdT + kb + t4;
+                    const double b[2] = {vb[0], vb[4]};
+                    dmma_16x8x8(acc[nb], a, b);
+                }
             }
         }
         if (!lift_only) {
@@ -122,22 +132,20 @@ __global__ void __launch_bounds__(kThreads, 2) k_rpca_lift_update(const double* 
             __syncthreads();
         }
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
-            const int li = ty + 16 * i;
-            const int64_t gi = i0 + li;
-            if (gi >= m) continue;
+        for (int nb = 0; nb < 4; ++nb) {
 #pragma unroll
-            for (int j = 0; j < 4; ++j) {
-                const int lj = tx + 16 * j;
-                const int64_t gj = j0 + lj;
-                if (gj >= n) continue;
-                const double l = acc[i][j];
+            for (int u = 0; u < 4; ++u) {
+                const int li = wm * 16 + g + 8 * (u >> 1);
+                const int lj = wn * 32 + nb * 8 + 2 * t4 + (u & 1);
+                const int64_t gi = i0 + li, gj = j0 + lj;
+                if (gi >= m || gj >= n) continue;
+                const double l = acc[nb][u];
                 if (lift_only) {
                     L[gi * ldl + gj] = l;
                     continue;
                 }
-                const double mv = sM[li * kTile + lj];
-                const double yv = sY[li * kTile + lj];
+                const double mv = sM[li * kLdM + lj];
+                const double yv = sY[li * kLdM + lj];
                 const double ml = __dsub_rn(mv, l);                        // m - l        (rpca.hpp:143)
                 const double w = __dadd_rn(ml, __dmul_rn(yv, p.inv_mu));   // += y·inv_mu  (:144)
                 const double mag = __dsub_rn(fabs(w), p.thresh);           // shrink       (:17-26, :145)
@@ -158,7 +166,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_rpca_lift_update(const double* 
     }
 }
 
-constexpr size_t kUpdSmem = size_t(2 * kTile * (kKc + 1) + 2 * kTile * kTile) * sizeof(double);
+constexpr size_t kUpdSmem = size_t(2 * kTile * kLdT + 2 * kTile * kLdM) * sizeof(double);
 
 __global__ void __launch_bounds__(kThreads) k_sumsq(const double* __restrict__ A, int64_t lda, int64_t m, int64_t n,
                                                     double* __restrict__ parts) {
@@ -221,7 +229,7 @@ __global__ void __launch_bounds__(kThreads) k_count_nonzero(const double* __rest
 
 int rpca_parts(int64_t m, int64_t n, int sms) {
     const int64_t tiles = ((m + kTile - 1) / kTile) * ((n + kTile - 1) / kTile);
-    return int(std::max<int64_t>(1, std::min<int64_t>(tiles, int64_t(sms) * 2)));
+    return int(std::max<int64_t>(1, std::min<int64_t>(tiles, int64_t(sms) * 2)));  // two CTAs per SM
 }
 
 cudaError_t rpca_lift_update(const double* Tp, int64_t ldt, const double* Vb, int64_t ldv, int d, int64_t m,
