@@ -903,6 +903,9 @@ template <typename T>
 cudaError_t qrcp(const T* M, int ldm, int d, T* Q, int ldq, T* Tout, int ldt, int64_t* perm, T* scratch,
                  int max_smem, cudaStream_t st) {
     if (d <= 32) return launch_qrcp_reg<T, 1, 2, 16>(M, ldm, d, Q, ldq, Tout, ldt, perm, st);
+    static const int nw = getenv("CORU_QRCP_NW") ? atoi(getenv("CORU_QRCP_NW")) : 16;  // tooling: warps x columns
+    if (d <= 64 && nw == 32) return launch_qrcp_reg<T, 2, 2, 32>(M, ldm, d, Q, ldq, Tout, ldt, perm, st);
+    if (d <= 64 && nw == 8) return launch_qrcp_reg<T, 2, 8, 8>(M, ldm, d, Q, ldq, Tout, ldt, perm, st);
     if (d <= 64) return launch_qrcp_reg<T, 2, 4, 16>(M, ldm, d, Q, ldq, Tout, ldt, perm, st);
     if (d <= 128) return launch_qrcp_reg<T, 4, 8, 16>(M, ldm, d, Q, ldq, Tout, ldt, perm, st);
     if (!getenv("CORU_QRCP_CTA")) {  // tooling switch: the one-CTA kernel below
