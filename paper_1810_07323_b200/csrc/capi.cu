@@ -610,22 +610,36 @@ __global__ void __launch_bounds__(256) k_tn_partial(const T* __restrict__ Q, int
             if (i < d && j < d) out[i * d + j] = acc[u][v];
         }
 }
+// 32 outputs per CTA (one per lane); the 8 warps sum contiguous eighths of the partials, then the
+// eight warp sums are added in warp order: a fixed order, so the result is deterministic.
 template <typename T>
-__global__ void k_tn_reduce(const T* __restrict__ part, int nblk, int d, T* __restrict__ C, int64_t ldc) {
-    for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < d * d; e += gridDim.x * blockDim.x) {
-        T s = part[e];
-        for (int b = 1; b < nblk; ++b) s += part[int64_t(b) * d * d + e];  // fixed order
-        C[int64_t(e / d) * ldc + e % d] = s;
+__global__ void __launch_bounds__(256) k_tn_reduce(const T* __restrict__ part, int nblk, int d, T* __restrict__ C,
+                                                   int64_t ldc) {
+    __shared__ T ws[8][32];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int e = blockIdx.x * 32 + lane;
+    const int per = (nblk + 7) / 8, b0 = warp * per, b1 = min(nblk, b0 + per);
+    T s = T(0);
+    if (e < d * d) {
+#pragma unroll 4
+        for (int b = b0; b < b1; ++b) s += part[int64_t(b) * d * d + e];
+    }
+    ws[warp][lane] = s;
+    __syncthreads();
+    if (warp == 0 && e < d * d) {
+        T t = ws[0][lane];
+        for (int w = 1; w < 8; ++w) t += ws[w][lane];
+        C[int64_t(e / d) * ldc + e % d] = t;
     }
 }
 template <typename T>
 int tn_small(coru_ctx* c, const T* Q, int64_t ldq, const T* W, int64_t ldw, int64_t m, int d, T* C, int64_t ldc,
              T* part) {
-    const int64_t want = (m + 63) / 64;
+    const int64_t want = (m + kTnRows - 1) / kTnRows;  // one staged chunk per CTA (C2: 125 CTAs)
     const int nblk = int(std::max<int64_t>(1, std::min<int64_t>(want, kTnMaxBlocks)));
     const int64_t rpb = (m + nblk - 1) / nblk;
     k_tn_partial<T><<<nblk, 256, 0, c->stream>>>(Q, ldq, W, ldw, m, d, rpb, part);
-    k_tn_reduce<T><<<(d * d + 255) / 256, 256, 0, c->stream>>>(part, nblk, d, C, ldc);
+    k_tn_reduce<T><<<(d * d + 31) / 32, 256, 0, c->stream>>>(part, nblk, d, C, ldc);
     g_launches += 2;
     CORU_CUDA(cudaGetLastError());
     return CORU_OK;
