@@ -417,6 +417,7 @@ struct Work {
     T *y1 = nullptr, *y2 = nullptr, *pinv = nullptr;  // approx-D core
     T *cbuf[2] = {nullptr, nullptr}, *b2n = nullptr, *part = nullptr;  // out-of-core chunk ring, next c2, partial
     T* tnp = nullptr;  // partials of the skinny Q^T·W core products (d <= 64)
+    T* wproj = nullptr;  // W = A·Q2 when it overlaps the Q1 tree (exact-D, single GPU, in-core)
     double* pws = nullptr;
     int64_t* perm = nullptr;
     int* flag = nullptr;
@@ -456,6 +457,9 @@ struct Work {
         r2 = cv.take<T>(int64_t(d) * d);
         m = cv.take<T>(int64_t(d) * dp);
         if (d <= 64) tnp = cv.take<T>(int64_t(kTnMaxBlocks) * d * d);
+        if (r.mode == Mode::Full && r.variant != CORU_D_APPROX && c->world == 1 && !r.a_host &&
+            getenv("CORU_EARLY_JOIN") == nullptr)
+            wproj = cv.take<T>(R * dp);
         qm = cv.take<T>(int64_t(dp) * dp);
         tm = cv.take<T>(int64_t(d) * d);
         qrcp_scr = cv.take<T>(qrcp_scratch_elems(d));
@@ -815,7 +819,10 @@ int run_impl(coru_ctx* c, const Request<T>& r, size_t extra_arena_off) {
         CORU_TRY(w.ts2.form_q(nullptr, w.q2, dp, st));
     }
     CORU_CUDA(cudaEventRecord(c->ev_join, c->aux));
-    CORU_CUDA(cudaStreamWaitEvent(st, c->ev_join, 0));
+    // exact-D, single GPU: the projection pass W = A·Q2 needs only Q2 (main stream), so it starts
+    // while the Q1 tree may still be finishing on the aux stream; the join moves after it.
+    const bool late_join = w.wproj != nullptr;  // W gets its own buffer: the Q1 tree may still read c1
+    if (!late_join) CORU_CUDA(cudaStreamWaitEvent(st, c->ev_join, 0));
 
     if (r.mode == Mode::Sketch) {
         CORU_CUDA(copy_block<T>(w.q1, dp, r.q1, r.ldq1, R, d, st));
@@ -854,13 +861,14 @@ int run_impl(coru_ctx* c, const Request<T>& r, size_t extra_arena_off) {
         CORU_TRY(rc);
     } else {
         // D = (Q1^T a) q2 (corutv.hpp:90) as Q1^T (A'·Q2): W = A'·Q2 reuses the B1 buffer.
-        T* W = w.b1;
+        T* W = w.wproj ? w.wproj : w.b1;
         if (r.a_host)
             CORU_TRY(stream_a([&](int64_t, int64_t r0, int64_t rows, const T* Ai) -> int {
                 return gemm<T>(c, Op::N, Ai, N, w.q2, dp, W + r0 * dp, dp, rows, N, d, w.gws, w.gws_elems);
             }));
         else
             CORU_TRY(gemm<T>(c, r.op_a(), r.A, r.lda, w.q2, dp, W, dp, R, N, d, w.gws, w.gws_elems));
+        if (late_join) CORU_CUDA(cudaStreamWaitEvent(st, c->ev_join, 0));  // Q1 (and the flag) from here on
         const bool p = c->prof;  // Q1^T·W is m x d x d, not an A-pass
         c->prof = false;
         const int rc = gemm_tn_core<T>(c, w.q1, dp, W, dp, R, d, w.m, dp, w.tnp, w.gws, w.gws_elems);
