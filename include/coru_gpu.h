@@ -132,7 +132,7 @@ int coru_corutv_f32(coru_ctx* ctx, const float* A, int64_t m, int64_t n, int64_t
                     int* conditioning_warning);
 
 /* Out-of-core corutv (§8 f4; the paper's pass model for externally stored data):
- * A stays in HOST memory (row-major m x n, lda >= n, m >= n) and is streamed to the GPU in row
+ * A stays in HOST memory (row-major m x n, lda >= n) and is streamed to the GPU in row
  * chunks of chunk_rows rows (<= 0: ~512 MB per chunk) through a two-buffer device ring, the H2D of
  * chunk i+1 overlapping the GEMMs of chunk i. Each power round reads A once (c1 rows = A_i·c2 and
  * the partial A_i^T·c1_i from the same chunk, summed in chunk order), the exact-D projection once
@@ -140,8 +140,9 @@ int coru_corutv_f32(coru_ctx* ctx, const float* A, int64_t m, int64_t n, int64_t
  * sketches (m x ell, cols x ell) and two chunks live on the device, so A may exceed HBM. Pageable
  * host memory is page-locked for the duration of the call. Outputs as coru_corutv_*_dev (device
  * U, T, V; host pointers are also accepted: the call then copies the factors back). rows < cols
- * returns CORU_ENOTSUP. Deterministic; differs from the in-core path at rounding level
- * (chunk-ordered partial sums). */
+ * runs the ULV orientation (lower = 1, corutv.hpp:82-87) with two reads of A per power round (the
+ * A^T-side partial sums must complete first). Deterministic; differs from the in-core path at
+ * rounding level (chunk-ordered partial sums). */
 int coru_corutv_f64_ooc(coru_ctx* ctx, const double* A, int64_t m, int64_t n, int64_t lda, int64_t ell, int q,
                         int variant, uint64_t seed, uint64_t stream, int64_t chunk_rows, coru_utv* out);
 int coru_corutv_f32_ooc(coru_ctx* ctx, const float* A, int64_t m, int64_t n, int64_t lda, int64_t ell, int q,
@@ -152,7 +153,7 @@ int coru_corutv_f32_ooc(coru_ctx* ctx, const float* A, int64_t m, int64_t n, int
  * and the exact file size (CORU_EIO with the reference's messages). The file entry memory-maps the
  * file and runs the out-of-core corutv on it directly (A never materialised in host RAM beyond the
  * page cache); non-finite entries return CORU_EIO like read_matrix_bin. U, T, V: device (or host)
- * buffers for rows x ell, ell x ell, cols x ell (rows >= cols). */
+ * buffers for rows x ell, ell x ell, cols x ell. */
 int coru_read_matrix_bin_header(const char* path, int64_t* rows, int64_t* cols);
 int coru_corutv_f64_file(coru_ctx* ctx, const char* path, int64_t ell, int q, int variant, uint64_t seed,
                          uint64_t stream, int64_t chunk_rows, coru_utv* out);

@@ -214,7 +214,7 @@ inline RpcaResult alm_rpca(const Matrix& m, const RpcaConfig& config, RngSeed se
     return r;
 }
 
-// Out-of-core corutv (§8 f4): A streamed from host memory in row chunks (rows >= cols); the same
+// Out-of-core corutv (§8 f4): A streamed from host memory in row chunks; the same
 // UtvApprox as corutv. chunk_rows = 0: ~512 MB chunks.
 inline UtvApprox corutv_streamed(const Matrix& a, std::size_t ell, int q, DVariant variant, RngSeed seed,
                                  std::int64_t chunk_rows = 0) {
@@ -230,6 +230,7 @@ inline UtvApprox corutv_streamed(const Matrix& a, std::size_t ell, int q, DVaria
                                              variant == DVariant::exact ? CORU_D_EXACT : CORU_D_APPROX, seed.seed,
                                              seed.stream, chunk_rows, &out));
     f.conditioning_warning = out.conditioning_warning != 0;
+    f.lower = out.lower != 0;
     return f;
 }
 
@@ -246,6 +247,7 @@ inline UtvApprox corutv_file(const std::string& path, std::size_t ell, int q, DV
                                               variant == DVariant::exact ? CORU_D_EXACT : CORU_D_APPROX, seed.seed,
                                               seed.stream, chunk_rows, &out));
     f.conditioning_warning = out.conditioning_warning != 0;
+    f.lower = out.lower != 0;
     return f;
 }
 

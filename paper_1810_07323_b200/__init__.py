@@ -689,7 +689,7 @@ def alm_rpca(m, config: RpcaConfig = RpcaConfig(), seed: RngSeed = RngSeed(),
 
 def corutv_ooc(a: np.ndarray, ell: int, q: int, variant: DVariant = DVariant.exact, seed: RngSeed = RngSeed(),
                chunk_rows: int = 0, ctx: Optional[Context] = None) -> UtvApprox:
-    """Out-of-core corutv (§8 f4): ``a`` is a host numpy array (rows >= cols) streamed to the GPU in row chunks
+    """Out-of-core corutv (§8 f4): ``a`` is a host numpy array streamed to the GPU in row chunks
     (coru_corutv_{f64,f32}_ooc); U, T, V come back as numpy arrays."""
     import torch
     ctx = ctx or default_context()
@@ -746,5 +746,5 @@ def corutv_file(path: str, ell: int, q: int, variant: DVariant = DVariant.exact,
     _check(ctx.lib.coru_corutv_f64_file(ctx.h, path.encode(), ell, q, int(variant), seed.seed, seed.stream, chunk_rows,
                                         C.byref(out)))
     torch.cuda.synchronize(dev)
-    return UtvApprox(u.cpu().numpy(), t.cpu().numpy(), v.cpu().numpy(), ell, q, variant, seed, False,
+    return UtvApprox(u.cpu().numpy(), t.cpu().numpy(), v.cpu().numpy(), ell, q, variant, seed, bool(out.lower),
                      bool(out.conditioning_warning), perm)

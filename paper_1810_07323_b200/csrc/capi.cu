@@ -435,13 +435,15 @@ struct Work {
                               gemm_ws<T>(Op::T, d, R, d, sms), gemm_ws<T>(Op::N, R, d, d, sms),
                               gemm_ws<T>(Op::T, d, N, d, sms), gemm_ws<T>(Op::N, d, d, d, sms)});
         if (r.a_host) {
-            const int64_t cr = std::min(r.ooc_rows, R), last = R - (R - 1) / cr * cr;
+            // host rows of A: rows of A' (URV) or its columns (ULV, A' = A^T); row length = the other side
+            const int64_t HR = r.trans ? N : R, HL = r.trans ? R : N;
+            const int64_t cr = std::min(r.ooc_rows, HR), last = HR - (HR - 1) / cr * cr;
             for (int64_t rows : {cr, last})
-                gws_elems = std::max({gws_elems, gemm_ws<T>(Op::N, rows, N, d, sms), gemm_ws<T>(Op::T, N, rows, d, sms)});
-            cbuf[0] = cv.take<T>(cr * N);
-            cbuf[1] = cv.take<T>(cr * N);
+                gws_elems = std::max({gws_elems, gemm_ws<T>(Op::N, rows, HL, d, sms), gemm_ws<T>(Op::T, HL, rows, d, sms)});
+            cbuf[0] = cv.take<T>(cr * HL);
+            cbuf[1] = cv.take<T>(cr * HL);
             b2n = cv.take<T>(N * dp);
-            part = cv.take<T>(N * dp);
+            part = cv.take<T>(HL * dp);
         }
         gws = cv.take<T>(gws_elems);
         // CholeskyQR2 for wide sketches, except for Q1 when sharded (its tree's top level is cross-rank)
@@ -717,17 +719,18 @@ int run_impl(coru_ctx* c, const Request<T>& r, size_t extra_arena_off) {
     if (r.a_host) {
         for (auto& e : ooc_ev) CORU_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
         CORU_CUDA(cudaMemsetAsync(w.b2n, 0, size_t(N) * dp * sizeof(T), st));  // padding columns stay zero
-        CORU_CUDA(cudaMemsetAsync(w.part, 0, size_t(N) * dp * sizeof(T), st));
+        CORU_CUDA(cudaMemsetAsync(w.part, 0, size_t(r.trans ? R : N) * dp * sizeof(T), st));
     }
+    const int64_t HR = r.trans ? N : R, HL = r.trans ? R : N;  // host rows of A, their length
     auto stream_a = [&](auto&& on_chunk) -> int {
-        const int64_t cr = std::min(r.ooc_rows, R);
-        const int64_t nch = (R + cr - 1) / cr;
+        const int64_t cr = std::min(r.ooc_rows, HR);
+        const int64_t nch = (HR + cr - 1) / cr;
         auto issue = [&](int64_t i) -> int {
-            const int64_t r0 = i * cr, rows = std::min(cr, R - r0);
+            const int64_t r0 = i * cr, rows = std::min(cr, HR - r0);
             const int b = int(i & 1);
             CORU_CUDA(cudaStreamWaitEvent(c->aux, ooc_ev[2 + b], 0));  // buffer b free again
-            CORU_CUDA(cudaMemcpy2DAsync(w.cbuf[b], size_t(N) * sizeof(T), r.a_host + r0 * r.lda,
-                                        size_t(r.lda) * sizeof(T), size_t(N) * sizeof(T), size_t(rows),
+            CORU_CUDA(cudaMemcpy2DAsync(w.cbuf[b], size_t(HL) * sizeof(T), r.a_host + r0 * r.lda,
+                                        size_t(r.lda) * sizeof(T), size_t(HL) * sizeof(T), size_t(rows),
                                         cudaMemcpyHostToDevice, c->aux));
             CORU_CUDA(cudaEventRecord(ooc_ev[b], c->aux));
             return CORU_OK;
@@ -739,7 +742,7 @@ int run_impl(coru_ctx* c, const Request<T>& r, size_t extra_arena_off) {
             if (i + 1 < nch) CORU_TRY(issue(i + 1));
             const int b = int(i & 1);
             CORU_CUDA(cudaStreamWaitEvent(st, ooc_ev[b], 0));
-            const int64_t r0 = i * cr, rows = std::min(cr, R - r0);
+            const int64_t r0 = i * cr, rows = std::min(cr, HR - r0);
             CORU_TRY(on_chunk(i, r0, rows, static_cast<const T*>(w.cbuf[b])));
             CORU_CUDA(cudaEventRecord(ooc_ev[2 + b], st));
         }
@@ -749,7 +752,36 @@ int run_impl(coru_ctx* c, const Request<T>& r, size_t extra_arena_off) {
         // Each power round reads A once: c1 rows of chunk i = A_i·c2, and the partial A_i^T·c1_i from
         // the same chunk, summed into the next c2 in chunk order (deterministic).
         CORU_CUDA(cudaMemsetAsync(w.flag + 1, 0, sizeof(int), st));
-        for (int i = 0; i <= r.q; ++i) {
+        // ULV (A' = A^T, host rows of A are columns of A'): c1 = A'·c2 = sum_i A_i^T c2_i needs the
+        // whole sum before c2' = A'^T c1 = [A_i c1]_i, so a round reads A twice (partials first).
+        for (int i = 0; i <= r.q && r.trans; ++i) {
+            CORU_TRY(stream_a([&](int64_t ch, int64_t r0, int64_t rows, const T* Ai) -> int {
+                if (i == 0) {
+                    CORU_CUDA(any_nonfinite_acc<T>(Ai, rows * HL, w.flag + 1, st));
+                    ++g_launches;
+                }
+                T* out = ch == 0 ? w.b1 : w.part;
+                CORU_TRY(gemm<T>(c, Op::T, Ai, HL, w.b2 + r0 * dp, dp, out, dp, R, rows, d, w.gws, w.gws_elems));
+                if (ch > 0) {
+                    CORU_CUDA(add_inplace<T>(w.b1, w.part, size_t(R) * dp, st));
+                    ++g_launches;
+                }
+                return CORU_OK;
+            }));
+            if (i == 0) {
+                int bad = 0;
+                CORU_CUDA(cudaMemcpyAsync(&bad, w.flag + 1, sizeof(int), cudaMemcpyDeviceToHost, st));
+                CORU_CUDA(cudaStreamSynchronize(st));
+                if (bad) return fail(CORU_EINVAL, "Matrix: non-finite entry");
+            }
+            if (i == r.q && w.b2prev)
+                CORU_CUDA(cudaMemcpyAsync(w.b2prev, w.b2, size_t(N) * dp * sizeof(T), cudaMemcpyDeviceToDevice, st));
+            CORU_TRY(stream_a([&](int64_t, int64_t r0, int64_t rows, const T* Ai) -> int {
+                return gemm<T>(c, Op::N, Ai, HL, w.b1, dp, w.b2n + r0 * dp, dp, rows, R, d, w.gws, w.gws_elems);
+            }));
+            std::swap(w.b2, w.b2n);
+        }
+        for (int i = 0; i <= r.q && !r.trans; ++i) {
             CORU_TRY(stream_a([&](int64_t ch, int64_t r0, int64_t rows, const T* Ai) -> int {
                 if (i == 0) {  // finiteness, as the Matrix constructor / read_matrix_bin (matrix.hpp:29-31)
                     CORU_CUDA(any_nonfinite_acc<T>(Ai, rows * N, w.flag + 1, st));
@@ -862,7 +894,17 @@ int run_impl(coru_ctx* c, const Request<T>& r, size_t extra_arena_off) {
     } else {
         // D = (Q1^T a) q2 (corutv.hpp:90) as Q1^T (A'·Q2): W = A'·Q2 reuses the B1 buffer.
         T* W = w.wproj ? w.wproj : w.b1;
-        if (r.a_host)
+        if (r.a_host && r.trans)  // W = A'·Q2 = sum_i A_i^T Q2_i, chunk-ordered partial sums
+            CORU_TRY(stream_a([&](int64_t ch, int64_t r0, int64_t rows, const T* Ai) -> int {
+                T* out = ch == 0 ? W : w.part;
+                CORU_TRY(gemm<T>(c, Op::T, Ai, HL, w.q2 + r0 * dp, dp, out, dp, R, rows, d, w.gws, w.gws_elems));
+                if (ch > 0) {
+                    CORU_CUDA(add_inplace<T>(W, w.part, size_t(R) * dp, st));
+                    ++g_launches;
+                }
+                return CORU_OK;
+            }));
+        else if (r.a_host)
             CORU_TRY(stream_a([&](int64_t, int64_t r0, int64_t rows, const T* Ai) -> int {
                 return gemm<T>(c, Op::N, Ai, N, w.q2, dp, W + r0 * dp, dp, rows, N, d, w.gws, w.gws_elems);
             }));
@@ -964,15 +1006,16 @@ int corutv_ooc(coru_ctx* c, const T* A, int64_t m, int64_t n, int64_t lda, int64
     if (!out || !A) return fail(CORU_EINVAL, "null argument");
     if (lda < n) return fail(CORU_EINVAL, "lda < n");
     if (c->world > 1) return fail(CORU_EINVAL, "out-of-core corutv is single-GPU");
-    if (m < n) return fail(CORU_ENOTSUP, "out-of-core corutv: rows < cols (ULV) is not provided");
     if (chunk_rows <= 0) chunk_rows = std::max<int64_t>(1, int64_t((size_t(512) << 20) / (size_t(n) * sizeof(T))));
     chunk_rows = std::min(chunk_rows, m);
+    const bool trans = m < n;  // corutv(a^T) then {v, t^T, u, lower = true} (corutv.hpp:82-87)
     Request<T> r;
     r.a_host = A;
     r.ooc_rows = chunk_rows;
     r.lda = lda;
-    r.rows = m;
-    r.cols = n;
+    r.trans = trans;
+    r.rows = trans ? n : m;
+    r.cols = trans ? m : n;
     r.d = int(ell);
     r.q = q;
     r.seed = seed;
@@ -980,13 +1023,14 @@ int corutv_ooc(coru_ctx* c, const T* A, int64_t m, int64_t n, int64_t lda, int64
     r.variant = variant;
     r.perm_host = out->perm;
     r.warn_host = &out->conditioning_warning;
-    r.u = static_cast<T*>(out->u);
-    r.ldu = out->ldu;
-    r.v = static_cast<T*>(out->v);
-    r.ldv = out->ldv;
+    r.u = static_cast<T*>(trans ? out->v : out->u);
+    r.ldu = trans ? out->ldv : out->ldu;
+    r.v = static_cast<T*>(trans ? out->u : out->v);
+    r.ldv = trans ? out->ldu : out->ldv;
     r.t = static_cast<T*>(out->t);
     r.ldt = out->ldt;
-    out->lower = 0;
+    r.t_transpose = trans;
+    out->lower = trans ? 1 : 0;
     // Host output buffers (the C++ drop-in passes coru::Matrix storage): run into device scratch
     // and copy back (U m x ell, T ell x ell, V n x ell with the caller's leading dimensions).
     auto is_host = [](const void* ptr) {
@@ -1004,11 +1048,13 @@ int corutv_ooc(coru_ctx* c, const T* A, int64_t m, int64_t n, int64_t lda, int64
             cudaGetLastError();
             return fail(CORU_ENOMEM, "cudaMalloc of the out-of-core output buffers failed");
         }
-        r.u = dev_out;
+        T* du = dev_out;                                          // U: m x ell
+        T* dv = dev_out + size_t(m) * ell + size_t(ell) * ell;    // V: n x ell
+        r.u = trans ? dv : du;
         r.ldu = ell;
         r.t = dev_out + size_t(m) * ell;
         r.ldt = ell;
-        r.v = dev_out + size_t(m) * ell + size_t(ell) * ell;
+        r.v = trans ? du : dv;
         r.ldv = ell;
     }
     bool registered = false;
@@ -1026,9 +1072,11 @@ int corutv_ooc(coru_ctx* c, const T* A, int64_t m, int64_t n, int64_t lda, int64
                 return cudaMemcpy2DAsync(dst, size_t(ldd) * sizeof(T), src, size_t(ell) * sizeof(T),
                                          size_t(ell) * sizeof(T), size_t(rows), cudaMemcpyDeviceToHost, c->stream);
             };
-            cudaError_t e = back(out->u, out->ldu, r.u, m);
+            const T* du = dev_out;
+            const T* dv = dev_out + size_t(m) * ell + size_t(ell) * ell;
+            cudaError_t e = back(out->u, out->ldu, du, m);
             if (e == cudaSuccess) e = back(out->t, out->ldt, r.t, ell);
-            if (e == cudaSuccess) e = back(out->v, out->ldv, r.v, n);
+            if (e == cudaSuccess) e = back(out->v, out->ldv, dv, n);
             if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
             if (e != cudaSuccess) rc = fail(CORU_ECUDA, std::string("output copy: ") + cudaGetErrorString(e));
         }

@@ -17,15 +17,15 @@ def _structure(f, d):
     assert orth_residual(f.u) <= 1e-12 * d and orth_residual(f.v) <= 1e-12 * d
 
 
-@pytest.mark.parametrize("case", [c for c in corutv_cases() if c["A"].shape[0] >= c["A"].shape[1]],
-                         ids=lambda c: c["name"])
+@pytest.mark.parametrize("case", corutv_cases(), ids=lambda c: c["name"])
 def test_ooc_reference_cases(ctx, case):
     import paper_1810_07323_b200 as cg
     a, ell, q = case["A"], case["ell"], case["q"]
     chunk = max(ell + 1, a.shape[0] // 5)  # several chunks, a ragged last one
     f = cg.corutv_ooc(a, ell, q, cg.DVariant.exact, cg.RngSeed(case["seed"], case["stream"]), chunk_rows=chunk, ctx=ctx)
-    assert not f.lower
-    _structure(f, ell)
+    assert f.lower == case["lower"]                                   # ULV for rows < cols (corutv.hpp:82-87)
+    assert np.all((np.triu(f.t, 1) if f.lower else np.tril(f.t, -1)) == 0.0)
+    assert orth_residual(f.u) <= 1e-12 * ell and orth_residual(f.v) <= 1e-12 * ell
     e_gpu = rel_recon_error(a, f.u, f.t, f.v)
     e_ref = rel_recon_error(a, case["U"], case["T"], case["V"])
     dg = np.abs(np.abs(np.diag(f.t)) - np.abs(np.diag(case["T"])))
@@ -116,8 +116,8 @@ def test_ooc_fp32(ctx):
 def test_ooc_errors(ctx):
     import paper_1810_07323_b200 as cg
     a = np.random.default_rng(0).standard_normal((50, 80))
-    with pytest.raises(NotImplementedError):
-        cg.corutv_ooc(a, 5, 0, ctx=ctx)                               # rows < cols
+    with pytest.raises(cg.CoruInvalidArgument):
+        cg.corutv_ooc(a, 50, 0, ctx=ctx)                              # ell >= min(rows, cols), ULV side
     with pytest.raises(cg.CoruInvalidArgument):
         cg.corutv_ooc(np.ascontiguousarray(a.T), 50, 0, ctx=ctx)      # ell >= min(rows, cols)
     with pytest.raises(cg.CoruInvalidArgument):
@@ -149,3 +149,23 @@ def test_corutv_file_matches_memory(ctx, tmp_path):
         cg.corutv_file(p, c["ell"], 0, seed=seed, ctx=ctx)
     with pytest.raises(cg.CoruInvalidArgument):
         cg.corutv_ooc(bad, c["ell"], 0, seed=seed, ctx=ctx)
+
+
+@pytest.mark.parametrize("q", [0, 1])
+def test_ooc_ulv_matches_in_core(ctx, q):
+    """rows < cols out of core (two reads of A per round) vs the in-core ULV path."""
+    import paper_1810_07323_b200 as cg
+    rng = np.random.default_rng(9)
+    x, _ = np.linalg.qr(rng.standard_normal((700, 40)))
+    y, _ = np.linalg.qr(rng.standard_normal((2500, 40)))
+    a = (x * (0.8 ** np.arange(40))) @ y.T + 1e-6 * rng.standard_normal((700, 2500))
+    seed = cg.RngSeed(5, 2)
+    f_in = cg.corutv(a, 20, q, cg.DVariant.exact, seed, ctx=ctx)
+    f = cg.corutv_ooc(a, 20, q, cg.DVariant.exact, seed, chunk_rows=150, ctx=ctx)
+    assert f.lower and f_in.lower
+    assert np.all(np.triu(f.t, 1) == 0.0)
+    e_in, e_oo = rel_recon_error(a, f_in.u, f_in.t, f_in.v), rel_recon_error(a, f.u, f.t, f.v)
+    assert abs(e_in - e_oo) <= 1e-8 * e_in
+    assert np.max(np.abs(np.abs(np.diag(f.t)) - np.abs(np.diag(f_in.t)))) <= 1e-10
+    g = cg.corutv_ooc(a, 20, q, cg.DVariant.approx, seed, chunk_rows=150, ctx=ctx)
+    assert g.lower and rel_recon_error(a, g.u, g.t, g.v) <= 1.01 * e_in
