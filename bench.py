@@ -1,19 +1,28 @@
 """Benchmark of the CoR-UTV hot path (BASELINE.json metric: decompositions/s and A-pass TFLOP/s vs roofline).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C2q1] [--impl ours|reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C3] [--impl ours|reference]
 
-One "step" is one coru::corutv-equivalent decomposition (corutv.hpp:79-100) of the synthetic
-BASELINE config (default C2: fp64 4000x4000, sigma_i = i^-2, d = 60, q = 1; BASELINE.json
-configs[1], the config the metric is quoted on that fits one GPU). With N > 1 (torchrun) A is
-row-block sharded over the ranks and one decomposition spans all of them (strong scaling).
+One "step" is one coru::corutv-equivalent decomposition (corutv.hpp:79-100) of a synthetic
+BASELINE config. Default: C3 (fp64 200000x2000, sigma_i = 10^(-i/20), d = 110, q = 1) — the
+largest fp64 config the metric is quoted on at 1/2/4/8 GPUs whose reference arm fits the driver's
+window; --config C1 / C2q1 / C2q2 / C4 / C5 select the others. With N > 1 A is row-block sharded
+over N ranks and one decomposition spans all of them (strong scaling); `--gpus N` without torchrun
+re-launches itself under torch.distributed.run.
+
+A is generated ONCE per arm by tests/workloads.make_device (seeded torch CUDA generator) and both
+arms decompose the identical bytes (its SHA-256 is in `config`). Φ is the reference's
+gaussian() bit for bit (host-exact mode, the library default), generated inside every timed step.
 
 Our arm prints one JSON line with: value (decomps/s, A resident in HBM, device-timed with CUDA
-events, max over ranks), e2e (same metric through the host-buffer C-ABI with the H2D of A and the
-D2H of U,T,V inside the timed region), roofline of the dominant kernel (the FP64 A-pass GEMM,
+events, max over ranks), e2e (same metric through the host-buffer C-ABI coru_corutv_f64 with a
+PAGEABLE A — the drop-in caller's std::vector storage — H2D of A and D2H of U,T,V inside the
+timed region; e2e_pinned: the same with page-locked A), roofline of the dominant kernel (the A-pass,
 timed live with CUDA events on its launch stream inside the library), cpu_baseline (the compiled
-reference on one host core, rank 0 at N=1), clocks sampled during the timed region, and
-gpu_launches. `--impl reference` times the unmodified reference (oracle/_ref/libcoru_ref.so,
-compiled from the reference headers) on the host's cores with its own trial-level fan-out.
+reference, rank 0 at N=1), clocks sampled during the timed region, and gpu_launches.
+`--impl reference` times the reference itself (oracle/_ref/libcoru_ref.so, compiled from the
+reference headers: ref_corutv_mt = coru::corutv's exact-D steps with its products spread over all
+host cores in the reference's per-entry summation order, bit-identical) — one decomposition per
+step on the same A bytes.
 """
 from __future__ import annotations
 
@@ -31,7 +40,7 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 sys.path.insert(0, os.path.join(ROOT, "tests"))
 
-from workloads import CONFIGS, make_device, make_host  # noqa: E402
+from workloads import CONFIGS, make_device, make_host, sha256  # noqa: E402
 
 METRIC = "CoR-UTV decomps/sec & A-pass TFLOPS / HBM GB/s vs roofline at 1/2/4/8 B200"
 UNIT = "decomps/s"
@@ -186,30 +195,72 @@ def ncu_traffic(config_name):
     return None
 
 
-# ---- CPU baselines ----------------------------------------------------------------------------------
-def cpu_baseline_sample(cfg, a_host, variant=0):
-    """The compiled reference (oracle/_ref) on ONE host core: bounded sample of whole decompositions."""
-    from oracle import Reference, has_reference, Oracle
-    if has_reference():
-        ref, kind = Reference(), "reference"
-        run = lambda s: ref.corutv(a_host, cfg.d, cfg.q, variant, 42, s)  # noqa: E731
-    else:
-        ora, kind = Oracle(), "port"
-        run = lambda s: ora.corutv(a_host, cfg.d, cfg.q, variant, 42, s, threads=1)  # noqa: E731
+# ---- workload ---------------------------------------------------------------------------------------
+def make_workload(cfg, want_host=True, device=None):
+    """A generated once (seeded torch CUDA generator, tests/workloads.py) -> (device tensor or None,
+    host numpy array or None, sha256 of the host bytes). Without a GPU (reference arm on a CPU-only
+    host) the numpy generator stands in and the SHA says which bytes were used."""
+    import torch
+    if torch.cuda.is_available():
+        a_dev = make_device(cfg.name, device=device or torch.device("cuda", 0))
+        torch.cuda.synchronize()
+        a_host = a_dev.cpu().numpy() if want_host else None
+        return a_dev, a_host, (sha256(a_host) if a_host is not None else None), "workloads.make_device (torch CUDA)"
+    a_host = make_host(cfg.name)
+    return None, a_host, sha256(a_host), "workloads.make_host (numpy; no GPU on this host)"
+
+
+def config_block(cfg, args, a_sha, gen):
+    """Identical in both arms (the driver compares them)."""
+    return {"workload": f"{cfg.name}: {cfg.dtype} {cfg.m}x{cfg.n}, {cfg.desc}, d={cfg.d}, q={cfg.q}, k={cfg.k}",
+            "m": cfg.m, "n": cfg.n, "d": cfg.d, "q": cfg.q, "k": cfg.k, "seed": "RngSeed{42, step}",
+            "variant": args.variant, "passes_over_A": 2 * cfg.q + (3 if args.variant == "exact" else 2),
+            "parallelism": f"row-sharded x{args.gpus}" if args.gpus > 1 else "single GPU",
+            "phi": "host-exact: coru::gaussian bit for bit (rng.hpp:86-112), generated inside every step",
+            "a_sha256": a_sha, "a_generator": gen,
+            "l2": ("GPU arm: 256 MB write between steps outside the per-step events (126 MB L2); "
+                   "reference arm: n/a (CPU)")}
+
+
+# ---- CPU reference ------------------------------------------------------------------------------
+def reference_runner(cfg, a_host, variant_id):
+    """One whole decomposition of the reference on all host cores, as a callable of the seed stream.
+
+    fp64 exact-D, m >= n: ref_corutv_mt (oracle/_ref: the reference headers compiled in place; its
+    gaussian / householder_qr / qrcp / flag are the reference's own serial functions, the A-products
+    run over all cores in the reference's per-entry order — bit-identical to coru::corutv).
+    Otherwise coru::corutv itself (single thread) or, for fp32 (no fp32 reference exists), the
+    bit-exact-restatement oracle in fp32 on all cores."""
+    from oracle import Oracle, Reference, has_reference
+    threads = os.cpu_count() or 1
+    if cfg.dtype == "f64" and has_reference():
+        ref = Reference()
+        if variant_id == 0 and cfg.m >= cfg.n:
+            return (lambda s: ref.corutv(a_host, cfg.d, cfg.q, 0, 42, s, threads=threads)), threads, "reference", \
+                "ref_corutv_mt: the reference's corutv steps, products over all host cores (bit-identical)"
+        return (lambda s: ref.corutv(a_host, cfg.d, cfg.q, variant_id, 42, s)), 1, "reference", \
+            "coru::corutv, single thread"
+    ora = Oracle()
+    return (lambda s: ora.corutv(a_host, cfg.d, cfg.q, variant_id, 42, s, threads=threads)), threads, "port", \
+        "oracle/coru_oracle.c (bit-exact restatement; fp32 instantiation for the fp32 config) on all cores"
+
+
+def cpu_baseline_sample(cfg, a_host, variant_id, budget_s=12.0):
+    """Bounded sample of whole reference decompositions (>= 1, stop after ~budget_s)."""
+    run, cores, kind, what = reference_runner(cfg, a_host, variant_id)
     times = []
-    budget = 12.0
     t_all = time.perf_counter()
     s = 0
     while True:
         t0 = time.perf_counter()
-        run(s)
+        run(10_000 + s)
         times.append(time.perf_counter() - t0)
         s += 1
-        if time.perf_counter() - t_all > budget or s >= 5:
+        if time.perf_counter() - t_all > budget_s or s >= 5:
             break
     per = sum(times) / len(times)
-    return {"value": 1.0 / per, "unit": UNIT, "cores": 1, "kind": kind,
-            "sample": f"{len(times)} full {cfg.name} decompositions, single thread, s/decomp={per:.3f}",
+    return {"value": 1.0 / per, "unit": UNIT, "cores": cores, "kind": kind,
+            "sample": f"{len(times)} full {cfg.name} decomposition(s) on the same A, {what}, s/decomp={per:.3f}",
             "host_cores_total": os.cpu_count()}
 
 
@@ -217,45 +268,30 @@ def run_reference_arm(args, cfg):
     rank = env_int("RANK", 0)
     if rank != 0:
         return 0
-    from oracle import Reference, has_reference, Oracle
-    a = make_host(cfg.name)
-    threads = min(os.cpu_count() or 1, 64)
-    if has_reference():
-        ref, kind = Reference(), "reference"
-        batch = lambda s0: ref.corutv_batch(a, cfg.d, cfg.q, 42, s0, threads, threads)  # noqa: E731
-    else:
-        ora, kind = Oracle(), "port"
-
-        def batch(s0):
-            import concurrent.futures as cf
-            with cf.ThreadPoolExecutor(threads) as ex:
-                list(ex.map(lambda i: ora.corutv(a, cfg.d, cfg.q, 0, 42, s0 + i, threads=1), range(threads)))
+    _, a_host, a_sha, gen = make_workload(cfg)
+    run, cores, kind, what = reference_runner(cfg, a_host, args.variant_id)
     for w in range(args.warmup):
-        batch(10_000 + w * threads)
-    t0 = time.perf_counter()
+        run(1_000_000 + w)
+    times = []
     for s in range(args.steps):
-        batch(s * threads)
-    dt = time.perf_counter() - t0
-    value = args.steps * threads / dt
+        t0 = time.perf_counter()
+        run(s)
+        times.append(time.perf_counter() - t0)
+    dt = sum(times)
+    value = args.steps / dt
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt / args.steps * 1e3,
-        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": cfg.dtype.replace("f", "f"),
-        "data": "synthetic", "config": config_block(cfg, args, l2="n/a (CPU)"),
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": kind,
-                         "sample": f"each step = {threads} concurrent unmodified corutv calls (trial fan-out, "
-                                   f"coru_cli.cpp:171-177), one per host thread"},
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": cfg.dtype,
+        "data": "synthetic", "config": config_block(cfg, args, a_sha, gen),
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": kind,
+                         "sample": f"each step = one whole {cfg.name} decomposition of the same A: {what}",
+                         "host_cores_total": os.cpu_count()},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "step_s": {"min": min(times), "median": statistics.median(times), "max": max(times)},
     }
     print(json.dumps(line), flush=True)
     return 0
-
-
-def config_block(cfg, args, l2):
-    return {"workload": f"{cfg.name}: {cfg.dtype} {cfg.m}x{cfg.n}, {cfg.desc}, d={cfg.d}, q={cfg.q}, k={cfg.k}",
-            "m": cfg.m, "n": cfg.n, "d": cfg.d, "q": cfg.q, "k": cfg.k, "seed": "RngSeed{42, step}",
-            "variant": args.variant, "passes_over_A": 2 * cfg.q + (3 if args.variant == "exact" else 2),
-            "parallelism": f"row-sharded x{args.gpus}" if args.gpus > 1 else "single GPU", "l2": l2}
 
 
 # ---- our arm --------------------------------------------------------------------------------------
@@ -265,6 +301,8 @@ def run_ours(args, cfg):
     import paper_1810_07323_b200 as cg
 
     rank, world, local = env_int("RANK", 0), env_int("WORLD_SIZE", 1), env_int("LOCAL_RANK", 0)
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: WORLD_SIZE={world} but --gpus {args.gpus}")
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
@@ -277,8 +315,9 @@ def run_ours(args, cfg):
     stream = torch.cuda.Stream(dev)
     ctx.set_stream(stream.cuda_stream)
 
-    # A: generated on the GPU (identical on every rank), this rank keeps its row block.
-    a_full = make_device(cfg.name, device=dev)
+    # A: generated on the GPU (identical bytes on every rank and in the reference arm); this rank
+    # keeps its row block. Rank 0 keeps a host copy for the e2e leg, the CPU baseline and the SHA.
+    a_full, a_host_full, a_sha, gen = make_workload(cfg, want_host=(rank == 0), device=dev)
     row0, rows = cg.shard_rows(cfg.m, rank, world)
     a = a_full[row0:row0 + rows].contiguous()
     del a_full
@@ -337,8 +376,10 @@ def run_ours(args, cfg):
         total_ms = float(tt.item())
     value = args.steps / (total_ms * 1e-3)
 
-    # e2e: the same decomposition through host buffers (pinned A in, U/T/V out) every step.
-    e2e = run_e2e(args, cfg, ctx, a, world, rank, local, dev, barrier)
+    # e2e: the same decomposition through host buffers every step (pageable A = the drop-in
+    # caller's storage; then page-locked A).
+    e2e = run_e2e(args, cfg, ctx, a, a_host_full, world, rank, local, dev, barrier, pinned=False)
+    e2e_pinned = run_e2e(args, cfg, ctx, a, a_host_full, world, rank, local, dev, barrier, pinned=True)
 
     peaks, peak_src = measured_peaks()
     roof = None
@@ -370,15 +411,15 @@ def run_ours(args, cfg):
 
     cpu = None
     if world == 1 and rank == 0 and not args.no_cpu_baseline:
-        cpu = cpu_baseline_sample(cfg, make_host(cfg.name), args.variant_id)
+        cpu = cpu_baseline_sample(cfg, a_host_full, args.variant_id)
 
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": cfg.dtype, "data": "synthetic",
-            "config": config_block(cfg, args, l2="flushed between steps (256 MB write outside the per-step events)"),
-            "e2e": e2e, "roofline": roof, "cpu_baseline": cpu, "gpu_launches": launches,
+            "config": config_block(cfg, args, a_sha, gen),
+            "e2e": e2e, "e2e_pinned": e2e_pinned, "roofline": roof, "cpu_baseline": cpu, "gpu_launches": launches,
             "clocks": clk.summary(), "wall_s_timed_region": wall,
             "step_ms": {"min": min(step_ms), "median": statistics.median(step_ms), "max": max(step_ms)},
         }
@@ -390,17 +431,27 @@ def run_ours(args, cfg):
     return 0
 
 
-def run_e2e(args, cfg, ctx, a, world, rank, local, dev, barrier):
+def run_e2e(args, cfg, ctx, a, a_host_full, world, rank, local, dev, barrier, pinned):
+    """Host buffers in, host buffers out, every step. Single GPU: the drop-in host entry
+    coru_corutv_{f64,f32} (validation, H2D of A overlapped with the first power round, D2H of
+    U/T/V). N > 1: per-rank H2D of the A shard + the device entry + D2H, max over ranks."""
     import ctypes as C
     import torch
     import paper_1810_07323_b200 as cg
     lib = cg.load_library()
     m_local, n, d = a.shape[0], cfg.n, cfg.d
     dt = a.dtype
-    a_host = a.cpu().pin_memory()
-    u_h = torch.empty((m_local, d), dtype=dt).pin_memory()
-    t_h = torch.empty((d, d), dtype=dt).pin_memory()
-    v_h = torch.empty((n, d), dtype=dt).pin_memory()
+    if world == 1:
+        a_np = np.ascontiguousarray(a_host_full)
+        a_h = torch.from_numpy(a_np).pin_memory() if pinned else None
+        a_ptr = a_h.data_ptr() if pinned else a_np.ctypes.data
+    else:
+        a_h = a.cpu()
+        if pinned:
+            a_h = a_h.pin_memory()
+        a_ptr = a_h.data_ptr()
+    mk = (lambda *s: torch.empty(s, dtype=dt).pin_memory()) if pinned else (lambda *s: torch.empty(s, dtype=dt))
+    u_h, t_h, v_h = mk(m_local, d), mk(d, d), mk(n, d)
     perm = np.zeros(d, np.int64)
     lower, warn = C.c_int(), C.c_int()
     sfx = "f64" if cfg.dtype == "f64" else "f32"
@@ -408,7 +459,7 @@ def run_e2e(args, cfg, ctx, a, world, rank, local, dev, barrier):
         fn = getattr(lib, f"coru_corutv_{sfx}")
 
         def step(s):
-            cg._check(fn(ctx.h, a_host.data_ptr(), cfg.m, n, d, cfg.q, args.variant_id, 42, 500_000 + s,
+            cg._check(fn(ctx.h, a_ptr, cfg.m, n, d, cfg.q, args.variant_id, 42, 500_000 + s,
                          u_h.data_ptr(), t_h.data_ptr(), v_h.data_ptr(), perm.ctypes.data, C.byref(lower),
                          C.byref(warn)))
     else:
@@ -423,7 +474,7 @@ def run_e2e(args, cfg, ctx, a, world, rank, local, dev, barrier):
 
         def step(s):
             with torch.cuda.stream(s_):
-                a_dev.copy_(a_host, non_blocking=True)
+                a_dev.copy_(a_h, non_blocking=True)
             cg._check(fn(ctx.h, a_dev.data_ptr(), m_local, cfg.m, n, a_dev.stride(0), d, cfg.q, args.variant_id, 42,
                          500_000 + s, C.byref(out)))
             with torch.cuda.stream(s_):
@@ -447,11 +498,31 @@ def run_e2e(args, cfg, ctx, a, world, rank, local, dev, barrier):
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         el = float(tt.item())
     es = a.element_size()
+    kind = "page-locked" if pinned else "pageable"
     return {"value": args.steps / el, "unit": UNIT, "h2d_bytes_per_step": int(a.numel() * es),
             "d2h_bytes_per_step": int((m_local * d + d * d + n * d) * es + d * 8 + 8),
-            "api": f"coru_corutv_{sfx} (host buffers, pinned)" if world == 1 else
-                   f"coru_corutv_{sfx}_dev + per-step H2D(A shard)/D2H(U,T,V)",
+            "host_memory": kind,
+            "api": (f"coru_corutv_{sfx} (host buffers, {kind})" if world == 1 else
+                    f"coru_corutv_{sfx}_dev + per-step H2D(A shard)/D2H(U,T,V), {kind} host buffers"),
             "timer": "host wall clock (each call returns synchronised), max over ranks"}
+
+
+def spawn_ranks(args):
+    """`--gpus N` outside torchrun: re-launch under torch.distributed.run (one rank per GPU)."""
+    import socket
+    import subprocess
+    import torch
+    have = torch.cuda.device_count()
+    if have < args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but only {have} CUDA device(s) visible")
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd, env=env)
 
 
 def main():
@@ -459,7 +530,7 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", default="C2q1", choices=sorted(CONFIGS))
+    ap.add_argument("--config", default="C3", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--variant", default="exact", choices=["exact", "approx"],
@@ -469,6 +540,8 @@ def main():
     cfg = CONFIGS[args.config]
     if args.impl == "reference":
         return run_reference_arm(args, cfg)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return spawn_ranks(args)
     return run_ours(args, cfg)
 
 

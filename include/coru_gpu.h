@@ -67,10 +67,11 @@ int coru_ctx_set_stream(coru_ctx* ctx, void* cuda_stream);
 /* Host threads used for the bit-exact Gaussian test matrix (default: hardware concurrency). */
 int coru_ctx_set_host_threads(coru_ctx* ctx, int threads);
 /* Where corutv draws Φ (corutv.hpp:51):
- *   CORU_PHI_DEVICE (default): generated on the GPU — the reference's xoshiro256++ word stream
- *     bit-for-bit, Box–Muller with the device log/sincos (entries within a few ulp of the host's);
- *   CORU_PHI_HOST_EXACT: generated on the host with the host libm (bit-identical to the
- *     reference's gaussian()) and copied in. */
+ *   CORU_PHI_HOST_EXACT (default): generated on the host with the host libm, bit-identical to the
+ *     reference's gaussian() (rng.hpp:86-112), by the worker pool in row chunks whose H2D copies
+ *     overlap the generation of the next chunk;
+ *   CORU_PHI_DEVICE (opt-in): generated on the GPU — the reference's xoshiro256++ word stream
+ *     bit-for-bit, Box–Muller with the device log/sincos (entries within a few ulp of the host's). */
 enum { CORU_PHI_DEVICE = 0, CORU_PHI_HOST_EXACT = 1 };
 int coru_ctx_set_phi_mode(coru_ctx* ctx, int mode);
 /* fp32 A-pass engine (the fp32 configuration; matmul at corutv.hpp:55,57,90):

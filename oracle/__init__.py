@@ -21,6 +21,8 @@ import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 ORACLE_SO = os.path.join(HERE, "liboracle.so")
+# the same restatement built with FMA contraction: SURVEY.md §8c protocol 2 (implementation floor)
+ORACLE_FMA_SO = os.path.join(HERE, "liboracle_fma.so")
 REF_SO = os.path.join(HERE, "_ref", "libcoru_ref.so")
 
 _i64, _u64, _int, _dbl = C.c_int64, C.c_uint64, C.c_int, C.c_double

@@ -13,24 +13,47 @@
 #define FN(name) CAT(name, SUFFIX)
 
 /* matmul (matrix.hpp:115-131): c(i,.) += a(i,k)·b(k,.) over k increasing. Rows are
- * independent, so the row-parallel split is bit-identical to the serial loop. */
+ * independent, so the row-parallel split is bit-identical to the serial loop. Four rows share
+ * each b(k,.) load (register blocking over i); each entry still sums over k increasing. */
 static void FN(mm_)(const T* a, int64_t m, int64_t kk, const T* b, int64_t n, T* c, int threads) {
     memset(c, 0, sizeof(T) * (size_t)(m * n));
+    const int64_t mb = (m + 3) / 4;
 #pragma omp parallel for schedule(static) num_threads(threads) if (threads > 1 && m > 64)
-    for (int64_t i = 0; i < m; ++i) {
-        T* ci = c + i * n;
-        const T* ai = a + i * kk;
+    for (int64_t ib = 0; ib < mb; ++ib) {
+        const int64_t i0 = ib * 4, cnt = m - i0 < 4 ? m - i0 : 4;
+        if (cnt < 4) {
+            for (int64_t i = i0; i < m; ++i) {
+                T* ci = c + i * n;
+                const T* ai = a + i * kk;
+                for (int64_t k = 0; k < kk; ++k) {
+                    const T aik = ai[k];
+                    const T* bk = b + k * n;
+                    for (int64_t j = 0; j < n; ++j) ci[j] += aik * bk[j];
+                }
+            }
+            continue;
+        }
+        T *c0 = c + i0 * n, *c1 = c0 + n, *c2 = c1 + n, *c3 = c2 + n;
+        const T *a0 = a + i0 * kk, *a1 = a0 + kk, *a2 = a1 + kk, *a3 = a2 + kk;
         for (int64_t k = 0; k < kk; ++k) {
-            const T aik = ai[k];
+            const T x0 = a0[k], x1 = a1[k], x2 = a2[k], x3 = a3[k];
             const T* bk = b + k * n;
-            for (int64_t j = 0; j < n; ++j) ci[j] += aik * bk[j];
+            for (int64_t j = 0; j < n; ++j) {
+                const T bj = bk[j];
+                c0[j] += x0 * bj;
+                c1[j] += x1 * bj;
+                c2[j] += x2 * bj;
+                c3[j] += x3 * bj;
+            }
         }
     }
 }
 
 /* matmul(a.transposed(), y) (corutv.hpp:50,57) without materialising a^T: output row j of
  * a^T·y accumulates a(i,j)·y(i,.) over i increasing, exactly the i-k-j order of
- * matmul(at, y); the loop below keeps that per-entry order, so the bits are unchanged. */
+ * matmul(at, y); the loop below keeps that per-entry order, so the bits are unchanged.
+ * Threads own output rows j; four rows i of a are folded into each accumulator load in
+ * sequence ((c + a_i y_i) + a_{i+1} y_{i+1} ...), which is still the serial order. */
 static void FN(mm_tn_)(const T* a, int64_t m, int64_t n, const T* y, int64_t d, T* c, int threads) {
     memset(c, 0, sizeof(T) * (size_t)(n * d));
     const int nt = threads > 1 ? threads : 1;
@@ -42,7 +65,24 @@ static void FN(mm_tn_)(const T* a, int64_t m, int64_t n, const T* y, int64_t d, 
         const int t = 0, tt = 1;
 #endif
         const int64_t j0 = n * t / tt, j1 = n * (t + 1) / tt;
-        for (int64_t i = 0; i < m; ++i) {
+        int64_t i = 0;
+        for (; i + 4 <= m; i += 4) {
+            const T *a0 = a + i * n, *a1 = a0 + n, *a2 = a1 + n, *a3 = a2 + n;
+            const T *y0 = y + i * d, *y1 = y0 + d, *y2 = y1 + d, *y3 = y2 + d;
+            for (int64_t j = j0; j < j1; ++j) {
+                const T x0 = a0[j], x1 = a1[j], x2 = a2[j], x3 = a3[j];
+                T* cj = c + j * d;
+                for (int64_t l = 0; l < d; ++l) {
+                    T s = cj[l];
+                    s += x0 * y0[l];
+                    s += x1 * y1[l];
+                    s += x2 * y2[l];
+                    s += x3 * y3[l];
+                    cj[l] = s;
+                }
+            }
+        }
+        for (; i < m; ++i) {
             const T* ai = a + i * n;
             const T* yi = y + i * d;
             for (int64_t j = j0; j < j1; ++j) {
@@ -98,23 +138,42 @@ static void FN(upper_triangle_)(const T* w, int64_t m, int64_t n, T* r) {
         for (int64_t i = 0; i <= j && i < n; ++i) r[i * n + j] = w[j * m + i];
 }
 
-/* householder_qr (qr.hpp:85-99). Returns 1 (EINVAL) when m < n. */
-int FN(oracle_householder_qr_)(const T* a, int64_t m, int64_t n, T* q, T* r) {
+/* householder_qr (qr.hpp:85-99). Returns 1 (EINVAL) when m < n. `threads` > 1 applies each
+ * reflector to the trailing columns (and accumulate_q's columns) in parallel: every column is
+ * updated by exactly the reference's loop, so the bits do not depend on the thread count. */
+static int FN(householder_qr_mt_)(const T* a, int64_t m, int64_t n, T* q, T* r, int threads) {
     if (m < n || n < 1) return 1;
     T* w = (T*)malloc(sizeof(T) * (size_t)(m * n));
     T* beta = (T*)calloc((size_t)n, sizeof(T));
     for (int64_t i = 0; i < m; ++i)
         for (int64_t j = 0; j < n; ++j) w[j * m + i] = a[i * n + j];
+    const int par = threads > 1 && m >= 4096;
     for (int64_t j = 0; j < n; ++j) {
         beta[j] = FN(make_reflector_)(m, j, w + j * m);
         const T* vcol = w + j * m;
+#pragma omp parallel for schedule(dynamic, 1) num_threads(threads) if (par)
         for (int64_t c = j + 1; c < n; ++c) FN(apply_reflector_)(vcol, beta[j], m, j, w + c * m);
     }
-    if (q) FN(accumulate_q_)(w, beta, m, n, q);
+    if (q) {
+        T* qc = (T*)calloc((size_t)(m * n), sizeof(T));
+        for (int64_t j = 0; j < n; ++j) qc[j * m + j] = 1;
+        for (int64_t j = n; j-- > 0;) {
+            const T* vcol = w + j * m;
+#pragma omp parallel for schedule(dynamic, 1) num_threads(threads) if (par)
+            for (int64_t c = 0; c < n; ++c) FN(apply_reflector_)(vcol, beta[j], m, j, qc + c * m);
+        }
+        for (int64_t i = 0; i < m; ++i)
+            for (int64_t j = 0; j < n; ++j) q[i * n + j] = qc[j * m + i];
+        free(qc);
+    }
     if (r) FN(upper_triangle_)(w, m, n, r);
     free(w);
     free(beta);
     return 0;
+}
+
+int FN(oracle_householder_qr_)(const T* a, int64_t m, int64_t n, T* q, T* r) {
+    return FN(householder_qr_mt_)(a, m, n, q, r, 1);
 }
 
 /* qrcp (qr.hpp:106-143): Businger–Golub, ties to the lowest index (strict >, :122-123),
@@ -183,8 +242,8 @@ int FN(oracle_sketch_bases_)(const T* a, int64_t m, int64_t n, int64_t ell, int 
         memcpy(c2p, c2, sizeof(T) * (size_t)(n * ell)); /* c2_prev (corutv.hpp:56) */
         FN(mm_tn_)(a, m, n, c1, ell, c2, threads);  /* c2 = a^T·c1 (corutv.hpp:57) */
     }
-    FN(oracle_householder_qr_)(c1, m, ell, q1, r1);
-    if (q2) FN(oracle_householder_qr_)(c2, n, ell, q2, NULL);
+    FN(householder_qr_mt_)(c1, m, ell, q1, r1, threads);
+    if (q2) FN(householder_qr_mt_)(c2, n, ell, q2, NULL, threads);
     const double r00 = fabs((double)r1[0]);
     const double rll = fabs((double)r1[(ell - 1) * ell + (ell - 1)]);
     if (warn) *warn = rll <= 1e-14 * r00;
@@ -243,13 +302,41 @@ int FN(oracle_corutv_)(const T* a, int64_t m, int64_t n, int64_t ell, int q, int
         /* d = (q1^T·a)·q2 (corutv.hpp:90): q1^T·a is the tn product of (a-as-m×n, q1). Its row l
          * accumulates q1(i,l)·a(i,.) over i increasing — matmul(q1.transposed(), a)'s order. */
         q1ta = (T*)calloc((size_t)(ell * n), sizeof(T));
-#pragma omp parallel for schedule(static) num_threads(threads) if (threads > 1)
-        for (int64_t l = 0; l < ell; ++l) {
-            T* row = q1ta + l * n;
-            for (int64_t i = 0; i < m; ++i) {
-                const T w = q1[i * ell + l];
+        /* threads split the columns j: each entry still sums over i increasing, and A is read
+         * once instead of once per row l */
+        const int nt = threads > 1 ? threads : 1;
+#pragma omp parallel num_threads(nt) if (nt > 1)
+        {
+#ifdef _OPENMP
+            const int th = omp_get_thread_num(), tt = omp_get_num_threads();
+#else
+            const int th = 0, tt = 1;
+#endif
+            const int64_t j0 = n * th / tt, j1 = n * (th + 1) / tt;
+            int64_t i = 0;
+            for (; i + 4 <= m; i += 4) {  /* four rows of a folded in sequence per load */
+                const T *a0 = a + i * n, *a1 = a0 + n, *a2 = a1 + n, *a3 = a2 + n;
+                for (int64_t l = 0; l < ell; ++l) {
+                    const T w0 = q1[i * ell + l], w1 = q1[(i + 1) * ell + l];
+                    const T w2 = q1[(i + 2) * ell + l], w3 = q1[(i + 3) * ell + l];
+                    T* row = q1ta + l * n;
+                    for (int64_t j = j0; j < j1; ++j) {
+                        T s = row[j];
+                        s += w0 * a0[j];
+                        s += w1 * a1[j];
+                        s += w2 * a2[j];
+                        s += w3 * a3[j];
+                        row[j] = s;
+                    }
+                }
+            }
+            for (; i < m; ++i) {
                 const T* ai = a + i * n;
-                for (int64_t j = 0; j < n; ++j) row[j] += w * ai[j];
+                for (int64_t l = 0; l < ell; ++l) {
+                    const T w = q1[i * ell + l];
+                    T* row = q1ta + l * n;
+                    for (int64_t j = j0; j < j1; ++j) row[j] += w * ai[j];
+                }
             }
         }
         FN(mm_)(q1ta, ell, n, q2, ell, d, 1);

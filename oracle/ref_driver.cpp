@@ -54,7 +54,8 @@ int guarded(F&& f) {
 }
 
 // Row-parallel i-k-j product. matmul's i loop carries no dependency
-// (matrix.hpp:121-129), so splitting it over threads leaves every output bit unchanged.
+// (matrix.hpp:121-129), so splitting it over threads leaves every output bit unchanged. Four rows
+// share each b(k,.) load; every entry still sums over k increasing.
 Matrix matmul_rows(const Matrix& a, const Matrix& b, int threads) {
     if (threads <= 1) return coru::matmul(a, b);
     Matrix c(a.rows(), b.cols());
@@ -63,7 +64,23 @@ Matrix matmul_rows(const Matrix& a, const Matrix& b, int threads) {
     for (int t = 0; t < threads; ++t) {
         pool.emplace_back([&, t] {
             const size_t lo = m * t / threads, hi = m * (t + 1) / threads;
-            for (size_t i = lo; i < hi; ++i) {
+            size_t i = lo;
+            for (; i + 4 <= hi; i += 4) {
+                double *c0 = c.row(i), *c1 = c.row(i + 1), *c2 = c.row(i + 2), *c3 = c.row(i + 3);
+                const double *a0 = a.row(i), *a1 = a.row(i + 1), *a2 = a.row(i + 2), *a3 = a.row(i + 3);
+                for (size_t k = 0; k < kk; ++k) {
+                    const double x0 = a0[k], x1 = a1[k], x2 = a2[k], x3 = a3[k];
+                    const double* bk = b.row(k);
+                    for (size_t j = 0; j < n; ++j) {
+                        const double bj = bk[j];
+                        c0[j] += x0 * bj;
+                        c1[j] += x1 * bj;
+                        c2[j] += x2 * bj;
+                        c3[j] += x3 * bj;
+                    }
+                }
+            }
+            for (; i < hi; ++i) {
                 double* ci = c.row(i);
                 const double* ai = a.row(i);
                 for (size_t k = 0; k < kk; ++k) {
@@ -90,6 +107,90 @@ Matrix transposed_rows(const Matrix& a, int threads) {
         });
     for (auto& th : pool) th.join();
     return t;
+}
+
+// matmul(a.transposed(), y) without forming a^T (corutv.hpp:50,57): out row i of a^T·y sums
+// a(k,i)·y(k,.) over k increasing, exactly coru::matmul's i-k-j order on the transpose. Threads
+// own ranges of output rows and sweep the rows k of a together, so a and y are streamed once per
+// thread instead of once per output row; every output entry keeps its summation order.
+Matrix matmul_tn_cols(const Matrix& a, const Matrix& y, int threads) {
+    const size_t m = a.rows(), n = a.cols(), d = y.cols();
+    Matrix c(n, d);
+    std::vector<std::thread> pool;
+    const int nt = std::max(1, threads);
+    for (int th = 0; th < nt; ++th)
+        pool.emplace_back([&, th] {
+            const size_t i0 = n * th / nt, i1 = n * (th + 1) / nt;
+            size_t k = 0;
+            for (; k + 4 <= m; k += 4) {  // four rows of a folded in sequence per accumulator load
+                const double *a0 = a.row(k), *a1 = a.row(k + 1), *a2 = a.row(k + 2), *a3 = a.row(k + 3);
+                const double *y0 = y.row(k), *y1 = y.row(k + 1), *y2 = y.row(k + 2), *y3 = y.row(k + 3);
+                for (size_t i = i0; i < i1; ++i) {
+                    const double x0 = a0[i], x1 = a1[i], x2 = a2[i], x3 = a3[i];
+                    double* ci = c.row(i);
+                    for (size_t j = 0; j < d; ++j) {
+                        double s = ci[j];
+                        s += x0 * y0[j];
+                        s += x1 * y1[j];
+                        s += x2 * y2[j];
+                        s += x3 * y3[j];
+                        ci[j] = s;
+                    }
+                }
+            }
+            for (; k < m; ++k) {
+                const double* ak = a.row(k);
+                const double* yk = y.row(k);
+                for (size_t i = i0; i < i1; ++i) {
+                    const double aki = ak[i];
+                    double* ci = c.row(i);
+                    for (size_t j = 0; j < d; ++j) ci[j] += aki * yk[j];
+                }
+            }
+        });
+    for (auto& t : pool) t.join();
+    return c;
+}
+
+// matmul(q.transposed(), a) (corutv.hpp:90's inner product): out row l sums q(k,l)·a(k,.) over k
+// increasing. Threads own column ranges of the output and sweep k, so a is read once in total.
+Matrix matmul_qt_a(const Matrix& q, const Matrix& a, int threads) {
+    const size_t m = a.rows(), n = a.cols(), d = q.cols();
+    Matrix c(d, n);
+    std::vector<std::thread> pool;
+    const int nt = std::max(1, threads);
+    for (int th = 0; th < nt; ++th)
+        pool.emplace_back([&, th] {
+            const size_t j0 = n * th / nt, j1 = n * (th + 1) / nt;
+            size_t k = 0;
+            for (; k + 4 <= m; k += 4) {
+                const double *a0 = a.row(k), *a1 = a.row(k + 1), *a2 = a.row(k + 2), *a3 = a.row(k + 3);
+                const double *q0 = q.row(k), *q1 = q.row(k + 1), *q2 = q.row(k + 2), *q3 = q.row(k + 3);
+                for (size_t l = 0; l < d; ++l) {
+                    const double w0 = q0[l], w1 = q1[l], w2 = q2[l], w3 = q3[l];
+                    double* cl = c.row(l);
+                    for (size_t j = j0; j < j1; ++j) {
+                        double s = cl[j];
+                        s += w0 * a0[j];
+                        s += w1 * a1[j];
+                        s += w2 * a2[j];
+                        s += w3 * a3[j];
+                        cl[j] = s;
+                    }
+                }
+            }
+            for (; k < m; ++k) {
+                const double* ak = a.row(k);
+                const double* qk = q.row(k);
+                for (size_t l = 0; l < d; ++l) {
+                    const double w = qk[l];
+                    double* cl = c.row(l);
+                    for (size_t j = j0; j < j1; ++j) cl[j] += w * ak[j];
+                }
+            }
+        });
+    for (auto& t : pool) t.join();
+    return c;
 }
 
 }  // namespace
@@ -189,9 +290,10 @@ int ref_corutv(const double* a, int64_t m, int64_t n, int64_t ell, int q, int va
     });
 }
 
-// Same steps as coru::corutv's exact-D, m >= n branch (corutv.hpp:49-65, 89-97), with the two
-// A-products and the transpose row-parallel over `threads` threads: bit-identical to ref_corutv.
-// QR, QRCP and the Gaussian are the reference's own serial functions.
+// Same steps as coru::corutv's exact-D, m >= n branch (corutv.hpp:49-65, 89-97), with the
+// A-products spread over `threads` threads in the reference's per-entry summation order (A^T is
+// never formed; the Q1^T·A product keeps matmul(q1.transposed(), a)'s order): bit-identical to
+// ref_corutv. QR, QRCP and the Gaussian are the reference's own serial functions.
 int ref_corutv_mt(const double* a_, int64_t m, int64_t n, int64_t ell, int q, uint64_t seed,
                   uint64_t stream, int threads, double* u, double* t, double* v, int* flags) {
     return guarded([&] {
@@ -199,18 +301,17 @@ int ref_corutv_mt(const double* a_, int64_t m, int64_t n, int64_t ell, int q, ui
         coru::detail::check_corutv_params(a, size_t(ell));
         if (q < 0) throw std::invalid_argument("corutv: q must be >= 0");
         if (m < n) throw std::invalid_argument("ref_corutv_mt: m >= n only");
-        const Matrix at = transposed_rows(a, threads);
         Matrix c2 = coru::gaussian(a.cols(), size_t(ell), {seed, stream});
         Matrix c1(a.rows(), size_t(ell));
         for (int i = 0; i <= q; ++i) {
             c1 = matmul_rows(a, c2, threads);
-            c2 = matmul_rows(at, c1, threads);
+            c2 = matmul_tn_cols(a, c1, threads);  // = matmul(a.transposed(), c1), same bits
         }
         coru::QrFactors f1 = coru::householder_qr(c1);
         coru::QrFactors f2 = coru::householder_qr(c2);
         const bool warn = std::abs(f1.r(size_t(ell) - 1, size_t(ell) - 1)) <= 1e-14 * std::abs(f1.r(0, 0));
         // D = (Q1^T A) Q2 (corutv.hpp:90)
-        const Matrix d = coru::matmul(matmul_rows(f1.q.transposed(), a, threads), f2.q);
+        const Matrix d = coru::matmul(matmul_qt_a(f1.q, a, threads), f2.q);
         coru::QrcpFactors cp = coru::qrcp(d);
         put(matmul_rows(f1.q, cp.q, threads), u);
         put(cp.r, t);

@@ -240,9 +240,9 @@ class Context:
     PHI_DEVICE, PHI_HOST_EXACT = 0, 1
 
     def set_phi_mode(self, mode: int):
-        """PHI_DEVICE (default): Φ generated on the GPU (reference word stream bit-for-bit, Box–Muller
-        values within a few ulp of the host libm's); PHI_HOST_EXACT: host-generated, bit-identical
-        to the reference's gaussian()."""
+        """PHI_HOST_EXACT (default): host-generated, bit-identical to the reference's gaussian()
+        (rng.hpp:86-112); PHI_DEVICE (opt-in): Φ generated on the GPU (reference word stream
+        bit-for-bit, Box–Muller values within a few ulp of the host libm's)."""
         _check(self.lib.coru_ctx_set_phi_mode(self.h, mode))
 
     F32_AUTO, F32_SIMT, F32_TC = 0, 1, 2

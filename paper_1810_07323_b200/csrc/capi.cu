@@ -23,6 +23,7 @@
 #include <cmath>
 #include <cstring>
 #include <condition_variable>
+#include <functional>
 #include <mutex>
 #include <string>
 #include <thread>
@@ -39,9 +40,13 @@
 #include "tsqr.cuh"
 
 namespace coru_gpu {
+void host_parallel(int n, const std::function<void(int)>& f);
 template <typename OutT>
 void gaussian_host(int64_t rows, int64_t cols, uint64_t seed, uint64_t stream, OutT* out, int64_t ldo, int threads,
                    int streaming);
+template <typename OutT>
+void gaussian_host_rows(int64_t rows, int64_t cols, uint64_t seed, uint64_t stream, OutT* out, int64_t ldo,
+                        int threads, int streaming, int64_t r0, int64_t r1);
 }  // namespace coru_gpu
 
 using namespace coru_gpu;
@@ -179,13 +184,20 @@ struct coru_ctx {
     int num_sms = 148;
     int max_smem = 227 * 1024;
     int host_threads = 1;
-    int phi_mode = CORU_PHI_DEVICE;
+    int phi_mode = CORU_PHI_HOST_EXACT;  // the reference's Φ bit for bit (rng.hpp:86-112)
     int f32_path = CORU_F32_AUTO;
     bool wide_qr = true;  // CholeskyQR2 (fp64) for sketches wider than 128 columns, Householder fall-back
     char* arena = nullptr;
     size_t arena_bytes = 0;
     char* pinned = nullptr;
     size_t pinned_bytes = 0;
+    // Staging ring for pageable host buffers (std::vector / coru::Matrix storage): the host worker
+    // pool copies piece k+1 into a pinned slot while the DMA engine moves piece k.
+    static constexpr int kStageSlots = 4;
+    static constexpr size_t kStageBytes = size_t(16) << 20;
+    char* stage = nullptr;
+    cudaEvent_t ev_stage[kStageSlots] = {};
+    int stage_next = 0;
     ncclComm_t comm = nullptr;
     coru_threadcomm* tcomm = nullptr;  // in-process backend (instead of NCCL)
     void* tscratch = nullptr;          // its reduction scratch
@@ -236,6 +248,91 @@ int ensure_pinned(coru_ctx* c, size_t bytes) {
         return fail(CORU_ENOMEM, "cudaMallocHost of " + std::to_string(bytes) + " bytes failed");
     }
     c->pinned_bytes = bytes;
+    return CORU_OK;
+}
+
+bool is_pinned_host(const void* p) {
+    cudaPointerAttributes a{};
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return a.type == cudaMemoryTypeHost;
+}
+
+int ensure_stage(coru_ctx* c) {
+    if (c->stage) return CORU_OK;
+    if (cudaMallocHost(&c->stage, coru_ctx::kStageBytes * coru_ctx::kStageSlots) != cudaSuccess) {
+        cudaGetLastError();
+        c->stage = nullptr;
+        return fail(CORU_ENOMEM, "cudaMallocHost of the staging ring failed");
+    }
+    for (auto& e : c->ev_stage) CORU_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    return CORU_OK;
+}
+
+// memcpy on the host worker pool (pieces of >= 1 MB per worker).
+void parallel_memcpy(void* dst, const void* src, size_t bytes, int threads) {
+    const int nt = int(std::max<size_t>(1, std::min<size_t>(size_t(std::max(threads, 1)), bytes >> 20)));
+    host_parallel(nt, [&](int t) {
+        const size_t b0 = bytes * size_t(t) / size_t(nt), b1 = bytes * size_t(t + 1) / size_t(nt);
+        std::memcpy(static_cast<char*>(dst) + b0, static_cast<const char*>(src) + b0, b1 - b0);
+    });
+}
+
+// Host -> device copy of `bytes` on `st`. Page-locked sources go straight to the DMA engine; pageable
+// ones (the drop-in caller's std::vector storage) are staged through the pinned ring: the host pool
+// fills slot k+1 while the DMA engine drains slot k, so the copy runs near link speed instead of the
+// driver's synchronous pageable path. Returns once every piece is enqueued.
+int h2d(coru_ctx* c, void* dst, const void* src, size_t bytes, cudaStream_t st) {
+    if (bytes == 0) return CORU_OK;
+    if (is_pinned_host(src)) {
+        CORU_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, st));
+        return CORU_OK;
+    }
+    CORU_TRY(ensure_stage(c));
+    for (size_t off = 0; off < bytes; off += coru_ctx::kStageBytes) {
+        const size_t len = std::min(coru_ctx::kStageBytes, bytes - off);
+        const int b = c->stage_next;
+        c->stage_next = (b + 1) % coru_ctx::kStageSlots;
+        char* slot = c->stage + size_t(b) * coru_ctx::kStageBytes;
+        CORU_CUDA(cudaEventSynchronize(c->ev_stage[b]));  // the slot's previous DMA has drained
+        parallel_memcpy(slot, static_cast<const char*>(src) + off, len, c->host_threads);
+        CORU_CUDA(cudaMemcpyAsync(static_cast<char*>(dst) + off, slot, len, cudaMemcpyHostToDevice, st));
+        CORU_CUDA(cudaEventRecord(c->ev_stage[b], st));
+    }
+    return CORU_OK;
+}
+
+// Device -> host copy; synchronises `st`. Pageable destinations: piece k+1 is in flight while the
+// host pool copies piece k out of its slot.
+int d2h_sync(coru_ctx* c, void* dst, const void* src, size_t bytes, cudaStream_t st) {
+    if (bytes == 0) return CORU_OK;
+    if (is_pinned_host(dst)) {
+        CORU_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, st));
+        CORU_CUDA(cudaStreamSynchronize(st));
+        return CORU_OK;
+    }
+    CORU_TRY(ensure_stage(c));
+    constexpr size_t P = coru_ctx::kStageBytes;
+    const size_t pieces = (bytes + P - 1) / P;
+    auto issue = [&](size_t k) -> int {
+        const int b = int(k % coru_ctx::kStageSlots);
+        const size_t off = k * P, len = std::min(P, bytes - off);
+        CORU_CUDA(cudaMemcpyAsync(c->stage + size_t(b) * P, static_cast<const char*>(src) + off, len,
+                                  cudaMemcpyDeviceToHost, st));
+        CORU_CUDA(cudaEventRecord(c->ev_stage[b], st));
+        return CORU_OK;
+    };
+    const size_t ahead = coru_ctx::kStageSlots - 1;
+    for (size_t k = 0; k < std::min(pieces, ahead); ++k) CORU_TRY(issue(k));
+    for (size_t k = 0; k < pieces; ++k) {
+        const int b = int(k % coru_ctx::kStageSlots);
+        const size_t off = k * P, len = std::min(P, bytes - off);
+        CORU_CUDA(cudaEventSynchronize(c->ev_stage[b]));
+        parallel_memcpy(static_cast<char*>(dst) + off, c->stage + size_t(b) * P, len, c->host_threads);
+        if (k + ahead < pieces) CORU_TRY(issue(k + ahead));
+    }
     return CORU_OK;
 }
 
@@ -543,8 +640,35 @@ int allgather(coru_ctx* c, const T* send, T* recv, size_t count) {
     return CORU_OK;
 }
 
-// Φ = gaussian(cols, ell, seed), padded to dp columns (corutv.hpp:51): on the device, or on the
-// host with the host libm (bit-exact) and one H2D.
+// Φ = gaussian(rows, cols, {seed, stream}) generated on the host with the host libm (bit-identical
+// to the reference's gaussian(), rng.hpp:86-112) into the pinned staging buffer, in row chunks:
+// chunk i+1 is generated by the worker pool while the DMA engine uploads chunk i on `st`.
+// Chunk boundaries start on Box–Muller pairs (row·cols even).
+template <typename T>
+int upload_phi_host(coru_ctx* c, int64_t rows, int cols, int ld, uint64_t seed, uint64_t stream, T* out,
+                    cudaStream_t st) {
+    const size_t bytes = size_t(rows) * ld * sizeof(T);
+    CORU_TRY(ensure_pinned(c, bytes));
+    CORU_CUDA(cudaStreamSynchronize(st));  // the pinned staging buffer is reused across calls
+    T* phi = reinterpret_cast<T*>(c->pinned);
+    const int64_t total = rows * int64_t(cols);
+    const int chunks = int(std::max<int64_t>(1, std::min<int64_t>(8, total / (1 << 17))));
+    int64_t r0 = 0;
+    for (int k = 1; k <= chunks; ++k) {
+        int64_t r1 = k == chunks ? rows : rows * k / chunks;
+        if ((r1 * cols) & 1) --r1;  // odd cols: end on an even row so the next chunk starts on a pair
+        if (r1 <= r0) continue;
+        gaussian_host_rows<T>(rows, cols, seed, stream, phi, ld, c->host_threads, 1, r0, r1);
+        CORU_CUDA(cudaMemcpyAsync(out + r0 * ld, phi + r0 * ld, size_t(r1 - r0) * ld * sizeof(T),
+                                  cudaMemcpyHostToDevice, st));
+        r0 = r1;
+    }
+    return CORU_OK;
+}
+
+// Φ = gaussian(cols, ell, seed), padded to dp columns (corutv.hpp:51). Default: host-generated,
+// bit-exact (upload_phi_host). CORU_PHI_DEVICE (opt-in): the device generator (same word stream,
+// device log/sincos, a few ulp off).
 template <typename T>
 int gen_phi(coru_ctx* c, const Request<T>& r, T* out, int dp) {
     const int64_t N = r.cols;
@@ -556,13 +680,7 @@ int gen_phi(coru_ctx* c, const Request<T>& r, T* out, int dp) {
         ++g_launches;
         return CORU_OK;
     }
-    const size_t phi_bytes = size_t(N) * dp * sizeof(T);
-    CORU_TRY(ensure_pinned(c, phi_bytes));
-    CORU_CUDA(cudaStreamSynchronize(st));  // the pinned staging buffer is reused across calls
-    T* phi = reinterpret_cast<T*>(c->pinned);
-    gaussian_host<T>(N, r.d, r.seed, r.stream, phi, dp, c->host_threads, 1);  // streaming stores, zero padding
-    CORU_CUDA(cudaMemcpyAsync(out, phi, phi_bytes, cudaMemcpyHostToDevice, st));
-    return CORU_OK;
+    return upload_phi_host<T>(c, N, r.d, dp, r.seed, r.stream, out, st);
 }
 
 template <typename T>
@@ -1198,18 +1316,18 @@ int corutv_host(coru_ctx* c, const T* A, int64_t m, int64_t n, int64_t ell, int 
         CORU_CUDA(cudaMemsetAsync(f_d, 0, sizeof(int), st));
         CORU_CUDA(cudaEventRecord(c->ev_fork, st));  // the copies may overwrite the arena from here on
         CORU_CUDA(cudaStreamWaitEvent(c->aux, c->ev_fork, 0));
-        for (int i = 0; i < C; ++i) {
-            int64_t r0, rows;
-            chunk_rows(i, r0, rows);
-            CORU_CUDA(cudaMemcpyAsync(a_d + r0 * n, A + r0 * n, sizeof(T) * rows * n, cudaMemcpyHostToDevice, c->aux));
-            CORU_CUDA(cudaEventRecord(c->ev_chunk[i], c->aux));
-        }
         const bool prof = c->prof;  // partial passes: not A-pass launches
         c->prof = false;
         int rc = CORU_OK;
         for (int i = 0; i < C && rc == CORU_OK; ++i) {
             int64_t r0, rows;
             chunk_rows(i, r0, rows);
+            // chunk i's H2D (staged when A is pageable) is enqueued before its GEMMs, so the host
+            // copies chunk i+1 while the GPU works on chunk i
+            rc = h2d(c, a_d + r0 * n, A + r0 * n, sizeof(T) * rows * n, c->aux);
+            if (rc == CORU_OK && cudaEventRecord(c->ev_chunk[i], c->aux) != cudaSuccess)
+                rc = fail(CORU_ECUDA, "cudaEventRecord failed");
+            if (rc != CORU_OK) break;
             const T* ai = a_d + r0 * n;
             if (cudaStreamWaitEvent(st, c->ev_chunk[i], 0) != cudaSuccess ||
                 any_nonfinite_acc<T>(ai, rows * n, f_d, st) != cudaSuccess) {
@@ -1229,7 +1347,7 @@ int corutv_host(coru_ctx* c, const T* A, int64_t m, int64_t n, int64_t ell, int 
         ++g_launches;
         r.first_done = true;
     } else {
-        CORU_CUDA(cudaMemcpyAsync(a_d, A, sizeof(T) * m * n, cudaMemcpyHostToDevice, st));
+        CORU_TRY(h2d(c, a_d, A, sizeof(T) * m * n, st));
         CORU_CUDA(any_nonfinite<T>(a_d, m * n, f_d, st));
         ++g_launches;
     }
@@ -1241,10 +1359,9 @@ int corutv_host(coru_ctx* c, const T* A, int64_t m, int64_t n, int64_t ell, int 
         if (bad) return fail(CORU_EINVAL, "Matrix: non-finite entry");
     }
     CORU_TRY(run<T>(c, r, head_bytes));
-    CORU_CUDA(cudaMemcpyAsync(U, u_d, sizeof(T) * m * ell, cudaMemcpyDeviceToHost, st));
-    CORU_CUDA(cudaMemcpyAsync(Tt, t_d, sizeof(T) * ell * ell, cudaMemcpyDeviceToHost, st));
-    CORU_CUDA(cudaMemcpyAsync(V, v_d, sizeof(T) * n * ell, cudaMemcpyDeviceToHost, st));
-    CORU_CUDA(cudaStreamSynchronize(st));
+    CORU_TRY(d2h_sync(c, U, u_d, sizeof(T) * m * ell, st));
+    CORU_TRY(d2h_sync(c, Tt, t_d, sizeof(T) * ell * ell, st));
+    CORU_TRY(d2h_sync(c, V, v_d, sizeof(T) * n * ell, st));
     if (lower) *lower = m < n ? 1 : 0;
     if (warn) *warn = out.conditioning_warning;
     return CORU_OK;
@@ -1272,13 +1389,7 @@ int fill_phi(coru_ctx* c, int64_t rows, int d, int dp, uint64_t seed, uint64_t s
         ++g_launches;
         return CORU_OK;
     }
-    const size_t bytes = size_t(rows) * dp * sizeof(double);
-    CORU_TRY(ensure_pinned(c, bytes));
-    CORU_CUDA(cudaStreamSynchronize(c->stream));  // the pinned staging buffer is reused
-    double* phi = reinterpret_cast<double*>(c->pinned);
-    gaussian_host<double>(rows, d, seed, stream, phi, dp, c->host_threads, 1);
-    CORU_CUDA(cudaMemcpyAsync(out, phi, bytes, cudaMemcpyHostToDevice, c->stream));
-    return CORU_OK;
+    return upload_phi_host<double>(c, rows, d, dp, seed, stream, out, c->stream);
 }
 
 // tsr_svd (baselines.hpp:43-56): two sketches (A·Φ1, A^T·Φ2), their QRs (two streams), the core
@@ -1876,6 +1987,9 @@ void coru_ctx_destroy(coru_ctx* c) {
     if (c->tscratch) cudaFree(c->tscratch);
     if (c->arena) cudaFree(c->arena);
     if (c->pinned) cudaFreeHost(c->pinned);
+    if (c->stage) cudaFreeHost(c->stage);
+    for (auto& e : c->ev_stage)
+        if (e) cudaEventDestroy(e);
     if (c->aux) {
         cudaStreamSynchronize(c->aux);
         cudaStreamDestroy(c->aux);

@@ -13,6 +13,7 @@
 //   * each Box–Muller pair is a pure function of its two words.
 // Workers come from a persistent pool (no thread creation per call). Compiled with
 // -ffp-contract=off (no FMA contraction on the host).
+#include <algorithm>
 #include <atomic>
 #include <cmath>
 #include <condition_variable>
@@ -197,6 +198,9 @@ Pool& pool() {
 
 }  // namespace
 
+// The same pool for other host-side bulk work (staging copies of pageable buffers, capi.cu).
+void host_parallel(int n, const std::function<void(int)>& f) { pool().run(n, f); }
+
 const uint64_t* jump_table_words(int* nbits) {
     static_assert(sizeof(Gf2) == 256 * 4 * sizeof(uint64_t), "dense table");
     *nbits = kJumpBits;
@@ -226,18 +230,23 @@ inline void store_stream(float* p, float v) {
 // converted to OutT (fp32 rounds the fp64 value). Identical output for any thread count.
 // streaming != 0: non-temporal stores, and the padding columns [cols, ldo) of every row are zeroed
 // (the buffer is a DMA source; see store_stream).
+// Only rows [r0, r1) are produced (r0·cols must be even: a row range starts on a Box–Muller pair);
+// the caller can upload finished row ranges while the next one is generated.
 template <typename OutT>
-void gaussian_host(int64_t rows, int64_t cols, uint64_t seed, uint64_t stream, OutT* out, int64_t ldo,
-                   int threads, int streaming) {
+void gaussian_host_rows(int64_t rows, int64_t cols, uint64_t seed, uint64_t stream, OutT* out, int64_t ldo,
+                        int threads, int streaming, int64_t r0, int64_t r1) {
     const int64_t total = rows * cols;
-    const int64_t pairs = (total + 1) / 2;
+    const int64_t e_lo = r0 * cols, e_hi = std::min(total, r1 * cols);
+    if (e_hi <= e_lo) return;
+    const int64_t q0 = e_lo / 2, q1 = (e_hi + 1) / 2;  // pairs of this range
+    const int64_t pairs = q1 - q0;
     const State s0 = seed_state(seed, stream);
     int nt = threads < 1 ? 1 : threads;
     if (pairs < 8192) nt = 1;
-    if (nt > 1) jump_table();  // build once, outside the timed fan-out
+    if (nt > 1 || q0 > 0) jump_table();  // build once, outside the timed fan-out
     pool().run(nt, [&](int t) {
-        const int64_t p0 = pairs * t / nt, p1 = pairs * (t + 1) / nt;
-        State st = t == 0 ? s0 : jump(s0, uint64_t(2 * p0));
+        const int64_t p0 = q0 + pairs * t / nt, p1 = q0 + pairs * (t + 1) / nt;
+        State st = p0 == 0 ? s0 : jump(s0, uint64_t(2 * p0));
         int64_t e = 2 * p0, r = e / cols, c = e % cols;
         auto put = [&](double v) {
             if (streaming) {
@@ -259,13 +268,23 @@ void gaussian_host(int64_t rows, int64_t cols, uint64_t seed, uint64_t stream, O
             const double theta = 2.0 * 3.141592653589793 * u2;  // 2·std::numbers::pi·u2
             const double sv = rad * std::sin(theta);
             put(rad * std::cos(theta));
-            if (2 * p + 1 < total) put(sv);
+            if (2 * p + 1 < e_hi) put(sv);
         }
         if (streaming) _mm_sfence();
     });
 }
 
+template <typename OutT>
+void gaussian_host(int64_t rows, int64_t cols, uint64_t seed, uint64_t stream, OutT* out, int64_t ldo, int threads,
+                   int streaming) {
+    gaussian_host_rows<OutT>(rows, cols, seed, stream, out, ldo, threads, streaming, 0, rows);
+}
+
 template void gaussian_host<double>(int64_t, int64_t, uint64_t, uint64_t, double*, int64_t, int, int);
 template void gaussian_host<float>(int64_t, int64_t, uint64_t, uint64_t, float*, int64_t, int, int);
+template void gaussian_host_rows<double>(int64_t, int64_t, uint64_t, uint64_t, double*, int64_t, int, int, int64_t,
+                                         int64_t);
+template void gaussian_host_rows<float>(int64_t, int64_t, uint64_t, uint64_t, float*, int64_t, int, int, int64_t,
+                                        int64_t);
 
 }  // namespace coru_gpu

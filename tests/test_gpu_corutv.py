@@ -58,9 +58,15 @@ def test_reference_cases(ctx, case):
         assert dg.max() <= 1e-8
         assert f.conditioning_warning == case["warning"]
     else:
-        # power rounds amplify rounding (SURVEY.md §0.1 finding 2): reconstruction quality must
-        # match the reference's to a few digits and the factors stay orthonormal.
+        # power rounds amplify rounding (SURVEY.md §0.1 finding 2): judged by the protocol of
+        # tests/parity_util.py against the oracle (bit-identical to this golden output) and its own
+        # floors at this input: |diag T| on the determined prefix within max(1e-8, 10x floor),
+        # reconstruction error within max(1e-10, 10x floor) and never worse, flag where determined.
+        from parity_util import parity_record
         assert e_gpu <= 1.5 * e_ref + 1e-13
+        rec, ok = parity_record(a, f, ell, q, ell, threads=4)
+        _record(case["name"], **rec)
+        assert ok["err"] and ok["never_worse"] and ok["diag"] and ok["flag"], rec
     if case["name"] == "fast_decay_120_q6":
         assert f.conditioning_warning  # test_corutv.cpp:198-206
     if case["name"] == "fast_decay_120_q0":
@@ -113,65 +119,29 @@ def test_determinism_bitwise(ctx):
     assert np.array_equal(f1.u, f2.u) and np.array_equal(f1.t, f2.t) and np.array_equal(f1.v, f2.v)
 
 
-def _floor(oracle, a, d, q, seed, k):
-    """SURVEY.md §8c protocol 1: the oracle against itself on A·(1 + s·2^-52), s in {-1,0,1}."""
-    w = oracle.xoshiro_words(99, 0, a.size)
-    s = (w % np.uint64(3)).astype(np.int64) - 1
-    ap = a * (1.0 + s.reshape(a.shape) * 2.0 ** -52)
-    f0 = oracle.corutv(a, d, q, seed=seed, threads=16)
-    f1 = oracle.corutv(ap, d, q, seed=seed, threads=16)
-    e0, e1 = rel_recon_error(a, f0.u, f0.t, f0.v), rel_recon_error(ap, f1.u, f1.t, f1.v)
-    dg = np.abs(np.abs(np.diag(f0.t)) - np.abs(np.diag(f1.t)))
-    return f0, abs(e0 - e1) / e0, dg[:k].max(), dg.max()
-
-
-def _floor_impl(oracle, a, d, q, seed, k, f0):
-    """Implementation floor: the reference algorithm with its A-products summed in a different
-    (blocked, BLAS) order and the oracle's own serial QR / QRCP — an equally valid execution of
-    the same algorithm, i.e. what "an independent implementation" may differ by."""
-    c2 = oracle.gaussian(a.shape[1], d, seed, 0)
-    for _ in range(q + 1):
-        c1 = a @ c2
-        c2 = a.T @ c1
-    q1, _ = oracle.householder_qr(c1)
-    q2, _ = oracle.householder_qr(c2)
-    qm, t, perm = oracle.qrcp((q1.T @ a) @ q2)
-    u, v = q1 @ qm, q2[:, perm]
-    e0, e1 = rel_recon_error(a, f0.u, f0.t, f0.v), rel_recon_error(a, u, t, v)
-    dg = np.abs(np.abs(np.diag(f0.t)) - np.abs(np.diag(t)))
-    return abs(e0 - e1) / e0, dg[:k].max(), dg.max()
-
-
 @pytest.mark.parametrize("name,m,n", [("C1", 1000, 1000), ("C2q1", 4000, 4000), ("C2q2", 4000, 4000),
                                       ("C3", 20000, 2000), ("C4", 4096, 4096)])
-def test_config_parity_vs_oracle(ctx, oracle, name, m, n):
+def test_config_parity_vs_oracle(ctx, name, m, n):
+    """BASELINE configs (full size for C1/C2, shape-scaled C3/C4; full-size C3 in
+    test_gpu_parity_fullsize.py) against the bit-exact oracle with the reference's Φ, judged by
+    the protocol of tests/parity_util.py (stated tolerance where the oracle's own floors allow it,
+    else 10x the larger floor on the determined |diag T| prefix; flag equal where determined)."""
     import paper_1810_07323_b200 as cg
-    from workloads import CONFIGS, make_host, sha256
+    from parity_util import parity_record
+    from workloads import CONFIGS, make_host
     c = CONFIGS[name]
     a = make_host(name, m, n)
-    seed = 42
-    f0, floor_err, floor_dk, floor_d = _floor(oracle, a, c.d, c.q, seed, c.k)
-    impl_err, impl_dk, impl_d = _floor_impl(oracle, a, c.d, c.q, seed, c.k, f0)
-    f = cg.corutv(a, c.d, c.q, seed=cg.RngSeed(seed, 0), ctx=ctx)
+    f = cg.corutv(a, c.d, c.q, seed=cg.RngSeed(42, 0), ctx=ctx)
     _check_structure(f, c.d)
-    e_gpu = rel_recon_error(a, f.u, f.t, f.v)
-    e_ora = rel_recon_error(a, f0.u, f0.t, f0.v)
-    rel_err_diff = abs(e_gpu - e_ora) / e_ora
-    dg = np.abs(np.abs(np.diag(f.t)) - np.abs(np.diag(f0.t)))
-    pivots_same = bool(np.array_equal(f.perm, f0.perm))
-    tol_err, tol_diag = 1e-10, 1e-8
-    _record(f"{name}_{m}x{n}", sha256=sha256(a), err_gpu=e_gpu, err_oracle=e_ora, rel_err_diff=rel_err_diff,
-            diag_k_absdiff=dg[:c.k].max(), diag_all_absdiff=dg.max(), floor_rel_err=floor_err,
-            floor_diag_k=floor_dk, floor_diag_all=floor_d, impl_floor_rel_err=impl_err,
-            impl_floor_diag_k=impl_dk, impl_floor_diag_all=impl_d, pivots_identical=pivots_same,
-            warn_gpu=f.conditioning_warning, warn_oracle=f0.conditioning_warning,
-            orth_u=orth_residual(f.u), orth_v=orth_residual(f.v),
-            baseline_tol_err_pass=bool(rel_err_diff <= tol_err), baseline_tol_diag_pass=bool(dg.max() <= tol_diag))
-    # The stated tolerance where the floors allow it; otherwise a small multiple of the floors.
-    assert rel_err_diff <= max(tol_err, 10 * floor_err, 5 * impl_err)
-    assert dg[:c.k].max() <= max(tol_diag, 10 * floor_dk, 5 * impl_dk)
-    # and never a worse approximation than the reference beyond that noise
-    assert e_gpu <= e_ora * (1 + max(tol_err, 5 * impl_err))
+    rec, ok = parity_record(a, f, c.d, c.q, c.k)
+    rec.update(orth_u=orth_residual(f.u), orth_v=orth_residual(f.v))
+    _record(f"{name}_{m}x{n}", **rec)
+    assert ok["err"] and ok["never_worse"], rec
+    assert ok["diag"], rec
+    assert ok["flag"], rec
+    if name == "C1":  # well-conditioned: the stated tolerances and identical pivots
+        assert rec["stated_tol_err_pass"] and rec["stated_tol_diag_all_pass"], rec
+        assert rec["first_pivot_divergence"] is None
 
 
 def test_cpp_wrapper_program(ctx):
