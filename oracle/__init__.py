@@ -72,7 +72,7 @@ class Oracle:
         L.oracle_sor_svd_f64.argtypes = [_p, _i64, _i64, _i64, _i64, _int, _u64, _u64, _int, _p]
         L.oracle_jacobi_svd_square.argtypes = [_p, _i64, _p, _p, _p]
         L.oracle_jacobi_svd_square.restype = _int
-        for sfx in ("f64", "f32"):
+        for sfx in ("f64", "f32", "f80"):
             getattr(L, f"oracle_matmul_{sfx}").argtypes = [_p, _i64, _i64, _p, _i64, _p, _int]
             getattr(L, f"oracle_matmul_tn_{sfx}").argtypes = [_p, _i64, _i64, _p, _i64, _p, _int]
             getattr(L, f"oracle_householder_qr_{sfx}").argtypes = [_p, _i64, _i64, _p, _p]
@@ -84,7 +84,12 @@ class Oracle:
 
     @staticmethod
     def _sfx(dtype):
-        return "f64" if np.dtype(dtype) == np.float64 else "f32"
+        dt = np.dtype(dtype)
+        if dt == np.float64:
+            return "f64"
+        if dt == np.longdouble and dt.itemsize == 16:
+            return "f80"
+        return "f32"
 
     def max_threads(self) -> int:
         return self.lib.oracle_max_threads()

@@ -240,6 +240,18 @@ void oracle_pinv_f64(const double* a, int64_t n, double* out) {
 #undef SUFFIX
 #undef SQRT
 
+/* Extended precision (x87 80-bit long double, 64-bit significand): the same algorithm with a
+ * unit roundoff 2^11 times smaller than fp64 — a stand-in for the exact-arithmetic result the
+ * fp64 executions (the reference, its FMA build, the GPU) approximate. Used only to measure
+ * which fp64 execution is closer to that result (tests/parity_util.py). */
+#define T long double
+#define SUFFIX f80
+#define SQRT sqrtl
+#include "coru_oracle_impl.h"
+#undef T
+#undef SUFFIX
+#undef SQRT
+
 int oracle_max_threads(void) {
 #ifdef _OPENMP
     return omp_get_max_threads();

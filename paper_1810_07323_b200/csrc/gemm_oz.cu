@@ -1,0 +1,658 @@
+// FP64 A-pass on the 5th-generation INT8 tensor cores: tcgen05.mma kind::i8, Ozaki-scheme
+// emulation of the fp64 product, TMA-fed, accumulators in TMEM.
+//
+// Replaces, for the fp64 configurations, the A-passes of corutv — matmul(a, c2) (corutv.hpp:55),
+// matmul(at, c1) (corutv.hpp:57, A^T never formed) and the A·Q2 half of the projection
+// (corutv.hpp:90) — with the gemm_f64 contract (C = op(A)·X, fp64 in/out, deterministic).
+//
+// Why. B200's FP64 path (DMMA) peaks at ~36 TFLOP/s, so a d = 110 A-pass over 3.2 GB (C3) is
+// compute-bound at 2.5 ms while its HBM time is 0.5 ms. The INT8 tensor cores run 4.5 POPS.
+// Ozaki's scheme splits each fp64 operand into 8-bit digit slices against a per-row (A) and
+// per-column (X) power-of-two scale; every slice product is EXACT in the int32 accumulator, and
+// the products are recombined in fp64. With S = 7 slices (55-bit significands) and the
+// triangular truncation s + t <= 6 (28 slice products) the result carries ~2^-55 relative error
+// against row-max x column-max, i.e. fp64-level accuracy (tests/test_gpu_oz.py measures it against
+// an extended-precision product next to the DMMA kernel's).
+//
+// Number format. Row i of op(A) has E_i with max_k |a_ik| < 2^E_i (gemm_oz_exponents, once per
+// decomposition: A does not change between passes). V_ik = rint(a_ik · 2^(55 - E_i)) is an
+// int64 with |V| < 2^55; its bytes are the digits: slice 0 = (int8) byte 6 (signed, the top
+// digit), slices 1..6 = bytes 5..0 (unsigned). So V = sum_s digit_s · 2^(8(6 - s)) with no carry
+// handling — the conversion is one F2I plus byte permutes. X is split the same way per column j
+// (F_j) by k_oz_split_x. The product a·x = V·W·2^(E_i + F_j - 110); level L = s + t collects the
+// slice products of weight 2^(8(12 - L)); levels 0..6 are accumulated (int32, one TMEM block of
+// 64 columns each = 448 of the 512 columns), the rest (< 2^-56 relative) dropped. int32 headroom:
+// a level sums <= 7 products of <= 2^16 per k, so accumulators are flushed to fp64 every
+// kOzChunkStages x 32 = 4096 k (< 2^31 / (7·2^16)).
+//
+// Data flow per CTA (one 128-row tile of op(A) x one N-chunk of nc <= 64 columns; 1 CTA / SM;
+// the nch CTAs of a row tile are adjacent in the grid so A comes from DRAM once and L2 after):
+//   warp 0      TMA producer: fp64 A tile (128 x 32) -> fp64 ring; the 7 X digit slices of the
+//               chunk (64 x 32 int8, SWIZZLE_32B) -> int8 ring
+//   warps 4..11 converters: thread (row r, k-half h) reads 16 fp64 of its row (op N: swizzled
+//               K-major tile; op T: a column of the [k][m] tile — A^T is never formed), scales,
+//               F2I, permutes bytes into the 7 A slices (K-major SW32 rows of 32 B) of the int8
+//               ring; at each flush they read the 7 level accumulators back (tcgen05.ld) and add
+//               sum_L acc_L 2^(-8L) · 2^(E_i + F_j - 14) into the fp64 output (own rows, fixed
+//               order: deterministic)
+//   warp 1      MMA issuer: 28 tcgen05.mma (M = 128, N = nc, K = 32) per stage, s8/u8 types per
+//               slice, A and B from shared memory descriptors
+//   warp 2      TMEM allocator
+// Split-K (op T: K = m rows of A) writes per-split fp64 partials summed in a fixed order.
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <mutex>
+
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include "common.cuh"
+#include "gemm.cuh"
+
+namespace coru_gpu {
+
+namespace {
+
+constexpr int kOzThreads = 384;
+constexpr int kOzBM = 128;
+constexpr int kOzBK = 32;              // k per stage = one UMMA K step of int8
+constexpr int kOzS = 7;                // digit slices per operand
+constexpr int kOzLevelCols = 64;       // TMEM columns per level accumulator
+constexpr int kOzNcMax = 64;           // columns per N-chunk
+constexpr int kOzMaxChunks = 4;        // N <= 256
+constexpr int kOzF = 2;                // fp64 ring stages
+constexpr int kOzI = 3;                // int8 ring stages
+constexpr int kOzChunkStages = 128;    // flush interval (stages)
+constexpr int kOzF64Bytes = kOzBM * kOzBK * 8;                  // 32 KB
+constexpr int kOzASlice = kOzBM * kOzBK;                        // 4 KB
+constexpr int kOzXSlice = kOzNcMax * kOzBK;                     // 2 KB
+constexpr int kOzIStage = kOzS * (kOzASlice + kOzXSlice);       // 42 KB
+constexpr int kOzXOff = kOzS * kOzASlice;                       // X slices after the A slices
+constexpr int kOzSmem = 1024 + kOzF * kOzF64Bytes + kOzI * kOzIStage + 256;
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
+    uint32_t ok;
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+        "selp.u32 %0, 1, 0, p;\n"
+        "}\n"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+    return ok != 0;
+}
+// Bounded wait: a pipeline bug traps (launch error) after ~4 s instead of hanging the GPU.
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    if (mbar_try_wait(bar, parity)) return;
+    const long long t0 = clock64();
+    while (!mbar_try_wait(bar, parity))
+        if (clock64() - t0 > 8000000000LL) __trap();
+}
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* tm, int c0, int c1, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];\n" ::"r"(
+            smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(tm)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+        : "memory");
+}
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory"); }
+
+// K-major SWIZZLE_32B operand: rows of 32 bytes (32 int8 k), 8-row groups 256 B apart; the
+// 16-byte half of row r holding k in [16c, 16c + 16) sits at half c ^ ((r >> 2) & 1).
+__device__ __forceinline__ uint64_t sdesc_sw32(uint32_t saddr) {
+    uint64_t d = uint64_t((saddr & 0x3FFFFu) >> 4);
+    d |= uint64_t(1) << 16;                  // LBO (unused by swizzled K-major)
+    d |= uint64_t(256 >> 4) << 32;           // SBO: 8 rows x 32 B
+    d |= uint64_t(1) << 46;                  // Blackwell descriptor version
+    d |= uint64_t(6) << 61;                  // SWIZZLE_32B
+    return d;
+}
+// Instruction descriptor, kind::i8: D s32, A/B u8 (0) or s8 (1), both K-major, M = 128, N = n.
+__device__ __forceinline__ uint32_t idesc_i8(bool a_signed, bool b_signed, int n) {
+    return (2u << 4) | (uint32_t(a_signed) << 7) | (uint32_t(b_signed) << 10) | (uint32_t(n >> 3) << 17) |
+           (uint32_t(kOzBM >> 4) << 24);
+}
+__device__ __forceinline__ void mma_i8(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
+                                       uint32_t accum) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "setp.ne.b32 p, %4, 0;\n"
+        "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n"
+        "}\n" ::"r"(d_tmem),
+        "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accum)
+        : "memory");
+}
+__device__ __forceinline__ void mma_commit(uint64_t* bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(smem_u32(bar))
+                 : "memory");
+}
+__device__ __forceinline__ void tmem_ld8(uint32_t taddr, uint32_t (&v)[8]) {
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];\n"
+                 : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7])
+                 : "r"(taddr)
+                 : "memory");
+}
+
+// 2^e as a double for e in [-1022, 1023].
+__device__ __forceinline__ double pow2(int e) { return __longlong_as_double(int64_t(e + 1023) << 52); }
+
+// Exponent E with max |x| < 2^E from the largest biased exponent field be of a group (0 for an
+// all-zero group); clamped so the conversion scale 2^(55 - E) stays finite.
+__host__ __device__ __forceinline__ int oz_exp_from_biased(int be) {
+    if (be <= 0) return 0;                      // all zero (or denormal): any scale works
+    const int e = be - 1022;                    // x = m·2^(be-1023), m in [1,2) -> x < 2^(be-1022)
+    return e < -960 ? -960 : (e > 1023 ? 1023 : e);
+}
+
+struct OzArgs {
+    int64_t Mo, K;
+    int N;
+    int nch;
+    int n0[kOzMaxChunks], nc[kOzMaxChunks];
+    int xrows;          // rows per slice in the X slice buffer
+    int mtiles;
+    int kt_per_split;   // stages per split
+    double* C;
+    int64_t ldc;
+    int64_t split_stride;  // > 0: split partials at C + split * split_stride, ld = N
+    const int* eA;      // per output row: E_i
+    const int* eX;      // per column of X: F_j
+};
+
+template <bool TRANS>
+__global__ void __launch_bounds__(kOzThreads, 1)
+    k_apass_oz(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmX, const OzArgs p) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    unsigned char* sm = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    unsigned char* fring = sm;
+    unsigned char* iring = sm + kOzF * kOzF64Bytes;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(iring + kOzI * kOzIStage);
+    uint64_t* f_full = bars;
+    uint64_t* f_empty = bars + kOzF;
+    uint64_t* x_full = bars + 2 * kOzF;
+    uint64_t* a_full = x_full + kOzI;
+    uint64_t* i_empty = a_full + kOzI;
+    uint64_t* acc_full = i_empty + kOzI;
+    uint64_t* acc_empty = acc_full + 1;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 1);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    int bid = blockIdx.x;
+    const int chunk = bid % p.nch;
+    bid /= p.nch;
+    const int mt = bid % p.mtiles;
+    const int split = bid / p.mtiles;
+    const int n0 = p.n0[chunk], nc = p.nc[chunk];
+    const int64_t m0 = int64_t(mt) * kOzBM;
+    const int64_t ktiles = (p.K + kOzBK - 1) / kOzBK;
+    const int64_t kt0 = int64_t(split) * p.kt_per_split;
+    const int nk = int((ktiles < kt0 + p.kt_per_split ? ktiles : kt0 + p.kt_per_split) - kt0);
+
+    if (warp == 0 && lane == 0) {
+        for (int s = 0; s < kOzF; ++s) {
+            mbar_init(&f_full[s], 1);
+            mbar_init(&f_empty[s], 8);
+        }
+        for (int s = 0; s < kOzI; ++s) {
+            mbar_init(&x_full[s], 1);
+            mbar_init(&a_full[s], 8);
+            mbar_init(&i_empty[s], 1);
+        }
+        mbar_init(acc_full, 1);
+        mbar_init(acc_empty, 8);
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+        asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
+        asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&tmX)) : "memory");
+    }
+    if (warp == 2) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;\n" ::"r"(smem_u32(tmem_slot))
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n" ::: "memory");
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+
+    if (warp == 0) {
+        // ===== TMA producer =====
+        for (int i = 0; i < nk; ++i) {
+            const int fs = i % kOzF, is = i % kOzI;
+            const int k0 = int((kt0 + i) * kOzBK);
+            if (i >= kOzF) mbar_wait(&f_empty[fs], ((i / kOzF) - 1) & 1);
+            if (lane == 0) {
+                unsigned char* dst = fring + fs * kOzF64Bytes;
+                mbar_expect_tx(&f_full[fs], uint32_t(kOzF64Bytes));
+                if constexpr (!TRANS) {
+                    tma_load_2d(dst, &tmA, k0, int(m0), &f_full[fs]);
+                    tma_load_2d(dst + kOzF64Bytes / 2, &tmA, k0 + 16, int(m0), &f_full[fs]);
+                } else {
+                    tma_load_2d(dst, &tmA, int(m0), k0, &f_full[fs]);
+                }
+            }
+            __syncwarp();
+            if (i >= kOzI) mbar_wait(&i_empty[is], ((i / kOzI) - 1) & 1);
+            if (lane == 0) {
+                unsigned char* xs = iring + is * kOzIStage + kOzXOff;
+                mbar_expect_tx(&x_full[is], uint32_t(kOzS * kOzXSlice));
+                for (int t = 0; t < kOzS; ++t) tma_load_2d(xs + t * kOzXSlice, &tmX, k0, t * p.xrows + n0, &x_full[is]);
+            }
+            __syncwarp();
+        }
+    } else if (warp == 1) {
+        // ===== MMA issuer =====
+        for (int i = 0; i < nk; ++i) {
+            const int is = i % kOzI;
+            const uint32_t ph = (i / kOzI) & 1;
+            const int ci = i / kOzChunkStages;
+            const bool first = (i % kOzChunkStages) == 0;
+            if (first && ci > 0) mbar_wait(acc_empty, (ci - 1) & 1);
+            mbar_wait(&x_full[is], ph);
+            mbar_wait(&a_full[is], ph);
+            tc_fence_after();
+            if (lane == 0) {
+                const uint32_t ab = smem_u32(iring + is * kOzIStage);
+                const uint32_t xb = ab + kOzXOff;
+#pragma unroll
+                for (int L = 0; L < kOzS; ++L) {
+#pragma unroll
+                    for (int s = 0; s <= L; ++s) {
+                        const int t = L - s;
+                        mma_i8(tmem + uint32_t(L * kOzLevelCols), sdesc_sw32(ab + s * kOzASlice),
+                               sdesc_sw32(xb + t * kOzXSlice), idesc_i8(s == 0, t == 0, nc),
+                               (first && s == 0) ? 0u : 1u);
+                    }
+                }
+                mma_commit(&i_empty[is]);
+                if ((i % kOzChunkStages) == kOzChunkStages - 1 || i == nk - 1) mma_commit(acc_full);
+            }
+            __syncwarp();
+        }
+    } else if (warp >= 4) {
+        // ===== converters, then the flushes =====
+        const int cw = warp - 4, q = cw & 3, h = cw >> 2;
+        const int r = q * 32 + lane;
+        const int64_t row = m0 + r;
+        const int E = row < p.Mo ? p.eA[row] : 0;
+        const double sc = pow2(55 - E);
+        const uint32_t lane_base = uint32_t(q * 32) << 16;
+        const int half = nc >> 1;
+        int nflush = 0;
+        for (int i = 0; i < nk; ++i) {
+            const int fs = i % kOzF, is = i % kOzI;
+            mbar_wait(&f_full[fs], (i / kOzF) & 1);
+            double v[16];
+            const unsigned char* ft = fring + fs * kOzF64Bytes;
+            if constexpr (!TRANS) {
+                // box h: 128 rows x 16 doubles, SW128: 16-byte chunk c of row r at c ^ (r & 7)
+                const unsigned char* rowp = ft + h * (kOzF64Bytes / 2) + r * 128;
+#pragma unroll
+                for (int c = 0; c < 8; ++c) {
+                    const double2 d2 = *reinterpret_cast<const double2*>(rowp + ((c ^ (r & 7)) << 4));
+                    v[2 * c] = d2.x;
+                    v[2 * c + 1] = d2.y;
+                }
+            } else {
+                const double* col = reinterpret_cast<const double*>(ft) + (16 * h) * kOzBM + r;
+#pragma unroll
+                for (int j = 0; j < 16; ++j) v[j] = col[j * kOzBM];
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&f_empty[fs]);
+            uint32_t lo[16], hi[16];
+#pragma unroll
+            for (int j = 0; j < 16; ++j) {
+                const long long w = __double2ll_rn(v[j] * sc);
+                lo[j] = uint32_t(w);
+                hi[j] = uint32_t(uint64_t(w) >> 32);
+            }
+            if (i >= kOzI) mbar_wait(&i_empty[is], ((i / kOzI) - 1) & 1);
+            unsigned char* as = iring + is * kOzIStage + r * 32 + ((h ^ ((r >> 2) & 1)) << 4);
+#pragma unroll
+            for (int s = 0; s < kOzS; ++s) {
+                const int b = 6 - s;  // byte of V holding slice s
+                uint32_t w4[4];
+#pragma unroll
+                for (int g = 0; g < 4; ++g) {
+                    const uint32_t* src = b < 4 ? lo : hi;
+                    const uint32_t bb = uint32_t(b & 3);
+                    const uint32_t t01 = __byte_perm(src[4 * g], src[4 * g + 1], bb | ((bb + 4) << 4));
+                    const uint32_t t23 = __byte_perm(src[4 * g + 2], src[4 * g + 3], bb | ((bb + 4) << 4));
+                    w4[g] = __byte_perm(t01, t23, 0x5410);
+                }
+                *reinterpret_cast<uint4*>(as + s * kOzASlice) = make_uint4(w4[0], w4[1], w4[2], w4[3]);
+            }
+            asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&a_full[is]);
+            if ((i % kOzChunkStages) == kOzChunkStages - 1 || i == nk - 1) {
+                // ---- flush: fp64 += sum_L acc_L 2^(-8L) · 2^(E + F_j - 14) ----
+                mbar_wait(acc_full, nflush & 1);
+                tc_fence_after();
+                double* out;
+                if (p.split_stride > 0)
+                    out = p.C + split * p.split_stride + row * p.N;
+                else
+                    out = p.C + row * p.ldc;
+                for (int cb = h * half; cb < (h + 1) * half; cb += 8) {
+                    uint32_t acc[kOzS][8];
+#pragma unroll
+                    for (int L = 0; L < kOzS; ++L) tmem_ld8(tmem + lane_base + uint32_t(L * kOzLevelCols + cb), acc[L]);
+                    asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) {
+                        const int col = n0 + cb + j;
+                        double s = double(int(acc[kOzS - 1][j]));
+#pragma unroll
+                        for (int L = kOzS - 2; L >= 0; --L) s = fma(s, 0.00390625, double(int(acc[L][j])));
+                        if (row < p.Mo && col < p.N && cb + j < nc) {
+                            const int ex = E + p.eX[col] - 14;
+                            // s · 2^ex in two exact steps (ex may leave the normal range of one factor)
+                            const double val = (s * pow2(ex >> 1)) * pow2(ex - (ex >> 1));
+                            out[col] = nflush == 0 ? val : out[col] + val;
+                        }
+                    }
+                }
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(acc_empty);
+                ++nflush;
+            }
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 2) {
+        tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;\n" ::"r"(tmem) : "memory");
+    }
+}
+
+// ---- exponents --------------------------------------------------------------------------------
+__device__ __forceinline__ int biased_exp(double x) { return int((__double_as_longlong(x) >> 52) & 0x7ff); }
+
+// Per-row and per-column maxima of the biased exponent field of A (rows x cols, lda): a CTA
+// owns a 32-row x 256-column tile (thread = column, coalesced rows); integer atomicMax, so the
+// result does not depend on the schedule.
+__global__ void __launch_bounds__(256) k_oz_aexp(const double* __restrict__ A, int64_t lda, int64_t rows, int64_t cols,
+                                                 int* __restrict__ erow, int* __restrict__ ecol) {
+    __shared__ int srow[32];
+    const int64_t c = int64_t(blockIdx.x) * 256 + threadIdx.x;
+    const int64_t r0 = int64_t(blockIdx.y) * 32;
+    if (threadIdx.x < 32) srow[threadIdx.x] = 0;
+    __syncthreads();
+    int cmax = 0;
+    const int lane = threadIdx.x & 31;
+    for (int rr = 0; rr < 32; ++rr) {
+        const int64_t r = r0 + rr;
+        int be = 0;
+        if (r < rows && c < cols) be = biased_exp(A[r * lda + c]);
+        be = be == 0x7ff ? 0x7fe : be;  // inf / nan: clamp (the host entry rejects them anyway)
+        cmax = max(cmax, be);
+        const int wm = __reduce_max_sync(0xffffffffu, unsigned(be));
+        if (lane == 0) atomicMax(&srow[rr], wm);
+    }
+    if (c < cols) atomicMax(&ecol[c], cmax);
+    __syncthreads();
+    if (threadIdx.x < 32 && r0 + threadIdx.x < rows) atomicMax(&erow[r0 + threadIdx.x], srow[threadIdx.x]);
+}
+
+__global__ void k_oz_finish_exp(int* __restrict__ e, int64_t n) {
+    for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x)
+        e[i] = oz_exp_from_biased(e[i]);
+}
+
+// Per-column maxima of the biased exponent of X (K x N, ldx).
+__global__ void __launch_bounds__(256) k_oz_xexp(const double* __restrict__ X, int64_t ldx, int64_t K, int N,
+                                                 int* __restrict__ fmax) {
+    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+    const int c = blockIdx.x * 32 + tx;
+    int m = 0;
+    for (int64_t k = int64_t(blockIdx.y) * 8 + ty; k < K; k += int64_t(gridDim.y) * 8)
+        if (c < N) m = max(m, biased_exp(X[k * ldx + c]));
+    if (c < N) atomicMax(&fmax[c], m == 0x7ff ? 0x7fe : m);
+}
+
+// X (K x N) -> 7 digit slices, K-major: Xs[(s·xrows + n)·ldk + k] = digit s of W_kn,
+// W = rint(x · 2^(55 - F_n)); zero for n >= N and k >= K. 32(k) x 32(n) tiles through smem;
+// a thread converts 4 consecutive k of one column and stores one 32-bit word per slice.
+__global__ void __launch_bounds__(256) k_oz_split_x(const double* __restrict__ X, int64_t ldx, int64_t K, int N,
+                                                    const int* __restrict__ fexp, int xrows, int64_t ldk,
+                                                    uint8_t* __restrict__ Xs) {
+    __shared__ double tile[32][33];
+    const int64_t k0 = int64_t(blockIdx.x) * 32;
+    const int nb = blockIdx.y * 32;
+    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+    for (int rr = ty; rr < 32; rr += 8) {
+        const int64_t k = k0 + rr;
+        const int n = nb + tx;
+        tile[rr][tx] = (k < K && n < N) ? X[k * ldx + n] : 0.0;
+    }
+    __syncthreads();
+    const int n = nb + (threadIdx.x >> 3), kg = threadIdx.x & 7;
+    if (n >= xrows) return;
+    const double sc = n < N ? pow2(55 - fexp[n]) : 0.0;
+    uint32_t lo[4], hi[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        const long long w = __double2ll_rn(tile[4 * kg + j][n - nb] * sc);
+        lo[j] = uint32_t(w);
+        hi[j] = uint32_t(uint64_t(w) >> 32);
+    }
+    const int64_t k = k0 + 4 * kg;
+    if (k >= ldk) return;
+#pragma unroll
+    for (int s = 0; s < kOzS; ++s) {
+        const int b = 6 - s;
+        const uint32_t* src = b < 4 ? lo : hi;
+        const uint32_t bb = uint32_t(b & 3);
+        const uint32_t t01 = __byte_perm(src[0], src[1], bb | ((bb + 4) << 4));
+        const uint32_t t23 = __byte_perm(src[2], src[3], bb | ((bb + 4) << 4));
+        *reinterpret_cast<uint32_t*>(Xs + (int64_t(s) * xrows + n) * ldk + k) = __byte_perm(t01, t23, 0x5410);
+    }
+}
+
+__global__ void k_oz_finish_xexp(int* __restrict__ f, int N) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < N) f[i] = oz_exp_from_biased(f[i]);
+}
+
+__global__ void k_oz_reduce(const double* __restrict__ P, int64_t split_stride, int splits, double* __restrict__ C,
+                            int64_t ldc, int64_t rows, int N) {
+    const int64_t total = rows * N;
+    for (int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < total; e += int64_t(gridDim.x) * blockDim.x) {
+        double s = P[e];
+        for (int k = 1; k < splits; ++k) s += P[k * split_stride + e];
+        C[(e / N) * ldc + e % N] = s;
+    }
+}
+
+// ---- host side ----------------------------------------------------------------------------------
+PFN_cuTensorMapEncodeTiled_v12000 oz_encode_fn() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    });
+    return fn;
+}
+
+bool oz_map(CUtensorMap* m, CUtensorMapDataType dt, const void* base, const cuuint64_t* dims, cuuint64_t stride_bytes,
+            const cuuint32_t* box, CUtensorMapSwizzle sw) {
+    auto fn = oz_encode_fn();
+    if (!fn) return false;
+    const cuuint64_t str[1] = {stride_bytes};
+    const cuuint32_t es[2] = {1, 1};
+    return fn(m, dt, 2, const_cast<void*>(base), dims, str, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, sw,
+              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+struct OzShape {
+    int nch, n0[kOzMaxChunks], nc[kOzMaxChunks], xrows;
+    int mtiles, splits, kt_per_split;
+    int64_t ldk;
+};
+
+OzShape oz_shape(int64_t Mo, int64_t K, int N, int num_sms) {
+    OzShape s{};
+    const int n16 = (N + 15) / 16 * 16;
+    s.nch = (n16 + kOzNcMax - 1) / kOzNcMax;
+    const int units = n16 / 16;  // 16-column units spread over the chunks, larger chunks first
+    int at = 0;
+    for (int c = 0; c < s.nch; ++c) {
+        const int u = units / s.nch + (c < units % s.nch ? 1 : 0);
+        s.n0[c] = at;
+        s.nc[c] = 16 * u;
+        at += 16 * u;
+    }
+    s.xrows = n16;
+    s.ldk = (K + 15) / 16 * 16;
+    s.mtiles = int((Mo + kOzBM - 1) / kOzBM);
+    const int64_t ktiles = (K + kOzBK - 1) / kOzBK;
+    const int64_t base = int64_t(s.mtiles) * s.nch;
+    double best = 1e30;
+    int best_s = 1;
+    const int max_s = int(std::max<int64_t>(1, std::min<int64_t>(ktiles / 64, 32)));
+    for (int sp = 1; sp <= max_s; ++sp) {
+        const double waves = std::ceil(double(base * sp) / num_sms);
+        const double cost = waves / sp + (sp > 1 ? 0.02 : 0.0);
+        if (cost < best - 1e-12) {
+            best = cost;
+            best_s = sp;
+        }
+    }
+    s.kt_per_split = int((ktiles + best_s - 1) / best_s);
+    s.splits = int((ktiles + s.kt_per_split - 1) / s.kt_per_split);
+    return s;
+}
+
+size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+}  // namespace
+
+bool gemm_oz_eligible(int64_t Mo, int64_t K, int N) {
+    return N >= 1 && N <= kOzMaxChunks * kOzNcMax && Mo >= kOzBM && K >= 8 * kOzBK && K < (int64_t(1) << 31) &&
+           Mo < (int64_t(1) << 31);
+}
+
+bool gemm_oz_supported(Op op, const double* A, int64_t lda, int64_t Mo, int64_t K, int N) {
+    (void)op;
+    if (!oz_encode_fn() || !gemm_oz_eligible(Mo, K, N)) return false;
+    return (lda * 8) % 16 == 0 && (reinterpret_cast<uintptr_t>(A) & 15) == 0;
+}
+
+size_t gemm_oz_ws_bytes(int64_t Mo, int64_t K, int N, int num_sms) {
+    const OzShape s = oz_shape(Mo, K, N, num_sms);
+    size_t b = align_up(size_t(kOzS) * s.xrows * size_t(s.ldk), 256);  // X slices
+    b += align_up(sizeof(int) * size_t(N), 256);                        // X exponents
+    if (s.splits > 1) b += sizeof(double) * size_t(s.splits) * size_t(Mo) * size_t(N);
+    return b + 256;
+}
+
+cudaError_t gemm_oz_exponents(const double* A, int64_t lda, int64_t rows, int64_t cols, int* erow, int* ecol,
+                              cudaStream_t st) {
+    cudaError_t e = cudaMemsetAsync(erow, 0, sizeof(int) * size_t(rows), st);
+    if (e == cudaSuccess) e = cudaMemsetAsync(ecol, 0, sizeof(int) * size_t(cols), st);
+    if (e != cudaSuccess) return e;
+    const dim3 grid(unsigned((cols + 255) / 256), unsigned((rows + 31) / 32));
+    k_oz_aexp<<<grid, 256, 0, st>>>(A, lda, rows, cols, erow, ecol);
+    k_oz_finish_exp<<<int(std::min<int64_t>((rows + 255) / 256, 1184)), 256, 0, st>>>(erow, rows);
+    k_oz_finish_exp<<<int(std::min<int64_t>((cols + 255) / 256, 1184)), 256, 0, st>>>(ecol, cols);
+    return cudaGetLastError();
+}
+
+cudaError_t gemm_oz(Op op, const double* A, int64_t lda, const int* eA, const double* X, int64_t ldx, double* C,
+                    int64_t ldc, int64_t Mo, int64_t K, int N, void* ws, int num_sms, cudaStream_t st) {
+    const OzShape s = oz_shape(Mo, K, N, num_sms);
+    unsigned char* w = static_cast<unsigned char*>(ws);
+    uint8_t* xs = w;
+    w += align_up(size_t(kOzS) * s.xrows * size_t(s.ldk), 256);
+    int* fx = reinterpret_cast<int*>(w);
+    w += align_up(sizeof(int) * size_t(N), 256);
+    double* part = reinterpret_cast<double*>(w);
+    cudaError_t e = cudaMemsetAsync(fx, 0, sizeof(int) * size_t(N), st);
+    if (e != cudaSuccess) return e;
+    {
+        const int gy = int(std::max<int64_t>(1, std::min<int64_t>((K + 7) / 8, 1184 / ((N + 31) / 32) + 1)));
+        k_oz_xexp<<<dim3(unsigned((N + 31) / 32), unsigned(gy)), 256, 0, st>>>(X, ldx, K, N, fx);
+        k_oz_finish_xexp<<<(N + 255) / 256, 256, 0, st>>>(fx, N);
+        const dim3 grid(unsigned((s.ldk + 31) / 32), unsigned((s.xrows + 31) / 32));
+        k_oz_split_x<<<grid, 256, 0, st>>>(X, ldx, K, N, fx, s.xrows, s.ldk, xs);
+        e = cudaGetLastError();
+        if (e != cudaSuccess) return e;
+    }
+    CUtensorMap ta, tx;
+    if (op == Op::N) {
+        const cuuint64_t dims[2] = {cuuint64_t(K), cuuint64_t(Mo)};
+        const cuuint32_t box[2] = {16, kOzBM};
+        if (!oz_map(&ta, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, A, dims, cuuint64_t(lda) * 8, box, CU_TENSOR_MAP_SWIZZLE_128B))
+            return cudaErrorInvalidValue;
+    } else {
+        const cuuint64_t dims[2] = {cuuint64_t(Mo), cuuint64_t(K)};
+        const cuuint32_t box[2] = {kOzBM, kOzBK};
+        if (!oz_map(&ta, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, A, dims, cuuint64_t(lda) * 8, box, CU_TENSOR_MAP_SWIZZLE_NONE))
+            return cudaErrorInvalidValue;
+    }
+    {
+        const cuuint64_t dims[2] = {cuuint64_t(K), cuuint64_t(kOzS) * cuuint64_t(s.xrows)};
+        const cuuint32_t box[2] = {kOzBK, kOzNcMax};
+        if (!oz_map(&tx, CU_TENSOR_MAP_DATA_TYPE_UINT8, xs, dims, cuuint64_t(s.ldk), box, CU_TENSOR_MAP_SWIZZLE_32B))
+            return cudaErrorInvalidValue;
+    }
+    OzArgs a{};
+    a.Mo = Mo;
+    a.K = K;
+    a.N = N;
+    a.nch = s.nch;
+    for (int c = 0; c < kOzMaxChunks; ++c) {
+        a.n0[c] = s.n0[c];
+        a.nc[c] = s.nc[c];
+    }
+    a.xrows = s.xrows;
+    a.mtiles = s.mtiles;
+    a.kt_per_split = s.kt_per_split;
+    a.C = s.splits > 1 ? part : C;
+    a.ldc = ldc;
+    a.split_stride = s.splits > 1 ? Mo * N : 0;
+    a.eA = eA;
+    a.eX = fx;
+    const unsigned grid = unsigned(int64_t(s.nch) * s.mtiles * s.splits);
+    if (op == Op::N) {
+        allow_max_smem(k_apass_oz<false>);
+        k_apass_oz<false><<<grid, kOzThreads, kOzSmem, st>>>(ta, tx, a);
+    } else {
+        allow_max_smem(k_apass_oz<true>);
+        k_apass_oz<true><<<grid, kOzThreads, kOzSmem, st>>>(ta, tx, a);
+    }
+    e = cudaGetLastError();
+    if (e != cudaSuccess || s.splits == 1) return e;
+    const int64_t total = Mo * N;
+    const int blocks = int(std::min<int64_t>((total + 255) / 256, int64_t(num_sms) * 8));
+    k_oz_reduce<<<blocks, 256, 0, st>>>(part, Mo * N, s.splits, C, ldc, Mo, N);
+    return cudaGetLastError();
+}
+
+int gemm_oz_launches(int64_t Mo, int64_t K, int N, int num_sms) {
+    return 4 + (oz_shape(Mo, K, N, num_sms).splits > 1 ? 1 : 0);
+}
+
+}  // namespace coru_gpu

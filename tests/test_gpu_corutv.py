@@ -64,7 +64,7 @@ def test_reference_cases(ctx, case):
         # reconstruction error within max(1e-10, 10x floor) and never worse, flag where determined.
         from parity_util import parity_record
         assert e_gpu <= 1.5 * e_ref + 1e-13
-        rec, ok = parity_record(a, f, ell, q, ell, threads=4)
+        rec, ok = parity_record(a, f, ell, q, ell, seed=case["seed"], stream=case["stream"], threads=4)
         _record(case["name"], **rec)
         assert ok["err"] and ok["never_worse"] and ok["diag"] and ok["flag"], rec
     if case["name"] == "fast_decay_120_q6":
