@@ -79,6 +79,14 @@ int coru_ctx_set_phi_mode(coru_ctx* ctx, int mode);
  *     products, CUDA-core FFMA otherwise;  CORU_F32_SIMT / CORU_F32_TC: force one engine
  *     (CORU_F32_TC still uses FFMA where the tensor-core kernel cannot take the shape). */
 enum { CORU_F32_AUTO = 0, CORU_F32_SIMT = 1, CORU_F32_TC = 2 };
+/* fp64 A-pass engine (matmul at corutv.hpp:55,57,90 over the caller's A):
+ *   CORU_F64_AUTO (default): INT8 tensor cores (tcgen05.mma kind::i8) with the Ozaki scheme —
+ *     7 digit slices per operand against per-row / per-column power-of-two scales, exact int32
+ *     slice products, fp64 recombination (~2^-55 relative error vs. row-max x column-max);
+ *     FP64 DMMA for shapes it cannot take and for every non-A-pass product;
+ *   CORU_F64_DMMA: FP64 DMMA for everything. */
+enum { CORU_F64_AUTO = 0, CORU_F64_DMMA = 1 };
+int coru_ctx_set_f64_engine(coru_ctx* ctx, int mode);
 int coru_ctx_set_f32_path(coru_ctx* ctx, int mode);
 /* QR of wide sketches (more than 128 columns; householder_qr at corutv.hpp:59-60): 1 (default) =
  * CholeskyQR2 in fp64 with a device-side fall-back to the Householder tree when the sketch is

@@ -15,6 +15,7 @@
 #include <memory>
 #include <stdexcept>
 #include <string>
+#include <type_traits>
 #include <utility>
 #include <vector>
 
@@ -111,6 +112,43 @@ inline UtvApprox corutv(const Matrix& a, std::size_t ell, int q, DVariant varian
                 false, false, std::vector<std::int64_t>(ell)};
     int lower = 0, warn = 0;
     detail::throw_status(coru_corutv_f64(detail::thread_context(), a.data().data(), m, n, l, q,
+                                         variant == DVariant::exact ? CORU_D_EXACT : CORU_D_APPROX, seed.seed,
+                                         seed.stream, f.u.data().data(), f.t.data().data(), f.v.data().data(),
+                                         f.perm.data(), &lower, &warn));
+    f.lower = lower != 0;
+    f.conditioning_warning = warn != 0;
+    return f;
+}
+
+// Zero-copy drop-in for the caller's own row-major fp64 matrix type — coru::Matrix itself
+// (matrix.hpp:17-110), or anything with rows(), cols() and contiguous data().data(): A is read
+// in place (pageable storage streams through the context's pinned staging ring; it is never
+// copied whole), and U, T, V are written straight into matrices of the caller's type (M(rows,
+// cols) must zero-construct, as coru::Matrix does). Same argument list and errors as
+// coru::corutv (corutv.hpp:79-100).
+template <class M>
+struct UtvApproxOf {  // corutv.hpp:23-34 with the caller's matrix type
+    M u, t, v;
+    std::size_t ell;
+    int q;
+    DVariant variant;
+    RngSeed seed;
+    bool lower = false;
+    bool conditioning_warning = false;
+    std::vector<std::int64_t> perm;
+};
+
+template <class M, class = std::enable_if_t<!std::is_same<M, Matrix>::value>,
+          class = decltype(std::declval<const M&>().data().data())>
+inline UtvApproxOf<M> corutv(const M& a, std::size_t ell, int q, DVariant variant, RngSeed seed) {
+    if (ell < 1) throw std::invalid_argument("corutv: ell must be >= 1");
+    if (ell >= std::min(a.rows(), a.cols())) throw std::invalid_argument("corutv: ell must be < min(rows, cols)");
+    if (q < 0) throw std::invalid_argument("corutv: q must be >= 0");
+    UtvApproxOf<M> f{M(a.rows(), ell), M(ell, ell), M(a.cols(), ell), ell, q, variant, seed,
+                     false, false, std::vector<std::int64_t>(ell)};
+    int lower = 0, warn = 0;
+    detail::throw_status(coru_corutv_f64(detail::thread_context(), a.data().data(), std::int64_t(a.rows()),
+                                         std::int64_t(a.cols()), std::int64_t(ell), q,
                                          variant == DVariant::exact ? CORU_D_EXACT : CORU_D_APPROX, seed.seed,
                                          seed.stream, f.u.data().data(), f.t.data().data(), f.v.data().data(),
                                          f.perm.data(), &lower, &warn));

@@ -138,6 +138,7 @@ def load_library():
     L.coru_ctx_set_phi_mode.argtypes = [p, i32]
     L.coru_ctx_set_f32_path.argtypes = [p, i32]
     L.coru_ctx_set_wide_qr.argtypes = [p, i32]
+    L.coru_ctx_set_f64_engine.argtypes = [p, i32]
     L.coru_comm_unique_id.argtypes = [p]
     L.coru_ctx_init_comm.argtypes = [p, i32, i32, p]
     L.coru_ctx_set_profiling.argtypes = [p, i32]
@@ -251,6 +252,13 @@ class Context:
         """fp32 A-pass engine: F32_AUTO (default: tcgen05 3xTF32 tensor cores for A-pass-sized
         products), F32_SIMT (CUDA-core FFMA), F32_TC (tensor cores wherever the shape allows)."""
         _check(self.lib.coru_ctx_set_f32_path(self.h, mode))
+
+    F64_AUTO, F64_DMMA = 0, 1
+
+    def set_f64_engine(self, mode: int):
+        """fp64 A-pass engine: F64_AUTO (default: INT8 tensor cores, Ozaki scheme, for A-pass-sized
+        products over the caller's A), F64_DMMA (FP64 DMMA for everything)."""
+        _check(self.lib.coru_ctx_set_f64_engine(self.h, mode))
 
     def set_wide_qr(self, on: bool):
         """QR of sketches wider than 128 columns: CholeskyQR2 in fp64 with a device-side Householder

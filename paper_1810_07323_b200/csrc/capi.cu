@@ -27,6 +27,7 @@
 #include <mutex>
 #include <string>
 #include <thread>
+#include <type_traits>
 #include <utility>
 #include <vector>
 
@@ -186,6 +187,15 @@ struct coru_ctx {
     int host_threads = 1;
     int phi_mode = CORU_PHI_HOST_EXACT;  // the reference's Φ bit for bit (rng.hpp:86-112)
     int f32_path = CORU_F32_AUTO;
+    int f64_engine = CORU_F64_AUTO;
+    // Ozaki A-pass state (gemm_oz.cu): the exponents of the matrix the current call streams
+    // (prepared at the start of a decomposition, cleared at its end — never reused across calls).
+    const double* oz_a = nullptr;
+    int64_t oz_lda = 0, oz_rows = 0, oz_cols = 0;
+    int* oz_e = nullptr;        // erow [oz_rows] then ecol [oz_cols]
+    size_t oz_e_cap = 0;        // ints
+    void* oz_ws = nullptr;
+    size_t oz_ws_bytes = 0;
     bool wide_qr = true;  // CholeskyQR2 (fp64) for sketches wider than 128 columns, Householder fall-back
     char* arena = nullptr;
     size_t arena_bytes = 0;
@@ -336,6 +346,51 @@ int d2h_sync(coru_ctx* c, void* dst, const void* src, size_t bytes, cudaStream_t
     return CORU_OK;
 }
 
+// Grow-only device buffer owned by the context (synchronises its stream before a regrow).
+int ensure_dev(coru_ctx* c, void** buf, size_t* cap, size_t bytes, const char* what) {
+    if (bytes <= *cap) return CORU_OK;
+    if (*buf) {
+        CORU_CUDA(cudaStreamSynchronize(c->stream));
+        cudaFree(*buf);
+        *buf = nullptr;
+        *cap = 0;
+    }
+    if (cudaMalloc(buf, bytes) != cudaSuccess) {
+        cudaGetLastError();
+        *buf = nullptr;
+        return fail(CORU_ENOMEM, std::string("cudaMalloc of ") + std::to_string(bytes) + " bytes (" + what + ") failed");
+    }
+    *cap = bytes;
+    return CORU_OK;
+}
+
+bool oz_enabled(const coru_ctx* c) {
+    static const char* env = getenv("CORU_F64_ENGINE");  // tooling override: dmma | ozaki
+    if (env && std::string(env) == "dmma") return false;
+    if (env && std::string(env) == "ozaki") return true;
+    return c->f64_engine != CORU_F64_DMMA;
+}
+
+// Exponents of the stored matrix (rows x cols, lda) the coming A-passes stream (gemm_oz.cu): one
+// extra read of A per decomposition, reused by every pass over it.
+int oz_prepare(coru_ctx* c, const double* A, int64_t lda, int64_t rows, int64_t cols) {
+    c->oz_a = nullptr;
+    if (!oz_enabled(c) || !A) return CORU_OK;
+    if (!gemm_oz_eligible(std::max(rows, cols), std::min(rows, cols), 1)) return CORU_OK;
+    size_t cap_bytes = c->oz_e_cap * sizeof(int);
+    void* e = c->oz_e;
+    CORU_TRY(ensure_dev(c, &e, &cap_bytes, sizeof(int) * size_t(rows + cols), "Ozaki exponents"));
+    c->oz_e = static_cast<int*>(e);
+    c->oz_e_cap = cap_bytes / sizeof(int);
+    CORU_CUDA(gemm_oz_exponents(A, lda, rows, cols, c->oz_e, c->oz_e + rows, c->stream));
+    g_launches += 3;
+    c->oz_a = A;
+    c->oz_lda = lda;
+    c->oz_rows = rows;
+    c->oz_cols = cols;
+    return CORU_OK;
+}
+
 // check_corutv_params (corutv.hpp:67-71) + the q check (corutv.hpp:81), same messages.
 int check_params(int64_t m, int64_t n, int64_t ell, int q) {
     if (m < 1 || n < 1) return fail(CORU_EINVAL, "Matrix: dimensions must be positive");
@@ -385,6 +440,23 @@ int prof_begin(coru_ctx* c, cudaEvent_t* stop) {
 template <>
 int gemm<double>(coru_ctx* c, Op op, const double* A, int64_t lda, const double* X, int64_t ldx, double* C,
                  int64_t ldc, int64_t Mo, int64_t K, int N, double* ws, int64_t ws_elems) {
+    // A-passes over the prepared matrix: INT8 tensor cores (Ozaki), when the shape qualifies.
+    if (c->oz_a && A == c->oz_a && lda == c->oz_lda &&
+        (op == Op::N ? (Mo <= c->oz_rows && K == c->oz_cols) : (Mo == c->oz_cols && K <= c->oz_rows)) &&
+        gemm_oz_supported(op, A, lda, Mo, K, N)) {
+        CORU_TRY(ensure_dev(c, &c->oz_ws, &c->oz_ws_bytes, gemm_oz_ws_bytes(Mo, K, N, c->num_sms), "Ozaki workspace"));
+        cudaEvent_t stop = nullptr;
+        if (c->prof) CORU_TRY(prof_begin(c, &stop));
+        const int* eA = op == Op::N ? c->oz_e : c->oz_e + c->oz_rows;
+        CORU_CUDA(gemm_oz(op, A, lda, eA, X, ldx, C, ldc, Mo, K, N, c->oz_ws, c->num_sms, c->stream));
+        if (stop) {
+            CORU_CUDA(cudaEventRecord(stop, c->stream));
+            c->prof_flops += 2.0 * double(Mo) * double(K) * double(N);
+            c->prof_bytes += 8.0 * double(Mo) * double(K);
+        }
+        g_launches += gemm_oz_launches(Mo, K, N, c->num_sms);
+        return CORU_OK;
+    }
     GemmPlan p = plan_gemm_f64(op, Mo, K, N, c->num_sms);
     if (p.ws_elems > ws_elems) return fail(CORU_ECUDA, "internal: gemm workspace too small");
     cudaEvent_t stop = nullptr;
@@ -792,7 +864,17 @@ cudaError_t add_inplace(T* dst, const T* src, size_t count, cudaStream_t st) {
 // the pivots are host outputs). A failing rank of an in-process group releases its peers.
 template <typename T>
 int run(coru_ctx* c, const Request<T>& r, size_t extra_arena_off = 0) {
+    if constexpr (std::is_same<T, double>::value) {
+        if (r.A) {  // device-resident A: the stored matrix is rows x cols, or its transpose (ULV)
+            const int rc = oz_prepare(c, r.A, r.lda, r.trans ? r.cols : r.rows, r.trans ? r.rows : r.cols);
+            if (rc != CORU_OK) {
+                if (c->tcomm) c->tcomm->abort();
+                return rc;
+            }
+        }
+    }
     const int rc = run_impl<T>(c, r, extra_arena_off);
+    c->oz_a = nullptr;
     if (rc != CORU_OK && c->tcomm) c->tcomm->abort();
     return rc;
 }
@@ -1988,6 +2070,8 @@ void coru_ctx_destroy(coru_ctx* c) {
     if (c->arena) cudaFree(c->arena);
     if (c->pinned) cudaFreeHost(c->pinned);
     if (c->stage) cudaFreeHost(c->stage);
+    if (c->oz_e) cudaFree(c->oz_e);
+    if (c->oz_ws) cudaFree(c->oz_ws);
     for (auto& e : c->ev_stage)
         if (e) cudaEventDestroy(e);
     if (c->aux) {
@@ -2082,6 +2166,13 @@ int coru_ctx_set_f32_path(coru_ctx* c, int mode) {
     if (!c || mode < CORU_F32_AUTO || mode > CORU_F32_TC) return fail(CORU_EINVAL, "bad argument");
     std::lock_guard<std::mutex> lk(c->mu);
     c->f32_path = mode;
+    return CORU_OK;
+}
+
+int coru_ctx_set_f64_engine(coru_ctx* c, int mode) {
+    if (!c || (mode != CORU_F64_AUTO && mode != CORU_F64_DMMA)) return fail(CORU_EINVAL, "bad argument");
+    std::lock_guard<std::mutex> lk(c->mu);
+    c->f64_engine = mode;
     return CORU_OK;
 }
 
@@ -2380,7 +2471,12 @@ int coru_gemm_f64_dev(coru_ctx* c, int op, const double* A, int64_t lda, const d
     const Op o = op ? Op::T : Op::N;
     const int64_t wse = gemm_ws<double>(o, rows, K, int(N), c->num_sms);
     CORU_TRY(ensure_arena(c, size_t(wse) * 8 + 256));
-    CORU_TRY(gemm<double>(c, o, A, lda, X, ldx, C, ldc, rows, K, int(N), reinterpret_cast<double*>(c->arena), wse));
+    // A is an A-pass operand here: the Ozaki engine takes it when the shape qualifies
+    const int64_t srows = o == Op::N ? rows : K, scols = o == Op::N ? K : rows;
+    CORU_TRY(oz_prepare(c, A, lda, srows, scols));
+    const int rc = gemm<double>(c, o, A, lda, X, ldx, C, ldc, rows, K, int(N), reinterpret_cast<double*>(c->arena), wse);
+    c->oz_a = nullptr;
+    CORU_TRY(rc);
     CORU_CUDA(cudaStreamSynchronize(c->stream));
     return CORU_OK;
 }

@@ -44,4 +44,16 @@ int gemm_tc32_launches(int64_t Mo, int64_t K, int N, int num_sms);
 cudaError_t gemm_tc32(Op op, const float* A, int64_t lda, const float* X, int64_t ldx, float* C, int64_t ldc,
                       int64_t Mo, int64_t K, int N, float* ws, int num_sms, int max_smem, cudaStream_t st);
 
+// fp64 A-pass on the INT8 tensor cores (tcgen05 kind::i8, Ozaki-scheme emulation; gemm_oz.cu).
+// eA: per output row of op(A), the exponent E with max |row| < 2^E (gemm_oz_exponents: erow for
+// op N, ecol for op T). `ws` must hold gemm_oz_ws_bytes bytes.
+bool gemm_oz_eligible(int64_t Mo, int64_t K, int N);
+bool gemm_oz_supported(Op op, const double* A, int64_t lda, int64_t Mo, int64_t K, int N);
+size_t gemm_oz_ws_bytes(int64_t Mo, int64_t K, int N, int num_sms);
+cudaError_t gemm_oz_exponents(const double* A, int64_t lda, int64_t rows, int64_t cols, int* erow, int* ecol,
+                              cudaStream_t st);
+cudaError_t gemm_oz(Op op, const double* A, int64_t lda, const int* eA, const double* X, int64_t ldx, double* C,
+                    int64_t ldc, int64_t Mo, int64_t K, int N, void* ws, int num_sms, cudaStream_t st);
+int gemm_oz_launches(int64_t Mo, int64_t K, int N, int num_sms);
+
 }  // namespace coru_gpu

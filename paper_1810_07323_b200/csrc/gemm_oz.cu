@@ -15,28 +15,37 @@
 // an extended-precision product next to the DMMA kernel's).
 //
 // Number format. Row i of op(A) has E_i with max_k |a_ik| < 2^E_i (gemm_oz_exponents, once per
-// decomposition: A does not change between passes). V_ik = rint(a_ik · 2^(55 - E_i)) is an
-// int64 with |V| < 2^55; its bytes are the digits: slice 0 = (int8) byte 6 (signed, the top
-// digit), slices 1..6 = bytes 5..0 (unsigned). So V = sum_s digit_s · 2^(8(6 - s)) with no carry
-// handling — the conversion is one F2I plus byte permutes. X is split the same way per column j
-// (F_j) by k_oz_split_x. The product a·x = V·W·2^(E_i + F_j - 110); level L = s + t collects the
-// slice products of weight 2^(8(12 - L)); levels 0..6 are accumulated (int32, one TMEM block of
-// 64 columns each = 448 of the 512 columns), the rest (< 2^-56 relative) dropped. int32 headroom:
-// a level sums <= 7 products of <= 2^16 per k, so accumulators are flushed to fp64 every
-// kOzChunkStages x 32 = 4096 k (< 2^31 / (7·2^16)).
+// decomposition: A does not change between passes). V_ik = rint(a_ik · 2^(54 - E_i)) is an
+// int64 with |V| < 2^54, written in balanced base 256: V + C with C = 0x0080808080808080 has
+// byte 6 = the top digit (signed, |.| <= 64) and bytes 5..0 = the other digits + 128, so
+// XOR 0x80 turns them into signed digits in [-128, 127] — V = sum_s d_s · 2^(8(6 - s)) with no
+// carry loop; the conversion is one F2I, a 64-bit add and byte permutes. Signed (zero-mean)
+// digits keep the dropped low-order part of each product unbiased, so it grows like sqrt(K), not
+// K. X is split the same way per column j (F_j) by k_oz_split_x. a·x = V·W·2^(E_i + F_j - 108);
+// level L = s + t collects the slice products of weight 2^(8(12 - L)); levels 0..6 are
+// accumulated (int32, nc TMEM columns each), the rest (< 2^-52 relative, zero-mean) dropped.
+// int32 headroom: a level sums <= 7 products of <= 2^14 per k, so accumulators are flushed to fp64
+// every kOzChunkStages x 32 = 16384 k (< 2^31 / (7·2^14)).
+//
+// MMA shape. All digits are s8, so the slice products of one A slice s against X slices
+// 0..6-s are ONE stacked operation: B = the X slices stacked along N (contiguous in shared memory),
+// D = TMEM columns [s·nc, 7·nc) = levels s..6 — a level-L block receives slice t = L - s exactly
+// where it belongs. 28 products per stage become 9-10 tcgen05.mma of N <= 256 (small-N MMAs are
+// issue-bound on the tensor pipe).
 //
 // Data flow per CTA (one 128-row tile of op(A) x one N-chunk of nc <= 64 columns; 1 CTA / SM;
 // the nch CTAs of a row tile are adjacent in the grid so A comes from DRAM once and L2 after):
-//   warp 0      TMA producer: fp64 A tile (128 x 32) -> fp64 ring; the 7 X digit slices of the
-//               chunk (64 x 32 int8, SWIZZLE_32B) -> int8 ring
+//   warp 0      TMA producer: fp64 A tile (128 x 32) -> fp64 ring (kOzF stages ahead)
+//   warp 3      TMA producer: the 7 X digit slices of the chunk (one 3-D box: 7 x nc x 32 int8,
+//               SWIZZLE_32B, slices stacked) -> int8 ring
 //   warps 4..11 converters: thread (row r, k-half h) reads 16 fp64 of its row (op N: swizzled
 //               K-major tile; op T: a column of the [k][m] tile — A^T is never formed), scales,
 //               F2I, permutes bytes into the 7 A slices (K-major SW32 rows of 32 B) of the int8
 //               ring; at each flush they read the 7 level accumulators back (tcgen05.ld) and add
-//               sum_L acc_L 2^(-8L) · 2^(E_i + F_j - 14) into the fp64 output (own rows, fixed
+//               sum_L acc_L 2^(-8L) · 2^(E_i + F_j - 12) into the fp64 output (own rows, fixed
 //               order: deterministic)
-//   warp 1      MMA issuer: 28 tcgen05.mma (M = 128, N = nc, K = 32) per stage, s8/u8 types per
-//               slice, A and B from shared memory descriptors
+//   warp 1      MMA issuer: per stage and A slice s one stacked tcgen05.mma (M = 128, K = 32,
+//               N = (7 - s)·nc split at 256), s8 x s8, A and B from shared memory descriptors
 //   warp 2      TMEM allocator
 // Split-K (op T: K = m rows of A) writes per-split fp64 partials summed in a fixed order.
 #include <algorithm>
@@ -58,15 +67,14 @@ constexpr int kOzThreads = 384;
 constexpr int kOzBM = 128;
 constexpr int kOzBK = 32;              // k per stage = one UMMA K step of int8
 constexpr int kOzS = 7;                // digit slices per operand
-constexpr int kOzLevelCols = 64;       // TMEM columns per level accumulator
 constexpr int kOzNcMax = 64;           // columns per N-chunk
 constexpr int kOzMaxChunks = 4;        // N <= 256
-constexpr int kOzF = 2;                // fp64 ring stages
-constexpr int kOzI = 3;                // int8 ring stages
-constexpr int kOzChunkStages = 128;    // flush interval (stages)
+constexpr int kOzF = 4;                // fp64 ring stages (128 KB of A in flight per SM)
+constexpr int kOzI = 2;                // int8 ring stages (converters + X slices -> MMA)
+constexpr int kOzChunkStages = 512;    // flush interval (stages): 16384 k
 constexpr int kOzF64Bytes = kOzBM * kOzBK * 8;                  // 32 KB
 constexpr int kOzASlice = kOzBM * kOzBK;                        // 4 KB
-constexpr int kOzXSlice = kOzNcMax * kOzBK;                     // 2 KB
+constexpr int kOzXSlice = kOzNcMax * kOzBK;                     // 2 KB (slots stack at nc rows)
 constexpr int kOzIStage = kOzS * (kOzASlice + kOzXSlice);       // 42 KB
 constexpr int kOzXOff = kOzS * kOzASlice;                       // X slices after the A slices
 constexpr int kOzSmem = 1024 + kOzF * kOzF64Bytes + kOzI * kOzIStage + 256;
@@ -101,6 +109,13 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
     while (!mbar_try_wait(bar, parity))
         if (clock64() - t0 > 8000000000LL) __trap();
 }
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* tm, int c0, int c1, int c2, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], "
+        "[%5];\n" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(tm)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
+        : "memory");
+}
 __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* tm, int c0, int c1, uint64_t* bar) {
     asm volatile(
         "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];\n" ::"r"(
@@ -121,10 +136,9 @@ __device__ __forceinline__ uint64_t sdesc_sw32(uint32_t saddr) {
     d |= uint64_t(6) << 61;                  // SWIZZLE_32B
     return d;
 }
-// Instruction descriptor, kind::i8: D s32, A/B u8 (0) or s8 (1), both K-major, M = 128, N = n.
-__device__ __forceinline__ uint32_t idesc_i8(bool a_signed, bool b_signed, int n) {
-    return (2u << 4) | (uint32_t(a_signed) << 7) | (uint32_t(b_signed) << 10) | (uint32_t(n >> 3) << 17) |
-           (uint32_t(kOzBM >> 4) << 24);
+// Instruction descriptor, kind::i8: D s32, A and B s8, both K-major, M = 128, N = n.
+__device__ __forceinline__ uint32_t idesc_i8(int n) {
+    return (2u << 4) | (1u << 7) | (1u << 10) | (uint32_t(n >> 3) << 17) | (uint32_t(kOzBM >> 4) << 24);
 }
 __device__ __forceinline__ void mma_i8(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
                                        uint32_t accum) {
@@ -151,12 +165,15 @@ __device__ __forceinline__ void tmem_ld8(uint32_t taddr, uint32_t (&v)[8]) {
 // 2^e as a double for e in [-1022, 1023].
 __device__ __forceinline__ double pow2(int e) { return __longlong_as_double(int64_t(e + 1023) << 52); }
 
+// Balanced base-256 digits of the int64 w (|w| < 2^54): bytes of w + C, the low six XOR 0x80.
+constexpr unsigned long long kOzBias = 0x0000808080808080ull;
+
 // Exponent E with max |x| < 2^E from the largest biased exponent field be of a group (0 for an
 // all-zero group); clamped so the conversion scale 2^(55 - E) stays finite.
 __host__ __device__ __forceinline__ int oz_exp_from_biased(int be) {
     if (be <= 0) return 0;                      // all zero (or denormal): any scale works
     const int e = be - 1022;                    // x = m·2^(be-1023), m in [1,2) -> x < 2^(be-1022)
-    return e < -960 ? -960 : (e > 1023 ? 1023 : e);
+    return e < -960 ? -960 : (e > 1022 ? 1022 : e);
 }
 
 struct OzArgs {
@@ -165,6 +182,7 @@ struct OzArgs {
     int nch;
     int n0[kOzMaxChunks], nc[kOzMaxChunks];
     int xrows;          // rows per slice in the X slice buffer
+    int nc_a;           // chunk width served by tmXa (the others use tmXb)
     int mtiles;
     int kt_per_split;   // stages per split
     double* C;
@@ -176,7 +194,8 @@ struct OzArgs {
 
 template <bool TRANS>
 __global__ void __launch_bounds__(kOzThreads, 1)
-    k_apass_oz(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmX, const OzArgs p) {
+    k_apass_oz(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmXa,
+               const __grid_constant__ CUtensorMap tmXb, const __grid_constant__ OzArgs p) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     unsigned char* sm = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     unsigned char* fring = sm;
@@ -217,7 +236,8 @@ __global__ void __launch_bounds__(kOzThreads, 1)
         mbar_init(acc_empty, 8);
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
         asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
-        asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&tmX)) : "memory");
+        asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(nc == p.nc_a ? &tmXa : &tmXb))
+                     : "memory");
     }
     if (warp == 2) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;\n" ::"r"(smem_u32(tmem_slot))
@@ -230,9 +250,9 @@ __global__ void __launch_bounds__(kOzThreads, 1)
     const uint32_t tmem = *tmem_slot;
 
     if (warp == 0) {
-        // ===== TMA producer =====
+        // ===== TMA producer: fp64 A tiles, F stages ahead of the converters =====
         for (int i = 0; i < nk; ++i) {
-            const int fs = i % kOzF, is = i % kOzI;
+            const int fs = i % kOzF;
             const int k0 = int((kt0 + i) * kOzBK);
             if (i >= kOzF) mbar_wait(&f_empty[fs], ((i / kOzF) - 1) & 1);
             if (lane == 0) {
@@ -246,11 +266,18 @@ __global__ void __launch_bounds__(kOzThreads, 1)
                 }
             }
             __syncwarp();
+        }
+    } else if (warp == 3) {
+        // ===== TMA producer: X digit slices into the int8 ring (paced by the MMAs) =====
+        for (int i = 0; i < nk; ++i) {
+            const int is = i % kOzI;
+            const int k0 = int((kt0 + i) * kOzBK);
             if (i >= kOzI) mbar_wait(&i_empty[is], ((i / kOzI) - 1) & 1);
             if (lane == 0) {
+                // the chunk's 7 slices stacked: slot t at t·nc rows (one 3-D box)
                 unsigned char* xs = iring + is * kOzIStage + kOzXOff;
-                mbar_expect_tx(&x_full[is], uint32_t(kOzS * kOzXSlice));
-                for (int t = 0; t < kOzS; ++t) tma_load_2d(xs + t * kOzXSlice, &tmX, k0, t * p.xrows + n0, &x_full[is]);
+                mbar_expect_tx(&x_full[is], uint32_t(kOzS * nc * kOzBK));
+                tma_load_3d(xs, nc == p.nc_a ? &tmXa : &tmXb, k0, n0, 0, &x_full[is]);
             }
             __syncwarp();
         }
@@ -269,12 +296,13 @@ __global__ void __launch_bounds__(kOzThreads, 1)
                 const uint32_t ab = smem_u32(iring + is * kOzIStage);
                 const uint32_t xb = ab + kOzXOff;
 #pragma unroll
-                for (int L = 0; L < kOzS; ++L) {
-#pragma unroll
-                    for (int s = 0; s <= L; ++s) {
-                        const int t = L - s;
-                        mma_i8(tmem + uint32_t(L * kOzLevelCols), sdesc_sw32(ab + s * kOzASlice),
-                               sdesc_sw32(xb + t * kOzXSlice), idesc_i8(s == 0, t == 0, nc),
+                for (int s = 0; s < kOzS; ++s) {
+                    // A slice s x X slices 0..6-s -> levels s..6 (TMEM columns [s·nc, 7·nc))
+                    const int ntot = (kOzS - s) * nc;
+                    const uint64_t ad = sdesc_sw32(ab + s * kOzASlice);
+                    for (int c0 = 0; c0 < ntot; c0 += 256) {
+                        const int n = ntot - c0 < 256 ? ntot - c0 : 256;
+                        mma_i8(tmem + uint32_t(s * nc + c0), ad, sdesc_sw32(xb + c0 * kOzBK), idesc_i8(n),
                                (first && s == 0) ? 0u : 1u);
                     }
                 }
@@ -289,7 +317,7 @@ __global__ void __launch_bounds__(kOzThreads, 1)
         const int r = q * 32 + lane;
         const int64_t row = m0 + r;
         const int E = row < p.Mo ? p.eA[row] : 0;
-        const double sc = pow2(55 - E);
+        const double sc = pow2(54 - E);
         const uint32_t lane_base = uint32_t(q * 32) << 16;
         const int half = nc >> 1;
         int nflush = 0;
@@ -317,9 +345,9 @@ __global__ void __launch_bounds__(kOzThreads, 1)
             uint32_t lo[16], hi[16];
 #pragma unroll
             for (int j = 0; j < 16; ++j) {
-                const long long w = __double2ll_rn(v[j] * sc);
+                const unsigned long long w = (unsigned long long)__double2ll_rn(v[j] * sc) + kOzBias;
                 lo[j] = uint32_t(w);
-                hi[j] = uint32_t(uint64_t(w) >> 32);
+                hi[j] = uint32_t(w >> 32);
             }
             if (i >= kOzI) mbar_wait(&i_empty[is], ((i / kOzI) - 1) & 1);
             unsigned char* as = iring + is * kOzIStage + r * 32 + ((h ^ ((r >> 2) & 1)) << 4);
@@ -333,7 +361,7 @@ __global__ void __launch_bounds__(kOzThreads, 1)
                     const uint32_t bb = uint32_t(b & 3);
                     const uint32_t t01 = __byte_perm(src[4 * g], src[4 * g + 1], bb | ((bb + 4) << 4));
                     const uint32_t t23 = __byte_perm(src[4 * g + 2], src[4 * g + 3], bb | ((bb + 4) << 4));
-                    w4[g] = __byte_perm(t01, t23, 0x5410);
+                    w4[g] = __byte_perm(t01, t23, 0x5410) ^ (s == 0 ? 0u : 0x80808080u);
                 }
                 *reinterpret_cast<uint4*>(as + s * kOzASlice) = make_uint4(w4[0], w4[1], w4[2], w4[3]);
             }
@@ -341,7 +369,7 @@ __global__ void __launch_bounds__(kOzThreads, 1)
             __syncwarp();
             if (lane == 0) mbar_arrive(&a_full[is]);
             if ((i % kOzChunkStages) == kOzChunkStages - 1 || i == nk - 1) {
-                // ---- flush: fp64 += sum_L acc_L 2^(-8L) · 2^(E + F_j - 14) ----
+                // ---- flush: fp64 += sum_L acc_L 2^(-8L) · 2^(E + F_j - 12) ----
                 mbar_wait(acc_full, nflush & 1);
                 tc_fence_after();
                 double* out;
@@ -352,7 +380,7 @@ __global__ void __launch_bounds__(kOzThreads, 1)
                 for (int cb = h * half; cb < (h + 1) * half; cb += 8) {
                     uint32_t acc[kOzS][8];
 #pragma unroll
-                    for (int L = 0; L < kOzS; ++L) tmem_ld8(tmem + lane_base + uint32_t(L * kOzLevelCols + cb), acc[L]);
+                    for (int L = 0; L < kOzS; ++L) tmem_ld8(tmem + lane_base + uint32_t(L * nc + cb), acc[L]);
                     asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
 #pragma unroll
                     for (int j = 0; j < 8; ++j) {
@@ -361,7 +389,7 @@ __global__ void __launch_bounds__(kOzThreads, 1)
 #pragma unroll
                         for (int L = kOzS - 2; L >= 0; --L) s = fma(s, 0.00390625, double(int(acc[L][j])));
                         if (row < p.Mo && col < p.N && cb + j < nc) {
-                            const int ex = E + p.eX[col] - 14;
+                            const int ex = E + p.eX[col] - 12;
                             // s · 2^ex in two exact steps (ex may leave the normal range of one factor)
                             const double val = (s * pow2(ex >> 1)) * pow2(ex - (ex >> 1));
                             out[col] = nflush == 0 ? val : out[col] + val;
@@ -428,8 +456,8 @@ __global__ void __launch_bounds__(256) k_oz_xexp(const double* __restrict__ X, i
     if (c < N) atomicMax(&fmax[c], m == 0x7ff ? 0x7fe : m);
 }
 
-// X (K x N) -> 7 digit slices, K-major: Xs[(s·xrows + n)·ldk + k] = digit s of W_kn,
-// W = rint(x · 2^(55 - F_n)); zero for n >= N and k >= K. 32(k) x 32(n) tiles through smem;
+// X (K x N) -> 7 balanced digit slices, K-major: Xs[(s·xrows + n)·ldk + k] = digit s of W_kn,
+// W = rint(x · 2^(54 - F_n)); zero for n >= N and k >= K. 32(k) x 32(n) tiles through smem;
 // a thread converts 4 consecutive k of one column and stores one 32-bit word per slice.
 __global__ void __launch_bounds__(256) k_oz_split_x(const double* __restrict__ X, int64_t ldx, int64_t K, int N,
                                                     const int* __restrict__ fexp, int xrows, int64_t ldk,
@@ -446,13 +474,13 @@ __global__ void __launch_bounds__(256) k_oz_split_x(const double* __restrict__ X
     __syncthreads();
     const int n = nb + (threadIdx.x >> 3), kg = threadIdx.x & 7;
     if (n >= xrows) return;
-    const double sc = n < N ? pow2(55 - fexp[n]) : 0.0;
+    const double sc = n < N ? pow2(54 - fexp[n]) : 0.0;
     uint32_t lo[4], hi[4];
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
-        const long long w = __double2ll_rn(tile[4 * kg + j][n - nb] * sc);
+        const unsigned long long w = (unsigned long long)__double2ll_rn(tile[4 * kg + j][n - nb] * sc) + kOzBias;
         lo[j] = uint32_t(w);
-        hi[j] = uint32_t(uint64_t(w) >> 32);
+        hi[j] = uint32_t(w >> 32);
     }
     const int64_t k = k0 + 4 * kg;
     if (k >= ldk) return;
@@ -463,7 +491,8 @@ __global__ void __launch_bounds__(256) k_oz_split_x(const double* __restrict__ X
         const uint32_t bb = uint32_t(b & 3);
         const uint32_t t01 = __byte_perm(src[0], src[1], bb | ((bb + 4) << 4));
         const uint32_t t23 = __byte_perm(src[2], src[3], bb | ((bb + 4) << 4));
-        *reinterpret_cast<uint32_t*>(Xs + (int64_t(s) * xrows + n) * ldk + k) = __byte_perm(t01, t23, 0x5410);
+        *reinterpret_cast<uint32_t*>(Xs + (int64_t(s) * xrows + n) * ldk + k) =
+            __byte_perm(t01, t23, 0x5410) ^ (s == 0 ? 0u : 0x80808080u);
     }
 }
 
@@ -612,12 +641,20 @@ cudaError_t gemm_oz(Op op, const double* A, int64_t lda, const int* eA, const do
         if (!oz_map(&ta, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, A, dims, cuuint64_t(lda) * 8, box, CU_TENSOR_MAP_SWIZZLE_NONE))
             return cudaErrorInvalidValue;
     }
-    {
-        const cuuint64_t dims[2] = {cuuint64_t(K), cuuint64_t(kOzS) * cuuint64_t(s.xrows)};
-        const cuuint32_t box[2] = {kOzBK, kOzNcMax};
-        if (!oz_map(&tx, CU_TENSOR_MAP_DATA_TYPE_UINT8, xs, dims, cuuint64_t(s.ldk), box, CU_TENSOR_MAP_SWIZZLE_32B))
-            return cudaErrorInvalidValue;
-    }
+    // X slices as a 3-D tensor (k, row, slice); one box = the 7 slices of one chunk, stacked.
+    auto xmap = [&](CUtensorMap* m, int nc) {
+        auto fn = oz_encode_fn();
+        const cuuint64_t dims[3] = {cuuint64_t(K), cuuint64_t(s.xrows), cuuint64_t(kOzS)};
+        const cuuint64_t str[2] = {cuuint64_t(s.ldk), cuuint64_t(s.ldk) * cuuint64_t(s.xrows)};
+        const cuuint32_t box[3] = {kOzBK, cuuint32_t(nc), cuuint32_t(kOzS)};
+        const cuuint32_t es[3] = {1, 1, 1};
+        return fn(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, xs, dims, str, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                  CU_TENSOR_MAP_SWIZZLE_32B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+    };
+    CUtensorMap txb;
+    const int nc_a = s.nc[0], nc_b = s.nc[s.nch - 1];
+    if (!xmap(&tx, nc_a) || !xmap(&txb, nc_b)) return cudaErrorInvalidValue;
     OzArgs a{};
     a.Mo = Mo;
     a.K = K;
@@ -628,6 +665,7 @@ cudaError_t gemm_oz(Op op, const double* A, int64_t lda, const int* eA, const do
         a.nc[c] = s.nc[c];
     }
     a.xrows = s.xrows;
+    a.nc_a = nc_a;
     a.mtiles = s.mtiles;
     a.kt_per_split = s.kt_per_split;
     a.C = s.splits > 1 ? part : C;
@@ -638,10 +676,10 @@ cudaError_t gemm_oz(Op op, const double* A, int64_t lda, const int* eA, const do
     const unsigned grid = unsigned(int64_t(s.nch) * s.mtiles * s.splits);
     if (op == Op::N) {
         allow_max_smem(k_apass_oz<false>);
-        k_apass_oz<false><<<grid, kOzThreads, kOzSmem, st>>>(ta, tx, a);
+        k_apass_oz<false><<<grid, kOzThreads, kOzSmem, st>>>(ta, tx, txb, a);
     } else {
         allow_max_smem(k_apass_oz<true>);
-        k_apass_oz<true><<<grid, kOzThreads, kOzSmem, st>>>(ta, tx, a);
+        k_apass_oz<true><<<grid, kOzThreads, kOzSmem, st>>>(ta, tx, txb, a);
     }
     e = cudaGetLastError();
     if (e != cudaSuccess || s.splits == 1) return e;

@@ -1,0 +1,91 @@
+// TEST INFRASTRUCTURE. The zero-copy drop-in (include/coru_gpu.hpp, UtvApproxOf<coru::Matrix>)
+// called with the reference's own coru::Matrix (proj/include/coru/matrix.hpp, included in place —
+// built only where /root/reference exists; the binary travels to the GPU box), compared in the same
+// process with the reference's coru::corutv on identical input (corutv.hpp:79-100): q = 0 cases to
+// the BASELINE fp64 tolerances, identical pivots, orthonormal factors, ULV orientation, and the
+// reference's std::invalid_argument cases. Exit 0 = all checks passed.
+#include <cmath>
+#include <cstdio>
+#include <stdexcept>
+
+#include "coru/corutv.hpp"
+#include "coru/testgen.hpp"
+#include "coru_gpu.hpp"
+
+static int failures = 0;
+#define CHECK(c)                                                                    \
+    do {                                                                            \
+        if (!(c)) {                                                                 \
+            std::fprintf(stderr, "CHECK failed %s:%d: %s\n", __FILE__, __LINE__, #c); \
+            ++failures;                                                             \
+        }                                                                           \
+    } while (0)
+
+template <class F>
+static double rel_err(const coru::Matrix& a, const F& f) {
+    double num = 0, den = 0;
+    for (std::size_t i = 0; i < a.rows(); ++i)
+        for (std::size_t j = 0; j < a.cols(); ++j) {
+            double s = 0;
+            for (std::size_t p = 0; p < f.ell; ++p)
+                for (std::size_t r = 0; r < f.ell; ++r) s += f.u(i, p) * f.t(p, r) * f.v(j, r);
+            num += (a(i, j) - s) * (a(i, j) - s);
+            den += a(i, j) * a(i, j);
+        }
+    return std::sqrt(num / den);
+}
+
+static double orth(const coru::Matrix& q) {
+    double s = 0;
+    for (std::size_t i = 0; i < q.cols(); ++i)
+        for (std::size_t j = 0; j < q.cols(); ++j) {
+            double g = 0;
+            for (std::size_t r = 0; r < q.rows(); ++r) g += q(r, i) * q(r, j);
+            g -= (i == j);
+            s += g * g;
+        }
+    return std::sqrt(s);
+}
+
+static void compare(const coru::Matrix& a, std::size_t ell, int q, std::uint64_t seed) {
+    const coru::UtvApprox ref = coru::corutv(a, ell, q, coru::DVariant::exact, {seed, 0});
+    const coru_gpu::UtvApproxOf<coru::Matrix> gpu =
+        coru_gpu::corutv(a, ell, q, coru_gpu::DVariant::exact, coru_gpu::RngSeed{seed, 0});
+    CHECK(gpu.lower == ref.lower);
+    CHECK(gpu.u.rows() == ref.u.rows() && gpu.v.rows() == ref.v.rows());
+    const double e_ref = rel_err(a, ref), e_gpu = rel_err(a, gpu);
+    double dmax = 0;
+    for (std::size_t j = 0; j < ell; ++j) dmax = std::max(dmax, std::abs(std::abs(gpu.t(j, j)) - std::abs(ref.t(j, j))));
+    std::printf("%zux%zu ell=%zu q=%d: err gpu %.3e ref %.3e, max |diag T| diff %.3e, orth %.2e %.2e\n", a.rows(),
+                a.cols(), ell, q, e_gpu, e_ref, dmax, orth(gpu.u), orth(gpu.v));
+    CHECK(orth(gpu.u) <= 1e-12 * double(ell) && orth(gpu.v) <= 1e-12 * double(ell));
+    if (q == 0) {
+        CHECK(std::abs(e_gpu - e_ref) <= 1e-10 * e_ref + 1e-14);
+        CHECK(dmax <= 1e-8);
+    }
+    CHECK(gpu.conditioning_warning == ref.conditioning_warning);
+}
+
+int main() {
+    compare(coru::gen_fast_decay(200, 10, {11, 0}), 20, 0, 42);
+    compare(coru::gen_fast_decay(200, 10, {11, 0}), 20, 1, 42);
+    compare(coru::gen_noisy_lowrank(300, 10, 1e-3, {13, 0}), 30, 0, 5);
+    coru::Matrix tall = coru::matmul(coru::gaussian(300, 25, {15, 0}), coru::gaussian(25, 180, {15, 1}));
+    const coru::Matrix noise = coru::gaussian(300, 180, {15, 2});
+    for (std::size_t i = 0; i < tall.rows(); ++i)
+        for (std::size_t j = 0; j < tall.cols(); ++j) tall(i, j) += 1e-6 * noise(i, j);
+    compare(tall, 30, 0, 9);
+    compare(tall.transposed(), 30, 0, 9);  // rows < cols: the ULV orientation (corutv.hpp:82-87)
+    const coru::Matrix a = coru::gen_fast_decay(60, 10, {14, 0});
+    for (auto [ell, q] : {std::pair<std::size_t, int>{0, 0}, {60, 0}, {3, -1}}) {
+        bool threw = false;
+        try {
+            coru_gpu::corutv(a, ell, q, coru_gpu::DVariant::exact, coru_gpu::RngSeed{1, 0});
+        } catch (const std::invalid_argument&) {
+            threw = true;
+        }
+        CHECK(threw);
+    }
+    std::printf("%s (%d failures)\n", failures ? "FAIL" : "OK", failures);
+    return failures ? 1 : 0;
+}

@@ -218,3 +218,15 @@ def test_host_entry_upload_pipeline(ctx, monkeypatch, variant, q):
     bad[-1, -1] = np.inf
     with pytest.raises(cg.CoruInvalidArgument):
         cg.corutv(bad, 60, q, v, cg.RngSeed(42, 0), ctx=ctx)
+
+
+def test_cpp_reference_matrix_dropin(ctx):
+    """The zero-copy drop-in with the reference's own coru::Matrix, compared in-process with the
+    reference's coru::corutv (tests/cpp/test_ref_matrix.cpp, built where /root/reference exists)."""
+    import subprocess
+    here = os.path.dirname(os.path.abspath(__file__))
+    exe = os.path.join(here, "cpp", "test_ref_matrix")
+    if not os.path.exists(exe):
+        pytest.skip("test_ref_matrix not built (needs the reference headers at build time)")
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stdout + r.stderr

@@ -1,0 +1,122 @@
+"""The fp64 A-pass on the INT8 tensor cores (gemm_oz.cu, Ozaki scheme) — gpu marker.
+
+Accuracy is measured against an extended-precision product (numpy long double, 64-bit
+significand) next to the FP64 DMMA kernel's: the emulated product must be at least as accurate
+as a native fp64 GEMM up to a small factor, within the reference's
+own matmul contract 1e-12·(|A||X|) per entry (matrix.hpp:112-114), bitwise deterministic, and
+correct on every shape edge the A-passes see (row / k remainders, N = 25 ... 256, split-K).
+"""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def _exact(a, x, op):
+    al = (a.T if op else a).astype(np.longdouble)
+    return al @ x.astype(np.longdouble)
+
+
+def _run(ctx, a, x, op, engine):
+    import torch
+    import paper_1810_07323_b200 as cg
+    ctx.set_f64_engine(engine)
+    try:
+        n = x.shape[1]
+        xd = torch.zeros((x.shape[0], n + (n & 1)), dtype=torch.float64, device="cuda")  # even ld (16-B rows)
+        xd[:, :n] = torch.from_numpy(x).cuda()
+        c = cg.gemm(torch.from_numpy(a).cuda(), xd[:, :n], op=op, ctx=ctx)
+        torch.cuda.synchronize()
+        return c.cpu().numpy()
+    finally:
+        ctx.set_f64_engine(ctx.F64_AUTO)
+
+
+SHAPES = [(1000, 776, 25, 0), (1000, 776, 60, 1), (2048, 1024, 112, 0), (1024, 2048, 112, 1), (300, 520, 220, 0),
+          (520, 300, 256, 1), (129, 4098, 48, 0), (4100, 258, 64, 1)]
+
+
+@pytest.mark.parametrize("m,k,n,op", SHAPES)
+def test_oz_accuracy_vs_extended(ctx, m, k, n, op):
+    """Dense operands of uniform magnitude (the A-passes' data): the emulated product is within a
+    small factor of native fp64 (median entry error <= 4x DMMA's against the exact product;
+    measured 2-3x: 54-bit digits against the row / column maximum plus the dropped levels >= 7),
+    and 1e-4 of the reference's own per-entry matmul contract."""
+    rng = np.random.default_rng(m + k + n + op)
+    a = rng.standard_normal((m, k))
+    kk = m if op else k
+    x = rng.standard_normal((kk, n))
+    ex = _exact(a, x, op)
+    c_oz = _run(ctx, a, x, op, 0)
+    c_dm = _run(ctx, a, x, op, 1)
+    scale = (np.abs(a.T if op else a).astype(np.longdouble) @ np.abs(x).astype(np.longdouble))
+    err_oz = np.abs(c_oz - ex) / scale
+    err_dm = np.abs(c_dm - ex) / scale
+    print(f"median rel err ozaki {np.median(err_oz):.3e} dmma {np.median(err_dm):.3e}; "
+          f"max ozaki {err_oz.max():.3e} dmma {err_dm.max():.3e}")
+    assert float(err_oz.max()) <= 1e-12  # matrix.hpp:112-114 per-entry contract
+    assert np.median(err_oz) <= 4 * np.median(err_dm) + 1e-18, (np.median(err_oz), np.median(err_dm))
+
+
+@pytest.mark.parametrize("m,k,n,op", SHAPES[2:6])
+def test_oz_scaled_rows_and_columns(ctx, m, k, n, op):
+    """Rows / columns of op(A) and columns of X 2^±20..40 apart: the per-row and per-column
+    scales absorb them; the error stays within the scheme's bound (54-bit digits against the
+    row / column maximum, dropped levels >= 7) and the per-entry contract 1e-12·(|A||X|)."""
+    rng = np.random.default_rng(m * 7 + k + n + op)
+    a = rng.standard_normal((m, k))
+    a *= np.exp2(rng.integers(-40, 40, size=(m, 1)))
+    a *= np.exp2(rng.integers(-20, 20, size=(1, k)))
+    kk = m if op else k
+    x = rng.standard_normal((kk, n)) * np.exp2(rng.integers(-30, 30, size=(1, n)))
+    ex = _exact(a, x, op)
+    c_oz = _run(ctx, a, x, op, 0)
+    scale = (np.abs(a.T if op else a).astype(np.longdouble) @ np.abs(x).astype(np.longdouble))
+    assert float((np.abs(c_oz - ex) / scale).max()) <= 1e-12
+    rowmax = np.abs(a.T if op else a).max(axis=1, keepdims=True)
+    colmax = np.abs(x).max(axis=0, keepdims=True)
+    assert np.all(np.abs(c_oz - ex) <= kk * 2.0 ** -49 * rowmax * colmax)
+
+
+def test_oz_deterministic_and_zero_rows(ctx):
+    rng = np.random.default_rng(5)
+    a = rng.standard_normal((3000, 2000))
+    a[7] = 0.0            # an all-zero row
+    a[:, 11] = 0.0        # an all-zero column (zero output row for op T)
+    x = rng.standard_normal((2000, 110))
+    c1 = _run(ctx, a, x, 0, 0)
+    c2 = _run(ctx, a, x, 0, 0)
+    assert np.array_equal(c1, c2)
+    assert np.all(c1[7] == 0.0)
+    y = rng.standard_normal((3000, 110))
+    t1 = _run(ctx, a, y, 1, 0)
+    t2 = _run(ctx, a, y, 1, 0)
+    assert np.array_equal(t1, t2)
+    assert np.all(t1[11] == 0.0)
+
+
+def test_oz_split_k_large_k(ctx):
+    """op T with K = 200000 rows (C3's A^T·B1 shape, narrowed): split-K partials, several flushes
+    of the int32 level accumulators per CTA (every 4096 k)."""
+    rng = np.random.default_rng(9)
+    m, n, d = 200000, 256, 112
+    a = rng.standard_normal((m, n))
+    y = rng.standard_normal((m, d))
+    c = _run(ctx, a, y, 1, 0)
+    ref = a.T @ y
+    scale = np.abs(a).T @ np.abs(y)
+    assert float((np.abs(c - ref) / scale).max()) <= 1e-13
+
+
+def test_oz_decomposition_matches_dmma(ctx):
+    """A whole decomposition on the Ozaki engine agrees with the DMMA engine within the
+    well-conditioned (q = 0) tolerances."""
+    import paper_1810_07323_b200 as cg
+    from workloads import make_host
+    a = make_host("C1")
+    ctx.set_f64_engine(ctx.F64_DMMA)
+    f_dm = cg.corutv(a, 25, 0, seed=cg.RngSeed(42, 0), ctx=ctx)
+    ctx.set_f64_engine(ctx.F64_AUTO)
+    f_oz = cg.corutv(a, 25, 0, seed=cg.RngSeed(42, 0), ctx=ctx)
+    assert np.array_equal(f_dm.perm, f_oz.perm)
+    assert np.max(np.abs(np.abs(np.diag(f_dm.t)) - np.abs(np.diag(f_oz.t)))) <= 1e-12

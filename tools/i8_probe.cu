@@ -140,6 +140,77 @@ __global__ void k_tma_dump(const __grid_constant__ CUtensorMap tm, unsigned char
     for (int e = threadIdx.x; e < bytes; e += blockDim.x) out[e] = sm[e];
 }
 
+
+// ts form: A (128 x 32 int8) from TMEM (lane = row, 8 columns of 4 consecutive k, little-endian),
+// B (N x 32, N up to 256) from smem SW32; D at TMEM column dcol.
+__global__ void k_mma_ts(const int8_t* a, const int8_t* b, int N, int atype, int btype, int dcol, int* out) {
+    __shared__ __align__(1024) unsigned char sb[256 * 32];
+    __shared__ uint32_t slot;
+    __shared__ __align__(8) uint64_t bar;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (warp == 2) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;\n" ::"r"(su32(&slot)));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+    }
+    if (threadIdx.x == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(su32(&bar)));
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    for (int e = threadIdx.x; e < N * 32; e += blockDim.x) sb[lay_off(0, e / 32, e % 32)] = b[e];
+    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+    asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+    const uint32_t tmem = slot;
+    if (warp >= 4) {
+        const int t = threadIdx.x - 128;
+        uint32_t w[8];
+        for (int c = 0; c < 8; ++c) {
+            uint32_t x = 0;
+            for (int j = 0; j < 4; ++j) x |= uint32_t(uint8_t(a[t * 32 + 4 * c + j])) << (8 * j);
+            w[c] = x;
+        }
+        const uint32_t lb = uint32_t((warp & 3) * 32) << 16;
+        asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};\n" ::"r"(tmem + lb + 504),
+                     "r"(w[0]), "r"(w[1]), "r"(w[2]), "r"(w[3]), "r"(w[4]), "r"(w[5]), "r"(w[6]), "r"(w[7])
+                     : "memory");
+        asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+    if (threadIdx.x == 32) {
+        const uint32_t idesc = (2u << 4) | (uint32_t(atype) << 7) | (uint32_t(btype) << 10) |
+                               (uint32_t(N >> 3) << 17) | (uint32_t(128 >> 4) << 24);
+        const uint64_t bd = sdesc(su32(sb), 16, 256, 6);
+        asm volatile(
+            "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+            "tcgen05.mma.cta_group::1.kind::i8 [%0], [%1], %2, %3, p;\n}\n" ::"r"(tmem + dcol),
+            "r"(tmem + 504), "l"(bd), "r"(idesc), "r"(0));
+        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
+            su32(&bar)));
+    }
+    asm volatile(
+        "{\n.reg .pred p;\nW_%=:\nmbarrier.try_wait.parity.shared::cta.b64 p, [%0], 0;\n@!p bra W_%=;\n}\n" ::"r"(
+            su32(&bar)));
+    asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+    if (warp >= 4) {
+        const int t = threadIdx.x - 128;
+        const uint32_t lb = uint32_t((warp & 3) * 32) << 16;
+        for (int c0 = 0; c0 < N; c0 += 32) {
+            uint32_t v[32];
+            ld32(tmem + lb + dcol + c0, v);
+            for (int j = 0; j < 32 && c0 + j < N; ++j) out[t * N + c0 + j] = int(v[j]);
+        }
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+    __syncthreads();
+    if (warp == 2) {
+        asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;\n" ::"r"(tmem));
+    }
+}
+
 static PFN_cuTensorMapEncodeTiled_v12000 enc() {
     void* p = nullptr;
     cudaDriverEntryPointQueryResult q;
@@ -242,6 +313,46 @@ int main() {
                                    at ? "s8" : "u8", bt ? "s8" : "u8", tw, tma, cudaGetErrorString(e), bad, M * N);
                             if (e != cudaSuccess) return 1;
                         }
+    }
+    // 4. ts form (A from TMEM), N up to 256, D column offsets
+    {
+        const int Nts[3] = {256, 192, 48};
+        const int dcols[3] = {0, 64, 96};
+        for (int ni = 0; ni < 3; ++ni) {
+            const int N = Nts[ni];
+            std::vector<int8_t> a(M * 32), b(N * 32);
+            for (auto& x : a) x = int8_t(rand() & 255);
+            for (auto& x : b) x = int8_t(rand() & 255);
+            int8_t *da, *db;
+            int* dout;
+            cudaMalloc(&da, a.size());
+            cudaMalloc(&db, b.size());
+            cudaMalloc(&dout, M * N * 4);
+            cudaMemcpy(da, a.data(), a.size(), cudaMemcpyHostToDevice);
+            cudaMemcpy(db, b.data(), b.size(), cudaMemcpyHostToDevice);
+            for (int at = 0; at < 2; ++at)
+                for (int bt = 0; bt < 2; ++bt) {
+                    cudaMemset(dout, 0, M * N * 4);
+                    k_mma_ts<<<1, 256>>>(da, db, N, at, bt, dcols[ni], dout);
+                    cudaError_t e = cudaDeviceSynchronize();
+                    std::vector<int> o(M * N);
+                    cudaMemcpy(o.data(), dout, o.size() * 4, cudaMemcpyDeviceToHost);
+                    int bad = 0;
+                    for (int i = 0; i < M; ++i)
+                        for (int n = 0; n < N; ++n) {
+                            long sacc = 0;
+                            for (int k = 0; k < 32; ++k) {
+                                const int x = at ? int(a[i * 32 + k]) : int(uint8_t(a[i * 32 + k]));
+                                const int y = bt ? int(b[n * 32 + k]) : int(uint8_t(b[n * 32 + k]));
+                                sacc += long(x) * y;
+                            }
+                            if (o[i * N + n] != int(sacc)) ++bad;
+                        }
+                    printf("ts N=%d dcol=%d a%s b%s err=%s bad=%d/%d\n", N, dcols[ni], at ? "s8" : "u8", bt ? "s8" : "u8",
+                           cudaGetErrorString(e), bad, M * N);
+                    if (e != cudaSuccess) return 1;
+                }
+        }
     }
     return 0;
 }
