@@ -100,7 +100,9 @@ int coru_comm_unique_id(unsigned char id[128]);
 int coru_ctx_init_comm(coru_ctx* ctx, int rank, int world, const unsigned char id[128]);
 /* In-process alternative to NCCL: ranks are host threads of one process (one context each, on one
  * GPU or on peer-accessible GPUs); collectives are a stream sync + host barrier + fixed-order
- * device sum, deterministic and identical on every rank. */
+ * device sum, deterministic and identical on every rank. coru_ctx_init_threadcomm enables peer
+ * access between the new rank's device and every device already in the group, and returns
+ * CORU_ENOTSUP if two of them cannot reach each other. */
 typedef struct coru_threadcomm coru_threadcomm;
 coru_threadcomm* coru_threadcomm_create(int world);
 void coru_threadcomm_destroy(coru_threadcomm* group);

@@ -44,6 +44,8 @@ __all__ = [
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _LIB_PATH = os.path.join(_HERE, "libcoru_gpu.so")
+if os.environ.get("CORU_LIB_VARIANT"):  # tooling: A/B builds of the same library (tools/oz_variants.sh)
+    _LIB_PATH = os.path.join(_HERE, f"libcoru_gpu_{os.environ['CORU_LIB_VARIANT']}.so")
 
 CORU_OK, CORU_EINVAL, CORU_ECUDA, CORU_ENCCL, CORU_ENOMEM, CORU_ENOTSUP, CORU_EIO = range(7)
 

@@ -152,8 +152,9 @@ struct coru_threadcomm {
     int arrived = 0;
     uint64_t generation = 0;
     std::vector<const void*> slots;
+    std::vector<int> devices;  // device of each rank (-1: not joined yet)
     bool failed = false;  // a rank failed: every pending and future barrier returns false
-    explicit coru_threadcomm(int w) : world(w), slots(size_t(w), nullptr) {}
+    explicit coru_threadcomm(int w) : world(w), slots(size_t(w), nullptr), devices(size_t(w), -1) {}
     bool barrier() {
         std::unique_lock<std::mutex> lk(mu);
         if (failed) return false;
@@ -2224,6 +2225,37 @@ void coru_threadcomm_destroy(coru_threadcomm* g) { delete g; }
 int coru_ctx_init_threadcomm(coru_ctx* c, coru_threadcomm* g, int rank) {
     CORU_TRY(enter(c));
     if (!g || rank < 0 || rank >= g->world) return fail(CORU_EINVAL, "bad thread group / rank");
+    // The group's collectives read the other ranks' device buffers directly (k_sum_slots, the
+    // all-gather copies): every pair of devices in the group must reach each other. Same device:
+    // nothing to do; different devices: enable peer access both ways or refuse (CORU_ENOTSUP).
+    {
+        std::lock_guard<std::mutex> gl(g->mu);
+        g->devices[size_t(rank)] = c->device;
+        for (int r = 0; r < g->world; ++r) {
+            const int other = g->devices[size_t(r)];
+            if (other < 0 || other == c->device) continue;
+            int a = 0, b = 0;
+            cudaDeviceCanAccessPeer(&a, c->device, other);
+            cudaDeviceCanAccessPeer(&b, other, c->device);
+            if (!a || !b) {
+                g->devices[size_t(rank)] = -1;
+                return fail(CORU_ENOTSUP, "thread group spans devices without peer access (" +
+                                              std::to_string(c->device) + " <-> " + std::to_string(other) + ")");
+            }
+            for (auto [from, to] : {std::pair<int, int>{c->device, other}, {other, c->device}}) {
+                cudaSetDevice(from);
+                const cudaError_t e = cudaDeviceEnablePeerAccess(to, 0);
+                if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) {
+                    cudaGetLastError();
+                    cudaSetDevice(c->device);
+                    g->devices[size_t(rank)] = -1;
+                    return fail(CORU_ENOTSUP, std::string("cudaDeviceEnablePeerAccess: ") + cudaGetErrorString(e));
+                }
+                cudaGetLastError();
+            }
+            cudaSetDevice(c->device);
+        }
+    }
     std::lock_guard<std::mutex> lk(c->mu);
     c->tcomm = g;
     c->rank = rank;

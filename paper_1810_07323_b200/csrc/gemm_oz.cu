@@ -69,8 +69,14 @@ constexpr int kOzBK = 32;              // k per stage = one UMMA K step of int8
 constexpr int kOzS = 7;                // digit slices per operand
 constexpr int kOzNcMax = 64;           // columns per N-chunk
 constexpr int kOzMaxChunks = 4;        // N <= 256
-constexpr int kOzF = 4;                // fp64 ring stages (128 KB of A in flight per SM)
-constexpr int kOzI = 2;                // int8 ring stages (converters + X slices -> MMA)
+#ifndef CORU_OZ_F
+#define CORU_OZ_F 3
+#endif
+#ifndef CORU_OZ_I
+#define CORU_OZ_I 3
+#endif
+constexpr int kOzF = CORU_OZ_F;        // fp64 ring stages (96 KB of A in flight per SM)
+constexpr int kOzI = CORU_OZ_I;        // int8 ring stages (converters + X slices -> MMA)
 constexpr int kOzChunkStages = 512;    // flush interval (stages): 16384 k
 constexpr int kOzF64Bytes = kOzBM * kOzBK * 8;                  // 32 KB
 constexpr int kOzASlice = kOzBM * kOzBK;                        // 4 KB
@@ -197,7 +203,9 @@ __global__ void __launch_bounds__(kOzThreads, 1)
     k_apass_oz(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmXa,
                const __grid_constant__ CUtensorMap tmXb, const __grid_constant__ OzArgs p) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    unsigned char* sm = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    // 1024-byte alignment for the swizzle atoms, by offsetting the shared pointer itself (an
+    // integer round trip would lose the address space and turn every smem access generic)
+    unsigned char* sm = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
     unsigned char* fring = sm;
     unsigned char* iring = sm + kOzF * kOzF64Bytes;
     uint64_t* bars = reinterpret_cast<uint64_t*>(iring + kOzI * kOzIStage);
@@ -415,29 +423,52 @@ __global__ void __launch_bounds__(kOzThreads, 1)
 __device__ __forceinline__ int biased_exp(double x) { return int((__double_as_longlong(x) >> 52) & 0x7ff); }
 
 // Per-row and per-column maxima of the biased exponent field of A (rows x cols, lda): a CTA
-// owns a 32-row x 256-column tile (thread = column, coalesced rows); integer atomicMax, so the
-// result does not depend on the schedule.
+// owns a 128-row x 512-column tile; thread = two adjacent columns (16-byte loads, 8 rows in
+// flight), the row maxima go through warp reductions and shared memory, one integer atomicMax
+// per row and per column per CTA — the result does not depend on the schedule.
+constexpr int kExpRows = 128, kExpCols = 512;
 __global__ void __launch_bounds__(256) k_oz_aexp(const double* __restrict__ A, int64_t lda, int64_t rows, int64_t cols,
                                                  int* __restrict__ erow, int* __restrict__ ecol) {
-    __shared__ int srow[32];
-    const int64_t c = int64_t(blockIdx.x) * 256 + threadIdx.x;
-    const int64_t r0 = int64_t(blockIdx.y) * 32;
-    if (threadIdx.x < 32) srow[threadIdx.x] = 0;
+    __shared__ int srow[kExpRows];
+    const int64_t c = int64_t(blockIdx.x) * kExpCols + 2 * threadIdx.x;
+    const int64_t r0 = int64_t(blockIdx.y) * kExpRows;
+    for (int i = threadIdx.x; i < kExpRows; i += 256) srow[i] = 0;
     __syncthreads();
-    int cmax = 0;
-    const int lane = threadIdx.x & 31;
-    for (int rr = 0; rr < 32; ++rr) {
-        const int64_t r = r0 + rr;
-        int be = 0;
-        if (r < rows && c < cols) be = biased_exp(A[r * lda + c]);
-        be = be == 0x7ff ? 0x7fe : be;  // inf / nan: clamp (the host entry rejects them anyway)
-        cmax = max(cmax, be);
-        const int wm = __reduce_max_sync(0xffffffffu, unsigned(be));
-        if (lane == 0) atomicMax(&srow[rr], wm);
+    const bool vec = (lda & 1) == 0 && (reinterpret_cast<uintptr_t>(A) & 15) == 0 && c + 1 < cols;
+    int cm0 = 0, cm1 = 0;
+    for (int rr = 0; rr < kExpRows; rr += 8) {
+        double a[8], b[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const int64_t r = r0 + rr + u;
+            a[u] = b[u] = 0.0;
+            if (r < rows) {
+                if (vec) {
+                    const double2 v = *reinterpret_cast<const double2*>(A + r * lda + c);
+                    a[u] = v.x;
+                    b[u] = v.y;
+                } else {
+                    if (c < cols) a[u] = A[r * lda + c];
+                    if (c + 1 < cols) b[u] = A[r * lda + c + 1];
+                }
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            int ea = biased_exp(a[u]), eb = biased_exp(b[u]);
+            ea = ea == 0x7ff ? 0x7fe : ea;  // inf / nan: clamp (the host entry rejects them anyway)
+            eb = eb == 0x7ff ? 0x7fe : eb;
+            cm0 = max(cm0, ea);
+            cm1 = max(cm1, eb);
+            const int wm = int(__reduce_max_sync(0xffffffffu, unsigned(max(ea, eb))));
+            if ((threadIdx.x & 31) == 0 && wm > 0) atomicMax(&srow[rr + u], wm);
+        }
     }
-    if (c < cols) atomicMax(&ecol[c], cmax);
+    if (c < cols && cm0 > 0) atomicMax(&ecol[c], cm0);
+    if (c + 1 < cols && cm1 > 0) atomicMax(&ecol[c + 1], cm1);
     __syncthreads();
-    if (threadIdx.x < 32 && r0 + threadIdx.x < rows) atomicMax(&erow[r0 + threadIdx.x], srow[threadIdx.x]);
+    for (int i = threadIdx.x; i < kExpRows; i += 256)
+        if (r0 + i < rows && srow[i] > 0) atomicMax(&erow[r0 + i], srow[i]);
 }
 
 __global__ void k_oz_finish_exp(int* __restrict__ e, int64_t n) {
@@ -602,7 +633,7 @@ cudaError_t gemm_oz_exponents(const double* A, int64_t lda, int64_t rows, int64_
     cudaError_t e = cudaMemsetAsync(erow, 0, sizeof(int) * size_t(rows), st);
     if (e == cudaSuccess) e = cudaMemsetAsync(ecol, 0, sizeof(int) * size_t(cols), st);
     if (e != cudaSuccess) return e;
-    const dim3 grid(unsigned((cols + 255) / 256), unsigned((rows + 31) / 32));
+    const dim3 grid(unsigned((cols + kExpCols - 1) / kExpCols), unsigned((rows + kExpRows - 1) / kExpRows));
     k_oz_aexp<<<grid, 256, 0, st>>>(A, lda, rows, cols, erow, ecol);
     k_oz_finish_exp<<<int(std::min<int64_t>((rows + 255) / 256, 1184)), 256, 0, st>>>(erow, rows);
     k_oz_finish_exp<<<int(std::min<int64_t>((cols + 255) / 256, 1184)), 256, 0, st>>>(ecol, cols);

@@ -177,7 +177,9 @@ __global__ void __launch_bounds__(kTcThreads, 1)
                    const __grid_constant__ CUtensorMap tmXl, const TcArgs p) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     // 1024-byte alignment for the SW128 atoms
-    unsigned char* sm = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    // 1024-byte alignment for the swizzle atoms, by offsetting the shared pointer itself (an
+    // integer round trip would lose the address space and turn every smem access generic)
+    unsigned char* sm = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
     const int xbytes = p.nc * kBK * 4;                      // one X operand tile per stage
     const int stage_bytes = kATileBytes + 2 * xbytes;       // multiple of 1024
     uint64_t* bars = reinterpret_cast<uint64_t*>(sm + p.stages * stage_bytes);
