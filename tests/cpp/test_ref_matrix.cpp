@@ -47,21 +47,31 @@ static double orth(const coru::Matrix& q) {
     return std::sqrt(s);
 }
 
-static void compare(const coru::Matrix& a, std::size_t ell, int q, std::uint64_t seed) {
+// ksig: how many leading |t_jj| carry signal. Entries past it sit in an iid-noise tail whose pivot
+// order and values are rounding-determined in the reference itself (measured with the oracle on
+// the rank-25 + 1e-6 noise input: 1-ulp floor 9e-9, FMA floor 4e-9, distance of the reference from
+// its extended-precision execution 2.8e-8 on |t_jj| ~ 2e-5; reconstruction error floors 1e-6 / 8e-6
+// relative), so the BASELINE tolerances apply to the signal prefix and the tail is held to 10x floor.
+static void compare(const coru::Matrix& a, std::size_t ell, int q, std::uint64_t seed, std::size_t ksig = 0) {
+    if (ksig == 0) ksig = ell;
     const coru::UtvApprox ref = coru::corutv(a, ell, q, coru::DVariant::exact, {seed, 0});
     const coru_gpu::UtvApproxOf<coru::Matrix> gpu =
         coru_gpu::corutv(a, ell, q, coru_gpu::DVariant::exact, coru_gpu::RngSeed{seed, 0});
     CHECK(gpu.lower == ref.lower);
     CHECK(gpu.u.rows() == ref.u.rows() && gpu.v.rows() == ref.v.rows());
     const double e_ref = rel_err(a, ref), e_gpu = rel_err(a, gpu);
-    double dmax = 0;
-    for (std::size_t j = 0; j < ell; ++j) dmax = std::max(dmax, std::abs(std::abs(gpu.t(j, j)) - std::abs(ref.t(j, j))));
-    std::printf("%zux%zu ell=%zu q=%d: err gpu %.3e ref %.3e, max |diag T| diff %.3e, orth %.2e %.2e\n", a.rows(),
-                a.cols(), ell, q, e_gpu, e_ref, dmax, orth(gpu.u), orth(gpu.v));
+    double dmax = 0, dtail = 0;
+    for (std::size_t j = 0; j < ell; ++j) {
+        const double dj = std::abs(std::abs(gpu.t(j, j)) - std::abs(ref.t(j, j)));
+        (j < ksig ? dmax : dtail) = std::max(j < ksig ? dmax : dtail, dj);
+    }
+    std::printf("%zux%zu ell=%zu q=%d: err gpu %.3e ref %.3e, max |diag T| diff %.3e (tail %.3e), orth %.2e %.2e\n", a.rows(),
+                a.cols(), ell, q, e_gpu, e_ref, dmax, dtail, orth(gpu.u), orth(gpu.v));
     CHECK(orth(gpu.u) <= 1e-12 * double(ell) && orth(gpu.v) <= 1e-12 * double(ell));
     if (q == 0) {
-        CHECK(std::abs(e_gpu - e_ref) <= 1e-10 * e_ref + 1e-14);
+        CHECK(std::abs(e_gpu - e_ref) <= (ksig < ell ? 1e-4 : 1e-10) * e_ref + 1e-14);
         CHECK(dmax <= 1e-8);
+        CHECK(dtail <= 3e-7);
     }
     CHECK(gpu.conditioning_warning == ref.conditioning_warning);
 }
@@ -74,8 +84,8 @@ int main() {
     const coru::Matrix noise = coru::gaussian(300, 180, {15, 2});
     for (std::size_t i = 0; i < tall.rows(); ++i)
         for (std::size_t j = 0; j < tall.cols(); ++j) tall(i, j) += 1e-6 * noise(i, j);
-    compare(tall, 30, 0, 9);
-    compare(tall.transposed(), 30, 0, 9);  // rows < cols: the ULV orientation (corutv.hpp:82-87)
+    compare(tall, 30, 0, 9, 25);
+    compare(tall.transposed(), 30, 0, 9, 25);  // rows < cols: the ULV orientation (corutv.hpp:82-87)
     const coru::Matrix a = coru::gen_fast_decay(60, 10, {14, 0});
     for (auto [ell, q] : {std::pair<std::size_t, int>{0, 0}, {60, 0}, {3, -1}}) {
         bool threw = false;
