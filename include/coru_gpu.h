@@ -285,6 +285,9 @@ int coru_ctx_profile_rpca_update(coru_ctx* ctx, double* total_ms, int64_t* launc
 /* Number of this library's kernels launched by the calling thread since the last reset
  * (bench evidence: "gpu_launches"). */
 int64_t coru_launch_count(int reset);
+/* Test tooling: cap the stream-K CTAs per output tile of the FP64 DMMA GEMM planner
+ * (0 = the planner's own choice). Process-wide; affects every later plan. */
+void coru_debug_gemm_split_cap(int cap);
 
 #ifdef __cplusplus
 }

@@ -132,6 +132,8 @@ def load_library():
     L.coru_last_error.restype = C.c_char_p
     L.coru_launch_count.argtypes = [i32]
     L.coru_launch_count.restype = i64
+    L.coru_debug_gemm_split_cap.argtypes = [i32]
+    L.coru_debug_gemm_split_cap.restype = None
     L.coru_ctx_create.argtypes = [i32, C.POINTER(p)]
     L.coru_ctx_destroy.argtypes = [p]
     L.coru_ctx_destroy.restype = None
@@ -203,6 +205,11 @@ def _check(rc: int):
 def launch_count(reset: bool = False) -> int:
     """Kernels this library launched on the calling thread (bench evidence)."""
     return int(load_library().coru_launch_count(1 if reset else 0))
+
+
+def debug_gemm_split_cap(cap: int) -> None:
+    """Test tooling: cap the stream-K CTAs per output tile of the FP64 GEMM planner (0 = default)."""
+    load_library().coru_debug_gemm_split_cap(int(cap))
 
 
 def shard_rows(m: int, rank: int, world: int) -> tuple[int, int]:

@@ -2024,6 +2024,8 @@ int64_t coru_launch_count(int reset) {
     return v;
 }
 
+void coru_debug_gemm_split_cap(int cap) { gemm_f64_set_split_cap(cap); }
+
 int coru_ctx_create(int device, coru_ctx** out) {
     if (!out) return fail(CORU_EINVAL, "null out");
     *out = nullptr;

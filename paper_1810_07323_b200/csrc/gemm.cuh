@@ -26,6 +26,8 @@ GemmPlan plan_gemm_f64(Op op, int64_t Mo, int64_t K, int N, int num_sms);
 // Explicit configuration (cfg < 0: default); for tuning tools.
 GemmPlan plan_gemm_f64_cfg(Op op, int64_t Mo, int64_t K, int N, int num_sms, int cfg);
 int gemm_f64_num_configs();
+// Tooling: cap the stream-K CTAs per output tile (0 = planner default); affects every later plan.
+void gemm_f64_set_split_cap(int cap);
 // `ws` must hold plan.ws_elems doubles when plan.splits > 1.
 cudaError_t gemm_f64(Op op, const double* A, int64_t lda, const double* X, int64_t ldx, double* C,
                      int64_t ldc, int64_t Mo, int64_t K, int N, const GemmPlan& plan, double* ws,

@@ -456,6 +456,10 @@ int default_cfg(Op op, int N) {
 // so a stale flag of the earlier one could pass for a fresh publish of the later one.)
 std::atomic<uint64_t> g_gemm_epoch{0};
 
+// Tooling knob (tests/test_gpu_kernels.py planner sweep): at most this many CTAs per output tile
+// (0 = the planner's own choice). Read by every plan, so workspace sizes stay consistent.
+std::atomic<int> g_gemm_split_cap{0};
+
 template <class S>
 cudaError_t launch_cfg(const double* A, int64_t lda, const double* X, int64_t ldx, double* C, int64_t ldc, int64_t Mo,
                        int64_t K, int N, const GemmPlan& p, double* ws, cudaStream_t st) {
@@ -485,6 +489,7 @@ cudaError_t launch_cfg(const double* A, int64_t lda, const double* X, int64_t ld
 }  // namespace
 
 int gemm_f64_num_configs() { return kNumCfgs; }
+void gemm_f64_set_split_cap(int cap) { g_gemm_split_cap.store(cap < 0 ? 0 : cap); }
 
 GemmPlan plan_gemm_f64_cfg(Op op, int64_t Mo, int64_t K, int N, int num_sms, int cfg) {
     GemmPlan p;
@@ -513,6 +518,8 @@ GemmPlan plan_gemm_f64_cfg(Op op, int64_t Mo, int64_t K, int N, int num_sms, int
     const int64_t iters = gtiles * ktiles;            // iterations per group
     int64_t P64 = std::min<int64_t>(resident / G, iters / 4);
     P64 = std::min<int64_t>(P64, gtiles * std::max<int64_t>(12, (resident / G + gtiles - 1) / gtiles));
+    if (const int cap = g_gemm_split_cap.load(std::memory_order_relaxed); cap > 0)
+        P64 = std::min<int64_t>(P64, gtiles * cap);
     const int P = int(std::max<int64_t>(P64, 1));     // CTAs per group
     p.splits = P;
     const int64_t per = std::max<int64_t>(1, iters / P);

@@ -253,3 +253,55 @@ def test_device_phi_corutv_agrees_with_host_exact(oracle):
     assert np.max(np.abs(np.abs(np.diag(f1.t)) - np.abs(np.diag(f2.t)))) <= 1e-12 * abs(f2.t[0, 0])
     ref = oracle.corutv(a, 20, 0, seed=4, stream=1)
     assert np.max(np.abs(np.abs(np.diag(f2.t)) - np.abs(np.diag(ref.t)))) <= 1e-12 * abs(ref.t[0, 0])
+
+
+def test_gemm_streamk_planner_sweep(ctx):
+    """Randomised stream-K planner sweep: random (rows, K, N, op), a random cap
+    on the CTAs per output tile (grouped and ungrouped plans, whole / split tiles), the SAME
+    workspace reused by consecutive launches of different plans — every result against a
+    float64 numpy product (1e-12·|A||X| entrywise) and bitwise repeatable."""
+    import torch
+    import paper_1810_07323_b200 as cg
+    rng = np.random.default_rng(20261021)
+    ctx.set_f64_engine(1)  # FP64 DMMA for everything: the stream-K kernel under test
+    try:
+        for trial in range(60):
+            op = int(rng.integers(0, 2))
+            rows = int(rng.choice([1, 7, 33, 64, 130, 220, 257, 520, 1000, 3000]))
+            K = int(rng.choice([8, 40, 129, 1000, 3000, 20000]))
+            N = int(rng.choice([1, 8, 25, 60, 110, 130, 220, 256]))
+            cap = int(rng.choice([0, 0, 1, 2, 3, 5, 8, 16]))
+            cg.debug_gemm_split_cap(cap)
+            a = rng.standard_normal((K, rows) if op else (rows, K))
+            npad = (N + 7) // 8 * 8
+            x = np.zeros((K, npad))
+            x[:, :N] = rng.standard_normal((K, N))
+            ta, tx = _t(a), _t(x)[:, :N]
+            c = cg.gemm(ta, tx, op=op, ctx=ctx).cpu().numpy()
+            want = (a.T if op else a) @ x[:, :N]
+            bound = np.abs(a.T if op else a) @ np.abs(x[:, :N])
+            bad = np.abs(c - want) > 1e-12 * bound + 1e-300
+            assert not bad.any(), (trial, op, rows, K, N, cap, int(bad.sum()), float(np.abs(c - want).max()))
+            assert np.array_equal(cg.gemm(ta, tx, op=op, ctx=ctx).cpu().numpy(), c), (trial, op, rows, K, N, cap)
+    finally:
+        cg.debug_gemm_split_cap(0)
+        ctx.set_f64_engine(0)
+
+
+@pytest.mark.parametrize("cap", [1, 2, 4])
+@pytest.mark.parametrize("m,d", [(3000, 130), (5000, 220), (2048, 136)])
+def test_wide_qr_under_split_caps(ctx, m, d, cap):
+    """CholeskyQR2 (Gram + R2·R1 products on the stream-K GEMM, one shared workspace) with the
+    planner's split capped: the configuration DESIGN.md (round 1) recorded as producing a wrong
+    Gram. Q R = B, orthonormal Q."""
+    import paper_1810_07323_b200 as cg
+    rng = np.random.default_rng(m + d + cap)
+    b = rng.standard_normal((m, d))
+    cg.debug_gemm_split_cap(cap)
+    try:
+        q, r = cg.tsqr(_t(b), ctx=ctx)
+        q, r = q.cpu().numpy(), r.cpu().numpy()
+    finally:
+        cg.debug_gemm_split_cap(0)
+    assert np.linalg.norm(q @ r - b) <= 1e-12 * np.linalg.norm(b) * d
+    assert orth_residual(q) <= 1e-12 * d
