@@ -84,8 +84,13 @@ enum { CORU_F32_AUTO = 0, CORU_F32_SIMT = 1, CORU_F32_TC = 2 };
  *     7 digit slices per operand against per-row / per-column power-of-two scales, exact int32
  *     slice products, fp64 recombination (~2^-55 relative error vs. row-max x column-max);
  *     FP64 DMMA for shapes it cannot take and for every non-A-pass product;
- *   CORU_F64_DMMA: FP64 DMMA for everything. */
-enum { CORU_F64_AUTO = 0, CORU_F64_DMMA = 1 };
+ *     A is either converted to digits inside every A-pass kernel (few passes, narrow sketch) or
+ *     once per decomposition into its digit planes (14 bytes per entry of extra device memory)
+ *     that every pass then streams — chosen from (passes over A) x (N-chunks of the sketch);
+ *   CORU_F64_DMMA: FP64 DMMA for everything;
+ *   CORU_F64_OZAKI_INLINE / CORU_F64_OZAKI_PLANES: the Ozaki engine with the conversion forced
+ *     into the A-pass kernel / into the once-per-decomposition digit planes. */
+enum { CORU_F64_AUTO = 0, CORU_F64_DMMA = 1, CORU_F64_OZAKI_INLINE = 2, CORU_F64_OZAKI_PLANES = 3 };
 int coru_ctx_set_f64_engine(coru_ctx* ctx, int mode);
 int coru_ctx_set_f32_path(coru_ctx* ctx, int mode);
 /* QR of wide sketches (more than 128 columns; householder_qr at corutv.hpp:59-60): 1 (default) =

@@ -262,11 +262,13 @@ class Context:
         products), F32_SIMT (CUDA-core FFMA), F32_TC (tensor cores wherever the shape allows)."""
         _check(self.lib.coru_ctx_set_f32_path(self.h, mode))
 
-    F64_AUTO, F64_DMMA = 0, 1
+    F64_AUTO, F64_DMMA, F64_OZAKI_INLINE, F64_OZAKI_PLANES = 0, 1, 2, 3
 
     def set_f64_engine(self, mode: int):
         """fp64 A-pass engine: F64_AUTO (default: INT8 tensor cores, Ozaki scheme, for A-pass-sized
-        products over the caller's A), F64_DMMA (FP64 DMMA for everything)."""
+        products over the caller's A; digits converted inside each pass or once per decomposition
+        into digit planes, by a cost model), F64_DMMA (FP64 DMMA for everything),
+        F64_OZAKI_INLINE / F64_OZAKI_PLANES (force where the conversion happens)."""
         _check(self.lib.coru_ctx_set_f64_engine(self.h, mode))
 
     def set_wide_qr(self, on: bool):

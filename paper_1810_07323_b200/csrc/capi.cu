@@ -197,6 +197,11 @@ struct coru_ctx {
     size_t oz_e_cap = 0;        // ints
     void* oz_ws = nullptr;
     size_t oz_ws_bytes = 0;
+    // Digit planes of the prepared matrix (converted once per decomposition; gemm_oz.cu). Null when
+    // they do not fit next to A (then the A-pass kernel converts A itself on every pass).
+    void* oz_planes = nullptr;
+    size_t oz_planes_cap = 0;
+    bool oz_planes_ready = false;
     bool wide_qr = true;  // CholeskyQR2 (fp64) for sketches wider than 128 columns, Householder fall-back
     char* arena = nullptr;
     size_t arena_bytes = 0;
@@ -374,7 +379,8 @@ bool oz_enabled(const coru_ctx* c) {
 
 // Exponents of the stored matrix (rows x cols, lda) the coming A-passes stream (gemm_oz.cu): one
 // extra read of A per decomposition, reused by every pass over it.
-int oz_prepare(coru_ctx* c, const double* A, int64_t lda, int64_t rows, int64_t cols) {
+// passes: A-passes the caller will run over A; ncols: their sketch width (decides digit planes).
+int oz_prepare(coru_ctx* c, const double* A, int64_t lda, int64_t rows, int64_t cols, int passes, int ncols) {
     c->oz_a = nullptr;
     if (!oz_enabled(c) || !A) return CORU_OK;
     if (!gemm_oz_eligible(std::max(rows, cols), std::min(rows, cols), 1)) return CORU_OK;
@@ -385,6 +391,34 @@ int oz_prepare(coru_ctx* c, const double* A, int64_t lda, int64_t rows, int64_t 
     c->oz_e_cap = cap_bytes / sizeof(int);
     CORU_CUDA(gemm_oz_exponents(A, lda, rows, cols, c->oz_e, c->oz_e + rows, c->stream));
     g_launches += 3;
+    // Digit planes (14 bytes per entry): converted once here, streamed by every A-pass. Skipped when
+    // they would not fit in what is free now (beyond what the context already holds for them).
+    // Worth it when the conversion would otherwise be repeated often enough: every pass converts A
+    // once per 64-column chunk of the sketch inside the A-pass kernel. Measured on B200: C3 (5
+    // passes x 2 chunks) 17.0 ms inline vs 18.2 ms with planes, C4 (7 x 4) 87.0 vs 83.5 ms.
+    c->oz_planes_ready = false;
+    static const char* planes_env = getenv("CORU_OZ_PLANES");  // tooling override: 0 | 1
+    const int nch = (ncols + 63) / 64;
+    bool want = passes * (nch - 1) >= 15;
+    if (c->f64_engine == CORU_F64_OZAKI_PLANES) want = true;
+    if (c->f64_engine == CORU_F64_OZAKI_INLINE) want = false;
+    if (planes_env) want = atoi(planes_env) != 0;
+    if (want) {
+        const OzPlaneDims pd = gemm_oz_plane_dims(rows, cols);
+        const size_t need = pd.pn_bytes + pd.pt_bytes;
+        bool fits = need <= c->oz_planes_cap;
+        if (!fits) {
+            size_t free_b = 0, total_b = 0;
+            CORU_CUDA(cudaMemGetInfo(&free_b, &total_b));
+            fits = need + (size_t(4) << 30) <= free_b + c->oz_planes_cap;
+        }
+        if (fits && ensure_dev(c, &c->oz_planes, &c->oz_planes_cap, need, "Ozaki digit planes") == CORU_OK) {
+            CORU_CUDA(gemm_oz_planes(A, lda, rows, cols, c->oz_e, c->oz_e + rows, static_cast<uint8_t*>(c->oz_planes),
+                                     c->stream));
+            ++g_launches;
+            c->oz_planes_ready = true;
+        }
+    }
     c->oz_a = A;
     c->oz_lda = lda;
     c->oz_rows = rows;
@@ -449,7 +483,16 @@ int gemm<double>(coru_ctx* c, Op op, const double* A, int64_t lda, const double*
         cudaEvent_t stop = nullptr;
         if (c->prof) CORU_TRY(prof_begin(c, &stop));
         const int* eA = op == Op::N ? c->oz_e : c->oz_e + c->oz_rows;
-        CORU_CUDA(gemm_oz(op, A, lda, eA, X, ldx, C, ldc, Mo, K, N, c->oz_ws, c->num_sms, c->stream));
+        OzPlanes pl;
+        if (c->oz_planes_ready) {
+            const OzPlaneDims pd = gemm_oz_plane_dims(c->oz_rows, c->oz_cols);
+            const uint8_t* base = static_cast<const uint8_t*>(c->oz_planes);
+            pl.p = op == Op::N ? base : base + pd.pn_bytes;
+            pl.ld = op == Op::N ? pd.ldn : pd.ldt;
+            pl.rows = op == Op::N ? c->oz_rows : c->oz_cols;
+        }
+        CORU_CUDA(gemm_oz(op, A, lda, c->oz_planes_ready ? &pl : nullptr, eA, X, ldx, C, ldc, Mo, K, N, c->oz_ws,
+                          c->num_sms, c->stream));
         if (stop) {
             CORU_CUDA(cudaEventRecord(stop, c->stream));
             c->prof_flops += 2.0 * double(Mo) * double(K) * double(N);
@@ -867,7 +910,8 @@ template <typename T>
 int run(coru_ctx* c, const Request<T>& r, size_t extra_arena_off = 0) {
     if constexpr (std::is_same<T, double>::value) {
         if (r.A) {  // device-resident A: the stored matrix is rows x cols, or its transpose (ULV)
-            const int rc = oz_prepare(c, r.A, r.lda, r.trans ? r.cols : r.rows, r.trans ? r.rows : r.cols);
+            const int passes = r.mode == Mode::Sketch ? 2 * r.q + 2 : 2 * r.q + (r.variant == CORU_D_APPROX ? 2 : 3);
+            const int rc = oz_prepare(c, r.A, r.lda, r.trans ? r.cols : r.rows, r.trans ? r.rows : r.cols, passes, r.d);
             if (rc != CORU_OK) {
                 if (c->tcomm) c->tcomm->abort();
                 return rc;
@@ -2075,6 +2119,7 @@ void coru_ctx_destroy(coru_ctx* c) {
     if (c->stage) cudaFreeHost(c->stage);
     if (c->oz_e) cudaFree(c->oz_e);
     if (c->oz_ws) cudaFree(c->oz_ws);
+    if (c->oz_planes) cudaFree(c->oz_planes);
     for (auto& e : c->ev_stage)
         if (e) cudaEventDestroy(e);
     if (c->aux) {
@@ -2173,7 +2218,7 @@ int coru_ctx_set_f32_path(coru_ctx* c, int mode) {
 }
 
 int coru_ctx_set_f64_engine(coru_ctx* c, int mode) {
-    if (!c || (mode != CORU_F64_AUTO && mode != CORU_F64_DMMA)) return fail(CORU_EINVAL, "bad argument");
+    if (!c || mode < CORU_F64_AUTO || mode > CORU_F64_OZAKI_PLANES) return fail(CORU_EINVAL, "bad argument");
     std::lock_guard<std::mutex> lk(c->mu);
     c->f64_engine = mode;
     return CORU_OK;
@@ -2507,7 +2552,7 @@ int coru_gemm_f64_dev(coru_ctx* c, int op, const double* A, int64_t lda, const d
     CORU_TRY(ensure_arena(c, size_t(wse) * 8 + 256));
     // A is an A-pass operand here: the Ozaki engine takes it when the shape qualifies
     const int64_t srows = o == Op::N ? rows : K, scols = o == Op::N ? K : rows;
-    CORU_TRY(oz_prepare(c, A, lda, srows, scols));
+    CORU_TRY(oz_prepare(c, A, lda, srows, scols, 1, int(N)));
     const int rc = gemm<double>(c, o, A, lda, X, ldx, C, ldc, rows, K, int(N), reinterpret_cast<double*>(c->arena), wse);
     c->oz_a = nullptr;
     CORU_TRY(rc);

@@ -54,8 +54,24 @@ bool gemm_oz_supported(Op op, const double* A, int64_t lda, int64_t Mo, int64_t 
 size_t gemm_oz_ws_bytes(int64_t Mo, int64_t K, int N, int num_sms);
 cudaError_t gemm_oz_exponents(const double* A, int64_t lda, int64_t rows, int64_t cols, int* erow, int* ecol,
                               cudaStream_t st);
-cudaError_t gemm_oz(Op op, const double* A, int64_t lda, const int* eA, const double* X, int64_t ldx, double* C,
-                    int64_t ldc, int64_t Mo, int64_t K, int N, void* ws, int num_sms, cudaStream_t st);
+// Digit planes of a prepared matrix (gemm_oz_planes): the 7 slices of every entry, converted once
+// per decomposition — PN (row scales, K-major for op N) followed by PT (column scales, transposed:
+// K-major for op T) in one buffer of pn_bytes + pt_bytes.
+struct OzPlaneDims {
+    int64_t ldn = 0, ldt = 0;       // bytes per plane row
+    size_t pn_bytes = 0, pt_bytes = 0;
+};
+OzPlaneDims gemm_oz_plane_dims(int64_t rows, int64_t cols);
+cudaError_t gemm_oz_planes(const double* A, int64_t lda, int64_t rows, int64_t cols, const int* erow, const int* ecol,
+                           uint8_t* planes, cudaStream_t st);
+struct OzPlanes {
+    const uint8_t* p = nullptr;     // plane set matching the op: [7][rows][ld]
+    int64_t ld = 0, rows = 0;       // rows = rows of the plane set (output rows of op(A) for the whole matrix)
+};
+// pl != nullptr: A-pass over the planes (A, lda unused); else A is converted inside the kernel.
+cudaError_t gemm_oz(Op op, const double* A, int64_t lda, const OzPlanes* pl, const int* eA, const double* X,
+                    int64_t ldx, double* C, int64_t ldc, int64_t Mo, int64_t K, int N, void* ws, int num_sms,
+                    cudaStream_t st);
 int gemm_oz_launches(int64_t Mo, int64_t K, int N, int num_sms);
 
 }  // namespace coru_gpu

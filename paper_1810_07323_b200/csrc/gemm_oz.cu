@@ -38,10 +38,12 @@
 //   warp 0      TMA producer: fp64 A tile (128 x 32) -> fp64 ring (kOzF stages ahead)
 //   warp 3      TMA producer: the 7 X digit slices of the chunk (one 3-D box: 7 x nc x 32 int8,
 //               SWIZZLE_32B, slices stacked) -> int8 ring
-//   warps 4..11 converters: thread (row r, k-half h) reads 16 fp64 of its row (op N: swizzled
+//   warps 4..19 converters: thread (row r, k-quarter kq) reads 8 fp64 of its row (op N: swizzled
 //               K-major tile; op T: a column of the [k][m] tile — A^T is never formed), scales,
 //               F2I, permutes bytes into the 7 A slices (K-major SW32 rows of 32 B) of the int8
-//               ring; at each flush they read the 7 level accumulators back (tcgen05.ld) and add
+//               ring (16 warps: four per scheduler hide the conversion latencies better than two,
+//               1.70 vs 1.83 ms per C3 pass); at each flush they read the 7 level accumulators
+//               back (tcgen05.ld) and add
 //               sum_L acc_L 2^(-8L) · 2^(E_i + F_j - 12) into the fp64 output (own rows, fixed
 //               order: deterministic)
 //   warp 1      MMA issuer: per stage and A slice s one stacked tcgen05.mma (M = 128, K = 32,
@@ -50,7 +52,9 @@
 // Split-K (op T: K = m rows of A) writes per-split fp64 partials summed in a fixed order.
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
+#include <string>
 #include <mutex>
 
 #include <cuda.h>
@@ -63,7 +67,13 @@ namespace coru_gpu {
 
 namespace {
 
-constexpr int kOzThreads = 384;
+#ifndef CORU_OZ_KQ
+#define CORU_OZ_KQ 4
+#endif
+constexpr int kOzKQ = CORU_OZ_KQ;      // k-groups per stage row (2 or 4): a converter thread takes 32 / kOzKQ doubles
+constexpr int kOzEPT = 32 / kOzKQ;     // elements per converter thread and stage
+constexpr int kOzConvWarps = 4 * kOzKQ;  // converter warps: kOzKQ per TMEM lane quadrant
+constexpr int kOzThreads = 128 + 32 * kOzConvWarps;
 constexpr int kOzBM = 128;
 constexpr int kOzBK = 32;              // k per stage = one UMMA K step of int8
 constexpr int kOzS = 7;                // digit slices per operand
@@ -174,6 +184,24 @@ __device__ __forceinline__ double pow2(int e) { return __longlong_as_double(int6
 // Balanced base-256 digits of the int64 w (|w| < 2^54): bytes of w + C, the low six XOR 0x80.
 constexpr unsigned long long kOzBias = 0x0000808080808080ull;
 
+// Tooling alternative (CORU_OZ_MAGIC) to F2I.S64.F64: rint(t) + kOzBias for |t| < 2^54,
+// bit-identical to (unsigned long long)__double2ll_rn(t) + kOzBias, on the FP64 pipe only — measured
+// SLOWER on B200 than the XU conversion (1.93 vs 1.70 ms per C3 pass), kept for the A/B.
+// H = rint(t·2^-28) and L = rint(t - H·2^28) by the add-magic-constant trick
+// (1.5·2^52 puts the rounded integer in the low mantissa word; both steps exact, ties keep their
+// parity because H·2^28 is even), four FP64-pipe operations and a few integer ones.
+// t = x·sc (sc a power of two, so x·sc and x·sc·2^-28 are exact): um = rn(t·2^-28 + M), H = um - M,
+// c = M - H·2^28 (exact: a multiple of 2^28 below 2^55), lm = rn(t + c) = rn((t - H·2^28) + M).
+__device__ __forceinline__ unsigned long long oz_round_biased(double x, double sc, double sc28) {
+    constexpr double M = 6755399441055744.0;  // 1.5 · 2^52
+    const double um = __fma_rn(x, sc28, M);
+    const double hr = __dadd_rn(um, -M);
+    const double c = __fma_rn(hr, -0x1p28, M);
+    const double lm = __fma_rn(x, sc, c);
+    const long long v = (static_cast<long long>(__double2loint(um)) << 28) + static_cast<long long>(__double2loint(lm));
+    return static_cast<unsigned long long>(v) + kOzBias;
+}
+
 // Exponent E with max |x| < 2^E from the largest biased exponent field be of a group (0 for an
 // all-zero group); clamped so the conversion scale 2^(55 - E) stays finite.
 __host__ __device__ __forceinline__ int oz_exp_from_biased(int be) {
@@ -233,15 +261,15 @@ __global__ void __launch_bounds__(kOzThreads, 1)
     if (warp == 0 && lane == 0) {
         for (int s = 0; s < kOzF; ++s) {
             mbar_init(&f_full[s], 1);
-            mbar_init(&f_empty[s], 8);
+            mbar_init(&f_empty[s], kOzConvWarps);
         }
         for (int s = 0; s < kOzI; ++s) {
             mbar_init(&x_full[s], 1);
-            mbar_init(&a_full[s], 8);
+            mbar_init(&a_full[s], kOzConvWarps);
             mbar_init(&i_empty[s], 1);
         }
         mbar_init(acc_full, 1);
-        mbar_init(acc_empty, 8);
+        mbar_init(acc_empty, kOzConvWarps);
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
         asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
         asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(nc == p.nc_a ? &tmXa : &tmXb))
@@ -321,57 +349,72 @@ __global__ void __launch_bounds__(kOzThreads, 1)
         }
     } else if (warp >= 4) {
         // ===== converters, then the flushes =====
-        const int cw = warp - 4, q = cw & 3, h = cw >> 2;
+        // warp cw: TMEM lane quadrant q = cw & 3 (= warp % 4, the lanes tcgen05.ld may touch),
+        // k-group kq = cw >> 2: thread (row r, kq) converts the kOzEPT doubles k = kq·EPT .. of its row.
+        const int cw = warp - 4, q = cw & 3, kq = cw >> 2;
         const int r = q * 32 + lane;
         const int64_t row = m0 + r;
         const int E = row < p.Mo ? p.eA[row] : 0;
-        const double sc = pow2(54 - E);
+        const double sc = pow2(54 - E), sc28 = pow2(26 - E);
         const uint32_t lane_base = uint32_t(q * 32) << 16;
-        const int half = nc >> 1;
+        const int k_first = kq * kOzEPT;        // first k of this thread within the stage
         int nflush = 0;
         for (int i = 0; i < nk; ++i) {
             const int fs = i % kOzF, is = i % kOzI;
             mbar_wait(&f_full[fs], (i / kOzF) & 1);
-            double v[16];
+            double v[kOzEPT];
             const unsigned char* ft = fring + fs * kOzF64Bytes;
             if constexpr (!TRANS) {
-                // box h: 128 rows x 16 doubles, SW128: 16-byte chunk c of row r at c ^ (r & 7)
-                const unsigned char* rowp = ft + h * (kOzF64Bytes / 2) + r * 128;
+                // box k/16: 128 rows x 16 doubles, SW128: 16-byte chunk c of row r at c ^ (r & 7)
+                const unsigned char* rowp = ft + (k_first >> 4) * (kOzF64Bytes / 2) + r * 128;
+                const int c0 = (k_first & 15) >> 1;
 #pragma unroll
-                for (int c = 0; c < 8; ++c) {
-                    const double2 d2 = *reinterpret_cast<const double2*>(rowp + ((c ^ (r & 7)) << 4));
+                for (int c = 0; c < kOzEPT / 2; ++c) {
+                    const double2 d2 = *reinterpret_cast<const double2*>(rowp + (((c0 + c) ^ (r & 7)) << 4));
                     v[2 * c] = d2.x;
                     v[2 * c + 1] = d2.y;
                 }
             } else {
-                const double* col = reinterpret_cast<const double*>(ft) + (16 * h) * kOzBM + r;
+                const double* col = reinterpret_cast<const double*>(ft) + k_first * kOzBM + r;
 #pragma unroll
-                for (int j = 0; j < 16; ++j) v[j] = col[j * kOzBM];
+                for (int j = 0; j < kOzEPT; ++j) v[j] = col[j * kOzBM];
             }
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&f_empty[fs]);
-            uint32_t lo[16], hi[16];
+            uint32_t lo[kOzEPT], hi[kOzEPT];
 #pragma unroll
-            for (int j = 0; j < 16; ++j) {
+            for (int j = 0; j < kOzEPT; ++j) {
+#if defined(CORU_OZ_MAGIC)                     // tooling: FP64-pipe rounding (measured slower than F2I: 1.93 vs 1.70 ms)
+                const unsigned long long w = oz_round_biased(v[j], sc, sc28);
+#else
+                (void)sc28;
                 const unsigned long long w = (unsigned long long)__double2ll_rn(v[j] * sc) + kOzBias;
+#endif
                 lo[j] = uint32_t(w);
                 hi[j] = uint32_t(w >> 32);
             }
+            // The fp64 slot is released once every lane has consumed its values: an arrive right
+            // after the loads were ISSUED let the next TMA fill overwrite the slot under a lane's
+            // outstanding load (seen with 16 converter warps: scattered wrong rows, tools/oz_stress.py).
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&f_empty[fs]);
             if (i >= kOzI) mbar_wait(&i_empty[is], ((i / kOzI) - 1) & 1);
-            unsigned char* as = iring + is * kOzIStage + r * 32 + ((h ^ ((r >> 2) & 1)) << 4);
+            // row r of a slice: 32 bytes, the 16-byte half holding k in [16c, 16c+16) at c ^ ((r >> 2) & 1)
+            unsigned char* as = iring + is * kOzIStage + r * 32 + ((((k_first >> 4) ^ ((r >> 2) & 1)) << 4) | (k_first & 15));
 #pragma unroll
             for (int s = 0; s < kOzS; ++s) {
                 const int b = 6 - s;  // byte of V holding slice s
-                uint32_t w4[4];
+                uint32_t w4[kOzEPT / 4];
 #pragma unroll
-                for (int g = 0; g < 4; ++g) {
+                for (int g = 0; g < kOzEPT / 4; ++g) {
                     const uint32_t* src = b < 4 ? lo : hi;
                     const uint32_t bb = uint32_t(b & 3);
                     const uint32_t t01 = __byte_perm(src[4 * g], src[4 * g + 1], bb | ((bb + 4) << 4));
                     const uint32_t t23 = __byte_perm(src[4 * g + 2], src[4 * g + 3], bb | ((bb + 4) << 4));
                     w4[g] = __byte_perm(t01, t23, 0x5410) ^ (s == 0 ? 0u : 0x80808080u);
                 }
-                *reinterpret_cast<uint4*>(as + s * kOzASlice) = make_uint4(w4[0], w4[1], w4[2], w4[3]);
+                if constexpr (kOzEPT == 16)
+                    *reinterpret_cast<uint4*>(as + s * kOzASlice) = make_uint4(w4[0], w4[1], w4[2], w4[3]);
+                else
+                    *reinterpret_cast<uint2*>(as + s * kOzASlice) = make_uint2(w4[0], w4[1]);
             }
             asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
             __syncwarp();
@@ -385,7 +428,7 @@ __global__ void __launch_bounds__(kOzThreads, 1)
                     out = p.C + split * p.split_stride + row * p.N;
                 else
                     out = p.C + row * p.ldc;
-                for (int cb = h * half; cb < (h + 1) * half; cb += 8) {
+                for (int cb = kq * 8; cb < nc; cb += 8 * kOzKQ) {
                     uint32_t acc[kOzS][8];
 #pragma unroll
                     for (int L = 0; L < kOzS; ++L) tmem_ld8(tmem + lane_base + uint32_t(L * nc + cb), acc[L]);
@@ -416,6 +459,240 @@ __global__ void __launch_bounds__(kOzThreads, 1)
     if (warp == 2) {
         tc_fence_after();
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;\n" ::"r"(tmem) : "memory");
+    }
+}
+
+// ---- pre-converted digit planes ----------------------------------------------------------------
+// A decomposition streams the same A 2q+3 times, and a sketch wider than one N-chunk is served by
+// several CTAs per row tile, so the kernel above converts every entry of A (2q+3) x nch times —
+// and the converters, not the tensor pipe, set its pace (ncu: tensor pipe 30 % active; F2I / PRMT
+// streams on two to four warps per scheduler; the shared-memory pipe at ~75 % carrying the fp64
+// staging next to the operands). Instead the decomposition converts A ONCE into its digit planes
+// (k_oz_planes: one read of A, 14 bytes written per entry) and every A-pass is a pure int8 GEMM
+// over them:
+//   PN [7][rows][ldn]  slices of V = rint(a · 2^(54 - E_row)), K-major for op N (rows x cols)
+//   PT [7][cols][ldt]  slices of rint(a · 2^(54 - F_col)), TRANSPOSED: K-major for op T (A^T is
+//                      stored as digit planes; the fp64 A^T is still never formed)
+// k_apass_ozp: warp 0 TMA producer (one 3-D box of the 7 A slices of the row tile + one of the 7
+// X slices of the chunk per stage, SWIZZLE_32B), warp 1 MMA issuer (the same stacked MMAs),
+// warps 4..7 read the level accumulators back at each flush. No converter, no fp64 staging: 139 KB
+// of shared-memory traffic per stage instead of 203 KB, and A costs 7 B/entry/pass from HBM.
+// (A slices through TMEM — tcgen05.st by the converters, "ts" MMAs — were measured too: 1.84 ms
+// per C3 pass against 1.70 ms, the converters stay the bottleneck.)
+constexpr int kPzStages = 5;
+constexpr int kPzStage = kOzS * (kOzASlice + kOzXSlice);        // 42 KB
+constexpr int kPzThreads = 256;
+constexpr int kPzSmem = 1024 + kPzStages * kPzStage + 256;
+
+__global__ void __launch_bounds__(kPzThreads, 1)
+    k_apass_ozp(const __grid_constant__ CUtensorMap tmP, const __grid_constant__ CUtensorMap tmXa,
+                const __grid_constant__ CUtensorMap tmXb, const __grid_constant__ OzArgs p) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    unsigned char* sm = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+    uint64_t* bars = reinterpret_cast<uint64_t*>(sm + kPzStages * kPzStage);
+    uint64_t* full = bars;
+    uint64_t* empty = bars + kPzStages;
+    uint64_t* acc_full = empty + kPzStages;
+    uint64_t* acc_empty = acc_full + 1;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 1);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    int bid = blockIdx.x;
+    const int chunk = bid % p.nch;
+    bid /= p.nch;
+    const int mt = bid % p.mtiles;
+    const int split = bid / p.mtiles;
+    const int n0 = p.n0[chunk], nc = p.nc[chunk];
+    const int64_t m0 = int64_t(mt) * kOzBM;
+    const int64_t ktiles = (p.K + kOzBK - 1) / kOzBK;
+    const int64_t kt0 = int64_t(split) * p.kt_per_split;
+    const int nk = int((ktiles < kt0 + p.kt_per_split ? ktiles : kt0 + p.kt_per_split) - kt0);
+
+    if (warp == 0 && lane == 0) {
+        for (int s = 0; s < kPzStages; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 1);
+        }
+        mbar_init(acc_full, 1);
+        mbar_init(acc_empty, 4);
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+        asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&tmP)) : "memory");
+        asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(nc == p.nc_a ? &tmXa : &tmXb))
+                     : "memory");
+    }
+    if (warp == 2) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;\n" ::"r"(smem_u32(tmem_slot))
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n" ::: "memory");
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+
+    if (warp == 0) {
+        // ===== TMA producer: the 7 A slices of the row tile and the 7 X slices of the chunk =====
+        const uint32_t tx = uint32_t(kOzS * kOzASlice + kOzS * nc * kOzBK);
+        for (int i = 0; i < nk; ++i) {
+            const int s = i % kPzStages;
+            const int k0 = int((kt0 + i) * kOzBK);
+            if (i >= kPzStages) mbar_wait(&empty[s], ((i / kPzStages) - 1) & 1);
+            if (lane == 0) {
+                unsigned char* st = sm + s * kPzStage;
+                mbar_expect_tx(&full[s], tx);
+                tma_load_3d(st, &tmP, k0, int(m0), 0, &full[s]);
+                tma_load_3d(st + kOzXOff, nc == p.nc_a ? &tmXa : &tmXb, k0, n0, 0, &full[s]);
+            }
+            __syncwarp();
+        }
+    } else if (warp == 1) {
+        // ===== MMA issuer =====
+        for (int i = 0; i < nk; ++i) {
+            const int s = i % kPzStages;
+            const int ci = i / kOzChunkStages;
+            const bool first = (i % kOzChunkStages) == 0;
+            if (first && ci > 0) mbar_wait(acc_empty, (ci - 1) & 1);
+            mbar_wait(&full[s], (i / kPzStages) & 1);
+            tc_fence_after();
+            if (lane == 0) {
+                const uint32_t ab = smem_u32(sm + s * kPzStage);
+                const uint32_t xb = ab + kOzXOff;
+#pragma unroll
+                for (int sl = 0; sl < kOzS; ++sl) {
+                    // A slice sl x X slices 0..6-sl -> levels sl..6 (TMEM columns [sl·nc, 7·nc))
+                    const int ntot = (kOzS - sl) * nc;
+                    const uint64_t ad = sdesc_sw32(ab + sl * kOzASlice);
+                    for (int c0 = 0; c0 < ntot; c0 += 256) {
+                        const int n = ntot - c0 < 256 ? ntot - c0 : 256;
+                        mma_i8(tmem + uint32_t(sl * nc + c0), ad, sdesc_sw32(xb + c0 * kOzBK), idesc_i8(n),
+                               (first && sl == 0) ? 0u : 1u);
+                    }
+                }
+                mma_commit(&empty[s]);
+                if ((i % kOzChunkStages) == kOzChunkStages - 1 || i == nk - 1) mma_commit(acc_full);
+            }
+            __syncwarp();
+        }
+    } else if (warp >= 4) {
+        // ===== flushes: fp64 += sum_L acc_L 2^(-8L) · 2^(E + F_j - 12), own row, fixed order =====
+        const int q = warp & 3;
+        const int r = q * 32 + lane;
+        const int64_t row = m0 + r;
+        const int E = row < p.Mo ? p.eA[row] : 0;
+        const uint32_t lane_base = uint32_t(q * 32) << 16;
+        double* out = p.split_stride > 0 ? p.C + split * p.split_stride + row * p.N : p.C + row * p.ldc;
+        const int nfl = (nk + kOzChunkStages - 1) / kOzChunkStages;
+        for (int f = 0; f < nfl; ++f) {
+            mbar_wait(acc_full, f & 1);
+            tc_fence_after();
+            for (int cb = 0; cb < nc; cb += 8) {
+                uint32_t acc[kOzS][8];
+#pragma unroll
+                for (int L = 0; L < kOzS; ++L) tmem_ld8(tmem + lane_base + uint32_t(L * nc + cb), acc[L]);
+                asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                    const int col = n0 + cb + j;
+                    double sum = double(int(acc[kOzS - 1][j]));
+#pragma unroll
+                    for (int L = kOzS - 2; L >= 0; --L) sum = fma(sum, 0.00390625, double(int(acc[L][j])));
+                    if (row < p.Mo && col < p.N) {
+                        const int ex = E + p.eX[col] - 12;
+                        // sum · 2^ex in two exact steps (ex may leave the normal range of one factor)
+                        const double val = (sum * pow2(ex >> 1)) * pow2(ex - (ex >> 1));
+                        out[col] = f == 0 ? val : out[col] + val;
+                    }
+                }
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(acc_empty);
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 2) {
+        tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;\n" ::"r"(tmem) : "memory");
+    }
+}
+
+// A (rows x cols, lda) -> PN and PT. One 64 x 64 tile per CTA through shared memory (row stride 66
+// doubles: the row-wise 16-byte reads of 8 consecutive rows and the column-wise 8-byte reads of 16
+// consecutive columns are both conflict-free); a thread converts 16 entries of one row (row scale)
+// and 16 entries of one column (column scale) and stores one 16-byte chunk per slice and plane.
+constexpr int kPlTile = 64, kPlLd = 66;
+__device__ __forceinline__ void oz_store_slices16(const double (&v)[16], double sc, uint8_t* dst, int64_t plane_stride) {
+    uint32_t lo[16], hi[16];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+        const unsigned long long w = (unsigned long long)__double2ll_rn(v[j] * sc) + kOzBias;
+        lo[j] = uint32_t(w);
+        hi[j] = uint32_t(w >> 32);
+    }
+#pragma unroll
+    for (int s = 0; s < kOzS; ++s) {
+        const int b = 6 - s;
+        uint32_t w4[4];
+#pragma unroll
+        for (int g = 0; g < 4; ++g) {
+            const uint32_t* src = b < 4 ? lo : hi;
+            const uint32_t bb = uint32_t(b & 3);
+            const uint32_t t01 = __byte_perm(src[4 * g], src[4 * g + 1], bb | ((bb + 4) << 4));
+            const uint32_t t23 = __byte_perm(src[4 * g + 2], src[4 * g + 3], bb | ((bb + 4) << 4));
+            w4[g] = __byte_perm(t01, t23, 0x5410) ^ (s == 0 ? 0u : 0x80808080u);
+        }
+        *reinterpret_cast<uint4*>(dst + s * plane_stride) = make_uint4(w4[0], w4[1], w4[2], w4[3]);
+    }
+}
+
+__global__ void __launch_bounds__(256) k_oz_planes(const double* __restrict__ A, int64_t lda, int64_t rows, int64_t cols,
+                                                   const int* __restrict__ erow, const int* __restrict__ ecol,
+                                                   uint8_t* __restrict__ PN, int64_t ldn, uint8_t* __restrict__ PT,
+                                                   int64_t ldt) {
+    __shared__ __align__(16) double tile[kPlTile * kPlLd];
+    const int64_t c0 = int64_t(blockIdx.x) * kPlTile, r0 = int64_t(blockIdx.y) * kPlTile;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const bool vec = (lda & 1) == 0 && (reinterpret_cast<uintptr_t>(A) & 15) == 0;
+#pragma unroll
+    for (int it = 0; it < 8; ++it) {
+        const int r = it * 8 + warp, c = 2 * lane;
+        const int64_t gr = r0 + r, gc = c0 + c;
+        double2 v = make_double2(0.0, 0.0);
+        if (gr < rows) {
+            if (vec && gc + 1 < cols) {
+                v = *reinterpret_cast<const double2*>(A + gr * lda + gc);
+            } else {
+                if (gc < cols) v.x = A[gr * lda + gc];
+                if (gc + 1 < cols) v.y = A[gr * lda + gc + 1];
+            }
+        }
+        *reinterpret_cast<double2*>(&tile[r * kPlLd + c]) = v;
+    }
+    __syncthreads();
+    {   // PN: row r = 8·warp + lane % 8, columns 16·(lane / 8) .. +15, row scale
+        const int r = 8 * warp + (lane & 7), cq = lane >> 3;
+        const int64_t gr = r0 + r, gc = c0 + 16 * cq;
+        if (gr < rows && gc < cols) {
+            double v[16];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                const double2 d2 = *reinterpret_cast<const double2*>(&tile[r * kPlLd + 16 * cq + 2 * i]);
+                v[2 * i] = d2.x;
+                v[2 * i + 1] = d2.y;
+            }
+            oz_store_slices16(v, pow2(54 - erow[gr]), PN + gr * ldn + gc, rows * ldn);
+        }
+    }
+    {   // PT: column c = 16·(warp % 4) + lane % 16, rows 16·(2·(warp / 4) + lane / 16) .. +15, column scale
+        const int c = 16 * (warp & 3) + (lane & 15), rg = 2 * (warp >> 2) + (lane >> 4);
+        const int64_t gc = c0 + c, gr = r0 + 16 * rg;
+        if (gc < cols && gr < rows) {
+            double v[16];
+#pragma unroll
+            for (int j = 0; j < 16; ++j) v[j] = tile[(16 * rg + j) * kPlLd + c];
+            oz_store_slices16(v, pow2(54 - ecol[gc]), PT + gc * ldt + gr, cols * ldt);
+        }
     }
 }
 
@@ -640,8 +917,28 @@ cudaError_t gemm_oz_exponents(const double* A, int64_t lda, int64_t rows, int64_
     return cudaGetLastError();
 }
 
-cudaError_t gemm_oz(Op op, const double* A, int64_t lda, const int* eA, const double* X, int64_t ldx, double* C,
-                    int64_t ldc, int64_t Mo, int64_t K, int N, void* ws, int num_sms, cudaStream_t st) {
+OzPlaneDims gemm_oz_plane_dims(int64_t rows, int64_t cols) {
+    OzPlaneDims d;
+    // plane rows start on 128-byte lines: a 32-byte box row never straddles two L2 sectors (an
+    // unaligned row pitch cost 1.5x the L2 -> SM traffic: ncu l1tex__m_xbar2l1tex_read_bytes)
+    d.ldn = (cols + 127) / 128 * 128;
+    d.ldt = (rows + 127) / 128 * 128;
+    d.pn_bytes = align_up(size_t(kOzS) * size_t(rows) * size_t(d.ldn), 256);
+    d.pt_bytes = align_up(size_t(kOzS) * size_t(cols) * size_t(d.ldt), 256);
+    return d;
+}
+
+cudaError_t gemm_oz_planes(const double* A, int64_t lda, int64_t rows, int64_t cols, const int* erow, const int* ecol,
+                           uint8_t* planes, cudaStream_t st) {
+    const OzPlaneDims d = gemm_oz_plane_dims(rows, cols);
+    const dim3 grid(unsigned((cols + kPlTile - 1) / kPlTile), unsigned((rows + kPlTile - 1) / kPlTile));
+    k_oz_planes<<<grid, 256, 0, st>>>(A, lda, rows, cols, erow, ecol, planes, d.ldn, planes + d.pn_bytes, d.ldt);
+    return cudaGetLastError();
+}
+
+cudaError_t gemm_oz(Op op, const double* A, int64_t lda, const OzPlanes* pl, const int* eA, const double* X,
+                    int64_t ldx, double* C, int64_t ldc, int64_t Mo, int64_t K, int N, void* ws, int num_sms,
+                    cudaStream_t st) {
     const OzShape s = oz_shape(Mo, K, N, num_sms);
     unsigned char* w = static_cast<unsigned char*>(ws);
     uint8_t* xs = w;
@@ -661,7 +958,18 @@ cudaError_t gemm_oz(Op op, const double* A, int64_t lda, const int* eA, const do
         if (e != cudaSuccess) return e;
     }
     CUtensorMap ta, tx;
-    if (op == Op::N) {
+    if (pl) {
+        // digit planes of op(A): (k, row, slice), one box = the 7 slices of a 128-row tile
+        auto fn = oz_encode_fn();
+        const cuuint64_t dims[3] = {cuuint64_t(K), cuuint64_t(Mo), cuuint64_t(kOzS)};
+        const cuuint64_t str[2] = {cuuint64_t(pl->ld), cuuint64_t(pl->ld) * cuuint64_t(pl->rows)};
+        const cuuint32_t box[3] = {kOzBK, kOzBM, cuuint32_t(kOzS)};
+        const cuuint32_t es[3] = {1, 1, 1};
+        if (fn(&ta, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<uint8_t*>(pl->p), dims, str, box, es,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_32B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+            return cudaErrorInvalidValue;
+    } else if (op == Op::N) {
         const cuuint64_t dims[2] = {cuuint64_t(K), cuuint64_t(Mo)};
         const cuuint32_t box[2] = {16, kOzBM};
         if (!oz_map(&ta, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, A, dims, cuuint64_t(lda) * 8, box, CU_TENSOR_MAP_SWIZZLE_128B))
@@ -705,7 +1013,10 @@ cudaError_t gemm_oz(Op op, const double* A, int64_t lda, const int* eA, const do
     a.eA = eA;
     a.eX = fx;
     const unsigned grid = unsigned(int64_t(s.nch) * s.mtiles * s.splits);
-    if (op == Op::N) {
+    if (pl) {
+        allow_max_smem(k_apass_ozp);
+        k_apass_ozp<<<grid, kPzThreads, kPzSmem, st>>>(ta, tx, txb, a);
+    } else if (op == Op::N) {
         allow_max_smem(k_apass_oz<false>);
         k_apass_oz<false><<<grid, kOzThreads, kOzSmem, st>>>(ta, tx, txb, a);
     } else {

@@ -36,8 +36,12 @@ SHAPES = [(1000, 776, 25, 0), (1000, 776, 60, 1), (2048, 1024, 112, 0), (1024, 2
           (520, 300, 256, 1), (129, 4098, 48, 0), (4100, 258, 64, 1)]
 
 
+OZ_ENGINES = [2, 3]  # F64_OZAKI_INLINE (digits converted inside the A-pass kernel), F64_OZAKI_PLANES (digit planes)
+
+
+@pytest.mark.parametrize("engine", OZ_ENGINES)
 @pytest.mark.parametrize("m,k,n,op", SHAPES)
-def test_oz_accuracy_vs_extended(ctx, m, k, n, op):
+def test_oz_accuracy_vs_extended(ctx, m, k, n, op, engine):
     """Dense operands of uniform magnitude (the A-passes' data): the emulated product is within a
     small factor of native fp64 (median entry error <= 4x DMMA's against the exact product;
     measured 2-3x: 54-bit digits against the row / column maximum plus the dropped levels >= 7),
@@ -47,7 +51,7 @@ def test_oz_accuracy_vs_extended(ctx, m, k, n, op):
     kk = m if op else k
     x = rng.standard_normal((kk, n))
     ex = _exact(a, x, op)
-    c_oz = _run(ctx, a, x, op, 0)
+    c_oz = _run(ctx, a, x, op, engine)
     c_dm = _run(ctx, a, x, op, 1)
     scale = (np.abs(a.T if op else a).astype(np.longdouble) @ np.abs(x).astype(np.longdouble))
     err_oz = np.abs(c_oz - ex) / scale
@@ -58,8 +62,9 @@ def test_oz_accuracy_vs_extended(ctx, m, k, n, op):
     assert np.median(err_oz) <= 4 * np.median(err_dm) + 1e-18, (np.median(err_oz), np.median(err_dm))
 
 
+@pytest.mark.parametrize("engine", OZ_ENGINES)
 @pytest.mark.parametrize("m,k,n,op", SHAPES[2:6])
-def test_oz_scaled_rows_and_columns(ctx, m, k, n, op):
+def test_oz_scaled_rows_and_columns(ctx, m, k, n, op, engine):
     """Rows / columns of op(A) and columns of X 2^±20..40 apart: the per-row and per-column
     scales absorb them; the error stays within the scheme's bound (54-bit digits against the
     row / column maximum, dropped levels >= 7) and the per-entry contract 1e-12·(|A||X|)."""
@@ -70,7 +75,7 @@ def test_oz_scaled_rows_and_columns(ctx, m, k, n, op):
     kk = m if op else k
     x = rng.standard_normal((kk, n)) * np.exp2(rng.integers(-30, 30, size=(1, n)))
     ex = _exact(a, x, op)
-    c_oz = _run(ctx, a, x, op, 0)
+    c_oz = _run(ctx, a, x, op, engine)
     scale = (np.abs(a.T if op else a).astype(np.longdouble) @ np.abs(x).astype(np.longdouble))
     assert float((np.abs(c_oz - ex) / scale).max()) <= 1e-12
     rowmax = np.abs(a.T if op else a).max(axis=1, keepdims=True)
@@ -78,21 +83,26 @@ def test_oz_scaled_rows_and_columns(ctx, m, k, n, op):
     assert np.all(np.abs(c_oz - ex) <= kk * 2.0 ** -49 * rowmax * colmax)
 
 
-def test_oz_deterministic_and_zero_rows(ctx):
+@pytest.mark.parametrize("engine", OZ_ENGINES)
+def test_oz_deterministic_and_zero_rows(ctx, engine):
+    """Bitwise repeatable (a multi-wave grid: 20000 rows = 157 row tiles x 2 chunks), exact zeros for
+    zero rows / columns, and the two Ozaki engines agree bit for bit (same digits, same MMAs)."""
     rng = np.random.default_rng(5)
-    a = rng.standard_normal((3000, 2000))
+    a = rng.standard_normal((20000, 2000))
     a[7] = 0.0            # an all-zero row
     a[:, 11] = 0.0        # an all-zero column (zero output row for op T)
     x = rng.standard_normal((2000, 110))
-    c1 = _run(ctx, a, x, 0, 0)
-    c2 = _run(ctx, a, x, 0, 0)
-    assert np.array_equal(c1, c2)
+    c1 = _run(ctx, a, x, 0, engine)
+    for _ in range(6):
+        assert np.array_equal(_run(ctx, a, x, 0, engine), c1)
     assert np.all(c1[7] == 0.0)
-    y = rng.standard_normal((3000, 110))
-    t1 = _run(ctx, a, y, 1, 0)
-    t2 = _run(ctx, a, y, 1, 0)
-    assert np.array_equal(t1, t2)
+    assert np.array_equal(c1, _run(ctx, a, x, 0, 5 - engine))
+    y = rng.standard_normal((20000, 110))
+    t1 = _run(ctx, a, y, 1, engine)
+    for _ in range(3):
+        assert np.array_equal(_run(ctx, a, y, 1, engine), t1)
     assert np.all(t1[11] == 0.0)
+    assert np.array_equal(t1, _run(ctx, a, y, 1, 5 - engine))
 
 
 def test_oz_split_k_large_k(ctx):
@@ -102,7 +112,8 @@ def test_oz_split_k_large_k(ctx):
     m, n, d = 200000, 256, 112
     a = rng.standard_normal((m, n))
     y = rng.standard_normal((m, d))
-    c = _run(ctx, a, y, 1, 0)
+    c = _run(ctx, a, y, 1, 3)
+    assert np.array_equal(c, _run(ctx, a, y, 1, 2))
     ref = a.T @ y
     scale = np.abs(a).T @ np.abs(y)
     assert float((np.abs(c - ref) / scale).max()) <= 1e-13
@@ -120,3 +131,22 @@ def test_oz_decomposition_matches_dmma(ctx):
     f_oz = cg.corutv(a, 25, 0, seed=cg.RngSeed(42, 0), ctx=ctx)
     assert np.array_equal(f_dm.perm, f_oz.perm)
     assert np.max(np.abs(np.abs(np.diag(f_dm.t)) - np.abs(np.diag(f_oz.t)))) <= 1e-12
+
+
+def test_oz_planes_decomposition_bit_identical_to_inline(ctx):
+    """A whole decomposition (q = 2, wide sketch) with the digit planes is bit-identical to the one
+    that converts A inside every A-pass kernel — the planes hold exactly the digits the kernel
+    would produce (both orientations: row scales for A·X, column scales for A^T·Y)."""
+    import paper_1810_07323_b200 as cg
+    rng = np.random.default_rng(77)
+    a = rng.standard_normal((1500, 900)) * np.exp2(rng.integers(-8, 8, size=(1500, 1)))
+    out = {}
+    for eng in (ctx.F64_OZAKI_INLINE, ctx.F64_OZAKI_PLANES):
+        ctx.set_f64_engine(eng)
+        try:
+            out[eng] = cg.corutv(a, 130, 2, seed=cg.RngSeed(42, 3), ctx=ctx)
+        finally:
+            ctx.set_f64_engine(ctx.F64_AUTO)
+    f1, f2 = out[ctx.F64_OZAKI_INLINE], out[ctx.F64_OZAKI_PLANES]
+    assert np.array_equal(f1.perm, f2.perm)
+    assert np.array_equal(f1.t, f2.t) and np.array_equal(f1.u, f2.u) and np.array_equal(f1.v, f2.v)

@@ -1,13 +1,16 @@
 #!/bin/bash
-# Builds A/B variants of libcoru_gpu.so that differ only in the Ozaki A-pass ring depths
-# (tooling for DESIGN.md §4: pipeline-depth sweep); select one with CORU_LIB_VARIANT=F<f>I<i>.
+# Builds A/B variants of libcoru_gpu.so that differ only in compile-time options of the Ozaki
+# A-pass (gemm_oz.cu): ring depths CORU_OZ_F / CORU_OZ_I and converter k-groups CORU_OZ_KQ
+# (tooling for DESIGN.md §4); select one with CORU_LIB_VARIANT=<name>.
+#   tools/oz_variants.sh "kq2:-DCORU_OZ_KQ=2" "kq4:-DCORU_OZ_KQ=4" "F2I4:-DCORU_OZ_F=2 -DCORU_OZ_I=4"
 set -e
 cd "$(dirname "$0")/../paper_1810_07323_b200/csrc"
 OBJ=../../build/obj
-for fi in "2 4" "3 3" "4 2" "2 3"; do
-  set -- $fi
+for spec in "$@"; do
+  name=${spec%%:*}
+  flags=${spec#*:}
   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 --extended-lambda -Xcompiler -fPIC \
-       -I../../include -DCORU_OZ_F=$1 -DCORU_OZ_I=$2 -c gemm_oz.cu -o $OBJ/gemm_oz_F$1I$2.o
+       -I../../include $flags -c gemm_oz.cu -o $OBJ/gemm_oz_$name.o
   objs=$(ls $OBJ/*.o | grep -v "gemm_oz")
-  nvcc -gencode arch=compute_100a,code=sm_100a -shared -o ../libcoru_gpu_F$1I$2.so $objs $OBJ/gemm_oz_F$1I$2.o -ldl -lpthread
+  nvcc -gencode arch=compute_100a,code=sm_100a -shared -o ../libcoru_gpu_$name.so $objs $OBJ/gemm_oz_$name.o -ldl -lpthread
 done
