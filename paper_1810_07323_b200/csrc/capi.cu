@@ -181,6 +181,7 @@ struct coru_ctx {
     cudaStream_t stream = nullptr;
     cudaStream_t aux = nullptr;  // second stream: the two TSQR trees run concurrently
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+    cudaEvent_t ev_phi = nullptr;  // last H2D copy out of the pinned Φ staging buffer
     static constexpr int kUploadChunks = 8;
     cudaEvent_t ev_chunk[kUploadChunks] = {};  // host-entry upload pipeline (corutv_host)
     int num_sms = 148;
@@ -384,6 +385,13 @@ int oz_prepare(coru_ctx* c, const double* A, int64_t lda, int64_t rows, int64_t 
     c->oz_a = nullptr;
     if (!oz_enabled(c) || !A) return CORU_OK;
     if (!gemm_oz_eligible(std::max(rows, cols), std::min(rows, cols), 1)) return CORU_OK;
+    // The int8 kernel runs one CTA per (128-row tile, 64-column chunk): on a small matrix it cannot
+    // fill the machine and the FP64 stream-K kernel is faster (C2, 4000^2 x 60: 32 CTAs, 187 us per
+    // pass against 83 us on DMMA; C1 likewise). Forced engines skip the test.
+    if (c->f64_engine == CORU_F64_AUTO && getenv("CORU_F64_ENGINE") == nullptr) {
+        const int64_t ctas = ((std::max(rows, cols) + 127) / 128) * ((ncols + 63) / 64);
+        if (ctas < 2 * int64_t(c->num_sms)) return CORU_OK;  // under two waves: DMMA (RPCA 8000^2 x 80 too)
+    }
     size_t cap_bytes = c->oz_e_cap * sizeof(int);
     void* e = c->oz_e;
     CORU_TRY(ensure_dev(c, &e, &cap_bytes, sizeof(int) * size_t(rows + cols), "Ozaki exponents"));
@@ -549,7 +557,7 @@ struct TsqrBufs {
     void carve(Carver& cv, int64_t rows, int d, int smem, int num_sms = 148, bool allow_chol = false) {
         max_smem = smem;
         sms = num_sms;
-        plan = plan_tsqr(rows, d, sizeof(T), smem);
+        plan = plan_tsqr(rows, d, sizeof(T), smem, num_sms);
         v = cv.take<T>(plan.v_elems);
         beta = cv.take<T>(plan.beta_elems);
         tarena = cv.take<T>(plan.t_elems);
@@ -765,7 +773,10 @@ int upload_phi_host(coru_ctx* c, int64_t rows, int cols, int ld, uint64_t seed, 
                     cudaStream_t st) {
     const size_t bytes = size_t(rows) * ld * sizeof(T);
     CORU_TRY(ensure_pinned(c, bytes));
-    CORU_CUDA(cudaStreamSynchronize(st));  // the pinned staging buffer is reused across calls
+    // The pinned staging buffer is reused across calls: wait for the LAST copy out of it only (not
+    // for the stream — the exponent / digit-plane kernels of this call keep running while the host
+    // generates Φ).
+    CORU_CUDA(cudaEventSynchronize(c->ev_phi));
     T* phi = reinterpret_cast<T*>(c->pinned);
     const int64_t total = rows * int64_t(cols);
     const int chunks = int(std::max<int64_t>(1, std::min<int64_t>(8, total / (1 << 17))));
@@ -779,6 +790,7 @@ int upload_phi_host(coru_ctx* c, int64_t rows, int cols, int ld, uint64_t seed, 
                                   cudaMemcpyHostToDevice, st));
         r0 = r1;
     }
+    CORU_CUDA(cudaEventRecord(c->ev_phi, st));
     return CORU_OK;
 }
 
@@ -2096,6 +2108,7 @@ int coru_ctx_create(int device, coru_ctx** out) {
     if (cudaStreamCreateWithFlags(&c->aux, cudaStreamNonBlocking) != cudaSuccess ||
         cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
         cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&c->ev_phi, cudaEventDisableTiming) != cudaSuccess ||
         [&] {
             for (auto& e : c->ev_chunk)
                 if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) return true;
@@ -2128,6 +2141,7 @@ void coru_ctx_destroy(coru_ctx* c) {
     }
     if (c->ev_fork) cudaEventDestroy(c->ev_fork);
     if (c->ev_join) cudaEventDestroy(c->ev_join);
+    if (c->ev_phi) cudaEventDestroy(c->ev_phi);
     for (auto& e : c->ev_chunk)
         if (e) cudaEventDestroy(e);
     if (c->own_stream) cudaStreamDestroy(c->own_stream);

@@ -145,6 +145,62 @@ __device__ __forceinline__ void cta_mm_f64(int M, int N, int K, const double* A,
     }
 }
 
+// Rank-k (k <= 16) update of a block in GLOBAL memory (L2): C(i,j) -= sum_k V(i,k) Z(k,j), with
+// V (M x k) and Z (k x N) in shared memory: V(i,k) = V[k*ldv + i], Z(k,j) = Z[k*ldz + j],
+// C(i,j) = C[j*ldc + i]. The trailing update of the big-block QR: every output tile is a
+// read-modify-write of C, so each warp handles four tiles per iteration and requests their C
+// values before the DMMAs — the generic loop's one-tile-at-a-time dependent load cost ~900 cycles
+// per tile. Same k order per entry as cta_mm_f64.
+__device__ __forceinline__ void cta_rank_update_global(int M, int N, int K, const double* V, int ldv, const double* Z,
+                                                       int ldz, double* C, int ldc) {
+    const int lane = threadIdx.x & 31, warp = int(threadIdx.x >> 5), nw = int(blockDim.x >> 5);
+    const int g = lane >> 2, t = lane & 3;
+    const int tm = (M + 15) >> 4, tn = (N + 7) >> 3, tiles = tm * tn;
+    const int ksteps = (K + 7) >> 3;
+    constexpr int TB = 4;
+    // tiles in column-major order (consecutive tiles of a warp batch walk down the rows of one
+    // 8-column strip: 64-byte segments of consecutive addresses)
+    for (int w0 = warp * TB; w0 < tiles; w0 += nw * TB) {
+        double acc[TB][4], cold[TB][4];
+        int i0[TB], j0[TB];
+#pragma unroll
+        for (int b = 0; b < TB; ++b) {
+            const int w = w0 + b;
+            const bool on = w < tiles;
+            i0[b] = on ? (w % tm) << 4 : M;  // off tiles: every predicate below fails
+            j0[b] = on ? (w / tm) << 3 : N;
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                const int i = i0[b] + g + ((e >> 1) << 3), j = j0[b] + 2 * t + (e & 1);
+                acc[b][e] = 0.0;
+                cold[b][e] = (i < M && j < N) ? C[int64_t(j) * ldc + i] : 0.0;
+            }
+        }
+        for (int ks = 0; ks < ksteps; ++ks) {
+            const int k0 = (ks << 3) + t, k1 = k0 + 4;
+#pragma unroll
+            for (int b = 0; b < TB; ++b) {
+                const int ia = i0[b] + g, ib = ia + 8, jb = j0[b] + g;
+                double a[4], bb[2];
+                a[0] = (ia < M && k0 < K) ? V[k0 * ldv + ia] : 0.0;
+                a[1] = (ib < M && k0 < K) ? V[k0 * ldv + ib] : 0.0;
+                a[2] = (ia < M && k1 < K) ? V[k1 * ldv + ia] : 0.0;
+                a[3] = (ib < M && k1 < K) ? V[k1 * ldv + ib] : 0.0;
+                bb[0] = (jb < N && k0 < K) ? Z[k0 * ldz + jb] : 0.0;
+                bb[1] = (jb < N && k1 < K) ? Z[k1 * ldz + jb] : 0.0;
+                dmma_16x8x8(acc[b], a, bb);
+            }
+        }
+#pragma unroll
+        for (int b = 0; b < TB; ++b)
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                const int i = i0[b] + g + ((e >> 1) << 3), j = j0[b] + 2 * t + (e & 1);
+                if (i < M && j < N) C[int64_t(j) * ldc + i] = cold[b][e] - acc[b][e];
+            }
+    }
+}
+
 // Same contract for any T on the CUDA cores (fp32 path; small fp64 shapes).
 template <typename T>
 __device__ __forceinline__ void cta_mm_simt(int M, int N, int K, const T* A, int ars, int acs, const T* B, int brs,

@@ -31,6 +31,12 @@
 namespace coru_gpu {
 
 #ifdef CORU_QR_PROFILE
+__device__ long long g_qrg_phase[12];  // k_qr_blocked_g, block 0: load, chain, gram, larft, Y, Z, update, export, total
+#define QRG_T(v) long long v = qrp_clock_fwd()
+// the clock is read in the same asm statement as a CTA barrier, so ptxas cannot hoist it above the wait
+#define QRG_ADD(i, v) { long long n_; asm volatile("bar.sync 0;\n\tmov.u64 %0, %%clock64;" : "=l"(n_)::"memory"); \
+                        if (threadIdx.x == 0 && blockIdx.x == 0) g_qrg_phase[i] += n_ - v; v = n_; }
+__device__ __forceinline__ long long qrp_clock_fwd() { long long v; asm volatile("mov.u64 %0, %%clock64;" : "=l"(v)::"memory"); return v; }
 __device__ long long g_qr_phase[12];
 __device__ long long g_qr_tl[3 * 256];  // block 0 chain timeline: arrive / wake / build-start per column  // cycles of block 0: load, panel chains, T factors, trailing, export
 __device__ __forceinline__ long long qrp_clock() {
@@ -59,6 +65,8 @@ __device__ long long g_qr_reg_ph[8];
 #define QRP_DECL
 #define QRP_TL(k, j)
 #define QRP_FLUSH
+#define QRG_T(v)
+#define QRG_ADD(i, v)
 #define QRR_CLK(v, dep)
 #define QRR_ADD(i, dt)
 #endif
@@ -502,7 +510,8 @@ template <typename T>
 struct BigSmem {
     int ldvp;
     T *Vp, *beta, *Gp, *Tp, *Y, *Z, *scratch;
-    __device__ BigSmem(unsigned char* raw, int d, int rb) : ldvp(ld_mod(rb, 8)) {
+    // reflector slots are read in whole 128-row chunks by the register panels: zero-padded past rb
+    __device__ BigSmem(unsigned char* raw, int d, int rb) : ldvp(ld_mod(rb + 128, 8)) {
         T* p = reinterpret_cast<T*>(raw);
         Vp = p;
         p += size_t(kNB) * ldvp;
@@ -519,7 +528,7 @@ struct BigSmem {
         scratch = p;
     }
     static size_t bytes(int d, int rb, size_t eb) {
-        return (size_t(kNB) * ld_mod(rb, 8) + d + (d & 1) + 2 * kNB * kNB + 2 * size_t(kNB) * d + kGemmScratch) * eb;
+        return (size_t(kNB) * ld_mod(rb + 128, 8) + d + (d & 1) + 2 * kNB * kNB + 2 * size_t(kNB) * d + kGemmScratch) * eb;
     }
 };
 
@@ -537,29 +546,159 @@ __global__ void __launch_bounds__(kBThreads, 1)
     const int ldvp = S.ldvp;
     T* W = V + int64_t(b) * d * ldv;  // column-major working block (ld = ldv) in global memory
     T* Tb = Tg + int64_t(b) * npanels(d) * kNB * kNB;
-    for (int cb = 0; cb < d; cb += 128)
-        for (int r = warp * 4; r < rb; r += (kBThreads / 32) * 4) {
-            T v[4][4];
-#pragma unroll
-            for (int q = 0; q < 4; ++q)
-#pragma unroll
-                for (int h = 0; h < 4; ++h) {
-                    const int c = cb + lane + 32 * h;
-                    v[q][h] = (r + q < rb && c < d) ? X[(r0 + r + q) * ldx + c] : T(0);
-                }
-#pragma unroll
-            for (int q = 0; q < 4; ++q)
-#pragma unroll
-                for (int h = 0; h < 4; ++h) {
-                    const int c = cb + lane + 32 * h;
-                    if (r + q < rb && c < d) W[int64_t(c) * ldv + r + q] = v[q][h];
-                }
+    QRG_T(tq);
+    // Rows [r0, r1) of X (row-major) -> column-major working block W, transposed through shared memory
+    // (the reflector slots are free now): 64-row chunks read along the rows, written along the
+    // columns, both coalesced (the direct transposing store touched one line per element).
+    {
+        // chunk rows: up to 64, fewer when d columns of them would not fit the kNB·ldvp slots
+        const int kLR = min(64, (kNB * ldvp) / d - 1), kLLd = kLR + 1;
+        T* stage = S.Vp;
+        for (int rc = 0; rc < rb; rc += kLR) {
+            const int nr = min(kLR, rb - rc);
+            for (int e = tid; e < nr * d; e += kBThreads) {
+                const int r = e / d, c = e % d;
+                stage[c * kLLd + r] = X[(r0 + rc + r) * ldx + c];
+            }
+            __syncthreads();
+            for (int e = tid; e < d * kLR; e += kBThreads) {
+                const int c = e / kLR, r = e % kLR;
+                if (r < nr) W[int64_t(c) * ldv + rc + r] = stage[c * kLLd + r];
+            }
+            __syncthreads();
         }
+    }
     __syncthreads();
+    QRG_ADD(0, tq);
 
+    // Blocks of up to 32·kGRPL rows keep each panel column in REGISTERS while the panel is factored
+    // (lane l holds rows l, l+32, ...): the d sequential reflector steps then run at shared-memory
+    // latency (the reflectors Vp) instead of one L2 round trip per read-modify-write of the column
+    // (~8 us per column step before: 4 levels x ~900 us at C3). Taller blocks use the in-place path.
+    constexpr int kGRPL = sizeof(T) == 8 ? 28 : 56;  // 56 registers of column per lane
+    const bool reg_panel = rb <= 32 * kGRPL;
     for (int p0 = 0, pi = 0; p0 < d; p0 += kNB, ++pi) {
         const int nbp = min(kNB, d - p0);
-        if (warp < nbp) {
+        if (warp < nbp && reg_panel) {
+            // Register layout of my column for this panel: `xs` = the 32-row block that holds the
+            // panel's diagonal rows (one row per lane; rows above the diagonal are final R entries
+            // and are masked by the explicit zeros of the reflectors), x[] = the rows after it in
+            // chunks of 4 x 32 — every loop over them is predicate-free (reflector slots are
+            // zero-padded past rb), with one uniform test per chunk.
+            const int c = p0 + warp;
+            T* col = W + int64_t(c) * ldv;
+            const int hb = (p0 >> 5) << 5, tb = hb + 32;     // head block / first tail row
+            const int nt4 = (max(rb - tb, 0) + 127) >> 7;    // live tail chunks
+            const int rh = hb + lane;
+            T xs = (rh >= p0 && rh < rb) ? col[rh] : T(0);
+            T x[kGRPL];
+#pragma unroll
+            for (int t4 = 0; t4 < kGRPL / 4; ++t4)
+#pragma unroll
+                for (int q4 = 0; q4 < 4; ++q4) {
+                    const int r = tb + 32 * (4 * t4 + q4) + lane;
+                    x[4 * t4 + q4] = (t4 < nt4 && r < rb) ? col[r] : T(0);
+                }
+            for (int jj = 0; jj <= warp; ++jj) {
+                const int j = p0 + jj, jl = j - hb;
+                const int bar = 1 + jj, cnt = 32 * (nbp - jj);
+                if (jj < warp) {
+                    // apply H_j (built by warp jj) to my column   (apply_reflector, qr.hpp:49-57)
+                    named_bar_sync(bar, cnt);
+                    const T bj = S.beta[j];
+                    if (bj == T(0)) continue;
+                    const T* vj = S.Vp + jj * ldvp;
+                    const T vh = vj[rh];
+                    const T* vt = vj + tb + lane;
+                    T s0 = vh * xs, s1 = 0, s2 = 0, s3 = 0;
+#pragma unroll
+                    for (int t4 = 0; t4 < kGRPL / 4; ++t4)
+                        if (t4 < nt4) {
+                            s0 += vt[128 * t4] * x[4 * t4];
+                            s1 += vt[128 * t4 + 32] * x[4 * t4 + 1];
+                            s2 += vt[128 * t4 + 64] * x[4 * t4 + 2];
+                            s3 += vt[128 * t4 + 96] * x[4 * t4 + 3];
+                        }
+                    const T s = warp_sum((s0 + s1) + (s2 + s3)) * bj;
+                    xs -= s * vh;
+#pragma unroll
+                    for (int t4 = 0; t4 < kGRPL / 4; ++t4)
+                        if (t4 < nt4) {
+                            x[4 * t4] -= s * vt[128 * t4];
+                            x[4 * t4 + 1] -= s * vt[128 * t4 + 32];
+                            x[4 * t4 + 2] -= s * vt[128 * t4 + 64];
+                            x[4 * t4 + 3] -= s * vt[128 * t4 + 96];
+                        }
+                } else {
+                    // build reflector j from my column   (make_reflector, qr.hpp:32-45)
+                    T q0 = lane > jl ? xs * xs : T(0), q1 = 0, q2 = 0, q3 = 0;
+#pragma unroll
+                    for (int t4 = 0; t4 < kGRPL / 4; ++t4)
+                        if (t4 < nt4) {
+                            q0 += x[4 * t4] * x[4 * t4];
+                            q1 += x[4 * t4 + 1] * x[4 * t4 + 1];
+                            q2 += x[4 * t4 + 2] * x[4 * t4 + 2];
+                            q3 += x[4 * t4 + 3] * x[4 * t4 + 3];
+                        }
+                    const T sig = warp_sum((q0 + q1) + (q2 + q3));
+                    const T x0 = __shfl_sync(0xffffffffu, xs, jl);
+                    T bj = 0;
+                    if (sig != T(0)) {
+                        T mu, v0, rv;
+                        reflector_scalars(x0, sig, mu, v0, bj, rv);
+                        xs = lane > jl ? xs * rv : (lane == jl ? mu : xs);
+#pragma unroll
+                        for (int t4 = 0; t4 < kGRPL / 4; ++t4)
+                            if (t4 < nt4) {
+                                x[4 * t4] *= rv;
+                                x[4 * t4 + 1] *= rv;
+                                x[4 * t4 + 2] *= rv;
+                                x[4 * t4 + 3] *= rv;
+                            }
+                    }
+                    // explicit reflector: 0 above j, 1 at j, v below, 0 past rb (x is 0 there)
+                    T* vj = S.Vp + jj * ldvp;
+                    const T vmine = lane > jl ? xs : (lane == jl ? T(1) : T(0));
+                    vj[rh] = vmine;
+                    T* vt = vj + tb + lane;
+#pragma unroll
+                    for (int t4 = 0; t4 < kGRPL / 4; ++t4)
+                        if (t4 < nt4) {
+                            vt[128 * t4] = x[4 * t4];
+                            vt[128 * t4 + 32] = x[4 * t4 + 1];
+                            vt[128 * t4 + 64] = x[4 * t4 + 2];
+                            vt[128 * t4 + 96] = x[4 * t4 + 3];
+                        }
+                    if (lane == 0) S.beta[j] = bj;
+                    if (jj + 1 < nbp) named_bar_arrive(bar, cnt);
+                    // Off the chain: G(a, w) = v_a^T v_w for the earlier reflectors of the panel (the
+                    // compact-WY recurrence needs the strict upper triangle), from the registers that
+                    // still hold v_w — instead of a 16 x 16 x K CTA GEMM after the panel.
+                    for (int a = 0; a < jj; ++a) {
+                        const T* va = S.Vp + a * ldvp + tb + lane;
+                        T g0 = S.Vp[a * ldvp + rh] * vmine, g1 = 0, g2 = 0, g3 = 0;
+#pragma unroll
+                        for (int t4 = 0; t4 < kGRPL / 4; ++t4)
+                            if (t4 < nt4) {
+                                g0 += va[128 * t4] * x[4 * t4];
+                                g1 += va[128 * t4 + 32] * x[4 * t4 + 1];
+                                g2 += va[128 * t4 + 64] * x[4 * t4 + 2];
+                                g3 += va[128 * t4 + 96] * x[4 * t4 + 3];
+                            }
+                        const T gsum = warp_sum((g0 + g1) + (g2 + g3));
+                        if (lane == 0) S.Gp[a * kNB + jj] = gsum;
+                    }
+                }
+            }
+            if (rh >= p0 && rh < rb) col[rh] = xs;
+#pragma unroll
+            for (int t4 = 0; t4 < kGRPL / 4; ++t4)
+#pragma unroll
+                for (int q4 = 0; q4 < 4; ++q4) {
+                    const int r = tb + 32 * (4 * t4 + q4) + lane;
+                    if (t4 < nt4 && r < rb) col[r] = x[4 * t4 + q4];
+                }
+        } else if (warp < nbp) {
             const int c = p0 + warp;
             T* col = W + int64_t(c) * ldv;
             for (int jj = 0; jj <= warp; ++jj) {
@@ -611,24 +750,36 @@ __global__ void __launch_bounds__(kBThreads, 1)
             }
         }
         __syncthreads();
+        QRG_ADD(1, tq);
         const int K = rb - p0;
-        cta_mm(nbp, nbp, K, S.Vp + p0, ldvp, 1, S.Vp + p0, 1, ldvp, S.Gp, kNB, 1, T(1), false, S.scratch, kGemmScratch);
-        __syncthreads();
+        if (!reg_panel) {
+            cta_mm(nbp, nbp, K, S.Vp + p0, ldvp, 1, S.Vp + p0, 1, ldvp, S.Gp, kNB, 1, T(1), false, S.scratch, kGemmScratch);
+            __syncthreads();
+        }
+        QRG_ADD(2, tq);
         if (warp == 0) {
             warp_larft<T>(nbp, S.Gp, kNB, S.beta + p0, S.Tp, kNB);
             T* Tpg = Tb + pi * kNB * kNB;
             for (int e = lane; e < kNB * kNB; e += 32) Tpg[e] = S.Tp[e];
         }
         __syncthreads();
+        QRG_ADD(3, tq);
         const int c0 = p0 + nbp, nc = d - c0;
         if (nc > 0) {
             T* C = W + int64_t(c0) * ldv + p0;
             cta_mm(nbp, nc, K, S.Vp + p0, ldvp, 1, C, 1, ldv, S.Y, d, 1, T(1), false, S.scratch, kGemmScratch);
             __syncthreads();
+            QRG_ADD(4, tq);
             cta_mm(nbp, nc, nbp, S.Tp, 1, kNB, S.Y, d, 1, S.Z, d, 1, T(1), false, S.scratch, kGemmScratch);
             __syncthreads();
-            cta_mm(K, nc, nbp, S.Vp + p0, 1, ldvp, S.Z, d, 1, C, 1, ldv, T(-1), true, S.scratch, kGemmScratch);
+            QRG_ADD(5, tq);
+            if constexpr (sizeof(T) == 8)
+                cta_rank_update_global(K, nc, nbp, reinterpret_cast<const double*>(S.Vp + p0), ldvp,
+                                       reinterpret_cast<const double*>(S.Z), d, reinterpret_cast<double*>(C), ldv);
+            else
+                cta_mm(K, nc, nbp, S.Vp + p0, 1, ldvp, S.Z, d, 1, C, 1, ldv, T(-1), true, S.scratch, kGemmScratch);
             __syncthreads();
+            QRG_ADD(6, tq);
         }
     }
     for (int e = tid; e < d * d; e += kBThreads) {
@@ -639,6 +790,7 @@ __global__ void __launch_bounds__(kBThreads, 1)
     __syncthreads();
     for (int c = warp; c < d; c += kBThreads / 32)  // explicit reflectors in place
         for (int r = lane; r <= c && r < rb; r += 32) W[int64_t(c) * ldv + r] = T(r == c ? 1 : 0);
+    QRG_ADD(7, tq);
 }
 
 template <typename T>
@@ -954,7 +1106,7 @@ size_t wide_factor_smem_bytes(int rbmax, int d, size_t eb) {
 
 }  // namespace
 
-TsqrPlan plan_tsqr(int64_t m, int d, size_t eb, int max_smem) {
+TsqrPlan plan_tsqr(int64_t m, int d, size_t eb, int max_smem, int num_sms) {
     TsqrPlan p;
     p.m = m;
     p.d = d;
@@ -998,6 +1150,10 @@ TsqrPlan plan_tsqr(int64_t m, int d, size_t eb, int max_smem) {
         L.rows = rows;
         // every block strictly taller than d (so the tree always shrinks), at most `target` rows
         int64_t nb = std::max<int64_t>(1, (rows + target - 1) / target);
+        // one CTA per block and SM: a level of more blocks than SMs runs in whole waves, so round
+        // the block count up to a multiple of the SM count (C3 level 0: 249 blocks of 803 rows were
+        // two waves; 296 blocks of 676 rows are two FULL waves of shorter blocks)
+        if (nb > num_sms) nb = (nb + num_sms - 1) / num_sms * num_sms;
         nb = std::max<int64_t>(1, std::min<int64_t>(nb, rows / (d + 1)));
         L.nb = int(nb);
         L.rbmax = int((rows + nb - 1) / nb);
@@ -1150,3 +1306,14 @@ template cudaError_t tsqr_form_q<float>(const TsqrPlan&, const float*, float*, f
                                         int, cudaStream_t, const int*);
 
 }  // namespace coru_gpu
+
+#ifdef CORU_QR_PROFILE
+// Tooling (tools/qrg_phases.py, a -DCORU_QR_PROFILE build): cycles block 0 of k_qr_blocked_g spent
+// per phase since the last reset.
+extern "C" int coru_debug_qrg_phases(long long* out, int reset) {
+    long long z[12] = {};
+    if (cudaMemcpyFromSymbol(out, coru_gpu::g_qrg_phase, sizeof(z)) != cudaSuccess) return 1;
+    if (reset && cudaMemcpyToSymbol(coru_gpu::g_qrg_phase, z, sizeof(z)) != cudaSuccess) return 1;
+    return 0;
+}
+#endif

@@ -33,7 +33,7 @@ struct TsqrPlan {
     size_t elem_bytes = 8;
 };
 
-TsqrPlan plan_tsqr(int64_t m, int d, size_t elem_bytes, int max_smem_bytes);
+TsqrPlan plan_tsqr(int64_t m, int d, size_t elem_bytes, int max_smem_bytes, int num_sms = 148);
 
 // Factor B (m x d, row-major, ldb) through the tree. R (d x d, row-major, upper, exact zeros
 // below) is written to r_out (ld = d) — on device.
