@@ -92,6 +92,9 @@ enum { CORU_F32_AUTO = 0, CORU_F32_SIMT = 1, CORU_F32_TC = 2 };
  *     into the A-pass kernel / into the once-per-decomposition digit planes. */
 enum { CORU_F64_AUTO = 0, CORU_F64_DMMA = 1, CORU_F64_OZAKI_INLINE = 2, CORU_F64_OZAKI_PLANES = 3 };
 int coru_ctx_set_f64_engine(coru_ctx* ctx, int mode);
+/* Engine the last fp64 decomposition's A-passes ran on: 0 = FP64 DMMA, 1 = Ozaki with in-kernel
+ * digits, 2 = Ozaki over digit planes (bench evidence: which roofline applies). */
+int coru_ctx_last_f64_engine(coru_ctx* ctx);
 int coru_ctx_set_f32_path(coru_ctx* ctx, int mode);
 /* QR of wide sketches (more than 128 columns; householder_qr at corutv.hpp:59-60): 1 (default) =
  * CholeskyQR2 in fp64 with a device-side fall-back to the Householder tree when the sketch is

@@ -143,6 +143,7 @@ def load_library():
     L.coru_ctx_set_f32_path.argtypes = [p, i32]
     L.coru_ctx_set_wide_qr.argtypes = [p, i32]
     L.coru_ctx_set_f64_engine.argtypes = [p, i32]
+    L.coru_ctx_last_f64_engine.argtypes = [p]
     L.coru_comm_unique_id.argtypes = [p]
     L.coru_ctx_init_comm.argtypes = [p, i32, i32, p]
     L.coru_ctx_set_profiling.argtypes = [p, i32]
@@ -270,6 +271,11 @@ class Context:
         into digit planes, by a cost model), F64_DMMA (FP64 DMMA for everything),
         F64_OZAKI_INLINE / F64_OZAKI_PLANES (force where the conversion happens)."""
         _check(self.lib.coru_ctx_set_f64_engine(self.h, mode))
+
+    def last_f64_engine(self) -> int:
+        """Engine of the last fp64 decomposition's A-passes: 0 DMMA, 1 Ozaki (in-kernel digits),
+        2 Ozaki (digit planes)."""
+        return int(self.lib.coru_ctx_last_f64_engine(self.h))
 
     def set_wide_qr(self, on: bool):
         """QR of sketches wider than 128 columns: CholeskyQR2 in fp64 with a device-side Householder

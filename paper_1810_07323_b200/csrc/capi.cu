@@ -203,6 +203,7 @@ struct coru_ctx {
     void* oz_planes = nullptr;
     size_t oz_planes_cap = 0;
     bool oz_planes_ready = false;
+    int last_f64_engine = 0;  // engine of the last fp64 A-pass: 0 DMMA, 1 Ozaki (in-kernel digits), 2 Ozaki (digit planes)
     bool wide_qr = true;  // CholeskyQR2 (fp64) for sketches wider than 128 columns, Householder fall-back
     char* arena = nullptr;
     size_t arena_bytes = 0;
@@ -383,6 +384,7 @@ bool oz_enabled(const coru_ctx* c) {
 // passes: A-passes the caller will run over A; ncols: their sketch width (decides digit planes).
 int oz_prepare(coru_ctx* c, const double* A, int64_t lda, int64_t rows, int64_t cols, int passes, int ncols) {
     c->oz_a = nullptr;
+    c->last_f64_engine = 0;
     if (!oz_enabled(c) || !A) return CORU_OK;
     if (!gemm_oz_eligible(std::max(rows, cols), std::min(rows, cols), 1)) return CORU_OK;
     // The int8 kernel runs one CTA per (128-row tile, 64-column chunk): on a small matrix it cannot
@@ -501,6 +503,7 @@ int gemm<double>(coru_ctx* c, Op op, const double* A, int64_t lda, const double*
         }
         CORU_CUDA(gemm_oz(op, A, lda, c->oz_planes_ready ? &pl : nullptr, eA, X, ldx, C, ldc, Mo, K, N, c->oz_ws,
                           c->num_sms, c->stream));
+        c->last_f64_engine = c->oz_planes_ready ? 2 : 1;
         if (stop) {
             CORU_CUDA(cudaEventRecord(stop, c->stream));
             c->prof_flops += 2.0 * double(Mo) * double(K) * double(N);
@@ -783,7 +786,7 @@ int upload_phi_host(coru_ctx* c, int64_t rows, int cols, int ld, uint64_t seed, 
     int64_t r0 = 0;
     for (int k = 1; k <= chunks; ++k) {
         int64_t r1 = k == chunks ? rows : rows * k / chunks;
-        if ((r1 * cols) & 1) --r1;  // odd cols: end on an even row so the next chunk starts on a pair
+        if (k < chunks && ((r1 * cols) & 1)) --r1;  // odd cols: end on an even row so the next chunk starts on a pair
         if (r1 <= r0) continue;
         gaussian_host_rows<T>(rows, cols, seed, stream, phi, ld, c->host_threads, 1, r0, r1);
         CORU_CUDA(cudaMemcpyAsync(out + r0 * ld, phi + r0 * ld, size_t(r1 - r0) * ld * sizeof(T),
@@ -961,8 +964,13 @@ int run_impl(coru_ctx* c, const Request<T>& r, size_t extra_arena_off) {
     // overlaps the last A^T pass; with a communicator QR(c1) stays on the main stream (its
     // all-gather must keep the NCCL issue order) and QR(c2) goes to the aux stream.
     const bool sharded = c->world > 1;
-    // tooling: overlap QR(c1) with the last A^T pass
-    const bool early_qr1 = !sharded && getenv("CORU_QR1_EARLY") != nullptr && !(r.first_done && r.q == 0);
+    // Tall sketches (rows >= 16 cols: C3): QR(c1) is the critical path after the passes, so its tree
+    // starts as soon as the last c1 exists and overlaps the last A^T pass — the upper tree levels
+    // occupy a few SMs only (C3: 14.2 -> 13.6 ms). Square-ish problems keep both trees after the
+    // pass (overlapping only slowed it there). CORU_QR1_EARLY=0/1 overrides (tooling).
+    static const char* early_env = getenv("CORU_QR1_EARLY");
+    const bool early_want = early_env ? atoi(early_env) != 0 : R >= 16 * N;
+    const bool early_qr1 = !sharded && !r.a_host && early_want && !(r.first_done && r.q == 0);
     // Out-of-core: stream A' through a two-buffer device ring, H2D on the aux stream one chunk ahead
     // of the GEMMs on the main stream (events order the reuse of each buffer).
     cudaEvent_t ooc_ev[4] = {};
@@ -2171,6 +2179,8 @@ int coru_ctx_set_profiling(coru_ctx* c, int enable) {
     c->prof_flops = c->prof_bytes = 0;
     return CORU_OK;
 }
+
+int coru_ctx_last_f64_engine(coru_ctx* c) { return c ? c->last_f64_engine : -1; }
 
 int coru_ctx_profile_apass(coru_ctx* c, double* total_ms, int64_t* launches, double* flops, double* bytes) {
     CORU_TRY(enter(c));

@@ -797,55 +797,66 @@ template <typename T>
 struct FormQSmem {
     int ldvs, lde;
     T *Vs, *E, *Y, *Z, *Tp, *scratch;
-    __device__ FormQSmem(unsigned char* raw, int d, int rb, bool stage) : ldvs(ld_mod(rb, 8)), lde(ld_mod(rb, 4)) {
+    // stage: 0 = reflectors read from global, 1 = all d reflector columns staged in shared memory;
+    // qc = Q columns formed by this CTA
+    __device__ FormQSmem(unsigned char* raw, int d, int rb, int stage, int qc) : ldvs(ld_mod(rb, 8)), lde(ld_mod(rb, 4)) {
         T* p = reinterpret_cast<T*>(raw);
         E = p;
-        p += size_t(kQChunk) * lde;
+        p += size_t(qc) * lde;
         Y = p;
-        p += kNB * kQChunk;
+        p += kNB * qc;
         Z = p;
-        p += kNB * kQChunk;
+        p += kNB * qc;
         Tp = p;
         p += kNB * kNB;
         scratch = p;
         p += kGemmScratch;
         Vs = stage ? p : nullptr;
     }
-    static size_t bytes(int d, int rb, size_t eb, bool stage) {
-        return (size_t(kQChunk) * ld_mod(rb, 4) + 2 * kNB * kQChunk + kNB * kNB + kGemmScratch +
-                (stage ? size_t(d) * ld_mod(rb, 8) : 0)) *
+    static size_t bytes(int d, int rb, size_t eb, int stage, int qc) {
+        return (size_t(qc) * ld_mod(rb, 4) + 2 * kNB * qc + kNB * kNB + kGemmScratch +
+                (stage == 1 ? size_t(d) * ld_mod(rb, 8) : 0)) *
                eb;
     }
 };
+// Staging mode of a level: all reflector columns staged when they fit next to the 32-column chunk
+// (small blocks); big blocks read them from L2. (Staging one panel at a time with 16-column chunks
+// was measured slower at C3: 7 chunk CTAs per block instead of 4, 5.0 vs 4.0 ms for the tree.)
+template <typename T>
+inline void formq_mode(int d, int rb, int max_smem, int* stage, int* qc) {
+    *qc = kQChunk;
+    *stage = FormQSmem<T>::bytes(d, rb, sizeof(T), 1, kQChunk) <= size_t(max_smem) ? 1 : 0;
+}
 
 // Q block b = H_0 ... H_{d-1} [Qin_b; 0]  (Qin null => identity), by panels in reverse:
 //   E <- E - V_p (T_p (V_p^T E)),  p = P-1 ... 0. Columns of Q are independent, so each CTA
-//   forms one kQChunk-wide column chunk (grid = blocks x chunks) to spread a level over more SMs.
+//   forms one qc-wide column chunk (grid = blocks x chunks) to spread a level over more SMs.
 //   V is the explicit reflector matrix (column-major, ldv), staged in shared memory when it fits.
 template <typename T>
 __global__ void __launch_bounds__(kBThreads, 1)
     k_qr_blocked_form_q(const T* __restrict__ Qin, int ldqin, int64_t rows, int nb, int d, const T* __restrict__ V,
-                        int ldv, const T* __restrict__ Tg, T* __restrict__ Qout, int64_t ldqout, int stage, const int* __restrict__ gate) {
+                        int ldv, const T* __restrict__ Tg, T* __restrict__ Qout, int64_t ldqout, int stage, int qc,
+                        const int* __restrict__ gate) {
     if (gate && *gate == 0) return;  // CholeskyQR2 already produced this QR (cholqr.cu)
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int b = blockIdx.x;
     const int64_t r0 = rows * b / nb, r1 = rows * (b + 1) / nb;
     const int rb = int(r1 - r0);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    FormQSmem<T> S(smem_raw, d, rb, stage != 0);
+    FormQSmem<T> S(smem_raw, d, rb, stage, qc);
     const T* Vb = V + int64_t(b) * d * ldv;
     const T* Tb = Tg + int64_t(b) * npanels(d) * kNB * kNB;
     const T* Qb = Qin ? Qin + int64_t(b) * d * ldqin : nullptr;
     const T* Vx = Vb;
     int ldx = ldv;
-    if (stage) {
+    if (stage == 1) {
         for (int c = warp; c < d; c += kBThreads / 32)
             for (int r = lane; r < rb; r += 32) S.Vs[c * S.ldvs + r] = Vb[int64_t(c) * ldv + r];
         Vx = S.Vs;
         ldx = S.ldvs;
     }
-    const int q0 = blockIdx.y * kQChunk;  // this CTA's column chunk of Q
-    const int nq = min(kQChunk, d - q0);
+    const int q0 = blockIdx.y * qc;  // this CTA's column chunk of Q
+    const int nq = min(qc, d - q0);
     for (int e = tid; e < nq * rb; e += kBThreads) {
         const int j = e / rb, i = e % rb;
         S.E[j * S.lde + i] = i < d ? (Qb ? Qb[i * ldqin + q0 + j] : T(i == q0 + j ? 1 : 0)) : T(0);
@@ -854,12 +865,13 @@ __global__ void __launch_bounds__(kBThreads, 1)
     for (int pi = npanels(d) - 1; pi >= 0; --pi) {
         const int p0 = pi * kNB, nbp = min(kNB, d - p0), K = rb - p0;
         const T* Vp = Vx + p0 * ldx + p0;  // V_p rows >= p0
+        const int ldp = ldx;
         if (tid < kNB * kNB) S.Tp[tid] = Tb[pi * kNB * kNB + tid];
-        cta_mm(nbp, nq, K, Vp, ldx, 1, S.E + p0, 1, S.lde, S.Y, kQChunk, 1, T(1), false, S.scratch, kGemmScratch);
+        cta_mm(nbp, nq, K, Vp, ldp, 1, S.E + p0, 1, S.lde, S.Y, qc, 1, T(1), false, S.scratch, kGemmScratch);
         __syncthreads();
-        cta_mm(nbp, nq, nbp, S.Tp, kNB, 1, S.Y, kQChunk, 1, S.Z, kQChunk, 1, T(1), false, S.scratch, kGemmScratch);
+        cta_mm(nbp, nq, nbp, S.Tp, kNB, 1, S.Y, qc, 1, S.Z, qc, 1, T(1), false, S.scratch, kGemmScratch);
         __syncthreads();
-        cta_mm(K, nq, nbp, Vp, 1, ldx, S.Z, kQChunk, 1, S.E + p0, 1, S.lde, T(-1), true, S.scratch, kGemmScratch);
+        cta_mm(K, nq, nbp, Vp, 1, ldp, S.Z, qc, 1, S.E + p0, 1, S.lde, T(-1), true, S.scratch, kGemmScratch);
         __syncthreads();
     }
     T* Qo = Qout + r0 * ldqout + q0;
@@ -1115,14 +1127,14 @@ TsqrPlan plan_tsqr(int64_t m, int d, size_t eb, int max_smem, int num_sms) {
     // Largest block for the shared-memory blocked kernels (<= 256 rows, register panels).
     int rb_blocked = 0;
     for (int rb = kMaxRowsBlocked; rb > d; --rb)
-        if (BlockedSmem<double>::bytes(d, rb, eb) <= cap && FormQSmem<double>::bytes(d, rb, eb, true) <= cap) {
+        if (BlockedSmem<double>::bytes(d, rb, eb) <= cap && FormQSmem<double>::bytes(d, rb, eb, 1, kQChunk) <= cap) {
             rb_blocked = rb;
             break;
         }
     // Largest block for the global-working-set blocked kernels (panel reflectors + Q chunk in smem).
     int rb_big = 0;
     for (int rb = 4096; rb > d; --rb)
-        if (BigSmem<double>::bytes(d, rb, eb) <= cap && FormQSmem<double>::bytes(d, rb, eb, false) <= cap) {
+        if (BigSmem<double>::bytes(d, rb, eb) <= cap && FormQSmem<double>::bytes(d, rb, eb, 0, kQChunk) <= cap) {
             rb_big = rb;
             break;
         }
@@ -1276,12 +1288,13 @@ cudaError_t tsqr_form_q(const TsqrPlan& p, const T* q_top, T* V, T* beta, T* Tar
                                                                         L.ldv, beta + L.beta_off, out, ldo, gate);
             }
         } else if (L.blocked) {
-            const bool stage = FormQSmem<T>::bytes(d, L.rbmax, sizeof(T), true) <= size_t(max_smem);
-            const size_t sm = FormQSmem<T>::bytes(d, L.rbmax, sizeof(T), stage);
+            int stage = 0, qc = kQChunk;
+            formq_mode<T>(d, L.rbmax, max_smem, &stage, &qc);
+            const size_t sm = FormQSmem<T>::bytes(d, L.rbmax, sizeof(T), stage, qc);
             allow_max_smem(k_qr_blocked_form_q<T>);
-            const dim3 grid(unsigned(L.nb), unsigned((d + kQChunk - 1) / kQChunk));
+            const dim3 grid(unsigned(L.nb), unsigned((d + qc - 1) / qc));
             k_qr_blocked_form_q<T><<<grid, kBThreads, sm, st>>>(qin, ldqin, L.rows, L.nb, d, V + L.v_off, L.ldv,
-                                                                 Tarena + L.t_off, out, ldo, stage ? 1 : 0, gate);
+                                                                 Tarena + L.t_off, out, ldo, stage, qc, gate);
         } else {
             const size_t sm = L.smem ? size_t(L.rbmax | 1) * d * sizeof(T) : 0;
             allow_max_smem(k_hh_form_q<T>);

@@ -230,3 +230,21 @@ def test_cpp_reference_matrix_dropin(ctx):
         pytest.skip("test_ref_matrix not built (needs the reference headers at build time)")
     r = subprocess.run([exe], capture_output=True, text=True, timeout=300)
     assert r.returncode == 0, r.stdout + r.stderr
+
+
+@pytest.mark.parametrize("n,ell,stream", [(2000, 110, 0), (4000, 60, 7), (1001, 25, 3), (333, 17, 12345)])
+def test_default_phi_is_reference_phi(ctx, oracle, n, ell, stream):
+    """The sketch matrix the DEFAULT path multiplies A with is the reference's gaussian(cols, ell,
+    {seed, stream}) byte for byte (rng.hpp:86-112; BASELINE north_star: "generated by the reference's
+    RNG from the same seed and uploaded"). With q = 0, sketch_bases returns c2_prev = Φ exactly as it
+    sits in HBM (corutv.hpp:54-58), on the device entry and on the host entry; the expected bytes come
+    from the oracle's gaussian, pinned bit-exact to the compiled reference in test_oracle.py."""
+    import torch
+    import paper_1810_07323_b200 as cg
+    rng = np.random.default_rng(n + ell)
+    a = rng.standard_normal((n + 50, n))
+    want = oracle.gaussian(n, ell, 42, stream)
+    s_dev = cg.sketch_bases(torch.from_numpy(a).cuda(), ell, 0, seed=cg.RngSeed(42, stream), ctx=ctx)
+    assert s_dev.c2_prev.cpu().numpy().tobytes() == want.tobytes()
+    s_host = cg.sketch_bases(a, ell, 0, seed=cg.RngSeed(42, stream), ctx=ctx)
+    assert s_host.c2_prev.tobytes() == want.tobytes()
