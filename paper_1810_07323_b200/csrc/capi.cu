@@ -573,24 +573,42 @@ struct TsqrBufs {
             status = cv.take<int>(1);
         }
     }
+    // ext_gate: another tree's CholeskyQR2 status gating THIS tree (the cross-rank top level of a
+    // sharded wide sketch runs only when the sharded CholeskyQR2 fell back).
+    const int* ext_gate = nullptr;
+    const int* gate() const { return chol ? status : ext_gate; }
+    // CholeskyQR2 alone (reduce: the cross-rank sum of the Gram matrices of a row-sharded sketch).
+    int factor_chol(const T* B, int64_t ldb, T* r_out, cudaStream_t st, const CholQrReduce* reduce = nullptr) {
+        CORU_CUDA(cholqr_factor<T>(cp, B, ldb, cws, status, r_out, max_smem, sms, st, reduce));
+        g_launches += cholqr_launches(plan.d);
+        return CORU_OK;
+    }
+    // The Householder tree alone (gated on the CholeskyQR2 status when there is one).
+    int factor_tree(const T* B, int64_t ldb, T* r_out, cudaStream_t st) {
+        CORU_CUDA(tsqr_factor<T>(plan, B, ldb, v, beta, tarena, rarena, r_out, st, gate()));
+        g_launches += int64_t(plan.levels.size());
+        return CORU_OK;
+    }
     int factor(const T* B, int64_t ldb, T* r_out, cudaStream_t st) {
-        if (chol) {
-            CORU_CUDA(cholqr_factor<T>(cp, B, ldb, cws, status, r_out, max_smem, sms, st));
-            g_launches += cholqr_launches(plan.d);
-        }
-        CORU_CUDA(tsqr_factor<T>(plan, B, ldb, v, beta, tarena, rarena, r_out, st, chol ? status : nullptr));
+        if (chol) CORU_TRY(factor_chol(B, ldb, r_out, st));
+        return factor_tree(B, ldb, r_out, st);
+    }
+    int form_q_chol(T* Q, int64_t ldq, cudaStream_t st) {
+        CORU_CUDA(cholqr_form_q<T>(cp, cws, Q, ldq, sms, st));
+        ++g_launches;
+        return CORU_OK;
+    }
+    int form_q_tree(const T* q_top, T* Q, int64_t ldq, cudaStream_t st) {
+        CORU_CUDA(tsqr_form_q<T>(plan, q_top, v, beta, tarena, scratch, Q, ldq, max_smem, st, gate()));
         g_launches += int64_t(plan.levels.size());
         return CORU_OK;
     }
     int form_q(const T* q_top, T* Q, int64_t ldq, cudaStream_t st) {
         if (chol) {
             if (q_top) return fail(CORU_ECUDA, "internal: CholeskyQR2 tree with a top-level Q");
-            CORU_CUDA(cholqr_form_q<T>(cp, cws, Q, ldq, sms, st));
-            ++g_launches;
+            CORU_TRY(form_q_chol(Q, ldq, st));
         }
-        CORU_CUDA(tsqr_form_q<T>(plan, q_top, v, beta, tarena, scratch, Q, ldq, max_smem, st, chol ? status : nullptr));
-        g_launches += int64_t(plan.levels.size());
-        return CORU_OK;
+        return form_q_tree(q_top, Q, ldq, st);
     }
 };
 
@@ -631,6 +649,16 @@ struct Request {
     Op op_at() const { return trans ? Op::N : Op::T; }  // A'^T·Y
 };
 
+// Sharded power rounds: B2 = sum_g A_g^T B1_g is an all-reduce of n x d per round (C4 58 MB, C5 136 MB).
+// Worth hiding when it is large: the product is then issued per 64-column chunk of the sketch and
+// each chunk's sum runs on the aux stream while the next chunk's GEMM runs.
+constexpr int kB2ChunkCols = 64;
+inline bool overlap_b2(const coru_ctx* c, int64_t n, int dp, size_t elem) {
+    const char* env = getenv("CORU_B2_OVERLAP");  // tooling / tests: 0 | 1 (read per call)
+    if (env) return atoi(env) != 0 && c->world > 1 && dp > kB2ChunkCols;
+    return c->world > 1 && dp > kB2ChunkCols && size_t(n) * size_t(dp) * elem >= (size_t(8) << 20);
+}
+
 template <typename T>
 struct Work {
     T *b2 = nullptr, *b2prev = nullptr, *b1 = nullptr, *q1 = nullptr, *q2 = nullptr, *gws = nullptr;
@@ -642,6 +670,7 @@ struct Work {
     T *cbuf[2] = {nullptr, nullptr}, *b2n = nullptr, *part = nullptr;  // out-of-core chunk ring, next c2, partial
     T* tnp = nullptr;  // partials of the skinny Q^T·W core products (d <= 64)
     T* wproj = nullptr;  // W = A·Q2 when it overlaps the Q1 tree (exact-D, single GPU, in-core)
+    T* b2chunks = nullptr;  // sharded: contiguous column chunks of A_g^T·B1_g, all-reduced chunk by chunk
     double* pws = nullptr;
     int64_t* perm = nullptr;
     int* flag = nullptr;
@@ -658,6 +687,9 @@ struct Work {
         gws_elems = std::max({gemm_ws<T>(r.op_a(), R, N, d, sms), gemm_ws<T>(r.op_at(), N, R, d, sms),
                               gemm_ws<T>(Op::T, d, R, d, sms), gemm_ws<T>(Op::N, R, d, d, sms),
                               gemm_ws<T>(Op::T, d, N, d, sms), gemm_ws<T>(Op::N, d, d, d, sms)});
+        if (overlap_b2(c, N, dp, sizeof(T)))  // the per-chunk A^T-products of the sharded power rounds
+            for (int nc : {std::min(kB2ChunkCols, d), d % kB2ChunkCols ? d % kB2ChunkCols : std::min(kB2ChunkCols, d)})
+                gws_elems = std::max(gws_elems, gemm_ws<T>(r.op_at(), N, R, nc, sms));
         if (r.a_host) {
             // host rows of A: rows of A' (URV) or its columns (ULV, A' = A^T); row length = the other side
             const int64_t HR = r.trans ? N : R, HL = r.trans ? R : N;
@@ -670,12 +702,16 @@ struct Work {
             part = cv.take<T>(HL * dp);
         }
         gws = cv.take<T>(gws_elems);
-        // CholeskyQR2 for wide sketches, except for Q1 when sharded (its tree's top level is cross-rank)
-        ts1.carve(cv, R, d, c->max_smem, sms, c->world == 1 && c->wide_qr);
+        // CholeskyQR2 for wide sketches; sharded, the Gram matrices of Q1's sketch are summed over the
+        // ranks and the cross-rank Householder top level is gated on its status
+        ts1.carve(cv, R, d, c->max_smem, sms, c->wide_qr);
         ts2.carve(cv, N, d, c->max_smem, sms, c->wide_qr);
         if (c->world > 1) {
+            // column chunks of the A^T-product, reduced on the aux stream under the next chunk's GEMM
+            if (overlap_b2(c, N, dp, sizeof(T))) b2chunks = cv.take<T>(N * int64_t(dp));
             rstack = cv.take<T>(int64_t(c->world) * d * d);
             tstop.carve(cv, int64_t(c->world) * d, d, c->max_smem);
+            tstop.ext_gate = ts1.chol ? ts1.status : nullptr;
             qtop = cv.take<T>(int64_t(c->world) * d * d);
         }
         r1loc = cv.take<T>(int64_t(d) * d);
@@ -710,31 +746,31 @@ __global__ void k_sum_slots(const T* const* slots, int world, T* out, size_t cou
 }
 
 template <typename T>
-int thread_allreduce(coru_ctx* c, T* buf, size_t count) {
+int thread_allreduce(coru_ctx* c, T* buf, size_t count, cudaStream_t stream) {
     coru_threadcomm* g = c->tcomm;
     const size_t bytes = count * sizeof(T) + size_t(g->world) * sizeof(void*);
     if (c->tscratch_bytes < bytes) {
-        CORU_CUDA(cudaStreamSynchronize(c->stream));
+        CORU_CUDA(cudaStreamSynchronize(stream));
         if (c->tscratch) cudaFree(c->tscratch);
         c->tscratch = nullptr;
         c->tscratch_bytes = 0;
         if (cudaMalloc(&c->tscratch, bytes) != cudaSuccess) return fail(CORU_ENOMEM, "thread-comm scratch");
         c->tscratch_bytes = bytes;
     }
-    CORU_CUDA(cudaStreamSynchronize(c->stream));
+    CORU_CUDA(cudaStreamSynchronize(stream));
     g->slots[size_t(c->rank)] = buf;
     if (!g->barrier()) return fail(CORU_ECUDA, "a peer rank of the thread group failed");
     const T** dslots = reinterpret_cast<const T**>(static_cast<char*>(c->tscratch) + count * sizeof(T));
     CORU_CUDA(cudaMemcpyAsync(dslots, g->slots.data(), size_t(g->world) * sizeof(void*), cudaMemcpyHostToDevice,
-                              c->stream));
+                              stream));
     T* tmp = static_cast<T*>(c->tscratch);
     const int blocks = int(std::min<size_t>((count + 255) / 256, 148 * 8));
-    k_sum_slots<T><<<std::max(blocks, 1), 256, 0, c->stream>>>(dslots, g->world, tmp, count);
+    k_sum_slots<T><<<std::max(blocks, 1), 256, 0, stream>>>(dslots, g->world, tmp, count);
     ++g_launches;
     CORU_CUDA(cudaGetLastError());
-    CORU_CUDA(cudaStreamSynchronize(c->stream));
+    CORU_CUDA(cudaStreamSynchronize(stream));
     if (!g->barrier()) return fail(CORU_ECUDA, "a peer rank of the thread group failed");
-    CORU_CUDA(cudaMemcpyAsync(buf, tmp, count * sizeof(T), cudaMemcpyDeviceToDevice, c->stream));
+    CORU_CUDA(cudaMemcpyAsync(buf, tmp, count * sizeof(T), cudaMemcpyDeviceToDevice, stream));
     return CORU_OK;
 }
 
@@ -753,10 +789,11 @@ int thread_allgather(coru_ctx* c, const T* send, T* recv, size_t count) {
 }
 
 template <typename T>
-int allreduce(coru_ctx* c, T* buf, size_t count) {
+int allreduce(coru_ctx* c, T* buf, size_t count, cudaStream_t stream = nullptr) {
     if (c->world <= 1 && !c->comm) return CORU_OK;
-    if (c->tcomm) return thread_allreduce<T>(c, buf, count);
-    CORU_NCCL(nccl()->AllReduce(buf, buf, count, nccl_type<T>(), ncclSum, c->comm, c->stream));
+    if (!stream) stream = c->stream;
+    if (c->tcomm) return thread_allreduce<T>(c, buf, count, stream);
+    CORU_NCCL(nccl()->AllReduce(buf, buf, count, nccl_type<T>(), ncclSum, c->comm, stream));
     return CORU_OK;
 }
 
@@ -1084,8 +1121,28 @@ int run_impl(coru_ctx* c, const Request<T>& r, size_t extra_arena_off) {
         }
         if (i == r.q && w.b2prev)
             CORU_CUDA(cudaMemcpyAsync(w.b2prev, w.b2, size_t(N) * dp * sizeof(T), cudaMemcpyDeviceToDevice, st));
-        CORU_TRY(gemm<T>(c, r.op_at(), r.A, r.lda, w.b1, dp, w.b2, dp, N, R, d, w.gws, w.gws_elems));
-        CORU_TRY(allreduce<T>(c, w.b2, size_t(N) * dp));
+        if (w.b2chunks) {
+            // per-chunk product -> contiguous chunk buffer -> all-reduce + scatter on the aux stream,
+            // overlapping the next chunk's product on the main stream
+            int64_t off = 0;
+            for (int c0 = 0; c0 < d; c0 += kB2ChunkCols) {
+                const int nc = std::min(kB2ChunkCols, d - c0);
+                const int ncp = int(round_up(nc, 8));
+                T* chunk = w.b2chunks + off;
+                CORU_TRY(gemm<T>(c, r.op_at(), r.A, r.lda, w.b1 + c0, dp, chunk, ncp, N, R, nc, w.gws, w.gws_elems));
+                CORU_CUDA(cudaEventRecord(c->ev_fork, st));
+                CORU_CUDA(cudaStreamWaitEvent(c->aux, c->ev_fork, 0));
+                CORU_TRY(allreduce<T>(c, chunk, size_t(N) * ncp, c->aux));
+                CORU_CUDA(copy_block<T>(chunk, ncp, w.b2 + c0, dp, N, nc, c->aux));
+                ++g_launches;
+                off += N * int64_t(ncp);
+            }
+            CORU_CUDA(cudaEventRecord(c->ev_join, c->aux));
+            CORU_CUDA(cudaStreamWaitEvent(st, c->ev_join, 0));
+        } else {
+            CORU_TRY(gemm<T>(c, r.op_at(), r.A, r.lda, w.b1, dp, w.b2, dp, N, R, d, w.gws, w.gws_elems));
+            CORU_TRY(allreduce<T>(c, w.b2, size_t(N) * dp));
+        }
     }
     if (sharded) {
         // Q2 = QR(c2) (corutv.hpp:60): c2 is replicated, every rank computes the same tree (aux).
@@ -1093,12 +1150,23 @@ int run_impl(coru_ctx* c, const Request<T>& r, size_t extra_arena_off) {
         CORU_CUDA(cudaStreamWaitEvent(c->aux, c->ev_fork, 0));
         CORU_TRY(w.ts2.factor(w.b2, dp, w.r2, c->aux));
         CORU_TRY(w.ts2.form_q(nullptr, w.q2, dp, c->aux));
-        // Q1, R1: local tree, all-gather of the R_g, redundant top level, local Q (main stream).
-        CORU_TRY(w.ts1.factor(w.b1, dp, w.r1loc, st));
+        // Q1, R1 (main stream). Wide sketches: CholeskyQR2 over all ranks — the two Gram matrices are
+        // all-reduced (d x d, identical bytes everywhere, so R1, the status and every rank's solve
+        // agree), Q1_g = c1_g R^{-1} is local. Then the Householder path, which for wide sketches
+        // runs only if that status says ill-conditioned (device-side gate, no host decision): local
+        // tree, all-gather of the R_g, redundant top level, local Q.
+        if (w.ts1.chol) {
+            const CholQrReduce red = [&](double* buf, size_t count) -> cudaError_t {
+                return allreduce<double>(c, buf, count) == CORU_OK ? cudaSuccess : cudaErrorUnknown;
+            };
+            CORU_TRY(w.ts1.factor_chol(w.b1, dp, w.r1, st, &red));
+            CORU_TRY(w.ts1.form_q_chol(w.q1, dp, st));
+        }
+        CORU_TRY(w.ts1.factor_tree(w.b1, dp, w.r1loc, st));
         CORU_TRY(allgather<T>(c, w.r1loc, w.rstack, size_t(d) * d));
         CORU_TRY(w.tstop.factor(w.rstack, d, w.r1, st));
         CORU_TRY(w.tstop.form_q(nullptr, w.qtop, d, st));
-        CORU_TRY(w.ts1.form_q(w.qtop + int64_t(c->rank) * d * d, w.q1, dp, st));
+        CORU_TRY(w.ts1.form_q_tree(w.qtop + int64_t(c->rank) * d * d, w.q1, dp, st));
         CORU_CUDA(conditioning_flag<T>(w.r1, d, d, w.flag, st));
         ++g_launches;
     } else {

@@ -239,7 +239,7 @@ int64_t cholqr_ws_doubles(const CholQrPlan& p) {
 
 template <typename T>
 cudaError_t cholqr_factor(const CholQrPlan& p, const T* B, int64_t ldb, double* ws, int* status, T* r_out, int max_smem,
-                          int num_sms, cudaStream_t st) {
+                          int num_sms, cudaStream_t st, const CholQrReduce* reduce) {
     const int64_t m = p.m;
     const int d = p.d;
     double* xd = ws;
@@ -269,11 +269,13 @@ cudaError_t cholqr_factor(const CholQrPlan& p, const T* B, int64_t ldb, double* 
     GemmPlan gp = plan_gemm_f64(Op::T, d, m, d, num_sms);
     const int ldw = p.ldw;
     if ((e = gemm_f64(Op::T, X, ldx, X, ldx, G, ldw, d, m, d, gp, gws, st)) != cudaSuccess) return e;
+    if (reduce && (e = (*reduce)(G, size_t(d) * size_t(ldw))) != cudaSuccess) return e;
     k_chol_blocked<<<1, kCholThreads, chol_smem(d), st>>>(G, ldw, d, R1, ldw, RinvD1, status, 0);
     const unsigned tb = unsigned((m + kTrsmRows - 1) / kTrsmRows);
     k_trsm_rinv<double><<<tb, kTrsmThreads, trsm_smem(d), st>>>(X, ldx, m, d, R1, ldw, RinvD1, q1, ldw, nullptr, 0);
     // pass 2: G = Q1^T Q1, R2; R = R2 R1 (Q = Q1 R2^{-1} is formed by cholqr_form_q)
     if ((e = gemm_f64(Op::T, q1, ldw, q1, ldw, G, ldw, d, m, d, gp, gws, st)) != cudaSuccess) return e;
+    if (reduce && (e = (*reduce)(G, size_t(d) * size_t(ldw))) != cudaSuccess) return e;
     k_chol_blocked<<<1, kCholThreads, chol_smem(d), st>>>(G, ldw, d, R2, ldw, RinvD2, status, 1);
     GemmPlan rp = plan_gemm_f64(Op::N, d, d, d, num_sms);
     if ((e = gemm_f64(Op::N, R2, ldw, R1, ldw, Rf, ldw, d, d, d, rp, gws, st)) != cudaSuccess) return e;
@@ -303,7 +305,7 @@ int cholqr_launches(int d) {
 
 #define CORU_INST(T)                                                                                               \
     template cudaError_t cholqr_factor<T>(const CholQrPlan&, const T*, int64_t, double*, int*, T*, int, int,       \
-                                          cudaStream_t);                                                          \
+                                          cudaStream_t, const CholQrReduce*);                                     \
     template cudaError_t cholqr_form_q<T>(const CholQrPlan&, double*, T*, int64_t, int, cudaStream_t);
 CORU_INST(double)
 CORU_INST(float)

@@ -1,6 +1,7 @@
 // Wide-sketch QR by CholeskyQR2 in fp64 with a device-side fall-back status (cholqr.cu).
 #pragma once
 #include <cstdint>
+#include <functional>
 #include <cuda_runtime.h>
 
 namespace coru_gpu {
@@ -24,9 +25,13 @@ int64_t cholqr_ws_doubles(const CholQrPlan& p);
 // R (d x d, row-major, ld d, exact zeros below) of B (m x d, ldb) by CholeskyQR2 in fp64.
 // status (device int): 0 = CholeskyQR2 result valid; nonzero = ill-conditioned or breakdown —
 // the caller's gated Householder kernels then overwrite R and Q.
+// Row-sharded B (every rank holds m local rows of the same tall matrix): `reduce` sums a buffer of
+// `count` doubles over the ranks in place on `st` (identical bytes on every rank); it is applied to
+// the two Gram matrices, so R, the status and the triangular solves are those of the stacked matrix.
+using CholQrReduce = std::function<cudaError_t(double* buf, size_t count)>;
 template <typename T>
 cudaError_t cholqr_factor(const CholQrPlan& p, const T* B, int64_t ldb, double* ws, int* status, T* r_out,
-                          int max_smem, int num_sms, cudaStream_t st);
+                          int max_smem, int num_sms, cudaStream_t st, const CholQrReduce* reduce = nullptr);
 // Q = Q1 · R2^{-1} (m x d, ldq) from the state cholqr_factor left in ws.
 template <typename T>
 cudaError_t cholqr_form_q(const CholQrPlan& p, double* ws, T* Q, int64_t ldq, int num_sms, cudaStream_t st);

@@ -73,8 +73,8 @@ def rel_err(a, u, t, v, rows: int = 8192) -> float:
         for r0 in range(0, A.shape[0], rows):
             blk = A[r0:r0 + rows].to(dev).double()
             den += (blk * blk).sum()
-            blk -= ut[r0:r0 + rows] @ vt
-            num += (blk * blk).sum()
+            res = blk - ut[r0:r0 + rows] @ vt   # out of place: a CUDA fp64 A would otherwise be overwritten
+            num += (res * res).sum()
         return float(torch.sqrt(num / den))
     a64 = np.asarray(a, np.float64)
     r = a64 - (np.asarray(u, np.float64) @ np.asarray(t, np.float64)) @ np.asarray(v, np.float64).T

@@ -119,3 +119,66 @@ def test_nccl_plumbing_world1(ctx, monkeypatch):
         f = cg.corutv(a, 40, 1, v, seed=cg.RngSeed(42, 0), ctx=c2, m_global=3000)
         assert torch.equal(f.u, r.u) and torch.equal(f.t, r.t) and torch.equal(f.v, r.v)
     c2.close()
+
+
+@pytest.mark.parametrize("world", [2, 4])
+@pytest.mark.parametrize("decay", [-2.0, -9.0])
+def test_sharded_wide_sketch_cholqr2(ctx, world, decay):
+    """Wide sketch (d = 136 > 128) row-sharded: the Q1 sketch is factored by CholeskyQR2 over all
+    ranks (all-reduced Gram matrices, local triangular solves) — decay -2: the well-conditioned case
+    it accepts; decay -9 with q = 1: cond(sketch) ~ 1e27 trips the device-side status and every rank
+    falls back to the gated Householder tree with its cross-rank top level. Either way the result
+    matches the single-GPU decomposition and replicated outputs are bit-identical across ranks."""
+    import torch
+    import paper_1810_07323_b200 as cg
+    m, n, d, q = 6000, 1200, 136, 1
+    rng = np.random.default_rng(world + int(-decay))
+    r = 2 * d
+    x, _ = np.linalg.qr(rng.standard_normal((m, r)))
+    y, _ = np.linalg.qr(rng.standard_normal((n, r)))
+    a = (x * np.logspace(0, decay, r)) @ y.T + 1e-9 * rng.standard_normal((m, n))
+    a_dev = torch.from_numpy(a).cuda()
+    single = cg.corutv(a_dev, d, q, seed=cg.RngSeed(42, 0), ctx=ctx)
+    parts = _run_sharded(a_dev, d, q, world)
+    for f in parts[1:]:
+        assert torch.equal(f.t, parts[0].t) and torch.equal(f.v, parts[0].v)
+        assert np.array_equal(f.perm, parts[0].perm)
+    u = torch.cat([f.u for f in parts]).cpu().numpy()
+    t, v = parts[0].t.cpu().numpy(), parts[0].v.cpu().numpy()
+    assert orth_residual(u) <= 1e-12 * d and orth_residual(v) <= 1e-12 * d
+    su, st, sv = single.u.cpu().numpy(), single.t.cpu().numpy(), single.v.cpu().numpy()
+    e_sh = np.linalg.norm(a - u @ t @ v.T) / np.linalg.norm(a)
+    e_1 = np.linalg.norm(a - su @ st @ sv.T) / np.linalg.norm(a)
+    assert e_sh <= 1.05 * e_1 + 1e-15
+    k = 60  # leading, well-determined part of the spectrum
+    assert np.max(np.abs(np.abs(np.diag(t))[:k] - np.abs(np.diag(st))[:k])) <= 1e-8 * abs(st[0, 0])
+    again = _run_sharded(a_dev, d, q, world)
+    assert torch.equal(again[0].t, parts[0].t)
+
+
+@pytest.mark.parametrize("world", [2, 4])
+@pytest.mark.parametrize("m,n,d,q", [(20000, 2000, 110, 1), (6000, 1200, 136, 2)])
+def test_sharded_b2_allreduce_per_chunk(ctx, monkeypatch, world, m, n, d, q):
+    """The sharded power rounds with the A^T-product issued per 64-column chunk and each chunk's
+    all-reduce (plus scatter) on the aux stream under the next chunk's product (the large-message
+    schedule, forced here with CORU_B2_OVERLAP=1): the same decomposition as the one-message
+    schedule — both reduce identical per-rank partials in rank order."""
+    import torch
+    import paper_1810_07323_b200 as cg
+    rng = np.random.default_rng(m + d + world)
+    r = 2 * d
+    x, _ = np.linalg.qr(rng.standard_normal((m, r)))
+    y, _ = np.linalg.qr(rng.standard_normal((n, r)))
+    a_dev = torch.from_numpy((x * np.logspace(0, -2, r)) @ y.T + 1e-7 * rng.standard_normal((m, n))).cuda()
+    monkeypatch.setenv("CORU_B2_OVERLAP", "0")
+    one = _run_sharded(a_dev, d, q, world)
+    monkeypatch.setenv("CORU_B2_OVERLAP", "1")
+    per = _run_sharded(a_dev, d, q, world)
+    for f in per[1:]:
+        assert torch.equal(f.t, per[0].t) and torch.equal(f.v, per[0].v)
+    # the chunked product sums over k in a different split order than the full-width one: agree to rounding
+    t1, t2 = one[0].t.cpu().numpy(), per[0].t.cpu().numpy()
+    assert np.array_equal(one[0].perm, per[0].perm)
+    assert np.max(np.abs(np.abs(np.diag(t1)) - np.abs(np.diag(t2)))) <= 1e-9 * abs(t1[0, 0])
+    u = torch.cat([f.u for f in per]).cpu().numpy()
+    assert orth_residual(u) <= 1e-12 * d
