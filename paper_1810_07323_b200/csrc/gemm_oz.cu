@@ -478,7 +478,10 @@ __global__ void __launch_bounds__(kOzThreads, 1)
 // warps 4..7 read the level accumulators back at each flush. No converter, no fp64 staging: 139 KB
 // of shared-memory traffic per stage instead of 203 KB, and A costs 7 B/entry/pass from HBM.
 // (A slices through TMEM — tcgen05.st by the converters, "ts" MMAs — were measured too: 1.84 ms
-// per C3 pass against 1.70 ms, the converters stay the bottleneck.)
+// per C3 pass against 1.70 ms, the converters stay the bottleneck. TMA multicast of the A planes
+// over a cluster of the row tile's chunk CTAs, with multicast commits on the empty barriers, was
+// slower as well — C4 pass 8.5 vs 7.2 ms: four unicast reads of a line within a short window
+// already cost L2 one read, and the cluster couples the four pipelines.)
 constexpr int kPzStages = 5;
 constexpr int kPzStage = kOzS * (kOzASlice + kOzXSlice);        // 42 KB
 constexpr int kPzThreads = 256;
