@@ -286,6 +286,10 @@ int coru_alm_rpca_f64(coru_ctx* ctx, const double* M, int64_t m, int64_t n, cons
  * (2·rows·cols·ell) and A bytes (rows·cols·sizeof(T)), then resets the counters. */
 int coru_ctx_set_profiling(coru_ctx* ctx, int enable);
 int coru_ctx_profile_apass(coru_ctx* ctx, double* total_ms, int64_t* launches, double* flops, double* bytes);
+/* The same counters restricted to the A-passes that had the GPU to themselves — not issued while
+ * the call's second stream runs QR kernels (the Q1 tree under the last A^T pass of tall sketches and
+ * under the projection pass). Does not reset; call before coru_ctx_profile_apass. */
+int coru_ctx_profile_apass_exclusive(coru_ctx* ctx, double* total_ms, int64_t* launches);
 /* The same for the fused lift + ALM update kernel of alm_rpca: algorithmic flops 2·m·n·ell (the lift
  * L = Tp·V^T) and bytes 40·m·n per launch (read M, Y; write S, Y, X). */
 int coru_ctx_profile_rpca_update(coru_ctx* ctx, double* total_ms, int64_t* launches, double* flops, double* bytes);

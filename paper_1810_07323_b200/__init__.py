@@ -149,6 +149,7 @@ def load_library():
     L.coru_ctx_set_profiling.argtypes = [p, i32]
     L.coru_ctx_profile_apass.argtypes = [p, C.POINTER(C.c_double), C.POINTER(i64), C.POINTER(C.c_double),
                                          C.POINTER(C.c_double)]
+    L.coru_ctx_profile_apass_exclusive.argtypes = [p, C.POINTER(C.c_double), C.POINTER(i64)]
     L.coru_threadcomm_create.argtypes = [i32]
     L.coru_threadcomm_create.restype = p
     L.coru_threadcomm_destroy.argtypes = [p]
@@ -286,10 +287,14 @@ class Context:
         _check(self.lib.coru_ctx_set_profiling(self.h, 1 if on else 0))
 
     def profile_apass(self) -> dict:
-        """Summed device time of the A-passes since the last read (CUDA events on the launch stream)."""
+        """Summed device time of the A-passes since the last read (CUDA events on the launch stream);
+        ms_exclusive / launches_exclusive: the passes not sharing the GPU with the call's QR stream."""
+        ems, en = C.c_double(), C.c_int64()
+        _check(self.lib.coru_ctx_profile_apass_exclusive(self.h, C.byref(ems), C.byref(en)))
         ms, n, fl, by = C.c_double(), C.c_int64(), C.c_double(), C.c_double()
         _check(self.lib.coru_ctx_profile_apass(self.h, C.byref(ms), C.byref(n), C.byref(fl), C.byref(by)))
-        return {"ms": ms.value, "launches": n.value, "flops": fl.value, "bytes": by.value}
+        return {"ms": ms.value, "launches": n.value, "flops": fl.value, "bytes": by.value,
+                "ms_exclusive": ems.value, "launches_exclusive": en.value}
 
     def profile_rpca_update(self) -> dict:
         """Summed device time of alm_rpca's fused lift + update kernel since the last read."""

@@ -228,6 +228,11 @@ struct coru_ctx {
     std::vector<std::pair<cudaEvent_t, cudaEvent_t>> prof_events;
     size_t prof_used = 0;
     double prof_flops = 0, prof_bytes = 0;
+    // A-passes issued while another stream of the same call runs QR kernels (early Q1 tree, late
+    // join) share the SMs with them: flagged, so the roofline can also be read from the passes that
+    // had the GPU to themselves.
+    bool prof_overlap = false;
+    std::vector<char> prof_shared;
     // the same for the fused ALM lift + update kernel of alm_rpca (rpca.cu)
     std::vector<std::pair<cudaEvent_t, cudaEvent_t>> upd_events;
     size_t upd_used = 0;
@@ -476,6 +481,8 @@ int prof_begin(coru_ctx* c, cudaEvent_t* stop) {
         CORU_CUDA(cudaEventCreate(&b));
         c->prof_events.emplace_back(a, b);
     }
+    if (c->prof_shared.size() < c->prof_events.size()) c->prof_shared.resize(c->prof_events.size(), 0);
+    c->prof_shared[c->prof_used] = c->prof_overlap ? 1 : 0;
     auto& ev = c->prof_events[c->prof_used++];
     CORU_CUDA(cudaEventRecord(ev.first, c->stream));
     *stop = ev.second;
@@ -1121,6 +1128,7 @@ int run_impl(coru_ctx* c, const Request<T>& r, size_t extra_arena_off) {
         }
         if (i == r.q && w.b2prev)
             CORU_CUDA(cudaMemcpyAsync(w.b2prev, w.b2, size_t(N) * dp * sizeof(T), cudaMemcpyDeviceToDevice, st));
+        c->prof_overlap = i == r.q && early_qr1;  // the Q1 tree runs on the aux stream under this pass
         if (w.b2chunks) {
             // per-chunk product -> contiguous chunk buffer -> all-reduce + scatter on the aux stream,
             // overlapping the next chunk's product on the main stream
@@ -1143,6 +1151,7 @@ int run_impl(coru_ctx* c, const Request<T>& r, size_t extra_arena_off) {
             CORU_TRY(gemm<T>(c, r.op_at(), r.A, r.lda, w.b1, dp, w.b2, dp, N, R, d, w.gws, w.gws_elems));
             CORU_TRY(allreduce<T>(c, w.b2, size_t(N) * dp));
         }
+        c->prof_overlap = false;
     }
     if (sharded) {
         // Q2 = QR(c2) (corutv.hpp:60): c2 is replicated, every rank computes the same tree (aux).
@@ -1241,8 +1250,12 @@ int run_impl(coru_ctx* c, const Request<T>& r, size_t extra_arena_off) {
             CORU_TRY(stream_a([&](int64_t, int64_t r0, int64_t rows, const T* Ai) -> int {
                 return gemm<T>(c, Op::N, Ai, N, w.q2, dp, W + r0 * dp, dp, rows, N, d, w.gws, w.gws_elems);
             }));
-        else
-            CORU_TRY(gemm<T>(c, r.op_a(), r.A, r.lda, w.q2, dp, W, dp, R, N, d, w.gws, w.gws_elems));
+        else {
+            c->prof_overlap = late_join;  // the Q1 tree may still be running on the aux stream
+            const int rc = gemm<T>(c, r.op_a(), r.A, r.lda, w.q2, dp, W, dp, R, N, d, w.gws, w.gws_elems);
+            c->prof_overlap = false;
+            CORU_TRY(rc);
+        }
         if (late_join) CORU_CUDA(cudaStreamWaitEvent(st, c->ev_join, 0));  // Q1 (and the flag) from here on
         const bool p = c->prof;  // Q1^T·W is m x d x d, not an A-pass
         c->prof = false;
@@ -2249,6 +2262,24 @@ int coru_ctx_set_profiling(coru_ctx* c, int enable) {
 }
 
 int coru_ctx_last_f64_engine(coru_ctx* c) { return c ? c->last_f64_engine : -1; }
+
+int coru_ctx_profile_apass_exclusive(coru_ctx* c, double* total_ms, int64_t* launches) {
+    CORU_TRY(enter(c));
+    std::lock_guard<std::mutex> lk(c->mu);
+    double ms = 0;
+    int64_t n = 0;
+    for (size_t i = 0; i < c->prof_used; ++i) {
+        if (i < c->prof_shared.size() && c->prof_shared[i]) continue;
+        float t = 0;
+        CORU_CUDA(cudaEventSynchronize(c->prof_events[i].second));
+        CORU_CUDA(cudaEventElapsedTime(&t, c->prof_events[i].first, c->prof_events[i].second));
+        ms += t;
+        ++n;
+    }
+    if (total_ms) *total_ms = ms;
+    if (launches) *launches = n;
+    return CORU_OK;
+}
 
 int coru_ctx_profile_apass(coru_ctx* c, double* total_ms, int64_t* launches, double* flops, double* bytes) {
     CORU_TRY(enter(c));
