@@ -182,6 +182,18 @@ struct coru_ctx {
     cudaStream_t aux = nullptr;  // second stream: the two TSQR trees run concurrently
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     cudaEvent_t ev_phi = nullptr;  // last H2D copy out of the pinned Φ staging buffer
+    // Φ of the NEXT inner decomposition of an iterative caller (alm_rpca: substream(seed, it + 1)),
+    // generated by a background host thread into its own pinned buffer while the GPU finishes the
+    // current iteration.
+    std::thread pf_thread;
+    bool pf_active = false;
+    uint64_t pf_seed = 0, pf_stream = 0;
+    int64_t pf_rows = 0;
+    int pf_cols = 0, pf_ld = 0;
+    size_t pf_elem = 0;
+    char* pf_buf = nullptr;
+    size_t pf_bytes = 0;
+    cudaEvent_t ev_pf = nullptr;
     static constexpr int kUploadChunks = 8;
     cudaEvent_t ev_chunk[kUploadChunks] = {};  // host-entry upload pipeline (corutv_host)
     int num_sms = 148;
@@ -815,10 +827,53 @@ int allgather(coru_ctx* c, const T* send, T* recv, size_t count) {
 // to the reference's gaussian(), rng.hpp:86-112) into the pinned staging buffer, in row chunks:
 // chunk i+1 is generated by the worker pool while the DMA engine uploads chunk i on `st`.
 // Chunk boundaries start on Box–Muller pairs (row·cols even).
+// Start generating gaussian(rows, cols, {seed, stream}) (padded to ld) in the background; the next
+// upload_phi_host with exactly these parameters takes it, any other discards it.
+template <typename T>
+int phi_prefetch(coru_ctx* c, int64_t rows, int cols, int ld, uint64_t seed, uint64_t stream) {
+    if (c->phi_mode != CORU_PHI_HOST_EXACT) return CORU_OK;
+    if (c->pf_thread.joinable()) c->pf_thread.join();
+    c->pf_active = false;
+    const size_t bytes = size_t(rows) * ld * sizeof(T);
+    if (bytes > c->pf_bytes) {
+        CORU_CUDA(cudaEventSynchronize(c->ev_pf));
+        if (c->pf_buf) cudaFreeHost(c->pf_buf);
+        c->pf_buf = nullptr;
+        c->pf_bytes = 0;
+        if (cudaMallocHost(&c->pf_buf, bytes) != cudaSuccess) {
+            cudaGetLastError();
+            return CORU_OK;  // no prefetch: the regular path generates it
+        }
+        c->pf_bytes = bytes;
+    }
+    CORU_CUDA(cudaEventSynchronize(c->ev_pf));  // the last copy out of the buffer has drained
+    c->pf_seed = seed;
+    c->pf_stream = stream;
+    c->pf_rows = rows;
+    c->pf_cols = cols;
+    c->pf_ld = ld;
+    c->pf_elem = sizeof(T);
+    T* buf = reinterpret_cast<T*>(c->pf_buf);
+    const int threads = c->host_threads;
+    c->pf_thread = std::thread([=] { gaussian_host_rows<T>(rows, cols, seed, stream, buf, ld, threads, 1, 0, rows); });
+    c->pf_active = true;
+    return CORU_OK;
+}
+
 template <typename T>
 int upload_phi_host(coru_ctx* c, int64_t rows, int cols, int ld, uint64_t seed, uint64_t stream, T* out,
                     cudaStream_t st) {
     const size_t bytes = size_t(rows) * ld * sizeof(T);
+    if (c->pf_active) {
+        c->pf_thread.join();
+        c->pf_active = false;
+        if (c->pf_seed == seed && c->pf_stream == stream && c->pf_rows == rows && c->pf_cols == cols && c->pf_ld == ld &&
+            c->pf_elem == sizeof(T)) {
+            CORU_CUDA(cudaMemcpyAsync(out, c->pf_buf, bytes, cudaMemcpyHostToDevice, st));
+            CORU_CUDA(cudaEventRecord(c->ev_pf, st));
+            return CORU_OK;
+        }
+    }
     CORU_TRY(ensure_pinned(c, bytes));
     // The pinned staging buffer is reused across calls: wait for the LAST copy out of it only (not
     // for the stream — the exponent / digit-plane kernels of this call keep running while the host
@@ -2029,6 +2084,7 @@ int rpca_impl(coru_ctx* c, const double* Min, int64_t m, int64_t n, int64_t ldm,
             r.ldt = dp;
             r.t_transpose = trans;
             CORU_TRY(run<double>(c, r, work_off));
+            if (!predict && it < cf.max_iter) CORU_TRY(phi_prefetch<double>(c, r.cols, d, dp, seed, it_stream + 1));
             CORU_TRY(cuda_ok(cor_truncate(l.dm, dp, d, inv_mu, trans ? 1 : 0, l.cc, dp, l.ints, st), "cor_truncate"));
             ++g_launches;
         } else {
@@ -2051,6 +2107,9 @@ int rpca_impl(coru_ctx* c, const double* Min, int64_t m, int64_t n, int64_t ldm,
             int warn = 0;
             r.warn_host = &warn;
             CORU_TRY(run<double>(c, r, work_off));
+            // Φ of the next iteration (substream(seed, it + 1), same ell) is generated on the host while
+            // the GPU runs the rest of this one
+            if (!predict && it < cf.max_iter) CORU_TRY(phi_prefetch<double>(c, r.cols, d, dp, seed, it_stream + 1));
             CORU_TRY(gemm<double>(c, Op::N, X, ldx, l.q2, dp, l.w, dp, m, n, d, l.gws, l.gwse));  // X·Q2 (A-pass)
             const bool prof = c->prof;
             c->prof = false;
@@ -2198,6 +2257,7 @@ int coru_ctx_create(int device, coru_ctx** out) {
         cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
         cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming) != cudaSuccess ||
         cudaEventCreateWithFlags(&c->ev_phi, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&c->ev_pf, cudaEventDisableTiming) != cudaSuccess ||
         [&] {
             for (auto& e : c->ev_chunk)
                 if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) return true;
@@ -2231,6 +2291,9 @@ void coru_ctx_destroy(coru_ctx* c) {
     if (c->ev_fork) cudaEventDestroy(c->ev_fork);
     if (c->ev_join) cudaEventDestroy(c->ev_join);
     if (c->ev_phi) cudaEventDestroy(c->ev_phi);
+    if (c->pf_thread.joinable()) c->pf_thread.join();
+    if (c->ev_pf) cudaEventDestroy(c->ev_pf);
+    if (c->pf_buf) cudaFreeHost(c->pf_buf);
     for (auto& e : c->ev_chunk)
         if (e) cudaEventDestroy(e);
     if (c->own_stream) cudaStreamDestroy(c->own_stream);
