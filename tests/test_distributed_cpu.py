@@ -101,3 +101,69 @@ def test_shard_rows_cover_all_rows_evenly():
             spans = [cg.shard_rows(m, r, world) for r in range(world)]
             assert [s[0] for s in spans] == [m * r // world for r in range(world)]
             assert sum(s[1] for s in spans) == m
+
+
+def sharded_corutv_wide(a_full, d, q, seed, stream, rank, world, chunk_cols=64):
+    """The wide-sketch (d > 128) variant of the sharded orchestration (capi.cu run_impl, sharded
+    branch with ts1.chol): B2 all-reduced per 64-column chunk, Q1 by CholeskyQR2 over all ranks —
+    both Gram matrices all-reduced, R1 = R2·R1', Q1_g = B1_g R1'^{-1} R2^{-1} — no all-gather."""
+    import paper_1810_07323_b200 as cg
+    from oracle import Oracle
+    o = Oracle()
+    m, n = a_full.shape
+    r0, rows = cg.shard_rows(m, rank, world)
+    a = np.ascontiguousarray(a_full[r0:r0 + rows])
+    b2 = cg.gaussian(n, d, cg.RngSeed(seed, stream))
+    for _ in range(q + 1):
+        b1 = o.matmul(a, b2)
+        nxt = np.empty((n, d))
+        for c0 in range(0, d, chunk_cols):                      # one message per column chunk
+            nxt[:, c0:c0 + chunk_cols] = _allreduce(o.matmul_tn(a, np.ascontiguousarray(b1[:, c0:c0 + chunk_cols])))
+        b2 = nxt
+    g1 = _allreduce(b1.T @ b1)
+    r1a = np.linalg.cholesky(g1).T
+    q1a = np.linalg.solve(r1a.T, b1.T).T
+    g2 = _allreduce(q1a.T @ q1a)
+    r2 = np.linalg.cholesky(g2).T
+    q1 = np.linalg.solve(r2.T, q1a.T).T
+    r1 = r2 @ r1a
+    warn = abs(r1[d - 1, d - 1]) <= 1e-14 * abs(r1[0, 0])
+    q2, _ = o.householder_qr(b2)
+    core = _allreduce(q1.T @ (a @ q2))
+    qm, t, perm = o.qrcp(core)
+    return q1 @ qm, t, q2[:, perm], perm, warn, (r0, rows)
+
+
+def _worker_wide(rank, world, init_file, a_full, d, q, seed, out_dir):
+    dist.init_process_group("gloo", init_method=f"file://{init_file}", rank=rank, world_size=world)
+    try:
+        u, t, v, perm, warn, (r0, rows) = sharded_corutv_wide(a_full, d, q, seed, 0, rank, world)
+        np.savez(os.path.join(out_dir, f"rank{rank}.npz"), u=u, t=t, v=v, perm=perm, warn=warn, r0=r0, rows=rows)
+    finally:
+        dist.destroy_process_group()
+
+
+def test_row_sharded_wide_sketch_cholqr2(tmp_path, oracle):
+    """d = 136 > 128, world 2 (gloo): CholeskyQR2 with all-reduced Gram matrices and chunked B2
+    all-reduces reproduce the single-process oracle decomposition; replicated outputs bit-identical."""
+    m, n, d, q = 900, 400, 136, 1
+    rng = np.random.default_rng(m + n + d)
+    x, _ = np.linalg.qr(rng.standard_normal((m, 2 * d)))
+    y, _ = np.linalg.qr(rng.standard_normal((n, 2 * d)))
+    a = (x * np.logspace(0, -1.5, 2 * d)) @ y.T + 1e-7 * rng.standard_normal((m, n))
+    world = 2
+    init_file = os.path.join(tempfile.mkdtemp(), "pg_init")
+    mp.start_processes(_worker_wide, args=(world, init_file, a, d, q, 42, str(tmp_path)), nprocs=world,
+                       join=True, start_method="fork")
+    res = [dict(np.load(tmp_path / f"rank{r}.npz")) for r in range(world)]
+    for key in ("t", "v", "perm", "warn"):
+        assert np.array_equal(res[0][key], res[1][key]), key
+    u = np.concatenate([r["u"] for r in res], axis=0)
+    t, v = res[0]["t"], res[0]["v"]
+    ref = oracle.corutv(a, d, q, seed=42)
+    e_sh = np.linalg.norm(a - u @ t @ v.T) / np.linalg.norm(a)
+    e_ref = np.linalg.norm(a - ref.u @ ref.t @ ref.v.T) / np.linalg.norm(a)
+    assert abs(e_sh - e_ref) <= 1e-7 * e_ref + 1e-14
+    k = 60
+    assert np.max(np.abs(np.abs(np.diag(t))[:k] - np.abs(np.diag(ref.t))[:k])) <= 1e-9 * abs(ref.t[0, 0])
+    assert np.linalg.norm(u.T @ u - np.eye(d)) <= 1e-12 * d
