@@ -239,7 +239,9 @@ def config_block(cfg, args, a_sha, gen):
             "phi": "host-exact: coru::gaussian bit for bit (rng.hpp:86-112), generated inside every step",
             "a_sha256": a_sha, "a_generator": gen,
             "l2": ("GPU arm: 256 MB write between steps outside the per-step events (126 MB L2); "
-                   "reference arm: n/a (CPU)")}
+                   "reference arm: n/a (CPU)"),
+            "launch": ("small configs (rows x cols <= 2^24): the library replays the decomposition from a CUDA graph "
+                       "from the third call on the same buffers on; larger ones: plain launches")}
 
 
 # ---- CPU reference ------------------------------------------------------------------------------
@@ -370,7 +372,11 @@ def run_ours(args, cfg):
     # Timed region: K steps; each step device-timed with CUDA events on the library's stream,
     # L2 flushed between steps outside the events. Max over ranks.
     evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
-    ctx.set_profiling(True)
+    # Small configs (C1, C2) are replayed from a CUDA graph by the library, which excludes the
+    # in-library A-pass events: their timed region runs without them and the A-pass durations are
+    # collected over a second loop of the same K steps (plain launches, the same kernels).
+    graph_cfg = world == 1 and cfg.m * cfg.n <= (1 << 24) and cfg.d <= 112
+    ctx.set_profiling(not graph_cfg)
     cg.launch_count(reset=True)
     barrier()
     torch.cuda.synchronize()
@@ -386,9 +392,23 @@ def run_ours(args, cfg):
         barrier()
         wall = time.perf_counter() - wall0
     launches = cg.launch_count(reset=True)
+    step_ms = [e0.elapsed_time(e1) for e0, e1 in evs]
+    graph_replays = ctx.graph_replays()
+    prof_step_ms = step_ms
+    if graph_cfg:
+        ctx.set_profiling(True)
+        pevs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+        for s in range(args.steps):
+            with torch.cuda.stream(stream):
+                flush.zero_()
+                pevs[s][0].record(stream)
+            step(s)
+            pevs[s][1].record(stream)
+        torch.cuda.synchronize()
+        prof_step_ms = [e0.elapsed_time(e1) for e0, e1 in pevs]
+        cg.launch_count(reset=True)
     prof = ctx.profile_apass()
     ctx.set_profiling(False)
-    step_ms = [e0.elapsed_time(e1) for e0, e1 in evs]
     total_ms = sum(step_ms)
     if world > 1:
         tt = torch.tensor([total_ms], dtype=torch.float64, device=dev)
@@ -434,7 +454,7 @@ def run_ours(args, cfg):
                     "avg_launch_ms": avg_ms, "launches": prof["launches"],
                     "hbm_gbs": bytes_per / (avg_ms * 1e-3) / 1e9, "hbm_peak_gbs": peaks.get("hbm_gbs"),
                     "hbm_frac": bytes_per / (avg_ms * 1e-3) / 1e9 / peaks.get("hbm_gbs", 6650.0),
-                    "apass_share_of_step": prof["ms"] / max(sum(step_ms), 1e-9)}
+                    "apass_share_of_step": prof["ms"] / max(sum(prof_step_ms), 1e-9)}
         elif cfg.dtype == "f64":
             # The fp64 A-pass runs on the INT8 tensor cores (Ozaki scheme, gemm_oz.cu): per launch
             # 28 slice products (levels 0..6 of 7 x 7 digit pairs) over the padded width d16.
@@ -466,7 +486,7 @@ def run_ours(args, cfg):
                     "fp64_equiv_vs_dgemm_peak": achieved / dgemm,
                     "hbm_gbs": bytes_per / (avg_ms * 1e-3) / 1e9, "hbm_peak_gbs": peaks.get("hbm_gbs"),
                     "hbm_frac": bytes_per / (avg_ms * 1e-3) / 1e9 / peaks.get("hbm_gbs", 6650.0),
-                    "apass_share_of_step": prof["ms"] / max(sum(step_ms), 1e-9)}
+                    "apass_share_of_step": prof["ms"] / max(sum(prof_step_ms), 1e-9)}
         else:
             tf32 = measured_tf32_peak_tflops(torch)
             peak = tf32 / 3.0
@@ -480,7 +500,7 @@ def run_ours(args, cfg):
                     "avg_launch_ms": avg_ms, "launches": prof["launches"],
                     "hbm_gbs": bytes_per / (avg_ms * 1e-3) / 1e9, "hbm_peak_gbs": peaks.get("hbm_gbs"),
                     "hbm_frac": bytes_per / (avg_ms * 1e-3) / 1e9 / peaks.get("hbm_gbs", 6650.0),
-                    "apass_share_of_step": prof["ms"] / max(sum(step_ms), 1e-9)}
+                    "apass_share_of_step": prof["ms"] / max(sum(prof_step_ms), 1e-9)}
 
     if roof is not None:
         roof["launches_timed_alone"] = int(n_ex) if n_ex else int(prof["launches"])
@@ -498,6 +518,7 @@ def run_ours(args, cfg):
             "scaling": "strong", "vs_baseline": None, "dtype": cfg.dtype, "data": "synthetic",
             "config": config_block(cfg, args, a_sha, gen),
             "e2e": e2e, "e2e_pinned": e2e_pinned, "roofline": roof, "cpu_baseline": cpu, "gpu_launches": launches,
+            "cuda_graph_replays": graph_replays,
             "clocks": clk.summary(), "wall_s_timed_region": wall,
             "step_ms": {"min": min(step_ms), "median": statistics.median(step_ms), "max": max(step_ms)},
         }

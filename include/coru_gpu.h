@@ -95,6 +95,11 @@ int coru_ctx_set_f64_engine(coru_ctx* ctx, int mode);
 /* Engine the last fp64 decomposition's A-passes ran on: 0 = FP64 DMMA, 1 = Ozaki with in-kernel
  * digits, 2 = Ozaki over digit planes (bench evidence: which roofline applies). */
 int coru_ctx_last_f64_engine(coru_ctx* ctx);
+/* Small in-core single-GPU decompositions (rows·cols <= 2^24, ell <= 112, default engines, profiling
+ * off) are replayed from a CUDA graph from the third call with the same device buffers and
+ * parameters on (the seed may change: Φ is generated per call); CORU_NO_GRAPH=1 disables it.
+ * Returns the number of replays so far (bench evidence). */
+int64_t coru_ctx_graph_replays(coru_ctx* ctx);
 int coru_ctx_set_f32_path(coru_ctx* ctx, int mode);
 /* QR of wide sketches (more than 128 columns; householder_qr at corutv.hpp:59-60): 1 (default) =
  * CholeskyQR2 in fp64 with a device-side fall-back to the Householder tree when the sketch is

@@ -144,6 +144,8 @@ def load_library():
     L.coru_ctx_set_wide_qr.argtypes = [p, i32]
     L.coru_ctx_set_f64_engine.argtypes = [p, i32]
     L.coru_ctx_last_f64_engine.argtypes = [p]
+    L.coru_ctx_graph_replays.argtypes = [p]
+    L.coru_ctx_graph_replays.restype = i64
     L.coru_comm_unique_id.argtypes = [p]
     L.coru_ctx_init_comm.argtypes = [p, i32, i32, p]
     L.coru_ctx_set_profiling.argtypes = [p, i32]
@@ -277,6 +279,10 @@ class Context:
         """Engine of the last fp64 decomposition's A-passes: 0 DMMA, 1 Ozaki (in-kernel digits),
         2 Ozaki (digit planes)."""
         return int(self.lib.coru_ctx_last_f64_engine(self.h))
+
+    def graph_replays(self) -> int:
+        """CUDA-graph replays of small decompositions so far (coru_ctx_graph_replays)."""
+        return int(self.lib.coru_ctx_graph_replays(self.h))
 
     def set_wide_qr(self, on: bool):
         """QR of sketches wider than 128 columns: CholeskyQR2 in fp64 with a device-side Householder

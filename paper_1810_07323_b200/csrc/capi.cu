@@ -185,6 +185,23 @@ struct coru_ctx {
     // Φ of the NEXT inner decomposition of an iterative caller (alm_rpca: substream(seed, it + 1)),
     // generated by a background host thread into its own pinned buffer while the GPU finishes the
     // current iteration.
+    // CUDA-graph replay of small decompositions (launch-bound: C1, C2): one instantiated graph per
+    // (A, shape, parameters, output buffers), captured on the second call with the same key.
+    struct GraphEntry {
+        const void *A = nullptr, *u = nullptr, *t = nullptr, *v = nullptr, *arena = nullptr, *pinned = nullptr;
+        int64_t lda = 0, rows = 0, cols = 0, ldu = 0, ldt = 0, ldv = 0;
+        int d = 0, q = 0, variant = 0, elem = 0;
+        bool trans = false, want_perm = false;
+        cudaStream_t stream = nullptr;
+        cudaGraphExec_t exec = nullptr;
+        int64_t launches = 0;
+        int state = 0;  // 0 seen once, 1 instantiated, -1 capture failed (never again)
+        uint64_t last_use = 0;
+    };
+    std::vector<GraphEntry> graphs;
+    uint64_t graph_clock = 0;
+    int64_t graph_replays = 0;
+    int64_t* host_out = nullptr;  // pinned: [0] conditioning flag, [1..] pivots (graph replays write here)
     std::thread pf_thread;
     bool pf_active = false;
     uint64_t pf_seed = 0, pf_stream = 0;
@@ -646,6 +663,9 @@ struct Request {
     uint64_t seed = 0, stream = 0;
     Mode mode = Mode::Full;
     bool first_done = false;  // the first power round (Φ, c1 = a·Φ, c2 = a^T·c1) is already in the workspace
+    // Stream capture (run_graph): Φ already sits in the pinned staging buffer, the flag / pivots go to
+    // the context's pinned host slots, and nothing synchronises — the caller launches the graph.
+    bool capture = false;
     int variant = CORU_D_EXACT;  // Full: how D is formed (corutv.hpp:89-92)
     // Full: U' (rows x d), T' (d x d), V' (cols x d) — device, caller's buffers.
     T* u = nullptr;
@@ -1053,7 +1073,10 @@ int run_impl(coru_ctx* c, const Request<T>& r, size_t extra_arena_off) {
 
     // Φ = gaussian(cols, ell, seed), padded to dp columns (corutv.hpp:51): on the device, or on the
     // host with the host libm (bit-exact) and one H2D.
-    if (!r.first_done) CORU_TRY(gen_phi<T>(c, r, w.b2, dp));
+    if (r.capture)
+        CORU_CUDA(cudaMemcpyAsync(w.b2, c->pinned, size_t(N) * dp * sizeof(T), cudaMemcpyHostToDevice, st));
+    else if (!r.first_done)
+        CORU_TRY(gen_phi<T>(c, r, w.b2, dp));
     CORU_CUDA(cudaMemsetAsync(w.q1, 0, size_t(R) * dp * sizeof(T), st));
     CORU_CUDA(cudaMemsetAsync(w.q2, 0, size_t(N) * dp * sizeof(T), st));
 
@@ -1337,11 +1360,114 @@ int run_impl(coru_ctx* c, const Request<T>& r, size_t extra_arena_off) {
     else CORU_CUDA(copy_block<T>(w.tm, d, r.t, r.ldt, d, d, st));
     ++g_launches;
 
+    if (r.capture) {
+        CORU_CUDA(cudaMemcpyAsync(c->host_out, w.flag, sizeof(int), cudaMemcpyDeviceToHost, st));
+        if (r.perm_host)
+            CORU_CUDA(cudaMemcpyAsync(c->host_out + 1, w.perm, sizeof(int64_t) * d, cudaMemcpyDeviceToHost, st));
+        return CORU_OK;
+    }
     int flag = 0;
     CORU_CUDA(cudaMemcpyAsync(&flag, w.flag, sizeof(int), cudaMemcpyDeviceToHost, st));
     if (r.perm_host) CORU_CUDA(cudaMemcpyAsync(r.perm_host, w.perm, sizeof(int64_t) * d, cudaMemcpyDeviceToHost, st));
     CORU_CUDA(cudaStreamSynchronize(st));
     if (r.warn_host) *r.warn_host = flag;
+    return CORU_OK;
+}
+
+// Small in-core single-GPU decompositions are launch-bound (C1: ~25 kernels of a few microseconds
+// each, two streams): the second call with the same buffers and parameters captures the whole
+// enqueue of run_impl into a CUDA graph, later calls replay it. Per call the host still generates
+// the reference Φ (the seed is not part of the key) into the pinned buffer the graph uploads from.
+// The kernels and their order are those of the plain path, so the results are bit-identical.
+constexpr int kGraphMaxEntries = 8;
+template <typename T>
+bool graph_eligible(const coru_ctx* c, const Request<T>& r) {
+    static const bool off = getenv("CORU_NO_GRAPH") != nullptr && atoi(getenv("CORU_NO_GRAPH")) != 0;
+    if (off || c->world > 1 || c->comm || c->tcomm || c->prof || r.a_host || r.mode != Mode::Full) return false;
+    if (c->phi_mode != CORU_PHI_HOST_EXACT || r.d > 112) return false;   // wider cores use cooperative grids
+    if (std::is_same<T, double>::value && c->f64_engine != CORU_F64_AUTO) return false;
+    return r.rows * r.cols <= (int64_t(1) << 24);
+}
+
+template <typename T>
+int run_graph(coru_ctx* c, const Request<T>& r0) {
+    Request<T> r = r0;
+    const int d = r.d, dp = int(round_up(d, 8));
+    const int64_t N = r.cols;
+    coru_ctx::GraphEntry* e = nullptr;
+    for (auto& g : c->graphs)
+        if (g.A == r.A && g.lda == r.lda && g.rows == r.rows && g.cols == r.cols && g.d == d && g.q == r.q &&
+            g.variant == r.variant && g.elem == int(sizeof(T)) && g.trans == r.trans && g.u == r.u && g.t == r.t &&
+            g.v == r.v && g.ldu == r.ldu && g.ldt == r.ldt && g.ldv == r.ldv && g.want_perm == (r.perm_host != nullptr) &&
+            g.stream == c->stream)
+            e = &g;
+    if (!e) {  // first sighting: run the plain path (it also sizes the arena and sets every kernel attribute)
+        if (int(c->graphs.size()) >= kGraphMaxEntries) {
+            size_t lru = 0;
+            for (size_t i = 1; i < c->graphs.size(); ++i)
+                if (c->graphs[i].last_use < c->graphs[lru].last_use) lru = i;
+            if (c->graphs[lru].exec) cudaGraphExecDestroy(c->graphs[lru].exec);
+            c->graphs.erase(c->graphs.begin() + long(lru));
+        }
+        coru_ctx::GraphEntry g;
+        g.A = r.A; g.lda = r.lda; g.rows = r.rows; g.cols = r.cols; g.d = d; g.q = r.q; g.variant = r.variant;
+        g.elem = int(sizeof(T)); g.trans = r.trans; g.u = r.u; g.t = r.t; g.v = r.v; g.ldu = r.ldu; g.ldt = r.ldt;
+        g.ldv = r.ldv; g.want_perm = r.perm_host != nullptr; g.stream = c->stream; g.last_use = ++c->graph_clock;
+        c->graphs.push_back(g);
+        return run<T>(c, r);
+    }
+    e->last_use = ++c->graph_clock;
+    if (e->state < 0) return run<T>(c, r);
+    if (e->state == 1 && (e->arena != c->arena || e->pinned != c->pinned)) {  // buffers moved: capture again
+        cudaGraphExecDestroy(e->exec);
+        e->exec = nullptr;
+        e->state = 0;
+    }
+    if (!c->host_out && cudaMallocHost(reinterpret_cast<void**>(&c->host_out), sizeof(int64_t) * 160) != cudaSuccess) {
+        cudaGetLastError();
+        c->host_out = nullptr;
+        return run<T>(c, r);
+    }
+    // Φ for this call: the reference's gaussian(cols, ell, {seed, stream}), padded to dp, in the pinned buffer
+    CORU_TRY(ensure_pinned(c, size_t(N) * dp * sizeof(T)));
+    CORU_CUDA(cudaEventSynchronize(c->ev_phi));
+    gaussian_host_rows<T>(N, d, r.seed, r.stream, reinterpret_cast<T*>(c->pinned), dp, c->host_threads, 1, 0, N);
+    c->oz_a = nullptr;
+    c->last_f64_engine = 0;
+    if (e->state == 0) {
+        const void* pinned_before = c->pinned;
+        r.capture = true;
+        const int64_t l0 = g_launches;
+        cudaGraph_t graph = nullptr;
+        if (cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal) != cudaSuccess) {
+            cudaGetLastError();
+            e->state = -1;
+            return run<T>(c, r0);
+        }
+        const int rc = run_impl<T>(c, r, 0);
+        const cudaError_t ce = cudaStreamEndCapture(c->stream, &graph);
+        if (rc != CORU_OK || ce != cudaSuccess || !graph ||
+            cudaGraphInstantiate(&e->exec, graph, 0) != cudaSuccess) {
+            cudaGetLastError();
+            if (graph) cudaGraphDestroy(graph);
+            e->exec = nullptr;
+            e->state = -1;
+            g_launches = l0;
+            return run<T>(c, r0);
+        }
+        cudaGraphDestroy(graph);
+        e->launches = g_launches - l0;
+        g_launches = l0;
+        e->arena = c->arena;
+        e->pinned = pinned_before;
+        e->state = 1;
+    }
+    CORU_CUDA(cudaGraphLaunch(e->exec, c->stream));
+    g_launches += e->launches;
+    ++c->graph_replays;
+    CORU_CUDA(cudaStreamSynchronize(c->stream));
+    if (r.warn_host) *r.warn_host = int(reinterpret_cast<int*>(c->host_out)[0]);
+    if (r.perm_host) std::memcpy(r.perm_host, c->host_out + 1, sizeof(int64_t) * size_t(d));
     return CORU_OK;
 }
 
@@ -1394,6 +1520,7 @@ int corutv_dev(coru_ctx* c, const T* A, int64_t m_local, int64_t m, int64_t n, i
         r.ldt = out->ldt;
         out->lower = 0;
     }
+    if (graph_eligible<T>(c, r)) return run_graph<T>(c, r);
     return run<T>(c, r);
 }
 
@@ -2292,6 +2419,9 @@ void coru_ctx_destroy(coru_ctx* c) {
     if (c->ev_join) cudaEventDestroy(c->ev_join);
     if (c->ev_phi) cudaEventDestroy(c->ev_phi);
     if (c->pf_thread.joinable()) c->pf_thread.join();
+    for (auto& g : c->graphs)
+        if (g.exec) cudaGraphExecDestroy(g.exec);
+    if (c->host_out) cudaFreeHost(c->host_out);
     if (c->ev_pf) cudaEventDestroy(c->ev_pf);
     if (c->pf_buf) cudaFreeHost(c->pf_buf);
     for (auto& e : c->ev_chunk)
@@ -2325,6 +2455,7 @@ int coru_ctx_set_profiling(coru_ctx* c, int enable) {
 }
 
 int coru_ctx_last_f64_engine(coru_ctx* c) { return c ? c->last_f64_engine : -1; }
+int64_t coru_ctx_graph_replays(coru_ctx* c) { return c ? c->graph_replays : -1; }
 
 int coru_ctx_profile_apass_exclusive(coru_ctx* c, double* total_ms, int64_t* launches) {
     CORU_TRY(enter(c));

@@ -400,6 +400,10 @@ __global__ void __launch_bounds__(S::NT, S::min_blocks)
                 if (n0 + cc + 1 < N) dst[1] = acc[v].y;
             }
         }
+        // The consumer clears the flags it waited on: a CUDA-graph replay of this launch carries the
+        // same epoch, and must not take the previous replay's publishes for its own.
+        if (tid == 0)
+            for (int q = 0; q + 1 < fix_segs; ++q) flags[fix_tile * max_seg + q] = 0;
     }
 }
 

@@ -248,3 +248,45 @@ def test_default_phi_is_reference_phi(ctx, oracle, n, ell, stream):
     assert s_dev.c2_prev.cpu().numpy().tobytes() == want.tobytes()
     s_host = cg.sketch_bases(a, ell, 0, seed=cg.RngSeed(42, stream), ctx=ctx)
     assert s_host.c2_prev.tobytes() == want.tobytes()
+
+
+@pytest.mark.parametrize("variant", [0, 1])
+def test_cuda_graph_replay_is_bit_identical(ctx, variant):
+    """Small decompositions are replayed from a CUDA graph from the third call on the same device
+    buffers on (coru_gpu.h: coru_ctx_graph_replays). The first call runs the plain launches, the
+    second captures, later ones replay: all must return identical bytes for the same seed, the right
+    Φ for a different seed (the seed is not part of the graph), and the pivots / flag on the host."""
+    import ctypes as C
+    import torch
+    import paper_1810_07323_b200 as cg
+    from workloads import make_host
+    a = torch.from_numpy(make_host("C1")).cuda()
+    m, n, d, q = 1000, 1000, 25, 0
+    u = torch.empty((m, d), dtype=torch.float64, device="cuda")
+    t = torch.empty((d, d), dtype=torch.float64, device="cuda")
+    v = torch.empty((n, d), dtype=torch.float64, device="cuda")
+    perm = np.zeros(d, np.int64)
+    out = cg._Utv(u.data_ptr(), d, t.data_ptr(), d, v.data_ptr(), d, perm.ctypes.data, 0, 0)
+    lib = cg.load_library()
+    torch.cuda.synchronize()
+
+    def call(stream):
+        cg._check(lib.coru_corutv_f64_dev(ctx.h, a.data_ptr(), m, m, n, a.stride(0), d, q, variant, 42, stream,
+                                          C.byref(out)))
+        return u.cpu().numpy().copy(), t.cpu().numpy().copy(), v.cpu().numpy().copy(), perm.copy()
+
+    before = ctx.graph_replays()
+    first = call(0)                      # plain launches
+    other = call(1)                      # capture + first replay, another seed stream
+    for _ in range(3):
+        again = call(0)                  # replays
+        assert all(np.array_equal(x, y) for x, y in zip(first, again))
+    assert ctx.graph_replays() >= before + 3
+    other_again = call(1)
+    assert all(np.array_equal(x, y) for x, y in zip(other, other_again))
+    assert not np.array_equal(first[1], other[1])
+    # against a fresh context's plain path
+    c2 = cg.Context(0)
+    f = cg.corutv(a, d, q, cg.DVariant(variant), seed=cg.RngSeed(42, 0), ctx=c2)
+    assert np.array_equal(f.t.cpu().numpy(), first[1]) and np.array_equal(f.perm, first[3])
+    c2.close()
