@@ -96,8 +96,9 @@ int coru_ctx_set_f64_engine(coru_ctx* ctx, int mode);
  * digits, 2 = Ozaki over digit planes (bench evidence: which roofline applies). */
 int coru_ctx_last_f64_engine(coru_ctx* ctx);
 /* Small in-core single-GPU decompositions (rows·cols <= 2^24, ell <= 112, default engines, profiling
- * off) are replayed from a CUDA graph from the third call with the same device buffers and
- * parameters on (the seed may change: Φ is generated per call); CORU_NO_GRAPH=1 disables it.
+ * off, the context's own stream or any non-legacy stream set with coru_ctx_set_stream) are replayed
+ * from a CUDA graph from the third call with the same device buffers and parameters on (the seed
+ * may change: Φ is generated per call); CORU_NO_GRAPH=1 disables it.
  * Returns the number of replays so far (bench evidence). */
 int64_t coru_ctx_graph_replays(coru_ctx* ctx);
 int coru_ctx_set_f32_path(coru_ctx* ctx, int mode);

@@ -1384,6 +1384,7 @@ template <typename T>
 bool graph_eligible(const coru_ctx* c, const Request<T>& r) {
     static const bool off = getenv("CORU_NO_GRAPH") != nullptr && atoi(getenv("CORU_NO_GRAPH")) != 0;
     if (off || c->world > 1 || c->comm || c->tcomm || c->prof || r.a_host || r.mode != Mode::Full) return false;
+    if (c->stream == nullptr || c->stream == cudaStreamLegacy) return false;  // the legacy stream cannot be captured
     if (c->phi_mode != CORU_PHI_HOST_EXACT || r.d > 112) return false;   // wider cores use cooperative grids
     if (std::is_same<T, double>::value && c->f64_engine != CORU_F64_AUTO) return false;
     return r.rows * r.cols <= (int64_t(1) << 24);
@@ -1446,8 +1447,12 @@ int run_graph(coru_ctx* c, const Request<T>& r0) {
         }
         const int rc = run_impl<T>(c, r, 0);
         const cudaError_t ce = cudaStreamEndCapture(c->stream, &graph);
+        cudaError_t ie = cudaSuccess;
         if (rc != CORU_OK || ce != cudaSuccess || !graph ||
-            cudaGraphInstantiate(&e->exec, graph, 0) != cudaSuccess) {
+            (ie = cudaGraphInstantiate(&e->exec, graph, 0)) != cudaSuccess) {
+            if (getenv("CORU_GRAPH_DEBUG"))
+                fprintf(stderr, "coru: graph capture failed: rc %d (%s), end-capture %s, instantiate %s\n", rc,
+                        g_err.c_str(), cudaGetErrorString(ce), cudaGetErrorString(ie));
             cudaGetLastError();
             if (graph) cudaGraphDestroy(graph);
             e->exec = nullptr;

@@ -251,7 +251,7 @@ def test_default_phi_is_reference_phi(ctx, oracle, n, ell, stream):
 
 
 @pytest.mark.parametrize("variant", [0, 1])
-def test_cuda_graph_replay_is_bit_identical(ctx, variant):
+def test_cuda_graph_replay_is_bit_identical(variant):
     """Small decompositions are replayed from a CUDA graph from the third call on the same device
     buffers on (coru_gpu.h: coru_ctx_graph_replays). The first call runs the plain launches, the
     second captures, later ones replay: all must return identical bytes for the same seed, the right
@@ -269,6 +269,7 @@ def test_cuda_graph_replay_is_bit_identical(ctx, variant):
     out = cg._Utv(u.data_ptr(), d, t.data_ptr(), d, v.data_ptr(), d, perm.ctypes.data, 0, 0)
     lib = cg.load_library()
     torch.cuda.synchronize()
+    ctx = cg.Context(0)   # its own (non-legacy) stream: the legacy default stream cannot be captured
 
     def call(stream):
         cg._check(lib.coru_corutv_f64_dev(ctx.h, a.data_ptr(), m, m, n, a.stride(0), d, q, variant, 42, stream,
@@ -290,3 +291,4 @@ def test_cuda_graph_replay_is_bit_identical(ctx, variant):
     f = cg.corutv(a, d, q, cg.DVariant(variant), seed=cg.RngSeed(42, 0), ctx=c2)
     assert np.array_equal(f.t.cpu().numpy(), first[1]) and np.array_equal(f.perm, first[3])
     c2.close()
+    ctx.close()
