@@ -469,7 +469,12 @@ def run_ours(args, cfg):
                      "balanced 8-bit digit slices per operand, levels 0..6 = 28 slice products; A TMA-staged, "
                      "converted in-kernel; + X split / exponent kernels)") if engine == 1 else (
                      "k_apass_ozp (fp64 A-pass on the INT8 tensor cores over digit planes converted once per "
-                     "decomposition by k_oz_planes: pure TMA -> tcgen05.mma kind::i8, 28 slice products)")
+                     "decomposition by k_oz_planes: pure TMA -> tcgen05.mma kind::i8, 28 slice products)"
+                     ) if engine == 2 else (
+                     "k_apass_oz / k_apass_ozp, hybrid (fp64 A-pass on the INT8 tensor cores: tcgen05.mma kind::i8, "
+                     "Ozaki scheme, 28 slice products; the first A.X pass converts A in the kernel and TMA-stores "
+                     "the row-scaled digit planes, the later A.X passes stream them (k_apass_ozp), the A^T.Y "
+                     "passes convert in the kernel; + X split / exponent kernels)")
             roof = {"bound": "tensor" if t_tensor >= t_hbm else "hbm",
                     "achieved": achieved_int8 if t_tensor >= t_hbm else bytes_per / (avg_ms * 1e-3) / 1e9,
                     "peak": int8 if t_tensor >= t_hbm else peaks.get("hbm_gbs"),

@@ -86,14 +86,20 @@ enum { CORU_F32_AUTO = 0, CORU_F32_SIMT = 1, CORU_F32_TC = 2 };
  *     FP64 DMMA for shapes it cannot take and for every non-A-pass product;
  *     A is either converted to digits inside every A-pass kernel (few passes, narrow sketch) or
  *     once per decomposition into its digit planes (14 bytes per entry of extra device memory)
- *     that every pass then streams — chosen from (passes over A) x (N-chunks of the sketch);
+ *     that every pass then streams — chosen from (passes over A) x (N-chunks of the sketch); in
+ *     between (three or more A·X passes), hybrid: the first A·X pass converts in the kernel and
+ *     also writes the row-scaled planes (7 bytes per entry), the later A·X passes stream them,
+ *     the A^T·Y passes convert in the kernel. All variants produce the same bits;
  *   CORU_F64_DMMA: FP64 DMMA for everything;
- *   CORU_F64_OZAKI_INLINE / CORU_F64_OZAKI_PLANES: the Ozaki engine with the conversion forced
- *     into the A-pass kernel / into the once-per-decomposition digit planes. */
-enum { CORU_F64_AUTO = 0, CORU_F64_DMMA = 1, CORU_F64_OZAKI_INLINE = 2, CORU_F64_OZAKI_PLANES = 3 };
+ *   CORU_F64_OZAKI_INLINE / CORU_F64_OZAKI_PLANES / CORU_F64_OZAKI_HYBRID: the Ozaki engine with the
+ *     conversion forced into the A-pass kernel / the once-per-decomposition digit planes / hybrid. */
+enum {
+    CORU_F64_AUTO = 0, CORU_F64_DMMA = 1, CORU_F64_OZAKI_INLINE = 2, CORU_F64_OZAKI_PLANES = 3,
+    CORU_F64_OZAKI_HYBRID = 4
+};
 int coru_ctx_set_f64_engine(coru_ctx* ctx, int mode);
 /* Engine the last fp64 decomposition's A-passes ran on: 0 = FP64 DMMA, 1 = Ozaki with in-kernel
- * digits, 2 = Ozaki over digit planes (bench evidence: which roofline applies). */
+ * digits, 2 = Ozaki over digit planes, 3 = Ozaki hybrid (bench evidence: which roofline applies). */
 int coru_ctx_last_f64_engine(coru_ctx* ctx);
 /* Small in-core single-GPU decompositions (rows·cols <= 2^24, ell <= 112, default engines, profiling
  * off, the context's own stream or any non-legacy stream set with coru_ctx_set_stream) are replayed

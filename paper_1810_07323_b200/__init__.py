@@ -266,18 +266,20 @@ class Context:
         products), F32_SIMT (CUDA-core FFMA), F32_TC (tensor cores wherever the shape allows)."""
         _check(self.lib.coru_ctx_set_f32_path(self.h, mode))
 
-    F64_AUTO, F64_DMMA, F64_OZAKI_INLINE, F64_OZAKI_PLANES = 0, 1, 2, 3
+    F64_AUTO, F64_DMMA, F64_OZAKI_INLINE, F64_OZAKI_PLANES, F64_OZAKI_HYBRID = 0, 1, 2, 3, 4
 
     def set_f64_engine(self, mode: int):
         """fp64 A-pass engine: F64_AUTO (default: INT8 tensor cores, Ozaki scheme, for A-pass-sized
         products over the caller's A; digits converted inside each pass or once per decomposition
         into digit planes, by a cost model), F64_DMMA (FP64 DMMA for everything),
-        F64_OZAKI_INLINE / F64_OZAKI_PLANES (force where the conversion happens)."""
+        F64_OZAKI_INLINE / F64_OZAKI_PLANES / F64_OZAKI_HYBRID (force where the conversion happens;
+        hybrid = the first A·X pass converts in the kernel and writes the row-scaled planes that the
+        later A·X passes stream)."""
         _check(self.lib.coru_ctx_set_f64_engine(self.h, mode))
 
     def last_f64_engine(self) -> int:
         """Engine of the last fp64 decomposition's A-passes: 0 DMMA, 1 Ozaki (in-kernel digits),
-        2 Ozaki (digit planes)."""
+        2 Ozaki (digit planes), 3 Ozaki hybrid."""
         return int(self.lib.coru_ctx_last_f64_engine(self.h))
 
     def graph_replays(self) -> int:

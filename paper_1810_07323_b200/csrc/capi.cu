@@ -232,7 +232,8 @@ struct coru_ctx {
     void* oz_planes = nullptr;
     size_t oz_planes_cap = 0;
     bool oz_planes_ready = false;
-    int last_f64_engine = 0;  // engine of the last fp64 A-pass: 0 DMMA, 1 Ozaki (in-kernel digits), 2 Ozaki (digit planes)
+    int oz_pn_state = 0;        // hybrid: 0 off, 1 the next full op-N pass writes the PN planes, 2 PN planes valid
+    int last_f64_engine = 0;  // engine of the last fp64 A-pass: 0 DMMA, 1 Ozaki (in-kernel digits), 2 Ozaki (digit planes), 3 Ozaki hybrid
     bool wide_qr = true;  // CholeskyQR2 (fp64) for sketches wider than 128 columns, Householder fall-back
     char* arena = nullptr;
     size_t arena_bytes = 0;
@@ -416,9 +417,12 @@ bool oz_enabled(const coru_ctx* c) {
 // Exponents of the stored matrix (rows x cols, lda) the coming A-passes stream (gemm_oz.cu): one
 // extra read of A per decomposition, reused by every pass over it.
 // passes: A-passes the caller will run over A; ncols: their sketch width (decides digit planes).
-int oz_prepare(coru_ctx* c, const double* A, int64_t lda, int64_t rows, int64_t cols, int passes, int ncols) {
+// passes_n: how many of them are op-N passes over the stored matrix (decides the hybrid mode).
+int oz_prepare(coru_ctx* c, const double* A, int64_t lda, int64_t rows, int64_t cols, int passes, int ncols,
+               int passes_n = 0) {
     c->oz_a = nullptr;
     c->last_f64_engine = 0;
+    c->oz_pn_state = 0;
     if (!oz_enabled(c) || !A) return CORU_OK;
     if (!gemm_oz_eligible(std::max(rows, cols), std::min(rows, cols), 1)) return CORU_OK;
     // The int8 kernel runs one CTA per (128-row tile, 64-column chunk): on a small matrix it cannot
@@ -445,7 +449,7 @@ int oz_prepare(coru_ctx* c, const double* A, int64_t lda, int64_t rows, int64_t 
     const int nch = (ncols + 63) / 64;
     bool want = passes * (nch - 1) >= 15;
     if (c->f64_engine == CORU_F64_OZAKI_PLANES) want = true;
-    if (c->f64_engine == CORU_F64_OZAKI_INLINE) want = false;
+    if (c->f64_engine == CORU_F64_OZAKI_INLINE || c->f64_engine == CORU_F64_OZAKI_HYBRID) want = false;
     if (planes_env) want = atoi(planes_env) != 0;
     if (want) {
         const OzPlaneDims pd = gemm_oz_plane_dims(rows, cols);
@@ -462,6 +466,26 @@ int oz_prepare(coru_ctx* c, const double* A, int64_t lda, int64_t rows, int64_t 
             ++g_launches;
             c->oz_planes_ready = true;
         }
+    }
+    // Hybrid (no conversion pass): the first full op-N pass converts in the kernel and ALSO writes
+    // the row-scaled planes (7 bytes per entry); the later op-N passes stream those. Op-T passes
+    // keep the in-kernel conversion (the plane kernel is not faster there). Worth it from two
+    // re-uses on (C3: pass 1.69 -> 1.29 ms twice, the storing pass +0.1 ms).
+    static const char* hybrid_env = getenv("CORU_OZ_HYBRID");  // tooling override: 0 | 1
+    bool hybrid = !c->oz_planes_ready && !want && passes_n >= 3;
+    if (hybrid_env) hybrid = !c->oz_planes_ready && atoi(hybrid_env) != 0 && passes_n >= 2;
+    if (c->f64_engine == CORU_F64_OZAKI_INLINE) hybrid = false;
+    if (c->f64_engine == CORU_F64_OZAKI_HYBRID) hybrid = passes_n >= 2;
+    if (hybrid) {
+        const size_t need = gemm_oz_plane_dims(rows, cols).pn_bytes;
+        bool fits = need <= c->oz_planes_cap;
+        if (!fits) {
+            size_t free_b = 0, total_b = 0;
+            CORU_CUDA(cudaMemGetInfo(&free_b, &total_b));
+            fits = need + (size_t(4) << 30) <= free_b + c->oz_planes_cap;
+        }
+        if (fits && ensure_dev(c, &c->oz_planes, &c->oz_planes_cap, need, "Ozaki digit planes") == CORU_OK)
+            c->oz_pn_state = 1;
     }
     c->oz_a = A;
     c->oz_lda = lda;
@@ -530,16 +554,19 @@ int gemm<double>(coru_ctx* c, Op op, const double* A, int64_t lda, const double*
         if (c->prof) CORU_TRY(prof_begin(c, &stop));
         const int* eA = op == Op::N ? c->oz_e : c->oz_e + c->oz_rows;
         OzPlanes pl;
-        if (c->oz_planes_ready) {
+        const bool use_pl = c->oz_planes_ready || (op == Op::N && c->oz_pn_state == 2);
+        const bool store_pl = !use_pl && op == Op::N && c->oz_pn_state == 1 && Mo == c->oz_rows;
+        if (use_pl || store_pl) {
             const OzPlaneDims pd = gemm_oz_plane_dims(c->oz_rows, c->oz_cols);
             const uint8_t* base = static_cast<const uint8_t*>(c->oz_planes);
             pl.p = op == Op::N ? base : base + pd.pn_bytes;
             pl.ld = op == Op::N ? pd.ldn : pd.ldt;
             pl.rows = op == Op::N ? c->oz_rows : c->oz_cols;
         }
-        CORU_CUDA(gemm_oz(op, A, lda, c->oz_planes_ready ? &pl : nullptr, eA, X, ldx, C, ldc, Mo, K, N, c->oz_ws,
-                          c->num_sms, c->stream));
-        c->last_f64_engine = c->oz_planes_ready ? 2 : 1;
+        CORU_CUDA(gemm_oz(op, A, lda, use_pl ? &pl : nullptr, eA, X, ldx, C, ldc, Mo, K, N, c->oz_ws, c->num_sms,
+                          c->stream, store_pl ? &pl : nullptr));
+        if (store_pl) c->oz_pn_state = 2;
+        c->last_f64_engine = c->oz_planes_ready ? 2 : (c->oz_pn_state ? 3 : 1);
         if (stop) {
             CORU_CUDA(cudaEventRecord(stop, c->stream));
             c->prof_flops += 2.0 * double(Mo) * double(K) * double(N);
@@ -729,6 +756,9 @@ struct Work {
         if (overlap_b2(c, N, dp, sizeof(T)))  // the per-chunk A^T-products of the sharded power rounds
             for (int nc : {std::min(kB2ChunkCols, d), d % kB2ChunkCols ? d % kB2ChunkCols : std::min(kB2ChunkCols, d)})
                 gws_elems = std::max(gws_elems, gemm_ws<T>(r.op_at(), N, R, nc, sms));
+        if (std::is_same<T, float>::value && N * int64_t(d) >= (int64_t(1) << 22))  // the sketch over Φ row chunks (run_impl)
+            for (int64_t kk : {N / 8 - 4, N / 8, N / 8 + 4, N - 7 * (N / 8) + 28})
+                gws_elems = std::max(gws_elems, gemm_ws<T>(Op::N, R, kk, d, sms));
         if (r.a_host) {
             // host rows of A: rows of A' (URV) or its columns (ULV, A' = A^T); row length = the other side
             const int64_t HR = r.trans ? N : R, HL = r.trans ? R : N;
@@ -880,9 +910,12 @@ int phi_prefetch(coru_ctx* c, int64_t rows, int cols, int ld, uint64_t seed, uin
     return CORU_OK;
 }
 
+// on_chunk(r0, r1), if given, is called after the upload of rows [r0, r1) has been enqueued on st
+// (r0 a multiple of 4): the caller's work on those rows then runs while the host generates the next.
+using PhiChunkFn = std::function<int(int64_t, int64_t)>;
 template <typename T>
 int upload_phi_host(coru_ctx* c, int64_t rows, int cols, int ld, uint64_t seed, uint64_t stream, T* out,
-                    cudaStream_t st) {
+                    cudaStream_t st, const PhiChunkFn* on_chunk = nullptr) {
     const size_t bytes = size_t(rows) * ld * sizeof(T);
     if (c->pf_active) {
         c->pf_thread.join();
@@ -891,7 +924,7 @@ int upload_phi_host(coru_ctx* c, int64_t rows, int cols, int ld, uint64_t seed, 
             c->pf_elem == sizeof(T)) {
             CORU_CUDA(cudaMemcpyAsync(out, c->pf_buf, bytes, cudaMemcpyHostToDevice, st));
             CORU_CUDA(cudaEventRecord(c->ev_pf, st));
-            return CORU_OK;
+            return on_chunk ? (*on_chunk)(0, rows) : CORU_OK;
         }
     }
     CORU_TRY(ensure_pinned(c, bytes));
@@ -906,10 +939,12 @@ int upload_phi_host(coru_ctx* c, int64_t rows, int cols, int ld, uint64_t seed, 
     for (int k = 1; k <= chunks; ++k) {
         int64_t r1 = k == chunks ? rows : rows * k / chunks;
         if (k < chunks && ((r1 * cols) & 1)) --r1;  // odd cols: end on an even row so the next chunk starts on a pair
+        if (k < chunks && on_chunk) r1 &= ~int64_t(3);  // 16-byte aligned sub-matrices for the caller (still even)
         if (r1 <= r0) continue;
         gaussian_host_rows<T>(rows, cols, seed, stream, phi, ld, c->host_threads, 1, r0, r1);
         CORU_CUDA(cudaMemcpyAsync(out + r0 * ld, phi + r0 * ld, size_t(r1 - r0) * ld * sizeof(T),
                                   cudaMemcpyHostToDevice, st));
+        if (on_chunk) CORU_TRY((*on_chunk)(r0, r1));
         r0 = r1;
     }
     CORU_CUDA(cudaEventRecord(c->ev_phi, st));
@@ -920,7 +955,7 @@ int upload_phi_host(coru_ctx* c, int64_t rows, int cols, int ld, uint64_t seed, 
 // bit-exact (upload_phi_host). CORU_PHI_DEVICE (opt-in): the device generator (same word stream,
 // device log/sincos, a few ulp off).
 template <typename T>
-int gen_phi(coru_ctx* c, const Request<T>& r, T* out, int dp) {
+int gen_phi(coru_ctx* c, const Request<T>& r, T* out, int dp, const PhiChunkFn* on_chunk = nullptr) {
     const int64_t N = r.cols;
     cudaStream_t st = c->stream;
     if (c->phi_mode == CORU_PHI_DEVICE) {
@@ -928,9 +963,9 @@ int gen_phi(coru_ctx* c, const Request<T>& r, T* out, int dp) {
         seed_state_words(r.seed, r.stream, s4);
         CORU_CUDA(gaussian_dev<T>(N, r.d, s4, out, dp, st));
         ++g_launches;
-        return CORU_OK;
+        return on_chunk ? (*on_chunk)(0, N) : CORU_OK;
     }
-    return upload_phi_host<T>(c, N, r.d, dp, r.seed, r.stream, out, st);
+    return upload_phi_host<T>(c, N, r.d, dp, r.seed, r.stream, out, st, on_chunk);
 }
 
 template <typename T>
@@ -1045,7 +1080,13 @@ int run(coru_ctx* c, const Request<T>& r, size_t extra_arena_off = 0) {
     if constexpr (std::is_same<T, double>::value) {
         if (r.A) {  // device-resident A: the stored matrix is rows x cols, or its transpose (ULV)
             const int passes = r.mode == Mode::Sketch ? 2 * r.q + 2 : 2 * r.q + (r.variant == CORU_D_APPROX ? 2 : 3);
-            const int rc = oz_prepare(c, r.A, r.lda, r.trans ? r.cols : r.rows, r.trans ? r.rows : r.cols, passes, r.d);
+            // op-N passes over the STORED matrix: a·c2 products (q + 1, + a·q2 for exact D) when it is
+            // A itself, the q + 1 a^T·c1 products when it holds the transpose; minus the one the host
+            // entry already ran chunk by chunk
+            int passes_n = r.trans ? r.q + 1 : passes - (r.q + 1);
+            if (r.first_done) --passes_n;
+            const int rc = oz_prepare(c, r.A, r.lda, r.trans ? r.cols : r.rows, r.trans ? r.rows : r.cols, passes, r.d,
+                                      passes_n);
             if (rc != CORU_OK) {
                 if (c->tcomm) c->tcomm->abort();
                 return rc;
@@ -1073,12 +1114,38 @@ int run_impl(coru_ctx* c, const Request<T>& r, size_t extra_arena_off) {
 
     // Φ = gaussian(cols, ell, seed), padded to dp columns (corutv.hpp:51): on the device, or on the
     // host with the host libm (bit-exact) and one H2D.
-    if (r.capture)
-        CORU_CUDA(cudaMemcpyAsync(w.b2, c->pinned, size_t(N) * dp * sizeof(T), cudaMemcpyHostToDevice, st));
-    else if (!r.first_done)
-        CORU_TRY(gen_phi<T>(c, r, w.b2, dp));
     CORU_CUDA(cudaMemsetAsync(w.q1, 0, size_t(R) * dp * sizeof(T), st));
     CORU_CUDA(cudaMemsetAsync(w.q2, 0, size_t(N) * dp * sizeof(T), st));
+    // A large Φ costs the host tens of milliseconds (C5: 34 M Gaussians, ~25 ms on 16 threads) during
+    // which a pass that needs all of it would leave the GPU idle. fp32 (no exponent / digit pre-pass
+    // to hide it under): the sketch c1 = a·Φ is accumulated over the row chunks of Φ as they arrive —
+    // a[:, r0:r1]·Φ[r0:r1, :] per chunk, summed in chunk order (q1 is the scratch; its d columns are
+    // rewritten by the explicit Q1 later) — so the GPU trails the generator by one chunk.
+    // CORU_PHI_SEGMENTS=0/1 overrides (tooling).
+    bool sketch_done = false;
+    if (r.capture) {
+        CORU_CUDA(cudaMemcpyAsync(w.b2, c->pinned, size_t(N) * dp * sizeof(T), cudaMemcpyHostToDevice, st));
+    } else if (!r.first_done) {
+        static const char* seg_env = getenv("CORU_PHI_SEGMENTS");
+        bool seg = std::is_same<T, float>::value && r.A && !r.trans && !r.a_host && c->phi_mode == CORU_PHI_HOST_EXACT &&
+                   N * int64_t(d) >= (int64_t(1) << 22);
+        if (seg_env) seg = seg && atoi(seg_env) != 0;
+        if (seg) {
+            const PhiChunkFn on_chunk = [&](int64_t r0, int64_t r1) -> int {
+                T* out = r0 == 0 ? w.b1 : w.q1;
+                CORU_TRY(gemm<T>(c, Op::N, r.A + r0, r.lda, w.b2 + r0 * dp, dp, out, dp, R, r1 - r0, d, w.gws, w.gws_elems));
+                if (r0 > 0) {
+                    CORU_CUDA(add_inplace<T>(w.b1, w.q1, size_t(R) * dp, st));
+                    ++g_launches;
+                }
+                return CORU_OK;
+            };
+            CORU_TRY(gen_phi<T>(c, r, w.b2, dp, &on_chunk));
+            sketch_done = true;
+        } else {
+            CORU_TRY(gen_phi<T>(c, r, w.b2, dp));
+        }
+    }
 
     // Sketch and power rounds (corutv.hpp:54-58): c1 = a·c2 ; c2_prev = c2 ; c2 = a^T·c1.
     // The two QRs are independent and latency-bound (one CTA per tree block), so they run on two
@@ -1195,7 +1262,8 @@ int run_impl(coru_ctx* c, const Request<T>& r, size_t extra_arena_off) {
         }
     }
     for (int i = r.first_done ? 1 : 0; i <= r.q && !r.a_host; ++i) {
-        CORU_TRY(gemm<T>(c, r.op_a(), r.A, r.lda, w.b2, dp, w.b1, dp, R, N, d, w.gws, w.gws_elems));
+        if (!(i == 0 && sketch_done))
+            CORU_TRY(gemm<T>(c, r.op_a(), r.A, r.lda, w.b2, dp, w.b1, dp, R, N, d, w.gws, w.gws_elems));
         if (i == r.q && early_qr1) {
             CORU_CUDA(cudaEventRecord(c->ev_fork, st));
             CORU_CUDA(cudaStreamWaitEvent(c->aux, c->ev_fork, 0));
@@ -2540,7 +2608,7 @@ int coru_ctx_set_f32_path(coru_ctx* c, int mode) {
 }
 
 int coru_ctx_set_f64_engine(coru_ctx* c, int mode) {
-    if (!c || mode < CORU_F64_AUTO || mode > CORU_F64_OZAKI_PLANES) return fail(CORU_EINVAL, "bad argument");
+    if (!c || mode < CORU_F64_AUTO || mode > CORU_F64_OZAKI_HYBRID) return fail(CORU_EINVAL, "bad argument");
     std::lock_guard<std::mutex> lk(c->mu);
     c->f64_engine = mode;
     return CORU_OK;

@@ -69,9 +69,11 @@ struct OzPlanes {
     int64_t ld = 0, rows = 0;       // rows = rows of the plane set (output rows of op(A) for the whole matrix)
 };
 // pl != nullptr: A-pass over the planes (A, lda unused); else A is converted inside the kernel.
+// store != nullptr (op N, in-kernel conversion only): the pass also writes the row-scaled digit
+// planes of the rows it covers to `store`, for later op-N passes to run with pl = store.
 cudaError_t gemm_oz(Op op, const double* A, int64_t lda, const OzPlanes* pl, const int* eA, const double* X,
                     int64_t ldx, double* C, int64_t ldc, int64_t Mo, int64_t K, int N, void* ws, int num_sms,
-                    cudaStream_t st);
+                    cudaStream_t st, const OzPlanes* store = nullptr);
 int gemm_oz_launches(int64_t Mo, int64_t K, int N, int num_sms);
 
 }  // namespace coru_gpu

@@ -139,6 +139,21 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* tm, in
         "l"(reinterpret_cast<uint64_t>(tm)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
         : "memory");
 }
+// Shared -> global tensor store (bulk async group of the issuing thread).
+__device__ __forceinline__ void tma_store_3d(const CUtensorMap* tm, int c0, int c1, int c2, const void* src) {
+    asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%1, %2, %3}], [%4];\n" ::"l"(
+                     reinterpret_cast<uint64_t>(tm)),
+                 "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(src))
+                 : "memory");
+    asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
+}
+template <int N>
+__device__ __forceinline__ void tma_store_wait_read() {
+    asm volatile("cp.async.bulk.wait_group.read %0;\n" ::"n"(N) : "memory");
+}
+__device__ __forceinline__ void prefetch_tensormap(const CUtensorMap* tm) {
+    asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(tm)) : "memory");
+}
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory"); }
 
@@ -226,10 +241,15 @@ struct OzArgs {
     const int* eX;      // per column of X: F_j
 };
 
-template <bool TRANS>
+// STORE (op N only): the chunk-0 CTA of every row tile also writes the A digit slices it has just
+// built to the PN digit planes (tmP, the map k_apass_ozp loads them with: the stage image in shared
+// memory IS the box), so that the later op-N passes of the decomposition run on k_apass_ozp
+// without a conversion pass of their own (capi.cu oz_prepare, "hybrid").
+template <bool TRANS, bool STORE>
 __global__ void __launch_bounds__(kOzThreads, 1)
     k_apass_oz(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmXa,
-               const __grid_constant__ CUtensorMap tmXb, const __grid_constant__ OzArgs p) {
+               const __grid_constant__ CUtensorMap tmXb, const __grid_constant__ CUtensorMap tmP,
+               const __grid_constant__ OzArgs p) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     // 1024-byte alignment for the swizzle atoms, by offsetting the shared pointer itself (an
     // integer round trip would lose the address space and turn every smem access generic)
@@ -258,6 +278,7 @@ __global__ void __launch_bounds__(kOzThreads, 1)
     const int64_t kt0 = int64_t(split) * p.kt_per_split;
     const int nk = int((ktiles < kt0 + p.kt_per_split ? ktiles : kt0 + p.kt_per_split) - kt0);
 
+    const bool storing = STORE && chunk == 0;  // an int8 slot is then released by the MMAs AND the store
     if (warp == 0 && lane == 0) {
         for (int s = 0; s < kOzF; ++s) {
             mbar_init(&f_full[s], 1);
@@ -266,7 +287,7 @@ __global__ void __launch_bounds__(kOzThreads, 1)
         for (int s = 0; s < kOzI; ++s) {
             mbar_init(&x_full[s], 1);
             mbar_init(&a_full[s], kOzConvWarps);
-            mbar_init(&i_empty[s], 1);
+            mbar_init(&i_empty[s], storing ? 2 : 1);
         }
         mbar_init(acc_full, 1);
         mbar_init(acc_empty, kOzConvWarps);
@@ -314,6 +335,29 @@ __global__ void __launch_bounds__(kOzThreads, 1)
                 unsigned char* xs = iring + is * kOzIStage + kOzXOff;
                 mbar_expect_tx(&x_full[is], uint32_t(kOzS * nc * kOzBK));
                 tma_load_3d(xs, nc == p.nc_a ? &tmXa : &tmXb, k0, n0, 0, &x_full[is]);
+            }
+            __syncwarp();
+        }
+    } else if (STORE && warp == 2) {
+        // ===== plane store: the A slices of each stage -> PN, one stage behind =====
+        if (storing) {
+            if (lane == 0) prefetch_tensormap(&tmP);
+            for (int i = 0; i < nk; ++i) {
+                const int is = i % kOzI;
+                mbar_wait(&a_full[is], (i / kOzI) & 1);
+                if (lane == 0) {
+                    tma_store_3d(&tmP, int((kt0 + i) * kOzBK), int(m0), 0, iring + is * kOzIStage);
+                    if (i > 0) {
+                        tma_store_wait_read<1>();  // the previous stage's slices have left shared memory
+                        mbar_arrive(&i_empty[(i - 1) % kOzI]);
+                    }
+                }
+                __syncwarp();
+            }
+            if (lane == 0) {
+                tma_store_wait_read<0>();
+                mbar_arrive(&i_empty[(nk - 1) % kOzI]);
+                asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory");
             }
             __syncwarp();
         }
@@ -941,7 +985,8 @@ cudaError_t gemm_oz_planes(const double* A, int64_t lda, int64_t rows, int64_t c
 
 cudaError_t gemm_oz(Op op, const double* A, int64_t lda, const OzPlanes* pl, const int* eA, const double* X,
                     int64_t ldx, double* C, int64_t ldc, int64_t Mo, int64_t K, int N, void* ws, int num_sms,
-                    cudaStream_t st) {
+                    cudaStream_t st, const OzPlanes* store) {
+    if (store && (pl || op != Op::N)) return cudaErrorInvalidValue;
     const OzShape s = oz_shape(Mo, K, N, num_sms);
     unsigned char* w = static_cast<unsigned char*>(ws);
     uint8_t* xs = w;
@@ -960,18 +1005,21 @@ cudaError_t gemm_oz(Op op, const double* A, int64_t lda, const OzPlanes* pl, con
         e = cudaGetLastError();
         if (e != cudaSuccess) return e;
     }
-    CUtensorMap ta, tx;
-    if (pl) {
-        // digit planes of op(A): (k, row, slice), one box = the 7 slices of a 128-row tile
+    CUtensorMap ta, tx, tp;
+    // digit planes of op(A): (k, row, slice), one box = the 7 slices of a 128-row tile
+    auto pmap = [&](CUtensorMap* m, const OzPlanes* q) {
         auto fn = oz_encode_fn();
         const cuuint64_t dims[3] = {cuuint64_t(K), cuuint64_t(Mo), cuuint64_t(kOzS)};
-        const cuuint64_t str[2] = {cuuint64_t(pl->ld), cuuint64_t(pl->ld) * cuuint64_t(pl->rows)};
+        const cuuint64_t str[2] = {cuuint64_t(q->ld), cuuint64_t(q->ld) * cuuint64_t(q->rows)};
         const cuuint32_t box[3] = {kOzBK, kOzBM, cuuint32_t(kOzS)};
         const cuuint32_t es[3] = {1, 1, 1};
-        if (fn(&ta, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<uint8_t*>(pl->p), dims, str, box, es,
-               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_32B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
-            return cudaErrorInvalidValue;
+        return fn(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<uint8_t*>(q->p), dims, str, box, es,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_32B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+    };
+    if (store && !pmap(&tp, store)) return cudaErrorInvalidValue;
+    if (pl) {
+        if (!pmap(&ta, pl)) return cudaErrorInvalidValue;
     } else if (op == Op::N) {
         const cuuint64_t dims[2] = {cuuint64_t(K), cuuint64_t(Mo)};
         const cuuint32_t box[2] = {16, kOzBM};
@@ -1019,12 +1067,15 @@ cudaError_t gemm_oz(Op op, const double* A, int64_t lda, const OzPlanes* pl, con
     if (pl) {
         allow_max_smem(k_apass_ozp);
         k_apass_ozp<<<grid, kPzThreads, kPzSmem, st>>>(ta, tx, txb, a);
+    } else if (op == Op::N && store) {
+        allow_max_smem(k_apass_oz<false, true>);
+        k_apass_oz<false, true><<<grid, kOzThreads, kOzSmem, st>>>(ta, tx, txb, tp, a);
     } else if (op == Op::N) {
-        allow_max_smem(k_apass_oz<false>);
-        k_apass_oz<false><<<grid, kOzThreads, kOzSmem, st>>>(ta, tx, txb, a);
+        allow_max_smem(k_apass_oz<false, false>);
+        k_apass_oz<false, false><<<grid, kOzThreads, kOzSmem, st>>>(ta, tx, txb, ta, a);
     } else {
-        allow_max_smem(k_apass_oz<true>);
-        k_apass_oz<true><<<grid, kOzThreads, kOzSmem, st>>>(ta, tx, txb, a);
+        allow_max_smem(k_apass_oz<true, false>);
+        k_apass_oz<true, false><<<grid, kOzThreads, kOzSmem, st>>>(ta, tx, txb, ta, a);
     }
     e = cudaGetLastError();
     if (e != cudaSuccess || s.splits == 1) return e;

@@ -177,6 +177,28 @@ def test_fp32_parity_vs_fp32_oracle(ctx, oracle, name, m, n, d, q):
     assert np.all(np.tril(f.t, -1) == 0.0)
 
 
+def test_fp32_sketch_over_phi_row_chunks(ctx, oracle):
+    """A Φ of >= 2^22 entries (here 8192 x 520) is generated on the host in row chunks and the fp32
+    sketch a·Φ is accumulated chunk by chunk while the next chunk is generated (device entry, C5's
+    path): same tolerances against the fp32 oracle as the one-pass sketch, and bitwise repeatable."""
+    import torch
+    import paper_1810_07323_b200 as cg
+    from workloads import make_host
+    a = make_host("C5", 8192, 8192).astype(np.float32)
+    a_dev = torch.from_numpy(a).cuda()
+    f = cg.corutv(a_dev, 520, 0, seed=cg.RngSeed(42, 5), ctx=ctx)
+    f2 = cg.corutv(a_dev, 520, 0, seed=cg.RngSeed(42, 5), ctx=ctx)
+    assert torch.equal(f.t, f2.t) and torch.equal(f.u, f2.u) and torch.equal(f.v, f2.v)
+    o = oracle.corutv(a, 520, 0, seed=42, stream=5, threads=16)
+    a64 = a.astype(np.float64)
+    u, t, v = (x.cpu().numpy().astype(np.float64) for x in (f.u, f.t, f.v))
+    e_gpu = rel_recon_error(a64, u, t, v)
+    e_ora = rel_recon_error(a64, o.u.astype(np.float64), o.t.astype(np.float64), o.v.astype(np.float64))
+    dg = np.abs(np.abs(np.diag(t)) - np.abs(np.diag(o.t)).astype(np.float64))
+    assert abs(e_gpu - e_ora) <= 1e-4 * e_ora
+    assert dg.max() <= 1e-3
+
+
 def test_repeat_determinism_wide_sketch(ctx):
     """Regression: the stream-K fix-up flags are tagged with a per-launch epoch; epochs must be
     unique across GEMM configurations that reuse one workspace (CholeskyQR2's Gram and R2·R1

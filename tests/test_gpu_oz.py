@@ -150,3 +150,29 @@ def test_oz_planes_decomposition_bit_identical_to_inline(ctx):
     f1, f2 = out[ctx.F64_OZAKI_INLINE], out[ctx.F64_OZAKI_PLANES]
     assert np.array_equal(f1.perm, f2.perm)
     assert np.array_equal(f1.t, f2.t) and np.array_equal(f1.u, f2.u) and np.array_equal(f1.v, f2.v)
+
+
+@pytest.mark.parametrize("shape,d,q", [((1500, 900), 130, 2), ((4000, 1112), 70, 1), ((700, 2600), 40, 1)])
+def test_oz_hybrid_decomposition_bit_identical_to_inline(ctx, shape, d, q):
+    """Hybrid conversion — the first A·X pass converts in the kernel AND writes the row-scaled digit
+    planes with TMA stores, the later A·X passes stream them — gives the bits of the all-in-kernel
+    conversion: ragged row tiles and k tails (clipped stores), a wide matrix (ULV: the stored matrix
+    is the transpose, so the planes serve the a^T·c1 products)."""
+    import torch
+    import paper_1810_07323_b200 as cg
+    rng = np.random.default_rng(78)
+    a = rng.standard_normal(shape) * np.exp2(rng.integers(-8, 8, size=(shape[0], 1)))
+    a_dev = torch.from_numpy(a).cuda()
+    out = {}
+    for eng in (ctx.F64_OZAKI_INLINE, ctx.F64_OZAKI_HYBRID):
+        ctx.set_f64_engine(eng)
+        try:
+            out[eng] = cg.corutv(a_dev, d, q, seed=cg.RngSeed(42, 3), ctx=ctx)
+            if eng == ctx.F64_OZAKI_HYBRID:
+                assert ctx.last_f64_engine() == 3
+        finally:
+            ctx.set_f64_engine(ctx.F64_AUTO)
+    f1, f2 = out[ctx.F64_OZAKI_INLINE], out[ctx.F64_OZAKI_HYBRID]
+    assert np.array_equal(f1.perm, f2.perm)
+    for x, y in ((f1.t, f2.t), (f1.u, f2.u), (f1.v, f2.v)):
+        assert np.array_equal(x.cpu().numpy(), y.cpu().numpy())
