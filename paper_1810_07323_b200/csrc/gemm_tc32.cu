@@ -46,6 +46,7 @@ constexpr int kBK = 32;          // K per stage (one 128-byte swizzle row of fp3
 constexpr int kAccCols = 384;    // TMEM columns reserved for the accumulator
 constexpr int kMaxStages = 2;    // TMEM A slots: 384 + 64 * 2 = 512
 constexpr int kATileBytes = kBM * kBK * 4;  // 16 KB
+constexpr int kMaxChainKTiles = 128;        // longest fp32 accumulation chain in TMEM: 4096 k, then a flush
 
 // ---- PTX wrappers -------------------------------------------------------------------------------
 __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
@@ -169,7 +170,10 @@ struct TcArgs {
     float* C;
     int64_t ldc;
     int64_t split_stride;  // > 0: write split partials to C + split * split_stride with ld = N
+    int flush_tiles;       // 1: shared memory holds the flush warps' transpose tiles (after the barriers)
 };
+constexpr int kFlushTileLd = 9;                             // floats per row of a 32 x 8 transpose tile
+constexpr int kFlushTileBytes = 4 * 32 * kFlushTileLd * 4;  // four flush warps
 
 template <bool TRANS>
 __global__ void __launch_bounds__(kTcThreads, 1)
@@ -186,8 +190,9 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     uint64_t* full = bars;                   // [stages] TMA landed
     uint64_t* conv = bars + kMaxStages;      // [stages] A hi/lo in TMEM
     uint64_t* empty = bars + 2 * kMaxStages; // [stages] MMAs of the stage done (smem + TMEM slot free)
-    uint64_t* accf = bars + 3 * kMaxStages;  // accumulator complete
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 3 * kMaxStages + 1);
+    uint64_t* accf = bars + 3 * kMaxStages;  // accumulator chunk complete
+    uint64_t* acce = accf + 1;               // accumulator chunk read back (4 flush warps)
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 3 * kMaxStages + 2);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     int bid = blockIdx.x;
@@ -207,6 +212,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
             mbar_init(&empty[s], 1);
         }
         mbar_init(accf, 1);
+        mbar_init(acce, 4);
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
         asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
         asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&tmXh)) : "memory");
@@ -251,6 +257,8 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         for (int i = 0; i < nk; ++i) {
             const int s = i % p.stages;
             const uint32_t ph = (i / p.stages) & 1;
+            const bool first = (i % kMaxChainKTiles) == 0;
+            if (first && i > 0) mbar_wait(acce, ((i / kMaxChainKTiles) - 1) & 1);  // the last chunk has been read back
             mbar_wait(&full[s], ph);
             mbar_wait(&conv[s], ph);
             tc_fence_after();
@@ -261,7 +269,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
 #pragma unroll
                 for (int ks = 0; ks < kBK / 8; ++ks) {
                     const uint32_t ahi = aslot + 8 * ks, alo = ahi + 32;
-                    const uint32_t acc0 = (i > 0 || ks > 0) ? 1u : 0u;
+                    const uint32_t acc0 = (!first || ks > 0) ? 1u : 0u;
                     // K-major SW128: rows of 128 B (32 k), 8-row groups 1024 B apart, K step = +32 B
                     const uint64_t bh = sdesc_sw128(xh + 32 * ks, 16, 1024);
                     const uint64_t bl = sdesc_sw128(xl + 32 * ks, 16, 1024);
@@ -278,15 +286,20 @@ __global__ void __launch_bounds__(kTcThreads, 1)
                     }
                 }
                 mma_commit(&empty[s]);
+                if ((i % kMaxChainKTiles) == kMaxChainKTiles - 1 || i == nk - 1) mma_commit(accf);
             }
             __syncwarp();
         }
-        if (lane == 0) mma_commit(accf);
-        __syncwarp();
     } else if (warp >= 4) {
         // ===== converters (row t of the tile = TMEM lane t), then the epilogue =====
         const int t = threadIdx.x - 128;
         const uint32_t lane_base = uint32_t((warp & 3) * 32) << 16;
+        const int64_t row = m0 + t;
+        const int n0 = chunk * p.nc;
+        float* cbase = p.split_stride > 0 ? p.C + split * p.split_stride : p.C;
+        const int64_t ldo = p.split_stride > 0 ? int64_t(p.N) : p.ldc;
+        float* crow = cbase + row * ldo;
+        int nflush = 0;
         for (int i = 0; i < nk; ++i) {
             const int s = i % p.stages;
             const uint32_t ph = (i / p.stages) & 1;
@@ -320,32 +333,79 @@ __global__ void __launch_bounds__(kTcThreads, 1)
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(&conv[s]);
-        }
-        // epilogue
-        mbar_wait(accf, 0);
-        tc_fence_after();
-        const int64_t row = m0 + t;
-        const int n0 = chunk * p.nc;
-        float* crow;
-        int64_t ldc;
-        if (p.split_stride > 0) {
-            crow = p.C + split * p.split_stride + row * p.N;
-            ldc = p.N;
-        } else {
-            crow = p.C + row * p.ldc;
-            ldc = p.ldc;
-        }
-        (void)ldc;
-        for (int cb = 0; cb < p.nc; cb += 32) {
-            uint32_t r[32];
-            tmem_ld32(tmem + lane_base + cb, r);
-            asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
-            if (row < p.Mo) {
+            if ((i % kMaxChainKTiles) == kMaxChainKTiles - 1 || i == nk - 1) {
+                // ---- flush: the accumulator of the last <= kMaxChainKTiles k-tiles is added to the
+                // output in fp32 round-to-nearest (the tensor core truncates when it accumulates, so
+                // one long chain would drift toward zero) and the MMAs restart from zero ----
+                if (p.flush_tiles) {
+                    // A thread holds 32 columns of ITS row: transposed through a 32 x 8 tile so that
+                    // each read-modify-write instruction covers 4 rows x 8 columns = four full
+                    // 32-byte sectors (row-per-thread stores touch 32 sectors for 128 bytes). The
+                    // output values of a 32-column block are fetched one block ahead (the first
+                    // before the accumulator is even complete): L2 latency stays off the chain.
+                    float* tile = reinterpret_cast<float*>(reinterpret_cast<unsigned char*>(tmem_slot) + 64) +
+                                  (warp & 3) * 32 * kFlushTileLd;
+                    const int rr = lane >> 3, cc = lane & 7;
+                    const int64_t grow0 = m0 + (warp & 3) * 32 + rr;
+                    float o[4][8], on[4][8];
+                    auto fetch = [&](int cb, float (&dst)[4][8]) {
 #pragma unroll
-                for (int j = 0; j < 32; ++j) {
-                    const int col = n0 + cb + j;
-                    if (cb + j < p.nc && col < p.N) crow[col] = __uint_as_float(r[j]);
+                        for (int g = 0; g < 4; ++g) {
+                            const int colc = cb + 8 * g + cc;
+                            const bool cok = nflush > 0 && colc < p.nc && n0 + colc < p.N;
+#pragma unroll
+                            for (int q = 0; q < 8; ++q)
+                                dst[g][q] = (cok && grow0 + 4 * q < p.Mo) ? cbase[(grow0 + 4 * q) * ldo + n0 + colc] : 0.f;
+                        }
+                    };
+                    fetch(0, o);
+                    mbar_wait(accf, nflush & 1);
+                    tc_fence_after();
+                    for (int cb = 0; cb < p.nc; cb += 32) {
+                        uint32_t r[32];
+                        tmem_ld32(tmem + lane_base + cb, r);
+                        if (cb + 32 < p.nc) fetch(cb + 32, on);
+                        asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+#pragma unroll
+                        for (int g = 0; g < 4; ++g) {
+#pragma unroll
+                            for (int j = 0; j < 8; ++j) tile[lane * kFlushTileLd + j] = __uint_as_float(r[8 * g + j]);
+                            __syncwarp();
+                            const int colc = cb + 8 * g + cc;
+                            const bool cok = colc < p.nc && n0 + colc < p.N;
+#pragma unroll
+                            for (int q = 0; q < 8; ++q) {
+                                const float v = tile[(4 * q + rr) * kFlushTileLd + cc];
+                                if (cok && grow0 + 4 * q < p.Mo) cbase[(grow0 + 4 * q) * ldo + n0 + colc] = o[g][q] + v;
+                            }
+                            __syncwarp();
+                        }
+#pragma unroll
+                        for (int g = 0; g < 4; ++g)
+#pragma unroll
+                            for (int q = 0; q < 8; ++q) o[g][q] = on[g][q];
+                    }
+                } else {
+                    mbar_wait(accf, nflush & 1);
+                    tc_fence_after();
+                    for (int cb = 0; cb < p.nc; cb += 32) {
+                        uint32_t r[32];
+                        tmem_ld32(tmem + lane_base + cb, r);
+                        asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+                        if (row < p.Mo) {
+#pragma unroll
+                            for (int j = 0; j < 32; ++j) {
+                                const int col = n0 + cb + j;
+                                if (cb + j < p.nc && col < p.N)
+                                    crow[col] = nflush == 0 ? __uint_as_float(r[j]) : crow[col] + __uint_as_float(r[j]);
+                            }
+                        }
+                    }
                 }
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(acce);
+                ++nflush;
             }
         }
     }
@@ -418,7 +478,7 @@ bool make_map(CUtensorMap* m, const void* base, int rank, const cuuint64_t* dims
 }
 
 struct TcShape {
-    int nch, nc, n1, xboxes, stages, splits, mtiles, kt_per_split;
+    int nch, nc, n1, xboxes, stages, splits, mtiles, kt_per_split, flush_tiles;
     size_t smem;
 };
 
@@ -432,16 +492,26 @@ TcShape tc_shape(int64_t Mo, int64_t K, int N, int num_sms, int max_smem) {
     const size_t stage = size_t(kATileBytes) + 2 * size_t(s.nc) * kBK * 4;
     s.stages = int(std::min<size_t>(kMaxStages, (size_t(max_smem) - 1024 - 256) / stage));
     s.smem = 1024 + s.stages * stage + 256;
+    s.flush_tiles = s.smem + kFlushTileBytes <= size_t(max_smem) ? 1 : 0;  // not with two 112 KB stages (nc = 384)
+    if (s.flush_tiles) s.smem += kFlushTileBytes;
     s.mtiles = int((Mo + kBM - 1) / kBM);
     const int64_t ktiles = (K + kBK - 1) / kBK;
     const int64_t base = int64_t(s.mtiles) * s.nch;
     double best = 1e30;
     int best_s = 1;
     const int max_s = int(std::max<int64_t>(1, std::min<int64_t>(ktiles / 16, 16)));
+    // Cost in k-tile times: every CTA pays ~6 k-tiles of fill / flush on top of its share of K,
+    // and split partials are written and summed at HBM speed (C5: 13 splits of the 6.9-wave grid
+    // looked 1 % better by wave count alone and cost 0.3 ms of reduce per pass — and 1.6x on the
+    // K = 8192 products of the sketch over Φ row chunks).
+    const double reduce_unit = double(Mo) * double(N) * 8.0 / 9.1e6;
+    // (Accuracy does not depend on the split count: the kernel restarts its fp32 TMEM accumulator
+    // every kMaxChainKTiles k-tiles — the tensor core truncates when it accumulates, and one
+    // 65536-long chain was measured to shrink C5's |t_11| by 3.7e-4 against 13 chains of 5041.)
     for (int sp = 1; sp <= max_s; ++sp) {
         const double waves = std::ceil(double(base * sp) / num_sms);
-        const double cost = waves / sp + (sp > 1 ? 0.03 : 0.0);
-        if (cost < best - 1e-12) { best = cost; best_s = sp; }
+        const double cost = waves * (double(ktiles) / sp + 6.0) + (sp > 1 ? sp * reduce_unit : 0.0);
+        if (cost < best - 1e-9) { best = cost; best_s = sp; }
     }
     s.kt_per_split = int((ktiles + best_s - 1) / best_s);
     s.splits = int((ktiles + s.kt_per_split - 1) / s.kt_per_split);
@@ -516,6 +586,7 @@ cudaError_t gemm_tc32(Op op, const float* A, int64_t lda, const float* X, int64_
     a.C = s.splits > 1 ? part : C;
     a.ldc = ldc;
     a.split_stride = s.splits > 1 ? Mo * N : 0;
+    a.flush_tiles = s.flush_tiles;
     const unsigned grid = unsigned(int64_t(s.nch) * s.mtiles * s.splits);
     if (op == Op::N) {
         allow_max_smem(k_apass_tf32x3<false>);

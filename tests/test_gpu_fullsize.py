@@ -68,7 +68,10 @@ def test_fullsize_properties(ctx, name):
     t = f.t.double()
     lower_zero = bool((torch.tril(t, -1) == 0).all())
     dg = torch.abs(torch.diagonal(t)).cpu().numpy()
-    nonincreasing = bool(np.all(dg[:-1] >= dg[1:] * (1 - 1e-12)))
+    # QRCP order: non-increasing up to the error of the downdated column norms the pivots are
+    # chosen by (qr.hpp:121-139) — rounding level in fp64; in fp32 nearly equal trailing |t_jj|
+    # (C5's noise floor) may swap by a few 1e-6 relative
+    nonincreasing = bool(np.all(dg[:-1] >= dg[1:] * (1 - (1e-12 if c.dtype == "f64" else 1e-4))))
     na = _fro(a)
     resid = _resid_fro(a, f.u, f.t, f.v)
     ident = np.sqrt(max(na * na - float((t * t).sum()), 0.0))
