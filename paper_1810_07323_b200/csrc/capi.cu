@@ -2453,7 +2453,16 @@ int coru_ctx_create(int device, coru_ctx** out) {
         return fail(CORU_ECUDA, "cudaStreamCreate failed");
     }
     c->stream = c->own_stream;
-    if (cudaStreamCreateWithFlags(&c->aux, cudaStreamNonBlocking) != cudaSuccess ||
+    // The aux stream carries the latency-bound work that runs beside the A-passes (the Q1 tree, the
+    // per-chunk all-reduces). It gets the highest stream priority: its CTAs are scheduled before the
+    // pass's queued ones, so the long dependent chain of tree levels starts at once and the
+    // throughput-bound pass fills in around it (C3: 13.33 -> 13.17 ms; low priority 13.30).
+    // CORU_AUX_PRIORITY=default|low overrides (tooling).
+    int prio_lo = 0, prio_hi = 0;
+    cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi);
+    const char* pe = getenv("CORU_AUX_PRIORITY");
+    const int aux_prio = pe && std::string(pe) == "default" ? 0 : (pe && std::string(pe) == "low" ? prio_lo : prio_hi);
+    if (cudaStreamCreateWithPriority(&c->aux, cudaStreamNonBlocking, aux_prio) != cudaSuccess ||
         cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
         cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming) != cudaSuccess ||
         cudaEventCreateWithFlags(&c->ev_phi, cudaEventDisableTiming) != cudaSuccess ||
