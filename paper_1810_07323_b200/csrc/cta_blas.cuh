@@ -201,6 +201,139 @@ __device__ __forceinline__ void cta_rank_update_global(int M, int N, int K, cons
     }
 }
 
+// E(i,j) -= sum_k V(i,k) Z(k,j) for a tall E (M x N, N <= 32) in shared memory, V (M x K, K <= 16)
+// in GLOBAL memory (L2) and Z (K x N) in shared memory:
+//   V(i,k) = V[k*ldv + i], Z(k,j) = Z[k*ldz + j], E(i,j) = E[j*lde + i].
+// The rank-16 step of the explicit-Q kernel on big TSQR blocks. The generic cta_mm_f64 spends ~170
+// instructions per 16 x 8 tile there (predicated element loads with runtime strides, once per
+// tile: ncu showed the kernel issue-bound at 0.8 % FP64-pipe activity); here a warp owns a 16-row
+// strip: the Z fragments of all column tiles are loaded once per call, the V fragments once per
+// strip and reused by its (up to four) tiles. Same DMMA order and the same c + (-acc) update per
+// entry as cta_mm_f64(alpha = -1, accumulate): bit-identical.
+__device__ __forceinline__ void cta_strip_update_ga(int M, int N, int K, const double* __restrict__ V, int ldv,
+                                                    const double* Z, int ldz, double* E, int lde) {
+    const int lane = threadIdx.x & 31, warp = int(threadIdx.x >> 5), nw = int(blockDim.x >> 5);
+    const int g = lane >> 2, t = lane & 3;
+    const int tm = (M + 15) >> 4, tn = (N + 7) >> 3;
+    double zb[2][4][2];
+#pragma unroll
+    for (int u = 0; u < 2; ++u)
+#pragma unroll
+        for (int jt = 0; jt < 4; ++jt) {
+            const int k0 = 8 * u + t, k1 = k0 + 4, jb = 8 * jt + g;
+            zb[u][jt][0] = (jb < N && k0 < K) ? Z[k0 * ldz + jb] : 0.0;
+            zb[u][jt][1] = (jb < N && k1 < K) ? Z[k1 * ldz + jb] : 0.0;
+        }
+    const bool two = K > 8;
+    for (int strip = warp; strip < tm; strip += nw) {
+        const int ia = (strip << 4) + g, ib = ia + 8;
+        double a[2][4];
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+            const int k0 = 8 * u + t, k1 = k0 + 4;
+            a[u][0] = (ia < M && k0 < K) ? V[k0 * ldv + ia] : 0.0;
+            a[u][1] = (ib < M && k0 < K) ? V[k0 * ldv + ib] : 0.0;
+            a[u][2] = (ia < M && k1 < K) ? V[k1 * ldv + ia] : 0.0;
+            a[u][3] = (ib < M && k1 < K) ? V[k1 * ldv + ib] : 0.0;
+        }
+#pragma unroll
+        for (int jt = 0; jt < 4; ++jt) {
+            if (jt >= tn) break;
+            double acc[4] = {0.0, 0.0, 0.0, 0.0};
+            dmma_16x8x8(acc, a[0], zb[0][jt]);
+            if (two) dmma_16x8x8(acc, a[1], zb[1][jt]);
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                const int i = (strip << 4) + g + ((e >> 1) << 3), j = 8 * jt + 2 * t + (e & 1);
+                if (i < M && j < N) {
+                    double* c = E + j * lde + i;
+                    *c = *c + (-1.0) * acc[e];
+                }
+            }
+        }
+    }
+}
+
+// Y(a,j) = sum_r V(r,a) E(r,j) for the same operands (a < M <= 16 reflector columns, j < N <= 32,
+// r < K rows): V(r,a) = V[a*ldv + r] (global), E(r,j) = E[j*lde + r] (shared), Y(a,j) = Y[a*ldy + j].
+// cta_mm_f64's partition exactly — (column tile, K split) per warp, the same k ranges, the partial
+// tiles summed in split order through `scratch` — with contiguous-k pointers and only the last
+// k-step predicated on k: bit-identical, ~3x fewer instructions.
+__device__ __forceinline__ void cta_vt_e_ga(int M, int N, int K, const double* __restrict__ V, int ldv, const double* E,
+                                            int lde, double* Y, int ldy, double* scratch, int scratch_elems) {
+    const int lane = threadIdx.x & 31, warp = int(threadIdx.x >> 5), nw = int(blockDim.x >> 5);
+    const int g = lane >> 2, t = lane & 3;
+    const int tn = (N + 7) >> 3, tiles = tn;  // M <= 16: one tile row
+    if (tiles == 0 || K <= 0) return;
+    const int ksteps = (K + 7) >> 3;
+    int S = 1;
+    if (tiles < nw) {
+        S = min(nw / tiles, max(1, ksteps / 4));
+        S = max(1, min(S, scratch_elems / (tiles * 128)));
+    }
+    const int kfull = K >> 3;  // k-steps with all 8 k inside [0, K)
+    for (int w = warp; w < tiles * S; w += nw) {
+        const int tile = w % tiles, s = w / tiles;
+        const int jb = (tile << 3) + g;
+        const int ks0 = (ksteps * s) / S, ks1 = (ksteps * (s + 1)) / S;
+        const bool va = g < M, vb = g + 8 < M, vj = jb < N;
+        const double* pa0 = V + (va ? g : 0) * ldv + t;
+        const double* pa1 = V + (vb ? g + 8 : 0) * ldv + t;
+        const double* pb = E + (vj ? jb : 0) * lde + t;
+        double acc[4] = {0.0, 0.0, 0.0, 0.0};
+        const int ksm = min(ks1, kfull);
+        int ks = ks0;
+#pragma unroll 4
+        for (; ks < ksm; ++ks) {
+            const int k = ks << 3;
+            double a[4], b[2];
+            a[0] = pa0[k];
+            a[1] = pa1[k];
+            a[2] = pa0[k + 4];
+            a[3] = pa1[k + 4];
+            b[0] = pb[k];
+            b[1] = pb[k + 4];
+            if (!va) a[0] = a[2] = 0.0;
+            if (!vb) a[1] = a[3] = 0.0;
+            if (!vj) b[0] = b[1] = 0.0;
+            dmma_16x8x8(acc, a, b);
+        }
+        for (; ks < ks1; ++ks) {  // the ragged last k-step
+            const int k0 = (ks << 3) + t, k1 = k0 + 4;
+            double a[4], b[2];
+            a[0] = (va && k0 < K) ? pa0[ks << 3] : 0.0;
+            a[1] = (vb && k0 < K) ? pa1[ks << 3] : 0.0;
+            a[2] = (va && k1 < K) ? pa0[(ks << 3) + 4] : 0.0;
+            a[3] = (vb && k1 < K) ? pa1[(ks << 3) + 4] : 0.0;
+            b[0] = (vj && k0 < K) ? pb[ks << 3] : 0.0;
+            b[1] = (vj && k1 < K) ? pb[(ks << 3) + 4] : 0.0;
+            dmma_16x8x8(acc, a, b);
+        }
+        if (S == 1) {
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                const int i = g + ((e >> 1) << 3), j = (tile << 3) + 2 * t + (e & 1);
+                if (i < M && j < N) Y[i * ldy + j] = 1.0 * acc[e];
+            }
+        } else {
+            double* p = scratch + (s * tiles + tile) * 128 + lane * 4;
+#pragma unroll
+            for (int e = 0; e < 4; ++e) p[e] = acc[e];
+        }
+    }
+    if (S > 1) {
+        __syncthreads();
+        for (int e = warp * 32 + lane; e < tiles * 128; e += nw * 32) {
+            const int tile = e >> 7, ln = (e >> 2) & 31, el = e & 3;
+            const int i = (ln >> 2) + ((el >> 1) << 3);
+            const int j = (tile << 3) + 2 * (ln & 3) + (el & 1);
+            double v = scratch[e];
+            for (int s = 1; s < S; ++s) v += scratch[s * tiles * 128 + e];
+            if (i < M && j < N) Y[i * ldy + j] = 1.0 * v;
+        }
+    }
+}
+
 // Same contract for any T on the CUDA cores (fp32 path; small fp64 shapes).
 template <typename T>
 __device__ __forceinline__ void cta_mm_simt(int M, int N, int K, const T* A, int ars, int acs, const T* B, int brs,

@@ -25,6 +25,7 @@
 #include <cmath>
 
 #include "common.cuh"
+#include <type_traits>
 #include "cta_blas.cuh"
 #include "tsqr.cuh"
 
@@ -857,27 +858,47 @@ __global__ void __launch_bounds__(kBThreads, 1)
     }
     const int q0 = blockIdx.y * qc;  // this CTA's column chunk of Q
     const int nq = min(qc, d - q0);
-    for (int e = tid; e < nq * rb; e += kBThreads) {
-        const int j = e / rb, i = e % rb;
-        S.E[j * S.lde + i] = i < d ? (Qb ? Qb[i * ldqin + q0 + j] : T(i == q0 + j ? 1 : 0)) : T(0);
-    }
+    for (int j = warp; j < nq; j += kBThreads / 32)
+        for (int i = lane; i < rb; i += 32)
+            S.E[j * S.lde + i] = i < d ? (Qb ? Qb[i * ldqin + q0 + j] : T(i == q0 + j ? 1 : 0)) : T(0);
     __syncthreads();
     for (int pi = npanels(d) - 1; pi >= 0; --pi) {
         const int p0 = pi * kNB, nbp = min(kNB, d - p0), K = rb - p0;
         const T* Vp = Vx + p0 * ldx + p0;  // V_p rows >= p0
         const int ldp = ldx;
         if (tid < kNB * kNB) S.Tp[tid] = Tb[pi * kNB * kNB + tid];
-        cta_mm(nbp, nq, K, Vp, ldp, 1, S.E + p0, 1, S.lde, S.Y, qc, 1, T(1), false, S.scratch, kGemmScratch);
+        if constexpr (std::is_same<T, double>::value) {
+            if (stage == 0 && nq <= 32)
+                cta_vt_e_ga(nbp, nq, K, Vp, ldp, S.E + p0, S.lde, S.Y, qc, S.scratch, kGemmScratch);
+            else
+                cta_mm(nbp, nq, K, Vp, ldp, 1, S.E + p0, 1, S.lde, S.Y, qc, 1, T(1), false, S.scratch, kGemmScratch);
+        } else {
+            cta_mm(nbp, nq, K, Vp, ldp, 1, S.E + p0, 1, S.lde, S.Y, qc, 1, T(1), false, S.scratch, kGemmScratch);
+        }
         __syncthreads();
         cta_mm(nbp, nq, nbp, S.Tp, kNB, 1, S.Y, qc, 1, S.Z, qc, 1, T(1), false, S.scratch, kGemmScratch);
         __syncthreads();
-        cta_mm(K, nq, nbp, Vp, 1, ldp, S.Z, qc, 1, S.E + p0, 1, S.lde, T(-1), true, S.scratch, kGemmScratch);
+        if constexpr (std::is_same<T, double>::value) {
+            if (stage == 0 && nq <= 32)  // reflectors in L2: the strip kernel (same bits, ~9x fewer instructions)
+                cta_strip_update_ga(K, nq, nbp, Vp, ldp, S.Z, qc, S.E + p0, S.lde);
+            else
+                cta_mm(K, nq, nbp, Vp, 1, ldp, S.Z, qc, 1, S.E + p0, 1, S.lde, T(-1), true, S.scratch, kGemmScratch);
+        } else {
+            cta_mm(K, nq, nbp, Vp, 1, ldp, S.Z, qc, 1, S.E + p0, 1, S.lde, T(-1), true, S.scratch, kGemmScratch);
+        }
         __syncthreads();
     }
     T* Qo = Qout + r0 * ldqout + q0;
-    for (int e = tid; e < nq * rb; e += kBThreads) {
-        const int i = e / nq, j = e % nq;
-        Qo[int64_t(i) * ldqout + j] = S.E[j * S.lde + i];
+    if (nq == 32) {
+        for (int e = tid; e < 32 * rb; e += kBThreads) {
+            const int i = e >> 5, j = e & 31;
+            Qo[int64_t(i) * ldqout + j] = S.E[j * S.lde + i];
+        }
+    } else {
+        for (int e = tid; e < nq * rb; e += kBThreads) {
+            const int i = e / nq, j = e % nq;
+            Qo[int64_t(i) * ldqout + j] = S.E[j * S.lde + i];
+        }
     }
 }
 
