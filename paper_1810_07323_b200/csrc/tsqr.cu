@@ -557,16 +557,14 @@ __global__ void __launch_bounds__(kBThreads, 1)
         T* stage = S.Vp;
         for (int rc = 0; rc < rb; rc += kLR) {
             const int nr = min(kLR, rb - rc);
-            // (nested loops: the flat index with its two runtime divisions per element made this
-            // phase issue-bound — 13 % of the kernel)
-            for (int r = warp; r < nr; r += kBThreads / 32) {
-                const T* xr = X + (r0 + rc + r) * ldx;
-                for (int c = lane; c < d; c += 32) stage[c * kLLd + r] = xr[c];
+            for (int e = tid; e < nr * d; e += kBThreads) {
+                const int r = e / d, c = e % d;
+                stage[c * kLLd + r] = X[(r0 + rc + r) * ldx + c];
             }
             __syncthreads();
-            for (int c = warp; c < d; c += kBThreads / 32) {
-                T* wc = W + int64_t(c) * ldv + rc;
-                for (int r = lane; r < nr; r += 32) wc[r] = stage[c * kLLd + r];
+            for (int e = tid; e < d * kLR; e += kBThreads) {
+                const int c = e / kLR, r = e % kLR;
+                if (r < nr) W[int64_t(c) * ldv + rc + r] = stage[c * kLLd + r];
             }
             __syncthreads();
         }
