@@ -236,6 +236,14 @@ __device__ __forceinline__ void cta_strip_update_ga(int M, int N, int K, const d
             a[u][2] = (ia < M && k1 < K) ? V[k1 * ldv + ia] : 0.0;
             a[u][3] = (ib < M && k1 < K) ? V[k1 * ldv + ib] : 0.0;
         }
+        double cold[4][4];  // the strip's E entries, requested before the DMMAs
+#pragma unroll
+        for (int jt = 0; jt < 4; ++jt)
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                const int i = (strip << 4) + g + ((e >> 1) << 3), j = 8 * jt + 2 * t + (e & 1);
+                cold[jt][e] = (i < M && j < N) ? E[j * lde + i] : 0.0;
+            }
 #pragma unroll
         for (int jt = 0; jt < 4; ++jt) {
             if (jt >= tn) break;
@@ -245,10 +253,7 @@ __device__ __forceinline__ void cta_strip_update_ga(int M, int N, int K, const d
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
                 const int i = (strip << 4) + g + ((e >> 1) << 3), j = 8 * jt + 2 * t + (e & 1);
-                if (i < M && j < N) {
-                    double* c = E + j * lde + i;
-                    *c = *c + (-1.0) * acc[e];
-                }
+                if (i < M && j < N) E[j * lde + i] = cold[jt][e] + (-1.0) * acc[e];
             }
         }
     }
@@ -283,16 +288,30 @@ __device__ __forceinline__ void cta_vt_e_ga(int M, int N, int K, const double* _
         double acc[4] = {0.0, 0.0, 0.0, 0.0};
         const int ksm = min(ks1, kfull);
         int ks = ks0;
-#pragma unroll 4
+        constexpr int KB = 5;  // k-steps whose V fragments (L2) are requested together
+        for (; ks + KB <= ksm; ks += KB) {
+            double a[KB][4];
+#pragma unroll
+            for (int u = 0; u < KB; ++u) {
+                const int k = (ks + u) << 3;
+                a[u][0] = pa0[k];
+                a[u][1] = pa1[k];
+                a[u][2] = pa0[k + 4];
+                a[u][3] = pa1[k + 4];
+            }
+#pragma unroll
+            for (int u = 0; u < KB; ++u) {
+                const int k = (ks + u) << 3;
+                double b[2] = {pb[k], pb[k + 4]};
+                if (!va) a[u][0] = a[u][2] = 0.0;
+                if (!vb) a[u][1] = a[u][3] = 0.0;
+                if (!vj) b[0] = b[1] = 0.0;
+                dmma_16x8x8(acc, a[u], b);
+            }
+        }
         for (; ks < ksm; ++ks) {
             const int k = ks << 3;
-            double a[4], b[2];
-            a[0] = pa0[k];
-            a[1] = pa1[k];
-            a[2] = pa0[k + 4];
-            a[3] = pa1[k + 4];
-            b[0] = pb[k];
-            b[1] = pb[k + 4];
+            double a[4] = {pa0[k], pa1[k], pa0[k + 4], pa1[k + 4]}, b[2] = {pb[k], pb[k + 4]};
             if (!va) a[0] = a[2] = 0.0;
             if (!vb) a[1] = a[3] = 0.0;
             if (!vj) b[0] = b[1] = 0.0;
