@@ -22,6 +22,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstring>
+#include <emmintrin.h>
 #include <condition_variable>
 #include <functional>
 #include <mutex>
@@ -243,6 +244,7 @@ struct coru_ctx {
     // pool copies piece k+1 into a pinned slot while the DMA engine moves piece k.
     static constexpr int kStageSlots = 4;
     static constexpr size_t kStageBytes = size_t(16) << 20;
+    bool stage_nt = false;  // streaming (non-temporal) stores into the ring: CORU_STAGE_NT=1 (tooling)
     char* stage = nullptr;
     cudaEvent_t ev_stage[kStageSlots] = {};
     int stage_next = 0;
@@ -324,12 +326,37 @@ int ensure_stage(coru_ctx* c) {
     return CORU_OK;
 }
 
+// Copy with streaming stores (no read-for-ownership of the destination, no cache pollution): for
+// destinations the CPU will not read again — the pinned ring the DMA engine drains.
+void memcpy_stream(char* dst, const char* src, size_t n) {
+    while (n && (reinterpret_cast<uintptr_t>(dst) & 15)) {
+        *dst++ = *src++;
+        --n;
+    }
+    size_t i = 0;
+    for (; i + 64 <= n; i += 64) {
+        const __m128i a = _mm_loadu_si128(reinterpret_cast<const __m128i*>(src + i));
+        const __m128i b = _mm_loadu_si128(reinterpret_cast<const __m128i*>(src + i + 16));
+        const __m128i c2 = _mm_loadu_si128(reinterpret_cast<const __m128i*>(src + i + 32));
+        const __m128i d2 = _mm_loadu_si128(reinterpret_cast<const __m128i*>(src + i + 48));
+        _mm_stream_si128(reinterpret_cast<__m128i*>(dst + i), a);
+        _mm_stream_si128(reinterpret_cast<__m128i*>(dst + i + 16), b);
+        _mm_stream_si128(reinterpret_cast<__m128i*>(dst + i + 32), c2);
+        _mm_stream_si128(reinterpret_cast<__m128i*>(dst + i + 48), d2);
+    }
+    if (i < n) std::memcpy(dst + i, src + i, n - i);
+    _mm_sfence();
+}
+
 // memcpy on the host worker pool (pieces of >= 1 MB per worker).
-void parallel_memcpy(void* dst, const void* src, size_t bytes, int threads) {
+void parallel_memcpy(void* dst, const void* src, size_t bytes, int threads, bool stream_stores = false) {
     const int nt = int(std::max<size_t>(1, std::min<size_t>(size_t(std::max(threads, 1)), bytes >> 20)));
     host_parallel(nt, [&](int t) {
         const size_t b0 = bytes * size_t(t) / size_t(nt), b1 = bytes * size_t(t + 1) / size_t(nt);
-        std::memcpy(static_cast<char*>(dst) + b0, static_cast<const char*>(src) + b0, b1 - b0);
+        if (stream_stores)
+            memcpy_stream(static_cast<char*>(dst) + b0, static_cast<const char*>(src) + b0, b1 - b0);
+        else
+            std::memcpy(static_cast<char*>(dst) + b0, static_cast<const char*>(src) + b0, b1 - b0);
     });
 }
 
@@ -344,13 +371,21 @@ int h2d(coru_ctx* c, void* dst, const void* src, size_t bytes, cudaStream_t st) 
         return CORU_OK;
     }
     CORU_TRY(ensure_stage(c));
-    for (size_t off = 0; off < bytes; off += coru_ctx::kStageBytes) {
-        const size_t len = std::min(coru_ctx::kStageBytes, bytes - off);
+    static const size_t piece = [] {
+        // 8 MB pieces, one worker per MB: measured best on the 16-core host (C3 pageable e2e 13.0
+        // decompositions/s; 16 MB x 16 workers 12.5, 4 MB 7.6, streaming stores 11.6 — the ring
+        // then no longer stays in the CPU caches the DMA engine reads it from). CORU_STAGE_MB: tooling.
+        const char* e = getenv("CORU_STAGE_MB");
+        const size_t mb = e ? size_t(std::max(1, std::min(16, atoi(e)))) : 8;
+        return mb << 20;
+    }();
+    for (size_t off = 0; off < bytes; off += piece) {
+        const size_t len = std::min(piece, bytes - off);
         const int b = c->stage_next;
         c->stage_next = (b + 1) % coru_ctx::kStageSlots;
         char* slot = c->stage + size_t(b) * coru_ctx::kStageBytes;
         CORU_CUDA(cudaEventSynchronize(c->ev_stage[b]));  // the slot's previous DMA has drained
-        parallel_memcpy(slot, static_cast<const char*>(src) + off, len, c->host_threads);
+        parallel_memcpy(slot, static_cast<const char*>(src) + off, len, c->host_threads, c->stage_nt);
         CORU_CUDA(cudaMemcpyAsync(static_cast<char*>(dst) + off, slot, len, cudaMemcpyHostToDevice, st));
         CORU_CUDA(cudaEventRecord(c->ev_stage[b], st));
     }
@@ -2458,6 +2493,7 @@ int coru_ctx_create(int device, coru_ctx** out) {
     // pass's queued ones, so the long dependent chain of tree levels starts at once and the
     // throughput-bound pass fills in around it (C3: 13.33 -> 13.17 ms; low priority 13.30).
     // CORU_AUX_PRIORITY=default|low overrides (tooling).
+    c->stage_nt = getenv("CORU_STAGE_NT") && atoi(getenv("CORU_STAGE_NT")) != 0;
     int prio_lo = 0, prio_hi = 0;
     cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi);
     const char* pe = getenv("CORU_AUX_PRIORITY");
