@@ -234,6 +234,9 @@ struct coru_ctx {
     size_t oz_planes_cap = 0;
     bool oz_planes_ready = false;
     int oz_pn_state = 0;        // hybrid: 0 off, 1 the next full op-N pass writes the PN planes, 2 PN planes valid
+    // exponents already in oz_e for this matrix (the host entry computes them chunk by chunk under the upload)
+    const double* oz_pre_a = nullptr;
+    int64_t oz_pre_lda = 0, oz_pre_rows = 0, oz_pre_cols = 0;
     int last_f64_engine = 0;  // engine of the last fp64 A-pass: 0 DMMA, 1 Ozaki (in-kernel digits), 2 Ozaki (digit planes), 3 Ozaki hybrid
     bool wide_qr = true;  // CholeskyQR2 (fp64) for sketches wider than 128 columns, Householder fall-back
     char* arena = nullptr;
@@ -453,27 +456,41 @@ bool oz_enabled(const coru_ctx* c) {
 // extra read of A per decomposition, reused by every pass over it.
 // passes: A-passes the caller will run over A; ncols: their sketch width (decides digit planes).
 // passes_n: how many of them are op-N passes over the stored matrix (decides the hybrid mode).
-int oz_prepare(coru_ctx* c, const double* A, int64_t lda, int64_t rows, int64_t cols, int passes, int ncols,
-               int passes_n = 0) {
-    c->oz_a = nullptr;
-    c->last_f64_engine = 0;
-    c->oz_pn_state = 0;
-    if (!oz_enabled(c) || !A) return CORU_OK;
-    if (!gemm_oz_eligible(std::max(rows, cols), std::min(rows, cols), 1)) return CORU_OK;
+// Will the A-passes over a rows x cols matrix with an ncols-wide sketch run on the Ozaki engine?
+bool oz_wanted(const coru_ctx* c, int64_t rows, int64_t cols, int ncols) {
+    if (!oz_enabled(c)) return false;
+    if (!gemm_oz_eligible(std::max(rows, cols), std::min(rows, cols), 1)) return false;
     // The int8 kernel runs one CTA per (128-row tile, 64-column chunk): on a small matrix it cannot
     // fill the machine and the FP64 stream-K kernel is faster (C2, 4000^2 x 60: 32 CTAs, 187 us per
     // pass against 83 us on DMMA; C1 likewise). Forced engines skip the test.
     if (c->f64_engine == CORU_F64_AUTO && getenv("CORU_F64_ENGINE") == nullptr) {
         const int64_t ctas = ((std::max(rows, cols) + 127) / 128) * ((ncols + 63) / 64);
-        if (ctas < 2 * int64_t(c->num_sms)) return CORU_OK;  // under two waves: DMMA (RPCA 8000^2 x 80 too)
+        if (ctas < 2 * int64_t(c->num_sms)) return false;  // under two waves: DMMA (RPCA 8000^2 x 80 too)
     }
+    return true;
+}
+int oz_ensure_exponents(coru_ctx* c, int64_t rows, int64_t cols) {
     size_t cap_bytes = c->oz_e_cap * sizeof(int);
     void* e = c->oz_e;
     CORU_TRY(ensure_dev(c, &e, &cap_bytes, sizeof(int) * size_t(rows + cols), "Ozaki exponents"));
     c->oz_e = static_cast<int*>(e);
     c->oz_e_cap = cap_bytes / sizeof(int);
-    CORU_CUDA(gemm_oz_exponents(A, lda, rows, cols, c->oz_e, c->oz_e + rows, c->stream));
-    g_launches += 3;
+    return CORU_OK;
+}
+
+int oz_prepare(coru_ctx* c, const double* A, int64_t lda, int64_t rows, int64_t cols, int passes, int ncols,
+               int passes_n = 0) {
+    c->oz_a = nullptr;
+    c->last_f64_engine = 0;
+    c->oz_pn_state = 0;
+    const bool pre = A && c->oz_pre_a == A && c->oz_pre_lda == lda && c->oz_pre_rows == rows && c->oz_pre_cols == cols;
+    c->oz_pre_a = nullptr;
+    if (!A || !oz_wanted(c, rows, cols, ncols)) return CORU_OK;
+    if (!pre) {
+        CORU_TRY(oz_ensure_exponents(c, rows, cols));
+        CORU_CUDA(gemm_oz_exponents(A, lda, rows, cols, c->oz_e, c->oz_e + rows, c->stream));
+        g_launches += 3;
+    }
     // Digit planes (14 bytes per entry): converted once here, streamed by every A-pass. Skipped when
     // they would not fit in what is free now (beyond what the context already holds for them).
     // Worth it when the conversion would otherwise be repeated often enough: every pass converts A
@@ -1755,6 +1772,7 @@ int corutv_host(coru_ctx* c, const T* A, int64_t m, int64_t n, int64_t ell, int 
     if (variant != CORU_D_EXACT && variant != CORU_D_APPROX) return fail(CORU_EINVAL, "corutv: unknown DVariant");
     if (!A || !U || !Tt || !V) return fail(CORU_EINVAL, "null argument");
     if (c->world > 1) return fail(CORU_EINVAL, "host-buffer entry is single-GPU; use the _dev entry per rank");
+    c->oz_pre_a = nullptr;  // nothing pre-computed yet for this call's A
     const bool trans = m < n;
     const int d = int(ell), dp = int(round_up(ell, 8));
     // Upload pipeline (m >= n, A of 32 MB and more): A arrives in row chunks on the aux stream while
@@ -1837,6 +1855,16 @@ int corutv_host(coru_ctx* c, const T* A, int64_t m, int64_t n, int64_t ell, int 
         const bool prof = c->prof;  // partial passes: not A-pass launches
         c->prof = false;
         int rc = CORU_OK;
+        // fp64 on the Ozaki engine: its exponent pass over A (0.7 ms at C3) runs chunk by chunk under
+        // the upload as well; run() finds the exponents in place (oz_prepare)
+        bool pre_exp = false;
+        if constexpr (std::is_same<T, double>::value) {
+            if (oz_wanted(c, m, n, d)) {
+                CORU_TRY(oz_ensure_exponents(c, m, n));
+                CORU_CUDA(gemm_oz_exponents_begin(m, n, c->oz_e, c->oz_e + m, st));
+                pre_exp = true;
+            }
+        }
         for (int i = 0; i < C && rc == CORU_OK; ++i) {
             int64_t r0, rows;
             chunk_rows(i, r0, rows);
@@ -1853,12 +1881,28 @@ int corutv_host(coru_ctx* c, const T* A, int64_t m, int64_t n, int64_t ell, int 
                 break;
             }
             ++g_launches;
+            if constexpr (std::is_same<T, double>::value) {
+                if (pre_exp && gemm_oz_exponents_rows(a_d, n, r0, rows, n, c->oz_e, c->oz_e + m, st) != cudaSuccess) {
+                    rc = fail(CORU_ECUDA, "upload pipeline launch failed");
+                    break;
+                }
+            }
             rc = gemm<T>(c, Op::N, ai, n, w.b2, dp, w.b1 + r0 * dp, dp, rows, n, d, cws, cwse);  // c1 rows
             if (rc == CORU_OK)
                 rc = gemm<T>(c, Op::T, ai, n, w.b1 + r0 * dp, dp, parts + int64_t(i) * n * dp, dp, n, rows, d, cws, cwse);
         }
         c->prof = prof;
         CORU_TRY(rc);
+        if constexpr (std::is_same<T, double>::value) {
+            if (pre_exp) {
+                CORU_CUDA(gemm_oz_exponents_end(m, n, c->oz_e, c->oz_e + m, st));
+                g_launches += 2 + C;
+                c->oz_pre_a = a_d;
+                c->oz_pre_lda = n;
+                c->oz_pre_rows = m;
+                c->oz_pre_cols = n;
+            }
+        }
         if (q == 0 && w.b2prev)  // c2_prev = Φ for the approx core (corutv.hpp:56)
             CORU_CUDA(cudaMemcpyAsync(w.b2prev, w.b2, sizeof(T) * n * dp, cudaMemcpyDeviceToDevice, st));
         CORU_CUDA(sum_chunks<T>(parts, C, n, d, dp, int64_t(n) * dp, w.b2, dp, st));  // c2 = a^T·c1, chunk order

@@ -54,6 +54,12 @@ bool gemm_oz_supported(Op op, const double* A, int64_t lda, int64_t Mo, int64_t 
 size_t gemm_oz_ws_bytes(int64_t Mo, int64_t K, int N, int num_sms);
 cudaError_t gemm_oz_exponents(const double* A, int64_t lda, int64_t rows, int64_t cols, int* erow, int* ecol,
                               cudaStream_t st);
+// The same pass in pieces, for a matrix that arrives in row chunks (the host entry's upload
+// pipeline): begin (clear) -> rows [r0, r0 + nrows) as they become resident -> end (finish).
+cudaError_t gemm_oz_exponents_begin(int64_t rows, int64_t cols, int* erow, int* ecol, cudaStream_t st);
+cudaError_t gemm_oz_exponents_rows(const double* A, int64_t lda, int64_t r0, int64_t nrows, int64_t cols, int* erow,
+                                   int* ecol, cudaStream_t st);
+cudaError_t gemm_oz_exponents_end(int64_t rows, int64_t cols, int* erow, int* ecol, cudaStream_t st);
 // Digit planes of a prepared matrix (gemm_oz_planes): the 7 slices of every entry, converted once
 // per decomposition — PN (row scales, K-major for op N) followed by PT (column scales, transposed:
 // K-major for op T) in one buffer of pn_bytes + pt_bytes.

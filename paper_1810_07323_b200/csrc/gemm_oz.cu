@@ -952,16 +952,28 @@ size_t gemm_oz_ws_bytes(int64_t Mo, int64_t K, int N, int num_sms) {
     return b + 256;
 }
 
-cudaError_t gemm_oz_exponents(const double* A, int64_t lda, int64_t rows, int64_t cols, int* erow, int* ecol,
-                              cudaStream_t st) {
+cudaError_t gemm_oz_exponents_begin(int64_t rows, int64_t cols, int* erow, int* ecol, cudaStream_t st) {
     cudaError_t e = cudaMemsetAsync(erow, 0, sizeof(int) * size_t(rows), st);
     if (e == cudaSuccess) e = cudaMemsetAsync(ecol, 0, sizeof(int) * size_t(cols), st);
-    if (e != cudaSuccess) return e;
-    const dim3 grid(unsigned((cols + kExpCols - 1) / kExpCols), unsigned((rows + kExpRows - 1) / kExpRows));
-    k_oz_aexp<<<grid, 256, 0, st>>>(A, lda, rows, cols, erow, ecol);
+    return e;
+}
+cudaError_t gemm_oz_exponents_rows(const double* A, int64_t lda, int64_t r0, int64_t nrows, int64_t cols, int* erow,
+                                   int* ecol, cudaStream_t st) {
+    const dim3 grid(unsigned((cols + kExpCols - 1) / kExpCols), unsigned((nrows + kExpRows - 1) / kExpRows));
+    k_oz_aexp<<<grid, 256, 0, st>>>(A + r0 * lda, lda, nrows, cols, erow + r0, ecol);
+    return cudaGetLastError();
+}
+cudaError_t gemm_oz_exponents_end(int64_t rows, int64_t cols, int* erow, int* ecol, cudaStream_t st) {
     k_oz_finish_exp<<<int(std::min<int64_t>((rows + 255) / 256, 1184)), 256, 0, st>>>(erow, rows);
     k_oz_finish_exp<<<int(std::min<int64_t>((cols + 255) / 256, 1184)), 256, 0, st>>>(ecol, cols);
     return cudaGetLastError();
+}
+cudaError_t gemm_oz_exponents(const double* A, int64_t lda, int64_t rows, int64_t cols, int* erow, int* ecol,
+                              cudaStream_t st) {
+    cudaError_t e = gemm_oz_exponents_begin(rows, cols, erow, ecol, st);
+    if (e == cudaSuccess) e = gemm_oz_exponents_rows(A, lda, 0, rows, cols, erow, ecol, st);
+    if (e == cudaSuccess) e = gemm_oz_exponents_end(rows, cols, erow, ecol, st);
+    return e;
 }
 
 OzPlaneDims gemm_oz_plane_dims(int64_t rows, int64_t cols) {

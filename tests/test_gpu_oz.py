@@ -176,3 +176,29 @@ def test_oz_hybrid_decomposition_bit_identical_to_inline(ctx, shape, d, q):
     assert np.array_equal(f1.perm, f2.perm)
     for x, y in ((f1.t, f2.t), (f1.u, f2.u), (f1.v, f2.v)):
         assert np.array_equal(x.cpu().numpy(), y.cpu().numpy())
+
+
+def test_oz_host_entry_exponents_under_upload(ctx):
+    """Host entry on an Ozaki-sized matrix: the exponent pass runs chunk by chunk under the upload
+    pipeline (row exponents per chunk, column exponents as a running maximum) and the later passes
+    use them — rows and columns scaled over 2^±6 so that wrong exponents would clip digits. Agrees
+    with the device entry (whose first power round runs on the Ozaki engine instead of on DMMA
+    chunks): leading |t_jj| to 1e-9 relative, equal reconstruction error."""
+    import torch
+    import paper_1810_07323_b200 as cg
+    rng = np.random.default_rng(79)
+    m, n, d = 40000, 512, 100
+    x = np.linalg.qr(rng.standard_normal((m, 120)))[0] * (0.97 ** np.arange(120))
+    a = x @ np.linalg.qr(rng.standard_normal((n, 120)))[0].T + 1e-4 / np.sqrt(m) * rng.standard_normal((m, n))
+    a *= np.exp2(rng.integers(-6, 6, size=(m, 1)).astype(np.float64))
+    a *= np.exp2(rng.integers(-6, 6, size=(1, n)).astype(np.float64))
+    f_host = cg.corutv(a, d, 1, seed=cg.RngSeed(42, 1), ctx=ctx)
+    assert ctx.last_f64_engine() in (1, 3)
+    f_dev = cg.corutv(torch.from_numpy(a).cuda(), d, 1, seed=cg.RngSeed(42, 1), ctx=ctx)
+    assert ctx.last_f64_engine() in (1, 3)
+    th, td = np.abs(np.diag(f_host.t)), np.abs(np.diag(f_dev.t.cpu().numpy()))
+    assert np.max(np.abs(th - td)[:20] / td[:20]) <= 1e-9
+    na = np.linalg.norm(a)
+    eh = np.linalg.norm(a - (f_host.u @ f_host.t) @ f_host.v.T) / na
+    ed = np.linalg.norm(a - (f_dev.u.cpu().numpy() @ f_dev.t.cpu().numpy()) @ f_dev.v.cpu().numpy().T) / na
+    assert abs(eh - ed) <= 1e-6 * ed
