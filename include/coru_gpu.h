@@ -87,7 +87,7 @@ enum { CORU_F32_AUTO = 0, CORU_F32_SIMT = 1, CORU_F32_TC = 2 };
  *     A is either converted to digits inside every A-pass kernel (few passes, narrow sketch) or
  *     once per decomposition into its digit planes (14 bytes per entry of extra device memory)
  *     that every pass then streams — chosen from (passes over A) x (N-chunks of the sketch); in
- *     between (three or more A·X passes), hybrid: the first A·X pass converts in the kernel and
+ *     between (two or more A·X passes), hybrid: the first A·X pass converts in the kernel and
  *     also writes the row-scaled planes (7 bytes per entry), the later A·X passes stream them,
  *     the A^T·Y passes convert in the kernel. All variants produce the same bits;
  *   CORU_F64_DMMA: FP64 DMMA for everything;

@@ -521,10 +521,10 @@ int oz_prepare(coru_ctx* c, const double* A, int64_t lda, int64_t rows, int64_t 
     }
     // Hybrid (no conversion pass): the first full op-N pass converts in the kernel and ALSO writes
     // the row-scaled planes (7 bytes per entry); the later op-N passes stream those. Op-T passes
-    // keep the in-kernel conversion (the plane kernel is not faster there). Worth it from two
-    // re-uses on (C3: pass 1.69 -> 1.29 ms twice, the storing pass +0.1 ms).
+    // keep the in-kernel conversion (the plane kernel is not faster there). Worth it from the
+    // first re-use on (C3: a plane pass 1.47 instead of 1.69 ms, the storing pass +0.13 ms).
     static const char* hybrid_env = getenv("CORU_OZ_HYBRID");  // tooling override: 0 | 1
-    bool hybrid = !c->oz_planes_ready && !want && passes_n >= 3;
+    bool hybrid = !c->oz_planes_ready && !want && passes_n >= 2;
     if (hybrid_env) hybrid = !c->oz_planes_ready && atoi(hybrid_env) != 0 && passes_n >= 2;
     if (c->f64_engine == CORU_F64_OZAKI_INLINE) hybrid = false;
     if (c->f64_engine == CORU_F64_OZAKI_HYBRID) hybrid = passes_n >= 2;
