@@ -363,6 +363,18 @@ void parallel_memcpy(void* dst, const void* src, size_t bytes, int threads, bool
     });
 }
 
+// Piece size of the staging ring: 8 MB, one worker per MB — measured best on the 16-core host (C3
+// pageable e2e 13.0 decompositions/s; 16 MB x 16 workers 12.5, 4 MB 7.6, streaming stores 11.6 — the
+// ring then no longer stays in the CPU caches the DMA engine reads it from). CORU_STAGE_MB: tooling.
+size_t stage_piece_bytes() {
+    static const size_t piece = [] {
+        const char* e = getenv("CORU_STAGE_MB");
+        const size_t mb = e ? size_t(std::max(1, std::min(16, atoi(e)))) : 8;
+        return mb << 20;
+    }();
+    return piece;
+}
+
 // Host -> device copy of `bytes` on `st`. Page-locked sources go straight to the DMA engine; pageable
 // ones (the drop-in caller's std::vector storage) are staged through the pinned ring: the host pool
 // fills slot k+1 while the DMA engine drains slot k, so the copy runs near link speed instead of the
@@ -374,14 +386,7 @@ int h2d(coru_ctx* c, void* dst, const void* src, size_t bytes, cudaStream_t st) 
         return CORU_OK;
     }
     CORU_TRY(ensure_stage(c));
-    static const size_t piece = [] {
-        // 8 MB pieces, one worker per MB: measured best on the 16-core host (C3 pageable e2e 13.0
-        // decompositions/s; 16 MB x 16 workers 12.5, 4 MB 7.6, streaming stores 11.6 — the ring
-        // then no longer stays in the CPU caches the DMA engine reads it from). CORU_STAGE_MB: tooling.
-        const char* e = getenv("CORU_STAGE_MB");
-        const size_t mb = e ? size_t(std::max(1, std::min(16, atoi(e)))) : 8;
-        return mb << 20;
-    }();
+    const size_t piece = stage_piece_bytes();
     for (size_t off = 0; off < bytes; off += piece) {
         const size_t len = std::min(piece, bytes - off);
         const int b = c->stage_next;
@@ -405,12 +410,16 @@ int d2h_sync(coru_ctx* c, void* dst, const void* src, size_t bytes, cudaStream_t
         return CORU_OK;
     }
     CORU_TRY(ensure_stage(c));
-    constexpr size_t P = coru_ctx::kStageBytes;
+    static const size_t Pd = [] {  // CORU_STAGE_D2H_MB: tooling (slot stride stays kStageBytes)
+        const char* e = getenv("CORU_STAGE_D2H_MB");
+        return size_t(e ? std::max(1, std::min(16, atoi(e))) : 16) << 20;
+    }();
+    const size_t P = Pd;
     const size_t pieces = (bytes + P - 1) / P;
     auto issue = [&](size_t k) -> int {
         const int b = int(k % coru_ctx::kStageSlots);
         const size_t off = k * P, len = std::min(P, bytes - off);
-        CORU_CUDA(cudaMemcpyAsync(c->stage + size_t(b) * P, static_cast<const char*>(src) + off, len,
+        CORU_CUDA(cudaMemcpyAsync(c->stage + size_t(b) * coru_ctx::kStageBytes, static_cast<const char*>(src) + off, len,
                                   cudaMemcpyDeviceToHost, st));
         CORU_CUDA(cudaEventRecord(c->ev_stage[b], st));
         return CORU_OK;
@@ -421,7 +430,7 @@ int d2h_sync(coru_ctx* c, void* dst, const void* src, size_t bytes, cudaStream_t
         const int b = int(k % coru_ctx::kStageSlots);
         const size_t off = k * P, len = std::min(P, bytes - off);
         CORU_CUDA(cudaEventSynchronize(c->ev_stage[b]));
-        parallel_memcpy(static_cast<char*>(dst) + off, c->stage + size_t(b) * P, len, c->host_threads);
+        parallel_memcpy(static_cast<char*>(dst) + off, c->stage + size_t(b) * coru_ctx::kStageBytes, len, c->host_threads);
         if (k + ahead < pieces) CORU_TRY(issue(k + ahead));
     }
     return CORU_OK;
