@@ -812,42 +812,51 @@ __global__ void __launch_bounds__(256) k_oz_xexp(const double* __restrict__ X, i
 }
 
 // X (K x N) -> 7 balanced digit slices, K-major: Xs[(s·xrows + n)·ldk + k] = digit s of W_kn,
-// W = rint(x · 2^(54 - F_n)); zero for n >= N and k >= K. 32(k) x 32(n) tiles through smem;
-// a thread converts 4 consecutive k of one column and stores one 32-bit word per slice.
+// W = rint(x · 2^(54 - F_n)); zero for n >= N and k >= K. 128(k) x 32(n) tiles through shared
+// memory, stored transposed (k contiguous): a thread converts 4 consecutive k of one column and
+// stores one 32-bit word per slice, a warp 128 contiguous bytes of one slice row (the 32-k tiles
+// of the first version wrote 32-byte pieces: 90 us for C3's 200000 x 110 c1).
+constexpr int kSplitK = 128, kSplitLd = kSplitK + 2;
 __global__ void __launch_bounds__(256) k_oz_split_x(const double* __restrict__ X, int64_t ldx, int64_t K, int N,
                                                     const int* __restrict__ fexp, int xrows, int64_t ldk,
                                                     uint8_t* __restrict__ Xs) {
-    __shared__ double tile[32][33];
-    const int64_t k0 = int64_t(blockIdx.x) * 32;
+    __shared__ __align__(16) double tile[32 * kSplitLd];
+    const int64_t k0 = int64_t(blockIdx.x) * kSplitK;
     const int nb = blockIdx.y * 32;
     const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
-    for (int rr = ty; rr < 32; rr += 8) {
+#pragma unroll 4
+    for (int rr = ty; rr < kSplitK; rr += 8) {
         const int64_t k = k0 + rr;
         const int n = nb + tx;
-        tile[rr][tx] = (k < K && n < N) ? X[k * ldx + n] : 0.0;
+        tile[tx * kSplitLd + rr] = (k < K && n < N) ? X[k * ldx + n] : 0.0;
     }
     __syncthreads();
-    const int n = nb + (threadIdx.x >> 3), kg = threadIdx.x & 7;
-    if (n >= xrows) return;
-    const double sc = n < N ? pow2(54 - fexp[n]) : 0.0;
-    uint32_t lo[4], hi[4];
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-        const unsigned long long w = (unsigned long long)__double2ll_rn(tile[4 * kg + j][n - nb] * sc) + kOzBias;
-        lo[j] = uint32_t(w);
-        hi[j] = uint32_t(w >> 32);
-    }
+    const int kg = tx;  // 4 consecutive k: 4·kg ..
     const int64_t k = k0 + 4 * kg;
-    if (k >= ldk) return;
+    for (int nn = ty; nn < 32; nn += 8) {
+        const int n = nb + nn;
+        if (n >= xrows || k >= ldk) continue;
+        const double sc = n < N ? pow2(54 - fexp[n]) : 0.0;
+        const double2 v01 = *reinterpret_cast<const double2*>(&tile[nn * kSplitLd + 4 * kg]);
+        const double2 v23 = *reinterpret_cast<const double2*>(&tile[nn * kSplitLd + 4 * kg + 2]);
+        const double v[4] = {v01.x, v01.y, v23.x, v23.y};
+        uint32_t lo[4], hi[4];
 #pragma unroll
-    for (int s = 0; s < kOzS; ++s) {
-        const int b = 6 - s;
-        const uint32_t* src = b < 4 ? lo : hi;
-        const uint32_t bb = uint32_t(b & 3);
-        const uint32_t t01 = __byte_perm(src[0], src[1], bb | ((bb + 4) << 4));
-        const uint32_t t23 = __byte_perm(src[2], src[3], bb | ((bb + 4) << 4));
-        *reinterpret_cast<uint32_t*>(Xs + (int64_t(s) * xrows + n) * ldk + k) =
-            __byte_perm(t01, t23, 0x5410) ^ (s == 0 ? 0u : 0x80808080u);
+        for (int j = 0; j < 4; ++j) {
+            const unsigned long long w = (unsigned long long)__double2ll_rn(v[j] * sc) + kOzBias;
+            lo[j] = uint32_t(w);
+            hi[j] = uint32_t(w >> 32);
+        }
+#pragma unroll
+        for (int s2 = 0; s2 < kOzS; ++s2) {
+            const int bq = 6 - s2;
+            const uint32_t* src = bq < 4 ? lo : hi;
+            const uint32_t bb = uint32_t(bq & 3);
+            const uint32_t t01 = __byte_perm(src[0], src[1], bb | ((bb + 4) << 4));
+            const uint32_t t23 = __byte_perm(src[2], src[3], bb | ((bb + 4) << 4));
+            *reinterpret_cast<uint32_t*>(Xs + (int64_t(s2) * xrows + n) * ldk + k) =
+                __byte_perm(t01, t23, 0x5410) ^ (s2 == 0 ? 0u : 0x80808080u);
+        }
     }
 }
 
@@ -1012,7 +1021,7 @@ cudaError_t gemm_oz(Op op, const double* A, int64_t lda, const OzPlanes* pl, con
         const int gy = int(std::max<int64_t>(1, std::min<int64_t>((K + 7) / 8, 1184 / ((N + 31) / 32) + 1)));
         k_oz_xexp<<<dim3(unsigned((N + 31) / 32), unsigned(gy)), 256, 0, st>>>(X, ldx, K, N, fx);
         k_oz_finish_xexp<<<(N + 255) / 256, 256, 0, st>>>(fx, N);
-        const dim3 grid(unsigned((s.ldk + 31) / 32), unsigned((s.xrows + 31) / 32));
+        const dim3 grid(unsigned((s.ldk + kSplitK - 1) / kSplitK), unsigned((s.xrows + 31) / 32));
         k_oz_split_x<<<grid, 256, 0, st>>>(X, ldx, K, N, fx, s.xrows, s.ldk, xs);
         e = cudaGetLastError();
         if (e != cudaSuccess) return e;
