@@ -750,46 +750,52 @@ __device__ __forceinline__ int biased_exp(double x) { return int((__double_as_lo
 // owns a 128-row x 512-column tile; thread = two adjacent columns (16-byte loads, 8 rows in
 // flight), the row maxima go through warp reductions and shared memory, one integer atomicMax
 // per row and per column per CTA — the result does not depend on the schedule.
-constexpr int kExpRows = 128, kExpCols = 512;
+constexpr int kExpRows = 128, kExpCols = 1024;
 __global__ void __launch_bounds__(256) k_oz_aexp(const double* __restrict__ A, int64_t lda, int64_t rows, int64_t cols,
                                                  int* __restrict__ erow, int* __restrict__ ecol) {
     __shared__ int srow[kExpRows];
-    const int64_t c = int64_t(blockIdx.x) * kExpCols + 2 * threadIdx.x;
+    const int64_t c = int64_t(blockIdx.x) * kExpCols + 4 * threadIdx.x;   // four consecutive columns per thread
     const int64_t r0 = int64_t(blockIdx.y) * kExpRows;
     for (int i = threadIdx.x; i < kExpRows; i += 256) srow[i] = 0;
     __syncthreads();
-    const bool vec = (lda & 1) == 0 && (reinterpret_cast<uintptr_t>(A) & 15) == 0 && c + 1 < cols;
-    int cm0 = 0, cm1 = 0;
-    for (int rr = 0; rr < kExpRows; rr += 8) {
-        double a[8], b[8];
+    const bool vec = (lda & 1) == 0 && (reinterpret_cast<uintptr_t>(A) & 15) == 0 && c + 3 < cols;
+    int cm[4] = {0, 0, 0, 0};
+    for (int rr = 0; rr < kExpRows; rr += 4) {
+        double x[4][4];
 #pragma unroll
-        for (int u = 0; u < 8; ++u) {
+        for (int u = 0; u < 4; ++u) {
             const int64_t r = r0 + rr + u;
-            a[u] = b[u] = 0.0;
+#pragma unroll
+            for (int q = 0; q < 4; ++q) x[u][q] = 0.0;
             if (r < rows) {
                 if (vec) {
-                    const double2 v = *reinterpret_cast<const double2*>(A + r * lda + c);
-                    a[u] = v.x;
-                    b[u] = v.y;
+                    const double2 v0 = *reinterpret_cast<const double2*>(A + r * lda + c);
+                    const double2 v1 = *reinterpret_cast<const double2*>(A + r * lda + c + 2);
+                    x[u][0] = v0.x; x[u][1] = v0.y; x[u][2] = v1.x; x[u][3] = v1.y;
                 } else {
-                    if (c < cols) a[u] = A[r * lda + c];
-                    if (c + 1 < cols) b[u] = A[r * lda + c + 1];
+#pragma unroll
+                    for (int q = 0; q < 4; ++q)
+                        if (c + q < cols) x[u][q] = A[r * lda + c + q];
                 }
             }
         }
 #pragma unroll
-        for (int u = 0; u < 8; ++u) {
-            int ea = biased_exp(a[u]), eb = biased_exp(b[u]);
-            ea = ea == 0x7ff ? 0x7fe : ea;  // inf / nan: clamp (the host entry rejects them anyway)
-            eb = eb == 0x7ff ? 0x7fe : eb;
-            cm0 = max(cm0, ea);
-            cm1 = max(cm1, eb);
-            const int wm = int(__reduce_max_sync(0xffffffffu, unsigned(max(ea, eb))));
+        for (int u = 0; u < 4; ++u) {
+            int em = 0;
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                int e = biased_exp(x[u][q]);
+                e = e == 0x7ff ? 0x7fe : e;  // inf / nan: clamp (the host entry rejects them anyway)
+                cm[q] = max(cm[q], e);
+                em = max(em, e);
+            }
+            const int wm = int(__reduce_max_sync(0xffffffffu, unsigned(em)));
             if ((threadIdx.x & 31) == 0 && wm > 0) atomicMax(&srow[rr + u], wm);
         }
     }
-    if (c < cols && cm0 > 0) atomicMax(&ecol[c], cm0);
-    if (c + 1 < cols && cm1 > 0) atomicMax(&ecol[c + 1], cm1);
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+        if (c + q < cols && cm[q] > 0) atomicMax(&ecol[c + q], cm[q]);
     __syncthreads();
     for (int i = threadIdx.x; i < kExpRows; i += 256)
         if (r0 + i < rows && srow[i] > 0) atomicMax(&erow[r0 + i], srow[i]);
